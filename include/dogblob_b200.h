@@ -1,0 +1,161 @@
+/*
+ * dogblob_b200.h -- C ABI of the B200-native DoG blob-detector hot path.
+ *
+ * The reference (`pkg/src/dogblob`, pure Python) has no FFI; its boundary is
+ * the Python detector API and the seam is the `backend` string
+ * (convolve.py:34,206-207).  A `backend="cuda"` implementation binds exactly
+ * the entry points below (ctypes stub: paper_2010_08486_b200/_lib.py, and
+ * INTEGRATION.md shows the reference-side patch).  Each entry point names the
+ * reference function it replaces.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; `stream` is a cudaStream_t passed as void*;
+ *   - every function returns 0 on success, a DOGBLOB_E* code otherwise;
+ *     `dogblob_last_error()` returns the thread-local message;
+ *   - nothing allocates device memory after plan creation: the caller owns the
+ *     workspace / result buffers (sizes come from the *_bytes queries);
+ *   - a plan is immutable and may be shared by concurrent callers as long as
+ *     each caller brings its own workspace, result buffer and stream
+ *     (mirrors the shared, immutable `Detector`, detector.py:309-331);
+ *   - all launches are asynchronous on `stream`; no host synchronisation
+ *     happens inside any entry point except the *_sync helpers;
+ *   - candidate-capacity overflow is reported in the result header
+ *     (`n_* > capacity`, DOGBLOB_FLAG_OVERFLOW), never silently truncated.
+ */
+#ifndef DOGBLOB_B200_H
+#define DOGBLOB_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DOGBLOB_ABI_VERSION 1
+
+enum {
+    DOGBLOB_OK = 0,
+    DOGBLOB_EINVAL = 1,   /* bad argument  -> Python ValueError   */
+    DOGBLOB_ECUDA = 2,    /* CUDA failure  -> Python RuntimeError */
+    DOGBLOB_ENOMEM = 3,   /* buffer too small */
+};
+
+/* One detected circle -- field-for-field `Blob` (detector.py:67-76) plus the
+ * DoG slice index it came from (-1 once pruning has merged it). */
+typedef struct dogblob_blob {
+    double x, y;          /* integer-valued in the pipeline; doubles so that the
+                             prune stage accepts the reference's float centres */
+    double sigma;
+    double radius;        /* sqrt(2) * sigma */
+    double response;      /* float32 DoG value widened */
+    int32_t slice;
+    uint32_t flags;       /* DOGBLOB_BLOB_* */
+} dogblob_blob;
+
+#define DOGBLOB_BLOB_SCALE_EDGE 1u   /* at_scale_boundary */
+#define DOGBLOB_BLOB_MERGED     2u   /* radius/sigma rewritten by pruning */
+
+/* Header at the start of every result buffer; blobs follow at offset 64. */
+typedef struct dogblob_result_header {
+    int32_t n_blobs;        /* records that follow (after pruning if requested) */
+    int32_t n_candidates;   /* blobs before pruning */
+    int32_t n_flagged;      /* voxels that passed the 3-D maximum + threshold test */
+    int32_t n_plateau;      /* of those, members of multi-voxel plateaus */
+    int32_t n_merges;       /* merges performed by pruning */
+    uint32_t flags;         /* DOGBLOB_FLAG_* */
+    int32_t capacity;       /* max blobs this buffer can hold */
+    int32_t reserved[9];
+} dogblob_result_header;
+
+#define DOGBLOB_FLAG_OVERFLOW 1u     /* a capacity was exceeded: result incomplete */
+#define DOGBLOB_RESULT_HEADER_BYTES 64
+
+typedef struct dogblob_plan dogblob_plan;
+
+int dogblob_abi_version(void);
+const char *dogblob_last_error(void);
+
+/* ---- plan: ladder + separable tap tables for one image shape -------------
+ * replaces Detector.__init__ / build_kernel_bank / Detector.plan_for
+ * (detector.py:316-331, scale_space.py:84-119).
+ *   sigmas[n_levels]     ladder (float64)
+ *   radii[n_levels]      ceil(truncate * sigma_i)
+ *   taps                 concatenated 1-D unit-sum taps w_i[-r_i..r_i] (float32)
+ *   tap_offsets[n_levels] start of level i inside `taps`
+ *   max_blobs            capacity for flagged voxels / candidates / blobs
+ */
+int dogblob_plan_create(int device, int height, int width, int n_levels,
+                        const double *sigmas, const int32_t *radii,
+                        const float *taps, const int64_t *tap_offsets,
+                        int max_blobs, dogblob_plan **out);
+void dogblob_plan_destroy(dogblob_plan *plan);
+size_t dogblob_workspace_bytes(const dogblob_plan *plan);
+size_t dogblob_result_bytes(const dogblob_plan *plan);
+/* row pitch (in floats) of the device image the plan expects, >= width */
+int64_t dogblob_image_pitch(const dogblob_plan *plan);
+
+/* ---- the hot path ---------------------------------------------------------
+ * replaces Detector.run minus preprocessing (detector.py:343-359):
+ * convolve_bank -> dog_stack -> find_extrema -> prune_overlaps.
+ *   d_image     device float32, `height` rows of dogblob_image_pitch() floats
+ *   d_result    device buffer of dogblob_result_bytes(): header + blobs, sorted
+ *               by (-response, y, x, sigma)
+ *   events      NULL or 4 cudaEvent_t recorded at: start, after the scale-space
+ *               + DoG kernels, after extrema, after pruning
+ */
+int dogblob_detect(const dogblob_plan *plan, const float *d_image,
+                   float threshold, int neighborhood, double overlap, int prune,
+                   void *d_workspace, void *d_result, void *stream,
+                   void *const *events);
+
+/* Same call with HOST buffers: pitched H2D copy of the frame, dogblob_detect,
+ * D2H of header + the first `h_result_blobs` records into pinned `h_result`.
+ * The caller synchronises the stream, reads the header, and fetches any
+ * remaining records with dogblob_fetch_blobs. */
+int dogblob_detect_host(const dogblob_plan *plan, const float *h_image,
+                        float threshold, int neighborhood, double overlap, int prune,
+                        void *d_image, void *d_workspace, void *d_result,
+                        void *h_result, int h_result_blobs, void *stream,
+                        void *const *events);
+int dogblob_upload_image(const dogblob_plan *plan, const float *h_image,
+                         void *d_image, void *stream);
+int dogblob_fetch_blobs(const void *d_result, int first, int count,
+                        dogblob_blob *h_out, void *stream);
+
+/* ---- stage entry points (the reference's stage functions) -----------------
+ * convolve_bank(..., backend="cuda") (convolve.py:189-218): levels in image
+ * orientation, dense float32 [n_levels][height][width]. */
+int dogblob_scale_space(const dogblob_plan *plan, const float *d_image,
+                        void *d_workspace, float *d_levels, void *stream);
+/* the fused scale-space + DoG kernels, result transposed back to
+ * [n_levels-1][height][width] (what dog_stack(convolve_bank(..)) returns). */
+int dogblob_dog(const dogblob_plan *plan, const float *d_image,
+                void *d_workspace, float *d_slices, void *stream);
+/* dog_stack (detector.py:117-126) on an existing dense level stack. */
+int dogblob_dog_from_levels(int n_levels, int height, int width,
+                            const float *d_levels, const double *sigmas,
+                            float *d_slices, void *stream);
+/* find_extrema (detector.py:149-188) on a dense [n_slices][height][width]
+ * stack. slice_sigmas is a HOST array; workspace from dogblob_blobspace_bytes. */
+size_t dogblob_blobspace_bytes(int max_blobs);
+size_t dogblob_result_bytes_for(int max_blobs);
+int dogblob_extrema(int n_slices, int height, int width, const float *d_slices,
+                    const double *slice_sigmas, float threshold, int neighborhood,
+                    int max_blobs, void *d_blobspace, void *d_result, void *stream);
+/* prune_overlaps (detector.py:250-280): d_blobs_in holds n records in any
+ * order; result buffer receives the survivors, sorted. */
+int dogblob_prune(int n, const dogblob_blob *d_blobs_in, double overlap,
+                  int max_blobs, void *d_blobspace, void *d_result, void *stream);
+
+/* ---- small helpers so that a non-CUDA host language can drive the ABI ----- */
+int dogblob_event_create(void **event);
+int dogblob_event_destroy(void *event);
+int dogblob_event_elapsed_ms(void *start, void *stop, float *ms);
+int dogblob_stream_sync(void *stream);
+int dogblob_device_count(int *count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DOGBLOB_B200_H */

@@ -1,0 +1,442 @@
+// C ABI of libdogblob_b200 (see include/dogblob_b200.h).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+namespace dogblob {
+
+static thread_local std::string g_error;
+void set_error(const std::string &msg) { g_error = msg; }
+
+static inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+size_t blobspace_bytes(int cap) {
+    size_t b = 0;
+    const size_t c = (size_t)cap;
+    b += align_up(sizeof(Counters), 256);
+    b += align_up(c * sizeof(Voxel), 256);
+    b += align_up(c * sizeof(int), 256) * 2;                  // parent, pl_count
+    b += align_up(c * sizeof(unsigned long long), 256) * 2;   // pl_sum_row/col
+    b += align_up(c * sizeof(dogblob_blob), 256) * 2;         // unsorted, sorted
+    b += align_up(c * sizeof(int), 256) * 4;                  // first, alive, cell_of, cell_items
+    b += align_up((size_t)(kMaxCells + 1) * sizeof(int), 256);
+    b += align_up((size_t)kMaxCells * sizeof(int), 256);
+    b += align_up(8 * sizeof(double), 256);
+    return b;
+}
+
+BlobSpace carve_blobspace(void *base, int cap) {
+    char *p = reinterpret_cast<char *>(base);
+    const size_t c = (size_t)cap;
+    auto take = [&](size_t bytes) { char *q = p; p += align_up(bytes, 256); return q; };
+    BlobSpace bs;
+    bs.ctr = reinterpret_cast<Counters *>(take(sizeof(Counters)));
+    bs.plateau = reinterpret_cast<Voxel *>(take(c * sizeof(Voxel)));
+    bs.parent = reinterpret_cast<int *>(take(c * sizeof(int)));
+    bs.pl_count = reinterpret_cast<int *>(take(c * sizeof(int)));
+    bs.pl_sum_row = reinterpret_cast<unsigned long long *>(take(c * sizeof(unsigned long long)));
+    bs.pl_sum_col = reinterpret_cast<unsigned long long *>(take(c * sizeof(unsigned long long)));
+    bs.unsorted = reinterpret_cast<dogblob_blob *>(take(c * sizeof(dogblob_blob)));
+    bs.sorted = reinterpret_cast<dogblob_blob *>(take(c * sizeof(dogblob_blob)));
+    bs.first = reinterpret_cast<int *>(take(c * sizeof(int)));
+    bs.alive = reinterpret_cast<int *>(take(c * sizeof(int)));
+    bs.cell_of = reinterpret_cast<int *>(take(c * sizeof(int)));
+    bs.cell_items = reinterpret_cast<int *>(take(c * sizeof(int)));
+    bs.cell_start = reinterpret_cast<int *>(take((size_t)(kMaxCells + 1) * sizeof(int)));
+    bs.cell_fill = reinterpret_cast<int *>(take((size_t)kMaxCells * sizeof(int)));
+    bs.grid_params = reinterpret_cast<double *>(take(8 * sizeof(double)));
+    bs.cap = cap;
+    return bs;
+}
+
+}  // namespace dogblob
+
+using namespace dogblob;
+
+struct dogblob_plan {
+    int device;
+    ConvGeometry geo;
+    int max_blobs;
+    std::vector<LevelDesc> levels;
+    std::vector<double> sigmas;
+    // device constants
+    LevelDesc *d_levels = nullptr;
+    float2 *d_taps = nullptr;
+    int *d_level_order = nullptr;
+    int *d_group_begin = nullptr;
+    int *d_unit_groups = nullptr;
+    double *d_slice_sigma = nullptr;
+    float *d_sigma_f32 = nullptr;
+    // workspace layout (bytes from the workspace base)
+    size_t off_rows_t = 0, off_dog_t = 0, off_blobspace = 0, total = 0;
+};
+
+namespace {
+
+int round_up(int v, int a) { return (v + a - 1) / a * a; }
+
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) { ok = false; return; }
+        if (prev != dev && cudaSetDevice(dev) != cudaSuccess) ok = false;
+    }
+    ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+// Partition levels into G contiguous groups for the fused column+DoG pass. Group g
+// emits slices [begin[g], begin[g+1]) and therefore sweeps levels begin[g]..begin[g+1].
+std::vector<int> balance_groups(const std::vector<LevelDesc> &lv, int G) {
+    const int S = (int)lv.size() - 1;
+    G = std::max(1, std::min(G, S));
+    std::vector<double> pre(S + 1, 0.0);
+    for (int i = 0; i < S; ++i) pre[i + 1] = pre[i] + lv[i].n_chunks;
+    std::vector<int> begin(G + 1, 0);
+    begin[G] = S;
+    for (int g = 1; g < G; ++g) {
+        const double target = pre[S] * g / G;
+        int b = (int)(std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
+        b = std::max(b, begin[g - 1] + 1);
+        b = std::min(b, S - (G - g));
+        begin[g] = b;
+    }
+    return begin;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dogblob_abi_version(void) { return DOGBLOB_ABI_VERSION; }
+const char *dogblob_last_error(void) { return g_error.c_str(); }
+
+int dogblob_plan_create(int device, int height, int width, int n_levels, const double *sigmas,
+                        const int32_t *radii, const float *taps, const int64_t *tap_offsets,
+                        int max_blobs, dogblob_plan **out) {
+    DB_REQUIRE(out != nullptr, "out must not be NULL");
+    *out = nullptr;
+    DB_REQUIRE(height >= 1 && width >= 1, "expected a non-empty 2-D image");
+    DB_REQUIRE(n_levels >= 2, "a ladder needs at least two levels");
+    DB_REQUIRE(sigmas && radii && taps && tap_offsets, "NULL table");
+    DB_REQUIRE(max_blobs >= 1, "max_blobs must be >= 1");
+    DB_REQUIRE(height <= 32768 && width <= 32768, "image dimension above 32768");
+    for (int i = 0; i < n_levels; ++i) {
+        DB_REQUIRE(sigmas[i] > 0.0, "sigma must be > 0");
+        DB_REQUIRE(radii[i] >= 0 && 2 * radii[i] + 1 <= 4097, "kernel width exceeds cap 4097");
+    }
+    DeviceGuard guard(device);
+    DB_REQUIRE(guard.ok, "cannot select CUDA device");
+
+    auto *plan = new dogblob_plan();
+    plan->device = device;
+    plan->max_blobs = max_blobs;
+    plan->sigmas.assign(sigmas, sigmas + n_levels);
+    ConvGeometry &g = plan->geo;
+    g.H = height; g.W = width; g.L = n_levels;
+    g.Hp = round_up(height, kPad);
+    g.Wp = round_up(width, kPad);
+
+    // padded, duplicated tap tables: P[m] = w[m-(kTY-1)] on [kTY-1, 2r+kTY-1], else 0
+    std::vector<float2> table;
+    plan->levels.resize(n_levels);
+    int max_table = 0;
+    for (int i = 0; i < n_levels; ++i) {
+        const int r = radii[i];
+        LevelDesc &lv = plan->levels[i];
+        lv.radius = r;
+        lv.n_chunks = (kTY + 2 * r + kTY - 1) / kTY;
+        lv.tap_ofs = (int)table.size();
+        lv.sigma_f32 = (float)sigmas[i];
+        const int len = lv.n_chunks * kTY + kTY - 1;
+        max_table = std::max(max_table, len);
+        const float *w = taps + tap_offsets[i];
+        for (int m = 0; m < len; ++m) {
+            const int k = m - (kTY - 1);
+            const float v = (k >= 0 && k <= 2 * r) ? w[k] : 0.f;
+            table.push_back(make_float2(v, v));
+        }
+    }
+    g.max_table = max_table;
+
+    // level groups of the fused pass: about two waves of CTAs at 2 CTAs / SM
+    const int tiles = (g.Hp / kTileCols) * (g.Wp / kTileRows);
+    int G = (2 * 2 * 148 + tiles - 1) / tiles;
+    if (const char *env = std::getenv("DOGBLOB_GROUPS")) G = std::max(1, std::atoi(env));
+    std::vector<int> group_begin = balance_groups(plan->levels, G);
+    g.G = (int)group_begin.size() - 1;
+
+    std::vector<int> order(n_levels);
+    for (int i = 0; i < n_levels; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        return plan->levels[a].n_chunks > plan->levels[b].n_chunks;   // longest first
+    });
+    std::vector<int> unit(n_levels + 1);
+    for (int i = 0; i <= n_levels; ++i) unit[i] = i;
+    std::vector<float> sig32(n_levels);
+    for (int i = 0; i < n_levels; ++i) sig32[i] = (float)sigmas[i];
+
+#define PLAN_CUDA(expr)                                                                \
+    do {                                                                               \
+        cudaError_t _e = (expr);                                                       \
+        if (_e != cudaSuccess) {                                                       \
+            set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));             \
+            dogblob_plan_destroy(plan);                                                \
+            return DOGBLOB_ECUDA;                                                      \
+        }                                                                              \
+    } while (0)
+    PLAN_CUDA(cudaMalloc(&plan->d_levels, n_levels * sizeof(LevelDesc)));
+    PLAN_CUDA(cudaMalloc(&plan->d_taps, table.size() * sizeof(float2)));
+    PLAN_CUDA(cudaMalloc(&plan->d_level_order, n_levels * sizeof(int)));
+    PLAN_CUDA(cudaMalloc(&plan->d_group_begin, group_begin.size() * sizeof(int)));
+    PLAN_CUDA(cudaMalloc(&plan->d_unit_groups, unit.size() * sizeof(int)));
+    PLAN_CUDA(cudaMalloc(&plan->d_slice_sigma, n_levels * sizeof(double)));
+    PLAN_CUDA(cudaMalloc(&plan->d_sigma_f32, n_levels * sizeof(float)));
+    PLAN_CUDA(cudaMemcpy(plan->d_levels, plan->levels.data(), n_levels * sizeof(LevelDesc),
+                         cudaMemcpyHostToDevice));
+    PLAN_CUDA(cudaMemcpy(plan->d_taps, table.data(), table.size() * sizeof(float2),
+                         cudaMemcpyHostToDevice));
+    PLAN_CUDA(cudaMemcpy(plan->d_level_order, order.data(), n_levels * sizeof(int),
+                         cudaMemcpyHostToDevice));
+    PLAN_CUDA(cudaMemcpy(plan->d_group_begin, group_begin.data(), group_begin.size() * sizeof(int),
+                         cudaMemcpyHostToDevice));
+    PLAN_CUDA(cudaMemcpy(plan->d_unit_groups, unit.data(), unit.size() * sizeof(int),
+                         cudaMemcpyHostToDevice));
+    PLAN_CUDA(cudaMemcpy(plan->d_slice_sigma, sigmas, n_levels * sizeof(double),
+                         cudaMemcpyHostToDevice));
+    PLAN_CUDA(cudaMemcpy(plan->d_sigma_f32, sig32.data(), n_levels * sizeof(float),
+                         cudaMemcpyHostToDevice));
+    PLAN_CUDA(configure_conv_kernels(max_table));
+#undef PLAN_CUDA
+
+    const size_t plane = (size_t)g.Hp * g.Wp * sizeof(float);
+    size_t off = 0;
+    plan->off_rows_t = off; off += align_up(plane * n_levels, 256);
+    plan->off_dog_t = off;  off += align_up(plane * n_levels, 256);   // L planes: also holds levels
+    plan->off_blobspace = off; off += blobspace_bytes(max_blobs);
+    plan->total = off;
+    *out = plan;
+    return DOGBLOB_OK;
+}
+
+void dogblob_plan_destroy(dogblob_plan *plan) {
+    if (!plan) return;
+    DeviceGuard guard(plan->device);
+    cudaFree(plan->d_levels);
+    cudaFree(plan->d_taps);
+    cudaFree(plan->d_level_order);
+    cudaFree(plan->d_group_begin);
+    cudaFree(plan->d_unit_groups);
+    cudaFree(plan->d_slice_sigma);
+    cudaFree(plan->d_sigma_f32);
+    delete plan;
+}
+
+size_t dogblob_workspace_bytes(const dogblob_plan *plan) { return plan ? plan->total : 0; }
+size_t dogblob_result_bytes_for(int max_blobs) {
+    return DOGBLOB_RESULT_HEADER_BYTES + (size_t)std::max(max_blobs, 0) * sizeof(dogblob_blob);
+}
+size_t dogblob_result_bytes(const dogblob_plan *plan) {
+    return plan ? dogblob_result_bytes_for(plan->max_blobs) : 0;
+}
+int64_t dogblob_image_pitch(const dogblob_plan *plan) { return plan ? plan->geo.Wp : 0; }
+size_t dogblob_blobspace_bytes(int max_blobs) { return blobspace_bytes(std::max(max_blobs, 1)); }
+
+static int check_threshold_args(int neighborhood, double overlap) {
+    DB_REQUIRE(neighborhood >= 1 && neighborhood % 2 == 1, "neighborhood must be odd and >= 1");
+    DB_REQUIRE(overlap >= 0.0 && overlap <= 1.0, "overlap threshold must be in [0, 1]");
+    return DOGBLOB_OK;
+}
+
+int dogblob_detect(const dogblob_plan *plan, const float *d_image, float threshold,
+                   int neighborhood, double overlap, int prune, void *d_workspace,
+                   void *d_result, void *stream, void *const *events) {
+    DB_REQUIRE(plan && d_image && d_workspace && d_result, "NULL argument");
+    if (int rc = check_threshold_args(neighborhood, overlap)) return rc;
+    DeviceGuard guard(plan->device);
+    DB_REQUIRE(guard.ok, "cannot select CUDA device");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    char *ws = reinterpret_cast<char *>(d_workspace);
+    float *rows_t = reinterpret_cast<float *>(ws + plan->off_rows_t);
+    float *dog_t = reinterpret_cast<float *>(ws + plan->off_dog_t);
+    BlobSpace bs = carve_blobspace(ws + plan->off_blobspace, plan->max_blobs);
+    const ConvGeometry &g = plan->geo;
+    auto ev = [&](int k) -> cudaError_t {
+        return events ? cudaEventRecord(reinterpret_cast<cudaEvent_t>(events[k]), st)
+                      : cudaSuccess;
+    };
+    DB_CUDA(ev(0));
+    DB_CUDA(launch_reset_counters(bs, st));
+    DB_CUDA(launch_row_pass(g, d_image, rows_t, plan->d_levels, plan->d_taps,
+                            plan->d_level_order, st));
+    DB_CUDA(launch_col_dog_pass(g, rows_t, dog_t, plan->d_levels, plan->d_taps,
+                                plan->d_group_begin, st));
+    DB_CUDA(ev(1));
+    // D^T planes: rows = x (W valid), cols = y (H valid)
+    DB_CUDA(launch_extrema(dog_t, g.L - 1, g.W, g.H, g.Hp, (int64_t)g.Hp * g.Wp, true,
+                           plan->d_slice_sigma, threshold, neighborhood / 2, bs, st));
+    DB_CUDA(ev(2));
+    DB_CUDA(launch_prune_and_pack(bs, overlap, prune != 0, d_result, plan->max_blobs, st));
+    DB_CUDA(ev(3));
+    return DOGBLOB_OK;
+}
+
+int dogblob_upload_image(const dogblob_plan *plan, const float *h_image, void *d_image,
+                         void *stream) {
+    DB_REQUIRE(plan && h_image && d_image, "NULL argument");
+    DeviceGuard guard(plan->device);
+    DB_REQUIRE(guard.ok, "cannot select CUDA device");
+    const ConvGeometry &g = plan->geo;
+    DB_CUDA(cudaMemcpy2DAsync(d_image, (size_t)g.Wp * sizeof(float), h_image,
+                              (size_t)g.W * sizeof(float), (size_t)g.W * sizeof(float), g.H,
+                              cudaMemcpyHostToDevice, reinterpret_cast<cudaStream_t>(stream)));
+    return DOGBLOB_OK;
+}
+
+int dogblob_detect_host(const dogblob_plan *plan, const float *h_image, float threshold,
+                        int neighborhood, double overlap, int prune, void *d_image,
+                        void *d_workspace, void *d_result, void *h_result, int h_result_blobs,
+                        void *stream, void *const *events) {
+    DB_REQUIRE(h_result != nullptr && h_result_blobs >= 0, "bad host result buffer");
+    if (int rc = dogblob_upload_image(plan, h_image, d_image, stream)) return rc;
+    if (int rc = dogblob_detect(plan, reinterpret_cast<const float *>(d_image), threshold,
+                                neighborhood, overlap, prune, d_workspace, d_result, stream,
+                                events))
+        return rc;
+    const int nb = std::min(h_result_blobs, plan->max_blobs);
+    DB_CUDA(cudaMemcpyAsync(h_result, d_result,
+                            DOGBLOB_RESULT_HEADER_BYTES + (size_t)nb * sizeof(dogblob_blob),
+                            cudaMemcpyDeviceToHost, reinterpret_cast<cudaStream_t>(stream)));
+    return DOGBLOB_OK;
+}
+
+int dogblob_fetch_blobs(const void *d_result, int first, int count, dogblob_blob *h_out,
+                        void *stream) {
+    DB_REQUIRE(d_result && h_out && first >= 0 && count >= 0, "bad argument");
+    if (count == 0) return DOGBLOB_OK;
+    const char *src = reinterpret_cast<const char *>(d_result) + DOGBLOB_RESULT_HEADER_BYTES +
+                      (size_t)first * sizeof(dogblob_blob);
+    DB_CUDA(cudaMemcpyAsync(h_out, src, (size_t)count * sizeof(dogblob_blob),
+                            cudaMemcpyDeviceToHost, reinterpret_cast<cudaStream_t>(stream)));
+    return DOGBLOB_OK;
+}
+
+int dogblob_scale_space(const dogblob_plan *plan, const float *d_image, void *d_workspace,
+                        float *d_levels, void *stream) {
+    DB_REQUIRE(plan && d_image && d_workspace && d_levels, "NULL argument");
+    DeviceGuard guard(plan->device);
+    DB_REQUIRE(guard.ok, "cannot select CUDA device");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    char *ws = reinterpret_cast<char *>(d_workspace);
+    float *rows_t = reinterpret_cast<float *>(ws + plan->off_rows_t);
+    float *lev_t = reinterpret_cast<float *>(ws + plan->off_dog_t);
+    const ConvGeometry &g = plan->geo;
+    DB_CUDA(launch_row_pass(g, d_image, rows_t, plan->d_levels, plan->d_taps,
+                            plan->d_level_order, st));
+    DB_CUDA(launch_col_levels_pass(g, rows_t, lev_t, plan->d_levels, plan->d_taps,
+                                   plan->d_unit_groups, st));
+    DB_CUDA(launch_untranspose(lev_t, g.L, g.Hp, g.Wp, g.H, g.W, d_levels, st));
+    return DOGBLOB_OK;
+}
+
+int dogblob_dog(const dogblob_plan *plan, const float *d_image, void *d_workspace,
+                float *d_slices, void *stream) {
+    DB_REQUIRE(plan && d_image && d_workspace && d_slices, "NULL argument");
+    DeviceGuard guard(plan->device);
+    DB_REQUIRE(guard.ok, "cannot select CUDA device");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    char *ws = reinterpret_cast<char *>(d_workspace);
+    float *rows_t = reinterpret_cast<float *>(ws + plan->off_rows_t);
+    float *dog_t = reinterpret_cast<float *>(ws + plan->off_dog_t);
+    const ConvGeometry &g = plan->geo;
+    DB_CUDA(launch_row_pass(g, d_image, rows_t, plan->d_levels, plan->d_taps,
+                            plan->d_level_order, st));
+    DB_CUDA(launch_col_dog_pass(g, rows_t, dog_t, plan->d_levels, plan->d_taps,
+                                plan->d_group_begin, st));
+    DB_CUDA(launch_untranspose(dog_t, g.L - 1, g.Hp, g.Wp, g.H, g.W, d_slices, st));
+    return DOGBLOB_OK;
+}
+
+int dogblob_dog_from_levels(int n_levels, int height, int width, const float *d_levels,
+                            const double *sigmas, float *d_slices, void *stream) {
+    DB_REQUIRE(n_levels >= 2 && height >= 1 && width >= 1, "bad stack shape");
+    DB_REQUIRE(d_levels && sigmas && d_slices, "NULL argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    std::vector<float> s32(n_levels);
+    for (int i = 0; i < n_levels; ++i) s32[i] = (float)sigmas[i];
+    float *d_s = nullptr;
+    DB_CUDA(cudaMallocAsync(&d_s, n_levels * sizeof(float), st));
+    DB_CUDA(cudaMemcpyAsync(d_s, s32.data(), n_levels * sizeof(float), cudaMemcpyHostToDevice, st));
+    DB_CUDA(cudaStreamSynchronize(st));   // s32 is a stack-lifetime host buffer
+    DB_CUDA(launch_dog_from_levels(n_levels, (int64_t)height * width, d_levels, d_s, d_slices, st));
+    DB_CUDA(cudaFreeAsync(d_s, st));
+    return DOGBLOB_OK;
+}
+
+int dogblob_extrema(int n_slices, int height, int width, const float *d_slices,
+                    const double *slice_sigmas, float threshold, int neighborhood, int max_blobs,
+                    void *d_blobspace, void *d_result, void *stream) {
+    DB_REQUIRE(n_slices >= 1 && height >= 1 && width >= 1, "bad stack shape");
+    DB_REQUIRE(d_slices && slice_sigmas && d_blobspace && d_result && max_blobs >= 1,
+               "bad argument");
+    if (int rc = check_threshold_args(neighborhood, 0.0)) return rc;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    BlobSpace bs = carve_blobspace(d_blobspace, max_blobs);
+    double *d_sig = nullptr;
+    DB_CUDA(cudaMallocAsync(&d_sig, n_slices * sizeof(double), st));
+    DB_CUDA(cudaMemcpyAsync(d_sig, slice_sigmas, n_slices * sizeof(double),
+                            cudaMemcpyHostToDevice, st));
+    DB_CUDA(cudaStreamSynchronize(st));
+    DB_CUDA(launch_reset_counters(bs, st));
+    DB_CUDA(launch_extrema(d_slices, n_slices, height, width, width, (int64_t)height * width,
+                           false, d_sig, threshold, neighborhood / 2, bs, st));
+    DB_CUDA(launch_prune_and_pack(bs, 0.0, false, d_result, max_blobs, st));
+    DB_CUDA(cudaFreeAsync(d_sig, st));
+    return DOGBLOB_OK;
+}
+
+int dogblob_prune(int n, const dogblob_blob *d_blobs_in, double overlap, int max_blobs,
+                  void *d_blobspace, void *d_result, void *stream) {
+    DB_REQUIRE(n >= 0 && max_blobs >= 1 && n <= max_blobs, "blob count exceeds max_blobs");
+    DB_REQUIRE(d_blobspace && d_result && (n == 0 || d_blobs_in), "NULL argument");
+    if (int rc = check_threshold_args(3, overlap)) return rc;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    BlobSpace bs = carve_blobspace(d_blobspace, max_blobs);
+    DB_CUDA(launch_reset_counters(bs, st));
+    DB_CUDA(launch_load_blobs(bs, d_blobs_in, n, st));
+    DB_CUDA(launch_prune_and_pack(bs, overlap, true, d_result, max_blobs, st));
+    return DOGBLOB_OK;
+}
+
+int dogblob_event_create(void **event) {
+    DB_REQUIRE(event != nullptr, "NULL argument");
+    cudaEvent_t e;
+    DB_CUDA(cudaEventCreate(&e));
+    *event = e;
+    return DOGBLOB_OK;
+}
+int dogblob_event_destroy(void *event) {
+    DB_CUDA(cudaEventDestroy(reinterpret_cast<cudaEvent_t>(event)));
+    return DOGBLOB_OK;
+}
+int dogblob_event_elapsed_ms(void *start, void *stop, float *ms) {
+    DB_REQUIRE(ms != nullptr, "NULL argument");
+    DB_CUDA(cudaEventElapsedTime(ms, reinterpret_cast<cudaEvent_t>(start),
+                                 reinterpret_cast<cudaEvent_t>(stop)));
+    return DOGBLOB_OK;
+}
+int dogblob_stream_sync(void *stream) {
+    DB_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
+    return DOGBLOB_OK;
+}
+int dogblob_device_count(int *count) {
+    DB_REQUIRE(count != nullptr, "NULL argument");
+    DB_CUDA(cudaGetDeviceCount(count));
+    return DOGBLOB_OK;
+}
+
+}  // extern "C"

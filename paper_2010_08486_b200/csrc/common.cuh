@@ -1,0 +1,122 @@
+// Shared declarations of the dogblob_b200 CUDA library (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string>
+
+#include "../../include/dogblob_b200.h"
+
+namespace dogblob {
+
+// ---- error plumbing --------------------------------------------------------
+void set_error(const std::string &msg);
+
+#define DB_CUDA(expr)                                                              \
+    do {                                                                           \
+        cudaError_t _e = (expr);                                                   \
+        if (_e != cudaSuccess) {                                                   \
+            ::dogblob::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+            return DOGBLOB_ECUDA;                                                  \
+        }                                                                          \
+    } while (0)
+
+#define DB_REQUIRE(cond, msg)                  \
+    do {                                       \
+        if (!(cond)) {                         \
+            ::dogblob::set_error(msg);         \
+            return DOGBLOB_EINVAL;             \
+        }                                      \
+    } while (0)
+
+// ---- tiling constants of the separable convolution ---------------------------
+constexpr int kTY = 16;                 // outputs per thread along the convolved axis
+constexpr int kWarps = 8;               // warps per CTA, stacked along the convolved axis
+constexpr int kTileRows = kTY * kWarps; // 128
+constexpr int kTileCols = 128;          // contiguous floats per CTA (4 per lane)
+constexpr int kPad = 128;               // plane dimensions are padded to this
+constexpr int kPrefetch = 4;            // input rows in flight per thread
+constexpr int kConvThreads = 32 * kWarps;
+
+struct LevelDesc {
+    int radius;       // r_i = ceil(truncate * sigma_i)
+    int n_chunks;     // ceil((kTY + 2 r) / kTY) sweeps of kTY input rows
+    int tap_ofs;      // start (in float2) of this level's padded tap table
+    float sigma_f32;  // float32(sigma_i), the DoG scale factor
+};
+
+// ---- blob bookkeeping shared by extrema / prune ------------------------------
+struct Counters {            // one per result, lives in the blob space
+    int n_flagged;           // voxels passing the NMS + threshold test
+    int n_plateau;           // plateau members appended to `plateau`
+    int n_candidates;        // blobs before pruning (singles + plateau components)
+    int n_blobs;             // final
+    int n_merges;
+    unsigned flags;
+    int pad[10];
+};
+
+struct Voxel { int s, row, col; float val; };
+
+// Layout of the blob space (device), all arrays sized by `cap`.
+struct BlobSpace {
+    Counters *ctr;
+    Voxel *plateau;              // plateau members
+    int *parent;                 // union-find over plateau members
+    int *pl_count;               // per-root member count
+    unsigned long long *pl_sum_row, *pl_sum_col;
+    dogblob_blob *unsorted;      // candidates in emission order
+    dogblob_blob *sorted;        // candidates in (-response, y, x, sigma) order
+    int *first;                  // prune: smallest offending partner j > i, or -1
+    int *alive;
+    int *cell_of;                // prune grid
+    int *cell_start;             // kMaxCells + 1
+    int *cell_fill;              // kMaxCells
+    int *cell_items;
+    double *grid_params;         // [0]=x0 [1]=y0 [2]=cell size [3]=gx [4]=gy
+    int cap;
+};
+
+constexpr int kMaxCellsPerAxis = 256;
+constexpr int kMaxCells = kMaxCellsPerAxis * kMaxCellsPerAxis;
+
+size_t blobspace_bytes(int cap);
+BlobSpace carve_blobspace(void *base, int cap);
+
+// ---- launchers (defined in the .cu files) ------------------------------------
+struct ConvGeometry {
+    int H, W;            // image
+    int Hp, Wp;          // padded to kPad
+    int L;               // levels
+    int G;               // level groups of the fused column+DoG pass
+    int max_table;       // float2 entries of the longest padded tap table
+};
+
+cudaError_t launch_row_pass(const ConvGeometry &g, const float *d_img, float *d_rows_t,
+                            const LevelDesc *d_levels, const float2 *d_taps,
+                            const int *d_level_order, cudaStream_t st);
+cudaError_t launch_col_dog_pass(const ConvGeometry &g, const float *d_rows_t, float *d_dog_t,
+                                const LevelDesc *d_levels, const float2 *d_taps,
+                                const int *d_group_begin, cudaStream_t st);
+cudaError_t launch_col_levels_pass(const ConvGeometry &g, const float *d_rows_t, float *d_lev_t,
+                                   const LevelDesc *d_levels, const float2 *d_taps,
+                                   const int *d_unit_groups, cudaStream_t st);
+cudaError_t launch_untranspose(const float *d_src_t, int planes, int Hp, int Wp, int H, int W,
+                               float *d_dst, cudaStream_t st);
+cudaError_t launch_dog_from_levels(int L, int64_t plane_elems, const float *d_levels,
+                                   const float *d_sigma_f32, float *d_out, cudaStream_t st);
+cudaError_t configure_conv_kernels(int max_table);
+
+// extrema: NMS + compaction + plateau coalescing + ordering
+cudaError_t launch_extrema(const float *d_slices, int S, int rows, int cols, int64_t pitch,
+                           int64_t plane, bool transposed, const double *d_slice_sigma,
+                           float threshold, int half, const BlobSpace &bs, cudaStream_t st);
+// pruning + final packing into the result buffer
+cudaError_t launch_prune_and_pack(const BlobSpace &bs, double overlap, bool prune,
+                                  void *d_result, int result_cap, cudaStream_t st);
+cudaError_t launch_load_blobs(const BlobSpace &bs, const dogblob_blob *d_in, int n,
+                              cudaStream_t st);
+cudaError_t launch_reset_counters(const BlobSpace &bs, cudaStream_t st);
+
+}  // namespace dogblob

@@ -1,0 +1,308 @@
+// Scale-space extrema for sm_100a: 3-D non-maximum suppression with threshold,
+// warp-ballot/popc stream compaction, plateau coalescing and ordering.
+//
+// Replaces find_extrema / _coalesce_plateaus / _sort_blobs
+// (pkg/src/dogblob/detector.py:129-193):
+//   flagged(v)  <=>  D[v] == max over the n^3 block (missing neighbours = -inf)
+//                    and D[v] > float32(threshold)
+//               <=>  D[v] > thr and no neighbour is strictly greater;
+//   8-connected flagged voxels of one slice form one blob at the half-even
+//   rounded centroid (adjacent flagged voxels necessarily share one value);
+//   blobs are ordered by (-response, y, x, sigma).
+//
+// The volume is read exactly once, as float4 along the contiguous axis; only
+// voxels above the threshold (a few per million) touch their neighbours.
+#include "common.cuh"
+
+namespace dogblob {
+
+namespace {
+
+struct Volume {
+    const float *__restrict__ data;
+    int S, rows, cols;           // valid extents
+    int64_t pitch, plane;
+    __device__ __forceinline__ float at(int s, int r, int c) const {
+        return __ldg(data + (int64_t)s * plane + (int64_t)r * pitch + c);
+    }
+};
+
+// no neighbour in the (2h+1)^3 block is strictly greater than v
+__device__ bool is_block_max(const Volume &vol, int s, int r, int c, float v, int h) {
+    const int s0 = max(s - h, 0), s1 = min(s + h, vol.S - 1);
+    const int r0 = max(r - h, 0), r1 = min(r + h, vol.rows - 1);
+    const int c0 = max(c - h, 0), c1 = min(c + h, vol.cols - 1);
+    for (int ss = s0; ss <= s1; ++ss)
+        for (int rr = r0; rr <= r1; ++rr)
+            for (int cc = c0; cc <= c1; ++cc)
+                if (vol.at(ss, rr, cc) > v) return false;
+    return true;
+}
+
+// does a flagged voxel share an in-slice 8-neighbour that is flagged too?
+__device__ bool has_flagged_neighbour(const Volume &vol, int s, int r, int c, float v, int h) {
+    for (int dr = -1; dr <= 1; ++dr)
+        for (int dc = -1; dc <= 1; ++dc) {
+            if (dr == 0 && dc == 0) continue;
+            const int rr = r + dr, cc = c + dc;
+            if (rr < 0 || rr >= vol.rows || cc < 0 || cc >= vol.cols) continue;
+            if (vol.at(s, rr, cc) == v && is_block_max(vol, s, rr, cc, v, h)) return true;
+        }
+    return false;
+}
+
+__device__ __forceinline__ dogblob_blob make_blob(int s, double x, double y, float val, int S,
+                                                  const double *__restrict__ slice_sigma) {
+    dogblob_blob b;
+    b.x = x;
+    b.y = y;
+    b.sigma = slice_sigma[s];
+    b.radius = 1.4142135623730951 * b.sigma;   // math.sqrt(2.0) * sigma, one rounding
+    b.response = (double)val;
+    b.slice = s;
+    b.flags = (s == 0 || s == S - 1) ? DOGBLOB_BLOB_SCALE_EDGE : 0u;
+    return b;
+}
+
+// ---- NMS + compaction -----------------------------------------------------------
+template <int VEC>
+__global__ void __launch_bounds__(256)
+nms_kernel(Volume vol, float thr, int h, bool transposed, const double *__restrict__ slice_sigma,
+           BlobSpace bs) {
+    const int cols_v = (vol.cols + VEC - 1) / VEC;
+    const int64_t total = (int64_t)vol.S * vol.rows * cols_v;
+    const unsigned lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    // all lanes of a warp run the same number of iterations (ballots below)
+    const int64_t first = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t warp_first = first - lane;
+    for (int64_t base = warp_first; base < total; base += stride) {
+        const int64_t i = base + lane;
+        float v[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        int s = 0, r = 0, c = 0;
+        if (i < total) {
+            const int cv = (int)(i % cols_v);
+            const int64_t t = i / cols_v;
+            r = (int)(t % vol.rows);
+            s = (int)(t / vol.rows);
+            c = cv * VEC;
+            const float *p = vol.data + (int64_t)s * vol.plane + (int64_t)r * vol.pitch + c;
+            if (VEC == 4) {
+                const float4 q = __ldg(reinterpret_cast<const float4 *>(p));
+                v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+            } else {
+                v[0] = __ldg(p);
+            }
+        }
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) any |= (v[k] > thr) && (c + k < vol.cols);
+        if (!__any_sync(0xffffffffu, any)) continue;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+            bool flagged = false, plateau = false;
+            if (v[k] > thr && c + k < vol.cols && is_block_max(vol, s, r, c + k, v[k], h)) {
+                flagged = true;
+                plateau = has_flagged_neighbour(vol, s, r, c + k, v[k], h);
+            }
+            // warp-aggregated append: one atomic per warp and list
+            const unsigned m_single = __ballot_sync(0xffffffffu, flagged && !plateau);
+            const unsigned m_plat = __ballot_sync(0xffffffffu, flagged && plateau);
+            if (m_single | m_plat) {
+                const unsigned lt = (1u << lane) - 1u;
+                int base_s = 0, base_p = 0;
+                if (lane == 0) {
+                    atomicAdd(&bs.ctr->n_flagged, __popc(m_single) + __popc(m_plat));
+                    if (m_single) base_s = atomicAdd(&bs.ctr->n_candidates, __popc(m_single));
+                    if (m_plat) base_p = atomicAdd(&bs.ctr->n_plateau, __popc(m_plat));
+                }
+                base_s = __shfl_sync(0xffffffffu, base_s, 0);
+                base_p = __shfl_sync(0xffffffffu, base_p, 0);
+                if (flagged && !plateau) {
+                    const int idx = base_s + __popc(m_single & lt);
+                    if (idx < bs.cap) {
+                        const int cc = c + k;
+                        bs.unsorted[idx] = make_blob(s, transposed ? r : cc, transposed ? cc : r,
+                                                     v[k], vol.S, slice_sigma);
+                    } else {
+                        atomicOr(&bs.ctr->flags, DOGBLOB_FLAG_OVERFLOW);
+                    }
+                } else if (flagged) {
+                    const int idx = base_p + __popc(m_plat & lt);
+                    if (idx < bs.cap) {
+                        bs.plateau[idx] = Voxel{s, r, c + k, v[k]};
+                        bs.parent[idx] = idx;
+                        bs.pl_count[idx] = 0;
+                        bs.pl_sum_row[idx] = 0ull;
+                        bs.pl_sum_col[idx] = 0ull;
+                    } else {
+                        atomicOr(&bs.ctr->flags, DOGBLOB_FLAG_OVERFLOW);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ---- plateau coalescing: lock-free union-find over the (rare) plateau members ----
+__device__ __forceinline__ int uf_find(int *parent, int x) {
+    int p = ((volatile int *)parent)[x];
+    while (p != x) { x = p; p = ((volatile int *)parent)[x]; }
+    return x;
+}
+__device__ void uf_union(int *parent, int a, int b) {
+    while (true) {
+        a = uf_find(parent, a);
+        b = uf_find(parent, b);
+        if (a == b) return;
+        if (a > b) { int t = a; a = b; b = t; }
+        if (atomicCAS(&parent[b], b, a) == b) return;   // larger root hooks under smaller
+    }
+}
+
+__global__ void __launch_bounds__(256) plateau_link_kernel(BlobSpace bs) {
+    const int n = min(bs.ctr->n_plateau, bs.cap);
+    if (n == 0) return;
+    __shared__ Voxel tile[256];
+    for (int a0 = blockIdx.x * blockDim.x; a0 < n; a0 += gridDim.x * blockDim.x) {
+        const int a = a0 + threadIdx.x;
+        Voxel va = (a < n) ? bs.plateau[a] : Voxel{-9, -9, -9, 0.f};
+        for (int b0 = 0; b0 < a0 + (int)blockDim.x && b0 < n; b0 += blockDim.x) {
+            __syncthreads();
+            if (b0 + (int)threadIdx.x < n) tile[threadIdx.x] = bs.plateau[b0 + threadIdx.x];
+            __syncthreads();
+            const int lim = min((int)blockDim.x, n - b0);
+            if (a < n)
+                for (int k = 0; k < lim; ++k) {
+                    const int b = b0 + k;
+                    if (b >= a) break;
+                    const Voxel vb = tile[k];
+                    if (vb.s == va.s && abs(vb.row - va.row) <= 1 && abs(vb.col - va.col) <= 1)
+                        uf_union(bs.parent, a, b);
+                }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) plateau_reduce_kernel(BlobSpace bs) {
+    const int n = min(bs.ctr->n_plateau, bs.cap);
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) {
+        const int root = uf_find(bs.parent, a);
+        const Voxel v = bs.plateau[a];
+        atomicAdd(&bs.pl_count[root], 1);
+        atomicAdd(&bs.pl_sum_row[root], (unsigned long long)v.row);
+        atomicAdd(&bs.pl_sum_col[root], (unsigned long long)v.col);
+    }
+}
+
+__global__ void __launch_bounds__(256)
+plateau_emit_kernel(BlobSpace bs, int S, bool transposed, const double *__restrict__ slice_sigma) {
+    const int n = min(bs.ctr->n_plateau, bs.cap);
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) {
+        if (bs.parent[a] != a) continue;
+        const Voxel v = bs.plateau[a];
+        const double cnt = (double)bs.pl_count[a];
+        // ndimage.center_of_mass: float64 sum / count, then Python round() = half-even
+        const double cr = rint((double)bs.pl_sum_row[a] / cnt);
+        const double cc = rint((double)bs.pl_sum_col[a] / cnt);
+        const int idx = atomicAdd(&bs.ctr->n_candidates, 1);
+        if (idx < bs.cap)
+            bs.unsorted[idx] = make_blob(v.s, transposed ? cr : cc, transposed ? cc : cr, v.val, S,
+                                         slice_sigma);
+        else
+            atomicOr(&bs.ctr->flags, DOGBLOB_FLAG_OVERFLOW);
+    }
+}
+
+// ---- ordering: rank sort on the full key (stable on the input index) ----------------
+struct SortKey { double resp, y, x, sigma; };
+
+__device__ __forceinline__ bool key_before(const SortKey &a, int ia, const SortKey &b, int ib) {
+    // sorted(key=(-response, y, x, sigma)); ties keep input order
+    if (a.resp != b.resp) return a.resp > b.resp;
+    if (a.y != b.y) return a.y < b.y;
+    if (a.x != b.x) return a.x < b.x;
+    if (a.sigma != b.sigma) return a.sigma < b.sigma;
+    return ia < ib;
+}
+
+__global__ void __launch_bounds__(256) rank_sort_kernel(BlobSpace bs) {
+    const int n = min(bs.ctr->n_candidates, bs.cap);
+    __shared__ SortKey tile[256];
+    for (int i0 = blockIdx.x * blockDim.x; i0 < n; i0 += gridDim.x * blockDim.x) {
+        const int i = i0 + threadIdx.x;
+        dogblob_blob me;
+        SortKey mk = {0, 0, 0, 0};
+        if (i < n) {
+            me = bs.unsorted[i];
+            mk = SortKey{me.response, me.y, me.x, me.sigma};
+        }
+        int rank = 0;
+        for (int j0 = 0; j0 < n; j0 += blockDim.x) {
+            __syncthreads();
+            if (j0 + (int)threadIdx.x < n) {
+                const dogblob_blob o = bs.unsorted[j0 + threadIdx.x];
+                tile[threadIdx.x] = SortKey{o.response, o.y, o.x, o.sigma};
+            }
+            __syncthreads();
+            const int lim = min((int)blockDim.x, n - j0);
+            if (i < n)
+                for (int k = 0; k < lim; ++k) rank += key_before(tile[k], j0 + k, mk, i) ? 1 : 0;
+        }
+        if (i < n) bs.sorted[rank] = me;
+    }
+}
+
+__global__ void reset_counters_kernel(BlobSpace bs) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        Counters z = {};
+        *bs.ctr = z;
+    }
+}
+
+__global__ void load_blobs_kernel(BlobSpace bs, const dogblob_blob *__restrict__ in, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        bs.unsorted[i] = in[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) bs.ctr->n_candidates = n;
+}
+
+}  // namespace
+
+cudaError_t launch_reset_counters(const BlobSpace &bs, cudaStream_t st) {
+    reset_counters_kernel<<<1, 32, 0, st>>>(bs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_load_blobs(const BlobSpace &bs, const dogblob_blob *d_in, int n,
+                              cudaStream_t st) {
+    int blocks = (n + 255) / 256;
+    if (blocks < 1) blocks = 1;
+    if (blocks > 296) blocks = 296;
+    load_blobs_kernel<<<blocks, 256, 0, st>>>(bs, d_in, n);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    rank_sort_kernel<<<296, 256, 0, st>>>(bs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_extrema(const float *d_slices, int S, int rows, int cols, int64_t pitch,
+                           int64_t plane, bool transposed, const double *d_slice_sigma,
+                           float threshold, int half, const BlobSpace &bs, cudaStream_t st) {
+    Volume vol{d_slices, S, rows, cols, pitch, plane};
+    const bool vec4 = (pitch % 4 == 0) && (plane % 4 == 0) &&
+                      ((reinterpret_cast<uintptr_t>(d_slices) & 15u) == 0);
+    const int grid = 148 * 8;
+    if (vec4)
+        nms_kernel<4><<<grid, 256, 0, st>>>(vol, threshold, half, transposed, d_slice_sigma, bs);
+    else
+        nms_kernel<1><<<grid, 256, 0, st>>>(vol, threshold, half, transposed, d_slice_sigma, bs);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    plateau_link_kernel<<<296, 256, 0, st>>>(bs);
+    plateau_reduce_kernel<<<148, 256, 0, st>>>(bs);
+    plateau_emit_kernel<<<148, 256, 0, st>>>(bs, S, transposed, d_slice_sigma);
+    rank_sort_kernel<<<296, 256, 0, st>>>(bs);
+    return cudaGetLastError();
+}
+
+}  // namespace dogblob

@@ -1,0 +1,368 @@
+// Overlap pruning on the GPU with the reference's exact sequential semantics.
+//
+// Replaces prune_overlaps / _overlap_matrix (pkg/src/dogblob/detector.py:221-280),
+// which the paper left on the CPU.  The reference repeats
+//   { dense N x N overlap matrix; take the row-major-first pair (i < j) of the
+//     response-sorted list with overlap > thr; blob i keeps centre/response,
+//     radius <- mean, sigma <- radius / sqrt 2, OR the boundary flags; delete j }
+// until no pair offends.  Here the blobs are bucketed on a uniform grid whose
+// cell is >= 2 r_max (an offending pair needs d < r_i + r_j, and merged radii
+// never exceed r_max), `first[i]` caches the smallest offending partner j > i,
+// and one persistent CTA replays the merge order, touching only the 3x3 cell
+// neighbourhoods a merge can change.  All overlap arithmetic is float64 with
+// the operation order of the reference (compiled with -fmad=false).
+#include <float.h>
+
+#include "common.cuh"
+
+namespace dogblob {
+
+namespace {
+
+constexpr int kLoopThreads = 1024;
+constexpr double kPi = 3.141592653589793;
+constexpr double kSqrt2 = 1.4142135623730951;
+
+// hypot for the centre distance: exact sqrt for integer offsets (the pipeline
+// case), one Newton correction otherwise; both agree with a correctly rounded
+// hypot except on rare half-ulp cases.
+__device__ __forceinline__ double centre_distance(double dx, double dy) {
+    const double s = dx * dx + dy * dy;
+    if (dx == rint(dx) && dy == rint(dy) && fabs(dx) < 33554432.0 && fabs(dy) < 33554432.0)
+        return sqrt(s);
+    return hypot(dx, dy);
+}
+
+// normalised overlap of matrix entry [i][j] (detector.py:221-247)
+__device__ double overlap_ij(double xi, double yi, double ri, double xj, double yj, double rj) {
+    const double d = centre_distance(xi - xj, yi - yj);
+    const double rmin = fmin(ri, rj), rmax = fmax(ri, rj);
+    if (d <= rmax - rmin) return 1.0;
+    if (!(d < ri + rj) || !(d > 0.0)) return 0.0;
+    double c1 = (d * d + ri * ri - rj * rj) / (2.0 * d * ri);
+    double c2 = (d * d + rj * rj - ri * ri) / (2.0 * d * rj);
+    c1 = fmin(fmax(c1, -1.0), 1.0);
+    c2 = fmin(fmax(c2, -1.0), 1.0);
+    const double a1 = ri * ri * acos(c1);
+    const double a2 = rj * rj * acos(c2);
+    double q = (-d + ri + rj) * (d + ri - rj) * (d - ri + rj) * (d + ri + rj);
+    q = fmax(q, 0.0);
+    const double s = 0.5 * sqrt(q);
+    return (a1 + a2 - s) / (kPi * rmin * rmin);
+}
+
+struct Grid {
+    double x0, y0, cell;
+    int gx, gy;
+    __device__ __forceinline__ int cx(double x) const {
+        int c = (int)floor((x - x0) / cell);
+        return min(max(c, 0), gx - 1);
+    }
+    __device__ __forceinline__ int cy(double y) const {
+        int c = (int)floor((y - y0) / cell);
+        return min(max(c, 0), gy - 1);
+    }
+};
+
+__device__ __forceinline__ Grid load_grid(const BlobSpace &bs) {
+    Grid g;
+    g.x0 = bs.grid_params[0];
+    g.y0 = bs.grid_params[1];
+    g.cell = bs.grid_params[2];
+    g.gx = (int)bs.grid_params[3];
+    g.gy = (int)bs.grid_params[4];
+    return g;
+}
+
+template <typename T, typename Op>
+__device__ T block_reduce(T v, Op op, T *scratch /* >= 32 */) {
+    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) scratch[w] = v;
+    __syncthreads();
+    const int nw = (blockDim.x + 31) >> 5;
+    T r = scratch[0];
+    for (int k = 1; k < nw; ++k) r = op(r, scratch[k]);
+    return r;
+}
+
+// ---- build the grid (single CTA): extents, cell size, counting sort -------------------
+__global__ void __launch_bounds__(kLoopThreads) prune_build_kernel(BlobSpace bs) {
+    __shared__ double sd[32];
+    __shared__ int si[32];
+    const int n = min(bs.ctr->n_candidates, bs.cap);
+    const int tid = threadIdx.x;
+    double xmin = DBL_MAX, xmax = -DBL_MAX, ymin = DBL_MAX, ymax = -DBL_MAX, rmax = 0.0;
+    for (int i = tid; i < n; i += blockDim.x) {
+        const dogblob_blob b = bs.sorted[i];
+        xmin = fmin(xmin, b.x); xmax = fmax(xmax, b.x);
+        ymin = fmin(ymin, b.y); ymax = fmax(ymax, b.y);
+        rmax = fmax(rmax, b.radius);
+        bs.alive[i] = 1;
+        bs.first[i] = -1;
+    }
+    auto fmn = [](double a, double b) { return fmin(a, b); };
+    auto fmx = [](double a, double b) { return fmax(a, b); };
+    xmin = block_reduce(xmin, fmn, sd); xmax = block_reduce(xmax, fmx, sd);
+    ymin = block_reduce(ymin, fmn, sd); ymax = block_reduce(ymax, fmx, sd);
+    rmax = block_reduce(rmax, fmx, sd);
+    if (n == 0) { xmin = ymin = 0.0; xmax = ymax = 1.0; }
+    double cell = fmax(2.0 * rmax, 1e-9) * 1.0000001;   // strictly covers d < r_i + r_j
+    cell = fmax(cell, fmax(xmax - xmin, ymax - ymin) / (double)(kMaxCellsPerAxis - 1));
+    const int gx = min(kMaxCellsPerAxis, (int)floor((xmax - xmin) / cell) + 1);
+    const int gy = min(kMaxCellsPerAxis, (int)floor((ymax - ymin) / cell) + 1);
+    if (tid == 0) {
+        bs.grid_params[0] = xmin; bs.grid_params[1] = ymin; bs.grid_params[2] = cell;
+        bs.grid_params[3] = (double)gx; bs.grid_params[4] = (double)gy;
+    }
+    Grid g{xmin, ymin, cell, gx, gy};
+    const int ncell = gx * gy;
+    for (int c = tid; c <= ncell; c += blockDim.x) bs.cell_start[c] = 0;
+    for (int c = tid; c < ncell; c += blockDim.x) bs.cell_fill[c] = 0;
+    __syncthreads();
+    for (int i = tid; i < n; i += blockDim.x) {
+        const dogblob_blob b = bs.sorted[i];
+        const int c = g.cy(b.y) * gx + g.cx(b.x);
+        bs.cell_of[i] = c;
+        atomicAdd(&bs.cell_start[c + 1], 1);
+    }
+    __syncthreads();
+    // inclusive scan of cell_start[1..ncell] in chunks of blockDim.x
+    __shared__ int carry;
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    for (int c0 = 1; c0 <= ncell; c0 += blockDim.x) {
+        const int c = c0 + tid;
+        int v = (c <= ncell) ? bs.cell_start[c] : 0;
+        const int lane = tid & 31, w = tid >> 5;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
+        }
+        if (lane == 31) si[w] = v;
+        __syncthreads();
+        if (w == 0) {
+            int t = si[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += u;
+            }
+            si[lane] = t;
+        }
+        __syncthreads();
+        const int prefix = carry + (w > 0 ? si[w - 1] : 0);
+        if (c <= ncell) bs.cell_start[c] = v + prefix;
+        __syncthreads();
+        if (tid == blockDim.x - 1) carry = v + prefix;
+        __syncthreads();
+    }
+    for (int i = tid; i < n; i += blockDim.x) {
+        const int c = bs.cell_of[i];
+        const int slot = bs.cell_start[c] + atomicAdd(&bs.cell_fill[c], 1);
+        bs.cell_items[slot] = i;
+    }
+}
+
+// smallest alive j > i (or, with below=true, test only partner `only`) offending with i
+__device__ int scan_first_partner(const BlobSpace &bs, const Grid &g, int i, double thr,
+                                  int t, int nt) {
+    const dogblob_blob bi = bs.sorted[i];
+    const int cx = g.cx(bi.x), cy = g.cy(bi.y);
+    int best = INT_MAX;
+    for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.gy - 1); ++yy)
+        for (int xx = max(cx - 1, 0); xx <= min(cx + 1, g.gx - 1); ++xx) {
+            const int c = yy * g.gx + xx;
+            const int e = bs.cell_start[c + 1];
+            for (int p = bs.cell_start[c] + t; p < e; p += nt) {
+                const int j = bs.cell_items[p];
+                if (j <= i || j >= best || !bs.alive[j]) continue;
+                const dogblob_blob bj = bs.sorted[j];
+                if (overlap_ij(bi.x, bi.y, bi.radius, bj.x, bj.y, bj.radius) > thr) best = j;
+            }
+        }
+    return best;
+}
+
+// ---- first[i] for every blob: one warp per blob, whole GPU ---------------------------
+__global__ void __launch_bounds__(256) prune_first_kernel(BlobSpace bs, double thr) {
+    const int n = min(bs.ctr->n_candidates, bs.cap);
+    if (n < 2) return;
+    const Grid g = load_grid(bs);
+    const int lane = threadIdx.x & 31;
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+        int best = scan_first_partner(bs, g, i, thr, lane, 32);
+        for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+        if (lane == 0) bs.first[i] = (best == INT_MAX) ? -1 : best;
+    }
+}
+
+// ---- the sequential merge loop + final packing (single persistent CTA) ------------------
+__global__ void __launch_bounds__(kLoopThreads)
+prune_loop_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_header *hdr,
+                  dogblob_blob *out, int out_cap) {
+    __shared__ int s_red[32];
+    __shared__ int s_pos, s_list_n, s_carry;
+    __shared__ int s_list[kLoopThreads];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = min(bs.ctr->n_candidates, bs.cap);
+    int merges = 0;
+    auto imin = [](int a, int b) { return min(a, b); };
+
+    if (do_prune && n >= 2) {
+        const Grid g = load_grid(bs);
+        if (tid == 0) s_pos = 0;
+        __syncthreads();
+        while (true) {
+            // invariant: every alive i < s_pos has first[i] == -1
+            int istar = INT_MAX;
+            for (int base = s_pos; base < n; base += blockDim.x) {
+                const int i = base + tid;
+                int mine = (i < n && bs.alive[i] && bs.first[i] >= 0) ? i : INT_MAX;
+                mine = block_reduce(mine, imin, s_red);
+                if (mine != INT_MAX) { istar = mine; break; }
+            }
+            if (istar == INT_MAX) break;
+            const int j = bs.first[istar];
+            __syncthreads();
+            if (tid == 0) {
+                dogblob_blob a = bs.sorted[istar];
+                const dogblob_blob w = bs.sorted[j];
+                const double nr = 0.5 * (a.radius + w.radius);
+                a.radius = nr;
+                a.sigma = nr / kSqrt2;
+                a.flags |= (w.flags & DOGBLOB_BLOB_SCALE_EDGE) | DOGBLOB_BLOB_MERGED;
+                a.slice = -1;
+                bs.sorted[istar] = a;
+                bs.alive[j] = 0;
+                s_pos = istar;
+                s_list_n = 0;
+            }
+            ++merges;
+            __syncthreads();
+            const dogblob_blob bi = bs.sorted[istar];
+            const dogblob_blob bj = bs.sorted[j];
+            // (a) first[istar] again; (b) rows k < istar can only gain istar as partner
+            int best = INT_MAX;
+            {
+                const int cx = g.cx(bi.x), cy = g.cy(bi.y);
+                for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.gy - 1); ++yy)
+                    for (int xx = max(cx - 1, 0); xx <= min(cx + 1, g.gx - 1); ++xx) {
+                        const int c = yy * g.gx + xx;
+                        const int e = bs.cell_start[c + 1];
+                        for (int p = bs.cell_start[c] + tid; p < e; p += blockDim.x) {
+                            const int k = bs.cell_items[p];
+                            if (k == istar || !bs.alive[k]) continue;
+                            const dogblob_blob bk = bs.sorted[k];
+                            if (k > istar) {
+                                if (k < best &&
+                                    overlap_ij(bi.x, bi.y, bi.radius, bk.x, bk.y, bk.radius) > thr)
+                                    best = k;
+                            } else if (overlap_ij(bk.x, bk.y, bk.radius, bi.x, bi.y, bi.radius) >
+                                       thr) {
+                                bs.first[k] = istar;
+                                atomicMin(&s_pos, k);
+                            }
+                        }
+                    }
+            }
+            best = block_reduce(best, imin, s_red);
+            if (tid == 0) bs.first[istar] = (best == INT_MAX) ? -1 : best;
+            // (c) rows k > istar that pointed at the deleted blob need a new partner
+            {
+                const int cx = g.cx(bj.x), cy = g.cy(bj.y);
+                for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.gy - 1); ++yy)
+                    for (int xx = max(cx - 1, 0); xx <= min(cx + 1, g.gx - 1); ++xx) {
+                        const int c = yy * g.gx + xx;
+                        const int e = bs.cell_start[c + 1];
+                        for (int p = bs.cell_start[c] + tid; p < e; p += blockDim.x) {
+                            const int k = bs.cell_items[p];
+                            if (k != istar && bs.alive[k] && bs.first[k] == j) {
+                                const int slot = atomicAdd(&s_list_n, 1);
+                                if (slot < kLoopThreads) s_list[slot] = k;
+                            }
+                        }
+                    }
+            }
+            __syncthreads();
+            const int ln = s_list_n;   // > kLoopThreads cannot happen: distinct k per slot, but guard
+            for (int q = warp; q < min(ln, kLoopThreads); q += (blockDim.x >> 5)) {
+                const int k = s_list[q];
+                int b2 = scan_first_partner(bs, g, k, thr, lane, 32);
+                for (int o = 16; o > 0; o >>= 1) b2 = min(b2, __shfl_xor_sync(0xffffffffu, b2, o));
+                if (lane == 0) bs.first[k] = (b2 == INT_MAX) ? -1 : b2;
+            }
+            if (ln > kLoopThreads) {   // pathological: finish the remainder serially per warp
+                for (int k = warp; k < n; k += (blockDim.x >> 5)) {
+                    if (!bs.alive[k] || bs.first[k] != j) continue;
+                    int b2 = scan_first_partner(bs, g, k, thr, lane, 32);
+                    for (int o = 16; o > 0; o >>= 1)
+                        b2 = min(b2, __shfl_xor_sync(0xffffffffu, b2, o));
+                    if (lane == 0) bs.first[k] = (b2 == INT_MAX) ? -1 : b2;
+                }
+            }
+            __syncthreads();
+        }
+    }
+
+    // ---- pack survivors in order ------------------------------------------------------
+    __syncthreads();
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (int base = 0; base < n; base += blockDim.x) {
+        const int i = base + tid;
+        const int keep = (i < n) && (!do_prune || n < 2 || bs.alive[i]);
+        int v = keep;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
+        }
+        if (lane == 31) s_red[warp] = v;
+        __syncthreads();
+        if (warp == 0) {
+            int t = s_red[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += u;
+            }
+            s_red[lane] = t;
+        }
+        __syncthreads();
+        const int pos = s_carry + (warp > 0 ? s_red[warp - 1] : 0) + v - keep;
+        if (keep && pos < out_cap) out[pos] = bs.sorted[i];
+        __syncthreads();
+        if (tid == blockDim.x - 1) s_carry = pos + keep;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const Counters c = *bs.ctr;
+        hdr->n_blobs = min(s_carry, out_cap);
+        hdr->n_candidates = c.n_candidates;
+        hdr->n_flagged = c.n_flagged;
+        hdr->n_plateau = c.n_plateau;
+        hdr->n_merges = merges;
+        unsigned f = c.flags;
+        if (c.n_candidates > bs.cap || c.n_plateau > bs.cap || s_carry > out_cap)
+            f |= DOGBLOB_FLAG_OVERFLOW;
+        hdr->flags = f;
+        hdr->capacity = out_cap;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_prune_and_pack(const BlobSpace &bs, double overlap, bool prune,
+                                  void *d_result, int result_cap, cudaStream_t st) {
+    auto *hdr = reinterpret_cast<dogblob_result_header *>(d_result);
+    auto *out = reinterpret_cast<dogblob_blob *>(reinterpret_cast<char *>(d_result) +
+                                                 DOGBLOB_RESULT_HEADER_BYTES);
+    if (prune) {
+        prune_build_kernel<<<1, kLoopThreads, 0, st>>>(bs);
+        prune_first_kernel<<<148 * 2, 256, 0, st>>>(bs, overlap);
+    }
+    prune_loop_kernel<<<1, kLoopThreads, 0, st>>>(bs, overlap, prune ? 1 : 0, hdr, out, result_cap);
+    return cudaGetLastError();
+}
+
+}  // namespace dogblob

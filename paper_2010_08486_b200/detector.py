@@ -1,0 +1,718 @@
+"""Drop-in detector API over the sm_100a CUDA hot path.
+
+Mirrors the reference detector module (`pkg/src/dogblob/detector.py`) and the
+stage function of `pkg/src/dogblob/convolve.py`: same names, argument meaning,
+result types and error behaviour, with `backend="cuda"` as the only backend.
+Everything numeric runs in libdogblob_b200.so (include/dogblob_b200.h); this
+file is plumbing: parameter records, device buffers (torch), streams, result
+decoding.  There is no CPU fallback - without the CUDA library and a GPU every
+compute entry point raises.
+
+Layout on the device (per frame slot):
+  image      [H][Wp]            float32, Wp = W rounded up to 128
+  rows^T     [L][Wp][Hp]        row-filtered planes, stored x-major
+  DoG^T      [S][Wp][Hp]        sigma_i (L_i - L_{i+1}), x-major (never transposed back)
+  blob space candidate lists, sort/prune scratch
+  result     header + blob records (dogblob_blob), sorted by (-response, y, x, sigma)
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import queue
+import threading
+from dataclasses import asdict, dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .scale_space import SigmaLadder, TapBank, build_kernel_bank, build_ladder
+
+__all__ = [
+    "BACKENDS", "ScaleStack", "DoGStack", "Blob", "BlobSet", "RadiusHistogram", "DetectionParams",
+    "DetectResult", "Detector", "convolve_bank", "dog_stack", "find_extrema", "prune_overlaps",
+    "normalized_overlap", "disk_intersection_area", "histogram", "detect",
+]
+
+BACKENDS = ("cuda",)
+RADIUS_PER_SIGMA = math.sqrt(2.0)
+DEFAULT_STACK_ELEMENT_CAP = 2 ** 28   # convolve.py:37 (the reference's host-RAM guard)
+DEFAULT_MAX_BLOBS = 1 << 16
+HOST_RESULT_BLOBS = 4096              # records copied back with the header in one D2H
+
+
+# --------------------------------------------------------------------------
+# records (field-for-field the reference's)
+# --------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class ScaleStack:
+    """convolve.py:40-53."""
+    levels: np.ndarray = field(repr=False)
+    sigmas: np.ndarray = field(repr=False)
+
+    @property
+    def n_levels(self) -> int:
+        return self.levels.shape[0]
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return self.levels.shape[1], self.levels.shape[2]
+
+
+@dataclass(frozen=True)
+class DoGStack:
+    """detector.py:55-64; slices[i] = sigmas[i] * (L_i - L_{i+1})."""
+    slices: np.ndarray = field(repr=False)
+    sigmas: np.ndarray = field(repr=False)
+
+    @property
+    def n_slices(self) -> int:
+        return self.slices.shape[0]
+
+
+@dataclass(frozen=True)
+class Blob:
+    """detector.py:67-76."""
+    x: int
+    y: int
+    sigma: float
+    radius: float
+    response: float
+    at_scale_boundary: bool = False
+
+
+@dataclass(frozen=True)
+class DetectionParams:
+    """detector.py:79-95; only the backend default differs ("cuda")."""
+    min_sigma: float = 1.0
+    max_sigma: float = 10.0
+    n_bin: int = 18
+    truncate: float = 5.0
+    threshold: float = 0.1
+    overlap: float = 0.5
+    neighborhood: int = 3
+    backend: str = "cuda"
+    preprocess: bool = True
+    smooth_sigma: float = 1.0
+    saturation: float = 0.0035
+    prune: bool = True
+
+    def to_dict(self) -> dict:
+        return asdict(self)
+
+
+class BlobSet:
+    """detector.py:98-105, backed by the device result records.
+
+    `blobs` (tuple of Blob) is materialised on first access so that batch
+    throughput is not bounded by Python object construction; `records`,
+    `yxs()` and `radii` expose the same data as arrays.
+    """
+
+    def __init__(self, blobs=None, source_shape=(0, 0), params=None, records=None):
+        if records is None:
+            blobs = tuple(blobs or ())
+            records = np.zeros(len(blobs), dtype=_lib.BLOB_DTYPE)
+            for i, b in enumerate(blobs):
+                records[i] = (b.x, b.y, b.sigma, b.radius, b.response, -1,
+                              _lib.BLOB_SCALE_EDGE if b.at_scale_boundary else 0)
+            self._blobs = blobs
+        else:
+            self._blobs = None
+        self.records = records
+        self.source_shape = tuple(source_shape)   # (width, height)
+        self.params = params if params is not None else DetectionParams()
+
+    @property
+    def blobs(self) -> tuple:
+        if self._blobs is None:
+            r = self.records
+            integral = bool(np.all(r["x"] == np.rint(r["x"])) and np.all(r["y"] == np.rint(r["y"])))
+            xs = r["x"].astype(np.int64).tolist() if integral else r["x"].tolist()
+            ys = r["y"].astype(np.int64).tolist() if integral else r["y"].tolist()
+            edge = ((r["flags"] & _lib.BLOB_SCALE_EDGE) != 0).tolist()
+            self._blobs = tuple(
+                Blob(x, y, s, rad, resp, e)
+                for x, y, s, rad, resp, e in zip(xs, ys, r["sigma"].tolist(), r["radius"].tolist(),
+                                                 r["response"].tolist(), edge))
+        return self._blobs
+
+    def yxs(self) -> np.ndarray:
+        """(N, 3) float64 array of (y, x, sigma) rows, strongest first."""
+        r = self.records
+        return np.stack([r["y"], r["x"], r["sigma"]], axis=1) if len(r) else np.zeros((0, 3))
+
+    @property
+    def radii(self) -> np.ndarray:
+        return self.records["radius"].copy()
+
+    def __len__(self) -> int:
+        return len(self.records)
+
+    def __eq__(self, other):
+        if not isinstance(other, BlobSet):
+            return NotImplemented
+        return (self.blobs == other.blobs and self.source_shape == other.source_shape
+                and self.params == other.params)
+
+    def __repr__(self):
+        return f"BlobSet(n={len(self)}, source_shape={self.source_shape})"
+
+
+@dataclass(frozen=True)
+class RadiusHistogram:
+    """detector.py:108-114."""
+    bin_centers: np.ndarray = field(repr=False)
+    counts: np.ndarray = field(repr=False)
+    volume_weights: np.ndarray = field(repr=False)
+
+
+@dataclass(frozen=True)
+class DetectResult:
+    blobs: BlobSet
+    histogram: RadiusHistogram
+    timings_ms: dict
+    stats: dict = field(default_factory=dict)   # n_flagged / n_plateau / n_candidates / n_merges
+
+
+# --------------------------------------------------------------------------
+# device plumbing
+# --------------------------------------------------------------------------
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("backend='cuda' needs a CUDA device; there is no CPU fallback")
+    return torch
+
+
+def _check_image(img) -> np.ndarray:
+    img = np.asarray(img)
+    if img.ndim != 2 or img.shape[0] < 1 or img.shape[1] < 1:
+        raise ValueError(f"expected a non-empty 2-D image, got shape {img.shape}")
+    return img
+
+
+def _check_backend(backend: str) -> None:
+    if backend not in BACKENDS:
+        raise ValueError(f"unknown backend {backend!r}; expected one of {BACKENDS}")
+
+
+def _check_dtype(dtype) -> None:
+    if np.dtype(dtype) != np.float32:
+        raise ValueError("backend='cuda' computes the scale space in float32; "
+                         f"dtype={np.dtype(dtype).name} is not available")
+
+
+class _Plan:
+    """Owns one dogblob_plan (ladder + taps for one image shape on one device)."""
+
+    def __init__(self, bank: TapBank, shape, device: int, max_blobs: int):
+        lib = _lib.load()
+        H, W = int(shape[0]), int(shape[1])
+        self.shape = (H, W)
+        self.device = device
+        self.max_blobs = int(max_blobs)
+        self.n_levels = bank.ladder.n_levels
+        sig = np.ascontiguousarray(bank.ladder.sigmas, dtype=np.float64)
+        radii = np.ascontiguousarray(bank.radii, dtype=np.int32)
+        taps = np.ascontiguousarray(bank.taps32, dtype=np.float32)
+        offs = np.ascontiguousarray(bank.offsets, dtype=np.int64)
+        handle = C.c_void_p()
+        _lib.check(lib.dogblob_plan_create(device, H, W, self.n_levels, _lib.ptr(sig),
+                                           _lib.ptr(radii), _lib.ptr(taps), _lib.ptr(offs),
+                                           self.max_blobs, C.byref(handle)))
+        self.handle = handle
+        self.workspace_bytes = int(lib.dogblob_workspace_bytes(handle))
+        self.result_bytes = int(lib.dogblob_result_bytes(handle))
+        self.pitch = int(lib.dogblob_image_pitch(handle))
+
+    def close(self):
+        if self.handle is not None:
+            _lib.load().dogblob_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _Slot:
+    """Buffers + stream of one in-flight frame (one per concurrent caller)."""
+
+    def __init__(self, plan: _Plan):
+        torch = _torch()
+        lib = _lib.load()
+        dev = torch.device("cuda", plan.device)
+        H, W = plan.shape
+        self.plan = plan
+        self.stream = torch.cuda.Stream(device=dev)
+        self.d_image = torch.zeros((H, plan.pitch), dtype=torch.float32, device=dev)
+        self.d_work = torch.zeros(plan.workspace_bytes, dtype=torch.uint8, device=dev)
+        self.d_result = torch.zeros(plan.result_bytes, dtype=torch.uint8, device=dev)
+        self.h_image = torch.empty((H, W), dtype=torch.float32).pin_memory()
+        n_host = min(HOST_RESULT_BLOBS, plan.max_blobs)
+        self.h_result = torch.zeros(_lib.RESULT_HEADER_BYTES + n_host * _lib.BLOB_DTYPE.itemsize,
+                                    dtype=torch.uint8).pin_memory()
+        self.h_result_np = self.h_result.numpy()
+        self.h_image_np = self.h_image.numpy()
+        self.n_host = n_host
+        self.events = (C.c_void_p * 4)()
+        for k in range(4):
+            e = C.c_void_p()
+            _lib.check(lib.dogblob_event_create(C.byref(e)))
+            self.events[k] = e
+        torch.cuda.synchronize(dev)
+        self.pending = None     # bookkeeping of run_batch
+
+    # ---- one frame --------------------------------------------------------------
+    def launch(self, frame, params: DetectionParams, prune: bool) -> None:
+        """H2D + all kernels + D2H of header/records, asynchronously on self.stream."""
+        lib = _lib.load()
+        src = self._host_pointer(frame)
+        _lib.check(lib.dogblob_detect_host(
+            self.plan.handle, src, float(np.float32(params.threshold)), int(params.neighborhood),
+            float(params.overlap), 1 if prune else 0, self.d_image.data_ptr(),
+            self.d_work.data_ptr(), self.d_result.data_ptr(), self.h_result.data_ptr(),
+            self.n_host, self.stream.cuda_stream, self.events))
+
+    def launch_device(self, d_frame, params: DetectionParams, prune: bool) -> None:
+        """Same, for a frame that is already resident: a float32 CUDA tensor [H][pitch]."""
+        lib = _lib.load()
+        _lib.check(lib.dogblob_detect(
+            self.plan.handle, d_frame.data_ptr(), float(np.float32(params.threshold)),
+            int(params.neighborhood), float(params.overlap), 1 if prune else 0,
+            self.d_work.data_ptr(), self.d_result.data_ptr(), self.stream.cuda_stream,
+            self.events))
+
+    def _host_pointer(self, frame) -> int:
+        torch = _torch()
+        H, W = self.plan.shape
+        if isinstance(frame, torch.Tensor):
+            if frame.device.type != "cpu":
+                raise ValueError("expected a host frame")
+            if (frame.dtype == torch.float32 and frame.is_contiguous() and frame.is_pinned()
+                    and tuple(frame.shape) == (H, W)):
+                self._keepalive = frame
+                return frame.data_ptr()
+            frame = frame.numpy()
+        np.copyto(self.h_image_np, np.asarray(frame), casting="same_kind")
+        return self.h_image.data_ptr()
+
+    def collect(self):
+        """Wait for the frame and decode header + records (numpy structured array)."""
+        lib = _lib.load()
+        self.stream.synchronize()
+        hdr = self.h_result_np[:_lib.RESULT_HEADER_BYTES].view(_lib.HEADER_DTYPE)[0].copy()
+        n = int(hdr["n_blobs"])
+        if int(hdr["flags"]) & _lib.FLAG_OVERFLOW:
+            return hdr, None
+        recs = np.empty(n, dtype=_lib.BLOB_DTYPE)
+        k = min(n, self.n_host)
+        body = self.h_result_np[_lib.RESULT_HEADER_BYTES:]
+        recs[:k] = body[:k * _lib.BLOB_DTYPE.itemsize].view(_lib.BLOB_DTYPE)
+        if n > k:
+            _lib.check(lib.dogblob_fetch_blobs(self.d_result.data_ptr(), k, n - k,
+                                               recs[k:].ctypes.data, self.stream.cuda_stream))
+            self.stream.synchronize()
+        return hdr, recs
+
+    def stage_times_ms(self) -> dict:
+        lib = _lib.load()
+        out = []
+        for a, b in ((0, 1), (1, 2), (2, 3)):
+            ms = C.c_float()
+            _lib.check(lib.dogblob_event_elapsed_ms(self.events[a], self.events[b], C.byref(ms)))
+            out.append(float(ms.value))
+        return {"convolve_ms": out[0], "extrema_ms": out[1], "prune_ms": out[2]}
+
+    def close(self):
+        lib = _lib.load()
+        for k in range(4):
+            if self.events[k]:
+                lib.dogblob_event_destroy(self.events[k])
+                self.events[k] = None
+
+
+class _Engine:
+    """Plan + slot pool for one image shape."""
+
+    def __init__(self, bank: TapBank, shape, device: int, max_blobs: int, n_slots: int):
+        self.plan = _Plan(bank, shape, device, max_blobs)
+        self.slots = [_Slot(self.plan) for _ in range(n_slots)]
+        self.free = queue.Queue()
+        for s in self.slots:
+            self.free.put(s)
+
+    def close(self):
+        for s in self.slots:
+            s.close()
+        self.plan.close()
+
+
+# --------------------------------------------------------------------------
+# the reusable pipeline
+# --------------------------------------------------------------------------
+
+def histogram(blobset: BlobSet, ladder: SigmaLadder) -> RadiusHistogram:
+    """Nearest ladder-radius bin, ties to the smaller (detector.py:283-299).
+
+    Evaluated on the host in float64 over the <= ~10^4 surviving radii so that
+    counts and volume weights are bit-identical to the reference's numpy
+    arithmetic (np.add.at order, libm pow).
+    """
+    centers = RADIUS_PER_SIGMA * ladder.sigmas
+    counts = np.zeros(centers.size, dtype=np.int64)
+    volumes = np.zeros(centers.size, dtype=np.float64)
+    if len(blobset) > 0:
+        radii = blobset.radii
+        mid = 0.5 * (centers[:-1] + centers[1:])
+        idx = np.searchsorted(mid, radii, side="left")
+        np.add.at(counts, idx, 1)
+        np.add.at(volumes, idx, (4.0 / 3.0) * np.pi * radii ** 3)
+    return RadiusHistogram(bin_centers=centers, counts=counts, volume_weights=volumes)
+
+
+class Detector:
+    """Reusable detection pipeline for a fixed parameter set (detector.py:302-360).
+
+    Immutable after construction apart from lock-guarded, append-only per-shape
+    engines, so one Detector may serve many images and threads concurrently
+    (each concurrent `run` borrows its own slot: stream + workspace).
+    """
+
+    def __init__(self, params: DetectionParams, device: int | None = None,
+                 max_blobs: int = DEFAULT_MAX_BLOBS, slots: int = 2):
+        _check_backend(params.backend)
+        self.params = params
+        self.ladder = build_ladder(params.min_sigma, params.max_sigma, params.n_bin)
+        self.bank = build_kernel_bank(self.ladder, params.truncate)
+        if params.neighborhood < 1 or params.neighborhood % 2 == 0:
+            raise ValueError(f"neighborhood must be odd and >= 1, got {params.neighborhood}")
+        if not 0.0 <= params.overlap <= 1.0:
+            raise ValueError(f"overlap threshold must be in [0, 1], got {params.overlap}")
+        self._device = device
+        self._max_blobs = int(max_blobs)
+        self._n_slots = max(1, int(slots))
+        self._engines: dict = {}
+        self._lock = threading.Lock()
+
+    # -- plumbing ---------------------------------------------------------------
+    @property
+    def device(self) -> int:
+        if self._device is None:
+            self._device = _torch().cuda.current_device()
+        return self._device
+
+    def plan_for(self, shape) -> _Engine:
+        """Per-shape engine, double-checked like the reference's plan cache (detector.py:323-331)."""
+        key = (int(shape[0]), int(shape[1]))
+        eng = self._engines.get(key)
+        if eng is None:
+            with self._lock:
+                eng = self._engines.get(key)
+                if eng is None:
+                    eng = _Engine(self.bank, key, self.device, self._max_blobs, self._n_slots)
+                    self._engines[key] = eng
+        return eng
+
+    def _grow(self, shape) -> None:
+        key = (int(shape[0]), int(shape[1]))
+        with self._lock:
+            old = self._engines.pop(key, None)
+            self._max_blobs *= 4
+            if old is not None:
+                old.close()
+
+    def close(self) -> None:
+        with self._lock:
+            for eng in self._engines.values():
+                eng.close()
+            self._engines.clear()
+
+    def _prepare(self, img, dtype):
+        _check_dtype(dtype)
+        torch = _torch()
+        if isinstance(img, torch.Tensor):
+            if img.ndim != 2 or img.shape[0] < 1 or img.shape[1] < 1:
+                raise ValueError(f"expected a non-empty 2-D image, got shape {tuple(img.shape)}")
+            return img
+        img = _check_image(img)
+        if img.dtype != np.float32:
+            img = img.astype(np.float32)
+        return img
+
+    def _finish(self, slot: _Slot, hdr, recs, shape, timings) -> DetectResult:
+        blobs = BlobSet(records=recs, source_shape=(shape[1], shape[0]), params=self.params)
+        stats = {k: int(hdr[k]) for k in ("n_flagged", "n_plateau", "n_candidates", "n_merges")}
+        return DetectResult(blobs=blobs, histogram=histogram(blobs, self.ladder),
+                            timings_ms=timings, stats=stats)
+
+    # -- public API -------------------------------------------------------------
+    def run(self, img, dtype=np.float32) -> DetectResult:
+        """Full pipeline on one frame; per-stage timings are CUDA-event milliseconds."""
+        p = self.params
+        if p.preprocess:
+            img = self._preprocess(img)
+        img = self._prepare(img, dtype)
+        shape = tuple(img.shape)
+        if shape[0] * shape[1] * self.ladder.n_levels > (1 << 34):
+            raise ValueError(f"stack of {self.ladder.n_levels} x {shape} exceeds element cap")
+        while True:
+            eng = self.plan_for(shape)
+            slot = eng.free.get()
+            try:
+                slot.launch(img, p, p.prune)
+                hdr, recs = slot.collect()
+                timings = {"preprocess_ms": 0.0, **slot.stage_times_ms()}
+            finally:
+                eng.free.put(slot)
+            if recs is not None:
+                return self._finish(slot, hdr, recs, shape, timings)
+            self._grow(shape)   # candidate capacity exceeded: retry with 4x the room
+
+    def run_batch(self, frames, timings: bool = False) -> list:
+        """Detect over a sequence of equally shaped host frames, pipelined over the
+        slot pool: the H2D copy and kernels of frame f+1 overlap the D2H/decode of f."""
+        p = self.params
+        if p.preprocess:
+            frames = [self._preprocess(f) for f in frames]
+        frames = [self._prepare(f, np.float32) for f in frames]
+        if not frames:
+            return []
+        shape = tuple(frames[0].shape)
+        for f in frames:
+            if tuple(f.shape) != shape:
+                raise ValueError("run_batch needs equally shaped frames")
+        eng = self.plan_for(shape)
+        slots = [eng.free.get() for _ in range(len(eng.slots))]
+        results = [None] * len(frames)
+        retry = []
+        try:
+            def drain(slot):
+                idx = slot.pending
+                slot.pending = None
+                hdr, recs = slot.collect()
+                if recs is None:
+                    retry.append(idx)
+                    return
+                t = {"preprocess_ms": 0.0, **slot.stage_times_ms()} if timings else {}
+                results[idx] = self._finish(slot, hdr, recs, shape, t)
+
+            for i, frame in enumerate(frames):
+                slot = slots[i % len(slots)]
+                if slot.pending is not None:
+                    drain(slot)
+                slot.launch(frame, p, p.prune)
+                slot.pending = i
+            for slot in slots:
+                if slot.pending is not None:
+                    drain(slot)
+        finally:
+            for s in slots:
+                s.pending = None
+                eng.free.put(s)
+        for idx in retry:
+            results[idx] = self.run(frames[idx])
+        return results
+
+    def _preprocess(self, img):
+        raise ValueError(
+            "preprocess=True is not implemented on backend='cuda' yet (SURVEY 8f1); "
+            "pass DetectionParams(preprocess=False) with an already pre-processed frame")
+
+
+def detect(img, params: DetectionParams) -> tuple:
+    """One-shot detection (detector.py:363-366)."""
+    det = Detector(params)
+    try:
+        result = det.run(img)
+    finally:
+        det.close()
+    return result.blobs, result.histogram
+
+
+# --------------------------------------------------------------------------
+# stage functions (convolve.py:189-218, detector.py:117-299) on the CUDA library
+# --------------------------------------------------------------------------
+
+_stage_lock = threading.Lock()
+
+
+def _stage_stream():
+    torch = _torch()
+    return torch.cuda.current_stream()
+
+
+def convolve_bank(img, bank: TapBank, backend: str = "cuda", dtype=np.float32, plan=None,
+                  stack_element_cap: int = DEFAULT_STACK_ELEMENT_CAP) -> ScaleStack:
+    """Scale-space stack levels[i] = k_i * img, reflect boundary, float32 [L][H][W].
+
+    Stage entry point for tests and diagnostics: it materialises every level,
+    which the fused production path (`Detector.run`) never does.
+    """
+    img = _check_image(img)
+    _check_backend(backend)
+    n_levels = bank.ladder.n_levels
+    if img.shape[0] * img.shape[1] * n_levels > stack_element_cap:
+        raise ValueError(f"stack of {n_levels} x {img.shape} exceeds element cap {stack_element_cap}")
+    _check_dtype(dtype)
+    if plan is not None and tuple(plan.shape) != tuple(img.shape):
+        raise ValueError(f"plan built for {plan.shape[1]}x{plan.shape[0]}, "
+                         f"image is {img.shape[1]}x{img.shape[0]}")
+    torch = _torch()
+    lib = _lib.load()
+    device = torch.cuda.current_device()
+    own = plan is None
+    if own:
+        plan = _Plan(bank, img.shape, device, 1024)
+    try:
+        dev = torch.device("cuda", plan.device)
+        H, W = img.shape
+        d_img = torch.zeros((H, plan.pitch), dtype=torch.float32, device=dev)
+        d_img[:, :W] = torch.from_numpy(np.ascontiguousarray(img, dtype=np.float32)).to(dev)
+        work = torch.zeros(plan.workspace_bytes, dtype=torch.uint8, device=dev)
+        out = torch.empty((n_levels, H, W), dtype=torch.float32, device=dev)
+        st = torch.cuda.current_stream(dev)
+        _lib.check(lib.dogblob_scale_space(plan.handle, d_img.data_ptr(), work.data_ptr(),
+                                           out.data_ptr(), st.cuda_stream))
+        levels = out.cpu().numpy()
+    finally:
+        if own:
+            plan.close()
+    return ScaleStack(levels=levels, sigmas=bank.ladder.sigmas)
+
+
+def fused_dog(img, bank: TapBank) -> DoGStack:
+    """DoG slices exactly as the production kernels compute them (row pass, then
+    column pass with the subtraction fused), transposed back to [S][H][W]."""
+    img = _check_image(img)
+    torch = _torch()
+    lib = _lib.load()
+    plan = _Plan(bank, img.shape, torch.cuda.current_device(), 1024)
+    try:
+        dev = torch.device("cuda", plan.device)
+        H, W = img.shape
+        d_img = torch.zeros((H, plan.pitch), dtype=torch.float32, device=dev)
+        d_img[:, :W] = torch.from_numpy(np.ascontiguousarray(img, dtype=np.float32)).to(dev)
+        work = torch.zeros(plan.workspace_bytes, dtype=torch.uint8, device=dev)
+        out = torch.empty((bank.ladder.n_levels - 1, H, W), dtype=torch.float32, device=dev)
+        st = torch.cuda.current_stream(dev)
+        _lib.check(lib.dogblob_dog(plan.handle, d_img.data_ptr(), work.data_ptr(), out.data_ptr(),
+                                   st.cuda_stream))
+        slices = out.cpu().numpy()
+    finally:
+        plan.close()
+    return DoGStack(slices=slices, sigmas=bank.ladder.sigmas[:-1])
+
+
+def dog_stack(stack: ScaleStack, ladder: SigmaLadder) -> DoGStack:
+    """Adjacent differences scaled by the lower sigma of each pair (detector.py:117-126)."""
+    if stack.n_levels != ladder.n_levels:
+        raise ValueError(f"stack has {stack.n_levels} levels, ladder expects {ladder.n_levels}")
+    if stack.levels.dtype != np.float32:
+        raise ValueError("backend='cuda' differences float32 stacks only")
+    torch = _torch()
+    lib = _lib.load()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    L, H, W = stack.levels.shape
+    d_lv = torch.from_numpy(np.ascontiguousarray(stack.levels)).to(dev)
+    out = torch.empty((L - 1, H, W), dtype=torch.float32, device=dev)
+    sig = np.ascontiguousarray(ladder.sigmas, dtype=np.float64)
+    st = torch.cuda.current_stream(dev)
+    _lib.check(lib.dogblob_dog_from_levels(L, H, W, d_lv.data_ptr(), _lib.ptr(sig), out.data_ptr(),
+                                           st.cuda_stream))
+    return DoGStack(slices=out.cpu().numpy(), sigmas=ladder.sigmas[:-1])
+
+
+def _read_result(d_result, max_blobs):
+    host = d_result.cpu().numpy()
+    hdr = host[:_lib.RESULT_HEADER_BYTES].view(_lib.HEADER_DTYPE)[0]
+    if int(hdr["flags"]) & _lib.FLAG_OVERFLOW:
+        return hdr, None
+    n = int(hdr["n_blobs"])
+    body = host[_lib.RESULT_HEADER_BYTES:_lib.RESULT_HEADER_BYTES + n * _lib.BLOB_DTYPE.itemsize]
+    return hdr, body.view(_lib.BLOB_DTYPE).copy()
+
+
+def find_extrema(dog: DoGStack, threshold: float = 0.1, neighborhood: int = 3,
+                 source_shape=None, params: DetectionParams | None = None,
+                 max_blobs: int = DEFAULT_MAX_BLOBS) -> BlobSet:
+    """Voxels equal to the max of their n^3 block and above threshold, plateaus
+    coalesced to their centroid, sorted (detector.py:149-193)."""
+    if neighborhood < 1 or neighborhood % 2 == 0:
+        raise ValueError(f"neighborhood must be odd and >= 1, got {neighborhood}")
+    data = np.asarray(dog.slices)
+    if data.ndim != 3:
+        raise ValueError(f"expected (n_slices, height, width) slices, got shape {data.shape}")
+    if data.dtype != np.float32:
+        raise ValueError("backend='cuda' searches float32 stacks only")
+    torch = _torch()
+    lib = _lib.load()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    S, H, W = data.shape
+    d_sl = torch.from_numpy(np.ascontiguousarray(data)).to(dev)
+    sig = np.ascontiguousarray(dog.sigmas, dtype=np.float64)
+    st = torch.cuda.current_stream(dev)
+    while True:
+        space = torch.zeros(int(lib.dogblob_blobspace_bytes(max_blobs)), dtype=torch.uint8, device=dev)
+        res = torch.zeros(int(lib.dogblob_result_bytes_for(max_blobs)), dtype=torch.uint8, device=dev)
+        _lib.check(lib.dogblob_extrema(S, H, W, d_sl.data_ptr(), _lib.ptr(sig),
+                                       float(np.float32(threshold)), int(neighborhood), max_blobs,
+                                       space.data_ptr(), res.data_ptr(), st.cuda_stream))
+        hdr, recs = _read_result(res, max_blobs)
+        if recs is not None:
+            break
+        max_blobs *= 4
+    shape = source_shape if source_shape is not None else (W, H)
+    return BlobSet(records=recs, source_shape=shape, params=params or DetectionParams())
+
+
+def disk_intersection_area(x1, y1, r1, x2, y2, r2) -> float:
+    """Exact lens area of two disks (detector.py:196-209); scalar host helper."""
+    d = math.hypot(x2 - x1, y2 - y1)
+    if d >= r1 + r2:
+        return 0.0
+    rmin = min(r1, r2)
+    if d <= abs(r1 - r2):
+        return math.pi * rmin * rmin
+    a1 = r1 * r1 * math.acos((d * d + r1 * r1 - r2 * r2) / (2.0 * d * r1))
+    a2 = r2 * r2 * math.acos((d * d + r2 * r2 - r1 * r1) / (2.0 * d * r2))
+    s = 0.5 * math.sqrt((-d + r1 + r2) * (d + r1 - r2) * (d - r1 + r2) * (d + r1 + r2))
+    return a1 + a2 - s
+
+
+def normalized_overlap(b1: Blob, b2: Blob) -> float:
+    """Lens area over the smaller disk's area (detector.py:212-218)."""
+    rmin = min(b1.radius, b2.radius)
+    if rmin <= 0:
+        return 0.0
+    return disk_intersection_area(b1.x, b1.y, b1.radius, b2.x, b2.y, b2.radius) / (
+        math.pi * rmin * rmin)
+
+
+def prune_overlaps(blobset: BlobSet, overlap_threshold: float = 0.5) -> BlobSet:
+    """Coalesce blob pairs whose normalised overlap exceeds the threshold, in the
+    reference's visiting order (detector.py:250-280), on the GPU."""
+    if not 0.0 <= overlap_threshold <= 1.0:
+        raise ValueError(f"overlap threshold must be in [0, 1], got {overlap_threshold}")
+    torch = _torch()
+    lib = _lib.load()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    recs = np.ascontiguousarray(blobset.records)
+    n = len(recs)
+    cap = max(n, 1)
+    d_in = torch.from_numpy(recs.view(np.uint8).reshape(-1).copy()).to(dev) if n else None
+    space = torch.zeros(int(lib.dogblob_blobspace_bytes(cap)), dtype=torch.uint8, device=dev)
+    res = torch.zeros(int(lib.dogblob_result_bytes_for(cap)), dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream(dev)
+    _lib.check(lib.dogblob_prune(n, d_in.data_ptr() if n else None, float(overlap_threshold), cap,
+                                 space.data_ptr(), res.data_ptr(), st.cuda_stream))
+    hdr, out = _read_result(res, cap)
+    if out is None:
+        raise RuntimeError("prune result overflow")
+    return BlobSet(records=out, source_shape=blobset.source_shape, params=blobset.params)
