@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""Headline benchmark: frames/s and single-frame latency of the 1024^2 DoG detector.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+
+Workload (BASELINE.json configs[1], SURVEY 8d "C2"): 1024x1024 PLIF-like synthetic
+frames, sigma in [1, 30], n_bin = 58 (59 levels, radii 5..150), threshold 0.1,
+overlap 0.5, pruning on, preprocess off.  A step is one pass of the hot path over
+a batch of BATCH distinct frames (scene seed 1000+f, noise seed 2000+f).
+
+  value  : frames/s, kernels only, frames resident in HBM (CUDA events, max over ranks)
+  e2e    : frames/s through Detector.run_batch with pinned HOST frames: H2D copy of
+           every frame and D2H + decoding of every blob list inside the timed region
+  latency: Detector.run on one pinned host frame, median wall-clock ms
+  roofline: the fused column+DoG kernel (dominant), CUDA-event duration per launch
+  cpu_baseline: the oracle port of the reference CPU path timed on this host
+
+Multi-GPU: frames shard by index, frame f -> rank f mod N, no collective on the data
+path (weak scaling: BATCH frames per GPU per step).
+`--impl reference` times the reference CPU algorithm (oracle port) on all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOAD = "C2"
+BATCH = 16
+KERNELS_PER_FRAME = 11   # reset, row pass, column+DoG, nms, 3 plateau, sort, 3 prune/pack
+
+
+def params_kw():
+    from paper_2010_08486_b200 import synth
+    return synth.config_params(WORKLOAD)
+
+
+def make_frames(indices):
+    from paper_2010_08486_b200 import synth
+    return [synth.config_frame("C3", int(f)) for f in indices]
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# --------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.idx)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._pump, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); mx.append(float(f[2])); power.append(float(f[3]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "power_w_max": float(max(power)), "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------------------------------
+def oracle_fps_single_core():
+    """cpu_baseline of the `ours` line: the oracle port of the reference CPU path
+    (fft backend, float32, as-is = 1 core) on one frame of the workload."""
+    from oracle import dog_oracle as O
+    frame = make_frames([0])[0]
+    det = O.OracleDetector(preprocess=False, **params_kw())
+    det.spectra_for(frame.shape, np.float32)     # amortised state, like bench.py:57-62 of the reference
+    t0 = time.perf_counter()
+    res = det.run(frame)
+    dt = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": "frames/s", "cores": 1, "kind": "port",
+            "sample": f"1 frame of {WORKLOAD} (1024x1024, 59 levels) after building kernel spectra; "
+                      f"{dt * 1e3:.0f} ms, {len(res.blobs)} blobs",
+            "stage_ms": {k: round(v, 1) for k, v in res.timings_ms.items()}}
+
+
+_WORKER = {}
+
+
+def _ref_worker_init():
+    os.environ["OMP_NUM_THREADS"] = "1"
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from oracle import dog_oracle as O
+    det = O.OracleDetector(preprocess=False, **params_kw())
+    det.spectra_for((1024, 1024), np.float32)
+    _WORKER["det"] = det
+
+
+def _ref_worker_run(frame_index):
+    frame = make_frames([frame_index])[0]
+    t0 = time.perf_counter()
+    res = _WORKER["det"].run(frame)
+    return time.perf_counter() - t0, len(res.blobs)
+
+
+def run_reference(args):
+    """The reference CPU implementation of the path (oracle port: /root/reference is pure
+    Python and does not exist on the GPU box), frame-parallel over all host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    procs = max(1, min(cores, 32))
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs, initializer=_ref_worker_init) as pool:
+        per_step = procs                                     # one frame per worker per step
+        for w in range(args.warmup):
+            pool.map(_ref_worker_run, range(per_step))
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            pool.map(_ref_worker_run, [k * per_step + i for i in range(per_step)])
+        dt = time.perf_counter() - t0
+    fps = per_step * args.steps / dt
+    line = {
+        "impl": "reference", "metric": "frames/sec, 1024x1024 DoG detector (sigma<=30, n_bin=58)",
+        "value": fps, "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{WORKLOAD}: 1024x1024 PLIF-like frames, sigma 1..30, n_bin 58, "
+                               "threshold 0.1, overlap 0.5, prune on, preprocess off",
+                   "frames_per_step": per_step},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": procs, "kind": "port",
+                         "sample": f"{per_step} frames per step, one per worker process "
+                                   f"({procs} processes, fft backend, float32)"},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2010_08486_b200 as P
+    from paper_2010_08486_b200 import detector as D
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise RuntimeError("bench.py --impl ours needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    kw = params_kw()
+    params = P.DetectionParams(preprocess=False, **kw)
+    n_slots = 4
+    det = P.Detector(params, device=local, slots=n_slots)
+    # frame f of the global batch goes to rank f mod world
+    my_frames = [f for f in range(BATCH * world) if f % world == rank]
+    frames = make_frames(my_frames)
+    H, W = frames[0].shape
+    eng = det.plan_for((H, W))
+    pitch = eng.plan.pitch
+    pinned = [torch.from_numpy(f).pin_memory() for f in frames]
+    resident = []
+    for f in frames:
+        d = torch.zeros((H, pitch), dtype=torch.float32, device=dev)
+        d[:, :W] = torch.from_numpy(f).to(dev)
+        resident.append(d)
+    slots = eng.slots
+    main = torch.cuda.current_stream(dev)
+    event_sets = [D.new_events() for _ in range(len(frames))]
+
+    def device_step(record_sets=None):
+        for i, d in enumerate(resident):
+            s = slots[i % len(slots)]
+            s.launch_device(d, params, True, events=None if record_sets is None else record_sets[i])
+
+    def fenced(fn, reps):
+        """reps x fn() on the slot streams, bracketed by events on the main stream."""
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize(dev)
+        start.record(main)
+        for s in slots:
+            s.stream.wait_event(start)
+        for r in range(reps):
+            fn(r)
+        for s in slots:
+            done = torch.cuda.Event()
+            done.record(s.stream)
+            main.wait_event(done)
+        end.record(main)
+        torch.cuda.synchronize(dev)
+        ms = start.elapsed_time(end)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    # ---- kernels only, frames resident in HBM ----
+    for _ in range(max(args.warmup, 3)):
+        device_step()
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
+        time.sleep(0.25)
+    ms_total = fenced(lambda r: device_step(event_sets if r == args.steps - 1 else None), args.steps)
+    clocks = sampler.stop() if rank == 0 else None
+    frames_per_step = BATCH * world
+    value = frames_per_step * args.steps / (ms_total * 1e-3)
+    stage = np.array([D.event_intervals_ms(es) for es in event_sets])   # [frame][row, col, extrema, prune]
+
+    # ---- isolated kernel durations: one stream, frames back to back ----
+    iso_sets = [D.new_events() for _ in range(len(frames))]
+    for i, d in enumerate(resident):
+        slots[0].launch_device(d, params, True, events=iso_sets[i])
+    torch.cuda.synchronize(dev)
+    iso = np.array([D.event_intervals_ms(es) for es in iso_sets])
+
+    # ---- end to end through the public API, pinned host frames ----
+    for _ in range(3):
+        det.run_batch(pinned)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    n_blobs = 0
+    for _ in range(args.steps):
+        out = det.run_batch(pinned)
+        n_blobs = sum(len(r.blobs) for r in out)
+    torch.cuda.synchronize(dev)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = frames_per_step * args.steps / e2e_s
+    h2d = frames_per_step * H * W * 4
+    d2h = frames_per_step * (64 + slots[0].n_host * 48)
+
+    # ---- single-frame latency (batch 1), pinned host frame in, decoded blobs out ----
+    lat = []
+    for i in range(10 + 100):
+        t0 = time.perf_counter()
+        res = det.run(pinned[i % len(pinned)])
+        dt = (time.perf_counter() - t0) * 1e3
+        if i >= 10:
+            lat.append(dt)
+    lat = np.array(lat)
+
+    if rank == 0:
+        L = len(det.ladder.sigmas)
+        S = L - 1
+        taps = int(sum(2 * int(r) + 1 for r in det.bank.radii))
+        col_bytes = 4.0 * H * W * (L + S)                  # read L row-filtered planes, write S slices
+        col_flops = 2.0 * H * W * taps + 2.0 * H * W * S
+        frame_bytes = 4.0 * H * W * (4 * (L - 1) + 3)      # SURVEY 8d algorithmic bytes per frame
+        frame_flops = 2.0 * H * W * 2 * taps + 2.0 * H * W * S
+        peak, peak_src = measured_peaks()
+        col_ms = float(stage[:, 1].mean())
+        col_ms_iso = float(iso[:, 1].mean())
+        achieved = col_bytes / (col_ms_iso * 1e-3) / 1e9
+        traffic = None
+        tp = ROOT / "profiles" / "ncu_traffic.json"
+        if tp.exists():
+            try:
+                traffic = json.loads(tp.read_text()).get("col_dog_kernel_dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        line = {
+            "metric": "frames/sec, 1024x1024 DoG detector (sigma<=30, n_bin=58)",
+            "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"{WORKLOAD}: 1024x1024 PLIF-like frames, sigma 1..30, n_bin 58, "
+                                   "threshold 0.1, overlap 0.5, prune on, preprocess off",
+                       "frames_per_step": frames_per_step, "frames_per_gpu": BATCH,
+                       "streams_per_gpu": len(slots), "sharding": "frame f -> rank f mod N, no collective",
+                       "l2": "per-frame working set 490 MB (59 + 58 planes of 4 MB) exceeds the 126 MB L2; "
+                             "16 distinct frames rotate"},
+            "latency_ms": {"single_frame_e2e_median": float(np.median(lat)),
+                           "p10": float(np.percentile(lat, 10)), "p90": float(np.percentile(lat, 90)),
+                           "what": "Detector.run(pinned host frame): H2D + kernels + D2H + decode, batch 1",
+                           "device_stage_ms_isolated": {"row_pass": float(iso[:, 0].mean()),
+                                                        "col_dog_pass": col_ms_iso,
+                                                        "extrema": float(iso[:, 2].mean()),
+                                                        "prune_pack": float(iso[:, 3].mean())}},
+            "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "blobs_per_step": n_blobs,
+                    "what": "Detector.run_batch over pinned host frames, wall clock"},
+            "gpu_launches": KERNELS_PER_FRAME * BATCH * args.steps,
+            "roofline": {"bound": "hbm", "kernel": "col_pass_kernel<true> (fused column pass + DoG)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "peak_source": peak_src,
+                         "bytes_per_launch": col_bytes, "ms_per_launch_isolated": col_ms_iso,
+                         "ms_per_launch_in_timed_region": col_ms,
+                         "fp32": {"note": "this kernel is FP32-FMA bound, not HBM bound (SURVEY 7, 8d): "
+                                          "arithmetic intensity 38 FLOP/B",
+                                  "flops_per_launch": col_flops,
+                                  "achieved_tflops": col_flops / (col_ms_iso * 1e-3) / 1e12,
+                                  "peak_tflops": 71.9,
+                                  "peak_source": "tools/ubench_fma.cu on this pool's B200 (FFMA, 1965 MHz)",
+                                  "frac": col_flops / (col_ms_iso * 1e-3) / 1e12 / 71.9},
+                         "whole_frame": {"bytes": frame_bytes, "flops": frame_flops,
+                                         "hbm_frac_at_value": frame_bytes * value / world / 1e9 / peak,
+                                         "fp32_frac_at_value": frame_flops * value / world / 1e12 / 71.9}},
+            "clocks": clocks,
+        }
+        if world == 1:
+            line["cpu_baseline"] = oracle_fps_single_core()
+        print(json.dumps(line), flush=True)
+    det.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    args = ap.parse_args()
+    if args.impl == "reference":
+        args.steps = 3 if args.steps is None else args.steps
+        args.warmup = 1 if args.warmup is None else args.warmup
+        run_reference(args)
+    else:
+        args.steps = 20 if args.steps is None else args.steps
+        args.warmup = 3 if args.warmup is None else args.warmup
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -33,6 +33,7 @@ extern "C" {
 #endif
 
 #define DOGBLOB_ABI_VERSION 1
+#define DOGBLOB_N_EVENTS 5
 
 enum {
     DOGBLOB_OK = 0,
@@ -101,8 +102,9 @@ int64_t dogblob_image_pitch(const dogblob_plan *plan);
  *   d_image     device float32, `height` rows of dogblob_image_pitch() floats
  *   d_result    device buffer of dogblob_result_bytes(): header + blobs, sorted
  *               by (-response, y, x, sigma)
- *   events      NULL or 4 cudaEvent_t recorded at: start, after the scale-space
- *               + DoG kernels, after extrema, after pruning
+ *   events      NULL or DOGBLOB_N_EVENTS cudaEvent_t recorded at: start, after
+ *               the row pass, after the fused column+DoG pass, after extrema,
+ *               after pruning/packing
  */
 int dogblob_detect(const dogblob_plan *plan, const float *d_image,
                    float threshold, int neighborhood, double overlap, int prune,

@@ -20,7 +20,7 @@ size_t blobspace_bytes(int cap) {
     b += align_up(sizeof(Counters), 256);
     b += align_up(c * sizeof(Voxel), 256);
     b += align_up(c * sizeof(int), 256) * 2;                  // parent, pl_count
-    b += align_up(c * sizeof(unsigned long long), 256) * 2;   // pl_sum_row/col
+    b += align_up(c * sizeof(unsigned long long), 256) * 3;   // pl_sum_row/col, pl_first
     b += align_up(c * sizeof(dogblob_blob), 256) * 2;         // unsorted, sorted
     b += align_up(c * sizeof(int), 256) * 4;                  // first, alive, cell_of, cell_items
     b += align_up((size_t)(kMaxCells + 1) * sizeof(int), 256);
@@ -40,6 +40,7 @@ BlobSpace carve_blobspace(void *base, int cap) {
     bs.pl_count = reinterpret_cast<int *>(take(c * sizeof(int)));
     bs.pl_sum_row = reinterpret_cast<unsigned long long *>(take(c * sizeof(unsigned long long)));
     bs.pl_sum_col = reinterpret_cast<unsigned long long *>(take(c * sizeof(unsigned long long)));
+    bs.pl_first = reinterpret_cast<unsigned long long *>(take(c * sizeof(unsigned long long)));
     bs.unsorted = reinterpret_cast<dogblob_blob *>(take(c * sizeof(dogblob_blob)));
     bs.sorted = reinterpret_cast<dogblob_blob *>(take(c * sizeof(dogblob_blob)));
     bs.first = reinterpret_cast<int *>(take(c * sizeof(int)));
@@ -123,7 +124,7 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
     DB_REQUIRE(height >= 1 && width >= 1, "expected a non-empty 2-D image");
     DB_REQUIRE(n_levels >= 2, "a ladder needs at least two levels");
     DB_REQUIRE(sigmas && radii && taps && tap_offsets, "NULL table");
-    DB_REQUIRE(max_blobs >= 1, "max_blobs must be >= 1");
+    DB_REQUIRE(max_blobs >= 1 && max_blobs < (1 << 24), "max_blobs must be in [1, 2^24)");
     DB_REQUIRE(height <= 32768 && width <= 32768, "image dimension above 32768");
     for (int i = 0; i < n_levels; ++i) {
         DB_REQUIRE(sigmas[i] > 0.0, "sigma must be > 0");
@@ -273,15 +274,16 @@ int dogblob_detect(const dogblob_plan *plan, const float *d_image, float thresho
     DB_CUDA(launch_reset_counters(bs, st));
     DB_CUDA(launch_row_pass(g, d_image, rows_t, plan->d_levels, plan->d_taps,
                             plan->d_level_order, st));
+    DB_CUDA(ev(1));
     DB_CUDA(launch_col_dog_pass(g, rows_t, dog_t, plan->d_levels, plan->d_taps,
                                 plan->d_group_begin, st));
-    DB_CUDA(ev(1));
+    DB_CUDA(ev(2));
     // D^T planes: rows = x (W valid), cols = y (H valid)
     DB_CUDA(launch_extrema(dog_t, g.L - 1, g.W, g.H, g.Hp, (int64_t)g.Hp * g.Wp, true,
                            plan->d_slice_sigma, threshold, neighborhood / 2, bs, st));
-    DB_CUDA(ev(2));
-    DB_CUDA(launch_prune_and_pack(bs, overlap, prune != 0, d_result, plan->max_blobs, st));
     DB_CUDA(ev(3));
+    DB_CUDA(launch_prune_and_pack(bs, overlap, prune != 0, d_result, plan->max_blobs, st));
+    DB_CUDA(ev(4));
     return DOGBLOB_OK;
 }
 

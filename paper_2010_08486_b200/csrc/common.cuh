@@ -66,6 +66,7 @@ struct BlobSpace {
     int *parent;                 // union-find over plateau members
     int *pl_count;               // per-root member count
     unsigned long long *pl_sum_row, *pl_sum_col;
+    unsigned long long *pl_first;   // min over members of (y << 44 | x << 24 | member): raster-first voxel
     dogblob_blob *unsorted;      // candidates in emission order
     dogblob_blob *sorted;        // candidates in (-response, y, x, sigma) order
     int *first;                  // prune: smallest offending partner j > i, or -1

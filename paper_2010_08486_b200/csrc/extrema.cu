@@ -39,14 +39,18 @@ __device__ bool is_block_max(const Volume &vol, int s, int r, int c, float v, in
     return true;
 }
 
-// does a flagged voxel share an in-slice 8-neighbour that is flagged too?
-__device__ bool has_flagged_neighbour(const Volume &vol, int s, int r, int c, float v, int h) {
+// does a flagged voxel share an in-slice 8-neighbour that is flagged too?  For
+// n >= 3 such a neighbour necessarily has the same value (each is >= the other);
+// for n == 1 every voxel above the threshold is flagged.
+__device__ bool has_flagged_neighbour(const Volume &vol, int s, int r, int c, float v, int h,
+                                      float thr) {
     for (int dr = -1; dr <= 1; ++dr)
         for (int dc = -1; dc <= 1; ++dc) {
             if (dr == 0 && dc == 0) continue;
             const int rr = r + dr, cc = c + dc;
             if (rr < 0 || rr >= vol.rows || cc < 0 || cc >= vol.cols) continue;
-            if (vol.at(s, rr, cc) == v && is_block_max(vol, s, rr, cc, v, h)) return true;
+            const float nv = vol.at(s, rr, cc);
+            if (h >= 1 ? (nv == v && is_block_max(vol, s, rr, cc, nv, h)) : (nv > thr)) return true;
         }
     return false;
 }
@@ -65,79 +69,133 @@ __device__ __forceinline__ dogblob_blob make_blob(int s, double x, double y, flo
 }
 
 // ---- NMS + compaction -----------------------------------------------------------
+// A CTA stages a (kNmsRows + 2) x (1024 + 2) tile of one DoG slice in shared memory
+// (every load issued up front: 10 independent 16-byte loads per thread), so the
+// threshold test and the 8 in-slice neighbours of the 3x3x3 block cost no global
+// traffic.  Only 2-D local maxima above the threshold (a few thousand per frame)
+// read their 18 cross-slice neighbours, in two batches of 9 independent loads.
+constexpr int kNmsRows = 8;
+constexpr int kNmsCols = 1024;                 // 256 threads x 4
+constexpr int kNmsPitch = kNmsCols + 8;        // halo column at index 3 and kNmsCols + 4
+
 template <int VEC>
 __global__ void __launch_bounds__(256)
 nms_kernel(Volume vol, float thr, int h, bool transposed, const double *__restrict__ slice_sigma,
            BlobSpace bs) {
-    const int cols_v = (vol.cols + VEC - 1) / VEC;
-    const int64_t total = (int64_t)vol.S * vol.rows * cols_v;
-    const unsigned lane = threadIdx.x & 31;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    // all lanes of a warp run the same number of iterations (ballots below)
-    const int64_t first = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t warp_first = first - lane;
-    for (int64_t base = warp_first; base < total; base += stride) {
-        const int64_t i = base + lane;
-        float v[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-        int s = 0, r = 0, c = 0;
-        if (i < total) {
-            const int cv = (int)(i % cols_v);
-            const int64_t t = i / cols_v;
-            r = (int)(t % vol.rows);
-            s = (int)(t / vol.rows);
-            c = cv * VEC;
-            const float *p = vol.data + (int64_t)s * vol.plane + (int64_t)r * vol.pitch + c;
+    __shared__ __align__(16) float tile[(kNmsRows + 2) * kNmsPitch];
+    const int s = blockIdx.z;
+    const int r0 = blockIdx.y * kNmsRows;
+    const int c0 = blockIdx.x * kNmsCols;
+    const int t = threadIdx.x;
+    const unsigned lane = t & 31;
+    const float *plane = vol.data + (int64_t)s * vol.plane;
+    const int c = c0 + 4 * t;
+    // ---- stage the tile (+1 halo on every side, -inf outside the plane) ----
+#pragma unroll
+    for (int rr = 0; rr < kNmsRows + 2; ++rr) {
+        const int r = r0 - 1 + rr;
+        float4 q = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        if (r >= 0 && r < vol.rows && c < vol.cols) {
+            const float *p = plane + (int64_t)r * vol.pitch + c;
             if (VEC == 4) {
-                const float4 q = __ldg(reinterpret_cast<const float4 *>(p));
-                v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+                q = __ldg(reinterpret_cast<const float4 *>(p));   // pitch-padded: in bounds
+                if (c + 1 >= vol.cols) q.y = -INFINITY;
+                if (c + 2 >= vol.cols) q.z = -INFINITY;
+                if (c + 3 >= vol.cols) q.w = -INFINITY;
             } else {
-                v[0] = __ldg(p);
+                q.x = __ldg(p);
+                if (c + 1 < vol.cols) q.y = __ldg(p + 1);
+                if (c + 2 < vol.cols) q.z = __ldg(p + 2);
+                if (c + 3 < vol.cols) q.w = __ldg(p + 3);
             }
         }
-        bool any = false;
-#pragma unroll
-        for (int k = 0; k < VEC; ++k) any |= (v[k] > thr) && (c + k < vol.cols);
+        *reinterpret_cast<float4 *>(&tile[rr * kNmsPitch + 4 + 4 * t]) = q;
+    }
+    if (t < 2 * (kNmsRows + 2)) {
+        const int rr = t >> 1, side = t & 1;
+        const int r = r0 - 1 + rr;
+        const int cc = side ? c0 + kNmsCols : c0 - 1;
+        float x = -INFINITY;
+        if (r >= 0 && r < vol.rows && cc >= 0 && cc < vol.cols)
+            x = __ldg(plane + (int64_t)r * vol.pitch + cc);
+        tile[rr * kNmsPitch + (side ? kNmsCols + 4 : 3)] = x;
+    }
+    __syncthreads();
+    // ---- test ----
+#pragma unroll 1
+    for (int q = 1; q <= kNmsRows; ++q) {
+        const int r = r0 - 1 + q;
+        const float *row = &tile[q * kNmsPitch + 4 + 4 * t];
+        const float4 mid = *reinterpret_cast<const float4 *>(row);
+        const float v[4] = {mid.x, mid.y, mid.z, mid.w};
+        const bool any = (mid.x > thr) | (mid.y > thr) | (mid.z > thr) | (mid.w > thr);
         if (!__any_sync(0xffffffffu, any)) continue;
 #pragma unroll
-        for (int k = 0; k < VEC; ++k) {
+        for (int k = 0; k < 4; ++k) {
+            const float val = v[k];
+            bool cand = val > thr;            // out-of-plane voxels hold -inf
+            if (cand && h >= 1) {             // the 8 in-slice neighbours are in every n >= 3 block
+                const float *u = row + k - kNmsPitch, *m = row + k, *d = row + k + kNmsPitch;
+                cand = !(u[-1] > val) && !(u[0] > val) && !(u[1] > val) && !(m[-1] > val) &&
+                       !(m[1] > val) && !(d[-1] > val) && !(d[0] > val) && !(d[1] > val);
+            }
+            if (!__any_sync(0xffffffffu, cand)) continue;
             bool flagged = false, plateau = false;
-            if (v[k] > thr && c + k < vol.cols && is_block_max(vol, s, r, c + k, v[k], h)) {
-                flagged = true;
-                plateau = has_flagged_neighbour(vol, s, r, c + k, v[k], h);
+            if (cand) {
+                if (h == 1) {                 // 3x3x3: in-slice part done, two batches of 9 loads
+                    flagged = true;
+#pragma unroll
+                    for (int ds = -1; ds <= 1; ds += 2) {
+                        const int ss = s + ds;
+                        if (ss < 0 || ss >= vol.S) continue;
+                        float nb[9];
+#pragma unroll
+                        for (int j = 0; j < 9; ++j) {
+                            const int rr = r + j / 3 - 1, cc = c + k + j % 3 - 1;
+                            nb[j] = (rr >= 0 && rr < vol.rows && cc >= 0 && cc < vol.cols)
+                                        ? vol.at(ss, rr, cc) : -INFINITY;
+                        }
+#pragma unroll
+                        for (int j = 0; j < 9; ++j) flagged = flagged && !(nb[j] > val);
+                    }
+                } else {
+                    flagged = is_block_max(vol, s, r, c + k, val, h);
+                }
+                if (flagged) plateau = has_flagged_neighbour(vol, s, r, c + k, val, h, thr);
             }
             // warp-aggregated append: one atomic per warp and list
             const unsigned m_single = __ballot_sync(0xffffffffu, flagged && !plateau);
             const unsigned m_plat = __ballot_sync(0xffffffffu, flagged && plateau);
-            if (m_single | m_plat) {
-                const unsigned lt = (1u << lane) - 1u;
-                int base_s = 0, base_p = 0;
-                if (lane == 0) {
-                    atomicAdd(&bs.ctr->n_flagged, __popc(m_single) + __popc(m_plat));
-                    if (m_single) base_s = atomicAdd(&bs.ctr->n_candidates, __popc(m_single));
-                    if (m_plat) base_p = atomicAdd(&bs.ctr->n_plateau, __popc(m_plat));
+            if (!(m_single | m_plat)) continue;
+            const unsigned lt = (1u << lane) - 1u;
+            int base_s = 0, base_p = 0;
+            if (lane == 0) {
+                atomicAdd(&bs.ctr->n_flagged, __popc(m_single) + __popc(m_plat));
+                if (m_single) base_s = atomicAdd(&bs.ctr->n_candidates, __popc(m_single));
+                if (m_plat) base_p = atomicAdd(&bs.ctr->n_plateau, __popc(m_plat));
+            }
+            base_s = __shfl_sync(0xffffffffu, base_s, 0);
+            base_p = __shfl_sync(0xffffffffu, base_p, 0);
+            if (flagged && !plateau) {
+                const int idx = base_s + __popc(m_single & lt);
+                if (idx < bs.cap) {
+                    const int cc = c + k;
+                    bs.unsorted[idx] = make_blob(s, transposed ? r : cc, transposed ? cc : r, val,
+                                                 vol.S, slice_sigma);
+                } else {
+                    atomicOr(&bs.ctr->flags, DOGBLOB_FLAG_OVERFLOW);
                 }
-                base_s = __shfl_sync(0xffffffffu, base_s, 0);
-                base_p = __shfl_sync(0xffffffffu, base_p, 0);
-                if (flagged && !plateau) {
-                    const int idx = base_s + __popc(m_single & lt);
-                    if (idx < bs.cap) {
-                        const int cc = c + k;
-                        bs.unsorted[idx] = make_blob(s, transposed ? r : cc, transposed ? cc : r,
-                                                     v[k], vol.S, slice_sigma);
-                    } else {
-                        atomicOr(&bs.ctr->flags, DOGBLOB_FLAG_OVERFLOW);
-                    }
-                } else if (flagged) {
-                    const int idx = base_p + __popc(m_plat & lt);
-                    if (idx < bs.cap) {
-                        bs.plateau[idx] = Voxel{s, r, c + k, v[k]};
-                        bs.parent[idx] = idx;
-                        bs.pl_count[idx] = 0;
-                        bs.pl_sum_row[idx] = 0ull;
-                        bs.pl_sum_col[idx] = 0ull;
-                    } else {
-                        atomicOr(&bs.ctr->flags, DOGBLOB_FLAG_OVERFLOW);
-                    }
+            } else if (flagged) {
+                const int idx = base_p + __popc(m_plat & lt);
+                if (idx < bs.cap) {
+                    bs.plateau[idx] = Voxel{s, r, c + k, val};
+                    bs.parent[idx] = idx;
+                    bs.pl_count[idx] = 0;
+                    bs.pl_sum_row[idx] = 0ull;
+                    bs.pl_sum_col[idx] = 0ull;
+                    bs.pl_first[idx] = ~0ull;
+                } else {
+                    atomicOr(&bs.ctr->flags, DOGBLOB_FLAG_OVERFLOW);
                 }
             }
         }
@@ -184,7 +242,7 @@ __global__ void __launch_bounds__(256) plateau_link_kernel(BlobSpace bs) {
     }
 }
 
-__global__ void __launch_bounds__(256) plateau_reduce_kernel(BlobSpace bs) {
+__global__ void __launch_bounds__(256) plateau_reduce_kernel(BlobSpace bs, bool transposed) {
     const int n = min(bs.ctr->n_plateau, bs.cap);
     for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) {
         const int root = uf_find(bs.parent, a);
@@ -192,6 +250,9 @@ __global__ void __launch_bounds__(256) plateau_reduce_kernel(BlobSpace bs) {
         atomicAdd(&bs.pl_count[root], 1);
         atomicAdd(&bs.pl_sum_row[root], (unsigned long long)v.row);
         atomicAdd(&bs.pl_sum_col[root], (unsigned long long)v.col);
+        // the component's response is the value at its raster-first (y, then x) voxel
+        const unsigned long long y = transposed ? v.col : v.row, x = transposed ? v.row : v.col;
+        atomicMin(&bs.pl_first[root], (y << 44) | (x << 24) | (unsigned long long)a);
     }
 }
 
@@ -200,7 +261,7 @@ plateau_emit_kernel(BlobSpace bs, int S, bool transposed, const double *__restri
     const int n = min(bs.ctr->n_plateau, bs.cap);
     for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) {
         if (bs.parent[a] != a) continue;
-        const Voxel v = bs.plateau[a];
+        const Voxel v = bs.plateau[(int)(bs.pl_first[a] & 0xFFFFFFull)];
         const double cnt = (double)bs.pl_count[a];
         // ndimage.center_of_mass: float64 sum / count, then Python round() = half-even
         const double cr = rint((double)bs.pl_sum_row[a] / cnt);
@@ -291,7 +352,7 @@ cudaError_t launch_extrema(const float *d_slices, int S, int rows, int cols, int
     Volume vol{d_slices, S, rows, cols, pitch, plane};
     const bool vec4 = (pitch % 4 == 0) && (plane % 4 == 0) &&
                       ((reinterpret_cast<uintptr_t>(d_slices) & 15u) == 0);
-    const int grid = 148 * 8;
+    const dim3 grid((cols + kNmsCols - 1) / kNmsCols, (rows + kNmsRows - 1) / kNmsRows, S);
     if (vec4)
         nms_kernel<4><<<grid, 256, 0, st>>>(vol, threshold, half, transposed, d_slice_sigma, bs);
     else
@@ -299,7 +360,7 @@ cudaError_t launch_extrema(const float *d_slices, int S, int rows, int cols, int
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     plateau_link_kernel<<<296, 256, 0, st>>>(bs);
-    plateau_reduce_kernel<<<148, 256, 0, st>>>(bs);
+    plateau_reduce_kernel<<<148, 256, 0, st>>>(bs, transposed);
     plateau_emit_kernel<<<148, 256, 0, st>>>(bs, S, transposed, d_slice_sigma);
     rank_sort_kernel<<<296, 256, 0, st>>>(bs);
     return cudaGetLastError();

@@ -241,6 +241,38 @@ class _Plan:
             pass
 
 
+N_EVENTS = 5   # DOGBLOB_N_EVENTS: start | row pass | column+DoG pass | extrema | prune+pack
+
+
+def new_events():
+    lib = _lib.load()
+    events = (C.c_void_p * N_EVENTS)()
+    for k in range(N_EVENTS):
+        e = C.c_void_p()
+        _lib.check(lib.dogblob_event_create(C.byref(e)))
+        events[k] = e
+    return events
+
+
+def free_events(events) -> None:
+    lib = _lib.load()
+    for k in range(N_EVENTS):
+        if events[k]:
+            lib.dogblob_event_destroy(events[k])
+            events[k] = None
+
+
+def event_intervals_ms(events) -> list:
+    """[row pass, column+DoG pass, extrema, prune+pack] in milliseconds."""
+    lib = _lib.load()
+    out = []
+    for k in range(N_EVENTS - 1):
+        ms = C.c_float()
+        _lib.check(lib.dogblob_event_elapsed_ms(events[k], events[k + 1], C.byref(ms)))
+        out.append(float(ms.value))
+    return out
+
+
 class _Slot:
     """Buffers + stream of one in-flight frame (one per concurrent caller)."""
 
@@ -261,11 +293,7 @@ class _Slot:
         self.h_result_np = self.h_result.numpy()
         self.h_image_np = self.h_image.numpy()
         self.n_host = n_host
-        self.events = (C.c_void_p * 4)()
-        for k in range(4):
-            e = C.c_void_p()
-            _lib.check(lib.dogblob_event_create(C.byref(e)))
-            self.events[k] = e
+        self.events = new_events()
         torch.cuda.synchronize(dev)
         self.pending = None     # bookkeeping of run_batch
 
@@ -280,14 +308,14 @@ class _Slot:
             self.d_work.data_ptr(), self.d_result.data_ptr(), self.h_result.data_ptr(),
             self.n_host, self.stream.cuda_stream, self.events))
 
-    def launch_device(self, d_frame, params: DetectionParams, prune: bool) -> None:
+    def launch_device(self, d_frame, params: DetectionParams, prune: bool, events=None) -> None:
         """Same, for a frame that is already resident: a float32 CUDA tensor [H][pitch]."""
         lib = _lib.load()
         _lib.check(lib.dogblob_detect(
             self.plan.handle, d_frame.data_ptr(), float(np.float32(params.threshold)),
             int(params.neighborhood), float(params.overlap), 1 if prune else 0,
             self.d_work.data_ptr(), self.d_result.data_ptr(), self.stream.cuda_stream,
-            self.events))
+            self.events if events is None else events))
 
     def _host_pointer(self, frame) -> int:
         torch = _torch()
@@ -322,20 +350,11 @@ class _Slot:
         return hdr, recs
 
     def stage_times_ms(self) -> dict:
-        lib = _lib.load()
-        out = []
-        for a, b in ((0, 1), (1, 2), (2, 3)):
-            ms = C.c_float()
-            _lib.check(lib.dogblob_event_elapsed_ms(self.events[a], self.events[b], C.byref(ms)))
-            out.append(float(ms.value))
-        return {"convolve_ms": out[0], "extrema_ms": out[1], "prune_ms": out[2]}
+        t = event_intervals_ms(self.events)
+        return {"convolve_ms": t[0] + t[1], "extrema_ms": t[2], "prune_ms": t[3]}
 
     def close(self):
-        lib = _lib.load()
-        for k in range(4):
-            if self.events[k]:
-                lib.dogblob_event_destroy(self.events[k])
-                self.events[k] = None
+        free_events(self.events)
 
 
 class _Engine:

@@ -1,0 +1,330 @@
+"""GPU parity, stage by stage, through the C ABI (libdogblob_b200.so).
+
+Ports the reference's tests/test_convolve.py and tests/test_detector.py to
+backend="cuda" and compares every stage with the CPU oracle on the same inputs.
+Tolerances (float32 arithmetic, stated per test):
+  levels : |gpu - float64 truth| <= 2e-6 (levels are O(1); the reference's own
+           float32 backends agree to 4.17e-7, pkg/test_output.txt:15)
+  DoG    : <= sigma_i * 2e-6
+  extrema, pruning, ordering, histogram: bit-exact on identical inputs.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_2010_08486_b200 as P
+from oracle import dog_oracle as O
+from paper_2010_08486_b200 import synth
+from parity import golden_blobs, golden_oblobs, oblob_tuples, records_tuples
+
+pytestmark = pytest.mark.gpu
+
+LEVEL_TOL = 2e-6
+
+
+def bank_for(lo, hi, n, truncate=5.0):
+    return P.build_kernel_bank(P.build_ladder(lo, hi, n), truncate)
+
+
+def truth_levels(img, bank):
+    return O.levels_separable(np.asarray(img, dtype=np.float64), bank.ladder.sigmas, bank.radii)
+
+
+class TestConvolveBank:
+    def test_constant_image_all_levels_constant(self):
+        bank = bank_for(1.0, 4.0, 3)
+        img = np.full((33, 47), 0.42, dtype=np.float32)
+        stack = P.convolve_bank(img, bank, "cuda")
+        assert stack.n_levels == 4 and stack.levels.dtype == np.float32
+        assert stack.shape == (33, 47)
+        assert np.allclose(stack.levels, 0.42, atol=1e-5)
+
+    def test_impulse_reproduces_kernel(self):
+        bank = bank_for(1.0, 2.0, 1)
+        img = np.zeros((41, 41), dtype=np.float32)
+        img[20, 20] = 1.0
+        r = int(bank.radii[0]); c = bank.max_width // 2
+        expected = bank.kernels[0, c - r:c + r + 1, c - r:c + r + 1]
+        got = P.convolve_bank(img, bank, "cuda").levels[0, 20 - r:20 + r + 1, 20 - r:20 + r + 1]
+        assert np.allclose(got, expected, atol=1e-7)
+
+    def test_matches_reference_backends(self, golden):
+        g = golden("small_stages.npz")
+        bank = bank_for(1.0, 4.0, 3)
+        got = P.convolve_bank(g["a_img"], bank, "cuda").levels
+        assert np.abs(got - g["a_levels_fft_f64"]).max() < LEVEL_TOL
+        assert np.abs(got - g["a_levels_direct_f32"]).max() < 1e-4   # the reference's own bar
+        assert np.abs(got - g["a_levels_fft_f32"]).max() < 1e-4
+
+    def test_matches_scipy_reflect_correlation(self):
+        from scipy import ndimage
+        bank = bank_for(1.0, 4.0, 3)
+        img = np.random.default_rng(23).random((40, 40)).astype(np.float32)
+        got = P.convolve_bank(img, bank, "cuda").levels
+        for i in range(2):
+            r = int(bank.radii[i]); c = bank.max_width // 2
+            ref = ndimage.correlate(img.astype(np.float64),
+                                    bank.kernels[i, c - r:c + r + 1, c - r:c + r + 1], mode="reflect")
+            assert np.abs(got[i] - ref).max() < LEVEL_TOL
+
+    def test_linearity(self):
+        bank = bank_for(1.0, 4.0, 3)
+        rng = np.random.default_rng(24)
+        a, b = 1.7, -0.6
+        i1 = rng.random((32, 32)).astype(np.float32)
+        i2 = rng.random((32, 32)).astype(np.float32)
+        s1 = P.convolve_bank(i1, bank).levels.astype(np.float64)
+        s2 = P.convolve_bank(i2, bank).levels.astype(np.float64)
+        s12 = P.convolve_bank((a * i1 + b * i2).astype(np.float32), bank).levels
+        assert np.abs(s12 - (a * s1 + b * s2)).max() < 5e-6
+
+    def test_kernel_wider_than_image_still_matches(self, golden):
+        g = golden("small_stages.npz")
+        bank = bank_for(5.0, 10.0, 1)
+        got = P.convolve_bank(g["b_img"].astype(np.float32), bank).levels
+        assert np.abs(got - g["b_levels_fft_f64"]).max() < LEVEL_TOL
+
+    @pytest.mark.parametrize("tag", ["c1", "c2", "c3", "c4"])
+    def test_ragged_and_single_pixel_shapes(self, golden, tag):
+        g = golden("small_stages.npz")
+        bank = bank_for(0.8, 2.4, 2)
+        got = P.convolve_bank(g[tag + "_img"], bank).levels
+        assert got.shape == g[tag + "_levels_fft_f64"].shape
+        assert np.abs(got - g[tag + "_levels_fft_f64"]).max() < LEVEL_TOL
+
+    @pytest.mark.parametrize("shape", [(127, 129), (128, 128), (130, 257), (300, 200)])
+    def test_tile_boundaries(self, shape):
+        bank = bank_for(1.0, 9.0, 4)
+        img = np.random.default_rng(shape[0]).random(shape).astype(np.float32)
+        got = P.convolve_bank(img, bank).levels
+        assert np.abs(got - truth_levels(img, bank)).max() < LEVEL_TOL
+
+    def test_wide_filters(self):
+        bank = bank_for(20.0, 60.0, 2)          # radii 100 .. 300
+        img = np.random.default_rng(5).random((256, 384)).astype(np.float32)
+        got = P.convolve_bank(img, bank).levels
+        assert np.abs(got - truth_levels(img, bank)).max() < LEVEL_TOL
+
+    def test_errors(self):
+        bank = bank_for(1.0, 4.0, 3)
+        with pytest.raises(ValueError, match="backend"):
+            P.convolve_bank(np.ones((4, 4)), bank, "gpu")
+        with pytest.raises(ValueError):
+            P.convolve_bank(np.ones((0, 4)), bank)
+        with pytest.raises(ValueError, match="cap"):
+            P.convolve_bank(np.ones((64, 64), np.float32), bank, stack_element_cap=1000)
+        with pytest.raises(ValueError):
+            P.convolve_bank(np.ones((8, 8)), bank, dtype=np.float64)
+
+
+class TestDogStack:
+    def test_constant_image_gives_zero_slices(self):
+        bank = bank_for(1.0, 3.0, 2)
+        stack = P.convolve_bank(np.full((20, 20), 0.5, dtype=np.float32), bank)
+        dog = P.dog_stack(stack, bank.ladder)
+        assert dog.n_slices == 2 and np.abs(dog.slices).max() < 1e-5
+
+    def test_dog_stack_bit_exact_on_same_levels(self, golden):
+        g = golden("small_stages.npz")
+        ladder = P.build_ladder(1.0, 4.0, 3)
+        dog = P.dog_stack(P.ScaleStack(g["a_levels_fft_f32"], ladder.sigmas), ladder)
+        assert np.array_equal(dog.slices, g["a_dog_f32"])
+
+    def test_impulse_center_value_from_kernel_oracle(self):
+        bank = bank_for(1.0, 2.0, 1)
+        img = np.zeros((41, 41), dtype=np.float32)
+        img[20, 20] = 1.0
+        dog = P.fused_dog(img, bank)
+        c = bank.max_width // 2
+        expected = 1.0 * (bank.kernels[0, c, c] - bank.kernels[1, c, c])
+        assert dog.slices[0, 20, 20] == pytest.approx(expected, rel=1e-5)
+        assert dog.slices[0, 20, 26] < 0
+
+    def test_fused_kernels_equal_staged_path(self):
+        """the production kernels (subtraction fused into the column pass) give
+        bit-identical slices to convolve_bank + dog_stack"""
+        bank = bank_for(1.0, 6.0, 9)
+        img = synth.sensor_noise(synth.droplet_scene(200, 160, 10, (4.0, 12.0), seed=7), seed=8).image
+        fused = P.fused_dog(img, bank)
+        staged = P.dog_stack(P.convolve_bank(img, bank), bank.ladder)
+        assert np.array_equal(fused.slices, staged.slices)
+
+    def test_fused_dog_against_float64_truth(self):
+        bank = bank_for(1.0, 10.0, 18)
+        img = synth.config_frame("C1")
+        got = P.fused_dog(img, bank).slices
+        want = O.dog_slices(truth_levels(img, bank), bank.ladder.sigmas)
+        err = np.abs(got - want).max(axis=(1, 2)) / bank.ladder.sigmas[:-1]
+        assert err.max() < LEVEL_TOL
+
+    def test_level_count_mismatch_rejected(self):
+        bank = bank_for(1.0, 3.0, 2)
+        stack = P.convolve_bank(np.ones((8, 8), np.float32), bank)
+        with pytest.raises(ValueError):
+            P.dog_stack(stack, P.build_ladder(1.0, 3.0, 4))
+
+
+def dog_of(slices, sigmas):
+    return P.DoGStack(slices=np.asarray(slices, dtype=np.float32), sigmas=np.asarray(sigmas, float))
+
+
+class TestFindExtrema:
+    def test_all_zero_stack_is_empty(self):
+        assert len(P.find_extrema(dog_of(np.zeros((3, 16, 16)), [1.0, 2.0, 3.0]))) == 0
+
+    def test_random_stack_bit_exact(self, golden):
+        g = golden("small_stages.npz")
+        got = P.find_extrema(dog_of(g["d_slices"], [1.0, 2.0, 3.0]), threshold=0.2)
+        assert records_tuples(got.records) == golden_blobs(g, "d_cand_")
+        assert [(b.x, b.y, b.sigma, b.radius, b.response, b.at_scale_boundary)
+                for b in got.blobs] == golden_blobs(g, "d_cand_")
+
+    @pytest.mark.parametrize("n", [1, 5])
+    def test_other_neighbourhoods(self, golden, n):
+        g = golden("small_stages.npz")
+        got = P.find_extrema(dog_of(g["d_slices"], [1.0, 2.0, 3.0]), threshold=0.2, neighborhood=n)
+        assert records_tuples(got.records) == golden_blobs(g, f"d_n{n}_cand_")
+
+    def test_plateau_coalesces_to_centroid(self, golden):
+        g = golden("small_stages.npz")
+        got = P.find_extrema(dog_of(g["e_slices"], [2.0, 3.0]), threshold=0.1)
+        assert records_tuples(got.records) == golden_blobs(g, "e_cand_")
+        slices = np.zeros((1, 21, 21), dtype=np.float32)
+        slices[0, 9:12, 8:14] = 0.5
+        one = P.find_extrema(dog_of(slices, [2.0]), threshold=0.1)
+        assert len(one) == 1
+        b = one.blobs[0]
+        assert (b.x, b.y) == (10, 10) and b.response == pytest.approx(0.5)
+
+    def test_on_reference_dog_bit_exact(self, golden):
+        g = golden("small_stages.npz")
+        got = P.find_extrema(dog_of(g["a_dog_f32"], g["a_sigmas"][:-1]), threshold=0.02)
+        assert records_tuples(got.records) == golden_blobs(g, "a_cand_")
+
+    def test_boundary_voxels_can_be_maxima(self):
+        slices = np.zeros((2, 9, 9), dtype=np.float32)
+        slices[0, 0, 0] = 1.0
+        blobs = P.find_extrema(dog_of(slices, [1.0, 2.0]), threshold=0.5)
+        assert len(blobs) == 1 and blobs.blobs[0].at_scale_boundary
+
+    def test_big_plateau_and_many_candidates(self):
+        """a 40x50 plateau (2000 members) and a checkerboard of ~10^4 singles,
+        against the oracle, unaligned width (scalar NMS path)"""
+        rng = np.random.default_rng(3)
+        sl = (rng.random((2, 203, 199)) * 0.05).astype(np.float32)
+        sl[0, 20:60, 30:80] = 0.9
+        sl[1, 100:200:2, 0:199:2] = 0.5 + (rng.random((50, 100)) * 0.4).astype(np.float32)
+        got = P.find_extrema(dog_of(sl, [1.5, 2.5]), threshold=0.1)
+        want = O.extrema(sl, np.array([1.5, 2.5]), 0.1)
+        assert records_tuples(got.records) == oblob_tuples(want)
+        assert len(want) > 4000
+
+    def test_capacity_overflow_grows_and_stays_exact(self):
+        rng = np.random.default_rng(4)
+        sl = np.zeros((1, 64, 64), dtype=np.float32)
+        sl[0, ::2, ::2] = 0.5 + (rng.random((32, 32)) * 0.4).astype(np.float32)
+        got = P.find_extrema(dog_of(sl, [1.0]), threshold=0.1, max_blobs=64)
+        assert records_tuples(got.records) == oblob_tuples(O.extrema(sl, np.array([1.0]), 0.1))
+
+    def test_neighborhood_must_be_odd(self):
+        with pytest.raises(ValueError):
+            P.find_extrema(dog_of(np.zeros((1, 8, 8)), [1.0]), neighborhood=4)
+
+    def test_single_disk_scale_selection(self):
+        img = synth.flat_disk(128, 128, 64, 64, 10.0)
+        ladder = P.build_ladder(4.0, 10.0, 12)
+        bank = P.build_kernel_bank(ladder)
+        blobs = P.find_extrema(P.fused_dog(img, bank), threshold=0.1)
+        assert len(blobs) == 1
+        got = blobs.blobs[0]
+        assert (got.x, got.y) == (64, 64)
+        assert abs(got.sigma - 10.0 / math.sqrt(2)) <= ladder.delta_sigma + 0.2
+        assert got.radius == pytest.approx(math.sqrt(2) * got.sigma)
+        assert not got.at_scale_boundary
+
+    def test_scale_boundary_flag(self):
+        img = synth.flat_disk(96, 96, 48, 48, 10.0)
+        bank = P.build_kernel_bank(P.build_ladder(3.0, 7.2, 6))
+        blobs = P.find_extrema(P.fused_dog(img, bank), threshold=0.05)
+        assert len(blobs) >= 1 and blobs.blobs[0].at_scale_boundary
+
+
+def mk(x, y, radius, response, sigma=None):
+    return P.Blob(x=x, y=y, sigma=sigma if sigma is not None else radius / math.sqrt(2),
+                  radius=radius, response=response)
+
+
+def bset(*blobs):
+    return P.BlobSet(blobs=tuple(blobs), source_shape=(100, 100), params=P.DetectionParams(backend="cuda"))
+
+
+class TestPruneOverlaps:
+    def test_identical_blobs_coalesce_keeping_stronger(self):
+        out = P.prune_overlaps(bset(mk(10, 10, 5.0, 0.9), mk(10, 10, 5.0, 0.8)), 0.5)
+        assert len(out) == 1
+        k = out.blobs[0]
+        assert (k.x, k.y, k.radius, k.response) == (10, 10, 5.0, 0.9)
+
+    def test_disjoint_blobs_unchanged(self):
+        assert len(P.prune_overlaps(bset(mk(10, 10, 5.0, 0.9), mk(40, 40, 5.0, 0.8)), 0.5)) == 2
+
+    def test_partial_overlap(self):
+        a, b = mk(0, 0, 5.0, 0.9), mk(4, 0, 5.0, 0.8)
+        assert P.normalized_overlap(a, b) > 0.5
+        out = P.prune_overlaps(bset(a, b), 0.5)
+        assert len(out) == 1 and out.blobs[0].radius == 5.0 and (out.blobs[0].x, out.blobs[0].y) == (0, 0)
+
+    def test_containment_counts_as_full_overlap(self):
+        out = P.prune_overlaps(bset(mk(20, 20, 10.0, 0.5), mk(22, 20, 2.0, 0.9)), 0.5)
+        assert len(out) == 1
+        assert (out.blobs[0].x, out.blobs[0].y) == (22, 20)
+        assert out.blobs[0].radius == pytest.approx(6.0)
+
+    def test_empty_and_single(self):
+        assert len(P.prune_overlaps(bset(), 0.5)) == 0
+        assert len(P.prune_overlaps(bset(mk(1, 1, 2.0, 0.5)), 0.5)) == 1
+
+    def test_golden_cases_bit_exact(self, golden):
+        p = golden("prune_cases.npz")
+        for c in range(int(p["n_cases"])):
+            blobs = [P.Blob(*t) for t in golden_blobs(p, f"p{c}_in_")]
+            out = P.prune_overlaps(bset(*blobs), float(p[f"p{c}_thr"]))
+            assert records_tuples(out.records) == golden_blobs(p, f"p{c}_out_"), c
+            h = P.histogram(out, P.build_ladder(1.0, 8.0, 10))
+            assert np.array_equal(h.counts, p[f"p{c}_hist_counts"])
+            assert np.array_equal(h.volume_weights, p[f"p{c}_hist_volumes"])
+
+    def test_float_centres_against_oracle(self):
+        rng = np.random.default_rng(47)
+        for trial in range(10):
+            blobs = [mk(float(rng.uniform(0, 60)), float(rng.uniform(0, 60)), float(rng.uniform(2, 9)),
+                        float(rng.uniform(0.1, 1.0))) for _ in range(15)]
+            out = P.prune_overlaps(bset(*blobs), 0.5)
+            want = O.prune([O.OBlob(b.x, b.y, b.sigma, b.radius, b.response, False) for b in blobs], 0.5)
+            assert records_tuples(out.records) == oblob_tuples(want)
+            for i in range(len(out.blobs)):
+                for j in range(i + 1, len(out.blobs)):
+                    assert P.normalized_overlap(out.blobs[i], out.blobs[j]) <= 0.5 + 1e-12
+
+    @pytest.mark.parametrize("thr", [0.5, 0.1])
+    def test_dense_c5_candidates_against_oracle(self, golden, thr):
+        """~10^4 reference candidates of the dense-droplet frame (stresses grid
+        bucketing and the merge loop)"""
+        g = golden("config_C5.npz")
+        cand = golden_oblobs(g, "t0_cand_")
+        out = P.prune_overlaps(bset(*[P.Blob(*t) for t in golden_blobs(g, "t0_cand_")]), thr)
+        if thr == 0.5:
+            assert records_tuples(out.records) == golden_blobs(g, "t0_kept_")
+        assert records_tuples(out.records) == oblob_tuples(O.prune(cand, thr))
+
+    def test_top2000_overlap01_against_reference(self, golden):
+        g = golden("config_C5.npz")
+        top = [P.Blob(*t) for t in golden_blobs(g, "t0_cand_")[:2000]]
+        out = P.prune_overlaps(bset(*top), 0.1)
+        assert records_tuples(out.records) == golden_blobs(g, "t0_top2000_kept01_")
+
+    def test_threshold_bounds(self):
+        with pytest.raises(ValueError):
+            P.prune_overlaps(bset(), 1.5)
