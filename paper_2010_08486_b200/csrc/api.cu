@@ -73,7 +73,7 @@ struct dogblob_plan {
     double *d_slice_sigma = nullptr;
     float *d_sigma_f32 = nullptr;
     // workspace layout (bytes from the workspace base)
-    size_t off_rows_t = 0, off_dog_t = 0, off_blobspace = 0, total = 0;
+    size_t off_rows_t = 0, off_dog_t = 0, off_edge = 0, off_blobspace = 0, total = 0;
 };
 
 namespace {
@@ -90,23 +90,38 @@ struct DeviceGuard {
     ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
 };
 
-// Partition levels into G contiguous groups for the fused column+DoG pass. Group g
-// emits slices [begin[g], begin[g+1]) and therefore sweeps levels begin[g]..begin[g+1].
+// Partition the L levels into G contiguous groups of similar tap count for the fused
+// column+DoG pass; group g sweeps levels [begin[g], begin[g+1]).
 std::vector<int> balance_groups(const std::vector<LevelDesc> &lv, int G) {
-    const int S = (int)lv.size() - 1;
-    G = std::max(1, std::min(G, S));
-    std::vector<double> pre(S + 1, 0.0);
-    for (int i = 0; i < S; ++i) pre[i + 1] = pre[i] + lv[i].n_chunks;
+    const int L = (int)lv.size();
+    G = std::max(1, std::min(G, L));
+    std::vector<double> pre(L + 1, 0.0);
+    for (int i = 0; i < L; ++i) pre[i + 1] = pre[i] + lv[i].n_mid + 1.07;   // first+last chunk = 136/128 of a full one
     std::vector<int> begin(G + 1, 0);
-    begin[G] = S;
+    begin[G] = L;
     for (int g = 1; g < G; ++g) {
-        const double target = pre[S] * g / G;
+        const double target = pre[L] * g / G;
         int b = (int)(std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
         b = std::max(b, begin[g - 1] + 1);
-        b = std::min(b, S - (G - g));
+        b = std::min(b, L - (G - g));
         begin[g] = b;
     }
     return begin;
+}
+
+// Number of level groups: fill whole waves of CTAs (2 resident per SM) as exactly as
+// possible; every extra group costs one boundary slice through the edge planes.
+int choose_groups(int tiles, int L) {
+    const double slots = 2.0 * 148.0;
+    int best = 1;
+    double best_score = -1.0;
+    for (int G = 1; G <= std::min(L, 24); ++G) {
+        const double waves = tiles * G / slots;
+        const double eff = waves / std::ceil(waves);
+        const double score = eff - 0.004 * G;
+        if (score > best_score) { best_score = score; best = G; }
+    }
+    return best;
 }
 
 }  // namespace
@@ -142,31 +157,35 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
     g.Hp = round_up(height, kPad);
     g.Wp = round_up(width, kPad);
 
-    // padded, duplicated tap tables: P[m] = w[m-(kTY-1)] on [kTY-1, 2r+kTY-1], else 0
+    // duplicated tap tables (w, w), radius zero-padded to a multiple of 8 so that the
+    // sliding-window sweep is a whole number of 16-row chunks (see sweep())
     std::vector<float2> table;
     plan->levels.resize(n_levels);
-    int max_table = 0;
+    int max_table = 0, max_rpad = 0;
     for (int i = 0; i < n_levels; ++i) {
         const int r = radii[i];
+        const int rpad = std::max(8, (r + 7) / 8 * 8);
         LevelDesc &lv = plan->levels[i];
-        lv.radius = r;
-        lv.n_chunks = (kTY + 2 * r + kTY - 1) / kTY;
+        lv.rpad = rpad;
+        lv.n_mid = (2 * rpad + kTY) / kTY - 2;
         lv.tap_ofs = (int)table.size();
         lv.sigma_f32 = (float)sigmas[i];
-        const int len = lv.n_chunks * kTY + kTY - 1;
+        const int len = 2 * rpad + 1;
         max_table = std::max(max_table, len);
+        max_rpad = std::max(max_rpad, rpad);
         const float *w = taps + tap_offsets[i];
         for (int m = 0; m < len; ++m) {
-            const int k = m - (kTY - 1);
+            const int k = m - (rpad - r);
             const float v = (k >= 0 && k <= 2 * r) ? w[k] : 0.f;
             table.push_back(make_float2(v, v));
         }
     }
     g.max_table = max_table;
+    g.max_rpad = max_rpad;
 
     // level groups of the fused pass: about two waves of CTAs at 2 CTAs / SM
     const int tiles = (g.Hp / kTileCols) * (g.Wp / kTileRows);
-    int G = (2 * 2 * 148 + tiles - 1) / tiles;
+    int G = choose_groups(tiles, n_levels);
     if (const char *env = std::getenv("DOGBLOB_GROUPS")) G = std::max(1, std::atoi(env));
     std::vector<int> group_begin = balance_groups(plan->levels, G);
     g.G = (int)group_begin.size() - 1;
@@ -174,7 +193,7 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
     std::vector<int> order(n_levels);
     for (int i = 0; i < n_levels; ++i) order[i] = i;
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-        return plan->levels[a].n_chunks > plan->levels[b].n_chunks;   // longest first
+        return plan->levels[a].n_mid > plan->levels[b].n_mid;   // longest first
     });
     std::vector<int> unit(n_levels + 1);
     for (int i = 0; i <= n_levels; ++i) unit[i] = i;
@@ -211,13 +230,14 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
                          cudaMemcpyHostToDevice));
     PLAN_CUDA(cudaMemcpy(plan->d_sigma_f32, sig32.data(), n_levels * sizeof(float),
                          cudaMemcpyHostToDevice));
-    PLAN_CUDA(configure_conv_kernels(max_table));
+    PLAN_CUDA(configure_conv_kernels(max_table, max_rpad));
 #undef PLAN_CUDA
 
     const size_t plane = (size_t)g.Hp * g.Wp * sizeof(float);
     size_t off = 0;
     plan->off_rows_t = off; off += align_up(plane * n_levels, 256);
     plan->off_dog_t = off;  off += align_up(plane * n_levels, 256);   // L planes: also holds levels
+    plan->off_edge = off;   off += align_up(plane * 2 * g.G, 256);       // boundary levels
     plan->off_blobspace = off; off += blobspace_bytes(max_blobs);
     plan->total = off;
     *out = plan;
@@ -275,8 +295,8 @@ int dogblob_detect(const dogblob_plan *plan, const float *d_image, float thresho
     DB_CUDA(launch_row_pass(g, d_image, rows_t, plan->d_levels, plan->d_taps,
                             plan->d_level_order, st));
     DB_CUDA(ev(1));
-    DB_CUDA(launch_col_dog_pass(g, rows_t, dog_t, plan->d_levels, plan->d_taps,
-                                plan->d_group_begin, st));
+    DB_CUDA(launch_col_dog_pass(g, rows_t, dog_t, reinterpret_cast<float *>(ws + plan->off_edge),
+                                plan->d_levels, plan->d_taps, plan->d_group_begin, st));
     DB_CUDA(ev(2));
     // D^T planes: rows = x (W valid), cols = y (H valid)
     DB_CUDA(launch_extrema(dog_t, g.L - 1, g.W, g.H, g.Hp, (int64_t)g.Hp * g.Wp, true,
@@ -357,8 +377,8 @@ int dogblob_dog(const dogblob_plan *plan, const float *d_image, void *d_workspac
     const ConvGeometry &g = plan->geo;
     DB_CUDA(launch_row_pass(g, d_image, rows_t, plan->d_levels, plan->d_taps,
                             plan->d_level_order, st));
-    DB_CUDA(launch_col_dog_pass(g, rows_t, dog_t, plan->d_levels, plan->d_taps,
-                                plan->d_group_begin, st));
+    DB_CUDA(launch_col_dog_pass(g, rows_t, dog_t, reinterpret_cast<float *>(ws + plan->off_edge),
+                                plan->d_levels, plan->d_taps, plan->d_group_begin, st));
     DB_CUDA(launch_untranspose(dog_t, g.L - 1, g.Hp, g.Wp, g.H, g.W, d_slices, st));
     return DOGBLOB_OK;
 }

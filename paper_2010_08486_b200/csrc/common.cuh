@@ -40,9 +40,9 @@ constexpr int kPrefetch = 4;            // input rows in flight per thread
 constexpr int kConvThreads = 32 * kWarps;
 
 struct LevelDesc {
-    int radius;       // r_i = ceil(truncate * sigma_i)
-    int n_chunks;     // ceil((kTY + 2 r) / kTY) sweeps of kTY input rows
-    int tap_ofs;      // start (in float2) of this level's padded tap table
+    int rpad;         // r_i = ceil(truncate * sigma_i) rounded up to a multiple of 8 (zero taps)
+    int n_mid;        // full chunks between the first and the last: (2 rpad + 16) / 16 - 2
+    int tap_ofs;      // start (in float2) of this level's duplicated tap table, 2 rpad + 1 long
     float sigma_f32;  // float32(sigma_i), the DoG scale factor
 };
 
@@ -91,14 +91,15 @@ struct ConvGeometry {
     int Hp, Wp;          // padded to kPad
     int L;               // levels
     int G;               // level groups of the fused column+DoG pass
-    int max_table;       // float2 entries of the longest padded tap table
+    int max_table;       // float2 entries of the longest tap table (2 max_rpad + 1)
+    int max_rpad;        // largest padded radius
 };
 
 cudaError_t launch_row_pass(const ConvGeometry &g, const float *d_img, float *d_rows_t,
                             const LevelDesc *d_levels, const float2 *d_taps,
                             const int *d_level_order, cudaStream_t st);
 cudaError_t launch_col_dog_pass(const ConvGeometry &g, const float *d_rows_t, float *d_dog_t,
-                                const LevelDesc *d_levels, const float2 *d_taps,
+                                float *d_edge, const LevelDesc *d_levels, const float2 *d_taps,
                                 const int *d_group_begin, cudaStream_t st);
 cudaError_t launch_col_levels_pass(const ConvGeometry &g, const float *d_rows_t, float *d_lev_t,
                                    const LevelDesc *d_levels, const float2 *d_taps,
@@ -107,7 +108,7 @@ cudaError_t launch_untranspose(const float *d_src_t, int planes, int Hp, int Wp,
                                float *d_dst, cudaStream_t st);
 cudaError_t launch_dog_from_levels(int L, int64_t plane_elems, const float *d_levels,
                                    const float *d_sigma_f32, float *d_out, cudaStream_t st);
-cudaError_t configure_conv_kernels(int max_table);
+cudaError_t configure_conv_kernels(int max_table, int max_rpad);
 
 // extrema: NMS + compaction + plateau coalescing + ordering
 cudaError_t launch_extrema(const float *d_slices, int S, int rows, int cols, int64_t pitch,

@@ -26,29 +26,22 @@ namespace {
 
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 
-// Reflect boundary as a bouncing cursor: ... 2 1 0 | 0 1 2 ... N-1 | N-1 N-2 ...
-// The row pointer is advanced incrementally (no per-step multiply): on a bounce
-// the edge row is repeated once and the direction flips.
-struct FoldCursor {
-    int m, dir, n;
-    const float *p;      // -> row m
-    int64_t dp;          // dir * pitch (elements)
-    __device__ __forceinline__ FoldCursor(const float *base, int64_t pitch, int start, int n_)
-        : n(n_) {
-        int period = 2 * n_;
-        int t = start % period;
-        if (t < 0) t += period;
-        if (t < n_) { m = t; dir = 1; } else { m = period - 1 - t; dir = -1; }
-        p = base + (int64_t)m * pitch;
-        dp = dir > 0 ? pitch : -pitch;
-    }
-    __device__ __forceinline__ void step() {
-        const int nm = m + dir;
-        const bool bounce = (nm == n) | (nm < 0);
-        if (bounce) { dir = -dir; dp = -dp; }
-        else { m = nm; p += dp; }
-    }
-};
+// Reflect boundary ("edge sample repeated", period 2n): folded row index of any integer.
+__device__ __forceinline__ int fold_row(int i, int n) {
+    const int period = 2 * n;
+    int t = i % period;
+    if (t < 0) t += period;
+    return t < n ? t : period - 1 - t;
+}
+
+// Per-CTA table of folded row offsets (in elements) for input rows
+// first_row .. first_row + count - 1; replaces per-step boundary arithmetic by one
+// broadcast LDS.
+__device__ __forceinline__ void stage_row_offsets(int *s_rows, int first_row, int count, int n_rows,
+                                                  int pitch) {
+    for (int i = threadIdx.x; i < count; i += blockDim.x)
+        s_rows[i] = fold_row(first_row + i, n_rows) * pitch;
+}
 
 template <bool ADJACENT>
 __device__ __forceinline__ void load_row(const float *__restrict__ row, int lane, float (&v)[4]) {
@@ -61,38 +54,54 @@ __device__ __forceinline__ void load_row(const float *__restrict__ row, int lane
     }
 }
 
-// One sweep: acc[j][p] = sum_k w[k] * in[fold(out_row0 + j + k)][cols(p)]
-// `taps` is the zero-padded, duplicated table P of this level in shared memory:
-// P[m] = w[m - (kTY-1)] for kTY-1 <= m <= 2r + kTY-1, else 0, so that the tap of
-// (input step s, output j) is P[s - j + kTY - 1] and no bounds test is needed.
+// One sweep: acc[j][p] = sum_k w[k] * in[fold(out_row0 + j + k - R)][cols(p)], R = lv.rpad.
+//
+// The tap radius is padded with zeros to a multiple of 8 (R), so the sweep is exactly
+// (2R + 16) / 16 chunks of 16 input rows and both ends are chunk aligned:
+//   step s (input row out_row0 - R + s) feeds output j with tap[s - j], 0 <= s - j <= 2R
+//   first chunk  : sub-step u feeds outputs j <= u          (136 FMA groups)
+//   middle chunks: every sub-step feeds all 16 outputs      (256 each)
+//   last chunk   : sub-step u feeds outputs j >= u          (136)
+// so no FMA is spent on the triangular head and tail of the sliding window.  The tap
+// window lives in a 16-entry ring that is statically indexed by full unrolling.
 template <bool ADJACENT>
-__device__ __forceinline__ void sweep(const float *__restrict__ in, int64_t pitch, int n_rows,
-                                      int first_in_row, int n_chunks,
-                                      const float2 *__restrict__ taps, int lane,
+__device__ __forceinline__ void sweep(const float *__restrict__ in, const int *__restrict__ rows,
+                                      int n_mid, const float2 *__restrict__ taps, int lane,
                                       float2 (&acc)[kTY][2]) {
-    FoldCursor cur(in, pitch, first_in_row, n_rows);
     float v[kPrefetch][4];
 #pragma unroll
-    for (int p = 0; p < kPrefetch; ++p) {
-        load_row<ADJACENT>(cur.p, lane, v[p]);
-        cur.step();
-    }
+    for (int p = 0; p < kPrefetch; ++p) load_row<ADJACENT>(in + rows[p], lane, v[p]);
+    rows += kPrefetch;
     float2 ring[kTY];
+    // ---- first chunk ----
 #pragma unroll
-    for (int j = 0; j < kTY; ++j) {
-        ring[j] = make_float2(0.f, 0.f);
-        acc[j][0] = make_float2(0.f, 0.f);
-        acc[j][1] = make_float2(0.f, 0.f);
+    for (int u = 0; u < kTY; ++u) {
+        ring[u] = taps[u];
+        const float2 a = make_float2(v[u % kPrefetch][0], v[u % kPrefetch][1]);
+        const float2 b = make_float2(v[u % kPrefetch][2], v[u % kPrefetch][3]);
+        load_row<ADJACENT>(in + rows[u], lane, v[u % kPrefetch]);
+#pragma unroll
+        for (int j = 0; j <= u; ++j) {
+            const float2 t = ring[u - j];
+            if (j == u) {          // first contribution to output j: multiply, no accumulate
+                acc[j][0] = make_float2(__fmul_rn(t.x, a.x), __fmul_rn(t.y, a.y));
+                acc[j][1] = make_float2(__fmul_rn(t.x, b.x), __fmul_rn(t.y, b.y));
+            } else {
+                acc[j][0] = ffma2(t, a, acc[j][0]);
+                acc[j][1] = ffma2(t, b, acc[j][1]);
+            }
+        }
     }
-    const float2 *tp = taps + (kTY - 1);
-    for (int chunk = 0; chunk < n_chunks; ++chunk) {
+    taps += kTY;
+    rows += kTY;
+    // ---- middle chunks ----
+    for (int chunk = 0; chunk < n_mid; ++chunk) {
 #pragma unroll
         for (int u = 0; u < kTY; ++u) {
-            ring[u] = tp[u];
+            ring[u] = taps[u];
             const float2 a = make_float2(v[u % kPrefetch][0], v[u % kPrefetch][1]);
             const float2 b = make_float2(v[u % kPrefetch][2], v[u % kPrefetch][3]);
-            load_row<ADJACENT>(cur.p, lane, v[u % kPrefetch]);
-            cur.step();
+            load_row<ADJACENT>(in + rows[u], lane, v[u % kPrefetch]);
 #pragma unroll
             for (int j = 0; j < kTY; ++j) {
                 const float2 t = ring[(u - j + kTY) % kTY];
@@ -100,13 +109,28 @@ __device__ __forceinline__ void sweep(const float *__restrict__ in, int64_t pitc
                 acc[j][1] = ffma2(t, b, acc[j][1]);
             }
         }
-        tp += kTY;
+        taps += kTY;
+        rows += kTY;
+    }
+    // ---- last chunk ----
+    ring[0] = taps[0];
+#pragma unroll
+    for (int u = 0; u < kTY; ++u) {
+        const float2 a = make_float2(v[u % kPrefetch][0], v[u % kPrefetch][1]);
+        const float2 b = make_float2(v[u % kPrefetch][2], v[u % kPrefetch][3]);
+        if (u + kPrefetch < kTY) load_row<ADJACENT>(in + rows[u], lane, v[u % kPrefetch]);
+#pragma unroll
+        for (int j = u; j < kTY; ++j) {
+            const float2 t = ring[(u - j + kTY) % kTY];
+            acc[j][0] = ffma2(t, a, acc[j][0]);
+            acc[j][1] = ffma2(t, b, acc[j][1]);
+        }
     }
 }
 
 __device__ __forceinline__ void stage_taps(float2 *s_taps, const float2 *__restrict__ g_taps,
                                            const LevelDesc &lv) {
-    const int n = lv.n_chunks * kTY + kTY - 1;
+    const int n = 2 * lv.rpad + 1;
     for (int i = threadIdx.x; i < n; i += blockDim.x) s_taps[i] = g_taps[lv.tap_ofs + i];
 }
 
@@ -117,10 +141,11 @@ __global__ void __launch_bounds__(kConvThreads, 2)
 row_pass_kernel(const float *__restrict__ img, int64_t img_pitch, int H,
                 float *__restrict__ out_t, int64_t out_pitch, int64_t out_plane,
                 const LevelDesc *__restrict__ levels, const float2 *__restrict__ g_taps,
-                const int *__restrict__ level_order) {
+                const int *__restrict__ level_order, int max_table) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float *tile = reinterpret_cast<float *>(smem_raw);                       // [128][129]
     float2 *s_taps = reinterpret_cast<float2 *>(tile + kTileCols * kTilePitch);
+    int *s_rows = reinterpret_cast<int *>(s_taps + max_table);
 
     const int level = level_order[blockIdx.z];
     const LevelDesc lv = levels[level];
@@ -128,11 +153,11 @@ row_pass_kernel(const float *__restrict__ img, int64_t img_pitch, int H,
     const int col0 = blockIdx.x * kTileCols;            // x
     const int row0 = blockIdx.y * kTileRows;            // y
     stage_taps(s_taps, g_taps, lv);
+    stage_row_offsets(s_rows, row0 - lv.rpad, kTileRows + 2 * lv.rpad + kPrefetch, H, (int)img_pitch);
     __syncthreads();
 
     float2 acc[kTY][2];
-    sweep<false>(img + col0, img_pitch, H, row0 + warp * kTY - lv.radius, lv.n_chunks, s_taps,
-                 lane, acc);
+    sweep<false>(img + col0, s_rows + warp * kTY, lv.n_mid, s_taps, lane, acc);
 
     // tile[x_local][y_local]; lane stride 1 in x -> bank = lane + const: conflict free
 #pragma unroll
@@ -152,64 +177,105 @@ row_pass_kernel(const float *__restrict__ img, int64_t img_pitch, int H,
 }
 
 // ---- pass 2: correlate along x (rows of the transposed planes), fused DoG ------
-// grid.z = level group g; the CTA walks levels group_begin[g] .. group_begin[g+1]
-// (inclusive: the first level of the next group is recomputed here so that no
-// level is ever written to memory) and emits D_i for i in [begin, end).
+// grid.z = level group g; the CTA walks levels [group_begin[g], group_begin[g+1])
+// keeping the previous level's tile in shared memory and emits
+// D_i = f32(sigma_i) (L_i - L_{i+1}) for every pair inside the group, so no level of
+// the group reaches memory.  Only the two levels at a group boundary are parked in
+// `edge` planes (first level of group g -> edge[2g], last level -> edge[2g+1]);
+// edge_dog_kernel turns each boundary pair into the one missing slice.
 template <bool DOG>
 __global__ void __launch_bounds__(kConvThreads, 2)
 col_pass_kernel(const float *__restrict__ rows_t, int64_t pitch, int64_t plane, int n_rows,
-                float *__restrict__ out, const LevelDesc *__restrict__ levels,
-                const float2 *__restrict__ g_taps, const int *__restrict__ group_begin,
-                int n_levels) {
+                float *__restrict__ out, float *__restrict__ edge,
+                const LevelDesc *__restrict__ levels, const float2 *__restrict__ g_taps,
+                const int *__restrict__ group_begin, int n_groups, int max_table, int max_rpad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float2 *s_prev = reinterpret_cast<float2 *>(smem_raw);                    // [kTY*2][256]
     float2 *s_taps = s_prev + (DOG ? kTY * 2 * kConvThreads : 0);
+    int *s_rows = reinterpret_cast<int *>(s_taps + max_table);
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int col0 = blockIdx.x * kTileCols;
     const int row0 = blockIdx.y * kTileRows + warp * kTY;
-    const int lev_begin = group_begin[blockIdx.z];
-    int lev_end = group_begin[blockIdx.z + 1];               // exclusive for outputs
-    const int lev_last = DOG ? min(lev_end, n_levels - 1) : lev_end - 1;
+    const int g = blockIdx.z;
+    const int lev_begin = group_begin[g];
+    const int lev_end = group_begin[g + 1];
+    const int64_t tile_ofs = (int64_t)row0 * pitch + col0;
+    // folded offsets of every input row any level of this CTA can touch
+    stage_row_offsets(s_rows, (int)blockIdx.y * kTileRows - max_rpad,
+                      kTileRows + 2 * max_rpad + kPrefetch, n_rows, (int)pitch);
 
-    for (int level = lev_begin; level <= lev_last; ++level) {
+    for (int level = lev_begin; level < lev_end; ++level) {
         const LevelDesc lv = levels[level];
         __syncthreads();                                     // previous taps no longer in use
         stage_taps(s_taps, g_taps, lv);
         __syncthreads();
         float2 acc[kTY][2];
-        sweep<true>(rows_t + (int64_t)level * plane + col0, pitch, n_rows, row0 - lv.radius,
-                    lv.n_chunks, s_taps, lane, acc);
+        sweep<true>(rows_t + (int64_t)level * plane + col0,
+                    s_rows + warp * kTY + (max_rpad - lv.rpad), lv.n_mid, s_taps, lane, acc);
         if (!DOG) {
-            float *dst = out + (int64_t)level * plane + (int64_t)row0 * pitch + col0;
+            float *dst = out + (int64_t)level * plane + tile_ofs;
 #pragma unroll
             for (int j = 0; j < kTY; ++j)
                 reinterpret_cast<float4 *>(dst + (int64_t)j * pitch)[lane] =
                     make_float4(acc[j][0].x, acc[j][0].y, acc[j][1].x, acc[j][1].y);
-        } else {
-            if (level > lev_begin) {
-                const float s = levels[level - 1].sigma_f32;
-                float *dst = out + (int64_t)(level - 1) * plane + (int64_t)row0 * pitch + col0;
+            continue;
+        }
+        const bool park_first = (level == lev_begin) && g > 0;
+        const bool park_last = (level == lev_end - 1) && g < n_groups - 1;
+        if (park_first || park_last) {
 #pragma unroll
-                for (int j = 0; j < kTY; ++j) {
-                    const float2 p0 = s_prev[(2 * j + 0) * kConvThreads + threadIdx.x];
-                    const float2 p1 = s_prev[(2 * j + 1) * kConvThreads + threadIdx.x];
-                    float4 d;   // sigma * (narrow - wide): subtract, then scale (two roundings)
-                    d.x = __fmul_rn(__fsub_rn(p0.x, acc[j][0].x), s);
-                    d.y = __fmul_rn(__fsub_rn(p0.y, acc[j][0].y), s);
-                    d.z = __fmul_rn(__fsub_rn(p1.x, acc[j][1].x), s);
-                    d.w = __fmul_rn(__fsub_rn(p1.y, acc[j][1].y), s);
-                    reinterpret_cast<float4 *>(dst + (int64_t)j * pitch)[lane] = d;
-                }
-            }
-            if (level < lev_last) {
-#pragma unroll
-                for (int j = 0; j < kTY; ++j) {
-                    s_prev[(2 * j + 0) * kConvThreads + threadIdx.x] = acc[j][0];
-                    s_prev[(2 * j + 1) * kConvThreads + threadIdx.x] = acc[j][1];
-                }
+            for (int j = 0; j < kTY; ++j) {
+                const float4 q = make_float4(acc[j][0].x, acc[j][0].y, acc[j][1].x, acc[j][1].y);
+                if (park_first)
+                    reinterpret_cast<float4 *>(edge + (int64_t)(2 * g) * plane + tile_ofs +
+                                               (int64_t)j * pitch)[lane] = q;
+                if (park_last)
+                    reinterpret_cast<float4 *>(edge + (int64_t)(2 * g + 1) * plane + tile_ofs +
+                                               (int64_t)j * pitch)[lane] = q;
             }
         }
+        if (level > lev_begin) {
+            const float s = levels[level - 1].sigma_f32;
+            float *dst = out + (int64_t)(level - 1) * plane + tile_ofs;
+#pragma unroll
+            for (int j = 0; j < kTY; ++j) {
+                const float2 p0 = s_prev[(2 * j + 0) * kConvThreads + threadIdx.x];
+                const float2 p1 = s_prev[(2 * j + 1) * kConvThreads + threadIdx.x];
+                float4 d;   // sigma * (narrow - wide): subtract, then scale (two roundings)
+                d.x = __fmul_rn(__fsub_rn(p0.x, acc[j][0].x), s);
+                d.y = __fmul_rn(__fsub_rn(p0.y, acc[j][0].y), s);
+                d.z = __fmul_rn(__fsub_rn(p1.x, acc[j][1].x), s);
+                d.w = __fmul_rn(__fsub_rn(p1.y, acc[j][1].y), s);
+                reinterpret_cast<float4 *>(dst + (int64_t)j * pitch)[lane] = d;
+            }
+        }
+        if (level < lev_end - 1) {
+#pragma unroll
+            for (int j = 0; j < kTY; ++j) {
+                s_prev[(2 * j + 0) * kConvThreads + threadIdx.x] = acc[j][0];
+                s_prev[(2 * j + 1) * kConvThreads + threadIdx.x] = acc[j][1];
+            }
+        }
+    }
+}
+
+// the slice that straddles groups g and g+1: D = f32(sigma) * (last(g) - first(g+1))
+__global__ void __launch_bounds__(256)
+edge_dog_kernel(const float *__restrict__ edge, int64_t plane, float *__restrict__ out,
+                const LevelDesc *__restrict__ levels, const int *__restrict__ group_begin) {
+    const int g = blockIdx.y;
+    const int slice = group_begin[g + 1] - 1;
+    const float s = levels[slice].sigma_f32;
+    const float4 *a = reinterpret_cast<const float4 *>(edge + (int64_t)(2 * g + 1) * plane);
+    const float4 *b = reinterpret_cast<const float4 *>(edge + (int64_t)(2 * (g + 1)) * plane);
+    float4 *d = reinterpret_cast<float4 *>(out + (int64_t)slice * plane);
+    const int64_t n4 = plane / 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 x = __ldg(a + i), y = __ldg(b + i);
+        d[i] = make_float4(__fmul_rn(__fsub_rn(x.x, y.x), s), __fmul_rn(__fsub_rn(x.y, y.y), s),
+                           __fmul_rn(__fsub_rn(x.z, y.z), s), __fmul_rn(__fsub_rn(x.w, y.w), s));
     }
 }
 
@@ -244,44 +310,57 @@ __global__ void dog_from_levels_kernel(int n_slices, int64_t plane, const float 
     }
 }
 
-size_t row_pass_smem(int max_table) {
-    return (size_t)kTileCols * kTilePitch * sizeof(float) + (size_t)max_table * sizeof(float2);
+size_t row_table_bytes(int max_rpad) {
+    return (size_t)(kTileRows + 2 * max_rpad + kPrefetch) * sizeof(int);
 }
-size_t col_pass_smem(int max_table, bool dog) {
+size_t row_pass_smem(int max_table, int max_rpad) {
+    return (size_t)kTileCols * kTilePitch * sizeof(float) + (size_t)max_table * sizeof(float2) +
+           row_table_bytes(max_rpad);
+}
+size_t col_pass_smem(int max_table, int max_rpad, bool dog) {
     return (dog ? (size_t)kTY * 2 * kConvThreads * sizeof(float2) : 0) +
-           (size_t)max_table * sizeof(float2);
+           (size_t)max_table * sizeof(float2) + row_table_bytes(max_rpad);
 }
 
 }  // namespace
 
-cudaError_t configure_conv_kernels(int max_table) {
+cudaError_t configure_conv_kernels(int max_table, int max_rpad) {
     cudaError_t e;
     e = cudaFuncSetAttribute(row_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)row_pass_smem(max_table));
+                             (int)row_pass_smem(max_table, max_rpad));
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(col_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)col_pass_smem(max_table, true));
+                             (int)col_pass_smem(max_table, max_rpad, true));
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(col_pass_kernel<false>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)col_pass_smem(max_table, false));
+                                (int)col_pass_smem(max_table, max_rpad, false));
 }
 
 cudaError_t launch_row_pass(const ConvGeometry &g, const float *d_img, float *d_rows_t,
                             const LevelDesc *d_levels, const float2 *d_taps,
                             const int *d_level_order, cudaStream_t st) {
     dim3 grid(g.Wp / kTileCols, g.Hp / kTileRows, g.L);
-    row_pass_kernel<<<grid, kConvThreads, row_pass_smem(g.max_table), st>>>(
-        d_img, g.Wp, g.H, d_rows_t, g.Hp, (int64_t)g.Hp * g.Wp, d_levels, d_taps, d_level_order);
+    row_pass_kernel<<<grid, kConvThreads, row_pass_smem(g.max_table, g.max_rpad), st>>>(
+        d_img, g.Wp, g.H, d_rows_t, g.Hp, (int64_t)g.Hp * g.Wp, d_levels, d_taps, d_level_order,
+        g.max_table);
     return cudaGetLastError();
 }
 
 cudaError_t launch_col_dog_pass(const ConvGeometry &g, const float *d_rows_t, float *d_dog_t,
-                                const LevelDesc *d_levels, const float2 *d_taps,
+                                float *d_edge, const LevelDesc *d_levels, const float2 *d_taps,
                                 const int *d_group_begin, cudaStream_t st) {
     dim3 grid(g.Hp / kTileCols, g.Wp / kTileRows, g.G);
-    col_pass_kernel<true><<<grid, kConvThreads, col_pass_smem(g.max_table, true), st>>>(
-        d_rows_t, g.Hp, (int64_t)g.Hp * g.Wp, g.W, d_dog_t, d_levels, d_taps, d_group_begin, g.L);
+    const int64_t plane = (int64_t)g.Hp * g.Wp;
+    col_pass_kernel<true><<<grid, kConvThreads, col_pass_smem(g.max_table, g.max_rpad, true), st>>>(
+        d_rows_t, g.Hp, plane, g.W, d_dog_t, d_edge, d_levels, d_taps, d_group_begin, g.G,
+        g.max_table, g.max_rpad);
+    if (g.G > 1) {
+        int bx = (int)((plane / 4 + 255) / 256);
+        if (bx > 148 * 2) bx = 148 * 2;
+        edge_dog_kernel<<<dim3(bx, g.G - 1), 256, 0, st>>>(d_edge, plane, d_dog_t, d_levels,
+                                                          d_group_begin);
+    }
     return cudaGetLastError();
 }
 
@@ -289,8 +368,9 @@ cudaError_t launch_col_levels_pass(const ConvGeometry &g, const float *d_rows_t,
                                    const LevelDesc *d_levels, const float2 *d_taps,
                                    const int *d_unit_groups, cudaStream_t st) {
     dim3 grid(g.Hp / kTileCols, g.Wp / kTileRows, g.L);
-    col_pass_kernel<false><<<grid, kConvThreads, col_pass_smem(g.max_table, false), st>>>(
-        d_rows_t, g.Hp, (int64_t)g.Hp * g.Wp, g.W, d_lev_t, d_levels, d_taps, d_unit_groups, g.L);
+    col_pass_kernel<false><<<grid, kConvThreads, col_pass_smem(g.max_table, g.max_rpad, false), st>>>(
+        d_rows_t, g.Hp, (int64_t)g.Hp * g.Wp, g.W, d_lev_t, nullptr, d_levels, d_taps,
+        d_unit_groups, g.L, g.max_table, g.max_rpad);
     return cudaGetLastError();
 }
 
