@@ -64,10 +64,19 @@ __device__ __forceinline__ void load_row(const float *__restrict__ row, int lane
 //   last chunk   : sub-step u feeds outputs j >= u          (136)
 // so no FMA is spent on the triangular head and tail of the sliding window.  The tap
 // window lives in a 16-entry ring that is statically indexed by full unrolling.
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// `frontier`: this warp is the first of its CTA to touch new input rows (the warp with
+// the highest row range); it pulls rows kL2Ahead steps ahead into L2 so that its
+// register prefetch (kPrefetch rows) only has to cover L2 latency, not HBM latency.
+constexpr int kL2Ahead = 16;
+
 template <bool ADJACENT>
 __device__ __forceinline__ void sweep(const float *__restrict__ in, const int *__restrict__ rows,
                                       int n_mid, const float2 *__restrict__ taps, int lane,
-                                      float2 (&acc)[kTY][2]) {
+                                      float2 (&acc)[kTY][2], bool frontier = false) {
     float v[kPrefetch][4];
 #pragma unroll
     for (int p = 0; p < kPrefetch; ++p) load_row<ADJACENT>(in + rows[p], lane, v[p]);
@@ -102,6 +111,8 @@ __device__ __forceinline__ void sweep(const float *__restrict__ in, const int *_
             const float2 a = make_float2(v[u % kPrefetch][0], v[u % kPrefetch][1]);
             const float2 b = make_float2(v[u % kPrefetch][2], v[u % kPrefetch][3]);
             load_row<ADJACENT>(in + rows[u], lane, v[u % kPrefetch]);
+            if (ADJACENT && frontier && (u & 3) == 0)     // 4 rows x 4 lines per request group
+                prefetch_l2(in + rows[u + kL2Ahead + (lane >> 3)] + (lane & 7) * 16);
 #pragma unroll
             for (int j = 0; j < kTY; ++j) {
                 const float2 t = ring[(u - j + kTY) % kTY];
@@ -203,7 +214,7 @@ col_pass_kernel(const float *__restrict__ rows_t, int64_t pitch, int64_t plane, 
     const int64_t tile_ofs = (int64_t)row0 * pitch + col0;
     // folded offsets of every input row any level of this CTA can touch
     stage_row_offsets(s_rows, (int)blockIdx.y * kTileRows - max_rpad,
-                      kTileRows + 2 * max_rpad + kPrefetch, n_rows, (int)pitch);
+                      kTileRows + 2 * max_rpad + kPrefetch + kL2Ahead + 4, n_rows, (int)pitch);
 
     for (int level = lev_begin; level < lev_end; ++level) {
         const LevelDesc lv = levels[level];
@@ -212,7 +223,8 @@ col_pass_kernel(const float *__restrict__ rows_t, int64_t pitch, int64_t plane, 
         __syncthreads();
         float2 acc[kTY][2];
         sweep<true>(rows_t + (int64_t)level * plane + col0,
-                    s_rows + warp * kTY + (max_rpad - lv.rpad), lv.n_mid, s_taps, lane, acc);
+                    s_rows + warp * kTY + (max_rpad - lv.rpad), lv.n_mid, s_taps, lane, acc,
+                    warp == kWarps - 1);
         if (!DOG) {
             float *dst = out + (int64_t)level * plane + tile_ofs;
 #pragma unroll
@@ -311,7 +323,7 @@ __global__ void dog_from_levels_kernel(int n_slices, int64_t plane, const float 
 }
 
 size_t row_table_bytes(int max_rpad) {
-    return (size_t)(kTileRows + 2 * max_rpad + kPrefetch) * sizeof(int);
+    return (size_t)(kTileRows + 2 * max_rpad + kPrefetch + kL2Ahead + 4) * sizeof(int);
 }
 size_t row_pass_smem(int max_table, int max_rpad) {
     return (size_t)kTileCols * kTilePitch * sizeof(float) + (size_t)max_table * sizeof(float2) +

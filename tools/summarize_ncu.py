@@ -1,0 +1,86 @@
+#!/usr/bin/env python
+"""Turn ncu outputs brought back in gpurun_out/ into the tracked summaries under profiles/.
+
+  python tools/summarize_ncu.py launches <launches.csv> <out.md> [title]
+  python tools/summarize_ncu.py full <report.ncu-rep> <out.md> [title]
+"""
+import csv
+import subprocess
+import sys
+from collections import OrderedDict
+
+KEYS = [
+    "gpu__time_duration.sum", "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+    "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
+    "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "lts__t_bytes.sum", "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "smsp__cycles_active.avg", "sm__cycles_elapsed.max", "smsp__inst_executed.sum",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+]
+
+
+def launches(path, out, title):
+    rows = list(csv.reader(open(path)))
+    h = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    cols = rows[h]
+    ki, vi, gi, bi = (cols.index(c) for c in ("Kernel Name", "Metric Value", "Grid Size", "Block Size"))
+    agg = OrderedDict()
+    lines = []
+    for r in rows[h + 1:]:
+        if len(r) <= vi:
+            continue
+        name = r[ki].split("(")[0].replace("void ", "").replace("unnamed>::", "").replace("dogblob::<", "")
+        ns = float(r[vi].replace(",", ""))
+        lines.append((name, r[gi], r[bi], ns))
+        a = agg.setdefault(name, [0, 0.0])
+        a[0] += 1
+        a[1] += ns
+    total = sum(v[1] for v in agg.values())
+    with open(out, "w") as f:
+        f.write(f"# {title}\n\n`ncu --metrics gpu__time_duration.sum --clock-control none` (per-launch times are "
+                "cold-cache and serialised: compare shares, not absolutes)\n\n")
+        f.write("| kernel | launches | total us | mean us | share |\n|---|---:|---:|---:|---:|\n")
+        for name, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+            f.write(f"| `{name}` | {n} | {t / 1e3:.1f} | {t / n / 1e3:.2f} | {100 * t / total:.1f}% |\n")
+        f.write(f"| total | {sum(v[0] for v in agg.values())} | {total / 1e3:.1f} | | |\n\n")
+        f.write("First launches in order:\n\n| # | kernel | grid | block | us |\n|---:|---|---|---|---:|\n")
+        for i, (name, g, b, ns) in enumerate(lines[:40]):
+            f.write(f"| {i} | `{name}` | {g} | {b} | {ns / 1e3:.2f} |\n")
+
+
+def full(path, out, title):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    hdr, units = rows[0], rows[1]
+    with open(out, "w") as f:
+        f.write(f"# {title}\n\n`ncu --set full --clock-control none --import-source on`, read with "
+                "`ncu -i ... --page raw --csv`\n")
+        for r in rows[2:]:
+            name = r[hdr.index("Kernel Name")]
+            f.write(f"\n## `{name[:110]}`\n\n| metric | value | unit |\n|---|---:|---|\n")
+            for k in KEYS:
+                if k in hdr:
+                    i = hdr.index(k)
+                    f.write(f"| {k} | {r[i]} | {units[i]} |\n")
+            stalls = []
+            for i, h in enumerate(hdr):
+                if "smsp__average_warps_issue_stalled" in h and h.endswith("_per_issue_active.ratio"):
+                    try:
+                        stalls.append((float(r[i]), h.split("stalled_")[1].replace("_per_issue_active.ratio", "")))
+                    except ValueError:
+                        pass
+            stalls.sort(reverse=True)
+            f.write("\nwarp stall reasons per issued instruction: " +
+                    ", ".join(f"{n} {v:.2f}" for v, n in stalls[:8]) + "\n")
+
+
+if __name__ == "__main__":
+    mode, src, dst = sys.argv[1:4]
+    title = sys.argv[4] if len(sys.argv) > 4 else src
+    (launches if mode == "launches" else full)(src, dst, title)
