@@ -124,6 +124,8 @@ int dogblob_upload_image(const dogblob_plan *plan, const float *h_image,
                          void *d_image, void *stream);
 int dogblob_fetch_blobs(const void *d_result, int first, int count,
                         dogblob_blob *h_out, void *stream);
+/* header + the first n_blobs records, as dogblob_detect_host copies them */
+int dogblob_fetch_result(const void *d_result, int n_blobs, void *h_result, void *stream);
 
 /* ---- stage entry points (the reference's stage functions) -----------------
  * convolve_bank(..., backend="cuda") (convolve.py:189-218): levels in image
@@ -150,9 +152,28 @@ int dogblob_extrema(int n_slices, int height, int width, const float *d_slices,
 int dogblob_prune(int n, const dogblob_blob *d_blobs_in, double overlap,
                   int max_blobs, void *d_blobspace, void *d_result, void *stream);
 
+/* ---- pre-processing --------------------------------------
+ * images.preprocess (images.py:112-157): Gaussian smoothing with scipy's
+ * float64 line filter, then the nearest-rank contrast stretch to [0, 1].
+ *   d_src/d_dst   device float32 images with row pitches in floats (may alias
+ *                 the pitched image buffer dogblob_detect reads)
+ *   radius        int(truncate * smooth_sigma + 0.5), 0 disables smoothing
+ *   weights       HOST array of radius + 1 float64 taps, centre first
+ *   rank_lo/hi    0-based ranks of the two order statistics in the sorted image:
+ *                 min(max(ceil(q * n) - 1, 0), n - 1), q = sat/2 and 1 - sat/2
+ *   d_scratch     dogblob_preprocess_bytes(height, width)
+ * dogblob_preprocess_status copies the status word (bit 0: the input held a
+ * NaN/Inf pixel, images.py:40-41) into pinned host memory. */
+size_t dogblob_preprocess_bytes(int height, int width);
+int dogblob_preprocess(int height, int width, const float *d_src, int64_t src_pitch,
+                       int radius, const double *weights, int64_t rank_lo, int64_t rank_hi,
+                       void *d_scratch, float *d_dst, int64_t dst_pitch, void *stream);
+int dogblob_preprocess_status(const void *d_scratch, uint32_t *h_status, void *stream);
+
 /* ---- small helpers so that a non-CUDA host language can drive the ABI ----- */
 int dogblob_event_create(void **event);
 int dogblob_event_destroy(void *event);
+int dogblob_event_record(void *event, void *stream);
 int dogblob_event_elapsed_ms(void *start, void *stop, float *ms);
 int dogblob_stream_sync(void *stream);
 int dogblob_device_count(int *count);

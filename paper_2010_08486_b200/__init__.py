@@ -28,6 +28,8 @@ from .detector import (
     prune_overlaps,
 )
 
+from .images import preprocess
+
 __version__ = "0.1.0"
 
 __all__ = [
@@ -35,5 +37,5 @@ __all__ = [
     "BACKENDS", "ScaleStack", "DoGStack", "Blob", "BlobSet", "RadiusHistogram",
     "DetectionParams", "DetectResult", "Detector", "convolve_bank", "dog_stack", "fused_dog",
     "find_extrema", "prune_overlaps", "normalized_overlap", "disk_intersection_area",
-    "histogram", "detect", "__version__",
+    "histogram", "detect", "preprocess", "__version__",
 ]

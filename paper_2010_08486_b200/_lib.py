@@ -43,6 +43,7 @@ SIGNATURES = {
     "dogblob_detect_host": (_i, [_vp, _vp, _f, _i, _d, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp]),
     "dogblob_upload_image": (_i, [_vp, _vp, _vp, _vp]),
     "dogblob_fetch_blobs": (_i, [_vp, _i, _i, _vp, _vp]),
+    "dogblob_fetch_result": (_i, [_vp, _i, _vp, _vp]),
     "dogblob_scale_space": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "dogblob_dog": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "dogblob_dog_from_levels": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp]),
@@ -50,6 +51,10 @@ SIGNATURES = {
     "dogblob_result_bytes_for": (_sz, [_i]),
     "dogblob_extrema": (_i, [_i, _i, _i, _vp, _vp, _f, _i, _i, _vp, _vp, _vp]),
     "dogblob_prune": (_i, [_i, _vp, _d, _i, _vp, _vp, _vp]),
+    "dogblob_preprocess_bytes": (_sz, [_i, _i]),
+    "dogblob_preprocess": (_i, [_i, _i, _vp, _i64, _i, _vp, _i64, _i64, _vp, _vp, _i64, _vp]),
+    "dogblob_preprocess_status": (_i, [_vp, _vp, _vp]),
+    "dogblob_event_record": (_i, [_vp, _vp]),
     "dogblob_event_create": (_i, [C.POINTER(_vp)]),
     "dogblob_event_destroy": (_i, [_vp]),
     "dogblob_event_elapsed_ms": (_i, [_vp, _vp, C.POINTER(_f)]),

@@ -347,6 +347,14 @@ int dogblob_fetch_blobs(const void *d_result, int first, int count, dogblob_blob
     return DOGBLOB_OK;
 }
 
+int dogblob_fetch_result(const void *d_result, int n_blobs, void *h_result, void *stream) {
+    DB_REQUIRE(d_result && h_result && n_blobs >= 0, "bad argument");
+    DB_CUDA(cudaMemcpyAsync(h_result, d_result,
+                            DOGBLOB_RESULT_HEADER_BYTES + (size_t)n_blobs * sizeof(dogblob_blob),
+                            cudaMemcpyDeviceToHost, reinterpret_cast<cudaStream_t>(stream)));
+    return DOGBLOB_OK;
+}
+
 int dogblob_scale_space(const dogblob_plan *plan, const float *d_image, void *d_workspace,
                         float *d_levels, void *stream) {
     DB_REQUIRE(plan && d_image && d_workspace && d_levels, "NULL argument");

@@ -287,6 +287,10 @@ class _Slot:
         self.d_work = torch.zeros(plan.workspace_bytes, dtype=torch.uint8, device=dev)
         self.d_result = torch.zeros(plan.result_bytes, dtype=torch.uint8, device=dev)
         self.h_image = torch.empty((H, W), dtype=torch.float32).pin_memory()
+        self.d_raw = None          # raw frame + scratch, allocated on first preprocess=True use
+        self.d_pre = None
+        self.h_status = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self.pre_events = None
         n_host = min(HOST_RESULT_BLOBS, plan.max_blobs)
         self.h_result = torch.zeros(_lib.RESULT_HEADER_BYTES + n_host * _lib.BLOB_DTYPE.itemsize,
                                     dtype=torch.uint8).pin_memory()
@@ -302,11 +306,45 @@ class _Slot:
         """H2D + all kernels + D2H of header/records, asynchronously on self.stream."""
         lib = _lib.load()
         src = self._host_pointer(frame)
+        self.preprocessed = bool(params.preprocess)
+        if params.preprocess:
+            self._launch_with_preprocess(src, params, prune)
+            return
         _lib.check(lib.dogblob_detect_host(
             self.plan.handle, src, float(np.float32(params.threshold)), int(params.neighborhood),
             float(params.overlap), 1 if prune else 0, self.d_image.data_ptr(),
             self.d_work.data_ptr(), self.d_result.data_ptr(), self.h_result.data_ptr(),
             self.n_host, self.stream.cuda_stream, self.events))
+
+    def _launch_with_preprocess(self, src: int, params: DetectionParams, prune: bool) -> None:
+        """raw frame H2D -> smooth + stretch on the device (images.py:153-157) -> detect."""
+        from .images import smooth_taps, stretch_ranks
+        torch = _torch()
+        lib = _lib.load()
+        H, W = self.plan.shape
+        if self.d_raw is None:
+            dev = self.d_image.device
+            self.d_raw = torch.zeros((H, self.plan.pitch), dtype=torch.float32, device=dev)
+            self.d_pre = torch.zeros(int(lib.dogblob_preprocess_bytes(H, W)), dtype=torch.uint8,
+                                     device=dev)
+            self.pre_events = (C.c_void_p * 2)()
+            for k in range(2):
+                e = C.c_void_p()
+                _lib.check(lib.dogblob_event_create(C.byref(e)))
+                self.pre_events[k] = e
+        radius, taps = smooth_taps(params.smooth_sigma)
+        lo, hi = stretch_ranks(H * W, params.saturation)
+        st = self.stream.cuda_stream
+        _lib.check(lib.dogblob_event_record(self.pre_events[0], st))
+        _lib.check(lib.dogblob_upload_image(self.plan.handle, src, self.d_raw.data_ptr(), st))
+        _lib.check(lib.dogblob_preprocess(H, W, self.d_raw.data_ptr(), self.plan.pitch, radius,
+                                          _lib.ptr(taps), lo, hi, self.d_pre.data_ptr(),
+                                          self.d_image.data_ptr(), self.plan.pitch, st))
+        _lib.check(lib.dogblob_preprocess_status(self.d_pre.data_ptr(), self.h_status.data_ptr(), st))
+        _lib.check(lib.dogblob_event_record(self.pre_events[1], st))
+        self.launch_device(self.d_image, params, prune)
+        n = min(self.n_host, self.plan.max_blobs)
+        _lib.check(lib.dogblob_fetch_result(self.d_result.data_ptr(), n, self.h_result.data_ptr(), st))
 
     def launch_device(self, d_frame, params: DetectionParams, prune: bool, events=None) -> None:
         """Same, for a frame that is already resident: a float32 CUDA tensor [H][pitch]."""
@@ -335,6 +373,8 @@ class _Slot:
         """Wait for the frame and decode header + records (numpy structured array)."""
         lib = _lib.load()
         self.stream.synchronize()
+        if getattr(self, "preprocessed", False) and (int(self.h_status.item()) & 1):
+            raise ValueError("image contains NaN or Inf values")
         hdr = self.h_result_np[:_lib.RESULT_HEADER_BYTES].view(_lib.HEADER_DTYPE)[0].copy()
         n = int(hdr["n_blobs"])
         if int(hdr["flags"]) & _lib.FLAG_OVERFLOW:
@@ -351,10 +391,23 @@ class _Slot:
 
     def stage_times_ms(self) -> dict:
         t = event_intervals_ms(self.events)
-        return {"convolve_ms": t[0] + t[1], "extrema_ms": t[2], "prune_ms": t[3]}
+        pre = 0.0
+        if getattr(self, "preprocessed", False):
+            ms = C.c_float()
+            _lib.check(_lib.load().dogblob_event_elapsed_ms(self.pre_events[0], self.pre_events[1],
+                                                            C.byref(ms)))
+            pre = float(ms.value)
+        return {"preprocess_ms": pre, "convolve_ms": t[0] + t[1], "extrema_ms": t[2],
+                "prune_ms": t[3]}
 
     def close(self):
         free_events(self.events)
+        if self.pre_events is not None:
+            lib = _lib.load()
+            for k in range(2):
+                if self.pre_events[k]:
+                    lib.dogblob_event_destroy(self.pre_events[k])
+                    self.pre_events[k] = None
 
 
 class _Engine:
@@ -475,8 +528,6 @@ class Detector:
     def run(self, img, dtype=np.float32) -> DetectResult:
         """Full pipeline on one frame; per-stage timings are CUDA-event milliseconds."""
         p = self.params
-        if p.preprocess:
-            img = self._preprocess(img)
         img = self._prepare(img, dtype)
         shape = tuple(img.shape)
         if shape[0] * shape[1] * self.ladder.n_levels > (1 << 34):
@@ -487,7 +538,7 @@ class Detector:
             try:
                 slot.launch(img, p, p.prune)
                 hdr, recs = slot.collect()
-                timings = {"preprocess_ms": 0.0, **slot.stage_times_ms()}
+                timings = slot.stage_times_ms()
             finally:
                 eng.free.put(slot)
             if recs is not None:
@@ -498,8 +549,6 @@ class Detector:
         """Detect over a sequence of equally shaped host frames, pipelined over the
         slot pool: the H2D copy and kernels of frame f+1 overlap the D2H/decode of f."""
         p = self.params
-        if p.preprocess:
-            frames = [self._preprocess(f) for f in frames]
         frames = [self._prepare(f, np.float32) for f in frames]
         if not frames:
             return []
@@ -519,7 +568,7 @@ class Detector:
                 if recs is None:
                     retry.append(idx)
                     return
-                t = {"preprocess_ms": 0.0, **slot.stage_times_ms()} if timings else {}
+                t = slot.stage_times_ms() if timings else {}
                 results[idx] = self._finish(slot, hdr, recs, shape, t)
 
             for i, frame in enumerate(frames):
@@ -538,11 +587,6 @@ class Detector:
         for idx in retry:
             results[idx] = self.run(frames[idx])
         return results
-
-    def _preprocess(self, img):
-        raise ValueError(
-            "preprocess=True is not implemented on backend='cuda' yet (SURVEY 8f1); "
-            "pass DetectionParams(preprocess=False) with an already pre-processed frame")
 
 
 def detect(img, params: DetectionParams) -> tuple:

@@ -214,3 +214,70 @@ class TestFullSizeProperties:
         bank = P.build_kernel_bank(P.build_ladder(1.0, 10.0, 18))
         dog = P.fused_dog(img, bank).slices.astype(np.float64)
         assert np.abs(dog.sum(axis=(1, 2))).max() < 1e-4
+
+
+class TestPreprocess:
+    """images.preprocess on the GPU, bit-exact against the reference."""
+
+    def test_preprocess_bit_exact(self, golden):
+        g = golden("scene256.npz")
+        frame = synth.sensor_noise(synth.droplet_scene(256, 256, 12, (4.0, 12.0), seed=5), seed=6).image
+        got = P.preprocess(frame)
+        assert got.dtype == np.float32 and np.array_equal(got, g["pre_image"])
+
+    @pytest.mark.parametrize("shape,sigma,sat", [((97, 131), 1.0, 0.0035), ((64, 200), 2.3, 0.01),
+                                                  ((33, 47), 0.0, 0.0), ((1, 50), 1.0, 0.1),
+                                                  ((300, 1), 0.7, 0.3)])
+    def test_preprocess_against_oracle(self, shape, sigma, sat):
+        rng = np.random.default_rng(shape[0] + shape[1])
+        img = (rng.random(shape) ** 3).astype(np.float32)
+        assert np.array_equal(P.preprocess(img, sigma, sat), O.preprocess(img, sigma, sat))
+
+    def test_constant_image_maps_to_zero_and_errors(self):
+        assert np.array_equal(P.preprocess(np.full((40, 40), 0.3, np.float32)), np.zeros((40, 40), np.float32))
+        bad = np.ones((8, 8), np.float32)
+        bad[3, 3] = np.nan
+        with pytest.raises(ValueError, match="NaN"):
+            P.preprocess(bad)
+        with pytest.raises(ValueError):
+            P.preprocess(np.ones((8, 8), np.float32), saturation=0.7)
+        with pytest.raises(ValueError):
+            P.preprocess(np.ones((8, 8), np.float32), smooth_sigma=-1.0)
+
+    def test_detector_with_default_preprocess(self, golden):
+        g = golden("scene256.npz")
+        frame = synth.sensor_noise(synth.droplet_scene(256, 256, 12, (4.0, 12.0), seed=5), seed=6).image
+        det = P.Detector(P.DetectionParams(min_sigma=2.5, max_sigma=9.0, n_bin=10))   # preprocess=True
+        res = det.run(frame)
+        det.close()
+        strip = lambda ts: [(t[0], t[1], t[2], t[3], t[5]) for t in ts]
+        assert strip(records_tuples(res.blobs.records)) == strip(golden_blobs(g, "pre_kept_"))
+        assert res.timings_ms["preprocess_ms"] > 0.0
+
+    def test_reference_demo_golden_vector_on_gpu(self):
+        """The reference's own committed fixture pkg/demos/output/03_blobs.json (1000x1000
+        scene, sigma 2.5..15, n_bin 25, preprocess ON): every blob reproduced on the GPU."""
+        import json
+        from conftest import GOLDEN
+        doc = json.loads((GOLDEN / "ref_demo03_blobs.json").read_text())
+        frame = synth.sensor_noise(synth.droplet_scene(1000, 1000, 100, (4.0, 20.0), seed=123),
+                                   seed=124).image
+        kw = {k: v for k, v in doc["params"].items() if k != "backend"}
+        det = P.Detector(P.DetectionParams(**kw))
+        res = det.run(frame)
+        got = records_tuples(res.blobs.records)
+        want = [(b["x"], b["y"], b["sigma"], b["radius"], b["response"], b["at_scale_boundary"])
+                for b in doc["blobs"]]
+        pre = O.preprocess(frame)
+        rep = classify_candidates(pre, det.ladder.sigmas, det.bank.radii, kw["threshold"], got, want)
+        det.close()
+        print(f"\n[demo03] gpu={len(got)} ref={len(want)} common={len(rep['common'])} "
+              f"fragile={len(rep['explained'])} unexplained={len(rep['unexplained'])}")
+        assert not rep["unexplained"]
+        if not rep["explained"]:
+            strip = lambda ts: [(t[0], t[1], t[2], t[3], t[5]) for t in ts]
+            assert strip(got) == strip(want)
+            rows = (GOLDEN / "ref_demo03_histogram.csv").read_text().strip().splitlines()[1:]
+            for row, c, n, v in zip(rows, res.histogram.bin_centers, res.histogram.counts,
+                                    res.histogram.volume_weights):
+                assert row == f"{float(c)!r},{int(n)},{float(v)!r}"
