@@ -231,6 +231,7 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
     PLAN_CUDA(cudaMemcpy(plan->d_sigma_f32, sig32.data(), n_levels * sizeof(float),
                          cudaMemcpyHostToDevice));
     PLAN_CUDA(configure_conv_kernels(max_table, max_rpad));
+    PLAN_CUDA(configure_finalize_kernels());
 #undef PLAN_CUDA
 
     const size_t plane = (size_t)g.Hp * g.Wp * sizeof(float);
@@ -421,6 +422,7 @@ int dogblob_extrema(int n_slices, int height, int width, const float *d_slices,
     DB_CUDA(cudaMemcpyAsync(d_sig, slice_sigmas, n_slices * sizeof(double),
                             cudaMemcpyHostToDevice, st));
     DB_CUDA(cudaStreamSynchronize(st));
+    DB_CUDA(configure_finalize_kernels());
     DB_CUDA(launch_reset_counters(bs, st));
     DB_CUDA(launch_extrema(d_slices, n_slices, height, width, width, (int64_t)height * width,
                            false, d_sig, threshold, neighborhood / 2, bs, st));
@@ -436,6 +438,7 @@ int dogblob_prune(int n, const dogblob_blob *d_blobs_in, double overlap, int max
     if (int rc = check_threshold_args(3, overlap)) return rc;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     BlobSpace bs = carve_blobspace(d_blobspace, max_blobs);
+    DB_CUDA(configure_finalize_kernels());
     DB_CUDA(launch_reset_counters(bs, st));
     DB_CUDA(launch_load_blobs(bs, d_blobs_in, n, st));
     DB_CUDA(launch_prune_and_pack(bs, overlap, true, d_result, max_blobs, st));

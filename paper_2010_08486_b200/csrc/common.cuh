@@ -54,7 +54,9 @@ struct Counters {            // one per result, lives in the blob space
     int n_blobs;             // final
     int n_merges;
     unsigned flags;
-    int pad[10];
+    int small_done;          // 1 once finalize_small_kernel has sorted / pruned / packed the frame
+    unsigned plateau_ticket; // CTA ticket of plateau_kernel
+    int pad[8];
 };
 
 struct Voxel { int s, row, col; float val; };
@@ -119,6 +121,9 @@ cudaError_t launch_prune_and_pack(const BlobSpace &bs, double overlap, bool prun
                                   void *d_result, int result_cap, cudaStream_t st);
 cudaError_t launch_load_blobs(const BlobSpace &bs, const dogblob_blob *d_in, int n,
                               cudaStream_t st);
+cudaError_t launch_rank_sort(const BlobSpace &bs, cudaStream_t st);
+cudaError_t configure_finalize_kernels();   // per device, before the first launch_prune_and_pack
+constexpr int kSmallMax = 1024;   // frames with at most this many candidates finish in one CTA
 cudaError_t launch_reset_counters(const BlobSpace &bs, cudaStream_t st);
 
 }  // namespace dogblob

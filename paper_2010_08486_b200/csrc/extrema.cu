@@ -218,10 +218,15 @@ __device__ void uf_union(int *parent, int a, int b) {
     }
 }
 
-__global__ void __launch_bounds__(256) plateau_link_kernel(BlobSpace bs) {
+// One launch: every CTA links its share of member pairs; the last CTA to finish reduces the
+// components and emits one blob per root.  With no plateau member (the usual case on noisy
+// frames) the kernel returns at once.
+__global__ void __launch_bounds__(256)
+plateau_kernel(BlobSpace bs, int S, bool transposed, const double *__restrict__ slice_sigma) {
     const int n = min(bs.ctr->n_plateau, bs.cap);
     if (n == 0) return;
     __shared__ Voxel tile[256];
+    __shared__ bool last;
     for (int a0 = blockIdx.x * blockDim.x; a0 < n; a0 += gridDim.x * blockDim.x) {
         const int a = a0 + threadIdx.x;
         Voxel va = (a < n) ? bs.plateau[a] : Voxel{-9, -9, -9, 0.f};
@@ -240,11 +245,13 @@ __global__ void __launch_bounds__(256) plateau_link_kernel(BlobSpace bs) {
                 }
         }
     }
-}
-
-__global__ void __launch_bounds__(256) plateau_reduce_kernel(BlobSpace bs, bool transposed) {
-    const int n = min(bs.ctr->n_plateau, bs.cap);
-    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(&bs.ctr->plateau_ticket, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int a = threadIdx.x; a < n; a += blockDim.x) {
         const int root = uf_find(bs.parent, a);
         const Voxel v = bs.plateau[a];
         atomicAdd(&bs.pl_count[root], 1);
@@ -254,18 +261,15 @@ __global__ void __launch_bounds__(256) plateau_reduce_kernel(BlobSpace bs, bool 
         const unsigned long long y = transposed ? v.col : v.row, x = transposed ? v.row : v.col;
         atomicMin(&bs.pl_first[root], (y << 44) | (x << 24) | (unsigned long long)a);
     }
-}
-
-__global__ void __launch_bounds__(256)
-plateau_emit_kernel(BlobSpace bs, int S, bool transposed, const double *__restrict__ slice_sigma) {
-    const int n = min(bs.ctr->n_plateau, bs.cap);
-    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) {
-        if (bs.parent[a] != a) continue;
-        const Voxel v = bs.plateau[(int)(bs.pl_first[a] & 0xFFFFFFull)];
-        const double cnt = (double)bs.pl_count[a];
+    __threadfence();
+    __syncthreads();
+    for (int a = threadIdx.x; a < n; a += blockDim.x) {
+        if (((volatile int *)bs.parent)[a] != a) continue;
+        const Voxel v = bs.plateau[(int)(((volatile unsigned long long *)bs.pl_first)[a] & 0xFFFFFFull)];
+        const double cnt = (double)((volatile int *)bs.pl_count)[a];
         // ndimage.center_of_mass: float64 sum / count, then Python round() = half-even
-        const double cr = rint((double)bs.pl_sum_row[a] / cnt);
-        const double cc = rint((double)bs.pl_sum_col[a] / cnt);
+        const double cr = rint((double)((volatile unsigned long long *)bs.pl_sum_row)[a] / cnt);
+        const double cc = rint((double)((volatile unsigned long long *)bs.pl_sum_col)[a] / cnt);
         const int idx = atomicAdd(&bs.ctr->n_candidates, 1);
         if (idx < bs.cap)
             bs.unsorted[idx] = make_blob(v.s, transposed ? cr : cc, transposed ? cc : cr, v.val, S,
@@ -288,6 +292,7 @@ __device__ __forceinline__ bool key_before(const SortKey &a, int ia, const SortK
 }
 
 __global__ void __launch_bounds__(256) rank_sort_kernel(BlobSpace bs) {
+    if (bs.ctr->small_done) return;
     const int n = min(bs.ctr->n_candidates, bs.cap);
     __shared__ SortKey tile[256];
     for (int i0 = blockIdx.x * blockDim.x; i0 < n; i0 += gridDim.x * blockDim.x) {
@@ -340,8 +345,10 @@ cudaError_t launch_load_blobs(const BlobSpace &bs, const dogblob_blob *d_in, int
     if (blocks < 1) blocks = 1;
     if (blocks > 296) blocks = 296;
     load_blobs_kernel<<<blocks, 256, 0, st>>>(bs, d_in, n);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rank_sort(const BlobSpace &bs, cudaStream_t st) {
     rank_sort_kernel<<<296, 256, 0, st>>>(bs);
     return cudaGetLastError();
 }
@@ -359,10 +366,7 @@ cudaError_t launch_extrema(const float *d_slices, int S, int rows, int cols, int
         nms_kernel<1><<<grid, 256, 0, st>>>(vol, threshold, half, transposed, d_slice_sigma, bs);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    plateau_link_kernel<<<296, 256, 0, st>>>(bs);
-    plateau_reduce_kernel<<<148, 256, 0, st>>>(bs, transposed);
-    plateau_emit_kernel<<<148, 256, 0, st>>>(bs, S, transposed, d_slice_sigma);
-    rank_sort_kernel<<<296, 256, 0, st>>>(bs);
+    plateau_kernel<<<148, 256, 0, st>>>(bs, S, transposed, d_slice_sigma);
     return cudaGetLastError();
 }
 

@@ -75,22 +75,27 @@ __device__ __forceinline__ Grid load_grid(const BlobSpace &bs) {
 }
 
 template <typename T, typename Op>
-__device__ T block_reduce(T v, Op op, T *scratch /* >= 32 */) {
+__device__ T block_reduce(T v, Op op, T *scratch /* >= 33 */) {
     for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
     __syncthreads();
     if (lane == 0) scratch[w] = v;
     __syncthreads();
-    const int nw = (blockDim.x + 31) >> 5;
-    T r = scratch[0];
-    for (int k = 1; k < nw; ++k) r = op(r, scratch[k]);
-    return r;
+    if (w == 0) {
+        T r = scratch[lane < nw ? lane : 0];
+        for (int o = 16; o > 0; o >>= 1) r = op(r, __shfl_xor_sync(0xffffffffu, r, o));
+        if (lane == 0) scratch[32] = r;
+    }
+    __syncthreads();
+    return scratch[32];
 }
 
 // ---- build the grid (single CTA): extents, cell size, counting sort -------------------
 __global__ void __launch_bounds__(kLoopThreads) prune_build_kernel(BlobSpace bs) {
-    __shared__ double sd[32];
-    __shared__ int si[32];
+    if (bs.ctr->small_done) return;
+    __shared__ double sd[33];
+    __shared__ int si[33];
     const int n = min(bs.ctr->n_candidates, bs.cap);
     const int tid = threadIdx.x;
     double xmin = DBL_MAX, xmax = -DBL_MAX, ymin = DBL_MAX, ymax = -DBL_MAX, rmax = 0.0;
@@ -186,6 +191,7 @@ __device__ int scan_first_partner(const BlobSpace &bs, const Grid &g, int i, dou
 
 // ---- first[i] for every blob: one warp per blob, whole GPU ---------------------------
 __global__ void __launch_bounds__(256) prune_first_kernel(BlobSpace bs, double thr) {
+    if (bs.ctr->small_done) return;
     const int n = min(bs.ctr->n_candidates, bs.cap);
     if (n < 2) return;
     const Grid g = load_grid(bs);
@@ -202,7 +208,8 @@ __global__ void __launch_bounds__(256) prune_first_kernel(BlobSpace bs, double t
 __global__ void __launch_bounds__(kLoopThreads)
 prune_loop_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_header *hdr,
                   dogblob_blob *out, int out_cap) {
-    __shared__ int s_red[32];
+    if (bs.ctr->small_done) return;
+    __shared__ int s_red[33];
     __shared__ int s_pos, s_list_n, s_carry;
     __shared__ int s_list[kLoopThreads];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -350,13 +357,191 @@ prune_loop_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_header 
     }
 }
 
+// ---- frames with <= kSmallMax candidates: order, prune and pack in ONE CTA ---------------
+// Same semantics as rank_sort + prune_build/first/loop, without the grid: every pair
+// is tested directly (n^2 / 2 cheap rejections), all state lives in shared memory.
+struct SmallBlob { double x, y, r, resp, sigma; int slice; unsigned flags; };
+
+__global__ void __launch_bounds__(kSmallMax)
+finalize_small_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_header *hdr,
+                      dogblob_blob *out, int out_cap) {
+    extern __shared__ __align__(16) unsigned char small_raw[];
+    SmallBlob *sb = reinterpret_cast<SmallBlob *>(small_raw);                 // sorted blobs
+    SmallBlob *raw = sb + kSmallMax;                                          // emission order
+    int *first = reinterpret_cast<int *>(raw + kSmallMax);
+    int *alive = first + kSmallMax;
+    __shared__ int s_red[33];
+    __shared__ int s_pos, s_carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n_raw = bs.ctr->n_candidates;
+    if (n_raw > kSmallMax || n_raw > bs.cap) {
+        if (tid == 0) bs.ctr->small_done = 0;
+        return;
+    }
+    const int n = n_raw;
+    auto imin = [](int a, int b) { return min(a, b); };
+
+    // ---- order: rank on (-response, y, x, sigma), ties by input index ----
+    if (tid < n) {
+        const dogblob_blob b = bs.unsorted[tid];
+        raw[tid] = SmallBlob{b.x, b.y, b.radius, b.response, b.sigma, b.slice, b.flags};
+    }
+    __syncthreads();
+    const int n_warps = blockDim.x >> 5;
+    for (int i = warp; i < n; i += n_warps) {            // one warp per blob, lanes over j
+        const SmallBlob me = raw[i];
+        int cnt = 0;
+        for (int j = lane; j < n; j += 32) {
+            const SmallBlob o = raw[j];
+            bool before;
+            if (o.resp != me.resp) before = o.resp > me.resp;
+            else if (o.y != me.y) before = o.y < me.y;
+            else if (o.x != me.x) before = o.x < me.x;
+            else if (o.sigma != me.sigma) before = o.sigma < me.sigma;
+            else before = j < i;
+            cnt += before ? 1 : 0;
+        }
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (lane == 0) {
+            sb[cnt] = me;
+            alive[cnt] = 1;
+        }
+    }
+    __syncthreads();
+    int merges = 0;
+    if (do_prune && n >= 2) {
+        // ---- first[i]: smallest j > i with overlap > thr ----
+        for (int i = warp; i < n; i += n_warps) {        // one warp per row, lanes over j
+            const SmallBlob a = sb[i];
+            int best = INT_MAX;
+            for (int j0 = i + 1; j0 < n && best == INT_MAX; j0 += 32) {
+                const int j = j0 + lane;
+                bool hit = false;
+                if (j < n) {
+                    const SmallBlob b = sb[j];
+                    const double dx = a.x - b.x, dy = a.y - b.y, rr = a.r + b.r;
+                    if (dx * dx + dy * dy < rr * rr * 1.0000001 + 1e-9)   // else disjoint for sure
+                        hit = overlap_ij(a.x, a.y, a.r, b.x, b.y, b.r) > thr;
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, hit);
+                if (m) best = j0 + __ffs(m) - 1;
+            }
+            if (lane == 0) first[i] = (best == INT_MAX) ? -1 : best;
+        }
+        if (tid == 0) s_pos = 0;
+        __syncthreads();
+        while (true) {
+            int mine = (tid >= s_pos && tid < n && alive[tid] && first[tid] >= 0) ? tid : INT_MAX;
+            const int istar = block_reduce(mine, imin, s_red);
+            if (istar == INT_MAX) break;
+            const int j = first[istar];
+            __syncthreads();
+            if (tid == 0) {
+                SmallBlob a = sb[istar];
+                const SmallBlob w = sb[j];
+                const double nr = 0.5 * (a.r + w.r);
+                a.r = nr;
+                a.sigma = nr / kSqrt2;
+                a.flags |= (w.flags & DOGBLOB_BLOB_SCALE_EDGE) | DOGBLOB_BLOB_MERGED;
+                a.slice = -1;
+                sb[istar] = a;
+                alive[j] = 0;
+                s_pos = istar;
+            }
+            ++merges;
+            __syncthreads();
+            const SmallBlob bi = sb[istar];
+            // (a) new first partner of istar: block-wide min over j > istar
+            int cand = INT_MAX;
+            if (tid > istar && tid < n && alive[tid]) {
+                const SmallBlob b = sb[tid];
+                if (overlap_ij(bi.x, bi.y, bi.r, b.x, b.y, b.r) > thr) cand = tid;
+            }
+            // (b) rows k < istar can only gain istar; (c) rows that pointed at j rescan
+            if (tid < istar && alive[tid]) {
+                const SmallBlob b = sb[tid];
+                if (overlap_ij(b.x, b.y, b.r, bi.x, bi.y, bi.r) > thr) {
+                    first[tid] = istar;
+                    atomicMin(&s_pos, tid);
+                }
+            } else if (tid > istar && tid < n && alive[tid] && first[tid] == j) {
+                const SmallBlob a = sb[tid];
+                int best = -1;
+                for (int q = tid + 1; q < n; ++q) {
+                    if (!alive[q]) continue;
+                    const SmallBlob b = sb[q];
+                    if (overlap_ij(a.x, a.y, a.r, b.x, b.y, b.r) > thr) { best = q; break; }
+                }
+                first[tid] = best;
+            }
+            cand = block_reduce(cand, imin, s_red);
+            if (tid == 0) first[istar] = (cand == INT_MAX) ? -1 : cand;
+            __syncthreads();
+        }
+    }
+    // ---- pack survivors in order ----
+    __syncthreads();
+    const int keep = (tid < n) && (!do_prune || n < 2 || alive[tid]);
+    int v = keep;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    if (lane == 31) s_red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        int t = s_red[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += u;
+        }
+        s_red[lane] = t;
+    }
+    __syncthreads();
+    const int pos = (warp > 0 ? s_red[warp - 1] : 0) + v - keep;
+    if (keep && pos < out_cap) {
+        const SmallBlob b = sb[tid];
+        dogblob_blob o;
+        o.x = b.x; o.y = b.y; o.sigma = b.sigma; o.radius = b.r; o.response = b.resp;
+        o.slice = b.slice; o.flags = b.flags;
+        out[pos] = o;
+    }
+    if (tid == blockDim.x - 1) s_carry = pos + keep;
+    __syncthreads();
+    if (tid == 0) {
+        const Counters c = *bs.ctr;
+        hdr->n_blobs = min(s_carry, out_cap);
+        hdr->n_candidates = c.n_candidates;
+        hdr->n_flagged = c.n_flagged;
+        hdr->n_plateau = c.n_plateau;
+        hdr->n_merges = merges;
+        unsigned f = c.flags;
+        if (c.n_plateau > bs.cap || s_carry > out_cap) f |= DOGBLOB_FLAG_OVERFLOW;
+        hdr->flags = f;
+        hdr->capacity = out_cap;
+        bs.ctr->small_done = 1;
+    }
+}
+
+constexpr size_t kSmallSmem = (size_t)kSmallMax * (2 * sizeof(SmallBlob) + 2 * sizeof(int));
+
 }  // namespace
+
+cudaError_t configure_finalize_kernels() {
+    return cudaFuncSetAttribute(finalize_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kSmallSmem);
+}
 
 cudaError_t launch_prune_and_pack(const BlobSpace &bs, double overlap, bool prune,
                                   void *d_result, int result_cap, cudaStream_t st) {
     auto *hdr = reinterpret_cast<dogblob_result_header *>(d_result);
     auto *out = reinterpret_cast<dogblob_blob *>(reinterpret_cast<char *>(d_result) +
                                                  DOGBLOB_RESULT_HEADER_BYTES);
+    // <= kSmallMax candidates: everything in one CTA; the general kernels then return at once
+    finalize_small_kernel<<<1, kSmallMax, kSmallSmem, st>>>(bs, overlap, prune ? 1 : 0, hdr, out,
+                                                            result_cap);
+    cudaError_t e = launch_rank_sort(bs, st);
+    if (e != cudaSuccess) return e;
     if (prune) {
         prune_build_kernel<<<1, kLoopThreads, 0, st>>>(bs);
         prune_first_kernel<<<148 * 2, 256, 0, st>>>(bs, overlap);

@@ -145,17 +145,25 @@ __device__ __forceinline__ void stage_taps(float2 *s_taps, const float2 *__restr
     for (int i = threadIdx.x; i < n; i += blockDim.x) s_taps[i] = g_taps[lv.tap_ofs + i];
 }
 
-constexpr int kTilePitch = kTileRows + 1;  // 129: conflict-free transposed writes
-
 // ---- pass 1: correlate along y, store transposed ------------------------------
+// The 128 x 128 output tile is transposed through shared memory with 16-byte accesses on
+// both sides: element (x, y) lives at x * 128 + (((y >> 2) ^ (x >> 2)) & 31) * 4 + (y & 3).
+// A thread owns 4 adjacent columns x = 4 lane + c and 16 consecutive y, so it writes
+// STS.128 whose 16-byte bank group is (const ^ lane) -> conflict free per quarter warp;
+// rows are read back as permuted 16-byte groups (conflict free) and stored with
+// fully coalesced STG.128.
+__device__ __forceinline__ int tile_index(int x, int y4) {        // y4 = y / 4
+    return x * kTileRows + (((y4 ^ (x >> 2)) & 31) << 2);
+}
+
 __global__ void __launch_bounds__(kConvThreads, 2)
 row_pass_kernel(const float *__restrict__ img, int64_t img_pitch, int H,
                 float *__restrict__ out_t, int64_t out_pitch, int64_t out_plane,
                 const LevelDesc *__restrict__ levels, const float2 *__restrict__ g_taps,
                 const int *__restrict__ level_order, int max_table) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float *tile = reinterpret_cast<float *>(smem_raw);                       // [128][129]
-    float2 *s_taps = reinterpret_cast<float2 *>(tile + kTileCols * kTilePitch);
+    float *tile = reinterpret_cast<float *>(smem_raw);                       // [128 x][128 y]
+    float2 *s_taps = reinterpret_cast<float2 *>(tile + kTileCols * kTileRows);
     int *s_rows = reinterpret_cast<int *>(s_taps + max_table);
 
     const int level = level_order[blockIdx.z];
@@ -168,22 +176,28 @@ row_pass_kernel(const float *__restrict__ img, int64_t img_pitch, int H,
     __syncthreads();
 
     float2 acc[kTY][2];
-    sweep<false>(img + col0, s_rows + warp * kTY, lv.n_mid, s_taps, lane, acc);
+    sweep<true>(img + col0, s_rows + warp * kTY, lv.n_mid, s_taps, lane, acc);
 
-    // tile[x_local][y_local]; lane stride 1 in x -> bank = lane + const: conflict free
 #pragma unroll
-    for (int j = 0; j < kTY; ++j) {
-        const int yl = warp * kTY + j;
-        tile[(lane + 0) * kTilePitch + yl] = acc[j][0].x;
-        tile[(lane + 32) * kTilePitch + yl] = acc[j][0].y;
-        tile[(lane + 64) * kTilePitch + yl] = acc[j][1].x;
-        tile[(lane + 96) * kTilePitch + yl] = acc[j][1].y;
+    for (int q = 0; q < kTY / 4; ++q) {                 // four consecutive y per store
+        const int y4 = warp * (kTY / 4) + q;
+        const int j = 4 * q;
+        *reinterpret_cast<float4 *>(&tile[tile_index(4 * lane + 0, y4)]) =
+            make_float4(acc[j][0].x, acc[j + 1][0].x, acc[j + 2][0].x, acc[j + 3][0].x);
+        *reinterpret_cast<float4 *>(&tile[tile_index(4 * lane + 1, y4)]) =
+            make_float4(acc[j][0].y, acc[j + 1][0].y, acc[j + 2][0].y, acc[j + 3][0].y);
+        *reinterpret_cast<float4 *>(&tile[tile_index(4 * lane + 2, y4)]) =
+            make_float4(acc[j][1].x, acc[j + 1][1].x, acc[j + 2][1].x, acc[j + 3][1].x);
+        *reinterpret_cast<float4 *>(&tile[tile_index(4 * lane + 3, y4)]) =
+            make_float4(acc[j][1].y, acc[j + 1][1].y, acc[j + 2][1].y, acc[j + 3][1].y);
     }
     __syncthreads();
     float *dst = out_t + (int64_t)level * out_plane + (int64_t)col0 * out_pitch + row0;
-    for (int i = threadIdx.x; i < kTileCols * kTileRows; i += kConvThreads) {
-        const int xl = i >> 7, yl = i & 127;
-        dst[(int64_t)xl * out_pitch + yl] = tile[xl * kTilePitch + yl];
+#pragma unroll 4
+    for (int i = threadIdx.x; i < kTileCols * (kTileRows / 4); i += kConvThreads) {
+        const int xl = i >> 5, y4 = i & 31;             // one warp = one x row, 512 B
+        const float4 q = *reinterpret_cast<const float4 *>(&tile[tile_index(xl, y4)]);
+        reinterpret_cast<float4 *>(dst + (int64_t)xl * out_pitch)[y4] = q;
     }
 }
 
@@ -216,7 +230,14 @@ col_pass_kernel(const float *__restrict__ rows_t, int64_t pitch, int64_t plane, 
     stage_row_offsets(s_rows, (int)blockIdx.y * kTileRows - max_rpad,
                       kTileRows + 2 * max_rpad + kPrefetch + kL2Ahead + 4, n_rows, (int)pitch);
 
-    for (int level = lev_begin; level < lev_end; ++level) {
+    // Co-resident CTAs (neighbouring tiles of one group) would otherwise march through the
+    // same level sequence in lock step and hit their per-level barriers together; every
+    // other tile walks its levels downwards so that their pipeline drains interleave.
+    const bool down = DOG && ((blockIdx.x + blockIdx.y) & 1);
+    const int n_lev = lev_end - lev_begin;
+
+    for (int k = 0; k < n_lev; ++k) {
+        const int level = down ? lev_end - 1 - k : lev_begin + k;
         const LevelDesc lv = levels[level];
         __syncthreads();                                     // previous taps no longer in use
         stage_taps(s_taps, g_taps, lv);
@@ -247,22 +268,25 @@ col_pass_kernel(const float *__restrict__ rows_t, int64_t pitch, int64_t plane, 
                                                (int64_t)j * pitch)[lane] = q;
             }
         }
-        if (level > lev_begin) {
-            const float s = levels[level - 1].sigma_f32;
-            float *dst = out + (int64_t)(level - 1) * plane + tile_ofs;
+        if (k > 0) {
+            // the pair (narrow, wide) = (prev, cur) going up, (cur, prev) going down
+            const int slice = down ? level : level - 1;
+            const float s = levels[slice].sigma_f32;
+            const float sgn = down ? -1.f : 1.f;             // exact: x * -1 only flips the sign
+            float *dst = out + (int64_t)slice * plane + tile_ofs;
 #pragma unroll
             for (int j = 0; j < kTY; ++j) {
                 const float2 p0 = s_prev[(2 * j + 0) * kConvThreads + threadIdx.x];
                 const float2 p1 = s_prev[(2 * j + 1) * kConvThreads + threadIdx.x];
                 float4 d;   // sigma * (narrow - wide): subtract, then scale (two roundings)
-                d.x = __fmul_rn(__fsub_rn(p0.x, acc[j][0].x), s);
-                d.y = __fmul_rn(__fsub_rn(p0.y, acc[j][0].y), s);
-                d.z = __fmul_rn(__fsub_rn(p1.x, acc[j][1].x), s);
-                d.w = __fmul_rn(__fsub_rn(p1.y, acc[j][1].y), s);
+                d.x = __fmul_rn(__fsub_rn(p0.x, acc[j][0].x) * sgn, s);
+                d.y = __fmul_rn(__fsub_rn(p0.y, acc[j][0].y) * sgn, s);
+                d.z = __fmul_rn(__fsub_rn(p1.x, acc[j][1].x) * sgn, s);
+                d.w = __fmul_rn(__fsub_rn(p1.y, acc[j][1].y) * sgn, s);
                 reinterpret_cast<float4 *>(dst + (int64_t)j * pitch)[lane] = d;
             }
         }
-        if (level < lev_end - 1) {
+        if (k < n_lev - 1) {
 #pragma unroll
             for (int j = 0; j < kTY; ++j) {
                 s_prev[(2 * j + 0) * kConvThreads + threadIdx.x] = acc[j][0];
@@ -326,7 +350,7 @@ size_t row_table_bytes(int max_rpad) {
     return (size_t)(kTileRows + 2 * max_rpad + kPrefetch + kL2Ahead + 4) * sizeof(int);
 }
 size_t row_pass_smem(int max_table, int max_rpad) {
-    return (size_t)kTileCols * kTilePitch * sizeof(float) + (size_t)max_table * sizeof(float2) +
+    return (size_t)kTileCols * kTileRows * sizeof(float) + (size_t)max_table * sizeof(float2) +
            row_table_bytes(max_rpad);
 }
 size_t col_pass_smem(int max_table, int max_rpad, bool dog) {
