@@ -202,10 +202,15 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if not torch.cuda.is_available():
         raise RuntimeError("bench.py --impl ours needs a CUDA device (no CPU fallback)")
+    local = local % torch.cuda.device_count()      # (a 1-GPU box can still exercise N > 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    ctl = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # control plane only (barrier + max of one scalar): the data path has no collective,
+        # so the NCCL communicator is registered but never needed on the hot path
+        dist.init_process_group("cpu:gloo,cuda:nccl")
+        ctl = dist.new_group(backend="gloo")
 
     kw = params_kw()
     params = P.DetectionParams(preprocess=False, **kw)
@@ -237,7 +242,7 @@ def run_ours(args):
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize(dev)
         if world > 1:
-            dist.barrier()
+            dist.barrier(group=ctl)
             torch.cuda.synchronize(dev)
         start.record(main)
         for s in slots:
@@ -252,8 +257,8 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         ms = start.elapsed_time(end)
         if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t = torch.tensor([ms], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=ctl)
             ms = float(t.item())
         return ms
 
@@ -283,7 +288,7 @@ def run_ours(args):
         det.run_batch(pinned)
     torch.cuda.synchronize(dev)
     if world > 1:
-        dist.barrier()
+        dist.barrier(group=ctl)
     t0 = time.perf_counter()
     n_blobs = 0
     for _ in range(args.steps):
@@ -292,9 +297,10 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t0
     if world > 1:
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        t = torch.tensor([e2e_s, float(n_blobs)], dtype=torch.float64)
+        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX, group=ctl)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM, group=ctl)
+        e2e_s, n_blobs = float(t[0].item()), int(t[1].item())
     e2e_value = frames_per_step * args.steps / e2e_s
     h2d = frames_per_step * H * W * 4
     d2h = frames_per_step * (64 + slots[0].n_host * 48)
@@ -373,7 +379,7 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     det.close()
     if world > 1:
-        dist.barrier()
+        dist.barrier(group=ctl)
         dist.destroy_process_group()
 
 

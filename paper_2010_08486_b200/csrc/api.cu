@@ -22,7 +22,8 @@ size_t blobspace_bytes(int cap) {
     b += align_up(c * sizeof(int), 256) * 2;                  // parent, pl_count
     b += align_up(c * sizeof(unsigned long long), 256) * 3;   // pl_sum_row/col, pl_first
     b += align_up(c * sizeof(dogblob_blob), 256) * 2;         // unsorted, sorted
-    b += align_up(c * sizeof(int), 256) * 4;                  // first, alive, cell_of, cell_items
+    b += align_up(c * sizeof(int), 256) * 6;                  // first, alive, cell_of, cell_items, comp, cmin
+    b += align_up(c * sizeof(unsigned long long), 256);       // bound
     b += align_up((size_t)(kMaxCells + 1) * sizeof(int), 256);
     b += align_up((size_t)kMaxCells * sizeof(int), 256);
     b += align_up(8 * sizeof(double), 256);
@@ -45,6 +46,9 @@ BlobSpace carve_blobspace(void *base, int cap) {
     bs.sorted = reinterpret_cast<dogblob_blob *>(take(c * sizeof(dogblob_blob)));
     bs.first = reinterpret_cast<int *>(take(c * sizeof(int)));
     bs.alive = reinterpret_cast<int *>(take(c * sizeof(int)));
+    bs.comp = reinterpret_cast<int *>(take(c * sizeof(int)));
+    bs.cmin = reinterpret_cast<int *>(take(c * sizeof(int)));
+    bs.bound = reinterpret_cast<unsigned long long *>(take(c * sizeof(unsigned long long)));
     bs.cell_of = reinterpret_cast<int *>(take(c * sizeof(int)));
     bs.cell_items = reinterpret_cast<int *>(take(c * sizeof(int)));
     bs.cell_start = reinterpret_cast<int *>(take((size_t)(kMaxCells + 1) * sizeof(int)));

@@ -73,6 +73,9 @@ struct BlobSpace {
     dogblob_blob *sorted;        // candidates in (-response, y, x, sigma) order
     int *first;                  // prune: smallest offending partner j > i, or -1
     int *alive;
+    int *comp;                   // prune: interaction component (root index) of every blob
+    int *cmin;                   // prune: per-root smallest row with an offending partner
+    unsigned long long *bound;   // prune: per-root largest radius (bits of a positive double)
     int *cell_of;                // prune grid
     int *cell_start;             // kMaxCells + 1
     int *cell_fill;              // kMaxCells

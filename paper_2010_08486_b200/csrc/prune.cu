@@ -181,7 +181,7 @@ __device__ int scan_first_partner(const BlobSpace &bs, const Grid &g, int i, dou
             const int e = bs.cell_start[c + 1];
             for (int p = bs.cell_start[c] + t; p < e; p += nt) {
                 const int j = bs.cell_items[p];
-                if (j <= i || j >= best || !bs.alive[j]) continue;
+                if (j <= i || j >= best || !(bs.alive[j] & 1)) continue;
                 const dogblob_blob bj = bs.sorted[j];
                 if (overlap_ij(bi.x, bi.y, bi.radius, bj.x, bj.y, bj.radius) > thr) best = j;
             }
@@ -204,111 +204,214 @@ __global__ void __launch_bounds__(256) prune_first_kernel(BlobSpace bs, double t
     }
 }
 
-// ---- the sequential merge loop + final packing (single persistent CTA) ------------------
+// ---- merge loop + final packing (single persistent CTA) -----------------------------------
+// The reference's loop is sequential, but merges only interact through blobs that can
+// overlap.  ub(a) bounds every radius blob a can ever take: a's radius only changes when a
+// (the lower index) absorbs some b > a and becomes the mean, so
+//     ub(a) = max(r_a, max{ ub(b) : b > a, dist(a, b) < ub(a) + ub(b) }),
+// taken as the least fixed point from below.  By induction no merge ever joins blobs that
+// are not linked by "dist < ub(a) + ub(b)", so the connected parts of that graph evolve
+// independently and the global row-major-first order restricted to a part is that part's
+// own sequential order: each round merges the smallest offending row of EVERY part at once
+// (one warp per row).  Rounds = longest merge chain of a part, not the number of merges.
+__device__ __forceinline__ int comp_find(int *comp, int x) {
+    int p = ((volatile int *)comp)[x];
+    while (p != x) { x = p; p = ((volatile int *)comp)[x]; }
+    return x;
+}
+__device__ void comp_union(int *comp, int a, int b) {
+    while (true) {
+        a = comp_find(comp, a);
+        b = comp_find(comp, b);
+        if (a == b) return;
+        if (a > b) { int t = a; a = b; b = t; }
+        if (atomicCAS(&comp[b], b, a) == b) return;
+    }
+}
+
+__device__ __forceinline__ double ub_of(const BlobSpace &bs, int i) {
+    return __longlong_as_double((long long)((volatile unsigned long long *)bs.bound)[i]);
+}
+
+// rows with an offending partner live in a compact list (bit 1 of alive[] = "listed")
+__device__ __forceinline__ void list_row(const BlobSpace &bs, int k, int *s_len) {
+    if (!(atomicOr(&bs.alive[k], 2) & 2)) bs.cell_of[atomicAdd(s_len, 1)] = k;
+}
+
+// one warp merges row i with its first partner and repairs the cached partners around it
+__device__ void merge_row(const BlobSpace &bs, const Grid &g, int i, double thr, int lane,
+                          int *s_len) {
+    const int j = bs.first[i];
+    if (lane == 0) {
+        dogblob_blob a = bs.sorted[i];
+        const dogblob_blob w = bs.sorted[j];
+        const double nr = 0.5 * (a.radius + w.radius);
+        a.radius = nr;
+        a.sigma = nr / kSqrt2;
+        a.flags |= (w.flags & DOGBLOB_BLOB_SCALE_EDGE) | DOGBLOB_BLOB_MERGED;
+        a.slice = -1;
+        bs.sorted[i] = a;
+        bs.alive[j] = 0;
+    }
+    __syncwarp();
+    const dogblob_blob bi = bs.sorted[i];
+    const dogblob_blob bj = bs.sorted[j];
+    // (a) first[i] again; (b) rows k < i of this part had no partner and can only gain i
+    int best = INT_MAX;
+    {
+        const int cx = g.cx(bi.x), cy = g.cy(bi.y);
+        for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.gy - 1); ++yy)
+            for (int xx = max(cx - 1, 0); xx <= min(cx + 1, g.gx - 1); ++xx) {
+                const int c = yy * g.gx + xx;
+                const int e = bs.cell_start[c + 1];
+                for (int p = bs.cell_start[c] + lane; p < e; p += 32) {
+                    const int k = bs.cell_items[p];
+                    if (k == i || !(bs.alive[k] & 1)) continue;
+                    const dogblob_blob bk = bs.sorted[k];
+                    if (k > i) {
+                        if (k < best && overlap_ij(bi.x, bi.y, bi.radius, bk.x, bk.y, bk.radius) > thr)
+                            best = k;
+                    } else if (overlap_ij(bk.x, bk.y, bk.radius, bi.x, bi.y, bi.radius) > thr) {
+                        bs.first[k] = i;
+                        list_row(bs, k, s_len);
+                    }
+                }
+            }
+    }
+    for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (lane == 0) bs.first[i] = (best == INT_MAX) ? -1 : best;
+    // (c) rows that pointed at the deleted blob need a new partner
+    {
+        const int cx = g.cx(bj.x), cy = g.cy(bj.y);
+        for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.gy - 1); ++yy)
+            for (int xx = max(cx - 1, 0); xx <= min(cx + 1, g.gx - 1); ++xx) {
+                const int c = yy * g.gx + xx;
+                const int s0 = bs.cell_start[c], e = bs.cell_start[c + 1];
+                for (int p0 = s0; p0 < e; p0 += 32) {
+                    const int p = p0 + lane;
+                    const int k = p < e ? bs.cell_items[p] : -1;
+                    const bool hit = k >= 0 && k != i && (bs.alive[k] & 1) && bs.first[k] == j;
+                    unsigned m = __ballot_sync(0xffffffffu, hit);
+                    while (m) {
+                        const int src = __ffs(m) - 1;
+                        m &= m - 1;
+                        const int kk = __shfl_sync(0xffffffffu, k, src);
+                        int b2 = scan_first_partner(bs, g, kk, thr, lane, 32);
+                        for (int o = 16; o > 0; o >>= 1)
+                            b2 = min(b2, __shfl_xor_sync(0xffffffffu, b2, o));
+                        if (lane == 0) bs.first[kk] = (b2 == INT_MAX) ? -1 : b2;   // kk stays listed
+                    }
+                }
+            }
+    }
+}
+
 __global__ void __launch_bounds__(kLoopThreads)
 prune_loop_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_header *hdr,
                   dogblob_blob *out, int out_cap) {
     if (bs.ctr->small_done) return;
     __shared__ int s_red[33];
-    __shared__ int s_pos, s_list_n, s_carry;
-    __shared__ int s_list[kLoopThreads];
+    __shared__ int s_flag, s_nact, s_len, s_carry;
+    __shared__ int s_act[kLoopThreads];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = min(bs.ctr->n_candidates, bs.cap);
     int merges = 0;
-    auto imin = [](int a, int b) { return min(a, b); };
 
     if (do_prune && n >= 2) {
         const Grid g = load_grid(bs);
-        if (tid == 0) s_pos = 0;
+        // ---- ub(): least fixed point from below (Jacobi sweeps over the grid neighbourhoods) ----
+        if (tid == 0) s_len = 0;
+        for (int i = tid; i < n; i += blockDim.x) {
+            bs.comp[i] = i;
+            bs.cmin[i] = INT_MAX;
+            bs.bound[i] = (unsigned long long)__double_as_longlong(bs.sorted[i].radius);
+        }
         __syncthreads();
         while (true) {
-            // invariant: every alive i < s_pos has first[i] == -1
-            int istar = INT_MAX;
-            for (int base = s_pos; base < n; base += blockDim.x) {
-                const int i = base + tid;
-                int mine = (i < n && bs.alive[i] && bs.first[i] >= 0) ? i : INT_MAX;
-                mine = block_reduce(mine, imin, s_red);
-                if (mine != INT_MAX) { istar = mine; break; }
-            }
-            if (istar == INT_MAX) break;
-            const int j = bs.first[istar];
+            if (tid == 0) s_flag = 0;
             __syncthreads();
-            if (tid == 0) {
-                dogblob_blob a = bs.sorted[istar];
-                const dogblob_blob w = bs.sorted[j];
-                const double nr = 0.5 * (a.radius + w.radius);
-                a.radius = nr;
-                a.sigma = nr / kSqrt2;
-                a.flags |= (w.flags & DOGBLOB_BLOB_SCALE_EDGE) | DOGBLOB_BLOB_MERGED;
-                a.slice = -1;
-                bs.sorted[istar] = a;
-                bs.alive[j] = 0;
-                s_pos = istar;
-                s_list_n = 0;
-            }
-            ++merges;
-            __syncthreads();
-            const dogblob_blob bi = bs.sorted[istar];
-            const dogblob_blob bj = bs.sorted[j];
-            // (a) first[istar] again; (b) rows k < istar can only gain istar as partner
-            int best = INT_MAX;
-            {
+            for (int i = tid; i < n; i += blockDim.x) {
+                const dogblob_blob bi = bs.sorted[i];
+                double ui = ub_of(bs, i);
                 const int cx = g.cx(bi.x), cy = g.cy(bi.y);
+                bool grew = false;
                 for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.gy - 1); ++yy)
                     for (int xx = max(cx - 1, 0); xx <= min(cx + 1, g.gx - 1); ++xx) {
                         const int c = yy * g.gx + xx;
                         const int e = bs.cell_start[c + 1];
-                        for (int p = bs.cell_start[c] + tid; p < e; p += blockDim.x) {
-                            const int k = bs.cell_items[p];
-                            if (k == istar || !bs.alive[k]) continue;
-                            const dogblob_blob bk = bs.sorted[k];
-                            if (k > istar) {
-                                if (k < best &&
-                                    overlap_ij(bi.x, bi.y, bi.radius, bk.x, bk.y, bk.radius) > thr)
-                                    best = k;
-                            } else if (overlap_ij(bk.x, bk.y, bk.radius, bi.x, bi.y, bi.radius) >
-                                       thr) {
-                                bs.first[k] = istar;
-                                atomicMin(&s_pos, k);
+                        for (int p = bs.cell_start[c]; p < e; ++p) {
+                            const int j = bs.cell_items[p];
+                            if (j <= i) continue;
+                            const double uj = ub_of(bs, j);
+                            if (uj <= ui) continue;
+                            const dogblob_blob bj = bs.sorted[j];
+                            const double dx = bi.x - bj.x, dy = bi.y - bj.y, reach = ui + uj;
+                            if (dx * dx + dy * dy < reach * reach * 1.0000001 + 1e-9) {
+                                ui = uj;
+                                grew = true;
                             }
                         }
                     }
-            }
-            best = block_reduce(best, imin, s_red);
-            if (tid == 0) bs.first[istar] = (best == INT_MAX) ? -1 : best;
-            // (c) rows k > istar that pointed at the deleted blob need a new partner
-            {
-                const int cx = g.cx(bj.x), cy = g.cy(bj.y);
-                for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.gy - 1); ++yy)
-                    for (int xx = max(cx - 1, 0); xx <= min(cx + 1, g.gx - 1); ++xx) {
-                        const int c = yy * g.gx + xx;
-                        const int e = bs.cell_start[c + 1];
-                        for (int p = bs.cell_start[c] + tid; p < e; p += blockDim.x) {
-                            const int k = bs.cell_items[p];
-                            if (k != istar && bs.alive[k] && bs.first[k] == j) {
-                                const int slot = atomicAdd(&s_list_n, 1);
-                                if (slot < kLoopThreads) s_list[slot] = k;
-                            }
-                        }
-                    }
-            }
-            __syncthreads();
-            const int ln = s_list_n;   // > kLoopThreads cannot happen: distinct k per slot, but guard
-            for (int q = warp; q < min(ln, kLoopThreads); q += (blockDim.x >> 5)) {
-                const int k = s_list[q];
-                int b2 = scan_first_partner(bs, g, k, thr, lane, 32);
-                for (int o = 16; o > 0; o >>= 1) b2 = min(b2, __shfl_xor_sync(0xffffffffu, b2, o));
-                if (lane == 0) bs.first[k] = (b2 == INT_MAX) ? -1 : b2;
-            }
-            if (ln > kLoopThreads) {   // pathological: finish the remainder serially per warp
-                for (int k = warp; k < n; k += (blockDim.x >> 5)) {
-                    if (!bs.alive[k] || bs.first[k] != j) continue;
-                    int b2 = scan_first_partner(bs, g, k, thr, lane, 32);
-                    for (int o = 16; o > 0; o >>= 1)
-                        b2 = min(b2, __shfl_xor_sync(0xffffffffu, b2, o));
-                    if (lane == 0) bs.first[k] = (b2 == INT_MAX) ? -1 : b2;
+                if (grew) {
+                    bs.bound[i] = (unsigned long long)__double_as_longlong(ui);
+                    s_flag = 1;
                 }
             }
+            __syncthreads();
+            const int changed = s_flag;
+            __syncthreads();
+            if (!changed) break;
+        }
+        // ---- parts: connected components of dist < ub(a) + ub(b) ----
+        for (int i = tid; i < n; i += blockDim.x) {
+            const dogblob_blob bi = bs.sorted[i];
+            const double ui = ub_of(bs, i);
+            const int cx = g.cx(bi.x), cy = g.cy(bi.y);
+            for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.gy - 1); ++yy)
+                for (int xx = max(cx - 1, 0); xx <= min(cx + 1, g.gx - 1); ++xx) {
+                    const int c = yy * g.gx + xx;
+                    const int e = bs.cell_start[c + 1];
+                    for (int p = bs.cell_start[c]; p < e; ++p) {
+                        const int j = bs.cell_items[p];
+                        if (j <= i) continue;
+                        const dogblob_blob bj = bs.sorted[j];
+                        const double dx = bi.x - bj.x, dy = bi.y - bj.y, reach = ui + ub_of(bs, j);
+                        if (dx * dx + dy * dy < reach * reach * 1.0000001 + 1e-9)
+                            comp_union(bs.comp, i, j);
+                    }
+                }
+        }
+        __syncthreads();
+        for (int i = tid; i < n; i += blockDim.x) bs.comp[i] = comp_find(bs.comp, i);
+        __syncthreads();
+        for (int i = tid; i < n; i += blockDim.x)
+            if (bs.first[i] >= 0) list_row(bs, i, &s_len);
+        __syncthreads();
+
+        // ---- rounds: the smallest offending row of every part, all parts at once ----
+        while (true) {
+            if (tid == 0) s_nact = 0;
+            __syncthreads();
+            const int len = s_len;
+            for (int q = tid; q < len; q += blockDim.x) {
+                const int i = bs.cell_of[q];
+                if ((bs.alive[i] & 1) && bs.first[i] >= 0) atomicMin(&bs.cmin[bs.comp[i]], i);
+            }
+            __syncthreads();
+            for (int q = tid; q < len; q += blockDim.x) {
+                const int i = bs.cell_of[q];
+                if ((bs.alive[i] & 1) && bs.first[i] >= 0 && bs.cmin[bs.comp[i]] == i) {
+                    bs.cmin[bs.comp[i]] = INT_MAX;
+                    const int slot = atomicAdd(&s_nact, 1);
+                    if (slot < kLoopThreads) s_act[slot] = i;   // the rest wait for the next round
+                }
+            }
+            __syncthreads();
+            const int nact = min(s_nact, kLoopThreads);
+            if (nact == 0) break;
+            for (int q = warp; q < nact; q += (blockDim.x >> 5))
+                merge_row(bs, g, s_act[q], thr, lane, &s_len);
+            merges += nact;
             __syncthreads();
         }
     }
@@ -319,7 +422,7 @@ prune_loop_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_header 
     __syncthreads();
     for (int base = 0; base < n; base += blockDim.x) {
         const int i = base + tid;
-        const int keep = (i < n) && (!do_prune || n < 2 || bs.alive[i]);
+        const int keep = (i < n) && (!do_prune || n < 2 || (bs.alive[i] & 1));
         int v = keep;
         for (int o = 1; o < 32; o <<= 1) {
             const int t = __shfl_up_sync(0xffffffffu, v, o);

@@ -308,6 +308,24 @@ class TestPruneOverlaps:
                 for j in range(i + 1, len(out.blobs)):
                     assert P.normalized_overlap(out.blobs[i], out.blobs[j]) <= 0.5 + 1e-12
 
+    @pytest.mark.parametrize("n,span,thr", [(900, 250, 0.5), (3000, 420, 0.5), (3000, 420, 0.1),
+                                            (6000, 700, 0.3), (2500, 160, 0.2)])
+    def test_dense_random_sets_against_oracle(self, n, span, thr):
+        """thousands of blobs, hundreds to thousands of merges: both the single-CTA path
+        (n <= 1024) and the grid-bucketed, component-parallel path, against the oracle"""
+        rng = np.random.default_rng(n + span)
+        blobs = [P.Blob(int(rng.integers(0, span)), int(rng.integers(0, span)), 0.0,
+                        float(rng.choice([2.0, 2.5, 3.0, 4.5, 6.0, 9.0]) * math.sqrt(2)),
+                        float(np.float32(rng.uniform(0.1, 1.0))), bool(rng.integers(0, 2)))
+                 for _ in range(n)]
+        blobs = [P.Blob(b.x, b.y, b.radius / math.sqrt(2), b.radius, b.response, b.at_scale_boundary)
+                 for b in blobs]
+        out = P.prune_overlaps(bset(*blobs), thr)
+        want = O.prune([O.OBlob(b.x, b.y, b.sigma, b.radius, b.response, b.at_scale_boundary)
+                        for b in blobs], thr)
+        assert len(want) < n
+        assert records_tuples(out.records) == oblob_tuples(want)
+
     @pytest.mark.parametrize("thr", [0.5, 0.1])
     def test_dense_c5_candidates_against_oracle(self, golden, thr):
         """~10^4 reference candidates of the dense-droplet frame (stresses grid
