@@ -39,7 +39,7 @@ sys.path.insert(0, str(ROOT))
 
 WORKLOAD = "C2"
 BATCH = 16
-KERNELS_PER_FRAME = 12   # reset, row pass, column+DoG, edge DoG, nms, plateau, finalize_small, sort, 3 prune (early exit), pack
+KERNELS_PER_FRAME = 11   # reset, row pass, column+DoG, edge DoG, nms, plateau, finalize_small, rank_sort, prune_build, prune_first, prune_loop
 
 
 def params_kw():
