@@ -126,7 +126,8 @@ cudaError_t launch_load_blobs(const BlobSpace &bs, const dogblob_blob *d_in, int
                               cudaStream_t st);
 cudaError_t launch_rank_sort(const BlobSpace &bs, cudaStream_t st);
 cudaError_t configure_finalize_kernels();   // per device, before the first launch_prune_and_pack
-constexpr int kSmallMax = 1024;   // frames with at most this many candidates finish in one CTA
+constexpr int kSmallMax = 1024;   // threads (and shared-memory slots) of the single-CTA finalize kernel
+int small_limit();                // frames with at most this many candidates finish in that one CTA
 cudaError_t launch_reset_counters(const BlobSpace &bs, cudaStream_t st);
 
 }  // namespace dogblob

@@ -12,6 +12,7 @@
 // neighbourhoods a merge can change.  All overlap arithmetic is float64 with
 // the operation order of the reference (compiled with -fmad=false).
 #include <float.h>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -467,7 +468,7 @@ struct SmallBlob { double x, y, r, resp, sigma; int slice; unsigned flags; };
 
 __global__ void __launch_bounds__(kSmallMax)
 finalize_small_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_header *hdr,
-                      dogblob_blob *out, int out_cap) {
+                      dogblob_blob *out, int out_cap, int limit) {
     extern __shared__ __align__(16) unsigned char small_raw[];
     SmallBlob *sb = reinterpret_cast<SmallBlob *>(small_raw);                 // sorted blobs
     SmallBlob *raw = sb + kSmallMax;                                          // emission order
@@ -477,7 +478,7 @@ finalize_small_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_hea
     __shared__ int s_pos, s_carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_raw = bs.ctr->n_candidates;
-    if (n_raw > kSmallMax || n_raw > bs.cap) {
+    if (n_raw > limit || n_raw > bs.cap) {
         if (tid == 0) bs.ctr->small_done = 0;
         return;
     }
@@ -630,6 +631,16 @@ constexpr size_t kSmallSmem = (size_t)kSmallMax * (2 * sizeof(SmallBlob) + 2 * s
 
 }  // namespace
 
+// One SM is faster than the multi-kernel grid path only for a few hundred candidates.
+int small_limit() {
+    static const int v = [] {
+        const char *e = std::getenv("DOGBLOB_SMALL_LIMIT");
+        const int x = e ? std::atoi(e) : 320;
+        return x < 0 ? 0 : (x > kSmallMax ? kSmallMax : x);
+    }();
+    return v;
+}
+
 cudaError_t configure_finalize_kernels() {
     return cudaFuncSetAttribute(finalize_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kSmallSmem);
@@ -642,7 +653,7 @@ cudaError_t launch_prune_and_pack(const BlobSpace &bs, double overlap, bool prun
                                                  DOGBLOB_RESULT_HEADER_BYTES);
     // <= kSmallMax candidates: everything in one CTA; the general kernels then return at once
     finalize_small_kernel<<<1, kSmallMax, kSmallSmem, st>>>(bs, overlap, prune ? 1 : 0, hdr, out,
-                                                            result_cap);
+                                                            result_cap, small_limit());
     cudaError_t e = launch_rank_sort(bs, st);
     if (e != cudaSuccess) return e;
     if (prune) {

@@ -19,6 +19,10 @@ for name in (sys.argv[1:] or ["C1", "C2", "C4", "C5"]):
     extra = {}
     if name == "C5b":
         frame, kw, extra = synth.config_frame("C5"), synth.config_params("C5"), {"overlap": 0.1}
+    elif name == "P1000":   # "typical blobs per sample ~1000": 1000 droplets, package default ladder
+        frame = synth.sensor_noise(synth.droplet_scene(1024, 1024, 1000, (3.0, 12.0), seed=21,
+                                                       allow_overlap=True), seed=22).image
+        kw = dict(min_sigma=1.0, max_sigma=10.0, n_bin=18)
     else:
         frame, kw = synth.config_frame(name), synth.config_params(name)
     det = P.Detector(P.DetectionParams(preprocess=False, **kw, **extra), slots=1)
