@@ -69,11 +69,9 @@ struct dogblob_plan {
     std::vector<LevelDesc> levels;
     std::vector<double> sigmas;
     // device constants
-    LevelDesc *d_levels = nullptr;
+    LevelTable table;        // fused pass: launch order + level groups
+    LevelTable unit_table;   // stage API: one level per group
     float2 *d_taps = nullptr;
-    int *d_level_order = nullptr;
-    int *d_group_begin = nullptr;
-    int *d_unit_groups = nullptr;
     double *d_slice_sigma = nullptr;
     float *d_sigma_f32 = nullptr;
     // workspace layout (bytes from the workspace base)
@@ -142,6 +140,7 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
     *out = nullptr;
     DB_REQUIRE(height >= 1 && width >= 1, "expected a non-empty 2-D image");
     DB_REQUIRE(n_levels >= 2, "a ladder needs at least two levels");
+    DB_REQUIRE(n_levels <= kMaxLevels, "more than 320 ladder levels are not supported");
     DB_REQUIRE(sigmas && radii && taps && tap_offsets, "NULL table");
     DB_REQUIRE(max_blobs >= 1 && max_blobs < (1 << 24), "max_blobs must be in [1, 2^24)");
     DB_REQUIRE(height <= 32768 && width <= 32768, "image dimension above 32768");
@@ -194,10 +193,12 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
     std::vector<int> group_begin = balance_groups(plan->levels, G);
     g.G = (int)group_begin.size() - 1;
 
+    // Row-pass launch order: longest levels first (short tail).  Interleaving long and short
+    // levels to de-phase co-resident CTAs was measured and does not help.
     std::vector<int> order(n_levels);
     for (int i = 0; i < n_levels; ++i) order[i] = i;
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-        return plan->levels[a].n_mid > plan->levels[b].n_mid;   // longest first
+        return plan->levels[a].n_mid > plan->levels[b].n_mid;
     });
     std::vector<int> unit(n_levels + 1);
     for (int i = 0; i <= n_levels; ++i) unit[i] = i;
@@ -213,22 +214,21 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
             return DOGBLOB_ECUDA;                                                      \
         }                                                                              \
     } while (0)
-    PLAN_CUDA(cudaMalloc(&plan->d_levels, n_levels * sizeof(LevelDesc)));
+    std::memset(&plan->table, 0, sizeof(LevelTable));
+    for (int i = 0; i < n_levels; ++i) {
+        plan->table.lv[i] = plan->levels[i];
+        plan->table.order[i] = order[i];
+    }
+    plan->table.n_levels = n_levels;
+    plan->unit_table = plan->table;
+    plan->table.n_groups = g.G;
+    for (int i = 0; i <= g.G; ++i) plan->table.group_begin[i] = group_begin[i];
+    plan->unit_table.n_groups = n_levels;
+    for (int i = 0; i <= n_levels; ++i) plan->unit_table.group_begin[i] = unit[i];
     PLAN_CUDA(cudaMalloc(&plan->d_taps, table.size() * sizeof(float2)));
-    PLAN_CUDA(cudaMalloc(&plan->d_level_order, n_levels * sizeof(int)));
-    PLAN_CUDA(cudaMalloc(&plan->d_group_begin, group_begin.size() * sizeof(int)));
-    PLAN_CUDA(cudaMalloc(&plan->d_unit_groups, unit.size() * sizeof(int)));
     PLAN_CUDA(cudaMalloc(&plan->d_slice_sigma, n_levels * sizeof(double)));
     PLAN_CUDA(cudaMalloc(&plan->d_sigma_f32, n_levels * sizeof(float)));
-    PLAN_CUDA(cudaMemcpy(plan->d_levels, plan->levels.data(), n_levels * sizeof(LevelDesc),
-                         cudaMemcpyHostToDevice));
     PLAN_CUDA(cudaMemcpy(plan->d_taps, table.data(), table.size() * sizeof(float2),
-                         cudaMemcpyHostToDevice));
-    PLAN_CUDA(cudaMemcpy(plan->d_level_order, order.data(), n_levels * sizeof(int),
-                         cudaMemcpyHostToDevice));
-    PLAN_CUDA(cudaMemcpy(plan->d_group_begin, group_begin.data(), group_begin.size() * sizeof(int),
-                         cudaMemcpyHostToDevice));
-    PLAN_CUDA(cudaMemcpy(plan->d_unit_groups, unit.data(), unit.size() * sizeof(int),
                          cudaMemcpyHostToDevice));
     PLAN_CUDA(cudaMemcpy(plan->d_slice_sigma, sigmas, n_levels * sizeof(double),
                          cudaMemcpyHostToDevice));
@@ -252,11 +252,7 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
 void dogblob_plan_destroy(dogblob_plan *plan) {
     if (!plan) return;
     DeviceGuard guard(plan->device);
-    cudaFree(plan->d_levels);
     cudaFree(plan->d_taps);
-    cudaFree(plan->d_level_order);
-    cudaFree(plan->d_group_begin);
-    cudaFree(plan->d_unit_groups);
     cudaFree(plan->d_slice_sigma);
     cudaFree(plan->d_sigma_f32);
     delete plan;
@@ -297,11 +293,10 @@ int dogblob_detect(const dogblob_plan *plan, const float *d_image, float thresho
     };
     DB_CUDA(ev(0));
     DB_CUDA(launch_reset_counters(bs, st));
-    DB_CUDA(launch_row_pass(g, d_image, rows_t, plan->d_levels, plan->d_taps,
-                            plan->d_level_order, st));
+    DB_CUDA(launch_row_pass(g, d_image, rows_t, plan->table, plan->d_taps, st));
     DB_CUDA(ev(1));
     DB_CUDA(launch_col_dog_pass(g, rows_t, dog_t, reinterpret_cast<float *>(ws + plan->off_edge),
-                                plan->d_levels, plan->d_taps, plan->d_group_begin, st));
+                                plan->table, plan->d_taps, st));
     DB_CUDA(ev(2));
     // D^T planes: rows = x (W valid), cols = y (H valid)
     DB_CUDA(launch_extrema(dog_t, g.L - 1, g.W, g.H, g.Hp, (int64_t)g.Hp * g.Wp, true,
@@ -370,10 +365,8 @@ int dogblob_scale_space(const dogblob_plan *plan, const float *d_image, void *d_
     float *rows_t = reinterpret_cast<float *>(ws + plan->off_rows_t);
     float *lev_t = reinterpret_cast<float *>(ws + plan->off_dog_t);
     const ConvGeometry &g = plan->geo;
-    DB_CUDA(launch_row_pass(g, d_image, rows_t, plan->d_levels, plan->d_taps,
-                            plan->d_level_order, st));
-    DB_CUDA(launch_col_levels_pass(g, rows_t, lev_t, plan->d_levels, plan->d_taps,
-                                   plan->d_unit_groups, st));
+    DB_CUDA(launch_row_pass(g, d_image, rows_t, plan->table, plan->d_taps, st));
+    DB_CUDA(launch_col_levels_pass(g, rows_t, lev_t, plan->unit_table, plan->d_taps, st));
     DB_CUDA(launch_untranspose(lev_t, g.L, g.Hp, g.Wp, g.H, g.W, d_levels, st));
     return DOGBLOB_OK;
 }
@@ -388,10 +381,9 @@ int dogblob_dog(const dogblob_plan *plan, const float *d_image, void *d_workspac
     float *rows_t = reinterpret_cast<float *>(ws + plan->off_rows_t);
     float *dog_t = reinterpret_cast<float *>(ws + plan->off_dog_t);
     const ConvGeometry &g = plan->geo;
-    DB_CUDA(launch_row_pass(g, d_image, rows_t, plan->d_levels, plan->d_taps,
-                            plan->d_level_order, st));
+    DB_CUDA(launch_row_pass(g, d_image, rows_t, plan->table, plan->d_taps, st));
     DB_CUDA(launch_col_dog_pass(g, rows_t, dog_t, reinterpret_cast<float *>(ws + plan->off_edge),
-                                plan->d_levels, plan->d_taps, plan->d_group_begin, st));
+                                plan->table, plan->d_taps, st));
     DB_CUDA(launch_untranspose(dog_t, g.L - 1, g.Hp, g.Wp, g.H, g.W, d_slices, st));
     return DOGBLOB_OK;
 }

@@ -46,6 +46,16 @@ struct LevelDesc {
     float sigma_f32;  // float32(sigma_i), the DoG scale factor
 };
 
+// Per-plan level table, passed to the convolution kernels BY VALUE as a __grid_constant__
+// parameter (constant bank): a CTA reads its level descriptor without a global round trip.
+constexpr int kMaxLevels = 320;
+struct LevelTable {
+    LevelDesc lv[kMaxLevels];
+    int order[kMaxLevels];            // row pass: launch order (longest first)
+    int group_begin[kMaxLevels + 1];  // column pass: level groups
+    int n_levels, n_groups;
+};
+
 // ---- blob bookkeeping shared by extrema / prune ------------------------------
 struct Counters {            // one per result, lives in the blob space
     int n_flagged;           // voxels passing the NMS + threshold test
@@ -101,14 +111,13 @@ struct ConvGeometry {
 };
 
 cudaError_t launch_row_pass(const ConvGeometry &g, const float *d_img, float *d_rows_t,
-                            const LevelDesc *d_levels, const float2 *d_taps,
-                            const int *d_level_order, cudaStream_t st);
+                            const LevelTable &tbl, const float2 *d_taps, cudaStream_t st);
 cudaError_t launch_col_dog_pass(const ConvGeometry &g, const float *d_rows_t, float *d_dog_t,
-                                float *d_edge, const LevelDesc *d_levels, const float2 *d_taps,
-                                const int *d_group_begin, cudaStream_t st);
+                                float *d_edge, const LevelTable &tbl, const float2 *d_taps,
+                                cudaStream_t st);
 cudaError_t launch_col_levels_pass(const ConvGeometry &g, const float *d_rows_t, float *d_lev_t,
-                                   const LevelDesc *d_levels, const float2 *d_taps,
-                                   const int *d_unit_groups, cudaStream_t st);
+                                   const LevelTable &unit_tbl, const float2 *d_taps,
+                                   cudaStream_t st);
 cudaError_t launch_untranspose(const float *d_src_t, int planes, int Hp, int Wp, int H, int W,
                                float *d_dst, cudaStream_t st);
 cudaError_t launch_dog_from_levels(int L, int64_t plane_elems, const float *d_levels,

@@ -18,6 +18,8 @@
 // that is statically indexed by full unrolling.  FMAs are issued as packed
 // fma.rn.f32x2 (FFMA2) so that loads and address arithmetic issue in the shadow
 // of the FMA pipe.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace dogblob {
@@ -76,10 +78,9 @@ constexpr int kL2Ahead = 16;
 template <bool ADJACENT>
 __device__ __forceinline__ void sweep(const float *__restrict__ in, const int *__restrict__ rows,
                                       int n_mid, const float2 *__restrict__ taps, int lane,
-                                      float2 (&acc)[kTY][2], bool frontier = false) {
-    float v[kPrefetch][4];
-#pragma unroll
-    for (int p = 0; p < kPrefetch; ++p) load_row<ADJACENT>(in + rows[p], lane, v[p]);
+                                      float (&v)[kPrefetch][4], float2 (&acc)[kTY][2],
+                                      bool frontier = false) {
+    // v[] holds input rows 0 .. kPrefetch-1 of this sweep, loaded by the caller
     rows += kPrefetch;
     float2 ring[kTY];
     // ---- first chunk ----
@@ -139,10 +140,17 @@ __device__ __forceinline__ void sweep(const float *__restrict__ in, const int *_
     }
 }
 
-__device__ __forceinline__ void stage_taps(float2 *s_taps, const float2 *__restrict__ g_taps,
-                                           const LevelDesc &lv) {
+// taps global -> shared without register staging (LDGSTS); completion via cp_async_wait_all
+__device__ __forceinline__ void stage_taps_async(float2 *s_taps, const float2 *__restrict__ g_taps,
+                                                 const LevelDesc &lv) {
     const int n = 2 * lv.rpad + 1;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) s_taps[i] = g_taps[lv.tap_ofs + i];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(s_taps + i);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(g_taps + lv.tap_ofs + i));
+    }
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // ---- pass 1: correlate along y, store transposed ------------------------------
@@ -159,24 +167,32 @@ __device__ __forceinline__ int tile_index(int x, int y4) {        // y4 = y / 4
 __global__ void __launch_bounds__(kConvThreads, 2)
 row_pass_kernel(const float *__restrict__ img, int64_t img_pitch, int H,
                 float *__restrict__ out_t, int64_t out_pitch, int64_t out_plane,
-                const LevelDesc *__restrict__ levels, const float2 *__restrict__ g_taps,
-                const int *__restrict__ level_order, int max_table) {
+                const __grid_constant__ LevelTable tbl, const float2 *__restrict__ g_taps,
+                int max_table) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float *tile = reinterpret_cast<float *>(smem_raw);                       // [128 x][128 y]
     float2 *s_taps = reinterpret_cast<float2 *>(tile + kTileCols * kTileRows);
     int *s_rows = reinterpret_cast<int *>(s_taps + max_table);
 
-    const int level = level_order[blockIdx.z];
-    const LevelDesc lv = levels[level];
+    const int level = tbl.order[blockIdx.z];
+    const LevelDesc lv = tbl.lv[level];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int col0 = blockIdx.x * kTileCols;            // x
     const int row0 = blockIdx.y * kTileRows;            // y
-    stage_taps(s_taps, g_taps, lv);
+    // everything with memory latency is issued before the barrier: taps (async copy) and
+    // the first input rows of this warp (offsets folded directly, the table is not ready yet)
+    stage_taps_async(s_taps, g_taps, lv);
+    float v[kPrefetch][4];
+#pragma unroll
+    for (int p = 0; p < kPrefetch; ++p)
+        load_row<true>(img + col0 + (int64_t)fold_row(row0 + warp * kTY - lv.rpad + p, H) * img_pitch,
+                       lane, v[p]);
     stage_row_offsets(s_rows, row0 - lv.rpad, kTileRows + 2 * lv.rpad + kPrefetch, H, (int)img_pitch);
+    cp_async_wait_all();
     __syncthreads();
 
     float2 acc[kTY][2];
-    sweep<true>(img + col0, s_rows + warp * kTY, lv.n_mid, s_taps, lane, acc);
+    sweep<true>(img + col0, s_rows + warp * kTY, lv.n_mid, s_taps, lane, v, acc);
 
 #pragma unroll
     for (int q = 0; q < kTY / 4; ++q) {                 // four consecutive y per store
@@ -212,19 +228,20 @@ template <bool DOG>
 __global__ void __launch_bounds__(kConvThreads, 2)
 col_pass_kernel(const float *__restrict__ rows_t, int64_t pitch, int64_t plane, int n_rows,
                 float *__restrict__ out, float *__restrict__ edge,
-                const LevelDesc *__restrict__ levels, const float2 *__restrict__ g_taps,
-                const int *__restrict__ group_begin, int n_groups, int max_table, int max_rpad) {
+                const __grid_constant__ LevelTable tbl, const float2 *__restrict__ g_taps,
+                int max_table, int max_rpad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float2 *s_prev = reinterpret_cast<float2 *>(smem_raw);                    // [kTY*2][256]
-    float2 *s_taps = s_prev + (DOG ? kTY * 2 * kConvThreads : 0);
-    int *s_rows = reinterpret_cast<int *>(s_taps + max_table);
+    float2 *s_taps0 = s_prev + (DOG ? kTY * 2 * kConvThreads : 0);            // double buffered
+    int *s_rows = reinterpret_cast<int *>(s_taps0 + 2 * max_table);
+    const int n_groups = tbl.n_groups;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int col0 = blockIdx.x * kTileCols;
     const int row0 = blockIdx.y * kTileRows + warp * kTY;
     const int g = blockIdx.z;
-    const int lev_begin = group_begin[g];
-    const int lev_end = group_begin[g + 1];
+    const int lev_begin = tbl.group_begin[g];
+    const int lev_end = tbl.group_begin[g + 1];
     const int64_t tile_ofs = (int64_t)row0 * pitch + col0;
     // folded offsets of every input row any level of this CTA can touch
     stage_row_offsets(s_rows, (int)blockIdx.y * kTileRows - max_rpad,
@@ -235,23 +252,36 @@ col_pass_kernel(const float *__restrict__ rows_t, int64_t pitch, int64_t plane, 
     // other tile walks its levels downwards so that their pipeline drains interleave.
     const bool down = DOG && ((blockIdx.x + blockIdx.y) & 1);
     const int n_lev = lev_end - lev_begin;
+    stage_taps_async(s_taps0, g_taps, tbl.lv[down ? lev_end - 1 : lev_begin]);
+    cp_async_wait_all();
+    __syncthreads();                                         // row table + first taps visible
 
     for (int k = 0; k < n_lev; ++k) {
         const int level = down ? lev_end - 1 - k : lev_begin + k;
-        const LevelDesc lv = levels[level];
-        __syncthreads();                                     // previous taps no longer in use
-        stage_taps(s_taps, g_taps, lv);
-        __syncthreads();
+        const LevelDesc lv = tbl.lv[level];
+        const float2 *s_taps = s_taps0 + (k & 1) * max_table;
+        // the next level's taps travel while this level is swept (the other buffer was last
+        // read two levels ago, before the barrier that closed that level)
+        if (k + 1 < n_lev)
+            stage_taps_async(s_taps0 + ((k + 1) & 1) * max_table, g_taps,
+                             tbl.lv[down ? level - 1 : level + 1]);
+        const float *in = rows_t + (int64_t)level * plane + col0;
+        const int *rows = s_rows + warp * kTY + (max_rpad - lv.rpad);
+        float v[kPrefetch][4];
+#pragma unroll
+        for (int p = 0; p < kPrefetch; ++p) load_row<true>(in + rows[p], lane, v[p]);
         float2 acc[kTY][2];
-        sweep<true>(rows_t + (int64_t)level * plane + col0,
-                    s_rows + warp * kTY + (max_rpad - lv.rpad), lv.n_mid, s_taps, lane, acc,
-                    warp == kWarps - 1);
+        sweep<true>(in, rows, lv.n_mid, s_taps, lane, v, acc, warp == kWarps - 1);
         if (!DOG) {
             float *dst = out + (int64_t)level * plane + tile_ofs;
 #pragma unroll
             for (int j = 0; j < kTY; ++j)
                 reinterpret_cast<float4 *>(dst + (int64_t)j * pitch)[lane] =
                     make_float4(acc[j][0].x, acc[j][0].y, acc[j][1].x, acc[j][1].y);
+            if (k < n_lev - 1) {
+                cp_async_wait_all();
+                __syncthreads();
+            }
             continue;
         }
         const bool park_first = (level == lev_begin) && g > 0;
@@ -271,7 +301,7 @@ col_pass_kernel(const float *__restrict__ rows_t, int64_t pitch, int64_t plane, 
         if (k > 0) {
             // the pair (narrow, wide) = (prev, cur) going up, (cur, prev) going down
             const int slice = down ? level : level - 1;
-            const float s = levels[slice].sigma_f32;
+            const float s = tbl.lv[slice].sigma_f32;
             const float sgn = down ? -1.f : 1.f;             // exact: x * -1 only flips the sign
             float *dst = out + (int64_t)slice * plane + tile_ofs;
 #pragma unroll
@@ -292,6 +322,8 @@ col_pass_kernel(const float *__restrict__ rows_t, int64_t pitch, int64_t plane, 
                 s_prev[(2 * j + 0) * kConvThreads + threadIdx.x] = acc[j][0];
                 s_prev[(2 * j + 1) * kConvThreads + threadIdx.x] = acc[j][1];
             }
+            cp_async_wait_all();
+            __syncthreads();        // next taps landed; everyone is done with this level's taps
         }
     }
 }
@@ -299,10 +331,10 @@ col_pass_kernel(const float *__restrict__ rows_t, int64_t pitch, int64_t plane, 
 // the slice that straddles groups g and g+1: D = f32(sigma) * (last(g) - first(g+1))
 __global__ void __launch_bounds__(256)
 edge_dog_kernel(const float *__restrict__ edge, int64_t plane, float *__restrict__ out,
-                const LevelDesc *__restrict__ levels, const int *__restrict__ group_begin) {
+                const __grid_constant__ LevelTable tbl) {
     const int g = blockIdx.y;
-    const int slice = group_begin[g + 1] - 1;
-    const float s = levels[slice].sigma_f32;
+    const int slice = tbl.group_begin[g + 1] - 1;
+    const float s = tbl.lv[slice].sigma_f32;
     const float4 *a = reinterpret_cast<const float4 *>(edge + (int64_t)(2 * g + 1) * plane);
     const float4 *b = reinterpret_cast<const float4 *>(edge + (int64_t)(2 * (g + 1)) * plane);
     float4 *d = reinterpret_cast<float4 *>(out + (int64_t)slice * plane);
@@ -350,12 +382,16 @@ size_t row_table_bytes(int max_rpad) {
     return (size_t)(kTileRows + 2 * max_rpad + kPrefetch + kL2Ahead + 4) * sizeof(int);
 }
 size_t row_pass_smem(int max_table, int max_rpad) {
+    static const size_t pad = [] {          // experiment knob: extra bytes lower the occupancy
+        const char *e = std::getenv("DOGBLOB_ROW_SMEM_PAD");
+        return e ? (size_t)std::atol(e) : (size_t)0;
+    }();
     return (size_t)kTileCols * kTileRows * sizeof(float) + (size_t)max_table * sizeof(float2) +
-           row_table_bytes(max_rpad);
+           row_table_bytes(max_rpad) + pad;
 }
 size_t col_pass_smem(int max_table, int max_rpad, bool dog) {
     return (dog ? (size_t)kTY * 2 * kConvThreads * sizeof(float2) : 0) +
-           (size_t)max_table * sizeof(float2) + row_table_bytes(max_rpad);
+           2 * (size_t)max_table * sizeof(float2) + row_table_bytes(max_rpad);
 }
 
 }  // namespace
@@ -374,39 +410,35 @@ cudaError_t configure_conv_kernels(int max_table, int max_rpad) {
 }
 
 cudaError_t launch_row_pass(const ConvGeometry &g, const float *d_img, float *d_rows_t,
-                            const LevelDesc *d_levels, const float2 *d_taps,
-                            const int *d_level_order, cudaStream_t st) {
+                            const LevelTable &tbl, const float2 *d_taps, cudaStream_t st) {
     dim3 grid(g.Wp / kTileCols, g.Hp / kTileRows, g.L);
     row_pass_kernel<<<grid, kConvThreads, row_pass_smem(g.max_table, g.max_rpad), st>>>(
-        d_img, g.Wp, g.H, d_rows_t, g.Hp, (int64_t)g.Hp * g.Wp, d_levels, d_taps, d_level_order,
-        g.max_table);
+        d_img, g.Wp, g.H, d_rows_t, g.Hp, (int64_t)g.Hp * g.Wp, tbl, d_taps, g.max_table);
     return cudaGetLastError();
 }
 
 cudaError_t launch_col_dog_pass(const ConvGeometry &g, const float *d_rows_t, float *d_dog_t,
-                                float *d_edge, const LevelDesc *d_levels, const float2 *d_taps,
-                                const int *d_group_begin, cudaStream_t st) {
+                                float *d_edge, const LevelTable &tbl, const float2 *d_taps,
+                                cudaStream_t st) {
     dim3 grid(g.Hp / kTileCols, g.Wp / kTileRows, g.G);
     const int64_t plane = (int64_t)g.Hp * g.Wp;
     col_pass_kernel<true><<<grid, kConvThreads, col_pass_smem(g.max_table, g.max_rpad, true), st>>>(
-        d_rows_t, g.Hp, plane, g.W, d_dog_t, d_edge, d_levels, d_taps, d_group_begin, g.G,
-        g.max_table, g.max_rpad);
+        d_rows_t, g.Hp, plane, g.W, d_dog_t, d_edge, tbl, d_taps, g.max_table, g.max_rpad);
     if (g.G > 1) {
         int bx = (int)((plane / 4 + 255) / 256);
         if (bx > 148 * 2) bx = 148 * 2;
-        edge_dog_kernel<<<dim3(bx, g.G - 1), 256, 0, st>>>(d_edge, plane, d_dog_t, d_levels,
-                                                          d_group_begin);
+        edge_dog_kernel<<<dim3(bx, g.G - 1), 256, 0, st>>>(d_edge, plane, d_dog_t, tbl);
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_col_levels_pass(const ConvGeometry &g, const float *d_rows_t, float *d_lev_t,
-                                   const LevelDesc *d_levels, const float2 *d_taps,
-                                   const int *d_unit_groups, cudaStream_t st) {
+                                   const LevelTable &unit_tbl, const float2 *d_taps,
+                                   cudaStream_t st) {
     dim3 grid(g.Hp / kTileCols, g.Wp / kTileRows, g.L);
     col_pass_kernel<false><<<grid, kConvThreads, col_pass_smem(g.max_table, g.max_rpad, false), st>>>(
-        d_rows_t, g.Hp, (int64_t)g.Hp * g.Wp, g.W, d_lev_t, nullptr, d_levels, d_taps,
-        d_unit_groups, g.L, g.max_table, g.max_rpad);
+        d_rows_t, g.Hp, (int64_t)g.Hp * g.Wp, g.W, d_lev_t, nullptr, unit_tbl, d_taps, g.max_table,
+        g.max_rpad);
     return cudaGetLastError();
 }
 

@@ -73,9 +73,9 @@ __global__ void __launch_bounds__(256, 2) sweep_kernel(const float *__restrict__
 }
 
 template <int MODE, int PF>
-void run(const char *name, const float *img, int64_t pitch, int n_rows) {
+void run(const char *name, const float *img, int64_t pitch, int n_rows, int chunks = 40, int waves = 4) {
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    int blocks = sms * 2 * 4, chunks = 40;     // 4 waves of short CTAs like the row pass
+    int blocks = sms * 2 * waves;
     float *out; cudaMalloc(&out, (size_t)blocks * 256 * 4);
     size_t smem = 1024 * 8 + 1024 * 16 + 4096 * 4 + 4096 * 8;
     cudaFuncSetAttribute(sweep_kernel<MODE, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -104,5 +104,10 @@ int main() {
     run<2, 2>("LDG int64 byte table PF=2", img, pitch, n_rows);
     run<2, 6>("LDG int64 byte table PF=6", img, pitch, n_rows);
     run<1, 8>("LDG int32 table PF=8", img, pitch, n_rows);
+    run<1, 4>("current, 160 chunks x 1 wave", img, pitch, n_rows, 160, 1);
+    run<1, 4>("current, 20 chunks x 8 waves", img, pitch, n_rows, 20, 8);
+    run<1, 4>("current, 11 chunks x 13 waves", img, pitch, n_rows, 11, 13);
+    run<1, 4>("current, 5 chunks x 32 waves", img, pitch, n_rows, 5, 32);
+    run<1, 4>("current, 2 chunks x 80 waves", img, pitch, n_rows, 2, 80);
     return 0;
 }
