@@ -127,18 +127,27 @@ nms_kernel(Volume vol, float thr, int h, bool transposed, const double *__restri
         const int r = r0 - 1 + q;
         const float *row = &tile[q * kNmsPitch + 4 + 4 * t];
         const float4 mid = *reinterpret_cast<const float4 *>(row);
-        const float v[4] = {mid.x, mid.y, mid.z, mid.w};
         const bool any = (mid.x > thr) | (mid.y > thr) | (mid.z > thr) | (mid.w > thr);
         if (!__any_sync(0xffffffffu, any)) continue;
+        // 3 x 6 window [left | 4 own columns | right] of rows q-1, q, q+1: three 16-byte and
+        // six 4-byte shared loads feed all 8 in-slice neighbours of the 4 voxels
+        float w[3][6];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const float *rp = row + (d - 1) * kNmsPitch;
+            const float4 c4 = *reinterpret_cast<const float4 *>(rp);
+            w[d][0] = rp[-1];
+            w[d][1] = c4.x; w[d][2] = c4.y; w[d][3] = c4.z; w[d][4] = c4.w;
+            w[d][5] = rp[4];
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const float val = v[k];
+            const float val = w[1][k + 1];
             bool cand = val > thr;            // out-of-plane voxels hold -inf
-            if (cand && h >= 1) {             // the 8 in-slice neighbours are in every n >= 3 block
-                const float *u = row + k - kNmsPitch, *m = row + k, *d = row + k + kNmsPitch;
-                cand = !(u[-1] > val) && !(u[0] > val) && !(u[1] > val) && !(m[-1] > val) &&
-                       !(m[1] > val) && !(d[-1] > val) && !(d[0] > val) && !(d[1] > val);
-            }
+            if (h >= 1)                       // the 8 in-slice neighbours are in every n >= 3 block
+                cand = cand && !(w[0][k] > val) && !(w[0][k + 1] > val) && !(w[0][k + 2] > val) &&
+                       !(w[1][k] > val) && !(w[1][k + 2] > val) &&
+                       !(w[2][k] > val) && !(w[2][k + 1] > val) && !(w[2][k + 2] > val);
             if (!__any_sync(0xffffffffu, cand)) continue;
             bool flagged = false, plateau = false;
             if (cand) {
