@@ -334,15 +334,14 @@ def normalized_overlap(b1: OBlob, b2: OBlob) -> float:
     return lens_area(b1.x, b1.y, b1.radius, b2.x, b2.y, b2.radius) / (math.pi * rmin * rmin)
 
 
-def overlap_row(xs, ys, rs, i: int, js: np.ndarray) -> np.ndarray:
-    """Normalised overlap of blob i with blobs js, the vector arithmetic of
-    _overlap_matrix (detector.py:221-247), float64."""
-    d = np.hypot(xs[i] - xs[js], ys[i] - ys[js])
-    r1 = np.full(js.shape, rs[i])
-    r2 = rs[js]
+def overlap_pairs(x1, y1, r1, x2, y2, r2) -> np.ndarray:
+    """Normalised overlap of matrix entries [row][col] for row blobs (x1, y1, r1) and column
+    blobs (x2, y2, r2), element-wise on equally shaped arrays: the vector arithmetic of
+    _overlap_matrix (detector.py:221-247), float64, same operand order."""
+    d = np.hypot(x1 - x2, y1 - y2)
     rmin = np.minimum(r1, r2)
     rmax = np.maximum(r1, r2)
-    out = np.zeros(js.shape)
+    out = np.zeros(d.shape)
     contained = d <= rmax - rmin
     out[contained] = 1.0
     partial = (~contained) & (d < r1 + r2) & (d > 0)
@@ -354,7 +353,24 @@ def overlap_row(xs, ys, rs, i: int, js: np.ndarray) -> np.ndarray:
             (-dd + p1 + p2) * (dd + p1 - p2) * (dd - p1 + p2) * (dd + p1 + p2), 0, None))
         rm = np.minimum(p1, p2)
         out[partial] = (a1 + a2 - s) / (np.pi * rm * rm)
+    return out
+
+
+def overlap_row(xs, ys, rs, i: int, js: np.ndarray) -> np.ndarray:
+    """Entries [i][js] of the overlap matrix (diagonal zeroed, detector.py:246)."""
+    js = np.asarray(js)
+    out = overlap_pairs(np.full(js.shape, xs[i]), np.full(js.shape, ys[i]), np.full(js.shape, rs[i]),
+                        xs[js], ys[js], rs[js])
     out[js == i] = 0.0
+    return out
+
+
+def overlap_col(xs, ys, rs, ks: np.ndarray, i: int) -> np.ndarray:
+    """Entries [ks][i] of the overlap matrix (row blob = k, column blob = i)."""
+    ks = np.asarray(ks)
+    out = overlap_pairs(xs[ks], ys[ks], rs[ks], np.full(ks.shape, xs[i]), np.full(ks.shape, ys[i]),
+                        np.full(ks.shape, rs[i]))
+    out[ks == i] = 0.0
     return out
 
 
@@ -415,8 +431,7 @@ def prune(blobs: list[OBlob], overlap_threshold: float = 0.5) -> list[OBlob]:
         # only pair of theirs whose overlap changed is (k, i).
         lower = alive_idx[alive_idx < i]
         if lower.size:
-            ov = np.array([overlap_row(xs, ys, rs, int(k), np.array([i]))[0] for k in lower])
-            first[lower[ov > overlap_threshold]] = i
+            first[lower[overlap_col(xs, ys, rs, lower, i) > overlap_threshold]] = i
         # rows k > i only lose j as a partner
         for k in alive_idx[(alive_idx > i) & (first[alive_idx] == j)]:
             first[int(k)] = first_partner(int(k), alive_idx)

@@ -99,6 +99,16 @@ class TestPruneAndHistogram:
             thr = float(p[f"p{c}_thr"])
             assert O.prune(blobs, thr) == O.prune_dense(blobs, thr)
 
+    def test_dense_c5_candidates(self, golden):
+        """9,714 reference candidates of the dense frame -> the reference's 9,023 survivors
+        (691 merges; the reference's dense-matrix loop needs 75 minutes for this)"""
+        g = golden("config_C5.npz")
+        out = O.prune(golden_oblobs(g, "t0_cand_"), 0.5)
+        assert oblob_tuples(out) == golden_blobs(g, "t0_kept_")
+        h = O.radius_histogram(out, O.ladder_sigmas(1.0, 6.0, 10))
+        assert np.array_equal(h.counts, g["t0_hist_counts"])
+        assert np.array_equal(h.volume_weights, g["t0_hist_volumes"])
+
     def test_threshold_bounds(self):
         with pytest.raises(ValueError):
             O.prune([], 1.5)
