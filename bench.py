@@ -214,7 +214,7 @@ def run_ours(args):
 
     kw = params_kw()
     params = P.DetectionParams(preprocess=False, **kw)
-    n_slots = 4
+    n_slots = int(os.environ.get("DOGBLOB_BENCH_SLOTS", "4"))   # frame slots = concurrent streams
     det = P.Detector(params, device=local, slots=n_slots)
     # frame f of the global batch goes to rank f mod world
     my_frames = [f for f in range(BATCH * world) if f % world == rank]

@@ -173,7 +173,7 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
         lv.n_mid = (2 * rpad + kTY) / kTY - 2;
         lv.tap_ofs = (int)table.size();
         lv.sigma_f32 = (float)sigmas[i];
-        const int len = 2 * rpad + 1;
+        const int len = 2 * rpad + kTY;      // 2 rpad + 1 taps, then 15 zeros
         max_table = std::max(max_table, len);
         max_rpad = std::max(max_rpad, rpad);
         const float *w = taps + tap_offsets[i];
@@ -191,7 +191,25 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
     int G = choose_groups(tiles, n_levels);
     if (const char *env = std::getenv("DOGBLOB_GROUPS")) G = std::max(1, std::atoi(env));
     std::vector<int> group_begin = balance_groups(plan->levels, G);
+    // the fused pass stages the tap tables of a whole group in shared memory: split further
+    // until two CTAs fit on an SM (one level per group always fits one CTA)
+    auto group_table = [&](const std::vector<int> &begin) {
+        int worst = 0;
+        for (size_t q = 0; q + 1 < begin.size(); ++q) {
+            int len = 0;
+            for (int i = begin[q]; i < begin[q + 1]; ++i) len += 2 * plan->levels[i].rpad + kTY;
+            worst = std::max(worst, len);
+        }
+        return worst;
+    };
+    const size_t smem_budget = 113 * 1024;
+    while ((int)group_begin.size() - 1 < n_levels &&
+           col_pass_smem(group_table(group_begin), max_rpad, true) > smem_budget) {
+        ++G;
+        group_begin = balance_groups(plan->levels, G);
+    }
     g.G = (int)group_begin.size() - 1;
+    g.max_group_table = group_table(group_begin);
 
     // Row-pass launch order: longest levels first (short tail).  Interleaving long and short
     // levels to de-phase co-resident CTAs was measured and does not help.
@@ -234,7 +252,7 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
                          cudaMemcpyHostToDevice));
     PLAN_CUDA(cudaMemcpy(plan->d_sigma_f32, sig32.data(), n_levels * sizeof(float),
                          cudaMemcpyHostToDevice));
-    PLAN_CUDA(configure_conv_kernels(max_table, max_rpad));
+    PLAN_CUDA(configure_conv_kernels(device));
     PLAN_CUDA(configure_finalize_kernels());
 #undef PLAN_CUDA
 

@@ -42,7 +42,8 @@ constexpr int kConvThreads = 32 * kWarps;
 struct LevelDesc {
     int rpad;         // r_i = ceil(truncate * sigma_i) rounded up to a multiple of 8 (zero taps)
     int n_mid;        // full chunks between the first and the last: (2 rpad + 16) / 16 - 2
-    int tap_ofs;      // start (in float2) of this level's duplicated tap table, 2 rpad + 1 long
+    int tap_ofs;      // start (in float2) of this level's duplicated tap table: 2 rpad + 1 taps
+                      // followed by 15 zeros (2 rpad + 16 entries = a whole number of chunks)
     float sigma_f32;  // float32(sigma_i), the DoG scale factor
 };
 
@@ -106,7 +107,8 @@ struct ConvGeometry {
     int Hp, Wp;          // padded to kPad
     int L;               // levels
     int G;               // level groups of the fused column+DoG pass
-    int max_table;       // float2 entries of the longest tap table (2 max_rpad + 1)
+    int max_table;       // float2 entries of the longest tap table (2 max_rpad + 16)
+    int max_group_table; // float2 entries of the longest level group's concatenated tables
     int max_rpad;        // largest padded radius
 };
 
@@ -122,7 +124,8 @@ cudaError_t launch_untranspose(const float *d_src_t, int planes, int Hp, int Wp,
                                float *d_dst, cudaStream_t st);
 cudaError_t launch_dog_from_levels(int L, int64_t plane_elems, const float *d_levels,
                                    const float *d_sigma_f32, float *d_out, cudaStream_t st);
-cudaError_t configure_conv_kernels(int max_table, int max_rpad);
+cudaError_t configure_conv_kernels(int device);
+size_t col_pass_smem(int group_table, int max_rpad, bool dog);
 
 // extrema: NMS + compaction + plateau coalescing + ordering
 cudaError_t launch_extrema(const float *d_slices, int S, int rows, int cols, int64_t pitch,

@@ -75,21 +75,48 @@ __device__ __forceinline__ void prefetch_l2(const void *p) {
 // register prefetch (kPrefetch rows) only has to cover L2 latency, not HBM latency.
 constexpr int kL2Ahead = 16;
 
-template <bool ADJACENT>
-__device__ __forceinline__ void sweep(const float *__restrict__ in, const int *__restrict__ rows,
-                                      int n_mid, const float2 *__restrict__ taps, int lane,
-                                      float (&v)[kPrefetch][4], float2 (&acc)[kTY][2],
-                                      bool frontier = false) {
-    // v[] holds input rows 0 .. kPrefetch-1 of this sweep, loaded by the caller
-    rows += kPrefetch;
-    float2 ring[kTY];
-    // ---- first chunk ----
+// one full chunk: 16 sub-steps, each feeds all 16 outputs
+__device__ __forceinline__ void full_chunk(const float *__restrict__ in,
+                                           const int *__restrict__ rows,
+                                           const float2 *__restrict__ taps, int lane,
+                                           float (&v)[kPrefetch][4], float2 (&ring)[kTY],
+                                           float2 (&acc)[kTY][2], bool frontier) {
 #pragma unroll
     for (int u = 0; u < kTY; ++u) {
         ring[u] = taps[u];
         const float2 a = make_float2(v[u % kPrefetch][0], v[u % kPrefetch][1]);
         const float2 b = make_float2(v[u % kPrefetch][2], v[u % kPrefetch][3]);
-        load_row<ADJACENT>(in + rows[u], lane, v[u % kPrefetch]);
+        load_row<true>(in + rows[u], lane, v[u % kPrefetch]);
+        if (frontier && (u & 3) == 0)     // 4 rows x 4 lines per request group
+            prefetch_l2(in + rows[u + kL2Ahead + (lane >> 3)] + (lane & 7) * 16);
+#pragma unroll
+        for (int j = 0; j < kTY; ++j) {
+            const float2 t = ring[(u - j + kTY) % kTY];
+            acc[j][0] = ffma2(t, a, acc[j][0]);
+            acc[j][1] = ffma2(t, b, acc[j][1]);
+        }
+    }
+}
+
+// v[] holds input rows 0 .. kPrefetch-1 of this sweep, loaded by the caller.
+// Measured alternatives that did NOT help (identical results, tools/sweep_modes.py history):
+// running the head and/or tail through the full-chunk code on zero taps (smaller code, no
+// cold straight-line blocks, but 256 instead of 136 FMA groups: row pass +3..10 %), and
+// 8 instead of 4 rows in flight during the head (+0 %): the FMA pipe, not the head's load
+// latency or instruction fetch, sets the pace.
+__device__ __forceinline__ void sweep(const float *__restrict__ in, const int *__restrict__ rows,
+                                      int n_mid, const float2 *__restrict__ taps, int lane,
+                                      float (&v)[kPrefetch][4], float2 (&acc)[kTY][2],
+                                      bool frontier = false) {
+    rows += kPrefetch;
+    float2 ring[kTY];
+    // ---- first chunk: sub-step u feeds outputs j <= u ----
+#pragma unroll
+    for (int u = 0; u < kTY; ++u) {
+        ring[u] = taps[u];
+        const float2 a = make_float2(v[u % kPrefetch][0], v[u % kPrefetch][1]);
+        const float2 b = make_float2(v[u % kPrefetch][2], v[u % kPrefetch][3]);
+        load_row<true>(in + rows[u], lane, v[u % kPrefetch]);
 #pragma unroll
         for (int j = 0; j <= u; ++j) {
             const float2 t = ring[u - j];
@@ -106,31 +133,17 @@ __device__ __forceinline__ void sweep(const float *__restrict__ in, const int *_
     rows += kTY;
     // ---- middle chunks ----
     for (int chunk = 0; chunk < n_mid; ++chunk) {
-#pragma unroll
-        for (int u = 0; u < kTY; ++u) {
-            ring[u] = taps[u];
-            const float2 a = make_float2(v[u % kPrefetch][0], v[u % kPrefetch][1]);
-            const float2 b = make_float2(v[u % kPrefetch][2], v[u % kPrefetch][3]);
-            load_row<ADJACENT>(in + rows[u], lane, v[u % kPrefetch]);
-            if (ADJACENT && frontier && (u & 3) == 0)     // 4 rows x 4 lines per request group
-                prefetch_l2(in + rows[u + kL2Ahead + (lane >> 3)] + (lane & 7) * 16);
-#pragma unroll
-            for (int j = 0; j < kTY; ++j) {
-                const float2 t = ring[(u - j + kTY) % kTY];
-                acc[j][0] = ffma2(t, a, acc[j][0]);
-                acc[j][1] = ffma2(t, b, acc[j][1]);
-            }
-        }
+        full_chunk(in, rows, taps, lane, v, ring, acc, frontier);
         taps += kTY;
         rows += kTY;
     }
-    // ---- last chunk ----
+    // ---- last chunk: sub-step u feeds outputs j >= u ----
     ring[0] = taps[0];
 #pragma unroll
     for (int u = 0; u < kTY; ++u) {
         const float2 a = make_float2(v[u % kPrefetch][0], v[u % kPrefetch][1]);
         const float2 b = make_float2(v[u % kPrefetch][2], v[u % kPrefetch][3]);
-        if (u + kPrefetch < kTY) load_row<ADJACENT>(in + rows[u], lane, v[u % kPrefetch]);
+        if (u + kPrefetch < kTY) load_row<true>(in + rows[u], lane, v[u % kPrefetch]);
 #pragma unroll
         for (int j = u; j < kTY; ++j) {
             const float2 t = ring[(u - j + kTY) % kTY];
@@ -140,18 +153,19 @@ __device__ __forceinline__ void sweep(const float *__restrict__ in, const int *_
     }
 }
 
-// taps global -> shared without register staging (LDGSTS); completion via cp_async_wait_all
+// n float2 entries global -> shared without register staging (LDGSTS, 16 bytes each; n is
+// even and both sides are 16-byte aligned); completion via cp_async_wait_all
 __device__ __forceinline__ void stage_taps_async(float2 *s_taps, const float2 *__restrict__ g_taps,
-                                                 const LevelDesc &lv) {
-    const int n = 2 * lv.rpad + 1;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                                                 int n) {
+    for (int i = 2 * threadIdx.x; i < n; i += 2 * blockDim.x) {
         const unsigned dst = (unsigned)__cvta_generic_to_shared(s_taps + i);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(g_taps + lv.tap_ofs + i));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(g_taps + i));
     }
 }
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;" ::: "memory");
 }
+__device__ __forceinline__ int table_len(const LevelDesc &lv) { return 2 * lv.rpad + kTY; }
 
 // ---- pass 1: correlate along y, store transposed ------------------------------
 // The 128 x 128 output tile is transposed through shared memory with 16-byte accesses on
@@ -181,7 +195,7 @@ row_pass_kernel(const float *__restrict__ img, int64_t img_pitch, int H,
     const int row0 = blockIdx.y * kTileRows;            // y
     // everything with memory latency is issued before the barrier: taps (async copy) and
     // the first input rows of this warp (offsets folded directly, the table is not ready yet)
-    stage_taps_async(s_taps, g_taps, lv);
+    stage_taps_async(s_taps, g_taps + lv.tap_ofs, table_len(lv));
     float v[kPrefetch][4];
 #pragma unroll
     for (int p = 0; p < kPrefetch; ++p)
@@ -192,7 +206,7 @@ row_pass_kernel(const float *__restrict__ img, int64_t img_pitch, int H,
     __syncthreads();
 
     float2 acc[kTY][2];
-    sweep<true>(img + col0, s_rows + warp * kTY, lv.n_mid, s_taps, lane, v, acc);
+    sweep(img + col0, s_rows + warp * kTY, lv.n_mid, s_taps, lane, v, acc);
 
 #pragma unroll
     for (int q = 0; q < kTY / 4; ++q) {                 // four consecutive y per store
@@ -219,21 +233,23 @@ row_pass_kernel(const float *__restrict__ img, int64_t img_pitch, int H,
 
 // ---- pass 2: correlate along x (rows of the transposed planes), fused DoG ------
 // grid.z = level group g; the CTA walks levels [group_begin[g], group_begin[g+1])
-// keeping the previous level's tile in shared memory and emits
+// keeping the previous level's outputs in shared memory (thread private slots) and emits
 // D_i = f32(sigma_i) (L_i - L_{i+1}) for every pair inside the group, so no level of
 // the group reaches memory.  Only the two levels at a group boundary are parked in
 // `edge` planes (first level of group g -> edge[2g], last level -> edge[2g+1]);
 // edge_dog_kernel turns each boundary pair into the one missing slice.
+// The tap tables of the whole group and the folded row offsets are staged once, so the
+// level loop has no barrier: the 8 warps of a CTA drift apart and their epilogues
+// (DoG, stores) overlap the FMA work of the others.
 template <bool DOG>
 __global__ void __launch_bounds__(kConvThreads, 2)
 col_pass_kernel(const float *__restrict__ rows_t, int64_t pitch, int64_t plane, int n_rows,
                 float *__restrict__ out, float *__restrict__ edge,
                 const __grid_constant__ LevelTable tbl, const float2 *__restrict__ g_taps,
-                int max_table, int max_rpad) {
+                int max_rpad, unsigned frontier_warps) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float2 *s_prev = reinterpret_cast<float2 *>(smem_raw);                    // [kTY*2][256]
-    float2 *s_taps0 = s_prev + (DOG ? kTY * 2 * kConvThreads : 0);            // double buffered
-    int *s_rows = reinterpret_cast<int *>(s_taps0 + 2 * max_table);
+    float2 *s_taps0 = s_prev + (DOG ? kTY * 2 * kConvThreads : 0);            // whole group
     const int n_groups = tbl.n_groups;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -242,88 +258,80 @@ col_pass_kernel(const float *__restrict__ rows_t, int64_t pitch, int64_t plane, 
     const int g = blockIdx.z;
     const int lev_begin = tbl.group_begin[g];
     const int lev_end = tbl.group_begin[g + 1];
+    const int tap_base = tbl.lv[lev_begin].tap_ofs;
+    const int tap_count = tbl.lv[lev_end - 1].tap_ofs + table_len(tbl.lv[lev_end - 1]) - tap_base;
+    int *s_rows = reinterpret_cast<int *>(s_taps0 + tap_count);
     const int64_t tile_ofs = (int64_t)row0 * pitch + col0;
+    stage_taps_async(s_taps0, g_taps + tap_base, tap_count);
     // folded offsets of every input row any level of this CTA can touch
     stage_row_offsets(s_rows, (int)blockIdx.y * kTileRows - max_rpad,
                       kTileRows + 2 * max_rpad + kPrefetch + kL2Ahead + 4, n_rows, (int)pitch);
-
-    // All tiles of a group walk their levels in the same direction: neighbouring tiles then
-    // read the halo rows they share at about the same time, i.e. from L2 (alternating the
-    // direction per tile was measured: no gain in time, +45 % DRAM reads).
-    const bool down = false;
-    const int n_lev = lev_end - lev_begin;
-    stage_taps_async(s_taps0, g_taps, tbl.lv[down ? lev_end - 1 : lev_begin]);
     cp_async_wait_all();
-    __syncthreads();                                         // row table + first taps visible
+    __syncthreads();                                         // row table + taps visible
 
-    for (int k = 0; k < n_lev; ++k) {
-        const int level = down ? lev_end - 1 - k : lev_begin + k;
-        const LevelDesc lv = tbl.lv[level];
-        const float2 *s_taps = s_taps0 + (k & 1) * max_table;
-        // the next level's taps travel while this level is swept (the other buffer was last
-        // read two levels ago, before the barrier that closed that level)
-        if (k + 1 < n_lev)
-            stage_taps_async(s_taps0 + ((k + 1) & 1) * max_table, g_taps,
-                             tbl.lv[down ? level - 1 : level + 1]);
-        const float *in = rows_t + (int64_t)level * plane + col0;
-        const int *rows = s_rows + warp * kTY + (max_rpad - lv.rpad);
-        float v[kPrefetch][4];
+    float v[kPrefetch][4];
+    {
+        const LevelDesc lv0 = tbl.lv[lev_begin];
+        const float *in = rows_t + (int64_t)lev_begin * plane + col0;
+        const int *rows = s_rows + warp * kTY + (max_rpad - lv0.rpad);
 #pragma unroll
         for (int p = 0; p < kPrefetch; ++p) load_row<true>(in + rows[p], lane, v[p]);
+    }
+    for (int level = lev_begin; level < lev_end; ++level) {
+        const LevelDesc lv = tbl.lv[level];
+        const float2 *s_taps = s_taps0 + (lv.tap_ofs - tap_base);
+        const float *in = rows_t + (int64_t)level * plane + col0;
+        const int *rows = s_rows + warp * kTY + (max_rpad - lv.rpad);
         float2 acc[kTY][2];
-        sweep<true>(in, rows, lv.n_mid, s_taps, lane, v, acc, warp == kWarps - 1);
+        sweep(in, rows, lv.n_mid, s_taps, lane, v, acc, (frontier_warps >> warp) & 1u);
         if (!DOG) {
             float *dst = out + (int64_t)level * plane + tile_ofs;
 #pragma unroll
             for (int j = 0; j < kTY; ++j)
                 reinterpret_cast<float4 *>(dst + (int64_t)j * pitch)[lane] =
                     make_float4(acc[j][0].x, acc[j][0].y, acc[j][1].x, acc[j][1].y);
-            if (k < n_lev - 1) {
-                cp_async_wait_all();
-                __syncthreads();
-            }
-            continue;
-        }
-        const bool park_first = (level == lev_begin) && g > 0;
-        const bool park_last = (level == lev_end - 1) && g < n_groups - 1;
-        if (park_first || park_last) {
+        } else {
+            const bool park_first = (level == lev_begin) && g > 0;
+            const bool park_last = (level == lev_end - 1) && g < n_groups - 1;
+#pragma unroll 1
+            for (int e = 0; e < 2; ++e) {        // rare path: kept rolled to save registers
+                if (e == 0 ? !park_first : !park_last) continue;
+                float *dst = edge + (int64_t)(2 * g + e) * plane + tile_ofs;
 #pragma unroll
-            for (int j = 0; j < kTY; ++j) {
-                const float4 q = make_float4(acc[j][0].x, acc[j][0].y, acc[j][1].x, acc[j][1].y);
-                if (park_first)
-                    reinterpret_cast<float4 *>(edge + (int64_t)(2 * g) * plane + tile_ofs +
-                                               (int64_t)j * pitch)[lane] = q;
-                if (park_last)
-                    reinterpret_cast<float4 *>(edge + (int64_t)(2 * g + 1) * plane + tile_ofs +
-                                               (int64_t)j * pitch)[lane] = q;
+                for (int j = 0; j < kTY; ++j) {
+                    reinterpret_cast<float4 *>(dst)[lane] =
+                        make_float4(acc[j][0].x, acc[j][0].y, acc[j][1].x, acc[j][1].y);
+                    dst += pitch;
+                }
+            }
+            if (level > lev_begin) {
+                const float s = tbl.lv[level - 1].sigma_f32;
+                float *dst = out + (int64_t)(level - 1) * plane + tile_ofs;
+#pragma unroll
+                for (int j = 0; j < kTY; ++j) {
+                    const float2 p0 = s_prev[(2 * j + 0) * kConvThreads + threadIdx.x];
+                    const float2 p1 = s_prev[(2 * j + 1) * kConvThreads + threadIdx.x];
+                    float4 d;   // sigma * (narrow - wide): subtract, then scale (two roundings)
+                    d.x = __fmul_rn(__fsub_rn(p0.x, acc[j][0].x), s);
+                    d.y = __fmul_rn(__fsub_rn(p0.y, acc[j][0].y), s);
+                    d.z = __fmul_rn(__fsub_rn(p1.x, acc[j][1].x), s);
+                    d.w = __fmul_rn(__fsub_rn(p1.y, acc[j][1].y), s);
+                    reinterpret_cast<float4 *>(dst + (int64_t)j * pitch)[lane] = d;
+                }
+            }
+            if (level < lev_end - 1) {
+#pragma unroll
+                for (int j = 0; j < kTY; ++j) {
+                    s_prev[(2 * j + 0) * kConvThreads + threadIdx.x] = acc[j][0];
+                    s_prev[(2 * j + 1) * kConvThreads + threadIdx.x] = acc[j][1];
+                }
             }
         }
-        if (k > 0) {
-            // the pair (narrow, wide) = (prev, cur) going up, (cur, prev) going down
-            const int slice = down ? level : level - 1;
-            const float s = tbl.lv[slice].sigma_f32;
-            const float sgn = down ? -1.f : 1.f;             // exact: x * -1 only flips the sign
-            float *dst = out + (int64_t)slice * plane + tile_ofs;
+        if (level + 1 < lev_end) {             // first rows of the next level
+            const float *in2 = in + plane;
+            const int *rows2 = s_rows + warp * kTY + (max_rpad - tbl.lv[level + 1].rpad);
 #pragma unroll
-            for (int j = 0; j < kTY; ++j) {
-                const float2 p0 = s_prev[(2 * j + 0) * kConvThreads + threadIdx.x];
-                const float2 p1 = s_prev[(2 * j + 1) * kConvThreads + threadIdx.x];
-                float4 d;   // sigma * (narrow - wide): subtract, then scale (two roundings)
-                d.x = __fmul_rn(__fsub_rn(p0.x, acc[j][0].x) * sgn, s);
-                d.y = __fmul_rn(__fsub_rn(p0.y, acc[j][0].y) * sgn, s);
-                d.z = __fmul_rn(__fsub_rn(p1.x, acc[j][1].x) * sgn, s);
-                d.w = __fmul_rn(__fsub_rn(p1.y, acc[j][1].y) * sgn, s);
-                reinterpret_cast<float4 *>(dst + (int64_t)j * pitch)[lane] = d;
-            }
-        }
-        if (k < n_lev - 1) {
-#pragma unroll
-            for (int j = 0; j < kTY; ++j) {
-                s_prev[(2 * j + 0) * kConvThreads + threadIdx.x] = acc[j][0];
-                s_prev[(2 * j + 1) * kConvThreads + threadIdx.x] = acc[j][1];
-            }
-            cp_async_wait_all();
-            __syncthreads();        // next taps landed; everyone is done with this level's taps
+            for (int p = 0; p < kPrefetch; ++p) load_row<true>(in2 + rows2[p], lane, v[p]);
         }
     }
 }
@@ -382,38 +390,50 @@ size_t row_table_bytes(int max_rpad) {
     return (size_t)(kTileRows + 2 * max_rpad + kPrefetch + kL2Ahead + 4) * sizeof(int);
 }
 size_t row_pass_smem(int max_table, int max_rpad) {
-    static const size_t pad = [] {          // experiment knob: extra bytes lower the occupancy
-        const char *e = std::getenv("DOGBLOB_ROW_SMEM_PAD");
-        return e ? (size_t)std::atol(e) : (size_t)0;
-    }();
     return (size_t)kTileCols * kTileRows * sizeof(float) + (size_t)max_table * sizeof(float2) +
-           row_table_bytes(max_rpad) + pad;
+           row_table_bytes(max_rpad);
 }
-size_t col_pass_smem(int max_table, int max_rpad, bool dog) {
+size_t col_pass_smem_impl(int group_table, int max_rpad, bool dog) {
     return (dog ? (size_t)kTY * 2 * kConvThreads * sizeof(float2) : 0) +
-           2 * (size_t)max_table * sizeof(float2) + row_table_bytes(max_rpad);
+           (size_t)group_table * sizeof(float2) + row_table_bytes(max_rpad);
+}
+
+// Which warps of a column-pass CTA pull rows kL2Ahead steps ahead into L2 (bit w = warp w).
+// Default: the warp with the highest row range, the first to touch new rows.
+unsigned frontier_warps() {
+    static const unsigned mask = [] {
+        const char *e = std::getenv("DOGBLOB_FRONTIER");
+        return e ? (unsigned)std::strtoul(e, nullptr, 0) : (1u << (kWarps - 1));
+    }();
+    return mask;
 }
 
 }  // namespace
 
-cudaError_t configure_conv_kernels(int max_table, int max_rpad) {
-    cudaError_t e;
-    e = cudaFuncSetAttribute(row_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)row_pass_smem(max_table, max_rpad));
+size_t col_pass_smem(int group_table, int max_rpad, bool dog) {
+    return col_pass_smem_impl(group_table, max_rpad, dog);
+}
+
+// Opt every convolution kernel in to the device's full shared-memory carve-out once; the
+// per-launch size is what the plan's geometry asks for.
+cudaError_t configure_conv_kernels(int device) {
+    int optin = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(col_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)col_pass_smem(max_table, max_rpad, true));
+    e = cudaFuncSetAttribute(row_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(col_pass_kernel<false>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)col_pass_smem(max_table, max_rpad, false));
+    e = cudaFuncSetAttribute(col_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(col_pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                optin);
 }
 
 cudaError_t launch_row_pass(const ConvGeometry &g, const float *d_img, float *d_rows_t,
                             const LevelTable &tbl, const float2 *d_taps, cudaStream_t st) {
     dim3 grid(g.Wp / kTileCols, g.Hp / kTileRows, g.L);
-    row_pass_kernel<<<grid, kConvThreads, row_pass_smem(g.max_table, g.max_rpad), st>>>(
-        d_img, g.Wp, g.H, d_rows_t, g.Hp, (int64_t)g.Hp * g.Wp, tbl, d_taps, g.max_table);
+    const size_t smem = row_pass_smem(g.max_table, g.max_rpad);
+    row_pass_kernel<<<grid, kConvThreads, smem, st>>>(d_img, g.Wp, g.H, d_rows_t, g.Hp,
+                                                      (int64_t)g.Hp * g.Wp, tbl, d_taps, g.max_table);
     return cudaGetLastError();
 }
 
@@ -422,8 +442,9 @@ cudaError_t launch_col_dog_pass(const ConvGeometry &g, const float *d_rows_t, fl
                                 cudaStream_t st) {
     dim3 grid(g.Hp / kTileCols, g.Wp / kTileRows, g.G);
     const int64_t plane = (int64_t)g.Hp * g.Wp;
-    col_pass_kernel<true><<<grid, kConvThreads, col_pass_smem(g.max_table, g.max_rpad, true), st>>>(
-        d_rows_t, g.Hp, plane, g.W, d_dog_t, d_edge, tbl, d_taps, g.max_table, g.max_rpad);
+    const size_t smem = col_pass_smem_impl(g.max_group_table, g.max_rpad, true);
+    col_pass_kernel<true><<<grid, kConvThreads, smem, st>>>(d_rows_t, g.Hp, plane, g.W, d_dog_t, d_edge,
+                                                            tbl, d_taps, g.max_rpad, frontier_warps());
     if (g.G > 1) {
         int bx = (int)((plane / 4 + 255) / 256);
         if (bx > 148 * 2) bx = 148 * 2;
@@ -436,9 +457,8 @@ cudaError_t launch_col_levels_pass(const ConvGeometry &g, const float *d_rows_t,
                                    const LevelTable &unit_tbl, const float2 *d_taps,
                                    cudaStream_t st) {
     dim3 grid(g.Hp / kTileCols, g.Wp / kTileRows, g.L);
-    col_pass_kernel<false><<<grid, kConvThreads, col_pass_smem(g.max_table, g.max_rpad, false), st>>>(
-        d_rows_t, g.Hp, (int64_t)g.Hp * g.Wp, g.W, d_lev_t, nullptr, unit_tbl, d_taps, g.max_table,
-        g.max_rpad);
+    col_pass_kernel<false><<<grid, kConvThreads, col_pass_smem_impl(g.max_table, g.max_rpad, false), st>>>(
+        d_rows_t, g.Hp, (int64_t)g.Hp * g.Wp, g.W, d_lev_t, nullptr, unit_tbl, d_taps, g.max_rpad, frontier_warps());
     return cudaGetLastError();
 }
 
