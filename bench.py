@@ -39,7 +39,7 @@ sys.path.insert(0, str(ROOT))
 
 WORKLOAD = "C2"
 BATCH = 16
-KERNELS_PER_FRAME = 11   # reset, row pass, column+DoG, edge DoG, nms, plateau, finalize_small, rank_sort, prune_build, prune_first, prune_loop
+KERNELS_PER_FRAME = 8    # reset, row pass, column+DoG, edge DoG, nms, plateau, finalize_small, prune_large
 
 
 def params_kw():

@@ -27,6 +27,7 @@ size_t blobspace_bytes(int cap) {
     b += align_up((size_t)(kMaxCells + 1) * sizeof(int), 256);
     b += align_up((size_t)kMaxCells * sizeof(int), 256);
     b += align_up(8 * sizeof(double), 256);
+    b += align_up(sizeof(PruneCtl), 256);
     return b;
 }
 
@@ -54,6 +55,7 @@ BlobSpace carve_blobspace(void *base, int cap) {
     bs.cell_start = reinterpret_cast<int *>(take((size_t)(kMaxCells + 1) * sizeof(int)));
     bs.cell_fill = reinterpret_cast<int *>(take((size_t)kMaxCells * sizeof(int)));
     bs.grid_params = reinterpret_cast<double *>(take(8 * sizeof(double)));
+    bs.ctl = reinterpret_cast<PruneCtl *>(take(sizeof(PruneCtl)));
     bs.cap = cap;
     return bs;
 }
@@ -98,7 +100,13 @@ std::vector<int> balance_groups(const std::vector<LevelDesc> &lv, int G) {
     const int L = (int)lv.size();
     G = std::max(1, std::min(G, L));
     std::vector<double> pre(L + 1, 0.0);
-    for (int i = 0; i < L; ++i) pre[i + 1] = pre[i] + lv[i].n_mid + 1.07;   // first+last chunk = 136/128 of a full one
+    // cost of a level in full-chunk units: middle chunks + head/tail (136/128 of a full one)
+    // + its fixed part (DoG epilogue, pipeline refill)
+    static const double fixed = [] {
+        const char *e = std::getenv("DOGBLOB_LEVEL_COST");
+        return e ? std::atof(e) : 1.07;
+    }();
+    for (int i = 0; i < L; ++i) pre[i + 1] = pre[i] + lv[i].n_mid + fixed;
     std::vector<int> begin(G + 1, 0);
     begin[G] = L;
     for (int g = 1; g < G; ++g) {

@@ -72,6 +72,20 @@ struct Counters {            // one per result, lives in the blob space
 
 struct Voxel { int s, row, col; float val; };
 
+// Device-side control block of prune_large_kernel (prune.cu): ticket dispenser, completion
+// counter and the log of published phases.
+constexpr int kMaxPhases = 128;
+struct PhaseRec { int type, first_item, n_items, pad; unsigned long long t_ns, pad2; };
+struct PruneCtl {
+    unsigned ticket, done;       // next work item / completed work items
+    int n_phases;                // published entries of phase[]
+    int changed, sweeps;         // radius-bound fixed point
+    int n_roots, merges, kept;
+    double ext[5];               // xmin, xmax, ymin, ymax, rmax of the candidates
+    double pad;
+    PhaseRec phase[kMaxPhases];
+};
+
 // Layout of the blob space (device), all arrays sized by `cap`.
 struct BlobSpace {
     Counters *ctr;
@@ -92,6 +106,7 @@ struct BlobSpace {
     int *cell_fill;              // kMaxCells
     int *cell_items;
     double *grid_params;         // [0]=x0 [1]=y0 [2]=cell size [3]=gx [4]=gy
+    PruneCtl *ctl;
     int cap;
 };
 
@@ -136,7 +151,6 @@ cudaError_t launch_prune_and_pack(const BlobSpace &bs, double overlap, bool prun
                                   void *d_result, int result_cap, cudaStream_t st);
 cudaError_t launch_load_blobs(const BlobSpace &bs, const dogblob_blob *d_in, int n,
                               cudaStream_t st);
-cudaError_t launch_rank_sort(const BlobSpace &bs, cudaStream_t st);
 cudaError_t configure_finalize_kernels();   // per device, before the first launch_prune_and_pack
 constexpr int kSmallMax = 1024;   // threads (and shared-memory slots) of the single-CTA finalize kernel
 int small_limit();                // frames with at most this many candidates finish in that one CTA

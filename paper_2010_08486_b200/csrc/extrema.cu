@@ -289,50 +289,13 @@ plateau_kernel(BlobSpace bs, int S, bool transposed, const double *__restrict__ 
 }
 
 // ---- ordering: rank sort on the full key (stable on the input index) ----------------
-struct SortKey { double resp, y, x, sigma; };
-
-__device__ __forceinline__ bool key_before(const SortKey &a, int ia, const SortKey &b, int ib) {
-    // sorted(key=(-response, y, x, sigma)); ties keep input order
-    if (a.resp != b.resp) return a.resp > b.resp;
-    if (a.y != b.y) return a.y < b.y;
-    if (a.x != b.x) return a.x < b.x;
-    if (a.sigma != b.sigma) return a.sigma < b.sigma;
-    return ia < ib;
-}
-
-__global__ void __launch_bounds__(256) rank_sort_kernel(BlobSpace bs) {
-    if (bs.ctr->small_done) return;
-    const int n = min(bs.ctr->n_candidates, bs.cap);
-    __shared__ SortKey tile[256];
-    for (int i0 = blockIdx.x * blockDim.x; i0 < n; i0 += gridDim.x * blockDim.x) {
-        const int i = i0 + threadIdx.x;
-        dogblob_blob me;
-        SortKey mk = {0, 0, 0, 0};
-        if (i < n) {
-            me = bs.unsorted[i];
-            mk = SortKey{me.response, me.y, me.x, me.sigma};
-        }
-        int rank = 0;
-        for (int j0 = 0; j0 < n; j0 += blockDim.x) {
-            __syncthreads();
-            if (j0 + (int)threadIdx.x < n) {
-                const dogblob_blob o = bs.unsorted[j0 + threadIdx.x];
-                tile[threadIdx.x] = SortKey{o.response, o.y, o.x, o.sigma};
-            }
-            __syncthreads();
-            const int lim = min((int)blockDim.x, n - j0);
-            if (i < n)
-                for (int k = 0; k < lim; ++k) rank += key_before(tile[k], j0 + k, mk, i) ? 1 : 0;
-        }
-        if (i < n) bs.sorted[rank] = me;
-    }
-}
-
 __global__ void reset_counters_kernel(BlobSpace bs) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         Counters z = {};
         *bs.ctr = z;
     }
+    // ticket, done, n_phases, changed, sweeps, n_roots, merges, kept of the pruning control block
+    if (blockIdx.x == 0 && threadIdx.x < 8) reinterpret_cast<int *>(bs.ctl)[threadIdx.x] = 0;
 }
 
 __global__ void load_blobs_kernel(BlobSpace bs, const dogblob_blob *__restrict__ in, int n) {
@@ -354,11 +317,6 @@ cudaError_t launch_load_blobs(const BlobSpace &bs, const dogblob_blob *d_in, int
     if (blocks < 1) blocks = 1;
     if (blocks > 296) blocks = 296;
     load_blobs_kernel<<<blocks, 256, 0, st>>>(bs, d_in, n);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_rank_sort(const BlobSpace &bs, cudaStream_t st) {
-    rank_sort_kernel<<<296, 256, 0, st>>>(bs);
     return cudaGetLastError();
 }
 

@@ -20,7 +20,6 @@ namespace dogblob {
 
 namespace {
 
-constexpr int kLoopThreads = 1024;
 constexpr double kPi = 3.141592653589793;
 constexpr double kSqrt2 = 1.4142135623730951;
 
@@ -65,16 +64,6 @@ struct Grid {
     }
 };
 
-__device__ __forceinline__ Grid load_grid(const BlobSpace &bs) {
-    Grid g;
-    g.x0 = bs.grid_params[0];
-    g.y0 = bs.grid_params[1];
-    g.cell = bs.grid_params[2];
-    g.gx = (int)bs.grid_params[3];
-    g.gy = (int)bs.grid_params[4];
-    return g;
-}
-
 template <typename T, typename Op>
 __device__ T block_reduce(T v, Op op, T *scratch /* >= 33 */) {
     for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -92,132 +81,147 @@ __device__ T block_reduce(T v, Op op, T *scratch /* >= 33 */) {
     return scratch[32];
 }
 
-// ---- build the grid (single CTA): extents, cell size, counting sort -------------------
-__global__ void __launch_bounds__(kLoopThreads) prune_build_kernel(BlobSpace bs) {
-    if (bs.ctr->small_done) return;
-    __shared__ double sd[33];
-    __shared__ int si[33];
-    const int n = min(bs.ctr->n_candidates, bs.cap);
-    const int tid = threadIdx.x;
-    double xmin = DBL_MAX, xmax = -DBL_MAX, ymin = DBL_MAX, ymax = -DBL_MAX, rmax = 0.0;
-    for (int i = tid; i < n; i += blockDim.x) {
-        const dogblob_blob b = bs.sorted[i];
-        xmin = fmin(xmin, b.x); xmax = fmax(xmax, b.x);
-        ymin = fmin(ymin, b.y); ymax = fmax(ymax, b.y);
-        rmax = fmax(rmax, b.radius);
-        bs.alive[i] = 1;
-        bs.first[i] = -1;
+// =========================================================================================
+// Frames above the single-CTA limit: ONE whole-GPU kernel, phases chained on the device.
+//
+// The work is a sequence of phases (order the candidates, bucket them, first partners,
+// radius bounds, parts, per-part merge loops, packing); how many bound sweeps are needed and
+// how many parts exist is only known on the device.  Work items of all phases are numbered
+// in one global order and handed out by an atomic ticket; phase k+1 is *published* (type,
+// first item, item count) by the CTA that completes the last item of phase k, so the
+// publication doubles as a grid-wide barrier.  A CTA only ever waits for items with smaller
+// tickets, and every ticket is held by a CTA that is already running: no co-residency
+// assumption, no cooperative launch, no host round trip, and a frame that finished in
+// finalize_small_kernel costs one immediate return.
+//
+// Everything that another SM may have written earlier in this kernel is read through L2
+// (ld.global.cg): L1 is not coherent across SMs and several arrays are re-used between phases.
+
+enum PhaseType : int {
+    PH_RANK = 0, PH_SCATTER, PH_COUNT, PH_SCAN, PH_FILL, PH_FIRST, PH_SWEEP, PH_SATURATE, PH_UNION,
+    PH_LINK, PH_MERGE, PH_PACK_COUNT, PH_PACK_WRITE, PH_END
+};
+
+constexpr int kLargeThreads = 256;
+constexpr int kItemBlobs = 256;       // thread-per-blob phases
+constexpr int kRankParts = 8;         // a candidate's rank is the sum of <= 8 partial ranks
+constexpr int kWarpBlobs = 32;        // warp-per-blob phases: 4 blobs per warp
+constexpr int kPackBlobs = 1024;      // 4 per thread
+constexpr int kMaxSweeps = 96;
+
+__device__ __forceinline__ int ldcg_i(const int *p) { return __ldcg(p); }
+__device__ __forceinline__ dogblob_blob ldcg_blob(const dogblob_blob *p) {
+    union { int4 q[3]; dogblob_blob b; } u;
+    const int4 *s = reinterpret_cast<const int4 *>(p);
+    u.q[0] = __ldcg(s); u.q[1] = __ldcg(s + 1); u.q[2] = __ldcg(s + 2);
+    return u.b;
+}
+__device__ __forceinline__ double ldcg_d(const double *p) { return __ldcg(p); }
+__device__ __forceinline__ double ldcg_bound(const BlobSpace &bs, int i) {
+    return __longlong_as_double((long long)__ldcg(bs.bound + i));
+}
+__device__ __forceinline__ unsigned long long now_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ void atomic_min_double(double *addr, double v) {
+    unsigned long long *a = reinterpret_cast<unsigned long long *>(addr);
+    unsigned long long old = *a;
+    while (v < __longlong_as_double((long long)old)) {
+        const unsigned long long seen = atomicCAS(a, old, (unsigned long long)__double_as_longlong(v));
+        if (seen == old) break;
+        old = seen;
     }
-    auto fmn = [](double a, double b) { return fmin(a, b); };
-    auto fmx = [](double a, double b) { return fmax(a, b); };
-    xmin = block_reduce(xmin, fmn, sd); xmax = block_reduce(xmax, fmx, sd);
-    ymin = block_reduce(ymin, fmn, sd); ymax = block_reduce(ymax, fmx, sd);
-    rmax = block_reduce(rmax, fmx, sd);
-    if (n == 0) { xmin = ymin = 0.0; xmax = ymax = 1.0; }
-    double cell = fmax(2.0 * rmax, 1e-9) * 1.0000001;   // strictly covers d < r_i + r_j
-    cell = fmax(cell, fmax(xmax - xmin, ymax - ymin) / (double)(kMaxCellsPerAxis - 1));
-    const int gx = min(kMaxCellsPerAxis, (int)floor((xmax - xmin) / cell) + 1);
-    const int gy = min(kMaxCellsPerAxis, (int)floor((ymax - ymin) / cell) + 1);
-    if (tid == 0) {
-        bs.grid_params[0] = xmin; bs.grid_params[1] = ymin; bs.grid_params[2] = cell;
-        bs.grid_params[3] = (double)gx; bs.grid_params[4] = (double)gy;
-    }
-    Grid g{xmin, ymin, cell, gx, gy};
-    const int ncell = gx * gy;
-    for (int c = tid; c <= ncell; c += blockDim.x) bs.cell_start[c] = 0;
-    for (int c = tid; c < ncell; c += blockDim.x) bs.cell_fill[c] = 0;
-    __syncthreads();
-    for (int i = tid; i < n; i += blockDim.x) {
-        const dogblob_blob b = bs.sorted[i];
-        const int c = g.cy(b.y) * gx + g.cx(b.x);
-        bs.cell_of[i] = c;
-        atomicAdd(&bs.cell_start[c + 1], 1);
-    }
-    __syncthreads();
-    // inclusive scan of cell_start[1..ncell] in chunks of blockDim.x
-    __shared__ int carry;
-    if (tid == 0) carry = 0;
-    __syncthreads();
-    for (int c0 = 1; c0 <= ncell; c0 += blockDim.x) {
-        const int c = c0 + tid;
-        int v = (c <= ncell) ? bs.cell_start[c] : 0;
-        const int lane = tid & 31, w = tid >> 5;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v += t;
-        }
-        if (lane == 31) si[w] = v;
-        __syncthreads();
-        if (w == 0) {
-            int t = si[lane];
-            for (int o = 1; o < 32; o <<= 1) {
-                const int u = __shfl_up_sync(0xffffffffu, t, o);
-                if (lane >= o) t += u;
-            }
-            si[lane] = t;
-        }
-        __syncthreads();
-        const int prefix = carry + (w > 0 ? si[w - 1] : 0);
-        if (c <= ncell) bs.cell_start[c] = v + prefix;
-        __syncthreads();
-        if (tid == blockDim.x - 1) carry = v + prefix;
-        __syncthreads();
-    }
-    for (int i = tid; i < n; i += blockDim.x) {
-        const int c = bs.cell_of[i];
-        const int slot = bs.cell_start[c] + atomicAdd(&bs.cell_fill[c], 1);
-        bs.cell_items[slot] = i;
+}
+__device__ void atomic_max_double(double *addr, double v) {
+    unsigned long long *a = reinterpret_cast<unsigned long long *>(addr);
+    unsigned long long old = *a;
+    while (v > __longlong_as_double((long long)old)) {
+        const unsigned long long seen = atomicCAS(a, old, (unsigned long long)__double_as_longlong(v));
+        if (seen == old) break;
+        old = seen;
     }
 }
 
-// smallest alive j > i (or, with below=true, test only partner `only`) offending with i
-__device__ int scan_first_partner(const BlobSpace &bs, const Grid &g, int i, double thr,
-                                  int t, int nt) {
-    const dogblob_blob bi = bs.sorted[i];
-    const int cx = g.cx(bi.x), cy = g.cy(bi.y);
+__device__ __forceinline__ Grid load_grid_cg(const BlobSpace &bs) {
+    Grid g;
+    g.x0 = ldcg_d(bs.grid_params + 0);
+    g.y0 = ldcg_d(bs.grid_params + 1);
+    g.cell = ldcg_d(bs.grid_params + 2);
+    g.gx = (int)ldcg_d(bs.grid_params + 3);
+    g.gy = (int)ldcg_d(bs.grid_params + 4);
+    return g;
+}
+
+struct SortKey { double resp, y, x, sigma; };
+__device__ __forceinline__ bool key_before(const SortKey &a, int ia, const SortKey &b, int ib) {
+    // sorted(key=(-response, y, x, sigma)); ties keep input order
+    if (a.resp != b.resp) return a.resp > b.resp;
+    if (a.y != b.y) return a.y < b.y;
+    if (a.x != b.x) return a.x < b.x;
+    if (a.sigma != b.sigma) return a.sigma < b.sigma;
+    return ia < ib;
+}
+
+// the geometric part of a record: x, y (first 16 bytes) and sigma, radius (next 16)
+struct XYR { double x, y, r; };
+__device__ __forceinline__ XYR ldcg_xyr(const dogblob_blob *p) {
+    const int4 *s = reinterpret_cast<const int4 *>(p);
+    const int4 a = __ldcg(s), b = __ldcg(s + 1);
+    XYR o;
+    o.x = __longlong_as_double(((long long)(unsigned)a.y << 32) | (unsigned)a.x);
+    o.y = __longlong_as_double(((long long)(unsigned)a.w << 32) | (unsigned)a.z);
+    o.r = __longlong_as_double(((long long)(unsigned)b.w << 32) | (unsigned)b.z);
+    return o;
+}
+__device__ __forceinline__ double2 ldcg_xy(const dogblob_blob *p) {
+    const int4 a = __ldcg(reinterpret_cast<const int4 *>(p));
+    return make_double2(__longlong_as_double(((long long)(unsigned)a.y << 32) | (unsigned)a.x),
+                        __longlong_as_double(((long long)(unsigned)a.w << 32) | (unsigned)a.z));
+}
+
+// Visit every blob bucketed in the 3 x 3 cells around (cx, cy).  The three cells of one grid
+// row are adjacent in cell order, so their items are ONE contiguous range of cell_items: the
+// warp splits into three lane groups (lane % 3 = row), each striding its row's range, and a
+// typical neighbourhood is covered in a single step.  f(k) is called with a blob index.
+template <typename F>
+__device__ __forceinline__ void for_neighbours_warp(const BlobSpace &bs, const Grid &g, int cx, int cy,
+                                                    int lane, F f) {
+    const int row = lane % 3, t = lane / 3, nt = row < 2 ? 11 : 10;
+    const int yy = cy - 1 + row;
+    if (yy < 0 || yy >= g.gy) return;
+    const int c0 = yy * g.gx + max(cx - 1, 0), c1 = yy * g.gx + min(cx + 1, g.gx - 1);
+    const int e = ldcg_i(bs.cell_start + c1 + 1);
+    for (int p = ldcg_i(bs.cell_start + c0) + t; p < e; p += nt) f(ldcg_i(bs.cell_items + p));
+}
+
+// smallest alive j > i offending with i (whole warp)
+__device__ int scan_first_partner(const BlobSpace &bs, const Grid &g, int i, double thr, int lane) {
+    const XYR bi = ldcg_xyr(bs.sorted + i);
     int best = INT_MAX;
-    for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.gy - 1); ++yy)
-        for (int xx = max(cx - 1, 0); xx <= min(cx + 1, g.gx - 1); ++xx) {
-            const int c = yy * g.gx + xx;
-            const int e = bs.cell_start[c + 1];
-            for (int p = bs.cell_start[c] + t; p < e; p += nt) {
-                const int j = bs.cell_items[p];
-                if (j <= i || j >= best || !(bs.alive[j] & 1)) continue;
-                const dogblob_blob bj = bs.sorted[j];
-                if (overlap_ij(bi.x, bi.y, bi.radius, bj.x, bj.y, bj.radius) > thr) best = j;
-            }
-        }
+    for_neighbours_warp(bs, g, g.cx(bi.x), g.cy(bi.y), lane, [&](int j) {
+        if (j <= i || j >= best || !(ldcg_i(bs.alive + j) & 1)) return;
+        const XYR bj = ldcg_xyr(bs.sorted + j);
+        if (overlap_ij(bi.x, bi.y, bi.r, bj.x, bj.y, bj.r) > thr) best = j;
+    });
+    for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
     return best;
 }
 
-// ---- first[i] for every blob: one warp per blob, whole GPU ---------------------------
-__global__ void __launch_bounds__(256) prune_first_kernel(BlobSpace bs, double thr) {
-    if (bs.ctr->small_done) return;
-    const int n = min(bs.ctr->n_candidates, bs.cap);
-    if (n < 2) return;
-    const Grid g = load_grid(bs);
-    const int lane = threadIdx.x & 31;
-    const int warps = (gridDim.x * blockDim.x) >> 5;
-    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
-        int best = scan_first_partner(bs, g, i, thr, lane, 32);
-        for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
-        if (lane == 0) bs.first[i] = (best == INT_MAX) ? -1 : best;
-    }
-}
-
-// ---- merge loop + final packing (single persistent CTA) -----------------------------------
 // The reference's loop is sequential, but merges only interact through blobs that can
 // overlap.  ub(a) bounds every radius blob a can ever take: a's radius only changes when a
 // (the lower index) absorbs some b > a and becomes the mean, so
 //     ub(a) = max(r_a, max{ ub(b) : b > a, dist(a, b) < ub(a) + ub(b) }),
-// taken as the least fixed point from below.  By induction no merge ever joins blobs that
-// are not linked by "dist < ub(a) + ub(b)", so the connected parts of that graph evolve
-// independently and the global row-major-first order restricted to a part is that part's
-// own sequential order: each round merges the smallest offending row of EVERY part at once
-// (one warp per row).  Rounds = longest merge chain of a part, not the number of merges.
+// taken as the least fixed point from below (monotone in-place sweeps until one full sweep
+// changes nothing; any pre-fixed point, e.g. the global r_max everywhere, is a valid
+// fallback).  By induction no merge ever joins blobs that are not linked by
+// "dist < ub(a) + ub(b)", so the connected parts of that graph evolve independently and the
+// global row-major-first order restricted to a part is that part's own sequential order:
+// one warp replays each part's merge loop on its own, all parts at once.
 __device__ __forceinline__ int comp_find(int *comp, int x) {
-    int p = ((volatile int *)comp)[x];
-    while (p != x) { x = p; p = ((volatile int *)comp)[x]; }
+    int p = __ldcg(comp + x);
+    while (p != x) { x = p; p = __ldcg(comp + x); }
     return x;
 }
 __device__ void comp_union(int *comp, int a, int b) {
@@ -230,22 +234,18 @@ __device__ void comp_union(int *comp, int a, int b) {
     }
 }
 
-__device__ __forceinline__ double ub_of(const BlobSpace &bs, int i) {
-    return __longlong_as_double((long long)((volatile unsigned long long *)bs.bound)[i]);
-}
-
-// rows with an offending partner live in a compact list (bit 1 of alive[] = "listed")
-__device__ __forceinline__ void list_row(const BlobSpace &bs, int k, int *s_len) {
-    if (!(atomicOr(&bs.alive[k], 2) & 2)) bs.cell_of[atomicAdd(s_len, 1)] = k;
+// offending rows of a part live in a linked list: head in cmin[root], links in cell_of[]
+// (free after the grid is built); bit 1 of alive[] = "listed"
+__device__ __forceinline__ void list_push(const BlobSpace &bs, int root, int k) {
+    if (!(atomicOr(&bs.alive[k], 2) & 2)) bs.cell_of[k] = atomicExch(&bs.cmin[root], k);
 }
 
 // one warp merges row i with its first partner and repairs the cached partners around it
-__device__ void merge_row(const BlobSpace &bs, const Grid &g, int i, double thr, int lane,
-                          int *s_len) {
-    const int j = bs.first[i];
+__device__ void merge_row(const BlobSpace &bs, const Grid &g, int root, int i, double thr, int lane) {
+    const int j = ldcg_i(bs.first + i);
     if (lane == 0) {
-        dogblob_blob a = bs.sorted[i];
-        const dogblob_blob w = bs.sorted[j];
+        dogblob_blob a = ldcg_blob(bs.sorted + i);
+        const dogblob_blob w = ldcg_blob(bs.sorted + j);
         const double nr = 0.5 * (a.radius + w.radius);
         a.radius = nr;
         a.sigma = nr / kSqrt2;
@@ -253,211 +253,492 @@ __device__ void merge_row(const BlobSpace &bs, const Grid &g, int i, double thr,
         a.slice = -1;
         bs.sorted[i] = a;
         bs.alive[j] = 0;
+        __threadfence();
     }
     __syncwarp();
-    const dogblob_blob bi = bs.sorted[i];
-    const dogblob_blob bj = bs.sorted[j];
+    const XYR bi = ldcg_xyr(bs.sorted + i);
+    const double2 bj = ldcg_xy(bs.sorted + j);
     // (a) first[i] again; (b) rows k < i of this part had no partner and can only gain i
     int best = INT_MAX;
-    {
-        const int cx = g.cx(bi.x), cy = g.cy(bi.y);
-        for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.gy - 1); ++yy)
-            for (int xx = max(cx - 1, 0); xx <= min(cx + 1, g.gx - 1); ++xx) {
-                const int c = yy * g.gx + xx;
-                const int e = bs.cell_start[c + 1];
-                for (int p = bs.cell_start[c] + lane; p < e; p += 32) {
-                    const int k = bs.cell_items[p];
-                    if (k == i || !(bs.alive[k] & 1)) continue;
-                    const dogblob_blob bk = bs.sorted[k];
-                    if (k > i) {
-                        if (k < best && overlap_ij(bi.x, bi.y, bi.radius, bk.x, bk.y, bk.radius) > thr)
-                            best = k;
-                    } else if (overlap_ij(bk.x, bk.y, bk.radius, bi.x, bi.y, bi.radius) > thr) {
-                        bs.first[k] = i;
-                        list_row(bs, k, s_len);
-                    }
-                }
-            }
-    }
+    for_neighbours_warp(bs, g, g.cx(bi.x), g.cy(bi.y), lane, [&](int k) {
+        if (k == i || !(ldcg_i(bs.alive + k) & 1)) return;
+        const XYR bk = ldcg_xyr(bs.sorted + k);
+        if (k > i) {
+            if (k < best && overlap_ij(bi.x, bi.y, bi.r, bk.x, bk.y, bk.r) > thr) best = k;
+        } else if (overlap_ij(bk.x, bk.y, bk.r, bi.x, bi.y, bi.r) > thr) {
+            bs.first[k] = i;
+            list_push(bs, root, k);
+        }
+    });
     for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
     if (lane == 0) bs.first[i] = (best == INT_MAX) ? -1 : best;
-    // (c) rows that pointed at the deleted blob need a new partner
+    // (c) rows that pointed at the deleted blob need a new partner: collect them (ballot per
+    // grid row of the neighbourhood), then the whole warp rescans each
     {
         const int cx = g.cx(bj.x), cy = g.cy(bj.y);
-        for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.gy - 1); ++yy)
-            for (int xx = max(cx - 1, 0); xx <= min(cx + 1, g.gx - 1); ++xx) {
-                const int c = yy * g.gx + xx;
-                const int s0 = bs.cell_start[c], e = bs.cell_start[c + 1];
-                for (int p0 = s0; p0 < e; p0 += 32) {
-                    const int p = p0 + lane;
-                    const int k = p < e ? bs.cell_items[p] : -1;
-                    const bool hit = k >= 0 && k != i && (bs.alive[k] & 1) && bs.first[k] == j;
-                    unsigned m = __ballot_sync(0xffffffffu, hit);
-                    while (m) {
-                        const int src = __ffs(m) - 1;
-                        m &= m - 1;
-                        const int kk = __shfl_sync(0xffffffffu, k, src);
-                        int b2 = scan_first_partner(bs, g, kk, thr, lane, 32);
-                        for (int o = 16; o > 0; o >>= 1)
-                            b2 = min(b2, __shfl_xor_sync(0xffffffffu, b2, o));
-                        if (lane == 0) bs.first[kk] = (b2 == INT_MAX) ? -1 : b2;   // kk stays listed
-                    }
+        for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.gy - 1); ++yy) {
+            const int s0 = ldcg_i(bs.cell_start + yy * g.gx + max(cx - 1, 0));
+            const int e = ldcg_i(bs.cell_start + yy * g.gx + min(cx + 1, g.gx - 1) + 1);
+            for (int p0 = s0; p0 < e; p0 += 32) {
+                const int p = p0 + lane;
+                const int k = p < e ? ldcg_i(bs.cell_items + p) : -1;
+                const bool hit = k >= 0 && k != i && (ldcg_i(bs.alive + k) & 1) &&
+                                 ldcg_i(bs.first + k) == j;
+                unsigned m = __ballot_sync(0xffffffffu, hit);
+                while (m) {
+                    const int src = __ffs(m) - 1;
+                    m &= m - 1;
+                    const int kk = __shfl_sync(0xffffffffu, k, src);
+                    const int b2 = scan_first_partner(bs, g, kk, thr, lane);
+                    if (lane == 0) bs.first[kk] = (b2 == INT_MAX) ? -1 : b2;   // kk stays listed
                 }
             }
+        }
+    }
+    __threadfence();
+    __syncwarp();
+}
+
+// the whole merge loop of one part, by one warp: repeatedly the smallest listed row that is
+// alive and still has a partner; rows that lost their partner are unlinked on the way
+__device__ int merge_part(const BlobSpace &bs, const Grid &g, int root, double thr, int lane) {
+    int merges = 0;
+    while (true) {
+        int best = INT_MAX;
+        if (lane == 0) {
+            int prev = -1;
+            int e = ldcg_i(bs.cmin + root);
+            while (e >= 0) {
+                const int nxt = ldcg_i(bs.cell_of + e);
+                if ((ldcg_i(bs.alive + e) & 1) && ldcg_i(bs.first + e) >= 0) {
+                    best = min(best, e);
+                    prev = e;
+                } else {                               // unlink; it may be pushed again later
+                    if (prev < 0) bs.cmin[root] = nxt; else bs.cell_of[prev] = nxt;
+                    atomicAnd(&bs.alive[e], ~2);
+                }
+                e = nxt;
+            }
+            __threadfence();
+        }
+        best = __shfl_sync(0xffffffffu, best, 0);
+        if (best == INT_MAX) break;
+        merge_row(bs, g, root, best, thr, lane);
+        ++merges;
+    }
+    return merges;
+}
+
+// ranking: the j range is cut into nj <= kRankParts chunks (multiples of 256)
+__device__ __forceinline__ int rank_chunk(int n) {
+    const int per = (n + kRankParts - 1) / kRankParts;
+    return max(kItemBlobs, (per + kItemBlobs - 1) / kItemBlobs * kItemBlobs);
+}
+__device__ int phase_items(int type, int n, int n_roots) {
+    switch (type) {
+        case PH_RANK: {
+            const int cj = rank_chunk(n);
+            return ((n + kItemBlobs - 1) / kItemBlobs) * ((n + cj - 1) / cj);
+        }
+        case PH_SCAN: return 1;
+        case PH_FIRST: case PH_SWEEP: case PH_UNION: return (n + kWarpBlobs - 1) / kWarpBlobs;
+        case PH_MERGE: return (n_roots + 7) / 8;
+        case PH_PACK_COUNT: case PH_PACK_WRITE: return (n + kPackBlobs - 1) / kPackBlobs;
+        default: return (n + kItemBlobs - 1) / kItemBlobs;
     }
 }
 
-__global__ void __launch_bounds__(kLoopThreads)
-prune_loop_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_header *hdr,
-                  dogblob_blob *out, int out_cap) {
+__global__ void __launch_bounds__(kLargeThreads)
+prune_large_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_header *hdr,
+                   dogblob_blob *out, int out_cap) {
     if (bs.ctr->small_done) return;
-    __shared__ int s_red[33];
-    __shared__ int s_flag, s_nact, s_len, s_carry;
-    __shared__ int s_act[kLoopThreads];
+    PruneCtl *ctl = bs.ctl;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = min(bs.ctr->n_candidates, bs.cap);
-    int merges = 0;
+    __shared__ int s_type, s_item, s_count, s_last;
+    __shared__ double sd[33];
+    __shared__ int si[33];
+    __shared__ SortKey s_keys[kItemBlobs];
+    const bool pruning = do_prune && n >= 2;
+    int cur = 0;                                   // phase this CTA looks at (thread 0)
+    int ph_first = 0, ph_count = 0, ph_type = PH_RANK;
 
-    if (do_prune && n >= 2) {
-        const Grid g = load_grid(bs);
-        // ---- ub(): least fixed point from below (Jacobi sweeps over the grid neighbourhoods) ----
-        if (tid == 0) s_len = 0;
-        for (int i = tid; i < n; i += blockDim.x) {
-            bs.comp[i] = i;
-            bs.cmin[i] = INT_MAX;
-            bs.bound[i] = (unsigned long long)__double_as_longlong(bs.sorted[i].radius);
-        }
-        __syncthreads();
-        while (true) {
-            if (tid == 0) s_flag = 0;
-            __syncthreads();
-            for (int i = tid; i < n; i += blockDim.x) {
-                const dogblob_blob bi = bs.sorted[i];
-                double ui = ub_of(bs, i);
-                const int cx = g.cx(bi.x), cy = g.cy(bi.y);
-                bool grew = false;
-                for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.gy - 1); ++yy)
-                    for (int xx = max(cx - 1, 0); xx <= min(cx + 1, g.gx - 1); ++xx) {
-                        const int c = yy * g.gx + xx;
-                        const int e = bs.cell_start[c + 1];
-                        for (int p = bs.cell_start[c]; p < e; ++p) {
-                            const int j = bs.cell_items[p];
-                            if (j <= i) continue;
-                            const double uj = ub_of(bs, j);
-                            if (uj <= ui) continue;
-                            const dogblob_blob bj = bs.sorted[j];
-                            const double dx = bi.x - bj.x, dy = bi.y - bj.y, reach = ui + uj;
-                            if (dx * dx + dy * dy < reach * reach * 1.0000001 + 1e-9) {
-                                ui = uj;
-                                grew = true;
-                            }
-                        }
-                    }
-                if (grew) {
-                    bs.bound[i] = (unsigned long long)__double_as_longlong(ui);
-                    s_flag = 1;
-                }
+    while (true) {
+        // ---- take a ticket, find its phase (waiting for the publication = grid barrier) ----
+        if (tid == 0) {
+            const int t = (int)atomicAdd(&ctl->ticket, 1u);
+            if (t == 0) {                          // the first ticket publishes phase 0
+                ctl->phase[0].type = n > 0 ? PH_RANK : PH_PACK_WRITE;
+                ctl->phase[0].first_item = 0;
+                ctl->phase[0].n_items = n > 0 ? phase_items(PH_RANK, n, 0) : 1;
+                ctl->ext[0] = DBL_MAX; ctl->ext[1] = -DBL_MAX;
+                ctl->ext[2] = DBL_MAX; ctl->ext[3] = -DBL_MAX; ctl->ext[4] = 0.0;
+                ctl->phase[0].t_ns = now_ns();
+                __threadfence();
+                *(volatile int *)&ctl->n_phases = 1;
             }
-            __syncthreads();
-            const int changed = s_flag;
-            __syncthreads();
-            if (!changed) break;
-        }
-        // ---- parts: connected components of dist < ub(a) + ub(b) ----
-        for (int i = tid; i < n; i += blockDim.x) {
-            const dogblob_blob bi = bs.sorted[i];
-            const double ui = ub_of(bs, i);
-            const int cx = g.cx(bi.x), cy = g.cy(bi.y);
-            for (int yy = max(cy - 1, 0); yy <= min(cy + 1, g.gy - 1); ++yy)
-                for (int xx = max(cx - 1, 0); xx <= min(cx + 1, g.gx - 1); ++xx) {
-                    const int c = yy * g.gx + xx;
-                    const int e = bs.cell_start[c + 1];
-                    for (int p = bs.cell_start[c]; p < e; ++p) {
-                        const int j = bs.cell_items[p];
-                        if (j <= i) continue;
-                        const dogblob_blob bj = bs.sorted[j];
-                        const double dx = bi.x - bj.x, dy = bi.y - bj.y, reach = ui + ub_of(bs, j);
-                        if (dx * dx + dy * dy < reach * reach * 1.0000001 + 1e-9)
-                            comp_union(bs.comp, i, j);
-                    }
-                }
+            int type;
+            while (true) {
+                while (*(volatile int *)&ctl->n_phases <= cur) __nanosleep(40);
+                __threadfence();
+                type = __ldcg(&ctl->phase[cur].type);
+                ph_first = __ldcg(&ctl->phase[cur].first_item);
+                ph_count = __ldcg(&ctl->phase[cur].n_items);
+                if (type == PH_END || t < ph_first + ph_count) break;
+                ++cur;
+            }
+            ph_type = type;
+            s_type = type;
+            s_item = t - ph_first;
+            s_count = ph_count;
         }
         __syncthreads();
-        for (int i = tid; i < n; i += blockDim.x) bs.comp[i] = comp_find(bs.comp, i);
-        __syncthreads();
-        for (int i = tid; i < n; i += blockDim.x)
-            if (bs.first[i] >= 0) list_row(bs, i, &s_len);
-        __syncthreads();
+        const int type = s_type, item = s_item, ph_count_all = s_count;
+        if (type == PH_END) return;
 
-        // ---- rounds: the smallest offending row of every part, all parts at once ----
-        while (true) {
-            if (tid == 0) s_nact = 0;
-            __syncthreads();
-            const int len = s_len;
-            for (int q = tid; q < len; q += blockDim.x) {
-                const int i = bs.cell_of[q];
-                if ((bs.alive[i] & 1) && bs.first[i] >= 0) atomicMin(&bs.cmin[bs.comp[i]], i);
+        // ---- the item ----
+        switch (type) {
+        case PH_RANK: {
+            // partial rank of candidate i against j chunk jb; the partials live in eight arrays
+            // that are free at this point.  The cell counters are cleared on the side.
+            int *const part[kRankParts] = {bs.first, bs.alive, bs.comp, bs.cmin,
+                                           bs.cell_of, bs.cell_items, bs.pl_count, bs.parent};
+            const int cj = rank_chunk(n);
+            const int nj = (n + cj - 1) / cj;
+            const int ib = item / nj, jb = item % nj;
+            const int i = ib * kItemBlobs + tid;
+            SortKey mk = {0, 0, 0, 0};
+            if (i < n) {
+                const dogblob_blob me = ldcg_blob(bs.unsorted + i);
+                mk = SortKey{me.response, me.y, me.x, me.sigma};
             }
-            __syncthreads();
-            for (int q = tid; q < len; q += blockDim.x) {
-                const int i = bs.cell_of[q];
-                if ((bs.alive[i] & 1) && bs.first[i] >= 0 && bs.cmin[bs.comp[i]] == i) {
-                    bs.cmin[bs.comp[i]] = INT_MAX;
-                    const int slot = atomicAdd(&s_nact, 1);
-                    if (slot < kLoopThreads) s_act[slot] = i;   // the rest wait for the next round
+            int rank = 0;
+            const int jend = min(n, (jb + 1) * cj);
+            for (int j0 = jb * cj; j0 < jend; j0 += kItemBlobs) {
+                __syncthreads();
+                if (j0 + tid < jend) {
+                    const dogblob_blob o = ldcg_blob(bs.unsorted + j0 + tid);
+                    s_keys[tid] = SortKey{o.response, o.y, o.x, o.sigma};
                 }
+                __syncthreads();
+                const int lim = min(kItemBlobs, jend - j0);
+                if (i < n)
+                    for (int k = 0; k < lim; ++k) rank += key_before(s_keys[k], j0 + k, mk, i) ? 1 : 0;
             }
-            __syncthreads();
-            const int nact = min(s_nact, kLoopThreads);
-            if (nact == 0) break;
-            for (int q = warp; q < nact; q += (blockDim.x >> 5))
-                merge_row(bs, g, s_act[q], thr, lane, &s_len);
-            merges += nact;
-            __syncthreads();
+            if (i < n) part[jb][i] = rank;
+            if (pruning)
+                for (int c = item * kLargeThreads + tid; c <= kMaxCells; c += ph_count_all * kLargeThreads) {
+                    bs.cell_start[c] = 0;
+                    if (c < kMaxCells) bs.cell_fill[c] = 0;
+                }
+            break;
         }
-    }
-
-    // ---- pack survivors in order ------------------------------------------------------
-    __syncthreads();
-    if (tid == 0) s_carry = 0;
-    __syncthreads();
-    for (int base = 0; base < n; base += blockDim.x) {
-        const int i = base + tid;
-        const int keep = (i < n) && (!do_prune || n < 2 || (bs.alive[i] & 1));
-        int v = keep;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v += t;
+        case PH_SCATTER: {
+            int *const part[kRankParts] = {bs.first, bs.alive, bs.comp, bs.cmin,
+                                           bs.cell_of, bs.cell_items, bs.pl_count, bs.parent};
+            const int cj = rank_chunk(n);
+            const int nj = (n + cj - 1) / cj;
+            const int i = item * kItemBlobs + tid;
+            double xmin = DBL_MAX, xmax = -DBL_MAX, ymin = DBL_MAX, ymax = -DBL_MAX, rmax = 0.0;
+            if (i < n) {
+                const dogblob_blob b = ldcg_blob(bs.unsorted + i);
+                int rank = 0;
+                for (int q = 0; q < nj; ++q) rank += ldcg_i(part[q] + i);
+                bs.sorted[rank] = b;
+                xmin = xmax = b.x; ymin = ymax = b.y; rmax = b.radius;
+            }
+            auto fmn = [](double a, double b) { return fmin(a, b); };
+            auto fmx = [](double a, double b) { return fmax(a, b); };
+            xmin = block_reduce(xmin, fmn, sd); xmax = block_reduce(xmax, fmx, sd);
+            ymin = block_reduce(ymin, fmn, sd); ymax = block_reduce(ymax, fmx, sd);
+            rmax = block_reduce(rmax, fmx, sd);
+            if (tid == 0) {
+                atomic_min_double(&ctl->ext[0], xmin); atomic_max_double(&ctl->ext[1], xmax);
+                atomic_min_double(&ctl->ext[2], ymin); atomic_max_double(&ctl->ext[3], ymax);
+                atomic_max_double(&ctl->ext[4], rmax);
+            }
+            break;
         }
-        if (lane == 31) s_red[warp] = v;
-        __syncthreads();
-        if (warp == 0) {
-            int t = s_red[lane];
+        case PH_COUNT: {
+            const Grid g = load_grid_cg(bs);
+            const int i = item * kItemBlobs + tid;
+            if (i < n) {
+                const double2 b = ldcg_xy(bs.sorted + i);
+                const int c = g.cy(b.y) * g.gx + g.cx(b.x);
+                bs.cell_of[i] = c;
+                bs.alive[i] = 1;
+                atomicAdd(&bs.cell_start[c + 1], 1);
+            }
+            break;
+        }
+        case PH_SCAN: {                            // one CTA: cell_start[c] = blobs in cells < c
+            const Grid g = load_grid_cg(bs);
+            const int ncell = g.gx * g.gy;
+            const int per = (ncell + kLargeThreads - 1) / kLargeThreads;
+            const int c0 = 1 + tid * per, c1 = min(c0 + per, ncell + 1);
+            int sum = 0;
+            for (int c = c0; c < c1; ++c) sum += ldcg_i(bs.cell_start + c);
+            int v = sum;
             for (int o = 1; o < 32; o <<= 1) {
-                const int u = __shfl_up_sync(0xffffffffu, t, o);
-                if (lane >= o) t += u;
+                const int t = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += t;
             }
-            s_red[lane] = t;
+            if (lane == 31) si[warp] = v;
+            __syncthreads();
+            if (warp == 0) {
+                int t = lane < kLargeThreads / 32 ? si[lane] : 0;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int u = __shfl_up_sync(0xffffffffu, t, o);
+                    if (lane >= o) t += u;
+                }
+                si[lane] = t;
+            }
+            __syncthreads();
+            int run = (warp > 0 ? si[warp - 1] : 0) + v - sum;      // exclusive prefix of this thread
+            for (int c = c0; c < c1; ++c) {
+                run += ldcg_i(bs.cell_start + c);
+                bs.cell_start[c] = run;
+            }
+            break;
+        }
+        case PH_FILL: {
+            const int i = item * kItemBlobs + tid;
+            if (i < n) {
+                const int c = ldcg_i(bs.cell_of + i);
+                const int slot = ldcg_i(bs.cell_start + c) + atomicAdd(&bs.cell_fill[c], 1);
+                bs.cell_items[slot] = i;
+            }
+            break;
+        }
+        case PH_FIRST: {
+            const Grid g = load_grid_cg(bs);
+            for (int q = 0; q < kWarpBlobs / 8; ++q) {
+                const int i = item * kWarpBlobs + warp * (kWarpBlobs / 8) + q;
+                if (i >= n) break;
+                const int best = scan_first_partner(bs, g, i, thr, lane);
+                if (lane == 0) {
+                    bs.first[i] = (best == INT_MAX) ? -1 : best;
+                    bs.comp[i] = i;
+                    bs.cmin[i] = -1;
+                    bs.bound[i] = (unsigned long long)__double_as_longlong(ldcg_xyr(bs.sorted + i).r);
+                }
+            }
+            break;
+        }
+        case PH_SWEEP: {
+            const Grid g = load_grid_cg(bs);
+            for (int q = 0; q < kWarpBlobs / 8; ++q) {
+                const int i = item * kWarpBlobs + warp * (kWarpBlobs / 8) + q;
+                if (i >= n) break;
+                const double2 bi = ldcg_xy(bs.sorted + i);
+                const double u0 = ldcg_bound(bs, i);
+                double ui = u0;
+                for_neighbours_warp(bs, g, g.cx(bi.x), g.cy(bi.y), lane, [&](int j) {
+                    if (j <= i) return;
+                    const double uj = ldcg_bound(bs, j);
+                    if (uj <= ui) return;
+                    const double2 bj = ldcg_xy(bs.sorted + j);
+                    const double dx = bi.x - bj.x, dy = bi.y - bj.y, reach = ui + uj;
+                    if (dx * dx + dy * dy < reach * reach * 1.0000001 + 1e-9) ui = uj;
+                });
+                for (int o = 16; o > 0; o >>= 1) ui = fmax(ui, __shfl_xor_sync(0xffffffffu, ui, o));
+                if (lane == 0 && ui > u0) {
+                    bs.bound[i] = (unsigned long long)__double_as_longlong(ui);
+                    *(volatile int *)&ctl->changed = 1;
+                }
+            }
+            break;
+        }
+        case PH_SATURATE: {                        // too many sweeps: r_max everywhere is a valid bound
+            const int i = item * kItemBlobs + tid;
+            if (i < n) bs.bound[i] = (unsigned long long)__double_as_longlong(ldcg_d(&ctl->ext[4]));
+            break;
+        }
+        case PH_UNION: {
+            const Grid g = load_grid_cg(bs);
+            for (int q = 0; q < kWarpBlobs / 8; ++q) {
+                const int i = item * kWarpBlobs + warp * (kWarpBlobs / 8) + q;
+                if (i >= n) break;
+                const double2 bi = ldcg_xy(bs.sorted + i);
+                const double ui = ldcg_bound(bs, i);
+                for_neighbours_warp(bs, g, g.cx(bi.x), g.cy(bi.y), lane, [&](int j) {
+                    if (j <= i) return;
+                    const double2 bj = ldcg_xy(bs.sorted + j);
+                    const double dx = bi.x - bj.x, dy = bi.y - bj.y;
+                    const double reach = ui + ldcg_bound(bs, j);
+                    if (dx * dx + dy * dy < reach * reach * 1.0000001 + 1e-9) comp_union(bs.comp, i, j);
+                });
+            }
+            break;
+        }
+        case PH_LINK: {
+            const int i = item * kItemBlobs + tid;
+            if (i < n) {
+                const int root = comp_find(bs.comp, i);
+                bs.comp[i] = root;
+                if (ldcg_i(bs.first + i) >= 0) {
+                    atomicOr(&bs.alive[i], 2);
+                    const int old = atomicExch(&bs.cmin[root], i);
+                    bs.cell_of[i] = old;
+                    if (old < 0) bs.pl_count[atomicAdd(&ctl->n_roots, 1)] = root;   // list of active parts
+                }
+            }
+            break;
+        }
+        case PH_MERGE: {
+            const Grid g = load_grid_cg(bs);
+            const int q = item * 8 + warp;
+            if (q < __ldcg(&ctl->n_roots)) {
+                const int m = merge_part(bs, g, ldcg_i(bs.pl_count + q), thr, lane);
+                if (lane == 0 && m) atomicAdd(&ctl->merges, m);
+            }
+            break;
+        }
+        case PH_PACK_COUNT: {
+            int keep = 0;
+            for (int k = 0; k < kPackBlobs / kLargeThreads; ++k) {
+                const int i = item * kPackBlobs + tid * (kPackBlobs / kLargeThreads) + k;
+                keep += __syncthreads_count((i < n) && (!pruning || (ldcg_i(bs.alive + i) & 1)));
+            }
+            if (tid == 0) bs.cell_fill[item] = keep;
+            break;
+        }
+        case PH_PACK_WRITE: {
+            if (n == 0) break;
+            constexpr int kPer = kPackBlobs / kLargeThreads;
+            const int i0 = item * kPackBlobs + tid * kPer;
+            int flag[kPer], mine = 0;
+            for (int k = 0; k < kPer; ++k) {
+                flag[k] = (i0 + k < n) && (!pruning || (ldcg_i(bs.alive + i0 + k) & 1));
+                mine += flag[k];
+            }
+            int v = mine;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += t;
+            }
+            if (lane == 31) si[warp] = v;
+            __syncthreads();
+            if (warp == 0) {
+                int t = lane < kLargeThreads / 32 ? si[lane] : 0;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int u = __shfl_up_sync(0xffffffffu, t, o);
+                    if (lane >= o) t += u;
+                }
+                si[lane] = t;
+            }
+            __syncthreads();
+            int pos = ldcg_i(bs.cell_start + item) + (warp > 0 ? si[warp - 1] : 0) + v - mine;
+            for (int k = 0; k < kPer; ++k)
+                if (flag[k]) {
+                    if (pos < out_cap) out[pos] = ldcg_blob(bs.sorted + i0 + k);
+                    ++pos;
+                }
+            break;
+        }
+        default: break;
+        }
+
+        // ---- completion; the CTA that completes a phase publishes the next one ----
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            const int done = (int)atomicAdd(&ctl->done, 1u) + 1;
+            s_last = (done == ph_first + ph_count);
+            if (s_last) {
+                __threadfence();
+                int next = PH_END;
+                switch (ph_type) {
+                    case PH_RANK: next = PH_SCATTER; break;
+                    case PH_SCATTER: {
+                        if (!pruning) { next = PH_PACK_COUNT; break; }
+                        next = PH_COUNT;
+                        const double xmin = ldcg_d(&ctl->ext[0]), xmax = ldcg_d(&ctl->ext[1]);
+                        const double ymin = ldcg_d(&ctl->ext[2]), ymax = ldcg_d(&ctl->ext[3]);
+                        const double rmax = ldcg_d(&ctl->ext[4]);
+                        double cell = fmax(2.0 * rmax, 1e-9) * 1.0000001;   // strictly covers d < r_i + r_j
+                        cell = fmax(cell, fmax(xmax - xmin, ymax - ymin) / (double)(kMaxCellsPerAxis - 1));
+                        const int gx = min(kMaxCellsPerAxis, (int)floor((xmax - xmin) / cell) + 1);
+                        const int gy = min(kMaxCellsPerAxis, (int)floor((ymax - ymin) / cell) + 1);
+                        bs.grid_params[0] = xmin; bs.grid_params[1] = ymin; bs.grid_params[2] = cell;
+                        bs.grid_params[3] = (double)gx; bs.grid_params[4] = (double)gy;
+                        break;
+                    }
+                    case PH_COUNT: next = PH_SCAN; break;
+                    case PH_SCAN: next = PH_FILL; break;
+                    case PH_FILL: next = PH_FIRST; break;
+                    case PH_FIRST: next = PH_SWEEP; ctl->changed = 0; ctl->sweeps = 1; break;
+                    case PH_SWEEP:
+                        if (__ldcg(&ctl->changed)) {
+                            ctl->changed = 0;
+                            if (ctl->sweeps < kMaxSweeps) { next = PH_SWEEP; ctl->sweeps += 1; }
+                            else next = PH_SATURATE;
+                        } else {
+                            next = PH_UNION;
+                        }
+                        break;
+                    case PH_SATURATE: next = PH_UNION; break;
+                    case PH_UNION: next = PH_LINK; break;
+                    case PH_LINK: next = __ldcg(&ctl->n_roots) > 0 ? PH_MERGE : PH_PACK_COUNT; break;
+                    case PH_MERGE: next = PH_PACK_COUNT; break;
+                    case PH_PACK_COUNT: {
+                        next = PH_PACK_WRITE;
+                        int run = 0;                                  // chunk offsets
+                        for (int c = 0; c < ph_count; ++c) {
+                            const int k = ldcg_i(bs.cell_fill + c);
+                            bs.cell_start[c] = run;
+                            run += k;
+                        }
+                        ctl->kept = run;
+                        break;
+                    }
+                    case PH_PACK_WRITE: {
+                        next = PH_END;
+                        const Counters c = *bs.ctr;
+                        const int kept = n > 0 ? ctl->kept : 0;
+                        hdr->n_blobs = min(kept, out_cap);
+                        hdr->n_candidates = c.n_candidates;
+                        hdr->n_flagged = c.n_flagged;
+                        hdr->n_plateau = c.n_plateau;
+                        hdr->n_merges = __ldcg(&ctl->merges);
+                        unsigned f = c.flags;
+                        if (c.n_candidates > bs.cap || c.n_plateau > bs.cap || kept > out_cap)
+                            f |= DOGBLOB_FLAG_OVERFLOW;
+                        hdr->flags = f;
+                        hdr->capacity = out_cap;
+                        // phase profile: us from the first ticket to the publication of ...
+                        const unsigned long long t0 = __ldcg(&ctl->phase[0].t_ns);
+                        // us from the first ticket to: grid build, first sweep, part labelling,
+                        // merge loops, packing (phases that did not run keep the next mark)
+                        int mark[5] = {-1, -1, -1, -1, -1};
+                        for (int k = 1; k <= cur; ++k) {
+                            const int ty = __ldcg(&ctl->phase[k].type);
+                            const int us = (int)((__ldcg(&ctl->phase[k].t_ns) - t0) / 1000);
+                            const int slot = ty == PH_COUNT ? 0 : ty == PH_SWEEP ? 1 : ty == PH_UNION ? 2
+                                           : ty == PH_MERGE ? 3 : ty == PH_PACK_COUNT ? 4 : -1;
+                            if (slot >= 0 && mark[slot] < 0) mark[slot] = us;
+                        }
+                        for (int q = 3; q >= 0; --q) if (mark[q] < 0) mark[q] = mark[q + 1];
+                        for (int q = 0; q < 5; ++q) hdr->reserved[q] = mark[q];
+                        hdr->reserved[6] = (int)((now_ns() - t0) / 1000);
+                        hdr->reserved[7] = ctl->sweeps;
+                        hdr->reserved[8] = __ldcg(&ctl->n_roots);
+                        break;
+                    }
+                    default: break;
+                }
+                const int k = cur + 1;
+                {
+                    ctl->phase[k].type = next;
+                    ctl->phase[k].first_item = ph_first + ph_count;
+                    ctl->phase[k].n_items = next == PH_END ? 0 : phase_items(next, n, __ldcg(&ctl->n_roots));
+                    ctl->phase[k].t_ns = now_ns();
+                    __threadfence();
+                    *(volatile int *)&ctl->n_phases = k + 1;
+                }
+            }
         }
         __syncthreads();
-        const int pos = s_carry + (warp > 0 ? s_red[warp - 1] : 0) + v - keep;
-        if (keep && pos < out_cap) out[pos] = bs.sorted[i];
-        __syncthreads();
-        if (tid == blockDim.x - 1) s_carry = pos + keep;
-        __syncthreads();
-    }
-    if (tid == 0) {
-        const Counters c = *bs.ctr;
-        hdr->n_blobs = min(s_carry, out_cap);
-        hdr->n_candidates = c.n_candidates;
-        hdr->n_flagged = c.n_flagged;
-        hdr->n_plateau = c.n_plateau;
-        hdr->n_merges = merges;
-        unsigned f = c.flags;
-        if (c.n_candidates > bs.cap || c.n_plateau > bs.cap || s_carry > out_cap)
-            f |= DOGBLOB_FLAG_OVERFLOW;
-        hdr->flags = f;
-        hdr->capacity = out_cap;
     }
 }
 
@@ -654,13 +935,9 @@ cudaError_t launch_prune_and_pack(const BlobSpace &bs, double overlap, bool prun
     // <= kSmallMax candidates: everything in one CTA; the general kernels then return at once
     finalize_small_kernel<<<1, kSmallMax, kSmallSmem, st>>>(bs, overlap, prune ? 1 : 0, hdr, out,
                                                             result_cap, small_limit());
-    cudaError_t e = launch_rank_sort(bs, st);
-    if (e != cudaSuccess) return e;
-    if (prune) {
-        prune_build_kernel<<<1, kLoopThreads, 0, st>>>(bs);
-        prune_first_kernel<<<148 * 2, 256, 0, st>>>(bs, overlap);
-    }
-    prune_loop_kernel<<<1, kLoopThreads, 0, st>>>(bs, overlap, prune ? 1 : 0, hdr, out, result_cap);
+    // larger frames: one whole-GPU kernel whose phases chain on the device
+    prune_large_kernel<<<148 * 2, kLargeThreads, 0, st>>>(bs, overlap, prune ? 1 : 0, hdr, out,
+                                                          result_cap);
     return cudaGetLastError();
 }
 

@@ -521,6 +521,11 @@ class Detector:
     def _finish(self, slot: _Slot, hdr, recs, shape, timings) -> DetectResult:
         blobs = BlobSet(records=recs, source_shape=(shape[1], shape[0]), params=self.params)
         stats = {k: int(hdr[k]) for k in ("n_flagged", "n_plateau", "n_candidates", "n_merges")}
+        if int(hdr["reserved"][6]):      # whole-GPU pruning kernel ran: its phase profile
+            r = [int(v) for v in hdr["reserved"]]
+            stats["prune_profile"] = {"order_us": r[0], "grid_first_us": r[1] - r[0], "bound_us": r[2] - r[1],
+                                      "parts_us": r[3] - r[2], "merge_us": r[4] - r[3], "pack_us": r[6] - r[4],
+                                      "total_us": r[6], "sweeps": r[7], "parts": r[8]}
         return DetectResult(blobs=blobs, histogram=histogram(blobs, self.ladder),
                             timings_ms=timings, stats=stats)
 

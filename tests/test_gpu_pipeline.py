@@ -153,6 +153,24 @@ class TestDetectorBehaviour:
             assert np.array_equal(a.histogram.counts, b.histogram.counts)
         det.close()
 
+    def test_dense_frames_on_concurrent_streams(self):
+        """several whole-GPU pruning kernels (device-chained phases, ticket-ordered waits) in
+        flight at once, next to the convolution kernels of other frames: same result as one
+        frame at a time, and the phase profile is reported"""
+        det = P.Detector(params_for("C5", overlap=0.3), slots=4)
+        frames = [synth.sensor_noise(synth.droplet_scene(512, 512, 3000 + 400 * i, (2.0, 5.0), seed=70 + i,
+                                                         allow_overlap=True), seed=80 + i).image
+                  for i in range(6)] + [synth.config_frame("C1")]
+        single = [det.run(f) for f in frames]
+        assert single[0].stats["n_candidates"] > 1500 and single[0].stats["n_merges"] > 0
+        assert single[0].stats["prune_profile"]["parts"] > 0
+        for _ in range(3):
+            batch = det.run_batch(frames)
+            for a, b in zip(single, batch):
+                assert np.array_equal(a.blobs.records, b.blobs.records)
+                assert a.stats["n_merges"] == b.stats["n_merges"]
+        det.close()
+
     def test_shared_detector_from_threads(self):
         det = P.Detector(params_for("C1"), slots=2)
         frame = synth.config_frame("C1")
