@@ -29,6 +29,18 @@ from .detector import (
 )
 
 from .images import preprocess
+from .formats import (
+    blobset_from_doc,
+    blobset_to_doc,
+    histogram_to_doc,
+    raw_from_bytes,
+    read_blobset_json,
+    read_raw,
+    read_raw_pinned,
+    write_blobset_json,
+    write_histogram_csv,
+    write_raw,
+)
 
 __version__ = "0.1.0"
 
@@ -37,5 +49,7 @@ __all__ = [
     "BACKENDS", "ScaleStack", "DoGStack", "Blob", "BlobSet", "RadiusHistogram",
     "DetectionParams", "DetectResult", "Detector", "convolve_bank", "dog_stack", "fused_dog",
     "find_extrema", "prune_overlaps", "normalized_overlap", "disk_intersection_area",
-    "histogram", "detect", "preprocess", "__version__",
+    "histogram", "detect", "preprocess", "raw_from_bytes", "read_raw", "read_raw_pinned", "write_raw",
+    "blobset_to_doc", "blobset_from_doc", "write_blobset_json", "read_blobset_json",
+    "histogram_to_doc", "write_histogram_csv", "__version__",
 ]

@@ -311,3 +311,51 @@ class TestPreprocess:
             for row, c, n, v in zip(rows, res.histogram.bin_centers, res.histogram.counts,
                                     res.histogram.volume_weights):
                 assert row == f"{float(c)!r},{int(n)},{float(v)!r}"
+
+
+class TestFormats:
+    """raw frame file -> pinned memory -> detector -> the reference's JSON / CSV."""
+
+    def test_raw_file_to_pinned_to_blob_json(self, tmp_path):
+        import json
+        import torch
+        from conftest import GOLDEN
+        from paper_2010_08486_b200 import formats as F
+        frame = synth.sensor_noise(synth.droplet_scene(1000, 1000, 100, (4.0, 20.0), seed=123),
+                                   seed=124).image
+        F.write_raw(tmp_path / "frame.raw", frame)
+        pinned = F.read_raw_pinned(tmp_path / "frame.raw")
+        assert isinstance(pinned, torch.Tensor) and pinned.is_pinned()
+        assert np.array_equal(pinned.numpy(), frame)
+        ring = torch.empty(1200 * 1000, dtype=torch.float32).pin_memory()        # re-used staging buffer
+        again = F.raw_into_pinned((tmp_path / "frame.raw").read_bytes(), out=ring)
+        assert again.data_ptr() == ring.data_ptr() and np.array_equal(again.numpy(), frame)
+        doc = json.loads((GOLDEN / "ref_demo03_blobs.json").read_text())
+        kw = {k: v for k, v in doc["params"].items() if k != "backend"}
+        det = P.Detector(P.DetectionParams(**kw))
+        res = det.run(pinned)
+        res2 = det.run(again)
+        det.close()
+        assert np.array_equal(res.blobs.records, res2.blobs.records)
+        # same blobs as the reference file (responses differ in the last float32 bits, so the
+        # bytes are compared after substituting the reference's responses)
+        text = F.blobs_json_text(res.blobs, "demo_scene")
+        got = json.loads(text)
+        assert got["params"] == {**doc["params"], "backend": "cuda"}
+        strip = lambda bl: [(b["x"], b["y"], b["sigma"], b["radius"], b["at_scale_boundary"]) for b in bl]
+        assert strip(got["blobs"]) == strip(doc["blobs"])
+        assert max(abs(a["response"] - b["response"]) for a, b in zip(got["blobs"], doc["blobs"])) < 2e-5
+        assert text == json.dumps(F.blobset_to_doc(res.blobs, "demo_scene"), indent=2)
+        F.write_histogram_csv(tmp_path / "h.csv", res.histogram)
+        assert (tmp_path / "h.csv").read_bytes() == (GOLDEN / "ref_demo03_histogram.csv").read_bytes()
+
+    def test_pinned_ingest_rejects_bad_frames(self, tmp_path):
+        from paper_2010_08486_b200 import formats as F
+        img = np.ones((8, 8), np.float32)
+        img[3, 3] = np.inf
+        (tmp_path / "bad.raw").write_bytes(b"\x08\x00\x00\x00\x08\x00\x00\x00" + img.tobytes())
+        with pytest.raises(ValueError, match="NaN or Inf"):
+            F.read_raw_pinned(tmp_path / "bad.raw")
+        (tmp_path / "short.raw").write_bytes(b"\x08\x00\x00\x00\x08\x00\x00\x00" + img.tobytes()[:-4])
+        with pytest.raises(ValueError, match="expected 264 bytes, found 260"):
+            F.read_raw_pinned(tmp_path / "short.raw")
