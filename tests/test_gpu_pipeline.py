@@ -359,3 +359,88 @@ class TestFormats:
         (tmp_path / "short.raw").write_bytes(b"\x08\x00\x00\x00\x08\x00\x00\x00" + img.tobytes()[:-4])
         with pytest.raises(ValueError, match="expected 264 bytes, found 260"):
             F.read_raw_pinned(tmp_path / "short.raw")
+
+
+class TestService:
+    """the HTTP service and the CLI call the same detector; their JSON is the offline
+    detector's, byte for byte apart from the timings (reference tests/test_service.py:82-94,
+    acceptance criterion 7)."""
+
+    @staticmethod
+    def _post(port, path, body, ctype="application/octet-stream"):
+        import http.client
+        c = http.client.HTTPConnection("127.0.0.1", port, timeout=60)
+        c.request("POST", path, body=body, headers={"Content-Type": ctype})
+        r = c.getresponse()
+        data = r.read()
+        c.close()
+        return r.status, data
+
+    def test_service_equals_offline_detector_and_cli(self, tmp_path):
+        import json
+        from paper_2010_08486_b200 import cli, formats as F, service as S
+        params = P.DetectionParams(min_sigma=2.5, max_sigma=9.0, n_bin=13)          # preprocess on
+        frames = [synth.sensor_noise(synth.droplet_scene(400, 300, 25, (4.0, 12.0), seed=30 + i,
+                                                         allow_overlap=True), seed=60 + i).image
+                  for i in range(5)]
+        det = P.Detector(params)
+        offline = [det.run(f) for f in frames]
+        det.close()
+        srv = S.make_server(S.ServiceConfig(port=0, params=params, workers=2, backlog=8))
+        t = threading.Thread(target=srv.serve_forever, daemon=True)
+        t.start()
+        port = srv.server_address[1]
+        try:
+            def strip(doc):
+                return {k: v for k, v in doc.items() if k != "timing_ms"}
+
+            out = [None] * len(frames)
+
+            def work(i):
+                out[i] = self._post(port, f"/detect?name=frame{i}", F.raw_to_bytes(frames[i]))
+
+            ts = [threading.Thread(target=work, args=(i,)) for i in range(len(frames))]
+            [x.start() for x in ts]
+            [x.join() for x in ts]
+            for i, (st, data) in enumerate(out):
+                assert st == 200
+                doc = json.loads(data)
+                want = json.loads(F.blobs_json_text(offline[i].blobs, f"frame{i}",
+                                                    extra={"histogram": F.histogram_to_doc(offline[i].histogram)}))
+                assert strip(doc) == want
+                assert set(doc["timing_ms"]) == {"preprocess_ms", "convolve_ms", "extrema_ms", "prune_ms"}
+                assert data == (json.dumps(doc, indent=2) + "\n").encode()
+            # per-request override: a second parameter set builds (and caches) a second detector
+            st, data = self._post(port, "/detect?n_bin=6&preprocess=false", F.raw_to_bytes(frames[0]))
+            d2 = P.Detector(P.DetectionParams(min_sigma=2.5, max_sigma=9.0, n_bin=6, preprocess=False))
+            assert st == 200 and json.loads(data)["blobs"] == F.blobset_to_doc(d2.run(frames[0]).blobs)["blobs"]
+            d2.close()
+            # batch path: same answers as the single-frame path
+            st, data = self._post(port, "/detect_batch?name=b", b"".join(F.raw_to_bytes(f) for f in frames))
+            assert st == 200
+            for i, fd in enumerate(json.loads(data)["frames"]):
+                assert fd["blobs"] == F.blobset_to_doc(offline[i].blobs)["blobs"] and fd["image"] == f"b[{i}]"
+            # detector argument errors surface as 400, like the reference's decode errors
+            assert self._post(port, "/detect?min_sigma=9&max_sigma=9.5&n_bin=300", F.raw_to_bytes(frames[0]))[0] == 400
+        finally:
+            srv.shutdown()
+            srv.server_close()
+        assert srv.state.cache.closed >= 2 and len(srv.state.cache) == 0     # device memory returned
+        # CLI detect on the raw file: same JSON file as the offline writer
+        F.write_raw(tmp_path / "f0.raw", frames[0])
+        rc = cli.main(["detect", "--input", str(tmp_path / "f0.raw"), "--min-sigma", "2.5", "--max-sigma", "9",
+                       "--n-bin", "13", "--out-json", str(tmp_path / "o.json"), "--out-hist", str(tmp_path / "h.csv")])
+        assert rc == 0
+        assert (tmp_path / "o.json").read_text() == F.blobs_json_text(offline[0].blobs, "f0.raw") + "\n"
+        assert (tmp_path / "h.csv").read_text() == F.histogram_csv_text(offline[0].histogram)
+
+    def test_cli_bench_sweep(self, tmp_path, capsys):
+        from paper_2010_08486_b200 import cli
+        out = tmp_path / "sweep.csv"
+        assert cli.main(["bench", "--sweep", "max_sigma", "--values", "4,8", "--seed", "3", "--width", "256",
+                         "--height", "256", "--n-bin", "6", "--out", str(out)]) == 0
+        rows = out.read_text().splitlines()
+        assert rows[0] == ("backend,n_bin,max_sigma,width,height,warmup_runs,timed_runs,median_ms,p10_ms,"
+                           "p90_ms,hardware")
+        assert len(rows) == 3 and rows[1].startswith("cuda,6,4.0,256,256,1,3,")
+        assert "median" in capsys.readouterr().out
