@@ -66,7 +66,15 @@ typedef struct dogblob_result_header {
     int32_t n_merges;       /* merges performed by pruning */
     uint32_t flags;         /* DOGBLOB_FLAG_* */
     int32_t capacity;       /* max blobs this buffer can hold */
-    int32_t reserved[9];
+    /* device-side stage times in ns (globaltimer): scale space + DoG | extrema | ordering +
+     * pruning + packing -- the convolve_ms / extrema_ms / prune_ms of Detector.run
+     * (detector.py:336-357) without any host-side event call */
+    int32_t conv_ns, extrema_ns, prune_ns;
+    /* phase profile of the whole-GPU pruning kernel (0 when the single-CTA path ran):
+     * [0..2] six 16-bit marks in us since its first ticket (grid build, first sweep, part
+     * labelling, merge loops, packing, end; saturating), [3] sweeps << 24 | parts */
+    int32_t prune_profile[4];
+    int32_t reserved[2];
 } dogblob_result_header;
 
 #define DOGBLOB_FLAG_OVERFLOW 1u     /* a capacity was exceeded: result incomplete */
@@ -175,6 +183,10 @@ int dogblob_event_create(void **event);
 int dogblob_event_destroy(void *event);
 int dogblob_event_record(void *event, void *stream);
 int dogblob_event_elapsed_ms(void *start, void *stop, float *ms);
+/* out_ms[k] = time from events[k] to events[k + 1], k < n_events - 1: the stage times of
+ * dogblob_detect's DOGBLOB_N_EVENTS events (timings_ms of Detector.run, detector.py:336-357)
+ * in one call */
+int dogblob_event_intervals_ms(void *const *events, int n_events, float *out_ms);
 int dogblob_stream_sync(void *stream);
 int dogblob_device_count(int *count);
 

@@ -26,7 +26,8 @@ BLOB_DTYPE = np.dtype([("x", "<f8"), ("y", "<f8"), ("sigma", "<f8"), ("radius", 
                        ("response", "<f8"), ("slice", "<i4"), ("flags", "<u4")])
 HEADER_DTYPE = np.dtype([("n_blobs", "<i4"), ("n_candidates", "<i4"), ("n_flagged", "<i4"),
                          ("n_plateau", "<i4"), ("n_merges", "<i4"), ("flags", "<u4"),
-                         ("capacity", "<i4"), ("reserved", "<i4", (9,))])
+                         ("capacity", "<i4"), ("conv_ns", "<i4"), ("extrema_ns", "<i4"),
+                         ("prune_ns", "<i4"), ("prune_profile", "<i4", (4,)), ("reserved", "<i4", (2,))])
 assert BLOB_DTYPE.itemsize == 48 and HEADER_DTYPE.itemsize == RESULT_HEADER_BYTES
 
 # every symbol include/dogblob_b200.h declares: name -> (restype, argtypes)
@@ -58,6 +59,7 @@ SIGNATURES = {
     "dogblob_event_create": (_i, [C.POINTER(_vp)]),
     "dogblob_event_destroy": (_i, [_vp]),
     "dogblob_event_elapsed_ms": (_i, [_vp, _vp, C.POINTER(_f)]),
+    "dogblob_event_intervals_ms": (_i, [_vp, _i, _vp]),
     "dogblob_stream_sync": (_i, [_vp]),
     "dogblob_device_count": (_i, [C.POINTER(_i)]),
 }

@@ -484,6 +484,13 @@ int dogblob_event_elapsed_ms(void *start, void *stop, float *ms) {
                                  reinterpret_cast<cudaEvent_t>(stop)));
     return DOGBLOB_OK;
 }
+int dogblob_event_intervals_ms(void *const *events, int n_events, float *out_ms) {
+    DB_REQUIRE(events != nullptr && out_ms != nullptr && n_events >= 2, "bad argument");
+    for (int k = 0; k + 1 < n_events; ++k)
+        DB_CUDA(cudaEventElapsedTime(out_ms + k, reinterpret_cast<cudaEvent_t>(events[k]),
+                                     reinterpret_cast<cudaEvent_t>(events[k + 1])));
+    return DOGBLOB_OK;
+}
 int dogblob_stream_sync(void *stream) {
     DB_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
     return DOGBLOB_OK;

@@ -57,6 +57,12 @@ struct LevelTable {
     int n_levels, n_groups;
 };
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // ---- blob bookkeeping shared by extrema / prune ------------------------------
 struct Counters {            // one per result, lives in the blob space
     int n_flagged;           // voxels passing the NMS + threshold test
@@ -67,7 +73,10 @@ struct Counters {            // one per result, lives in the blob space
     unsigned flags;
     int small_done;          // 1 once finalize_small_kernel has sorted / pruned / packed the frame
     unsigned plateau_ticket; // CTA ticket of plateau_kernel
-    int pad[8];
+    // device-side stage stamps (globaltimer, ns): start of the frame, start of extrema, start of
+    // ordering/pruning; the kernel that finishes the frame turns them into the header's stage times
+    unsigned long long t_start, t_extrema, t_prune;
+    int pad[2];
 };
 
 struct Voxel { int s, row, col; float val; };

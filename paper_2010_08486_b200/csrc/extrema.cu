@@ -158,6 +158,7 @@ nms_window_kernel(Volume vol, float thr, bool transposed, const double *__restri
     const int s = blockIdx.z;
     const unsigned lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
+    if ((blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.x) == 0) bs.ctr->t_extrema = globaltimer_ns();
     // the 8 warps of a CTA sit side by side on the same rows: together they read 4 KB runs
     const int r_first = blockIdx.y * kBandRows;            // first tested row
     const int c = (blockIdx.x * 8 + warp) * 128 + 4 * (int)lane;
@@ -295,6 +296,7 @@ __global__ void __launch_bounds__(256)
 nms_kernel(Volume vol, float thr, int h, bool transposed, const double *__restrict__ slice_sigma,
            BlobSpace bs) {
     __shared__ __align__(16) float tile[(kNmsRows + 2) * kNmsPitch];
+    if ((blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.x) == 0) bs.ctr->t_extrema = globaltimer_ns();
     const int s = blockIdx.z;
     const int r0 = blockIdx.y * kNmsRows;
     const int c0 = blockIdx.x * kNmsCols;
@@ -447,6 +449,7 @@ plateau_kernel(BlobSpace bs, int S, bool transposed, const double *__restrict__ 
 __global__ void reset_counters_kernel(BlobSpace bs) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         Counters z = {};
+        z.t_start = globaltimer_ns();
         *bs.ctr = z;
     }
     // ticket, done, n_phases, changed, sweeps, n_roots, merges, kept of the pruning control block

@@ -65,10 +65,10 @@ struct Grid {
 };
 
 template <typename T, typename Op>
-__device__ T block_reduce(T v, Op op, T *scratch /* >= 33 */) {
+__device__ T block_reduce(T v, Op op, T *scratch /* >= 33 */, int nw = 0 /* live warps, 0 = all */) {
     for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int nw = (blockDim.x + 31) >> 5;
+    if (nw == 0) nw = (blockDim.x + 31) >> 5;
     __syncthreads();
     if (lane == 0) scratch[w] = v;
     __syncthreads();
@@ -120,10 +120,17 @@ __device__ __forceinline__ double ldcg_d(const double *p) { return __ldcg(p); }
 __device__ __forceinline__ double ldcg_bound(const BlobSpace &bs, int i) {
     return __longlong_as_double((long long)__ldcg(bs.bound + i));
 }
-__device__ __forceinline__ unsigned long long now_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
+__device__ __forceinline__ unsigned long long now_ns() { return globaltimer_ns(); }
+
+__device__ __forceinline__ int clamp_ns(unsigned long long a, unsigned long long b) {
+    return b > a ? (int)min(b - a, 2000000000ull) : 0;
+}
+// the kernel that finishes a frame fills the header's device-side stage times
+__device__ void write_stage_times(const Counters &c, dogblob_result_header *hdr) {
+    const unsigned long long t_end = globaltimer_ns();
+    hdr->conv_ns = c.t_extrema ? clamp_ns(c.t_start, c.t_extrema) : 0;
+    hdr->extrema_ns = c.t_extrema ? clamp_ns(c.t_extrema, c.t_prune) : 0;
+    hdr->prune_ns = clamp_ns(c.t_prune, t_end);
 }
 __device__ void atomic_min_double(double *addr, double v) {
     unsigned long long *a = reinterpret_cast<unsigned long long *>(addr);
@@ -719,10 +726,14 @@ prune_large_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_header
                             if (slot >= 0 && mark[slot] < 0) mark[slot] = us;
                         }
                         for (int q = 3; q >= 0; --q) if (mark[q] < 0) mark[q] = mark[q + 1];
-                        for (int q = 0; q < 5; ++q) hdr->reserved[q] = mark[q];
-                        hdr->reserved[6] = (int)((now_ns() - t0) / 1000);
-                        hdr->reserved[7] = ctl->sweeps;
-                        hdr->reserved[8] = __ldcg(&ctl->n_roots);
+                        const int total = (int)((now_ns() - t0) / 1000);
+                        auto u16 = [](int v) { return (unsigned)min(max(v, 0), 65535); };
+                        hdr->prune_profile[0] = (int)(u16(mark[0]) | (u16(mark[1]) << 16));
+                        hdr->prune_profile[1] = (int)(u16(mark[2]) | (u16(mark[3]) << 16));
+                        hdr->prune_profile[2] = (int)(u16(mark[4]) | (u16(total) << 16));
+                        hdr->prune_profile[3] = (ctl->sweeps << 24) | (__ldcg(&ctl->n_roots) & 0xFFFFFF);
+                        hdr->reserved[0] = hdr->reserved[1] = 0;
+                        write_stage_times(c, hdr);
                         break;
                     }
                     default: break;
@@ -759,6 +770,7 @@ finalize_small_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_hea
     __shared__ int s_pos, s_carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_raw = bs.ctr->n_candidates;
+    if (tid == 0) bs.ctr->t_prune = globaltimer_ns();
     if (n_raw > limit || n_raw > bs.cap) {
         if (tid == 0) bs.ctr->small_done = 0;
         return;
@@ -814,10 +826,16 @@ finalize_small_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_hea
             if (lane == 0) first[i] = (best == INT_MAX) ? -1 : best;
         }
         if (tid == 0) s_pos = 0;
-        __syncthreads();
+    }
+    // Only the warps that hold a blob stay for the sequential part: every barrier of the merge
+    // loop then spans ceil(n / 32) warps instead of 32 (exited warps leave the barrier count).
+    __syncthreads();
+    const int nw = max(1, (n + 31) >> 5);
+    if (warp >= nw) return;
+    if (do_prune && n >= 2) {
         while (true) {
             int mine = (tid >= s_pos && tid < n && alive[tid] && first[tid] >= 0) ? tid : INT_MAX;
-            const int istar = block_reduce(mine, imin, s_red);
+            const int istar = block_reduce(mine, imin, s_red, nw);
             if (istar == INT_MAX) break;
             const int j = first[istar];
             __syncthreads();
@@ -859,7 +877,7 @@ finalize_small_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_hea
                 }
                 first[tid] = best;
             }
-            cand = block_reduce(cand, imin, s_red);
+            cand = block_reduce(cand, imin, s_red, nw);
             if (tid == 0) first[istar] = (cand == INT_MAX) ? -1 : cand;
             __syncthreads();
         }
@@ -875,7 +893,7 @@ finalize_small_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_hea
     if (lane == 31) s_red[warp] = v;
     __syncthreads();
     if (warp == 0) {
-        int t = s_red[lane];
+        int t = lane < nw ? s_red[lane] : 0;
         for (int o = 1; o < 32; o <<= 1) {
             const int u = __shfl_up_sync(0xffffffffu, t, o);
             if (lane >= o) t += u;
@@ -884,6 +902,7 @@ finalize_small_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_hea
     }
     __syncthreads();
     const int pos = (warp > 0 ? s_red[warp - 1] : 0) + v - keep;
+    if (tid == 0) s_carry = s_red[nw - 1];
     if (keep && pos < out_cap) {
         const SmallBlob b = sb[tid];
         dogblob_blob o;
@@ -891,8 +910,6 @@ finalize_small_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_hea
         o.slice = b.slice; o.flags = b.flags;
         out[pos] = o;
     }
-    if (tid == blockDim.x - 1) s_carry = pos + keep;
-    __syncthreads();
     if (tid == 0) {
         const Counters c = *bs.ctr;
         hdr->n_blobs = min(s_carry, out_cap);
@@ -904,6 +921,9 @@ finalize_small_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_hea
         if (c.n_plateau > bs.cap || s_carry > out_cap) f |= DOGBLOB_FLAG_OVERFLOW;
         hdr->flags = f;
         hdr->capacity = out_cap;
+        for (int q = 0; q < 4; ++q) hdr->prune_profile[q] = 0;
+        hdr->reserved[0] = hdr->reserved[1] = 0;
+        write_stage_times(c, hdr);
         bs.ctr->small_done = 1;
     }
 }

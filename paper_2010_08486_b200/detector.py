@@ -169,12 +169,28 @@ class RadiusHistogram:
     volume_weights: np.ndarray = field(repr=False)
 
 
-@dataclass(frozen=True)
 class DetectResult:
-    blobs: BlobSet
-    histogram: RadiusHistogram
-    timings_ms: dict
-    stats: dict = field(default_factory=dict)   # n_flagged / n_plateau / n_candidates / n_merges
+    """detector.py:55-64 `DetectResult(blobs, histogram, timings_ms)`, plus `stats`.
+
+    `histogram` may be given as a zero-argument callable: it is then evaluated on first access
+    (the single-frame latency path does not pay for a histogram nobody reads)."""
+    __slots__ = ("blobs", "_histogram", "timings_ms", "stats")
+
+    def __init__(self, blobs, histogram, timings_ms, stats=None):
+        self.blobs = blobs
+        self._histogram = histogram
+        self.timings_ms = timings_ms
+        self.stats = {} if stats is None else stats   # n_flagged / n_plateau / n_candidates / n_merges
+
+    @property
+    def histogram(self) -> "RadiusHistogram":
+        h = self._histogram
+        if callable(h):
+            h = self._histogram = h()
+        return h
+
+    def __repr__(self):
+        return f"DetectResult(blobs={self.blobs!r}, timings_ms={self.timings_ms!r})"
 
 
 # --------------------------------------------------------------------------
@@ -264,13 +280,9 @@ def free_events(events) -> None:
 
 def event_intervals_ms(events) -> list:
     """[row pass, column+DoG pass, extrema, prune+pack] in milliseconds."""
-    lib = _lib.load()
-    out = []
-    for k in range(N_EVENTS - 1):
-        ms = C.c_float()
-        _lib.check(lib.dogblob_event_elapsed_ms(events[k], events[k + 1], C.byref(ms)))
-        out.append(float(ms.value))
-    return out
+    out = (C.c_float * (N_EVENTS - 1))()
+    _lib.check(_lib.load().dogblob_event_intervals_ms(events, N_EVENTS, out))
+    return list(out)
 
 
 class _Slot:
@@ -297,7 +309,6 @@ class _Slot:
         self.h_result_np = self.h_result.numpy()
         self.h_image_np = self.h_image.numpy()
         self.n_host = n_host
-        self.events = new_events()
         torch.cuda.synchronize(dev)
         self.pending = None     # bookkeeping of run_batch
 
@@ -314,7 +325,7 @@ class _Slot:
             self.plan.handle, src, float(np.float32(params.threshold)), int(params.neighborhood),
             float(params.overlap), 1 if prune else 0, self.d_image.data_ptr(),
             self.d_work.data_ptr(), self.d_result.data_ptr(), self.h_result.data_ptr(),
-            self.n_host, self.stream.cuda_stream, self.events))
+            self.n_host, self.stream.cuda_stream, None))   # stage times come back in the header
 
     def _launch_with_preprocess(self, src: int, params: DetectionParams, prune: bool) -> None:
         """raw frame H2D -> smooth + stretch on the device (images.py:153-157) -> detect."""
@@ -352,8 +363,7 @@ class _Slot:
         _lib.check(lib.dogblob_detect(
             self.plan.handle, d_frame.data_ptr(), float(np.float32(params.threshold)),
             int(params.neighborhood), float(params.overlap), 1 if prune else 0,
-            self.d_work.data_ptr(), self.d_result.data_ptr(), self.stream.cuda_stream,
-            self.events if events is None else events))
+            self.d_work.data_ptr(), self.d_result.data_ptr(), self.stream.cuda_stream, events))
 
     def _host_pointer(self, frame) -> int:
         torch = _torch()
@@ -389,19 +399,19 @@ class _Slot:
             self.stream.synchronize()
         return hdr, recs
 
-    def stage_times_ms(self) -> dict:
-        t = event_intervals_ms(self.events)
+    def stage_times_ms(self, hdr) -> dict:
+        """timings_ms of the frame just collected: device-side stamps from the result header
+        (no event calls on the latency path); pre-processing is bracketed by two events."""
         pre = 0.0
         if getattr(self, "preprocessed", False):
             ms = C.c_float()
             _lib.check(_lib.load().dogblob_event_elapsed_ms(self.pre_events[0], self.pre_events[1],
                                                             C.byref(ms)))
             pre = float(ms.value)
-        return {"preprocess_ms": pre, "convolve_ms": t[0] + t[1], "extrema_ms": t[2],
-                "prune_ms": t[3]}
+        return {"preprocess_ms": pre, "convolve_ms": int(hdr["conv_ns"]) * 1e-6,
+                "extrema_ms": int(hdr["extrema_ns"]) * 1e-6, "prune_ms": int(hdr["prune_ns"]) * 1e-6}
 
     def close(self):
-        free_events(self.events)
         if self.pre_events is not None:
             lib = _lib.load()
             for k in range(2):
@@ -521,12 +531,14 @@ class Detector:
     def _finish(self, slot: _Slot, hdr, recs, shape, timings) -> DetectResult:
         blobs = BlobSet(records=recs, source_shape=(shape[1], shape[0]), params=self.params)
         stats = {k: int(hdr[k]) for k in ("n_flagged", "n_plateau", "n_candidates", "n_merges")}
-        if int(hdr["reserved"][6]):      # whole-GPU pruning kernel ran: its phase profile
-            r = [int(v) for v in hdr["reserved"]]
+        prof = [int(v) & 0xFFFFFFFF for v in hdr["prune_profile"]]
+        if prof[3]:                      # whole-GPU pruning kernel ran: its phase profile
+            r = [prof[0] & 0xFFFF, prof[0] >> 16, prof[1] & 0xFFFF, prof[1] >> 16, prof[2] & 0xFFFF, prof[2] >> 16]
             stats["prune_profile"] = {"order_us": r[0], "grid_first_us": r[1] - r[0], "bound_us": r[2] - r[1],
-                                      "parts_us": r[3] - r[2], "merge_us": r[4] - r[3], "pack_us": r[6] - r[4],
-                                      "total_us": r[6], "sweeps": r[7], "parts": r[8]}
-        return DetectResult(blobs=blobs, histogram=histogram(blobs, self.ladder),
+                                      "parts_us": r[3] - r[2], "merge_us": r[4] - r[3], "pack_us": r[5] - r[4],
+                                      "total_us": r[5], "sweeps": prof[3] >> 24, "parts": prof[3] & 0xFFFFFF}
+        ladder = self.ladder
+        return DetectResult(blobs=blobs, histogram=lambda: histogram(blobs, ladder),
                             timings_ms=timings, stats=stats)
 
     # -- public API -------------------------------------------------------------
@@ -543,7 +555,7 @@ class Detector:
             try:
                 slot.launch(img, p, p.prune)
                 hdr, recs = slot.collect()
-                timings = slot.stage_times_ms()
+                timings = slot.stage_times_ms(hdr)
             finally:
                 eng.free.put(slot)
             if recs is not None:
@@ -573,7 +585,7 @@ class Detector:
                 if recs is None:
                     retry.append(idx)
                     return
-                t = slot.stage_times_ms() if timings else {}
+                t = slot.stage_times_ms(hdr) if timings else {}
                 results[idx] = self._finish(slot, hdr, recs, shape, t)
 
             for i, frame in enumerate(frames):

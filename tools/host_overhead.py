@@ -27,7 +27,7 @@ for name in (sys.argv[1:] or ["C1", "C2"]):
         t2 = time.perf_counter()
         hdr, recs = slot.collect()
         t3 = time.perf_counter()
-        tm = slot.stage_times_ms()
+        tm = slot.stage_times_ms(hdr)
         t4 = time.perf_counter()
         eng.free.put(slot)
         res = det._finish(slot, hdr, recs, tuple(frame.shape), tm)
@@ -35,6 +35,6 @@ for name in (sys.argv[1:] or ["C1", "C2"]):
         acc += [t1 - t0, t2 - t1, t3 - t2, t4 - t3, t5 - t4, t5 - t0]
     acc *= 1e6 / n
     dev = sum(tm.values()) * 1e3
-    print(f"{name}: slot {acc[0]:.1f} us | launch call {acc[1]:.1f} | wait+decode {acc[2]:.1f} | event times {acc[3]:.1f} "
+    print(f"{name}: slot {acc[0]:.1f} us | launch call {acc[1]:.1f} | wait+decode {acc[2]:.1f} | stage times {acc[3]:.1f} "
           f"| finish (BlobSet, histogram) {acc[4]:.1f} | total {acc[5]:.1f} us | device stages {dev:.1f} us")
     det.close()
