@@ -128,6 +128,25 @@ int dogblob_detect_host(const dogblob_plan *plan, const float *h_image,
                         void *d_image, void *d_workspace, void *d_result,
                         void *h_result, int h_result_blobs, void *stream,
                         void *const *events);
+/* dogblob_detect_host with the upload overlapped: the frame goes up in row chunks on
+ * `copy_stream`, each followed by a 4-byte copy of a gate word, while the row pass already runs
+ * on `stream` and every tile waits only for the image rows it reads (a 1024^2 frame starts
+ * computing after the first quarter has arrived).
+ *   h_image      PINNED host frame (stays untouched until the stream has been synchronised)
+ *   copy_stream  a second stream of the caller, different from `stream`
+ *   h_gate       pinned int32[DOGBLOB_GATE_INTS], zeroed once; belongs to this buffer set
+ *   frame_done   event (dogblob_event_create) of this buffer set: recorded here behind the
+ *                frame's last operation; the next call waits on it before it overwrites d_image
+ * One buffer set (d_image, d_workspace, d_result, h_result, h_gate, frame_done) = one frame in
+ * flight: synchronise `stream` before the set is used again. */
+#define DOGBLOB_GATE_CHUNKS 4
+#define DOGBLOB_GATE_INTS 16
+int dogblob_detect_host_streamed(const dogblob_plan *plan, const float *h_image,
+                                 float threshold, int neighborhood, double overlap, int prune,
+                                 void *d_image, void *d_workspace, void *d_result,
+                                 void *h_result, int h_result_blobs, void *stream,
+                                 void *copy_stream, int32_t *h_gate, void *frame_done,
+                                 void *const *events);
 int dogblob_upload_image(const dogblob_plan *plan, const float *h_image,
                          void *d_image, void *stream);
 int dogblob_fetch_blobs(const void *d_result, int first, int count,

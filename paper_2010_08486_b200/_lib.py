@@ -20,6 +20,7 @@ FLAG_OVERFLOW = 1
 BLOB_SCALE_EDGE = 1
 BLOB_MERGED = 2
 RESULT_HEADER_BYTES = 64
+GATE_INTS = 16
 
 # numpy mirrors of the C structs
 BLOB_DTYPE = np.dtype([("x", "<f8"), ("y", "<f8"), ("sigma", "<f8"), ("radius", "<f8"),
@@ -42,6 +43,8 @@ SIGNATURES = {
     "dogblob_image_pitch": (_i64, [_vp]),
     "dogblob_detect": (_i, [_vp, _vp, _f, _i, _d, _i, _vp, _vp, _vp, _vp]),
     "dogblob_detect_host": (_i, [_vp, _vp, _f, _i, _d, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp]),
+    "dogblob_detect_host_streamed": (_i, [_vp, _vp, _f, _i, _d, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp,
+                                          _vp, _vp]),
     "dogblob_upload_image": (_i, [_vp, _vp, _vp, _vp]),
     "dogblob_fetch_blobs": (_i, [_vp, _i, _i, _vp, _vp]),
     "dogblob_fetch_result": (_i, [_vp, _i, _vp, _vp]),

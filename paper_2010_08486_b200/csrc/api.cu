@@ -77,7 +77,7 @@ struct dogblob_plan {
     double *d_slice_sigma = nullptr;
     float *d_sigma_f32 = nullptr;
     // workspace layout (bytes from the workspace base)
-    size_t off_rows_t = 0, off_dog_t = 0, off_edge = 0, off_blobspace = 0, total = 0;
+    size_t off_rows_t = 0, off_dog_t = 0, off_edge = 0, off_blobspace = 0, off_gate = 0, total = 0;
 };
 
 namespace {
@@ -270,6 +270,7 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
     plan->off_dog_t = off;  off += align_up(plane * n_levels, 256);   // L planes: also holds levels
     plan->off_edge = off;   off += align_up(plane * 2 * g.G, 256);       // boundary levels
     plan->off_blobspace = off; off += blobspace_bytes(max_blobs);
+    plan->off_gate = off;   off += 256;                                   // streamed upload: gate word
     plan->total = off;
     *out = plan;
     return DOGBLOB_OK;
@@ -300,14 +301,22 @@ static int check_threshold_args(int neighborhood, double overlap) {
     return DOGBLOB_OK;
 }
 
-int dogblob_detect(const dogblob_plan *plan, const float *d_image, float threshold,
-                   int neighborhood, double overlap, int prune, void *d_workspace,
-                   void *d_result, void *stream, void *const *events) {
-    DB_REQUIRE(plan && d_image && d_workspace && d_result, "NULL argument");
-    if (int rc = check_threshold_args(neighborhood, overlap)) return rc;
-    DeviceGuard guard(plan->device);
-    DB_REQUIRE(guard.ok, "cannot select CUDA device");
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+// reset + row pass (optionally gated on a streamed upload), then the rest of the frame
+static int launch_frame_head(const dogblob_plan *plan, const float *d_image, void *d_workspace,
+                             cudaStream_t st, void *const *events, const RowGate *gate) {
+    char *ws = reinterpret_cast<char *>(d_workspace);
+    float *rows_t = reinterpret_cast<float *>(ws + plan->off_rows_t);
+    BlobSpace bs = carve_blobspace(ws + plan->off_blobspace, plan->max_blobs);
+    if (events) DB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(events[0]), st));
+    DB_CUDA(launch_reset_counters(bs, st));
+    DB_CUDA(launch_row_pass(plan->geo, d_image, rows_t, plan->table, plan->d_taps, st, gate));
+    if (events) DB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(events[1]), st));
+    return DOGBLOB_OK;
+}
+
+static int launch_frame_tail(const dogblob_plan *plan, float threshold, int neighborhood,
+                             double overlap, int prune, void *d_workspace, void *d_result,
+                             cudaStream_t st, void *const *events) {
     char *ws = reinterpret_cast<char *>(d_workspace);
     float *rows_t = reinterpret_cast<float *>(ws + plan->off_rows_t);
     float *dog_t = reinterpret_cast<float *>(ws + plan->off_dog_t);
@@ -317,10 +326,6 @@ int dogblob_detect(const dogblob_plan *plan, const float *d_image, float thresho
         return events ? cudaEventRecord(reinterpret_cast<cudaEvent_t>(events[k]), st)
                       : cudaSuccess;
     };
-    DB_CUDA(ev(0));
-    DB_CUDA(launch_reset_counters(bs, st));
-    DB_CUDA(launch_row_pass(g, d_image, rows_t, plan->table, plan->d_taps, st));
-    DB_CUDA(ev(1));
     DB_CUDA(launch_col_dog_pass(g, rows_t, dog_t, reinterpret_cast<float *>(ws + plan->off_edge),
                                 plan->table, plan->d_taps, st));
     DB_CUDA(ev(2));
@@ -331,6 +336,19 @@ int dogblob_detect(const dogblob_plan *plan, const float *d_image, float thresho
     DB_CUDA(launch_prune_and_pack(bs, overlap, prune != 0, d_result, plan->max_blobs, st));
     DB_CUDA(ev(4));
     return DOGBLOB_OK;
+}
+
+int dogblob_detect(const dogblob_plan *plan, const float *d_image, float threshold,
+                   int neighborhood, double overlap, int prune, void *d_workspace,
+                   void *d_result, void *stream, void *const *events) {
+    DB_REQUIRE(plan && d_image && d_workspace && d_result, "NULL argument");
+    if (int rc = check_threshold_args(neighborhood, overlap)) return rc;
+    DeviceGuard guard(plan->device);
+    DB_REQUIRE(guard.ok, "cannot select CUDA device");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (int rc = launch_frame_head(plan, d_image, d_workspace, st, events, nullptr)) return rc;
+    return launch_frame_tail(plan, threshold, neighborhood, overlap, prune, d_workspace, d_result, st,
+                             events);
 }
 
 int dogblob_upload_image(const dogblob_plan *plan, const float *h_image, void *d_image,
@@ -359,6 +377,73 @@ int dogblob_detect_host(const dogblob_plan *plan, const float *h_image, float th
     DB_CUDA(cudaMemcpyAsync(h_result, d_result,
                             DOGBLOB_RESULT_HEADER_BYTES + (size_t)nb * sizeof(dogblob_blob),
                             cudaMemcpyDeviceToHost, reinterpret_cast<cudaStream_t>(stream)));
+    return DOGBLOB_OK;
+}
+
+int dogblob_detect_host_streamed(const dogblob_plan *plan, const float *h_image, float threshold,
+                                 int neighborhood, double overlap, int prune, void *d_image,
+                                 void *d_workspace, void *d_result, void *h_result,
+                                 int h_result_blobs, void *stream, void *copy_stream,
+                                 int32_t *h_gate, void *frame_done, void *const *events) {
+    DB_REQUIRE(plan && h_image && d_image && d_workspace && d_result, "NULL argument");
+    DB_REQUIRE(h_result != nullptr && h_result_blobs >= 0, "bad host result buffer");
+    DB_REQUIRE(copy_stream && h_gate && frame_done && copy_stream != stream,
+               "streamed upload needs its own copy stream, a pinned gate array and an event");
+    if (int rc = check_threshold_args(neighborhood, overlap)) return rc;
+    DeviceGuard guard(plan->device);
+    DB_REQUIRE(guard.ok, "cannot select CUDA device");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(copy_stream);
+    cudaEvent_t done = reinterpret_cast<cudaEvent_t>(frame_done);
+    const ConvGeometry &g = plan->geo;
+    int *d_word = reinterpret_cast<int *>(reinterpret_cast<char *>(d_workspace) + plan->off_gate);
+
+    // row chunks: at most DOGBLOB_GATE_CHUNKS, whole multiples of 64 rows
+    int rows_per_chunk = ((g.H + DOGBLOB_GATE_CHUNKS - 1) / DOGBLOB_GATE_CHUNKS + 63) / 64 * 64;
+    const int n_chunks = (g.H + rows_per_chunk - 1) / rows_per_chunk;
+    // h_gate[0]: gate value before this frame (0 = first use: initialise the device word);
+    // h_gate[1 + c]: value copied behind chunk c.  The previous frame of these buffers has been
+    // collected by the caller, so its copies are complete and the array can be rewritten.
+    if (h_gate[0] == 0) {
+        h_gate[0] = 1;
+        DB_CUDA(cudaMemcpy(d_word, h_gate, sizeof(int), cudaMemcpyHostToDevice));
+    }
+    const int base = h_gate[0];
+    for (int c = 0; c < n_chunks; ++c) h_gate[1 + c] = base + c + 1;
+    h_gate[0] = base + n_chunks;
+    if (h_gate[0] > 0x3fffffff) h_gate[0] = 0;   // re-initialise long before the counter wraps
+
+    DB_CUDA(cudaStreamWaitEvent(cs, done, 0));    // the buffers' previous frame is off the device
+    BlobSpace bs0 = carve_blobspace(reinterpret_cast<char *>(d_workspace) + plan->off_blobspace,
+                                    plan->max_blobs);
+    const RowGate gate{d_word, base, rows_per_chunk, &bs0.ctr->t_start};
+    if (int rc = launch_frame_head(plan, reinterpret_cast<const float *>(d_image), d_workspace, st,
+                                   events, &gate))
+        return rc;
+    // from here on the row pass is spinning on the gate: every path must deliver the last value
+    cudaError_t err = cudaSuccess;
+    for (int c = 0; c < n_chunks && err == cudaSuccess; ++c) {
+        const int r0 = c * rows_per_chunk, nr = std::min(rows_per_chunk, g.H - r0);
+        err = cudaMemcpy2DAsync(reinterpret_cast<float *>(d_image) + (size_t)r0 * g.Wp,
+                                (size_t)g.Wp * sizeof(float), h_image + (size_t)r0 * g.W,
+                                (size_t)g.W * sizeof(float), (size_t)g.W * sizeof(float), nr,
+                                cudaMemcpyHostToDevice, cs);
+        if (err == cudaSuccess)
+            err = cudaMemcpyAsync(d_word, h_gate + 1 + c, sizeof(int), cudaMemcpyHostToDevice, cs);
+    }
+    if (err != cudaSuccess) {
+        cudaMemcpy(d_word, h_gate + n_chunks, sizeof(int), cudaMemcpyHostToDevice);   // release the kernel
+        set_error(std::string("streamed upload: ") + cudaGetErrorString(err));
+        return DOGBLOB_ECUDA;
+    }
+    if (int rc = launch_frame_tail(plan, threshold, neighborhood, overlap, prune, d_workspace,
+                                   d_result, st, events))
+        return rc;
+    const int nb = std::min(h_result_blobs, plan->max_blobs);
+    DB_CUDA(cudaMemcpyAsync(h_result, d_result,
+                            DOGBLOB_RESULT_HEADER_BYTES + (size_t)nb * sizeof(dogblob_blob),
+                            cudaMemcpyDeviceToHost, st));
+    DB_CUDA(cudaEventRecord(done, st));
     return DOGBLOB_OK;
 }
 

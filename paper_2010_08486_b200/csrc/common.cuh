@@ -136,8 +136,12 @@ struct ConvGeometry {
     int max_rpad;        // largest padded radius
 };
 
+// streamed row pass: `word` (device int) holds base + k once row chunks 0..k-1 of the frame are
+// resident; chunk c = image rows [c * rows_per_chunk, (c + 1) * rows_per_chunk)
+struct RowGate { const int *word; int base; int rows_per_chunk; unsigned long long *t_start; };
 cudaError_t launch_row_pass(const ConvGeometry &g, const float *d_img, float *d_rows_t,
-                            const LevelTable &tbl, const float2 *d_taps, cudaStream_t st);
+                            const LevelTable &tbl, const float2 *d_taps, cudaStream_t st,
+                            const RowGate *gate = nullptr);
 cudaError_t launch_col_dog_pass(const ConvGeometry &g, const float *d_rows_t, float *d_dog_t,
                                 float *d_edge, const LevelTable &tbl, const float2 *d_taps,
                                 cudaStream_t st);

@@ -45,10 +45,14 @@ __device__ __forceinline__ void stage_row_offsets(int *s_rows, int first_row, in
         s_rows[i] = fold_row(first_row + i, n_rows) * pitch;
 }
 
-template <bool ADJACENT>
+template <bool ADJACENT, bool NC = true>
 __device__ __forceinline__ void load_row(const float *__restrict__ row, int lane, float (&v)[4]) {
     if (ADJACENT) {
-        float4 q = __ldg(reinterpret_cast<const float4 *>(row) + lane);
+        // NC = false: the frame may still be arriving while the kernel runs (streamed row
+        // pass), so the read-only (non-coherent) path is not allowed
+        float4 q;
+        if (NC) q = __ldg(reinterpret_cast<const float4 *>(row) + lane);
+        else q = __ldcg(reinterpret_cast<const float4 *>(row) + lane);
         v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
     } else {
 #pragma unroll
@@ -76,6 +80,7 @@ __device__ __forceinline__ void prefetch_l2(const void *p) {
 constexpr int kL2Ahead = 16;
 
 // one full chunk: 16 sub-steps, each feeds all 16 outputs
+template <bool NC>
 __device__ __forceinline__ void full_chunk(const float *__restrict__ in,
                                            const int *__restrict__ rows,
                                            const float2 *__restrict__ taps, int lane,
@@ -86,7 +91,7 @@ __device__ __forceinline__ void full_chunk(const float *__restrict__ in,
         ring[u] = taps[u];
         const float2 a = make_float2(v[u % kPrefetch][0], v[u % kPrefetch][1]);
         const float2 b = make_float2(v[u % kPrefetch][2], v[u % kPrefetch][3]);
-        load_row<true>(in + rows[u], lane, v[u % kPrefetch]);
+        load_row<true, NC>(in + rows[u], lane, v[u % kPrefetch]);
         if (frontier && (u & 3) == 0)     // 4 rows x 4 lines per request group
             prefetch_l2(in + rows[u + kL2Ahead + (lane >> 3)] + (lane & 7) * 16);
 #pragma unroll
@@ -104,6 +109,7 @@ __device__ __forceinline__ void full_chunk(const float *__restrict__ in,
 // cold straight-line blocks, but 256 instead of 136 FMA groups: row pass +3..10 %), and
 // 8 instead of 4 rows in flight during the head (+0 %): the FMA pipe, not the head's load
 // latency or instruction fetch, sets the pace.
+template <bool NC = true>
 __device__ __forceinline__ void sweep(const float *__restrict__ in, const int *__restrict__ rows,
                                       int n_mid, const float2 *__restrict__ taps, int lane,
                                       float (&v)[kPrefetch][4], float2 (&acc)[kTY][2],
@@ -116,7 +122,7 @@ __device__ __forceinline__ void sweep(const float *__restrict__ in, const int *_
         ring[u] = taps[u];
         const float2 a = make_float2(v[u % kPrefetch][0], v[u % kPrefetch][1]);
         const float2 b = make_float2(v[u % kPrefetch][2], v[u % kPrefetch][3]);
-        load_row<true>(in + rows[u], lane, v[u % kPrefetch]);
+        load_row<true, NC>(in + rows[u], lane, v[u % kPrefetch]);
 #pragma unroll
         for (int j = 0; j <= u; ++j) {
             const float2 t = ring[u - j];
@@ -133,7 +139,7 @@ __device__ __forceinline__ void sweep(const float *__restrict__ in, const int *_
     rows += kTY;
     // ---- middle chunks ----
     for (int chunk = 0; chunk < n_mid; ++chunk) {
-        full_chunk(in, rows, taps, lane, v, ring, acc, frontier);
+        full_chunk<NC>(in, rows, taps, lane, v, ring, acc, frontier);
         taps += kTY;
         rows += kTY;
     }
@@ -143,7 +149,7 @@ __device__ __forceinline__ void sweep(const float *__restrict__ in, const int *_
     for (int u = 0; u < kTY; ++u) {
         const float2 a = make_float2(v[u % kPrefetch][0], v[u % kPrefetch][1]);
         const float2 b = make_float2(v[u % kPrefetch][2], v[u % kPrefetch][3]);
-        if (u + kPrefetch < kTY) load_row<true>(in + rows[u], lane, v[u % kPrefetch]);
+        if (u + kPrefetch < kTY) load_row<true, NC>(in + rows[u], lane, v[u % kPrefetch]);
 #pragma unroll
         for (int j = u; j < kTY; ++j) {
             const float2 t = ring[(u - j + kTY) % kTY];
@@ -178,35 +184,53 @@ __device__ __forceinline__ int tile_index(int x, int y4) {        // y4 = y / 4
     return x * kTileRows + (((y4 ^ (x >> 2)) & 31) << 2);
 }
 
+// STREAMED: the frame is still being copied in (row chunks on another stream, each followed by
+// a copy of the gate word: gate.base + k once chunks 0..k-1 are resident).  Tile rows are the
+// slowest grid index, so early CTAs need early chunks only; a CTA waits for the last image row
+// it reads.  The kernel must not be launched unless the copies WILL be issued (it spins).
+template <bool STREAMED>
 __global__ void __launch_bounds__(kConvThreads, 2)
 row_pass_kernel(const float *__restrict__ img, int64_t img_pitch, int H,
                 float *__restrict__ out_t, int64_t out_pitch, int64_t out_plane,
                 const __grid_constant__ LevelTable tbl, const float2 *__restrict__ g_taps,
-                int max_table) {
+                int max_table, RowGate gate) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float *tile = reinterpret_cast<float *>(smem_raw);                       // [128 x][128 y]
     float2 *s_taps = reinterpret_cast<float2 *>(tile + kTileCols * kTileRows);
     int *s_rows = reinterpret_cast<int *>(s_taps + max_table);
 
-    const int level = tbl.order[blockIdx.z];
+    const int level = tbl.order[STREAMED ? blockIdx.y : blockIdx.z];
     const LevelDesc lv = tbl.lv[level];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int col0 = blockIdx.x * kTileCols;            // x
-    const int row0 = blockIdx.y * kTileRows;            // y
+    const int row0 = (STREAMED ? blockIdx.z : blockIdx.y) * kTileRows;   // y
+    if (STREAMED) {
+        // last image row this tile touches (reflection folds rows below 0 upwards)
+        const int need_row = lv.rpad >= H ? H - 1
+                                          : min(H - 1, max(row0 + kTileRows - 1 + lv.rpad, lv.rpad - row0 - 1));
+        const int need = need_row / gate.rows_per_chunk + 1;
+        if (threadIdx.x == 0) {
+            while (*(const volatile int *)gate.word - gate.base < need) __nanosleep(200);
+            __threadfence();
+            // the frame's compute clock starts when its first tile has its rows
+            if ((blockIdx.x | blockIdx.y | blockIdx.z) == 0 && gate.t_start) *gate.t_start = globaltimer_ns();
+        }
+        __syncthreads();
+    }
     // everything with memory latency is issued before the barrier: taps (async copy) and
     // the first input rows of this warp (offsets folded directly, the table is not ready yet)
     stage_taps_async(s_taps, g_taps + lv.tap_ofs, table_len(lv));
     float v[kPrefetch][4];
 #pragma unroll
     for (int p = 0; p < kPrefetch; ++p)
-        load_row<true>(img + col0 + (int64_t)fold_row(row0 + warp * kTY - lv.rpad + p, H) * img_pitch,
-                       lane, v[p]);
+        load_row<true, !STREAMED>(img + col0 + (int64_t)fold_row(row0 + warp * kTY - lv.rpad + p, H) * img_pitch,
+                                  lane, v[p]);
     stage_row_offsets(s_rows, row0 - lv.rpad, kTileRows + 2 * lv.rpad + kPrefetch, H, (int)img_pitch);
     cp_async_wait_all();
     __syncthreads();
 
     float2 acc[kTY][2];
-    sweep(img + col0, s_rows + warp * kTY, lv.n_mid, s_taps, lane, v, acc);
+    sweep<!STREAMED>(img + col0, s_rows + warp * kTY, lv.n_mid, s_taps, lane, v, acc);
 
 #pragma unroll
     for (int q = 0; q < kTY / 4; ++q) {                 // four consecutive y per store
@@ -420,7 +444,9 @@ cudaError_t configure_conv_kernels(int device) {
     int optin = 0;
     cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(row_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    e = cudaFuncSetAttribute(row_pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(row_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(col_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e != cudaSuccess) return e;
@@ -429,11 +455,20 @@ cudaError_t configure_conv_kernels(int device) {
 }
 
 cudaError_t launch_row_pass(const ConvGeometry &g, const float *d_img, float *d_rows_t,
-                            const LevelTable &tbl, const float2 *d_taps, cudaStream_t st) {
-    dim3 grid(g.Wp / kTileCols, g.Hp / kTileRows, g.L);
+                            const LevelTable &tbl, const float2 *d_taps, cudaStream_t st,
+                            const RowGate *gate) {
     const size_t smem = row_pass_smem(g.max_table, g.max_rpad);
-    row_pass_kernel<<<grid, kConvThreads, smem, st>>>(d_img, g.Wp, g.H, d_rows_t, g.Hp,
-                                                      (int64_t)g.Hp * g.Wp, tbl, d_taps, g.max_table);
+    if (gate) {
+        dim3 grid(g.Wp / kTileCols, g.L, g.Hp / kTileRows);
+        row_pass_kernel<true><<<grid, kConvThreads, smem, st>>>(d_img, g.Wp, g.H, d_rows_t, g.Hp,
+                                                                (int64_t)g.Hp * g.Wp, tbl, d_taps,
+                                                                g.max_table, *gate);
+    } else {
+        dim3 grid(g.Wp / kTileCols, g.Hp / kTileRows, g.L);
+        row_pass_kernel<false><<<grid, kConvThreads, smem, st>>>(d_img, g.Wp, g.H, d_rows_t, g.Hp,
+                                                                 (int64_t)g.Hp * g.Wp, tbl, d_taps,
+                                                                 g.max_table, RowGate{nullptr, 0, 1, nullptr});
+    }
     return cudaGetLastError();
 }
 

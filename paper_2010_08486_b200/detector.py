@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import queue
 import threading
 from dataclasses import asdict, dataclass, field
@@ -40,6 +41,8 @@ RADIUS_PER_SIGMA = math.sqrt(2.0)
 DEFAULT_STACK_ELEMENT_CAP = 2 ** 28   # convolve.py:37 (the reference's host-RAM guard)
 DEFAULT_MAX_BLOBS = 1 << 16
 HOST_RESULT_BLOBS = 4096              # records copied back with the header in one D2H
+STREAM_MIN_BYTES = 1 << 20            # frames from 1 MiB upload in row chunks under the row pass
+STREAMED_UPLOAD = os.environ.get("DOGBLOB_STREAMED_UPLOAD", "1") != "0"
 
 
 # --------------------------------------------------------------------------
@@ -302,6 +305,12 @@ class _Slot:
         self.d_raw = None          # raw frame + scratch, allocated on first preprocess=True use
         self.d_pre = None
         self.h_status = torch.zeros(1, dtype=torch.int32).pin_memory()
+        # streamed upload (frames of at least STREAM_MIN_BYTES): second stream, gate, frame event
+        self.copy_stream = torch.cuda.Stream(device=dev)
+        self.h_gate = torch.zeros(_lib.GATE_INTS, dtype=torch.int32).pin_memory()
+        done = C.c_void_p()
+        _lib.check(lib.dogblob_event_create(C.byref(done)))
+        self.frame_done = done
         self.pre_events = None
         n_host = min(HOST_RESULT_BLOBS, plan.max_blobs)
         self.h_result = torch.zeros(_lib.RESULT_HEADER_BYTES + n_host * _lib.BLOB_DTYPE.itemsize,
@@ -320,6 +329,16 @@ class _Slot:
         self.preprocessed = bool(params.preprocess)
         if params.preprocess:
             self._launch_with_preprocess(src, params, prune)
+            return
+        H, W = self.plan.shape
+        if STREAMED_UPLOAD and H * W * 4 >= STREAM_MIN_BYTES:
+            # row chunks on the copy stream while the row pass already runs
+            _lib.check(lib.dogblob_detect_host_streamed(
+                self.plan.handle, src, float(np.float32(params.threshold)), int(params.neighborhood),
+                float(params.overlap), 1 if prune else 0, self.d_image.data_ptr(),
+                self.d_work.data_ptr(), self.d_result.data_ptr(), self.h_result.data_ptr(),
+                self.n_host, self.stream.cuda_stream, self.copy_stream.cuda_stream,
+                self.h_gate.data_ptr(), self.frame_done, None))
             return
         _lib.check(lib.dogblob_detect_host(
             self.plan.handle, src, float(np.float32(params.threshold)), int(params.neighborhood),
@@ -412,6 +431,9 @@ class _Slot:
                 "extrema_ms": int(hdr["extrema_ns"]) * 1e-6, "prune_ms": int(hdr["prune_ns"]) * 1e-6}
 
     def close(self):
+        if self.frame_done is not None:
+            _lib.load().dogblob_event_destroy(self.frame_done)
+            self.frame_done = None
         if self.pre_events is not None:
             lib = _lib.load()
             for k in range(2):

@@ -171,6 +171,30 @@ class TestDetectorBehaviour:
                 assert a.stats["n_merges"] == b.stats["n_merges"]
         det.close()
 
+    @pytest.mark.parametrize("shape,kw", [((600, 700), dict(min_sigma=1.0, max_sigma=8.0, n_bin=7)),
+                                          ((515, 520), dict(min_sigma=30.0, max_sigma=120.0, n_bin=3)),
+                                          ((1024, 1024), dict(min_sigma=2.0, max_sigma=12.0, n_bin=10))])
+    def test_streamed_upload_equals_plain_upload(self, shape, kw, monkeypatch):
+        """frames of >= 1 MiB go up in row chunks under the running row pass (gate word per
+        chunk); same records as the single pitched copy, also when the widest kernel exceeds
+        the image (every tile then waits for the whole frame) and with ragged last chunks"""
+        from paper_2010_08486_b200 import detector as D
+        frames = [synth.sensor_noise(synth.droplet_scene(shape[1], shape[0], 40, (3.0, 14.0), seed=11 + i,
+                                                         allow_overlap=True), seed=31 + i).image for i in range(3)]
+        params = P.DetectionParams(preprocess=False, **kw)
+        monkeypatch.setattr(D, "STREAMED_UPLOAD", False)
+        det = P.Detector(params)
+        plain = [det.run(f).blobs.records for f in frames]
+        det.close()
+        monkeypatch.setattr(D, "STREAMED_UPLOAD", True)
+        det = P.Detector(params, slots=2)
+        for _ in range(3):                               # the gate counter advances from frame to frame
+            for f, want in zip(frames, plain):
+                assert np.array_equal(det.run(f).blobs.records, want)
+        for got, want in zip(det.run_batch(frames * 2), plain * 2):
+            assert np.array_equal(got.blobs.records, want)
+        det.close()
+
     def test_shared_detector_from_threads(self):
         det = P.Detector(params_for("C1"), slots=2)
         frame = synth.config_frame("C1")
