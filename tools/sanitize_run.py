@@ -26,6 +26,10 @@ det = P.Detector(P.DetectionParams(preprocess=False, min_sigma=1.0, max_sigma=6.
 res = det.run(dense)
 print("dense", len(res.blobs), res.stats)
 det.close()
+big = synth.sensor_noise(synth.droplet_scene(700, 600, 30, (3.0, 9.0), seed=7, allow_overlap=True), seed=8).image
+det = P.Detector(P.DetectionParams(preprocess=False, min_sigma=1.0, max_sigma=5.0, n_bin=4))
+print("streamed upload", [len(det.run(big).blobs) for _ in range(2)])     # >= 1 MiB: row chunks + gate word
+det.close()
 sl = (rng.random((2, 60, 70)) * 0.05).astype(np.float32)
 sl[0, 10:30, 20:50] = 0.9
 print("plateau", len(P.find_extrema(P.DoGStack(sl, np.array([1.5, 2.5])), threshold=0.1)))
