@@ -261,6 +261,7 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
     PLAN_CUDA(cudaMemcpy(plan->d_sigma_f32, sig32.data(), n_levels * sizeof(float),
                          cudaMemcpyHostToDevice));
     PLAN_CUDA(configure_conv_kernels(device));
+    PLAN_CUDA(configure_umma_kernels(device));
     PLAN_CUDA(configure_finalize_kernels());
 #undef PLAN_CUDA
 
@@ -301,6 +302,31 @@ static int check_threshold_args(int neighborhood, double overlap) {
     return DOGBLOB_OK;
 }
 
+// Which engine runs the two convolution passes: the tensor-core Toeplitz GEMM
+// (scale_space_umma.cu) or the FP32 sliding-window kernels (scale_space.cu).
+// DOGBLOB_CONV=fma|umma overrides (read per call: tools compare both in one process).
+static bool use_umma(const dogblob_plan *plan) {
+    if (!umma_supported(plan->geo)) return false;
+    const char *e = std::getenv("DOGBLOB_CONV");
+    if (e && e[0] == 'u') return true;
+    return false;
+}
+static cudaError_t row_pass_any(const dogblob_plan *plan, const float *d_image, float *rows_t,
+                                cudaStream_t st, const RowGate *gate) {
+    if (!gate && use_umma(plan))
+        return launch_row_pass_umma(plan->geo, d_image, rows_t, plan->table, plan->d_taps, st);
+    return launch_row_pass(plan->geo, d_image, rows_t, plan->table, plan->d_taps, st, gate);
+}
+static cudaError_t col_dog_pass_any(const dogblob_plan *plan, const float *rows_t, float *dog_t,
+                                    float *edge, cudaStream_t st) {
+    if (use_umma(plan)) {
+        cudaError_t e = launch_col_dog_pass_umma(plan->geo, rows_t, dog_t, edge, plan->table, plan->d_taps, st);
+        if (e != cudaSuccess) return e;
+        return launch_edge_dog(plan->geo, edge, dog_t, plan->table, st);
+    }
+    return launch_col_dog_pass(plan->geo, rows_t, dog_t, edge, plan->table, plan->d_taps, st);
+}
+
 // reset + row pass (optionally gated on a streamed upload), then the rest of the frame
 static int launch_frame_head(const dogblob_plan *plan, const float *d_image, void *d_workspace,
                              cudaStream_t st, void *const *events, const RowGate *gate) {
@@ -309,7 +335,7 @@ static int launch_frame_head(const dogblob_plan *plan, const float *d_image, voi
     BlobSpace bs = carve_blobspace(ws + plan->off_blobspace, plan->max_blobs);
     if (events) DB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(events[0]), st));
     DB_CUDA(launch_reset_counters(bs, st));
-    DB_CUDA(launch_row_pass(plan->geo, d_image, rows_t, plan->table, plan->d_taps, st, gate));
+    DB_CUDA(row_pass_any(plan, d_image, rows_t, st, gate));
     if (events) DB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(events[1]), st));
     return DOGBLOB_OK;
 }
@@ -326,8 +352,7 @@ static int launch_frame_tail(const dogblob_plan *plan, float threshold, int neig
         return events ? cudaEventRecord(reinterpret_cast<cudaEvent_t>(events[k]), st)
                       : cudaSuccess;
     };
-    DB_CUDA(launch_col_dog_pass(g, rows_t, dog_t, reinterpret_cast<float *>(ws + plan->off_edge),
-                                plan->table, plan->d_taps, st));
+    DB_CUDA(col_dog_pass_any(plan, rows_t, dog_t, reinterpret_cast<float *>(ws + plan->off_edge), st));
     DB_CUDA(ev(2));
     // D^T planes: rows = x (W valid), cols = y (H valid)
     DB_CUDA(launch_extrema(dog_t, g.L - 1, g.W, g.H, g.Hp, (int64_t)g.Hp * g.Wp, true,
@@ -476,8 +501,11 @@ int dogblob_scale_space(const dogblob_plan *plan, const float *d_image, void *d_
     float *rows_t = reinterpret_cast<float *>(ws + plan->off_rows_t);
     float *lev_t = reinterpret_cast<float *>(ws + plan->off_dog_t);
     const ConvGeometry &g = plan->geo;
-    DB_CUDA(launch_row_pass(g, d_image, rows_t, plan->table, plan->d_taps, st));
-    DB_CUDA(launch_col_levels_pass(g, rows_t, lev_t, plan->unit_table, plan->d_taps, st));
+    DB_CUDA(row_pass_any(plan, d_image, rows_t, st, nullptr));
+    if (use_umma(plan))
+        DB_CUDA(launch_col_levels_pass_umma(g, rows_t, lev_t, plan->unit_table, plan->d_taps, st));
+    else
+        DB_CUDA(launch_col_levels_pass(g, rows_t, lev_t, plan->unit_table, plan->d_taps, st));
     DB_CUDA(launch_untranspose(lev_t, g.L, g.Hp, g.Wp, g.H, g.W, d_levels, st));
     return DOGBLOB_OK;
 }
@@ -492,9 +520,8 @@ int dogblob_dog(const dogblob_plan *plan, const float *d_image, void *d_workspac
     float *rows_t = reinterpret_cast<float *>(ws + plan->off_rows_t);
     float *dog_t = reinterpret_cast<float *>(ws + plan->off_dog_t);
     const ConvGeometry &g = plan->geo;
-    DB_CUDA(launch_row_pass(g, d_image, rows_t, plan->table, plan->d_taps, st));
-    DB_CUDA(launch_col_dog_pass(g, rows_t, dog_t, reinterpret_cast<float *>(ws + plan->off_edge),
-                                plan->table, plan->d_taps, st));
+    DB_CUDA(row_pass_any(plan, d_image, rows_t, st, nullptr));
+    DB_CUDA(col_dog_pass_any(plan, rows_t, dog_t, reinterpret_cast<float *>(ws + plan->off_edge), st));
     DB_CUDA(launch_untranspose(dog_t, g.L - 1, g.Hp, g.Wp, g.H, g.W, d_slices, st));
     return DOGBLOB_OK;
 }

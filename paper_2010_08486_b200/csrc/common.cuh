@@ -148,6 +148,19 @@ cudaError_t launch_col_dog_pass(const ConvGeometry &g, const float *d_rows_t, fl
 cudaError_t launch_col_levels_pass(const ConvGeometry &g, const float *d_rows_t, float *d_lev_t,
                                    const LevelTable &unit_tbl, const float2 *d_taps,
                                    cudaStream_t st);
+cudaError_t launch_edge_dog(const ConvGeometry &g, const float *d_edge, float *d_dog_t,
+                            const LevelTable &tbl, cudaStream_t st);
+// tensor-core (tcgen05) versions of the three passes, scale_space_umma.cu
+bool umma_supported(const ConvGeometry &g);
+cudaError_t configure_umma_kernels(int device);
+cudaError_t launch_row_pass_umma(const ConvGeometry &g, const float *d_img, float *d_rows_t,
+                                 const LevelTable &tbl, const float2 *d_taps, cudaStream_t st);
+cudaError_t launch_col_dog_pass_umma(const ConvGeometry &g, const float *d_rows_t, float *d_dog_t,
+                                     float *d_edge, const LevelTable &tbl, const float2 *d_taps,
+                                     cudaStream_t st);
+cudaError_t launch_col_levels_pass_umma(const ConvGeometry &g, const float *d_rows_t, float *d_lev_t,
+                                        const LevelTable &unit_tbl, const float2 *d_taps,
+                                        cudaStream_t st);
 cudaError_t launch_untranspose(const float *d_src_t, int planes, int Hp, int Wp, int H, int W,
                                float *d_dst, cudaStream_t st);
 cudaError_t launch_dog_from_levels(int L, int64_t plane_elems, const float *d_levels,

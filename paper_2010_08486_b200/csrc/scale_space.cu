@@ -480,6 +480,13 @@ cudaError_t launch_col_dog_pass(const ConvGeometry &g, const float *d_rows_t, fl
     const size_t smem = col_pass_smem_impl(g.max_group_table, g.max_rpad, true);
     col_pass_kernel<true><<<grid, kConvThreads, smem, st>>>(d_rows_t, g.Hp, plane, g.W, d_dog_t, d_edge,
                                                             tbl, d_taps, g.max_rpad, frontier_warps());
+    return launch_edge_dog(g, d_edge, d_dog_t, tbl, st);
+}
+
+// the slices that straddle two level groups, from the parked boundary levels
+cudaError_t launch_edge_dog(const ConvGeometry &g, const float *d_edge, float *d_dog_t,
+                            const LevelTable &tbl, cudaStream_t st) {
+    const int64_t plane = (int64_t)g.Hp * g.Wp;
     if (g.G > 1) {
         int bx = (int)((plane / 4 + 255) / 256);
         if (bx > 148 * 2) bx = 148 * 2;
