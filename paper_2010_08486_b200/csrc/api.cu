@@ -73,7 +73,10 @@ struct dogblob_plan {
     // device constants
     LevelTable table;        // fused pass: launch order + level groups
     LevelTable unit_table;   // stage API: one level per group
+    LevelTable umma_table;   // tensor-core column pass: groups balanced for persistent CTAs
     float2 *d_taps = nullptr;
+    ToeplitzTable toeplitz;  // tensor-core passes: prebuilt Toeplitz operands of every level
+    float *d_toeplitz = nullptr;
     double *d_slice_sigma = nullptr;
     float *d_sigma_f32 = nullptr;
     // workspace layout (bytes from the workspace base)
@@ -96,16 +99,17 @@ struct DeviceGuard {
 
 // Partition the L levels into G contiguous groups of similar tap count for the fused
 // column+DoG pass; group g sweeps levels [begin[g], begin[g+1]).
-std::vector<int> balance_groups(const std::vector<LevelDesc> &lv, int G) {
+std::vector<int> balance_groups(const std::vector<LevelDesc> &lv, int G, double fixed_cost = -1.0) {
     const int L = (int)lv.size();
     G = std::max(1, std::min(G, L));
     std::vector<double> pre(L + 1, 0.0);
     // cost of a level in full-chunk units: middle chunks + head/tail (136/128 of a full one)
     // + its fixed part (DoG epilogue, pipeline refill)
-    static const double fixed = [] {
+    static const double fixed_fma = [] {
         const char *e = std::getenv("DOGBLOB_LEVEL_COST");
         return e ? std::atof(e) : 1.07;
     }();
+    const double fixed = fixed_cost >= 0.0 ? fixed_cost : fixed_fma;
     for (int i = 0; i < L; ++i) pre[i + 1] = pre[i] + lv[i].n_mid + fixed;
     std::vector<int> begin(G + 1, 0);
     begin[G] = L;
@@ -121,8 +125,7 @@ std::vector<int> balance_groups(const std::vector<LevelDesc> &lv, int G) {
 
 // Number of level groups: fill whole waves of CTAs (2 resident per SM) as exactly as
 // possible; every extra group costs one boundary slice through the edge planes.
-int choose_groups(int tiles, int L) {
-    const double slots = 2.0 * 148.0;
+int choose_groups(int tiles, int L, double slots = 2.0 * 148.0) {
     int best = 1;
     double best_score = -1.0;
     for (int G = 1; G <= std::min(L, 24); ++G) {
@@ -251,6 +254,21 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
     for (int i = 0; i <= g.G; ++i) plan->table.group_begin[i] = group_begin[i];
     plan->unit_table.n_groups = n_levels;
     for (int i = 0; i <= n_levels; ++i) plan->unit_table.group_begin[i] = unit[i];
+    // tensor-core column pass: one persistent CTA per SM walks (tile, group) units round robin;
+    // a level costs (128 + 2 rpad) / 16 stages = n_mid + 9 (+1 for its drain)
+    int G_umma = choose_groups(tiles, n_levels, 148.0);
+    if (const char *env = std::getenv("DOGBLOB_UMMA_GROUPS")) G_umma = std::max(1, std::atoi(env));
+    {
+        static const double fixed_umma = [] {
+            const char *e = std::getenv("DOGBLOB_UMMA_LEVEL_COST");
+            return e ? std::atof(e) : 10.0;
+        }();
+        const std::vector<int> ub = balance_groups(plan->levels, G_umma, fixed_umma);
+        G_umma = (int)ub.size() - 1;
+        plan->umma_table = plan->table;
+        plan->umma_table.n_groups = G_umma;
+        for (int i = 0; i <= G_umma; ++i) plan->umma_table.group_begin[i] = ub[i];
+    }
     PLAN_CUDA(cudaMalloc(&plan->d_taps, table.size() * sizeof(float2)));
     PLAN_CUDA(cudaMalloc(&plan->d_slice_sigma, n_levels * sizeof(double)));
     PLAN_CUDA(cudaMalloc(&plan->d_sigma_f32, n_levels * sizeof(float)));
@@ -260,6 +278,14 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
                          cudaMemcpyHostToDevice));
     PLAN_CUDA(cudaMemcpy(plan->d_sigma_f32, sig32.data(), n_levels * sizeof(float),
                          cudaMemcpyHostToDevice));
+    if (umma_supported(g)) {
+        std::vector<float> toep;
+        std::memset(&plan->toeplitz, 0, sizeof(ToeplitzTable));
+        build_toeplitz(plan->levels.data(), n_levels, table.data(), toep, plan->toeplitz);
+        PLAN_CUDA(cudaMalloc(&plan->d_toeplitz, toep.size() * sizeof(float)));
+        PLAN_CUDA(cudaMemcpy(plan->d_toeplitz, toep.data(), toep.size() * sizeof(float),
+                             cudaMemcpyHostToDevice));
+    }
     PLAN_CUDA(configure_conv_kernels(device));
     PLAN_CUDA(configure_umma_kernels(device));
     PLAN_CUDA(configure_finalize_kernels());
@@ -269,7 +295,7 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
     size_t off = 0;
     plan->off_rows_t = off; off += align_up(plane * n_levels, 256);
     plan->off_dog_t = off;  off += align_up(plane * n_levels, 256);   // L planes: also holds levels
-    plan->off_edge = off;   off += align_up(plane * 2 * g.G, 256);       // boundary levels
+    plan->off_edge = off;   off += align_up(plane * 2 * std::max(g.G, plan->umma_table.n_groups), 256);   // boundary levels
     plan->off_blobspace = off; off += blobspace_bytes(max_blobs);
     plan->off_gate = off;   off += 256;                                   // streamed upload: gate word
     plan->total = off;
@@ -281,6 +307,7 @@ void dogblob_plan_destroy(dogblob_plan *plan) {
     if (!plan) return;
     DeviceGuard guard(plan->device);
     cudaFree(plan->d_taps);
+    cudaFree(plan->d_toeplitz);
     cudaFree(plan->d_slice_sigma);
     cudaFree(plan->d_sigma_f32);
     delete plan;
@@ -306,7 +333,7 @@ static int check_threshold_args(int neighborhood, double overlap) {
 // (scale_space_umma.cu) or the FP32 sliding-window kernels (scale_space.cu).
 // DOGBLOB_CONV=fma|umma overrides (read per call: tools compare both in one process).
 static bool use_umma(const dogblob_plan *plan) {
-    if (!umma_supported(plan->geo)) return false;
+    if (!plan->d_toeplitz) return false;
     const char *e = std::getenv("DOGBLOB_CONV");
     if (e && e[0] == 'u') return true;
     return false;
@@ -314,15 +341,17 @@ static bool use_umma(const dogblob_plan *plan) {
 static cudaError_t row_pass_any(const dogblob_plan *plan, const float *d_image, float *rows_t,
                                 cudaStream_t st, const RowGate *gate) {
     if (!gate && use_umma(plan))
-        return launch_row_pass_umma(plan->geo, d_image, rows_t, plan->table, plan->d_taps, st);
+        return launch_row_pass_umma(plan->geo, d_image, rows_t, plan->table, plan->toeplitz,
+                                    plan->d_toeplitz, st);
     return launch_row_pass(plan->geo, d_image, rows_t, plan->table, plan->d_taps, st, gate);
 }
 static cudaError_t col_dog_pass_any(const dogblob_plan *plan, const float *rows_t, float *dog_t,
                                     float *edge, cudaStream_t st) {
     if (use_umma(plan)) {
-        cudaError_t e = launch_col_dog_pass_umma(plan->geo, rows_t, dog_t, edge, plan->table, plan->d_taps, st);
+        cudaError_t e = launch_col_dog_pass_umma(plan->geo, rows_t, dog_t, edge, plan->umma_table,
+                                                 plan->toeplitz, plan->d_toeplitz, st);
         if (e != cudaSuccess) return e;
-        return launch_edge_dog(plan->geo, edge, dog_t, plan->table, st);
+        return launch_edge_dog(plan->geo, edge, dog_t, plan->umma_table, st);
     }
     return launch_col_dog_pass(plan->geo, rows_t, dog_t, edge, plan->table, plan->d_taps, st);
 }
@@ -503,7 +532,8 @@ int dogblob_scale_space(const dogblob_plan *plan, const float *d_image, void *d_
     const ConvGeometry &g = plan->geo;
     DB_CUDA(row_pass_any(plan, d_image, rows_t, st, nullptr));
     if (use_umma(plan))
-        DB_CUDA(launch_col_levels_pass_umma(g, rows_t, lev_t, plan->unit_table, plan->d_taps, st));
+        DB_CUDA(launch_col_levels_pass_umma(g, rows_t, lev_t, plan->unit_table, plan->toeplitz,
+                                            plan->d_toeplitz, st));
     else
         DB_CUDA(launch_col_levels_pass(g, rows_t, lev_t, plan->unit_table, plan->d_taps, st));
     DB_CUDA(launch_untranspose(lev_t, g.L, g.Hp, g.Wp, g.H, g.W, d_levels, st));

@@ -5,6 +5,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <string>
+#include <vector>
 
 #include "../../include/dogblob_b200.h"
 
@@ -151,16 +152,20 @@ cudaError_t launch_col_levels_pass(const ConvGeometry &g, const float *d_rows_t,
 cudaError_t launch_edge_dog(const ConvGeometry &g, const float *d_edge, float *d_dog_t,
                             const LevelTable &tbl, cudaStream_t st);
 // tensor-core (tcgen05) versions of the three passes, scale_space_umma.cu
+struct ToeplitzTable { int ofs[kMaxLevels]; int rows[kMaxLevels]; };   // per level: float offset, rows
 bool umma_supported(const ConvGeometry &g);
+void build_toeplitz(const LevelDesc *lv, int n_levels, const float2 *taps, std::vector<float> &out,
+                    ToeplitzTable &tab);
 cudaError_t configure_umma_kernels(int device);
 cudaError_t launch_row_pass_umma(const ConvGeometry &g, const float *d_img, float *d_rows_t,
-                                 const LevelTable &tbl, const float2 *d_taps, cudaStream_t st);
+                                 const LevelTable &tbl, const ToeplitzTable &ttab,
+                                 const float *d_toep, cudaStream_t st);
 cudaError_t launch_col_dog_pass_umma(const ConvGeometry &g, const float *d_rows_t, float *d_dog_t,
-                                     float *d_edge, const LevelTable &tbl, const float2 *d_taps,
-                                     cudaStream_t st);
+                                     float *d_edge, const LevelTable &tbl, const ToeplitzTable &ttab,
+                                     const float *d_toep, cudaStream_t st);
 cudaError_t launch_col_levels_pass_umma(const ConvGeometry &g, const float *d_rows_t, float *d_lev_t,
-                                        const LevelTable &unit_tbl, const float2 *d_taps,
-                                        cudaStream_t st);
+                                        const LevelTable &unit_tbl, const ToeplitzTable &ttab,
+                                        const float *d_toep, cudaStream_t st);
 cudaError_t launch_untranspose(const float *d_src_t, int planes, int Hp, int Wp, int H, int W,
                                float *d_dst, cudaStream_t st);
 cudaError_t launch_dog_from_levels(int L, int64_t plane_elems, const float *d_levels,

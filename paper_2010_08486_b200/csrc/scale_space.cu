@@ -487,10 +487,10 @@ cudaError_t launch_col_dog_pass(const ConvGeometry &g, const float *d_rows_t, fl
 cudaError_t launch_edge_dog(const ConvGeometry &g, const float *d_edge, float *d_dog_t,
                             const LevelTable &tbl, cudaStream_t st) {
     const int64_t plane = (int64_t)g.Hp * g.Wp;
-    if (g.G > 1) {
+    if (tbl.n_groups > 1) {
         int bx = (int)((plane / 4 + 255) / 256);
         if (bx > 148 * 2) bx = 148 * 2;
-        edge_dog_kernel<<<dim3(bx, g.G - 1), 256, 0, st>>>(d_edge, plane, d_dog_t, tbl);
+        edge_dog_kernel<<<dim3(bx, tbl.n_groups - 1), 256, 0, st>>>(d_edge, plane, d_dog_t, tbl);
     }
     return cudaGetLastError();
 }

@@ -30,7 +30,12 @@
 //                           level kept in thread-private shared-memory slots, global stores.
 //                           Two accumulators: the drain of level i overlaps the MMAs of i+1.
 // TMEM columns: [0,256) two 128 x 128 float32 accumulators, [256,512) A staging.
+#include <algorithm>
 #include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include <cuda.h>      // CUtensorMap (types only: the encoder is fetched through the runtime)
 
 #include "common.cuh"
 
@@ -40,13 +45,14 @@ namespace {
 
 constexpr int kUT = 128;              // tile edge on both axes
 constexpr int kUThreads = 512;
-constexpr int kStages = 8;            // A staging stages
-constexpr int kStageRows = 16;        // input rows per stage = 2 k-steps of 8
-constexpr int kStageCols = 32;        // TMEM columns per stage: (hi 8 + lo 8) per k-step
+constexpr int kStages = 4;            // A staging stages
+constexpr int kStageK = 4;            // k-steps (8 input rows each) per stage
+constexpr int kStageRows = 8 * kStageK;   // input rows per stage
+constexpr int kStageCols = 16 * kStageK;  // TMEM columns per stage: (hi 8 + lo 8) per k-step
 constexpr int kAccCols = 128;
 constexpr int kStageCol0 = 2 * kAccCols;
 constexpr int kLoaderGroups = 2;      // groups of 4 warps; group g fills stages with index % 2 == g
-constexpr int kBuilderWarps = 3;
+constexpr int kMaxRawStages = 8;      // raw input-row stages in shared memory (16 KB each)
 constexpr uint32_t kSpinLimit = 1u << 27;
 
 enum UmmaMode { kModeRows = 0, kModeDog = 1, kModeLevels = 2 };
@@ -59,7 +65,11 @@ struct UmmaArgs {
     float *out;
     int64_t out_pitch, out_plane;
     float *edge;            // DoG mode: parked boundary levels
-    const float2 *taps;     // duplicated (w, w) tap tables, see api.cu
+    const float *toep;      // prebuilt Toeplitz arrays of every level (hi | lo), see build_toeplitz
+    int raw_stages;         // raw input-row stages that fit in shared memory
+    int by_order;           // units are single levels in tbl.order[] (longest first): row pass
+    int use_tma;            // interior stages arrive as one TMA box (tensor map valid)
+    int tma_plane_rows;     // rows between level planes in the tensor map (0: one plane)
     int tiles_c, tiles_r;   // tiles along the contiguous / the convolved axis
     int n_units;            // tiles_c * tiles_r * n_groups
     int toep_floats;        // floats of one Toeplitz array (hi or lo) of the widest level
@@ -99,6 +109,56 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int tag
         }
     }
 }
+// long waits (drain, copiers): back off so that the spinning warp leaves its issue slots to
+// the converters that share the SM sub-partition
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, int tag) {
+    uint32_t spins = 0;
+    while (!mbar_try_wait(bar, parity)) {
+        __nanosleep(64);
+        if (++spins > (kSpinLimit >> 4)) {
+            if ((threadIdx.x & 31) == 0)
+                printf("umma: barrier timeout tag=%d block=%d warp=%d parity=%u\n", tag, blockIdx.x,
+                       threadIdx.x >> 5, parity);
+            __trap();
+        }
+    }
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+// global -> shared bulk copy (no tensor map), completion counted in bytes on `bar`
+__device__ __forceinline__ void bulk_copy_g2s(uint32_t dst_smem, const void *src, uint32_t bytes,
+                                              uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(dst_smem), "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_only(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+// one TMA box (tensor map: rows of the input planes, 128 floats x 16 rows, no swizzle)
+__device__ __forceinline__ void tma_load_2d(uint32_t dst_smem, const CUtensorMap *map, int col, int row,
+                                            uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(dst_smem), "l"(map), "r"(col), "r"(row), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst_smem, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_smem), "l"(src) : "memory");
+}
+// the barrier gets one (pre-counted) arrival once all earlier cp.async of this thread landed
+__device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ uint64_t make_desc(uint32_t lo, uint32_t hi) {
+    uint64_t d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "r"(lo), "r"(hi));
+    return d;
+}
 __device__ __forceinline__ void fence_barrier_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -133,6 +193,26 @@ __device__ __forceinline__ void umma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, u
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
         ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
+}
+// Warp-uniform variants: the whole warp executes them, one elected lane issues.  Keeping the
+// issuer's control flow and operands warp uniform lets ptxas hold descriptors in uniform
+// registers instead of wrapping every tcgen05.mma in a per-lane (ELECT / R2UR) loop.
+__device__ __forceinline__ void umma_tf32_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                                   uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
+        ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
+        ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ uint32_t tf32_rna(float x) {
     uint32_t u;
@@ -178,10 +258,6 @@ __device__ __forceinline__ void tmem_wait_ld() {
 //   bits [46,48) version = 1 (Blackwell)   bits [61,64) layout type = 0 (SWIZZLE_NONE)
 // Toeplitz array: 8-row group g at g * 256 bytes: [K half 0: 8 rows x 16 B][K half 1: 8 rows x 16 B]
 constexpr uint32_t kToepGroupBytes = 256, kToepHalfBytes = 128;
-__device__ __forceinline__ uint64_t toeplitz_desc(uint32_t smem_addr) {
-    return (uint64_t)((smem_addr >> 4) & 0x3FFFu) | ((uint64_t)(kToepHalfBytes >> 4) << 16) |
-           ((uint64_t)(kToepGroupBytes >> 4) << 32) | (1ull << 46);
-}
 // Instruction descriptor (cute::UMMA::InstrDescriptor): D = F32, A = B = TF32, both K-major,
 // dense, N at bits [17,23) as N >> 3, M at bits [24,29) as M >> 4.
 __host__ __device__ constexpr uint32_t instr_desc(int M, int N) {
@@ -223,30 +299,39 @@ __device__ __forceinline__ Unit decode_unit(int u, const UmmaArgs &a) {
 }
 
 struct SharedCtl {
+    unsigned long long raw_full[kMaxRawStages], raw_empty[kMaxRawStages];
     unsigned long long data_full[kStages], data_empty[kStages];
     unsigned long long toep_full[2], toep_empty[2];
     unsigned long long acc_full[2], acc_empty[2];
     uint32_t tmem_base;
     uint32_t pad[3];
 };
+static_assert(sizeof(SharedCtl) <= 1024, "control block");
 
 template <int MODE>
 __global__ void __launch_bounds__(kUThreads, 1)
-umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl) {
+umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
+                 const __grid_constant__ ToeplitzTable ttab, const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     SharedCtl *ctl = reinterpret_cast<SharedCtl *>(smem_raw);
-    float *toep = reinterpret_cast<float *>(smem_raw + 1024);     // [buffer 2][hi, lo][toep_floats]
+    float *toep = reinterpret_cast<float *>(smem_raw + 1024);     // [buffer 2][hi | lo][toep_floats]
     float *s_prev = toep + 4 * (size_t)a.toep_floats;              // DoG: [n 128][m 128]
+    float *raw = s_prev + (MODE == kModeDog ? kUT * kUT : 0);      // [raw stage][16 rows][128]
+    const int R = a.raw_stages;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
+        for (int s = 0; s < R; ++s) {
+            mbar_init(smem_u32(&ctl->raw_full[s]), 64);
+            mbar_init(smem_u32(&ctl->raw_empty[s]), 4);
+        }
         for (int s = 0; s < kStages; ++s) {
             mbar_init(smem_u32(&ctl->data_full[s]), 4);
             mbar_init(smem_u32(&ctl->data_empty[s]), 1);
         }
         for (int b = 0; b < 2; ++b) {
-            mbar_init(smem_u32(&ctl->toep_full[b]), kBuilderWarps);
+            mbar_init(smem_u32(&ctl->toep_full[b]), 1);
             mbar_init(smem_u32(&ctl->toep_empty[b]), 1);
             mbar_init(smem_u32(&ctl->acc_full[b]), 1);
             mbar_init(smem_u32(&ctl->acc_empty[b]), 4);
@@ -257,19 +342,28 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl) {
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *reinterpret_cast<volatile uint32_t *>(&ctl->tmem_base);
+    const uint32_t tmem = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile uint32_t *>(&ctl->tmem_base), 0);
 
     if (warp == 0) {
-        // ================= issuer =================
+        // ================= issuer (one thread) =================
+        // Band structure: k-step m0 only feeds outputs n in [m0 - 2 rpad, m0 + 7], so its MMAs are
+        // issued for that column range only (N rounded to 16; the Toeplitz window and the
+        // accumulator address move with it).  K-step 0 runs full width with accumulate = 0, which
+        // also zeroes the columns later steps accumulate into.
+        {
         uint32_t stage_it = 0, lvl_it = 0;
-        constexpr uint32_t idesc = instr_desc(kUT, kUT);
+        constexpr uint32_t idesc0 = instr_desc(kUT, 0);
+        constexpr uint32_t desc_hi = (kToepGroupBytes >> 4) | (1u << 14);        // SBO, version 1
         RoleClock rc(a.prof != nullptr && lane == 0);
+        const bool shrink = !(a.debug & 64);
         for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
             const Unit un = decode_unit(u, a);
-            const int lb = tbl.group_begin[un.g], le = tbl.group_begin[un.g + 1];
+            const int lb = a.by_order ? tbl.order[un.g] : tbl.group_begin[un.g];
+            const int le = a.by_order ? lb + 1 : tbl.group_begin[un.g + 1];
             for (int level = lb; level < le; ++level, ++lvl_it) {
-                const int Kp = kUT + 2 * tbl.lv[level].rpad;
-                const int n_stage = Kp / kStageRows;
+                const int rpad2 = 2 * tbl.lv[level].rpad;
+                const int Kp = kUT + rpad2;
+                const int n_k = Kp >> 3;
                 const uint32_t b = lvl_it & 1, par = (lvl_it >> 1) & 1;
                 rc.lap(3);
                 mbar_wait(smem_u32(&ctl->toep_full[b]), par, 1);
@@ -277,98 +371,123 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl) {
                 mbar_wait(smem_u32(&ctl->acc_empty[b]), par ^ 1, 2);
                 rc.lap(1);
                 tc_fence_after();
+                // low descriptor words of the window of k-step 0 (row Kp - 8); every k-step moves
+                // the window up by 8 rows = one 256-byte group = 16 descriptor units
                 const uint32_t t_hi = smem_u32(toep + (size_t)(2 * b) * a.toep_floats);
-                const uint32_t t_lo = smem_u32(toep + (size_t)(2 * b + 1) * a.toep_floats);
+                const uint32_t lo_off = (uint32_t)ttab.rows[level] * 2u;            // hi -> lo array
+                uint32_t d_hi = ((t_hi + (uint32_t)((Kp - 8) >> 3) * kToepGroupBytes) >> 4) |
+                                ((kToepHalfBytes >> 4) << 16);
                 const uint32_t acc = tmem + b * kAccCols;
-                for (int st = 0; st < n_stage; ++st, ++stage_it) {
+                int m0 = 0;
+                for (int k0 = 0; k0 < n_k; k0 += kStageK, ++stage_it) {
                     const uint32_t s = stage_it % kStages, sp = (stage_it / kStages) & 1;
                     rc.lap(3);
                     mbar_wait(smem_u32(&ctl->data_full[s]), sp, 3);
                     rc.lap(2);
                     tc_fence_after();
-                    if (lane == 0) {
+                    if (!(a.debug & 8)) {
+                        const uint32_t a0 = tmem + kStageCol0 + s * kStageCols;
 #pragma unroll
-                        for (int ks = 0; ks < 2; ++ks) {
-                            if (a.debug & 8) break;
-                            if (a.debug & 48) {     // timing experiments: independent chains / fewer MMAs
-                                const int m0x = st * kStageRows + ks * 8;
-                                const uint32_t winx = (uint32_t)((Kp - 8 - m0x) >> 3) * kToepGroupBytes;
-                                const uint32_t ax = tmem + kStageCol0 + s * kStageCols + ks * 16;
-                                const uint32_t other = tmem + (b ^ 1) * kAccCols;
-                                if (a.debug & 16) {
-                                    umma_tf32_ts(other, ax, toeplitz_desc(t_lo + winx), idesc, 1);
-                                    umma_tf32_ts(acc, ax, toeplitz_desc(t_hi + winx), idesc, (st | ks) != 0);
-                                    umma_tf32_ts(other, ax + 8, toeplitz_desc(t_hi + winx), idesc, 1);
-                                } else {
-                                    umma_tf32_ts(acc, ax, toeplitz_desc(t_hi + winx), idesc, (st | ks) != 0);
+                        for (int ks = 0; ks < kStageK; ++ks) {
+                            if (k0 + ks < n_k) {
+                                int ns = 0, ne = kUT;
+                                if (shrink && m0 != 0) {
+                                    ns = max(0, m0 - rpad2) & ~15;
+                                    ne = min(kUT, (m0 + 8 + 15) & ~15);
                                 }
-                                continue;
+                                const uint32_t idesc = idesc0 | ((uint32_t)((ne - ns) >> 3) << 17);
+                                const uint32_t dh = d_hi + 2u * (uint32_t)ns;   // window rows ns.. (16 units / 8 rows)
+                                const uint32_t dcol = acc + (uint32_t)ns;
+                                umma_tf32_ts_elect(dcol, a0 + ks * 16, make_desc(dh + lo_off, desc_hi), idesc, m0 != 0);
+                                umma_tf32_ts_elect(dcol, a0 + ks * 16 + 8, make_desc(dh, desc_hi), idesc, 1);
+                                umma_tf32_ts_elect(dcol, a0 + ks * 16, make_desc(dh, desc_hi), idesc, 1);
+                                d_hi -= 16u;
+                                m0 += 8;
                             }
-                            const int m0 = st * kStageRows + ks * 8;
-                            const uint32_t win = (uint32_t)((Kp - 8 - m0) >> 3) * kToepGroupBytes;
-                            const uint64_t d_hi = toeplitz_desc(t_hi + win);
-                            const uint64_t d_lo = toeplitz_desc(t_lo + win);
-                            const uint32_t a_hi = tmem + kStageCol0 + s * kStageCols + ks * 16;
-                            const uint32_t a_lo = a_hi + 8;
-                            umma_tf32_ts(acc, a_hi, d_lo, idesc, (st | ks) != 0);
-                            umma_tf32_ts(acc, a_lo, d_hi, idesc, 1);
-                            umma_tf32_ts(acc, a_hi, d_hi, idesc, 1);
                         }
-                        umma_commit(smem_u32(&ctl->data_empty[s]));
                     }
-                    __syncwarp();
+                    umma_commit_elect(smem_u32(&ctl->data_empty[s]));
                 }
-                if (lane == 0) {
-                    umma_commit(smem_u32(&ctl->toep_empty[b]));
-                    umma_commit(smem_u32(&ctl->acc_full[b]));
-                }
-                __syncwarp();
+                umma_commit_elect(smem_u32(&ctl->toep_empty[b]));
+                umma_commit_elect(smem_u32(&ctl->acc_full[b]));
             }
         }
         rc.lap(3);
         rc.flush(a.prof, 0);
-    } else if (warp <= kBuilderWarps) {
-        // ================= Toeplitz builders =================
-        const int tid = threadIdx.x - 32;
+        if (rc.on) {        // slowest / fastest CTA (issuer's whole life)
+            const unsigned long long tot = rc.acc[0] + rc.acc[1] + rc.acc[2] + rc.acc[3];
+            atomicMax(a.prof + 10, tot);
+            atomicMin(a.prof + 11, tot);
+        }
+        }
+    } else if (warp == 1) {
+        // ================= Toeplitz copier: prebuilt hi|lo arrays, one bulk copy per level ========
         uint32_t lvl_it = 0;
-        RoleClock rc(a.prof != nullptr && tid == 0);
+        RoleClock rc(a.prof != nullptr && lane == 0);
         for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
             const Unit un = decode_unit(u, a);
-            const int lb = tbl.group_begin[un.g], le = tbl.group_begin[un.g + 1];
+            const int lb = a.by_order ? tbl.order[un.g] : tbl.group_begin[un.g];
+            const int le = a.by_order ? lb + 1 : tbl.group_begin[un.g + 1];
             for (int level = lb; level < le; ++level, ++lvl_it) {
-                const LevelDesc lv = tbl.lv[level];
-                const int Kp = kUT + 2 * lv.rpad;
                 const uint32_t b = lvl_it & 1, par = (lvl_it >> 1) & 1;
                 rc.lap(1);
-                mbar_wait(smem_u32(&ctl->toep_empty[b]), par ^ 1, 4);
+                mbar_wait_sleep(smem_u32(&ctl->toep_empty[b]), par ^ 1, 4);
                 rc.lap(0);
-                float *g_hi = toep + (size_t)(2 * b) * a.toep_floats;
-                float *g_lo = g_hi + a.toep_floats;
-                const float2 *w = a.taps + lv.tap_ofs;
-                int n4 = (Kp - 8 + kUT) * 2;            // 16-byte pieces: rows x 2 K halves
-                if ((a.debug & 2) && lvl_it >= 2) n4 = 0;
-                for (int i = tid; i < n4; i += 32 * kBuilderWarps) {
-                    const int p = i >> 1, half = i & 1;
-                    // G[p][kk] = w[kk - (p - (Kp - 8))], kk = 4 half .. 4 half + 3
-                    const int t0 = 4 * half - p + (Kp - 8);
-                    uint32_t hi[4], lo[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int t = t0 + e;
-                        const float v = (t >= 0 && t <= 2 * lv.rpad) ? __ldg(&w[t].x) : 0.f;
-                        split_tf32(v, hi[e], lo[e]);
-                    }
-                    const int ofs = (p >> 3) * 64 + half * 32 + (p & 7) * 4;     // floats
-                    *reinterpret_cast<uint4 *>(g_hi + ofs) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-                    *reinterpret_cast<uint4 *>(g_lo + ofs) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                if (lane == 0) {
+                    const uint32_t bytes = (uint32_t)ttab.rows[level] * 64u;     // hi + lo
+                    const uint32_t bar = smem_u32(&ctl->toep_full[b]);
+                    mbar_expect_tx(bar, bytes);
+                    bulk_copy_g2s(smem_u32(toep + (size_t)(2 * b) * a.toep_floats),
+                                  a.toep + ttab.ofs[level], bytes, bar);
                 }
-                fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&ctl->toep_full[b]));
             }
         }
         rc.lap(1);
         rc.flush(a.prof, 4);
+    } else if (warp < 4) {
+        // ================= row loaders: 32 input rows x 512 B per raw stage =====================
+        // interior stages: one TMA box; stages that cross the image border: 64 threads x 16
+        // LDGSTS of 16 bytes with folded rows (thread t: column group t & 31 of rows (t >> 5) + 2 i).
+        const int t = threadIdx.x - 64;
+        const int cg = t & 31, rsub = t >> 5;
+        uint32_t rs = 0, rp = 0;                          // raw stage and its phase parity
+        RoleClock rc(a.prof != nullptr && t == 0);
+        for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+            const Unit un = decode_unit(u, a);
+            const int lb = a.by_order ? tbl.order[un.g] : tbl.group_begin[un.g];
+            const int le = a.by_order ? lb + 1 : tbl.group_begin[un.g + 1];
+            for (int level = lb; level < le; ++level) {
+                const int rpad = tbl.lv[level].rpad;
+                const int n_stage = (kUT + 2 * rpad + kStageRows - 1) / kStageRows;
+                const float *src = a.in + (int64_t)level * a.in_plane + un.c0 + 4 * cg;
+                int row0 = un.r0 - rpad;
+                for (int st = 0; st < n_stage; ++st, row0 += kStageRows, rp ^= (rs + 1 == (uint32_t)R),
+                         rs = (rs + 1 == (uint32_t)R) ? 0 : rs + 1) {
+                    rc.lap(1);
+                    mbar_wait(smem_u32(&ctl->raw_empty[rs]), rp ^ 1, 7);
+                    rc.lap(0);
+                    const uint32_t bar = smem_u32(&ctl->raw_full[rs]);
+                    if (a.use_tma && row0 >= 0 && row0 + kStageRows <= a.n_rows) {
+                        if (t == 0) {
+                            mbar_expect_tx_only(bar, kStageRows * kUT * 4);
+                            tma_load_2d(smem_u32(raw + (size_t)rs * kStageRows * kUT), &tmap, un.c0,
+                                        level * a.tma_plane_rows + row0, bar);
+                        }
+                        mbar_arrive(bar);
+                        continue;
+                    }
+                    const uint32_t dst = smem_u32(raw + ((size_t)rs * kStageRows + rsub) * kUT + 4 * cg);
+#pragma unroll 4
+                    for (int i = 0; i < kStageRows / 2; ++i)
+                        cp_async16(dst + i * 2 * kUT * 4,
+                                   src + (int64_t)fold_row_u(row0 + rsub + 2 * i, a.n_rows) * a.in_pitch);
+                    cp_async_arrive_noinc(bar);
+                }
+            }
+        }
+        rc.lap(1);
+        rc.flush(a.prof, 6);
     } else if (warp < 8) {
         // ================= drain (accumulator -> DoG -> global) =================
         const int q = warp & 3;
@@ -377,11 +496,12 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl) {
         RoleClock rc(a.prof != nullptr && warp == 4 && lane == 0);
         for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
             const Unit un = decode_unit(u, a);
-            const int lb = tbl.group_begin[un.g], le = tbl.group_begin[un.g + 1];
+            const int lb = a.by_order ? tbl.order[un.g] : tbl.group_begin[un.g];
+            const int le = a.by_order ? lb + 1 : tbl.group_begin[un.g + 1];
             for (int level = lb; level < le; ++level, ++lvl_it) {
                 const uint32_t b = lvl_it & 1, par = (lvl_it >> 1) & 1;
                 rc.lap(1);
-                mbar_wait(smem_u32(&ctl->acc_full[b]), par, 5);
+                mbar_wait_sleep(smem_u32(&ctl->acc_full[b]), par, 5);
                 rc.lap(0);
                 tc_fence_after();
                 const uint32_t acc = tmem + b * kAccCols + ((uint32_t)(32 * q) << 16);
@@ -444,47 +564,56 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl) {
         rc.lap(1);
         rc.flush(a.prof, 8);
     } else {
-        // ================= loaders (global -> hi/lo -> TMEM A staging) =================
+        // ================= converters (raw rows -> hi/lo -> TMEM A staging) =================
         const int q = warp & 3;
         const int grp = (warp - 8) >> 2;
         const int m = 32 * q + lane;
-        uint32_t stage_it = 0;
         RoleClock rc(a.prof != nullptr && warp == 8 && lane == 0);
+        int total = 0;                                   // stages this CTA processes
         for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
             const Unit un = decode_unit(u, a);
-            const int lb = tbl.group_begin[un.g], le = tbl.group_begin[un.g + 1];
-            for (int level = lb; level < le; ++level) {
-                const int rpad = tbl.lv[level].rpad;
-                const int n_stage = (kUT + 2 * rpad) / kStageRows;
-                const float *src = a.in + (int64_t)level * a.in_plane + un.c0 + m;
-                const int row_base = un.r0 - rpad;
-                for (int st = 0; st < n_stage; ++st, ++stage_it) {
-                    if ((int)(stage_it % kLoaderGroups) != grp) continue;
-                    const uint32_t s = stage_it % kStages, sp = (stage_it / kStages) & 1;
-                    float v[kStageRows];
+            const int lb = a.by_order ? tbl.order[un.g] : tbl.group_begin[un.g];
+            const int le = a.by_order ? lb + 1 : tbl.group_begin[un.g + 1];
+            for (int level = lb; level < le; ++level)
+                total += (kUT + 2 * tbl.lv[level].rpad + kStageRows - 1) / kStageRows;
+        }
+        uint32_t rs = grp % R, rp = (grp / R) & 1;
+        for (uint32_t stage_it = grp; stage_it < (uint32_t)total; stage_it += kLoaderGroups,
+                      rs += kLoaderGroups, rp ^= (rs >= (uint32_t)R), rs -= (rs >= (uint32_t)R) ? R : 0) {
+            const uint32_t s = stage_it % kStages, sp = (stage_it / kStages) & 1;
+            rc.lap(3);
+            mbar_wait(smem_u32(&ctl->raw_full[rs]), rp, 8);
+            rc.lap(0);
+            const float *src = raw + (size_t)rs * kStageRows * kUT + m;
+            const uint32_t dst = tmem + kStageCol0 + s * kStageCols + ((uint32_t)(32 * q) << 16);
 #pragma unroll
-                    for (int k = 0; k < kStageRows; ++k)
-                        v[k] = (a.debug & 1) ? 1.f : __ldg(src + (int64_t)fold_row_u(row_base + st * kStageRows + k, a.n_rows) * a.in_pitch);
-                    rc.lap(3);
-                    mbar_wait(smem_u32(&ctl->data_empty[s]), sp ^ 1, 6);
-                    rc.lap(0);
-                    tc_fence_after();
-                    const uint32_t dst = tmem + kStageCol0 + s * kStageCols + ((uint32_t)(32 * q) << 16);
+            for (int h = 0; h < kStageK / 2; ++h) {       // 16 rows = 2 k-steps at a time
+                float v[16];
 #pragma unroll
-                    for (int ks = 0; ks < 2; ++ks) {
-                        uint32_t r[16];
+                for (int k = 0; k < 16; ++k) v[k] = src[(16 * h + k) * kUT];
+                uint32_t r0[16], r1[16];
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) split_tf32(v[ks * 8 + k], r[k], r[8 + k]);
-                        tmem_st16(dst + ks * 16, r);
-                    }
-                    rc.lap(1);
-                    tmem_wait_st();
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(smem_u32(&ctl->data_full[s]));
-                    rc.lap(2);
+                for (int k = 0; k < 8; ++k) {
+                    split_tf32(v[k], r0[k], r0[8 + k]);
+                    split_tf32(v[8 + k], r1[k], r1[8 + k]);
                 }
+                if (h == kStageK / 2 - 1) {               // all rows of the raw stage are in registers
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(smem_u32(&ctl->raw_empty[rs]));
+                }
+                if (h == 0) {
+                    rc.lap(1);
+                    mbar_wait(smem_u32(&ctl->data_empty[s]), sp ^ 1, 6);
+                    rc.lap(2);
+                    tc_fence_after();
+                }
+                tmem_st16(dst + 32 * h, r0);
+                tmem_st16(dst + 32 * h + 16, r1);
             }
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&ctl->data_full[s]));
         }
         rc.lap(3);
         rc.flush(a.prof, 12);
@@ -495,11 +624,47 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl) {
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
-int toeplitz_floats(int max_rpad) { return (kUT + 2 * max_rpad - 8 + kUT) * 8; }
+int toeplitz_rows(int rpad) { return kUT + 2 * rpad - 8 + kUT; }
+int toeplitz_floats(int max_rpad) { return toeplitz_rows(max_rpad) * 8; }
 
-size_t umma_smem(int max_rpad, bool dog) {
+constexpr size_t kSmemLimit = 227 * 1024;
+size_t umma_fixed_smem(int max_rpad, bool dog) {
     return 1024 + 4 * (size_t)toeplitz_floats(max_rpad) * sizeof(float) +
            (dog ? (size_t)kUT * kUT * sizeof(float) : 0);
+}
+int raw_stages_for(int max_rpad, bool dog) {
+    const size_t fixed = umma_fixed_smem(max_rpad, dog);
+    if (fixed + 2 * kStageRows * kUT * 4 > kSmemLimit) return 0;
+    // a multiple of the number of converter groups: a raw stage is then always converted by the
+    // same group, so no waiter is ever two phases behind its barrier (a parity wait cannot tell
+    // phase n from phase n + 2)
+    const size_t r = std::min<size_t>(kMaxRawStages, (kSmemLimit - fixed) / (kStageRows * kUT * 4));
+    return (int)(r / kLoaderGroups * kLoaderGroups);
+}
+
+// 2-D tensor map over the input rows: inner dimension = the pitch (contiguous axis), outer = all
+// rows of all level planes; box = 128 floats x 16 rows, no swizzle, no interleave.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+bool encode_rows_map(CUtensorMap *map, const float *base, uint64_t pitch, uint64_t rows) {
+    static EncodeTiledFn fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {pitch, rows};
+    const cuuint64_t strides[1] = {pitch * sizeof(float)};
+    const cuuint32_t box[2] = {(cuuint32_t)kUT, (cuuint32_t)kStageRows};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 int persistent_ctas(int n_units) {
@@ -514,40 +679,90 @@ int persistent_ctas(int n_units) {
 }
 
 template <int MODE>
-cudaError_t launch_umma(const UmmaArgs &a, const LevelTable &tbl, int max_rpad, cudaStream_t st) {
-    const size_t smem = umma_smem(max_rpad, MODE == kModeDog);
+cudaError_t launch_umma(const UmmaArgs &a, const LevelTable &tbl, const ToeplitzTable &ttab,
+                        int max_rpad, cudaStream_t st) {
     UmmaArgs b = a;
+    b.toep_floats = toeplitz_floats(max_rpad);
+    b.raw_stages = raw_stages_for(max_rpad, MODE == kModeDog);
+    if (const char *e = std::getenv("DOGBLOB_UMMA_RAW")) b.raw_stages = std::max(2, std::min(b.raw_stages, std::atoi(e))) / kLoaderGroups * kLoaderGroups;
+    const size_t smem = umma_fixed_smem(max_rpad, MODE == kModeDog) +
+                        (size_t)b.raw_stages * kStageRows * kUT * 4;
     if (const char *e = std::getenv("DOGBLOB_UMMA_DEBUG")) b.debug = std::atoi(e);
     static unsigned long long *d_prof = nullptr;
     const bool prof = std::getenv("DOGBLOB_UMMA_PROF") != nullptr;
     if (prof) {
         if (!d_prof) cudaMalloc(&d_prof, 16 * sizeof(unsigned long long));
         cudaMemsetAsync(d_prof, 0, 16 * sizeof(unsigned long long), st);
+        cudaMemsetAsync(d_prof + 11, 0xff, sizeof(unsigned long long), st);
         b.prof = d_prof;
     }
+    CUtensorMap tmap;
+    std::memset(&tmap, 0, sizeof(tmap));
+    b.use_tma = 0;
+    if (!std::getenv("DOGBLOB_UMMA_NO_TMA")) {
+        const int planes = b.in_plane ? tbl.n_levels : 1;
+        const int plane_rows = b.in_plane ? (int)(b.in_plane / b.in_pitch) : b.n_rows;
+        b.tma_plane_rows = b.in_plane ? plane_rows : 0;
+        if (encode_rows_map(&tmap, b.in, (uint64_t)b.in_pitch, (uint64_t)planes * plane_rows)) b.use_tma = 1;
+    }
     const int ctas = persistent_ctas(b.n_units);
-    umma_pass_kernel<MODE><<<ctas, kUThreads, smem, st>>>(b, tbl);
+    umma_pass_kernel<MODE><<<ctas, kUThreads, smem, st>>>(b, tbl, ttab, tmap);
     if (prof) {
         unsigned long long h[16];
         cudaStreamSynchronize(st);
         cudaMemcpy(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost);
         static const char *names[16] = {
-            "issuer  wait toeplitz", "issuer  wait acc free", "issuer  wait data", "issuer  issue+other",
-            "builder wait buffer", "builder build", "-", "-",
-            "drain   wait acc", "drain   ld+store", "-", "-",
-            "loader  wait stage free", "loader  split+st (load latency)", "loader  wait::st+arrive", "loader  loads issue+other"};
-        fprintf(stderr, "umma mode %d, %d CTAs, kilo-cycles per CTA:", MODE, ctas);
+            "issuer    wait toeplitz", "issuer    wait acc free", "issuer    wait data", "issuer    issue+other",
+            "toeplitz  wait buffer", "toeplitz  issue", "rows      wait raw stage free", "rows      cp.async issue",
+            "drain     wait acc", "drain     ld+store", "-", "-",
+            "converter wait raw rows", "converter lds+split", "converter wait stage free", "converter st+arrive"};
+        fprintf(stderr, "umma mode %d, %d CTAs, %d raw stages, kilo-cycles per CTA:", MODE, ctas, b.raw_stages);
         for (int i = 0; i < 16; ++i)
             if (names[i][0] != '-') fprintf(stderr, "\n   %-34s %8.1f", names[i], h[i] / 1e3 / ctas);
-        fprintf(stderr, "\n");
+        fprintf(stderr, "\n   issuer total: slowest CTA %.1f, fastest %.1f\n", h[10] / 1e3, h[11] / 1e3);
     }
     return cudaGetLastError();
 }
 
 }  // namespace
 
-bool umma_supported(const ConvGeometry &g) {
-    return umma_smem(g.max_rpad, true) <= 227 * 1024;
+bool umma_supported(const ConvGeometry &g) { return raw_stages_for(g.max_rpad, true) >= 2; }
+
+// Toeplitz operand of every level, as the kernel wants it in shared memory (see the header of
+// this file): per level `rows` = Kp - 8 + 128 rows of 8 taps, hi array then lo array, 8-row groups
+// of 256 bytes = [K half 0: 8 rows x 16 B][K half 1: 8 rows x 16 B].
+// G[p][kk] = w[kk - p + Kp - 8]; taps: the plan's duplicated table (entry t = offset t - rpad).
+static uint32_t host_tf32_rna(float x) {
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    u = (u + 0x1000u) & 0xFFFFE000u;        // round to nearest, ties away (finite inputs)
+    return u;
+}
+void build_toeplitz(const LevelDesc *lv, int n_levels, const float2 *taps, std::vector<float> &out,
+                    ToeplitzTable &tab) {
+    out.clear();
+    for (int i = 0; i < n_levels; ++i) {
+        const int rpad = lv[i].rpad, Kp = kUT + 2 * rpad, rows = toeplitz_rows(rpad);
+        tab.ofs[i] = (int)out.size();
+        tab.rows[i] = rows;
+        out.resize(out.size() + (size_t)rows * 16, 0.f);
+        float *hi = out.data() + tab.ofs[i], *lo = hi + (size_t)rows * 8;
+        const float2 *w = taps + lv[i].tap_ofs;
+        for (int p = 0; p < rows; ++p)
+            for (int kk = 0; kk < 8; ++kk) {
+                const int t = kk - p + (Kp - 8);
+                const float v = (t >= 0 && t <= 2 * rpad) ? w[t].x : 0.f;
+                const uint32_t h = host_tf32_rna(v);
+                float hf;
+                std::memcpy(&hf, &h, 4);
+                const uint32_t l = host_tf32_rna(v - hf);
+                float lf;
+                std::memcpy(&lf, &l, 4);
+                const size_t o = (size_t)(p >> 3) * 64 + (kk >> 2) * 32 + (p & 7) * 4 + (kk & 3);
+                hi[o] = hf;
+                lo[o] = lf;
+            }
+    }
 }
 
 cudaError_t configure_umma_kernels(int device) {
@@ -563,42 +778,41 @@ cudaError_t configure_umma_kernels(int device) {
 
 // img[y][x] -> T_i[x][y]: contiguous axis x, convolved axis y, stored transposed
 cudaError_t launch_row_pass_umma(const ConvGeometry &g, const float *d_img, float *d_rows_t,
-                                 const LevelTable &tbl, const float2 *d_taps, cudaStream_t st) {
+                                 const LevelTable &tbl, const ToeplitzTable &ttab,
+                                 const float *d_toep, cudaStream_t st) {
     UmmaArgs a{};
     a.in = d_img; a.in_pitch = g.Wp; a.in_plane = 0; a.n_rows = g.H;
     a.out = d_rows_t; a.out_pitch = g.Hp; a.out_plane = (int64_t)g.Hp * g.Wp;
-    a.edge = nullptr; a.taps = d_taps;
+    a.edge = nullptr; a.toep = d_toep;
     a.tiles_c = g.Wp / kUT; a.tiles_r = g.Hp / kUT;
-    a.n_units = a.tiles_c * a.tiles_r * tbl.n_groups;
-    a.toep_floats = toeplitz_floats(g.max_rpad);
-    return launch_umma<kModeRows>(a, tbl, g.max_rpad, st);
+    a.by_order = 1;                       // independent levels: finest units, longest first
+    a.n_units = a.tiles_c * a.tiles_r * tbl.n_levels;
+    return launch_umma<kModeRows>(a, tbl, ttab, g.max_rpad, st);
 }
 
 // T_i[x][y] -> D_i^T[x][y]: contiguous axis y, convolved axis x
 cudaError_t launch_col_dog_pass_umma(const ConvGeometry &g, const float *d_rows_t, float *d_dog_t,
-                                     float *d_edge, const LevelTable &tbl, const float2 *d_taps,
-                                     cudaStream_t st) {
+                                     float *d_edge, const LevelTable &tbl, const ToeplitzTable &ttab,
+                                     const float *d_toep, cudaStream_t st) {
     UmmaArgs a{};
     a.in = d_rows_t; a.in_pitch = g.Hp; a.in_plane = (int64_t)g.Hp * g.Wp; a.n_rows = g.W;
     a.out = d_dog_t; a.out_pitch = g.Hp; a.out_plane = a.in_plane;
-    a.edge = d_edge; a.taps = d_taps;
+    a.edge = d_edge; a.toep = d_toep;
     a.tiles_c = g.Hp / kUT; a.tiles_r = g.Wp / kUT;
     a.n_units = a.tiles_c * a.tiles_r * tbl.n_groups;
-    a.toep_floats = toeplitz_floats(g.max_rpad);
-    return launch_umma<kModeDog>(a, tbl, g.max_rpad, st);
+    return launch_umma<kModeDog>(a, tbl, ttab, g.max_rpad, st);
 }
 
 cudaError_t launch_col_levels_pass_umma(const ConvGeometry &g, const float *d_rows_t, float *d_lev_t,
-                                        const LevelTable &unit_tbl, const float2 *d_taps,
-                                        cudaStream_t st) {
+                                        const LevelTable &unit_tbl, const ToeplitzTable &ttab,
+                                        const float *d_toep, cudaStream_t st) {
     UmmaArgs a{};
     a.in = d_rows_t; a.in_pitch = g.Hp; a.in_plane = (int64_t)g.Hp * g.Wp; a.n_rows = g.W;
     a.out = d_lev_t; a.out_pitch = g.Hp; a.out_plane = a.in_plane;
-    a.edge = nullptr; a.taps = d_taps;
+    a.edge = nullptr; a.toep = d_toep;
     a.tiles_c = g.Hp / kUT; a.tiles_r = g.Wp / kUT;
     a.n_units = a.tiles_c * a.tiles_r * unit_tbl.n_groups;
-    a.toep_floats = toeplitz_floats(g.max_rpad);
-    return launch_umma<kModeLevels>(a, unit_tbl, g.max_rpad, st);
+    return launch_umma<kModeLevels>(a, unit_tbl, ttab, g.max_rpad, st);
 }
 
 }  // namespace dogblob

@@ -45,6 +45,28 @@ def run(label):
     print(f"{label:24s} rows + cols + untranspose: {np.median(ts[2:]):.4f} ms", flush=True)
 
 
+def stage_times(label):
+    """row / column+DoG / extrema / prune from CUDA events of the detect entry point"""
+    det = P.Detector(params, slots=1)
+    eng = det.plan_for((H, W))
+    slot = eng.slots[0]
+    for _ in range(5):
+        slot.launch_device(d_img, params, True)
+    torch.cuda.synchronize()
+    sets = [D.new_events() for _ in range(20)]
+    for es in sets:
+        slot.launch_device(d_img, params, True, events=es)
+    torch.cuda.synchronize()
+    med = np.median(np.array([D.event_intervals_ms(es) for es in sets]), axis=0)
+    print(f"{label:24s} row {med[0]:.4f}  col+dog {med[1]:.4f}  extrema {med[2]:.4f}  prune {med[3]:.4f} ms",
+          flush=True)
+    det.close()
+
+
+os.environ["DOGBLOB_CONV"] = "fma"
+stage_times("fma")
+os.environ["DOGBLOB_CONV"] = "umma"
+stage_times("umma")
 os.environ["DOGBLOB_CONV"] = "fma"
 run("fma")
 os.environ["DOGBLOB_CONV"] = "umma"
