@@ -75,6 +75,7 @@ struct dogblob_plan {
     LevelTable unit_table;   // stage API: one level per group
     LevelTable umma_table;   // tensor-core column pass: groups balanced for persistent CTAs
     float2 *d_taps = nullptr;
+    bool prefer_umma = false; // plan-time choice of the convolution engine (see dogblob_plan_create)
     ToeplitzTable toeplitz;  // tensor-core passes: prebuilt Toeplitz operands of every level
     float *d_toeplitz = nullptr;
     double *d_slice_sigma = nullptr;
@@ -278,6 +279,14 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
                          cudaMemcpyHostToDevice));
     PLAN_CUDA(cudaMemcpy(plan->d_sigma_f32, sig32.data(), n_levels * sizeof(float),
                          cudaMemcpyHostToDevice));
+    // Engine choice.  The Toeplitz GEMM spends 128 + 2 rpad input rows per 128 outputs and level,
+    // the sliding window 2 rpad + 33, at about 2.4 times the cost per row (measured, C2): the
+    // tensor-core passes win for wide filters on frames that fill the 148 persistent CTAs.
+    {
+        double sum_rpad = 0.0;
+        for (int i = 0; i < n_levels; ++i) sum_rpad += plan->levels[i].rpad;
+        plan->prefer_umma = umma_supported(g) && sum_rpad / n_levels >= 48.0 && tiles >= 48;
+    }
     if (umma_supported(g)) {
         std::vector<float> toep;
         std::memset(&plan->toeplitz, 0, sizeof(ToeplitzTable));
@@ -335,14 +344,15 @@ static int check_threshold_args(int neighborhood, double overlap) {
 static bool use_umma(const dogblob_plan *plan) {
     if (!plan->d_toeplitz) return false;
     const char *e = std::getenv("DOGBLOB_CONV");
+    if (e && e[0] == 'f') return false;
     if (e && e[0] == 'u') return true;
-    return false;
+    return plan->prefer_umma;
 }
 static cudaError_t row_pass_any(const dogblob_plan *plan, const float *d_image, float *rows_t,
                                 cudaStream_t st, const RowGate *gate) {
-    if (!gate && use_umma(plan))
+    if (use_umma(plan))
         return launch_row_pass_umma(plan->geo, d_image, rows_t, plan->table, plan->toeplitz,
-                                    plan->d_toeplitz, st);
+                                    plan->d_toeplitz, st, gate);
     return launch_row_pass(plan->geo, d_image, rows_t, plan->table, plan->d_taps, st, gate);
 }
 static cudaError_t col_dog_pass_any(const dogblob_plan *plan, const float *rows_t, float *dog_t,

@@ -159,7 +159,7 @@ void build_toeplitz(const LevelDesc *lv, int n_levels, const float2 *taps, std::
 cudaError_t configure_umma_kernels(int device);
 cudaError_t launch_row_pass_umma(const ConvGeometry &g, const float *d_img, float *d_rows_t,
                                  const LevelTable &tbl, const ToeplitzTable &ttab,
-                                 const float *d_toep, cudaStream_t st);
+                                 const float *d_toep, cudaStream_t st, const RowGate *gate = nullptr);
 cudaError_t launch_col_dog_pass_umma(const ConvGeometry &g, const float *d_rows_t, float *d_dog_t,
                                      float *d_edge, const LevelTable &tbl, const ToeplitzTable &ttab,
                                      const float *d_toep, cudaStream_t st);

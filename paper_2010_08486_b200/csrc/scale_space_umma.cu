@@ -45,12 +45,16 @@ namespace {
 
 constexpr int kUT = 128;              // tile edge on both axes
 constexpr int kUThreads = 512;
-constexpr int kStages = 4;            // A staging stages
+constexpr int kStages = 2;            // A staging stages
 constexpr int kStageK = 4;            // k-steps (8 input rows each) per stage
 constexpr int kStageRows = 8 * kStageK;   // input rows per stage
 constexpr int kStageCols = 16 * kStageK;  // TMEM columns per stage: (hi 8 + lo 8) per k-step
 constexpr int kAccCols = 128;
-constexpr int kStageCol0 = 2 * kAccCols;
+// TMEM columns: three 128 x 128 float32 accumulators (hi*hi of even k-steps, hi*hi of odd k-steps,
+// the two cross terms), then the A staging
+constexpr int kAccHiA = 0, kAccHiB = kAccCols, kAccLo = 2 * kAccCols;
+constexpr int kStageCol0 = 3 * kAccCols;
+constexpr int kHalf = kUT / 2;        // accumulators are handed to the drain in two column halves
 constexpr int kLoaderGroups = 2;      // groups of 4 warps; group g fills stages with index % 2 == g
 constexpr int kMaxRawStages = 8;      // raw input-row stages in shared memory (16 KB each)
 constexpr uint32_t kSpinLimit = 1u << 27;
@@ -68,6 +72,13 @@ struct UmmaArgs {
     const float *toep;      // prebuilt Toeplitz arrays of every level (hi | lo), see build_toeplitz
     int raw_stages;         // raw input-row stages that fit in shared memory
     int by_order;           // units are single levels in tbl.order[] (longest first): row pass
+    int n_order;            // by_order: number of levels
+    // streamed upload (row pass only, see RowGate in common.cuh): the frame arrives in row chunks
+    // while the kernel runs; *gate_word - gate_base = chunks resident.  Tile rows are then the
+    // slowest unit index, so early units only need early chunks.
+    const int *gate_word;
+    int gate_base, gate_rows_per_chunk;
+    unsigned long long *gate_t_start;
     int use_tma;            // interior stages arrive as one TMA box (tensor map valid)
     int tma_plane_rows;     // rows between level planes in the tensor map (0: one plane)
     int tiles_c, tiles_r;   // tiles along the contiguous / the convolved axis
@@ -248,6 +259,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         : "r"(taddr)
         : "memory");
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+}
 __device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -293,8 +314,13 @@ __device__ __forceinline__ Unit decode_unit(int u, const UmmaArgs &a) {
     Unit x;
     x.c0 = (u % a.tiles_c) * kUT;
     const int t = u / a.tiles_c;
-    x.r0 = (t % a.tiles_r) * kUT;
-    x.g = t / a.tiles_r;
+    if (a.gate_word) {                  // streamed: tile row slowest, levels (longest first) inside
+        x.g = t % a.n_order;
+        x.r0 = (t / a.n_order) * kUT;
+    } else {
+        x.r0 = (t % a.tiles_r) * kUT;
+        x.g = t / a.tiles_r;
+    }
     return x;
 }
 
@@ -342,20 +368,31 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile uint32_t *>(&ctl->tmem_base), 0);
+    // The CTA owns all 512 columns, so the allocation starts at TMEM address 0; using the literal
+    // keeps every TMEM address and descriptor of the issuer in uniform registers.
+    if (*reinterpret_cast<volatile uint32_t *>(&ctl->tmem_base) != 0u) __trap();
+    constexpr uint32_t tmem = 0u;
 
     if (warp == 0) {
-        // ================= issuer (one thread) =================
+        // ================= issuer (whole warp, one elected lane issues) =================
+        // (Measured: a tcgen05.mma costs about 70 cycles here whatever its width N <= 128, and
+        // splitting the issue over two warps does not change that: the tensor pipe, not the
+        // issuing warp, sets the pace.)
         // Band structure: k-step m0 only feeds outputs n in [m0 - 2 rpad, m0 + 7], so its MMAs are
-        // issued for that column range only (N rounded to 16; the Toeplitz window and the
-        // accumulator address move with it).  K-step 0 runs full width with accumulate = 0, which
-        // also zeroes the columns later steps accumulate into.
+        // issued for that column range only (rounded to 16; the Toeplitz window and the
+        // accumulator address move with it).
+        // Accuracy: the tensor core truncates the float32 accumulator after every MMA, a bias of
+        // half an ulp of the running sum per MMA.  The hi*hi products of even and odd k-steps
+        // therefore go to two accumulators (half the chain length, about half the magnitude each)
+        // and the small cross terms to a third one; the drain adds the three in float32.
+        // The accumulators are single buffered and handed over in two column halves: outputs
+        // n < 64 are complete after k-step (63 + 2 rpad) / 8 and the next level's first 8 k-steps
+        // only touch n < 64, so the drain of one half overlaps the MMAs of the other.
         {
         uint32_t stage_it = 0, lvl_it = 0;
         constexpr uint32_t idesc0 = instr_desc(kUT, 0);
         constexpr uint32_t desc_hi = (kToepGroupBytes >> 4) | (1u << 14);        // SBO, version 1
         RoleClock rc(a.prof != nullptr && lane == 0);
-        const bool shrink = !(a.debug & 64);
         for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
             const Unit un = decode_unit(u, a);
             const int lb = a.by_order ? tbl.order[un.g] : tbl.group_begin[un.g];
@@ -364,11 +401,12 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                 const int rpad2 = 2 * tbl.lv[level].rpad;
                 const int Kp = kUT + rpad2;
                 const int n_k = Kp >> 3;
-                const uint32_t b = lvl_it & 1, par = (lvl_it >> 1) & 1;
+                const int k_low_last = (kHalf - 1 + rpad2) >> 3;    // last k-step that feeds n < 64
+                const uint32_t b = lvl_it & 1, par = (lvl_it >> 1) & 1, lpar = lvl_it & 1;
                 rc.lap(3);
                 mbar_wait(smem_u32(&ctl->toep_full[b]), par, 1);
                 rc.lap(0);
-                mbar_wait(smem_u32(&ctl->acc_empty[b]), par ^ 1, 2);
+                mbar_wait(smem_u32(&ctl->acc_empty[0]), lpar ^ 1, 2);
                 rc.lap(1);
                 tc_fence_after();
                 // low descriptor words of the window of k-step 0 (row Kp - 8); every k-step moves
@@ -377,39 +415,53 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                 const uint32_t lo_off = (uint32_t)ttab.rows[level] * 2u;            // hi -> lo array
                 uint32_t d_hi = ((t_hi + (uint32_t)((Kp - 8) >> 3) * kToepGroupBytes) >> 4) |
                                 ((kToepHalfBytes >> 4) << 16);
-                const uint32_t acc = tmem + b * kAccCols;
-                int m0 = 0;
+                int kidx = 0;
                 for (int k0 = 0; k0 < n_k; k0 += kStageK, ++stage_it) {
                     const uint32_t s = stage_it % kStages, sp = (stage_it / kStages) & 1;
                     rc.lap(3);
                     mbar_wait(smem_u32(&ctl->data_full[s]), sp, 3);
                     rc.lap(2);
                     tc_fence_after();
-                    if (!(a.debug & 8)) {
-                        const uint32_t a0 = tmem + kStageCol0 + s * kStageCols;
+                    const uint32_t a0 = tmem + kStageCol0 + s * kStageCols;
 #pragma unroll
-                        for (int ks = 0; ks < kStageK; ++ks) {
-                            if (k0 + ks < n_k) {
-                                int ns = 0, ne = kUT;
-                                if (shrink && m0 != 0) {
-                                    ns = max(0, m0 - rpad2) & ~15;
-                                    ne = min(kUT, (m0 + 8 + 15) & ~15);
-                                }
+                    for (int ks = 0; ks < kStageK; ++ks) {
+                        if (kidx < n_k && !(a.debug & 8)) {
+                            const int m0 = 8 * kidx;
+                            const uint32_t a_hi = a0 + ks * 16, a_lo = a_hi + 8;
+                            const uint32_t acc_hi = tmem + ((kidx & 1) ? kAccHiB : kAccHiA);
+                            const uint32_t acc_lo = tmem + kAccLo;
+                            // one column range [ns, ne) with the given initialisation flags
+                            auto issue = [&](int ns, int ne, uint32_t keep_hi, uint32_t keep_lo) {
+                                if (a.debug & 16) ne = ns + 16;          // timing experiment: narrow MMAs
                                 const uint32_t idesc = idesc0 | ((uint32_t)((ne - ns) >> 3) << 17);
-                                const uint32_t dh = d_hi + 2u * (uint32_t)ns;   // window rows ns.. (16 units / 8 rows)
-                                const uint32_t dcol = acc + (uint32_t)ns;
-                                umma_tf32_ts_elect(dcol, a0 + ks * 16, make_desc(dh + lo_off, desc_hi), idesc, m0 != 0);
-                                umma_tf32_ts_elect(dcol, a0 + ks * 16 + 8, make_desc(dh, desc_hi), idesc, 1);
-                                umma_tf32_ts_elect(dcol, a0 + ks * 16, make_desc(dh, desc_hi), idesc, 1);
-                                d_hi -= 16u;
-                                m0 += 8;
+                                const uint32_t dh = d_hi + 2u * (uint32_t)ns;
+                                umma_tf32_ts_elect(acc_lo + ns, a_hi, make_desc(dh + lo_off, desc_hi), idesc, keep_lo);
+                                umma_tf32_ts_elect(acc_lo + ns, a_lo, make_desc(dh, desc_hi), idesc, 1);
+                                umma_tf32_ts_elect(acc_hi + ns, a_hi, make_desc(dh, desc_hi), idesc, keep_hi);
+                            };
+                            if (kidx < 2) {
+                                // first use of the low halves: full-half MMAs that overwrite (the
+                                // Toeplitz rows outside the band are zero)
+                                issue(0, kHalf, 0, kidx);
+                            } else if (kidx == 8 || kidx == 9) {
+                                if (kidx == 8) {
+                                    mbar_wait(smem_u32(&ctl->acc_empty[1]), lpar ^ 1, 9);
+                                    tc_fence_after();
+                                }
+                                issue(max(0, m0 - rpad2) & ~15, kHalf, 1, 1);
+                                issue(kHalf, kUT, 0, kidx == 9);          // first use of the high halves
+                            } else {
+                                issue(max(0, m0 - rpad2) & ~15, min(kUT, (m0 + 8 + 15) & ~15), 1, 1);
                             }
+                            d_hi -= 16u;
                         }
+                        if (kidx == k_low_last) umma_commit_elect(smem_u32(&ctl->acc_full[0]));
+                        ++kidx;
                     }
                     umma_commit_elect(smem_u32(&ctl->data_empty[s]));
                 }
                 umma_commit_elect(smem_u32(&ctl->toep_empty[b]));
-                umma_commit_elect(smem_u32(&ctl->acc_full[b]));
+                umma_commit_elect(smem_u32(&ctl->acc_full[1]));
             }
         }
         rc.lap(3);
@@ -452,6 +504,8 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
         const int t = threadIdx.x - 64;
         const int cg = t & 31, rsub = t >> 5;
         uint32_t rs = 0, rp = 0;                          // raw stage and its phase parity
+        int gate_have = 0;
+        bool gate_stamped = false;
         RoleClock rc(a.prof != nullptr && t == 0);
         for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
             const Unit un = decode_unit(u, a);
@@ -467,6 +521,23 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                     rc.lap(1);
                     mbar_wait(smem_u32(&ctl->raw_empty[rs]), rp ^ 1, 7);
                     rc.lap(0);
+                    if (a.gate_word) {
+                        // last image row this stage reads (rows above 0 / below n_rows fold inwards)
+                        int need_row = row0 + kStageRows - 1;
+                        if (row0 < 0) need_row = max(need_row, -row0 - 1);
+                        need_row = min(need_row, a.n_rows - 1);
+                        if (a.n_rows < kStageRows + tbl.lv[level].rpad) need_row = a.n_rows - 1;
+                        const int need = need_row / a.gate_rows_per_chunk + 1;
+                        if (need > gate_have) {
+                            while ((gate_have = *(const volatile int *)a.gate_word - a.gate_base) < need)
+                                __nanosleep(200);
+                            __threadfence();
+                        }
+                        if (!gate_stamped) {
+                            gate_stamped = true;
+                            if (blockIdx.x == 0 && t == 0 && a.gate_t_start) *a.gate_t_start = globaltimer_ns();
+                        }
+                    }
                     const uint32_t bar = smem_u32(&ctl->raw_full[rs]);
                     if (a.use_tma && row0 >= 0 && row0 + kStageRows <= a.n_rows) {
                         if (t == 0) {
@@ -489,76 +560,84 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
         rc.lap(1);
         rc.flush(a.prof, 6);
     } else if (warp < 8) {
-        // ================= drain (accumulator -> DoG -> global) =================
+        // ================= drain (accumulators -> DoG -> global), one column half at a time ======
         const int q = warp & 3;
         const int m = 32 * q + lane;
         uint32_t lvl_it = 0;
         RoleClock rc(a.prof != nullptr && warp == 4 && lane == 0);
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
         for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
             const Unit un = decode_unit(u, a);
             const int lb = a.by_order ? tbl.order[un.g] : tbl.group_begin[un.g];
             const int le = a.by_order ? lb + 1 : tbl.group_begin[un.g + 1];
             for (int level = lb; level < le; ++level, ++lvl_it) {
-                const uint32_t b = lvl_it & 1, par = (lvl_it >> 1) & 1;
-                rc.lap(1);
-                mbar_wait_sleep(smem_u32(&ctl->acc_full[b]), par, 5);
-                rc.lap(0);
-                tc_fence_after();
-                const uint32_t acc = tmem + b * kAccCols + ((uint32_t)(32 * q) << 16);
+                const uint32_t lpar = lvl_it & 1;
                 const bool park_first = MODE == kModeDog && level == lb && un.g > 0;
                 const bool park_last = MODE == kModeDog && level == le - 1 && un.g < tbl.n_groups - 1;
                 const float sig = MODE == kModeDog && level > lb ? tbl.lv[level - 1].sigma_f32 : 0.f;
 #pragma unroll 1
-                for (int c = 0; c < kUT / 32; ++c) {
-                    uint32_t r[32];
-                    tmem_ld32(acc + c * 32, r);
-                    tmem_wait_ld();
-                    if (a.debug & 4) continue;
-                    if (MODE == kModeRows) {
-                        // lane = x (contiguous input axis), registers = 32 consecutive y of T[x][y]
-                        float *dst = a.out + (int64_t)level * a.out_plane +
-                                     (int64_t)(un.c0 + m) * a.out_pitch + un.r0 + c * 32;
+                for (int half = 0; half < 2; ++half) {
+                    rc.lap(1);
+                    mbar_wait_sleep(smem_u32(&ctl->acc_full[half]), lpar, 5);
+                    rc.lap(0);
+                    tc_fence_after();
+#pragma unroll 1
+                    for (int c = 0; c < kHalf / 16; ++c) {
+                        const int n0 = half * kHalf + c * 16;
+                        uint32_t ra[16], rb[16], rl[16];
+                        tmem_ld16(lane_base + kAccHiA + n0, ra);
+                        tmem_ld16(lane_base + kAccHiB + n0, rb);
+                        tmem_ld16(lane_base + kAccLo + n0, rl);
+                        tmem_wait_ld();
+                        if (a.debug & 4) continue;
+                        float r[16];
 #pragma unroll
-                        for (int j = 0; j < 32; j += 4)
-                            *reinterpret_cast<uint4 *>(dst + j) = make_uint4(r[j], r[j + 1], r[j + 2], r[j + 3]);
-                    } else {
-                        // lane = y (contiguous), registers = 32 consecutive output rows x
-                        const int64_t tile_ofs = (int64_t)(un.r0 + c * 32) * a.out_pitch + un.c0 + m;
-                        if (MODE == kModeLevels) {
-                            float *dst = a.out + (int64_t)level * a.out_plane + tile_ofs;
+                        for (int j = 0; j < 16; ++j)
+                            r[j] = __fadd_rn(__fadd_rn(__uint_as_float(ra[j]), __uint_as_float(rb[j])),
+                                             __uint_as_float(rl[j]));
+                        if (MODE == kModeRows) {
+                            // lane = x (contiguous input axis), registers = 16 consecutive y of T[x][y]
+                            float *dst = a.out + (int64_t)level * a.out_plane +
+                                         (int64_t)(un.c0 + m) * a.out_pitch + un.r0 + n0;
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) dst[(int64_t)j * a.out_pitch] = __uint_as_float(r[j]);
+                            for (int j = 0; j < 16; j += 4)
+                                *reinterpret_cast<float4 *>(dst + j) = make_float4(r[j], r[j + 1], r[j + 2], r[j + 3]);
                         } else {
-                            if (park_first || park_last) {
-                                float *dst = a.edge + (int64_t)(2 * un.g + (park_first ? 0 : 1)) * a.out_plane + tile_ofs;
+                            // lane = y (contiguous), registers = 16 consecutive output rows x
+                            const int64_t tile_ofs = (int64_t)(un.r0 + n0) * a.out_pitch + un.c0 + m;
+                            if (MODE == kModeLevels) {
+                                float *dst = a.out + (int64_t)level * a.out_plane + tile_ofs;
 #pragma unroll
-                                for (int j = 0; j < 32; ++j) dst[(int64_t)j * a.out_pitch] = __uint_as_float(r[j]);
-                                if (park_first && park_last) {      // single-level group
-                                    dst = a.edge + (int64_t)(2 * un.g + 1) * a.out_plane + tile_ofs;
+                                for (int j = 0; j < 16; ++j) dst[(int64_t)j * a.out_pitch] = r[j];
+                            } else {
+                                if (park_first || park_last) {
+                                    float *dst = a.edge + (int64_t)(2 * un.g + (park_first ? 0 : 1)) * a.out_plane + tile_ofs;
 #pragma unroll
-                                    for (int j = 0; j < 32; ++j) dst[(int64_t)j * a.out_pitch] = __uint_as_float(r[j]);
+                                    for (int j = 0; j < 16; ++j) dst[(int64_t)j * a.out_pitch] = r[j];
+                                    if (park_first && park_last) {      // single-level group
+                                        dst = a.edge + (int64_t)(2 * un.g + 1) * a.out_plane + tile_ofs;
+#pragma unroll
+                                        for (int j = 0; j < 16; ++j) dst[(int64_t)j * a.out_pitch] = r[j];
+                                    }
                                 }
-                            }
-                            float *slot = s_prev + (c * 32) * kUT + m;
-                            if (level > lb) {
-                                float *dst = a.out + (int64_t)(level - 1) * a.out_plane + tile_ofs;
+                                float *slot = s_prev + n0 * kUT + m;
+                                if (level > lb) {
+                                    float *dst = a.out + (int64_t)(level - 1) * a.out_plane + tile_ofs;
 #pragma unroll
-                                for (int j = 0; j < 32; ++j) {
-                                    const float prev = slot[j * kUT];
-                                    dst[(int64_t)j * a.out_pitch] =
-                                        __fmul_rn(__fsub_rn(prev, __uint_as_float(r[j])), sig);
+                                    for (int j = 0; j < 16; ++j)
+                                        dst[(int64_t)j * a.out_pitch] = __fmul_rn(__fsub_rn(slot[j * kUT], r[j]), sig);
                                 }
-                            }
-                            if (level < le - 1) {
+                                if (level < le - 1) {
 #pragma unroll
-                                for (int j = 0; j < 32; ++j) slot[j * kUT] = __uint_as_float(r[j]);
+                                    for (int j = 0; j < 16; ++j) slot[j * kUT] = r[j];
+                                }
                             }
                         }
                     }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(smem_u32(&ctl->acc_empty[half]));
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&ctl->acc_empty[b]));
             }
         }
         rc.lap(1);
@@ -779,14 +858,19 @@ cudaError_t configure_umma_kernels(int device) {
 // img[y][x] -> T_i[x][y]: contiguous axis x, convolved axis y, stored transposed
 cudaError_t launch_row_pass_umma(const ConvGeometry &g, const float *d_img, float *d_rows_t,
                                  const LevelTable &tbl, const ToeplitzTable &ttab,
-                                 const float *d_toep, cudaStream_t st) {
+                                 const float *d_toep, cudaStream_t st, const RowGate *gate) {
     UmmaArgs a{};
     a.in = d_img; a.in_pitch = g.Wp; a.in_plane = 0; a.n_rows = g.H;
     a.out = d_rows_t; a.out_pitch = g.Hp; a.out_plane = (int64_t)g.Hp * g.Wp;
     a.edge = nullptr; a.toep = d_toep;
     a.tiles_c = g.Wp / kUT; a.tiles_r = g.Hp / kUT;
     a.by_order = 1;                       // independent levels: finest units, longest first
+    a.n_order = tbl.n_levels;
     a.n_units = a.tiles_c * a.tiles_r * tbl.n_levels;
+    if (gate) {
+        a.gate_word = gate->word; a.gate_base = gate->base;
+        a.gate_rows_per_chunk = gate->rows_per_chunk; a.gate_t_start = gate->t_start;
+    }
     return launch_umma<kModeRows>(a, tbl, ttab, g.max_rpad, st);
 }
 
