@@ -331,9 +331,53 @@ def run_ours(args):
         tp = ROOT / "profiles" / "ncu_traffic.json"
         if tp.exists():
             try:
-                traffic = json.loads(tp.read_text()).get("col_dog_kernel_dram_bytes_per_launch")
+                traffic = json.loads(tp.read_text()).get(
+                    "umma_col_dog_kernel_dram_bytes_per_launch" if eng.plan.conv_engine == 1
+                    else "col_dog_kernel_dram_bytes_per_launch")
             except Exception:
                 traffic = None
+        tensor_engine = eng.plan.conv_engine == 1
+        if tensor_engine:
+            # tcgen05 Toeplitz GEMM: every level spends (128 + 2 rpad) / 8 k-steps of three
+            # 128 x 128 x 8 tf32 MMAs per 128 x 128 tile (hi*hi, hi*lo, lo*hi)
+            rpads = [max(8, (int(r) + 7) // 8 * 8) for r in det.bank.radii]
+            tiles = ((H + 127) // 128) * ((W + 127) // 128)
+            mma_flops = tiles * sum((128 + 2 * rp) // 8 for rp in rpads) * 3 * (2.0 * 128 * 128 * 8)
+            tf32_peak = None
+            try:
+                tf32_peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["bf16_tflops"] / 2.0
+            except Exception:
+                tf32_peak = 1125.0
+            engine_roof = {
+                "note": "tcgen05 kind::tf32 Toeplitz GEMM, float32 accuracy from a 3-way hi/lo split; the "
+                        "kernel is bound by the tensor pipe's fixed cost per MMA (about 70 cycles for "
+                        "N <= 128), see DESIGN.md 3",
+                "useful_flops_per_launch": col_flops,
+                "useful_tflops": col_flops / (col_ms_iso * 1e-3) / 1e12,
+                "issued_mma_flops_per_launch": mma_flops,
+                "issued_mma_tflops": mma_flops / (col_ms_iso * 1e-3) / 1e12,
+                "tf32_peak_tflops": tf32_peak,
+                "tf32_peak_source": "half of MEASURED_PEAKS.json bf16_tflops (kind::tf32 runs at half the bf16 rate)",
+                "frac_of_tf32_peak": mma_flops / (col_ms_iso * 1e-3) / 1e12 / tf32_peak,
+            }
+            kernel_name = "umma_pass_kernel<kModeDog> (tcgen05 Toeplitz-GEMM column pass + fused DoG)"
+        else:
+            engine_roof = {"note": "this kernel is FP32-FMA bound, not HBM bound (SURVEY 7, 8d): "
+                                   "arithmetic intensity 38 FLOP/B",
+                           "flops_per_launch": col_flops,
+                           "achieved_tflops": col_flops / (col_ms_iso * 1e-3) / 1e12,
+                           "peak_tflops": 71.9,
+                           "peak_source": "tools/ubench_fma.cu on this pool's B200 (FFMA, 1965 MHz)",
+                           "frac": col_flops / (col_ms_iso * 1e-3) / 1e12 / 71.9}
+            kernel_name = "col_pass_kernel<true> (fused column pass + DoG)"
+        roofline = {"bound": "hbm", "kernel": kernel_name,
+                    "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": traffic, "peak_source": peak_src,
+                    "bytes_per_launch": col_bytes, "ms_per_launch_isolated": col_ms_iso,
+                    "ms_per_launch_in_timed_region": col_ms,
+                    "tensor" if tensor_engine else "fp32": engine_roof,
+                    "whole_frame": {"bytes": frame_bytes, "flops": frame_flops,
+                                    "hbm_frac_at_value": frame_bytes * value / world / 1e9 / peak}}
         line = {
             "metric": "frames/sec, 1024x1024 DoG detector (sigma<=30, n_bin=58)",
             "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
@@ -357,21 +401,7 @@ def run_ours(args):
                     "d2h_bytes_per_step": d2h, "blobs_per_step": n_blobs,
                     "what": "Detector.run_batch over pinned host frames, wall clock"},
             "gpu_launches": KERNELS_PER_FRAME * BATCH * args.steps,
-            "roofline": {"bound": "hbm", "kernel": "col_pass_kernel<true> (fused column pass + DoG)",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "peak_source": peak_src,
-                         "bytes_per_launch": col_bytes, "ms_per_launch_isolated": col_ms_iso,
-                         "ms_per_launch_in_timed_region": col_ms,
-                         "fp32": {"note": "this kernel is FP32-FMA bound, not HBM bound (SURVEY 7, 8d): "
-                                          "arithmetic intensity 38 FLOP/B",
-                                  "flops_per_launch": col_flops,
-                                  "achieved_tflops": col_flops / (col_ms_iso * 1e-3) / 1e12,
-                                  "peak_tflops": 71.9,
-                                  "peak_source": "tools/ubench_fma.cu on this pool's B200 (FFMA, 1965 MHz)",
-                                  "frac": col_flops / (col_ms_iso * 1e-3) / 1e12 / 71.9},
-                         "whole_frame": {"bytes": frame_bytes, "flops": frame_flops,
-                                         "hbm_frac_at_value": frame_bytes * value / world / 1e9 / peak,
-                                         "fp32_frac_at_value": frame_flops * value / world / 1e12 / 71.9}},
+            "roofline": roofline,
             "clocks": clocks,
         }
         if world == 1:

@@ -57,7 +57,7 @@ constexpr int kStageCol0 = 3 * kAccCols;
 constexpr int kHalf = kUT / 2;        // accumulators are handed to the drain in two column halves
 constexpr int kLoaderGroups = 2;      // groups of 4 warps; group g fills stages with index % 2 == g
 constexpr int kMaxRawStages = 8;      // raw input-row stages in shared memory (16 KB each)
-constexpr uint32_t kSpinLimit = 1u << 27;
+constexpr unsigned long long kWaitLimitNs = 20ull * 1000 * 1000 * 1000;   // deadlock trap (20 s)
 
 enum UmmaMode { kModeRows = 0, kModeDog = 1, kModeLevels = 2 };
 
@@ -108,30 +108,30 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
         : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
     return ok != 0;
 }
-// A deadlock here would hang the GPU; trap instead (the launch then reports an error).
+// A deadlock here would hang the GPU; trap instead (the launch then reports an error).  The limit
+// is wall time, not spins: under a profiler's replay a wait can legitimately be very long.
+__device__ __noinline__ void mbar_timeout(int tag, uint32_t parity) {
+    if ((threadIdx.x & 31) == 0)
+        printf("umma: barrier timeout tag=%d block=%d warp=%d parity=%u\n", tag, blockIdx.x, threadIdx.x >> 5,
+               parity);
+    __trap();
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int tag) {
+    if (mbar_try_wait(bar, parity)) return;
+    const unsigned long long t0 = globaltimer_ns();
     uint32_t spins = 0;
-    while (!mbar_try_wait(bar, parity)) {
-        if (++spins > kSpinLimit) {
-            if ((threadIdx.x & 31) == 0)
-                printf("umma: barrier timeout tag=%d block=%d warp=%d parity=%u\n", tag, blockIdx.x,
-                       threadIdx.x >> 5, parity);
-            __trap();
-        }
-    }
+    while (!mbar_try_wait(bar, parity))
+        if ((++spins & 0xfffu) == 0 && globaltimer_ns() - t0 > kWaitLimitNs) mbar_timeout(tag, parity);
 }
 // long waits (drain, copiers): back off so that the spinning warp leaves its issue slots to
 // the converters that share the SM sub-partition
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, int tag) {
+    if (mbar_try_wait(bar, parity)) return;
+    const unsigned long long t0 = globaltimer_ns();
     uint32_t spins = 0;
     while (!mbar_try_wait(bar, parity)) {
         __nanosleep(64);
-        if (++spins > (kSpinLimit >> 4)) {
-            if ((threadIdx.x & 31) == 0)
-                printf("umma: barrier timeout tag=%d block=%d warp=%d parity=%u\n", tag, blockIdx.x,
-                       threadIdx.x >> 5, parity);
-            __trap();
-        }
+        if ((++spins & 0xfffu) == 0 && globaltimer_ns() - t0 > kWaitLimitNs) mbar_timeout(tag, parity);
     }
 }
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
@@ -287,6 +287,8 @@ __host__ __device__ constexpr uint32_t instr_desc(int M, int N) {
 
 __device__ __forceinline__ int fold_row_u(int i, int n) {
     if ((unsigned)i < (unsigned)n) return i;
+    const int once = i < 0 ? -i - 1 : 2 * n - 1 - i;      // one reflection covers radius <= n
+    if ((unsigned)once < (unsigned)n) return once;
     const int period = 2 * n;
     int t = i % period;
     if (t < 0) t += period;
