@@ -44,7 +44,8 @@ namespace dogblob {
 namespace {
 
 constexpr int kUT = 128;              // tile edge on both axes
-constexpr int kUThreads = 512;
+constexpr int kUThreads = 544;       // 17 warps, see the role list in the kernel
+constexpr int kIssuerB = 16;          // warp index of the second issuer
 constexpr int kStages = 2;            // A staging stages
 constexpr int kStageK = 4;            // k-steps (8 input rows each) per stage
 constexpr int kStageRows = 8 * kStageK;   // input rows per stage
@@ -326,6 +327,19 @@ __device__ __forceinline__ Unit decode_unit(int u, const UmmaArgs &a) {
     return x;
 }
 
+// this warp's 32 lanes x 64 columns of the three accumulators <- 0
+__device__ __forceinline__ void zero_acc_half(uint32_t lane_base, int half) {
+    const uint32_t z[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int c = 0; c < kHalf / 16; ++c) {
+        const uint32_t col = (uint32_t)(half * kHalf + c * 16);
+        tmem_st16(lane_base + kAccHiA + col, z);
+        tmem_st16(lane_base + kAccHiB + col, z);
+        tmem_st16(lane_base + kAccLo + col, z);
+    }
+    tmem_wait_st();
+}
+
 struct SharedCtl {
     unsigned long long raw_full[kMaxRawStages], raw_empty[kMaxRawStages];
     unsigned long long data_full[kStages], data_empty[kStages];
@@ -360,8 +374,8 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(smem_u32(&ctl->toep_full[b]), 1);
-            mbar_init(smem_u32(&ctl->toep_empty[b]), 1);
-            mbar_init(smem_u32(&ctl->acc_full[b]), 1);
+            mbar_init(smem_u32(&ctl->toep_empty[b]), 2);       // both issuers
+            mbar_init(smem_u32(&ctl->acc_full[b]), 2);
             mbar_init(smem_u32(&ctl->acc_empty[b]), 4);
         }
         fence_barrier_init();
@@ -375,11 +389,18 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
     if (*reinterpret_cast<volatile uint32_t *>(&ctl->tmem_base) != 0u) __trap();
     constexpr uint32_t tmem = 0u;
 
-    if (warp == 0) {
-        // ================= issuer (whole warp, one elected lane issues) =================
-        // (Measured: a tcgen05.mma costs about 70 cycles here whatever its width N <= 128, and
-        // splitting the issue over two warps does not change that: the tensor pipe, not the
-        // issuing warp, sets the pace.)
+    // the accumulators start zeroed: the issuers only ever accumulate
+    if (warp >= 4 && warp < 8) {
+        const uint32_t lane_base0 = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+        zero_acc_half(lane_base0, 0);
+        zero_acc_half(lane_base0, 1);
+        tc_fence_before();
+    }
+    __syncthreads();
+    tc_fence_after();
+
+    if (warp == 0 || warp == kIssuerB) {
+        // ================= two issuers (whole warps, one elected lane issues) =================
         // Band structure: k-step m0 only feeds outputs n in [m0 - 2 rpad, m0 + 7], so its MMAs are
         // issued for that column range only (rounded to 16; the Toeplitz window and the
         // accumulator address move with it).
@@ -390,11 +411,17 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
         // The accumulators are single buffered and handed over in two column halves: outputs
         // n < 64 are complete after k-step (63 + 2 rpad) / 8 and the next level's first 8 k-steps
         // only touch n < 64, so the drain of one half overlaps the MMAs of the other.
-        {
-        uint32_t stage_it = 0, lvl_it = 0;
+        // Issue rate: preparing and issuing one tcgen05.mma costs the issuing warp about 120 cycles
+        // (operands travel vector -> uniform registers), three times what the tensor pipe needs
+        // for it (ncu: pipe 27 % busy with one issuer).  Stages therefore alternate between two
+        // issuing warps (stage parity = TMEM stage = warp).  This is order free: the drain hands
+        // the accumulator halves back ZEROED, so every MMA accumulates and the tensor pipe may
+        // take the two warps' instructions in any interleaving; each warp commits what it issued.
+        const uint32_t me = warp == 0 ? 0u : 1u;
+        uint32_t stage_it = 0, lvl_it = 0, my_it = 0;
         constexpr uint32_t idesc0 = instr_desc(kUT, 0);
         constexpr uint32_t desc_hi = (kToepGroupBytes >> 4) | (1u << 14);        // SBO, version 1
-        RoleClock rc(a.prof != nullptr && lane == 0);
+        RoleClock rc(a.prof != nullptr && lane == 0 && warp == 0);
         for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
             const Unit un = decode_unit(u, a);
             const int lb = a.by_order ? tbl.order[un.g] : tbl.group_begin[un.g];
@@ -403,7 +430,10 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                 const int rpad2 = 2 * tbl.lv[level].rpad;
                 const int Kp = kUT + rpad2;
                 const int n_k = Kp >> 3;
-                const int k_low_last = (kHalf - 1 + rpad2) >> 3;    // last k-step that feeds n < 64
+                const int n_stage = (n_k + kStageK - 1) / kStageK;
+                // my last stage with a k-step that feeds n < 64 (k-steps up to (63 + 2 rpad) / 8)
+                int st_low = ((kHalf - 1 + rpad2) >> 3) / kStageK;
+                if (((stage_it + st_low) & 1u) != me) --st_low;
                 const uint32_t b = lvl_it & 1, par = (lvl_it >> 1) & 1, lpar = lvl_it & 1;
                 rc.lap(3);
                 mbar_wait(smem_u32(&ctl->toep_full[b]), par, 1);
@@ -411,57 +441,44 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                 mbar_wait(smem_u32(&ctl->acc_empty[0]), lpar ^ 1, 2);
                 rc.lap(1);
                 tc_fence_after();
-                // low descriptor words of the window of k-step 0 (row Kp - 8); every k-step moves
-                // the window up by 8 rows = one 256-byte group = 16 descriptor units
+                // low descriptor word of the window of k-step 0 (row Kp - 8); every k-step moves the
+                // window up by 8 rows = one 256-byte group = 16 descriptor units
                 const uint32_t t_hi = smem_u32(toep + (size_t)(2 * b) * a.toep_floats);
                 const uint32_t lo_off = (uint32_t)ttab.rows[level] * 2u;            // hi -> lo array
-                uint32_t d_hi = ((t_hi + (uint32_t)((Kp - 8) >> 3) * kToepGroupBytes) >> 4) |
-                                ((kToepHalfBytes >> 4) << 16);
-                int kidx = 0;
-                for (int k0 = 0; k0 < n_k; k0 += kStageK, ++stage_it) {
-                    const uint32_t s = stage_it % kStages, sp = (stage_it / kStages) & 1;
+                const uint32_t win0 = ((t_hi + (uint32_t)((Kp - 8) >> 3) * kToepGroupBytes) >> 4) |
+                                      ((kToepHalfBytes >> 4) << 16);
+                const uint32_t a0 = tmem + kStageCol0 + me * kStageCols;
+                bool high_ok = false;
+                for (int st = (int)((stage_it ^ me) & 1u); st < n_stage; st += 2, ++my_it) {
+                    if (!high_ok && st >= 8 / kStageK) {          // k-steps from 8 on reach n >= 64
+                        mbar_wait(smem_u32(&ctl->acc_empty[1]), lpar ^ 1, 9);
+                        high_ok = true;
+                    }
                     rc.lap(3);
-                    mbar_wait(smem_u32(&ctl->data_full[s]), sp, 3);
+                    mbar_wait(smem_u32(&ctl->data_full[me]), my_it & 1, 3);
                     rc.lap(2);
                     tc_fence_after();
-                    const uint32_t a0 = tmem + kStageCol0 + s * kStageCols;
 #pragma unroll
                     for (int ks = 0; ks < kStageK; ++ks) {
+                        const int kidx = st * kStageK + ks;
                         if (kidx < n_k && !(a.debug & 8)) {
                             const int m0 = 8 * kidx;
                             const uint32_t a_hi = a0 + ks * 16, a_lo = a_hi + 8;
-                            const uint32_t acc_hi = tmem + ((kidx & 1) ? kAccHiB : kAccHiA);
-                            const uint32_t acc_lo = tmem + kAccLo;
-                            // one column range [ns, ne) with the given initialisation flags
-                            auto issue = [&](int ns, int ne, uint32_t keep_hi, uint32_t keep_lo) {
-                                if (a.debug & 16) ne = ns + 16;          // timing experiment: narrow MMAs
-                                const uint32_t idesc = idesc0 | ((uint32_t)((ne - ns) >> 3) << 17);
-                                const uint32_t dh = d_hi + 2u * (uint32_t)ns;
-                                umma_tf32_ts_elect(acc_lo + ns, a_hi, make_desc(dh + lo_off, desc_hi), idesc, keep_lo);
-                                umma_tf32_ts_elect(acc_lo + ns, a_lo, make_desc(dh, desc_hi), idesc, 1);
-                                umma_tf32_ts_elect(acc_hi + ns, a_hi, make_desc(dh, desc_hi), idesc, keep_hi);
-                            };
-                            if (kidx < 2) {
-                                // first use of the low halves: full-half MMAs that overwrite (the
-                                // Toeplitz rows outside the band are zero)
-                                issue(0, kHalf, 0, kidx);
-                            } else if (kidx == 8 || kidx == 9) {
-                                if (kidx == 8) {
-                                    mbar_wait(smem_u32(&ctl->acc_empty[1]), lpar ^ 1, 9);
-                                    tc_fence_after();
-                                }
-                                issue(max(0, m0 - rpad2) & ~15, kHalf, 1, 1);
-                                issue(kHalf, kUT, 0, kidx == 9);          // first use of the high halves
-                            } else {
-                                issue(max(0, m0 - rpad2) & ~15, min(kUT, (m0 + 8 + 15) & ~15), 1, 1);
-                            }
-                            d_hi -= 16u;
+                            const int ns = max(0, m0 - rpad2) & ~15;
+                            const int ne = min(kUT, (m0 + 8 + 15) & ~15);
+                            const uint32_t idesc = idesc0 | ((uint32_t)((ne - ns) >> 3) << 17);
+                            const uint32_t dh = win0 - 16u * (uint32_t)kidx + 2u * (uint32_t)ns;
+                            const uint32_t acc_hi = tmem + ((kidx & 1) ? kAccHiB : kAccHiA) + ns;
+                            const uint32_t acc_lo = tmem + kAccLo + ns;
+                            umma_tf32_ts_elect(acc_lo, a_hi, make_desc(dh + lo_off, desc_hi), idesc, 1);
+                            umma_tf32_ts_elect(acc_lo, a_lo, make_desc(dh, desc_hi), idesc, 1);
+                            umma_tf32_ts_elect(acc_hi, a_hi, make_desc(dh, desc_hi), idesc, 1);
                         }
-                        if (kidx == k_low_last) umma_commit_elect(smem_u32(&ctl->acc_full[0]));
-                        ++kidx;
                     }
-                    umma_commit_elect(smem_u32(&ctl->data_empty[s]));
+                    umma_commit_elect(smem_u32(&ctl->data_empty[me]));
+                    if (st == st_low) umma_commit_elect(smem_u32(&ctl->acc_full[0]));
                 }
+                stage_it += (uint32_t)n_stage;
                 umma_commit_elect(smem_u32(&ctl->toep_empty[b]));
                 umma_commit_elect(smem_u32(&ctl->acc_full[1]));
             }
@@ -472,7 +489,6 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
             const unsigned long long tot = rc.acc[0] + rc.acc[1] + rc.acc[2] + rc.acc[3];
             atomicMax(a.prof + 10, tot);
             atomicMin(a.prof + 11, tot);
-        }
         }
     } else if (warp == 1) {
         // ================= Toeplitz copier: prebuilt hi|lo arrays, one bulk copy per level ========
@@ -636,6 +652,7 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                             }
                         }
                     }
+                    zero_acc_half(lane_base, half);          // every MMA accumulates (order free)
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(smem_u32(&ctl->acc_empty[half]));
