@@ -31,6 +31,12 @@ NVCC_FLAGS = [
 ]
 
 
+# experiment knobs of the tensor-core passes (compile-time): DOGBLOB_UMMA_ISSUERS, DOGBLOB_UMMA_STAGEK
+for _k in ("DOGBLOB_UMMA_ISSUERS", "DOGBLOB_UMMA_STAGEK"):
+    if os.environ.get(_k):
+        NVCC_FLAGS.append(f"-D{_k}={os.environ[_k]}")
+
+
 def _nvcc() -> str:
     cand = os.environ.get("NVCC") or shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
     if not Path(cand).exists():

@@ -12,24 +12,28 @@
 //
 // float32 accuracy from tf32 tensor cores: both operands are split x = hi + lo with
 // hi = rna_tf32(x), lo = rna_tf32(x - hi) (22 significant bits) and every k-step issues the three
-// products hi*lo + lo*hi + hi*hi into one float32 accumulator (the lo*lo term is below 2^-22).
+// products hi*hi, hi*lo and lo*hi (the lo*lo term is below 2^-22).  The tensor core truncates its
+// float32 accumulator after every MMA, so the hi*hi products of even / odd k-steps and the cross
+// terms go to three accumulators that the drain adds in float32 (see the issuer).
 //
-// Data flow of one CTA (persistent, one per SM, 512 threads):
-//   warps 8..15 "loaders"   global rows -> registers (coalesced along m) -> hi/lo split ->
-//                           tcgen05.st into the A staging columns of TMEM (A never touches
-//                           shared memory; 8 stages of 2 k-steps)
-//   warps 1..3  "builders"  the level's Toeplitz operand in shared memory, K-major, no swizzle.
-//                           T only depends on k - n, so ONE array G[p][kk] = w[kk - p + Kp - 8]
-//                           serves every k-step: step m0 reads the 128-row window that starts
-//                           at row Kp - 8 - m0 (the descriptor's start address slides, nothing
-//                           is copied).  Double buffered across levels.
-//   warp 0      "issuer"    one thread: 3 tcgen05.mma per k-step, tcgen05.commit releases the
-//                           A stage / the Toeplitz buffer / publishes the accumulator
-//   warps 4..7  "drain"     tcgen05.ld of the finished accumulator (lane = m, so a warp's
-//                           store of one n is 128 contiguous bytes), DoG against the previous
-//                           level kept in thread-private shared-memory slots, global stores.
-//                           Two accumulators: the drain of level i overlaps the MMAs of i+1.
-// TMEM columns: [0,256) two 128 x 128 float32 accumulators, [256,512) A staging.
+// Data flow of one CTA (persistent, one per SM, 544 threads):
+//   warps 2..3  "loaders"    32 input rows x 512 B per stage into shared memory: one TMA box
+//                            (interior) or 16-byte cp.async with folded rows (image border)
+//   warps 8..15 "converters" read the rows back with lane = m, split hi/lo, tcgen05.st into the A
+//                            staging columns of TMEM (A is an MMA operand from TMEM only)
+//   warp 1      "Toeplitz"   the level's Toeplitz operand, prebuilt on the host, one bulk copy per
+//                            level into shared memory (K-major, no swizzle).  T only depends on
+//                            k - n, so ONE array G[p][kk] = w[kk - p + Kp - 8] serves every k-step:
+//                            step m0 reads the 128-row window that starts at row Kp - 8 - m0 (the
+//                            descriptor's start address slides).  Double buffered across levels.
+//   warps 0, 16 "issuers"    stages alternate between the two warps; one elected lane issues
+//                            3 tcgen05.mma per k-step, tcgen05.commit releases the A stage / the
+//                            Toeplitz buffer / publishes the accumulator halves
+//   warps 4..7  "drain"      tcgen05.ld of a finished accumulator half (lane = m, so a warp's store
+//                            of one n is 128 contiguous bytes), sum of the three accumulators, DoG
+//                            against the previous level kept in thread-private shared-memory
+//                            slots, global stores; hands the half back zeroed
+// TMEM columns: [0,384) three 128 x 128 float32 accumulators, [384,512) two A stages.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -44,17 +48,22 @@ namespace dogblob {
 namespace {
 
 constexpr int kUT = 128;              // tile edge on both axes
-constexpr int kUThreads = 544;       // 17 warps, see the role list in the kernel
+#ifndef DOGBLOB_UMMA_ISSUERS
+#define DOGBLOB_UMMA_ISSUERS 2
+#endif
+constexpr int kIssuers = DOGBLOB_UMMA_ISSUERS;      // issuing warps: warp 0 and warps 16 ..
+constexpr int kUThreads = 32 * (16 + kIssuers - 1);
 constexpr int kIssuerB = 16;          // warp index of the second issuer
-constexpr int kStages = 2;            // A staging stages
-constexpr int kStageK = 4;            // k-steps (8 input rows each) per stage
+#ifndef DOGBLOB_UMMA_STAGEK
+#define DOGBLOB_UMMA_STAGEK 4
+#endif
+constexpr int kStageK = DOGBLOB_UMMA_STAGEK;          // k-steps (8 input rows each) per stage
+constexpr int kStages = 16 / kStageK; // A staging stages (256 TMEM columns)
 constexpr int kStageRows = 8 * kStageK;   // input rows per stage
 constexpr int kStageCols = 16 * kStageK;  // TMEM columns per stage: (hi 8 + lo 8) per k-step
 constexpr int kAccCols = 128;
-// TMEM columns: three 128 x 128 float32 accumulators (hi*hi of even k-steps, hi*hi of odd k-steps,
-// the two cross terms), then the A staging
-constexpr int kAccHiA = 0, kAccHiB = kAccCols, kAccLo = 2 * kAccCols;
-constexpr int kStageCol0 = 3 * kAccCols;
+// TMEM columns: one 128 x 128 float32 accumulator per issuing warp, then the A staging
+constexpr int kStageCol0 = kIssuers * kAccCols;
 constexpr int kHalf = kUT / 2;        // accumulators are handed to the drain in two column halves
 constexpr int kLoaderGroups = 2;      // groups of 4 warps; group g fills stages with index % 2 == g
 constexpr int kMaxRawStages = 8;      // raw input-row stages in shared memory (16 KB each)
@@ -333,9 +342,8 @@ __device__ __forceinline__ void zero_acc_half(uint32_t lane_base, int half) {
 #pragma unroll
     for (int c = 0; c < kHalf / 16; ++c) {
         const uint32_t col = (uint32_t)(half * kHalf + c * 16);
-        tmem_st16(lane_base + kAccHiA + col, z);
-        tmem_st16(lane_base + kAccHiB + col, z);
-        tmem_st16(lane_base + kAccLo + col, z);
+#pragma unroll
+        for (int i = 0; i < kIssuers; ++i) tmem_st16(lane_base + i * kAccCols + col, z);
     }
     tmem_wait_st();
 }
@@ -374,8 +382,8 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(smem_u32(&ctl->toep_full[b]), 1);
-            mbar_init(smem_u32(&ctl->toep_empty[b]), 2);       // both issuers
-            mbar_init(smem_u32(&ctl->acc_full[b]), 2);
+            mbar_init(smem_u32(&ctl->toep_empty[b]), kIssuers);
+            mbar_init(smem_u32(&ctl->acc_full[b]), kIssuers);
             mbar_init(smem_u32(&ctl->acc_empty[b]), 4);
         }
         fence_barrier_init();
@@ -399,26 +407,26 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
     __syncthreads();
     tc_fence_after();
 
-    if (warp == 0 || warp == kIssuerB) {
-        // ================= two issuers (whole warps, one elected lane issues) =================
+    if (warp == 0 || warp >= kIssuerB) {
+        // ================= issuers (whole warps, one elected lane issues) =================
         // Band structure: k-step m0 only feeds outputs n in [m0 - 2 rpad, m0 + 7], so its MMAs are
         // issued for that column range only (rounded to 16; the Toeplitz window and the
         // accumulator address move with it).
         // Accuracy: the tensor core truncates the float32 accumulator after every MMA, a bias of
-        // half an ulp of the running sum per MMA.  The hi*hi products of even and odd k-steps
-        // therefore go to two accumulators (half the chain length, about half the magnitude each)
-        // and the small cross terms to a third one; the drain adds the three in float32.
+        // half an ulp of the running sum per MMA.  Every issuing warp owns one accumulator (half
+        // the chain length, about half the magnitude each); the drain adds them in float32.
         // The accumulators are single buffered and handed over in two column halves: outputs
         // n < 64 are complete after k-step (63 + 2 rpad) / 8 and the next level's first 8 k-steps
         // only touch n < 64, so the drain of one half overlaps the MMAs of the other.
         // Issue rate: preparing and issuing one tcgen05.mma costs the issuing warp about 120 cycles
         // (operands travel vector -> uniform registers), three times what the tensor pipe needs
         // for it (ncu: pipe 27 % busy with one issuer).  Stages therefore alternate between two
-        // issuing warps (stage parity = TMEM stage = warp).  This is order free: the drain hands
-        // the accumulator halves back ZEROED, so every MMA accumulates and the tensor pipe may
-        // take the two warps' instructions in any interleaving; each warp commits what it issued.
-        const uint32_t me = warp == 0 ? 0u : 1u;
-        uint32_t stage_it = 0, lvl_it = 0, my_it = 0;
+        // issuing warps.  Each warp accumulates into its OWN accumulator, so the summation order
+        // of every output is fixed (results are bit-reproducible from run to run) however the
+        // tensor pipe interleaves the two instruction streams; the drain hands the accumulator
+        // halves back zeroed, so no MMA has to be "the first"; each warp commits what it issued.
+        const uint32_t me = warp == 0 ? 0u : (uint32_t)(warp - kIssuerB + 1);
+        uint32_t stage_it = 0, lvl_it = 0;
         constexpr uint32_t idesc0 = instr_desc(kUT, 0);
         constexpr uint32_t desc_hi = (kToepGroupBytes >> 4) | (1u << 14);        // SBO, version 1
         RoleClock rc(a.prof != nullptr && lane == 0 && warp == 0);
@@ -433,7 +441,7 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                 const int n_stage = (n_k + kStageK - 1) / kStageK;
                 // my last stage with a k-step that feeds n < 64 (k-steps up to (63 + 2 rpad) / 8)
                 int st_low = ((kHalf - 1 + rpad2) >> 3) / kStageK;
-                if (((stage_it + st_low) & 1u) != me) --st_low;
+                st_low -= (int)((stage_it + (uint32_t)st_low + kIssuers - me) % kIssuers);
                 const uint32_t b = lvl_it & 1, par = (lvl_it >> 1) & 1, lpar = lvl_it & 1;
                 rc.lap(3);
                 mbar_wait(smem_u32(&ctl->toep_full[b]), par, 1);
@@ -447,15 +455,16 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                 const uint32_t lo_off = (uint32_t)ttab.rows[level] * 2u;            // hi -> lo array
                 const uint32_t win0 = ((t_hi + (uint32_t)((Kp - 8) >> 3) * kToepGroupBytes) >> 4) |
                                       ((kToepHalfBytes >> 4) << 16);
-                const uint32_t a0 = tmem + kStageCol0 + me * kStageCols;
                 bool high_ok = false;
-                for (int st = (int)((stage_it ^ me) & 1u); st < n_stage; st += 2, ++my_it) {
+                for (int st = (int)((me + kIssuers - stage_it % kIssuers) % kIssuers); st < n_stage; st += kIssuers) {
                     if (!high_ok && st >= 8 / kStageK) {          // k-steps from 8 on reach n >= 64
                         mbar_wait(smem_u32(&ctl->acc_empty[1]), lpar ^ 1, 9);
                         high_ok = true;
                     }
+                    const uint32_t g = stage_it + (uint32_t)st, sl = g % kStages;
+                    const uint32_t a0 = tmem + kStageCol0 + sl * kStageCols;
                     rc.lap(3);
-                    mbar_wait(smem_u32(&ctl->data_full[me]), my_it & 1, 3);
+                    mbar_wait(smem_u32(&ctl->data_full[sl]), (g / kStages) & 1, 3);
                     rc.lap(2);
                     tc_fence_after();
 #pragma unroll
@@ -468,14 +477,13 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                             const int ne = min(kUT, (m0 + 8 + 15) & ~15);
                             const uint32_t idesc = idesc0 | ((uint32_t)((ne - ns) >> 3) << 17);
                             const uint32_t dh = win0 - 16u * (uint32_t)kidx + 2u * (uint32_t)ns;
-                            const uint32_t acc_hi = tmem + ((kidx & 1) ? kAccHiB : kAccHiA) + ns;
-                            const uint32_t acc_lo = tmem + kAccLo + ns;
-                            umma_tf32_ts_elect(acc_lo, a_hi, make_desc(dh + lo_off, desc_hi), idesc, 1);
-                            umma_tf32_ts_elect(acc_lo, a_lo, make_desc(dh, desc_hi), idesc, 1);
-                            umma_tf32_ts_elect(acc_hi, a_hi, make_desc(dh, desc_hi), idesc, 1);
+                            const uint32_t acc = tmem + me * kAccCols + ns;       // this warp's accumulator
+                            umma_tf32_ts_elect(acc, a_hi, make_desc(dh + lo_off, desc_hi), idesc, 1);
+                            umma_tf32_ts_elect(acc, a_lo, make_desc(dh, desc_hi), idesc, 1);
+                            umma_tf32_ts_elect(acc, a_hi, make_desc(dh, desc_hi), idesc, 1);
                         }
                     }
-                    umma_commit_elect(smem_u32(&ctl->data_empty[me]));
+                    umma_commit_elect(smem_u32(&ctl->data_empty[sl]));
                     if (st == st_low) umma_commit_elect(smem_u32(&ctl->acc_full[0]));
                 }
                 stage_it += (uint32_t)n_stage;
@@ -602,17 +610,18 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
 #pragma unroll 1
                     for (int c = 0; c < kHalf / 16; ++c) {
                         const int n0 = half * kHalf + c * 16;
-                        uint32_t ra[16], rb[16], rl[16];
-                        tmem_ld16(lane_base + kAccHiA + n0, ra);
-                        tmem_ld16(lane_base + kAccHiB + n0, rb);
-                        tmem_ld16(lane_base + kAccLo + n0, rl);
+                        uint32_t ra[kIssuers][16];
+#pragma unroll
+                        for (int i = 0; i < kIssuers; ++i) tmem_ld16(lane_base + i * kAccCols + n0, ra[i]);
                         tmem_wait_ld();
                         if (a.debug & 4) continue;
                         float r[16];
 #pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            r[j] = __fadd_rn(__fadd_rn(__uint_as_float(ra[j]), __uint_as_float(rb[j])),
-                                             __uint_as_float(rl[j]));
+                        for (int j = 0; j < 16; ++j) {
+                            r[j] = __uint_as_float(ra[0][j]);
+#pragma unroll
+                            for (int i = 1; i < kIssuers; ++i) r[j] = __fadd_rn(r[j], __uint_as_float(ra[i][j]));
+                        }
                         if (MODE == kModeRows) {
                             // lane = x (contiguous input axis), registers = 16 consecutive y of T[x][y]
                             float *dst = a.out + (int64_t)level * a.out_plane +
