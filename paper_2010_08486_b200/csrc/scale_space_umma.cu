@@ -54,11 +54,14 @@ constexpr int kUT = 128;              // tile edge on both axes
 constexpr int kIssuers = DOGBLOB_UMMA_ISSUERS;      // issuing warps: warp 0 and warps 16 ..
 constexpr int kUThreads = 32 * (16 + kIssuers - 1);
 constexpr int kIssuerB = 16;          // warp index of the second issuer
+#ifndef DOGBLOB_UMMA_ISSUERS
+#define DOGBLOB_UMMA_ISSUERS 2
+#endif
 #ifndef DOGBLOB_UMMA_STAGEK
 #define DOGBLOB_UMMA_STAGEK 4
 #endif
 constexpr int kStageK = DOGBLOB_UMMA_STAGEK;          // k-steps (8 input rows each) per stage
-constexpr int kStages = 16 / kStageK; // A staging stages (256 TMEM columns)
+constexpr int kStages = (512 - 128 * DOGBLOB_UMMA_ISSUERS) / (16 * kStageK);   // A staging stages (the TMEM columns the accumulators leave)
 constexpr int kStageRows = 8 * kStageK;   // input rows per stage
 constexpr int kStageCols = 16 * kStageK;  // TMEM columns per stage: (hi 8 + lo 8) per k-step
 constexpr int kAccCols = 128;
