@@ -41,7 +41,12 @@ RADIUS_PER_SIGMA = math.sqrt(2.0)
 DEFAULT_STACK_ELEMENT_CAP = 2 ** 28   # convolve.py:37 (the reference's host-RAM guard)
 DEFAULT_MAX_BLOBS = 1 << 16
 HOST_RESULT_BLOBS = 4096              # records copied back with the header in one D2H
-STREAM_MIN_BYTES = 1 << 20            # frames from 1 MiB upload in row chunks under the row pass
+# Frames upload in row chunks under the row pass when that hides the copy (measured, round 1):
+# from 4 MiB on the tensor-core engine (wide ladders: C2 0.64 vs 0.65 ms, C4 2.68 vs 2.87 ms), from
+# 8 MiB on the FP32 engine; below that the gate only delays a row pass that is shorter than the
+# copy (C1 0.21 vs 0.16 ms, C5 0.88 vs 0.84 ms).
+STREAM_MIN_BYTES = 4 << 20
+STREAM_MIN_BYTES_FP32 = 8 << 20
 STREAMED_UPLOAD = os.environ.get("DOGBLOB_STREAMED_UPLOAD", "1") != "0"
 
 
@@ -332,7 +337,8 @@ class _Slot:
             self._launch_with_preprocess(src, params, prune)
             return
         H, W = self.plan.shape
-        if STREAMED_UPLOAD and H * W * 4 >= STREAM_MIN_BYTES:
+        if STREAMED_UPLOAD and H * W * 4 >= (STREAM_MIN_BYTES if self.plan.conv_engine == 1
+                                             else STREAM_MIN_BYTES_FP32):
             # row chunks on the copy stream while the row pass already runs
             _lib.check(lib.dogblob_detect_host_streamed(
                 self.plan.handle, src, float(np.float32(params.threshold)), int(params.neighborhood),

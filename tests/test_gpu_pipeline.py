@@ -171,14 +171,19 @@ class TestDetectorBehaviour:
                 assert a.stats["n_merges"] == b.stats["n_merges"]
         det.close()
 
+    @pytest.mark.parametrize("engine", ["fma", "umma"])
     @pytest.mark.parametrize("shape,kw", [((600, 700), dict(min_sigma=1.0, max_sigma=8.0, n_bin=7)),
                                           ((515, 520), dict(min_sigma=30.0, max_sigma=120.0, n_bin=3)),
                                           ((1024, 1024), dict(min_sigma=2.0, max_sigma=12.0, n_bin=10))])
-    def test_streamed_upload_equals_plain_upload(self, shape, kw, monkeypatch):
-        """frames of >= 1 MiB go up in row chunks under the running row pass (gate word per
-        chunk); same records as the single pitched copy, also when the widest kernel exceeds
-        the image (every tile then waits for the whole frame) and with ragged last chunks"""
+    def test_streamed_upload_equals_plain_upload(self, shape, kw, engine, monkeypatch):
+        """large frames go up in row chunks under the running row pass (gate word per chunk);
+        same records as the single pitched copy on both convolution engines, also when the
+        widest kernel exceeds the image (every tile then waits for the whole frame) and with
+        ragged last chunks (the size thresholds are lowered to 1 MiB for the test)"""
         from paper_2010_08486_b200 import detector as D
+        monkeypatch.setenv("DOGBLOB_CONV", engine)
+        monkeypatch.setattr(D, "STREAM_MIN_BYTES", 1 << 20)
+        monkeypatch.setattr(D, "STREAM_MIN_BYTES_FP32", 1 << 20)
         frames = [synth.sensor_noise(synth.droplet_scene(shape[1], shape[0], 40, (3.0, 14.0), seed=11 + i,
                                                          allow_overlap=True), seed=31 + i).image for i in range(3)]
         params = P.DetectionParams(preprocess=False, **kw)

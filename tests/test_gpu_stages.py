@@ -106,8 +106,9 @@ class TestConvolveBank:
         got = P.convolve_bank(img, bank).levels
         assert np.abs(got - truth_levels(img, bank)).max() < LEVEL_TOL
 
-    def test_wide_filters(self):
-        bank = bank_for(20.0, 60.0, 2)          # radii 100 .. 300
+    def test_wide_filters(self, monkeypatch):
+        monkeypatch.delenv("DOGBLOB_CONV", raising=False)   # the plan's own engine (FP32 at this size);
+        bank = bank_for(20.0, 60.0, 2)          # radii 100 .. 300; tensor engine: TestEngines
         img = np.random.default_rng(5).random((256, 384)).astype(np.float32)
         got = P.convolve_bank(img, bank).levels
         assert np.abs(got - truth_levels(img, bank)).max() < LEVEL_TOL

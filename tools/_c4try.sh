@@ -1,10 +1,11 @@
 rm -f gpurun_out/variants.log
-cp paper_2010_08486_b200/libdogblob_b200.so /tmp/lib_default.so
-for v in i3_k4 i3_k2; do
-  cp tools/_bin/lib_$v.so paper_2010_08486_b200/libdogblob_b200.so
-  echo "=== $v" >> gpurun_out/variants.log
-  timeout 200 python tools/umma_probe.py C2 2>&1 | grep "^umma  .*row\|rror\|timeout" >> gpurun_out/variants.log
-  timeout 200 python tools/umma_debug.py C2 2>&1 | grep "umma\] levels\|umma\] fused\|blob sets" | cut -c1-160 >> gpurun_out/variants.log
-  timeout 300 python tools/umma_probe.py C4 2>&1 | grep "^umma  .*row" >> gpurun_out/variants.log
+for s in 1 0; do
+  echo "=== streamed=$s" >> gpurun_out/variants.log
+  DOGBLOB_STREAMED_UPLOAD=$s python tools/config_timings.py C1 C2 C4 C5 2>&1 | python -c "
+import sys, json
+for l in sys.stdin:
+    try: c=json.loads(l)
+    except Exception: print(l[:150]); continue
+    print(c['config'], 'lat', round(c['latency_ms_median'],3), 'p90', round(c['latency_ms_p90'],3), 'conv', round(c['convolve_ms'],3))
+" >> gpurun_out/variants.log
 done
-cp /tmp/lib_default.so paper_2010_08486_b200/libdogblob_b200.so
