@@ -52,7 +52,12 @@ constexpr int kUT = 128;              // tile edge on both axes
 #define DOGBLOB_UMMA_ISSUERS 2
 #endif
 constexpr int kIssuers = DOGBLOB_UMMA_ISSUERS;      // issuing warps: warp 0 and warps 16 ..
-constexpr int kUThreads = 32 * (16 + kIssuers - 1);
+#ifndef DOGBLOB_UMMA_DRAIN_GROUPS
+#define DOGBLOB_UMMA_DRAIN_GROUPS 1      // 2: column pass -3 %, row pass +6 % (672 threads cap the registers at 80)
+#endif
+constexpr int kDrainGroups = DOGBLOB_UMMA_DRAIN_GROUPS;   // 4 warps each; group 0 = warps 4..7, group 1 = the last 4 warps
+constexpr int kDrainB = 16 + kIssuers - 1;                 // first warp of the second drain group
+constexpr int kUThreads = 32 * (kDrainB + 4 * (kDrainGroups - 1));
 constexpr int kIssuerB = 16;          // warp index of the second issuer
 #ifndef DOGBLOB_UMMA_ISSUERS
 #define DOGBLOB_UMMA_ISSUERS 2
@@ -231,6 +236,23 @@ __device__ __forceinline__ void umma_tf32_ts_elect(uint32_t d_tmem, uint32_t a_t
         ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// The three MMAs of one k-step (hi*lo, lo*hi, hi*hi into one accumulator) in ONE statement: the
+// operands are moved to uniform registers once per k-step instead of once per MMA.
+__device__ __forceinline__ void umma_tf32_triple_elect(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo,
+                                                       uint32_t desc_b_lo, uint32_t desc_b_hi,
+                                                       uint32_t desc_upper, uint32_t idesc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 dl, dh;\n\t"
+        "setp.eq.b32 p, 0, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "mov.b64 dl, {%3, %5};\n\t"
+        "mov.b64 dh, {%4, %5};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], dl, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], dh, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], dh, %6, p;\n\t}"
+        ::"r"(d_tmem), "r"(a_hi), "r"(a_lo), "r"(desc_b_lo), "r"(desc_b_hi), "r"(desc_upper), "r"(idesc)
+        : "memory");
+}
 __device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t"
@@ -340,10 +362,10 @@ __device__ __forceinline__ Unit decode_unit(int u, const UmmaArgs &a) {
 }
 
 // this warp's 32 lanes x 64 columns of the three accumulators <- 0
-__device__ __forceinline__ void zero_acc_half(uint32_t lane_base, int half) {
+__device__ __forceinline__ void zero_acc_half(uint32_t lane_base, int half, int dgroup) {
     const uint32_t z[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-    for (int c = 0; c < kHalf / 16; ++c) {
+    for (int c = dgroup; c < kHalf / 16; c += kDrainGroups) {
         const uint32_t col = (uint32_t)(half * kHalf + c * 16);
 #pragma unroll
         for (int i = 0; i < kIssuers; ++i) tmem_st16(lane_base + i * kAccCols + col, z);
@@ -387,7 +409,7 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
             mbar_init(smem_u32(&ctl->toep_full[b]), 1);
             mbar_init(smem_u32(&ctl->toep_empty[b]), kIssuers);
             mbar_init(smem_u32(&ctl->acc_full[b]), kIssuers);
-            mbar_init(smem_u32(&ctl->acc_empty[b]), 4);
+            mbar_init(smem_u32(&ctl->acc_empty[b]), 4 * kDrainGroups);
         }
         fence_barrier_init();
     }
@@ -401,16 +423,18 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
     constexpr uint32_t tmem = 0u;
 
     // the accumulators start zeroed: the issuers only ever accumulate
-    if (warp >= 4 && warp < 8) {
+    const bool is_drain = (warp >= 4 && warp < 8) || (kDrainGroups > 1 && warp >= kDrainB);
+    const int dgroup = warp >= kDrainB ? 1 : 0;
+    if (is_drain) {
         const uint32_t lane_base0 = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-        zero_acc_half(lane_base0, 0);
-        zero_acc_half(lane_base0, 1);
+        zero_acc_half(lane_base0, 0, dgroup);
+        zero_acc_half(lane_base0, 1, dgroup);
         tc_fence_before();
     }
     __syncthreads();
     tc_fence_after();
 
-    if (warp == 0 || warp >= kIssuerB) {
+    if (warp == 0 || (warp >= kIssuerB && warp < kDrainB)) {
         // ================= issuers (whole warps, one elected lane issues) =================
         // Band structure: k-step m0 only feeds outputs n in [m0 - 2 rpad, m0 + 7], so its MMAs are
         // issued for that column range only (rounded to 16; the Toeplitz window and the
@@ -481,9 +505,7 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                             const uint32_t idesc = idesc0 | ((uint32_t)((ne - ns) >> 3) << 17);
                             const uint32_t dh = win0 - 16u * (uint32_t)kidx + 2u * (uint32_t)ns;
                             const uint32_t acc = tmem + me * kAccCols + ns;       // this warp's accumulator
-                            umma_tf32_ts_elect(acc, a_hi, make_desc(dh + lo_off, desc_hi), idesc, 1);
-                            umma_tf32_ts_elect(acc, a_lo, make_desc(dh, desc_hi), idesc, 1);
-                            umma_tf32_ts_elect(acc, a_hi, make_desc(dh, desc_hi), idesc, 1);
+                            umma_tf32_triple_elect(acc, a_hi, a_lo, dh + lo_off, dh, desc_hi, idesc);
                         }
                     }
                     umma_commit_elect(smem_u32(&ctl->data_empty[sl]));
@@ -588,7 +610,7 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
         }
         rc.lap(1);
         rc.flush(a.prof, 6);
-    } else if (warp < 8) {
+    } else if (is_drain) {
         // ================= drain (accumulators -> DoG -> global), one column half at a time ======
         const int q = warp & 3;
         const int m = 32 * q + lane;
@@ -611,7 +633,7 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                     rc.lap(0);
                     tc_fence_after();
 #pragma unroll 1
-                    for (int c = 0; c < kHalf / 16; ++c) {
+                    for (int c = dgroup; c < kHalf / 16; c += kDrainGroups) {   // the groups share a half
                         const int n0 = half * kHalf + c * 16;
                         uint32_t ra[kIssuers][16];
 #pragma unroll
@@ -664,7 +686,7 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                             }
                         }
                     }
-                    zero_acc_half(lane_base, half);          // every MMA accumulates (order free)
+                    zero_acc_half(lane_base, half, dgroup);  // every MMA accumulates (none is "first")
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(smem_u32(&ctl->acc_empty[half]));

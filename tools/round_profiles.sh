@@ -1,3 +1,6 @@
+# Round-end validation on the GPU box: parity tests (default and tensor engine forced), sanitizer, config timings,
+# bench (both arms), ncu launch lists and the full capture of the tensor-core passes.  Run under gpurun:
+#   gpurun -- 'bash tools/round_profiles.sh > gpurun_out/round_profiles.log 2>&1'
 set -x
 timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1
 DOGBLOB_CONV=umma DOGBLOB_STREAMED_UPLOAD=0 timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu_umma_forced.log 2>&1
