@@ -350,18 +350,29 @@ static bool use_umma(const dogblob_plan *plan) {
     if (e && e[0] == 'u') return true;
     return plan->prefer_umma;
 }
+// fp16 build of the tensor-core passes: float bits of the frame's max |x| (scale of the fp16 split)
+static uint32_t *frame_max_word(const dogblob_plan *plan, void *d_workspace) {
+    return reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(d_workspace) + plan->off_gate + 64);
+}
 static cudaError_t row_pass_any(const dogblob_plan *plan, const float *d_image, float *rows_t,
                                 cudaStream_t st, const RowGate *gate) {
-    if (use_umma(plan))
+    if (use_umma(plan)) {
+        uint32_t *mx = frame_max_word(plan, rows_t);     // rows_t is the workspace base (off_rows_t = 0)
+        if (umma_needs_frame_max()) {
+            cudaError_t e = launch_frame_max(d_image, (int64_t)plan->geo.H * plan->geo.Wp, mx, st);
+            if (e != cudaSuccess) return e;
+        }
         return launch_row_pass_umma(plan->geo, d_image, rows_t, plan->table, plan->toeplitz,
-                                    plan->d_toeplitz, st, gate);
+                                    plan->d_toeplitz, st, gate, mx);
+    }
     return launch_row_pass(plan->geo, d_image, rows_t, plan->table, plan->d_taps, st, gate);
 }
 static cudaError_t col_dog_pass_any(const dogblob_plan *plan, const float *rows_t, float *dog_t,
                                     float *edge, cudaStream_t st) {
     if (use_umma(plan)) {
         cudaError_t e = launch_col_dog_pass_umma(plan->geo, rows_t, dog_t, edge, plan->umma_table,
-                                                 plan->toeplitz, plan->d_toeplitz, st);
+                                                 plan->toeplitz, plan->d_toeplitz, st,
+                                                 frame_max_word(plan, const_cast<float *>(rows_t)));
         if (e != cudaSuccess) return e;
         return launch_edge_dog(plan->geo, edge, dog_t, plan->umma_table, st);
     }
@@ -456,6 +467,9 @@ int dogblob_detect_host_streamed(const dogblob_plan *plan, const float *h_image,
     DB_REQUIRE(copy_stream && h_gate && frame_done && copy_stream != stream,
                "streamed upload needs its own copy stream, a pinned gate array and an event");
     if (int rc = check_threshold_args(neighborhood, overlap)) return rc;
+    if (use_umma(plan) && umma_needs_frame_max())     // the fp16 split needs the whole frame's max first
+        return dogblob_detect_host(plan, h_image, threshold, neighborhood, overlap, prune, d_image,
+                                   d_workspace, d_result, h_result, h_result_blobs, stream, events);
     DeviceGuard guard(plan->device);
     DB_REQUIRE(guard.ok, "cannot select CUDA device");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -545,7 +559,7 @@ int dogblob_scale_space(const dogblob_plan *plan, const float *d_image, void *d_
     DB_CUDA(row_pass_any(plan, d_image, rows_t, st, nullptr));
     if (use_umma(plan))
         DB_CUDA(launch_col_levels_pass_umma(g, rows_t, lev_t, plan->unit_table, plan->toeplitz,
-                                            plan->d_toeplitz, st));
+                                            plan->d_toeplitz, st, frame_max_word(plan, rows_t)));
     else
         DB_CUDA(launch_col_levels_pass(g, rows_t, lev_t, plan->unit_table, plan->d_taps, st));
     DB_CUDA(launch_untranspose(lev_t, g.L, g.Hp, g.Wp, g.H, g.W, d_levels, st));

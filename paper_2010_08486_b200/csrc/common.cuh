@@ -152,20 +152,29 @@ cudaError_t launch_col_levels_pass(const ConvGeometry &g, const float *d_rows_t,
 cudaError_t launch_edge_dog(const ConvGeometry &g, const float *d_edge, float *d_dog_t,
                             const LevelTable &tbl, cudaStream_t st);
 // tensor-core (tcgen05) versions of the three passes, scale_space_umma.cu
-struct ToeplitzTable { int ofs[kMaxLevels]; int rows[kMaxLevels]; };   // per level: float offset, rows
+struct ToeplitzTable {               // per level: float offset, rows, log2 of the tap scale (fp16 mode)
+    int ofs[kMaxLevels];
+    int rows[kMaxLevels];
+    int tscale[kMaxLevels];
+};
 bool umma_supported(const ConvGeometry &g);
 void build_toeplitz(const LevelDesc *lv, int n_levels, const float2 *taps, std::vector<float> &out,
                     ToeplitzTable &tab);
 cudaError_t configure_umma_kernels(int device);
+bool umma_needs_frame_max();
+cudaError_t launch_frame_max(const float *d_img, int64_t n_floats, uint32_t *d_max_bits, cudaStream_t st);
 cudaError_t launch_row_pass_umma(const ConvGeometry &g, const float *d_img, float *d_rows_t,
                                  const LevelTable &tbl, const ToeplitzTable &ttab,
-                                 const float *d_toep, cudaStream_t st, const RowGate *gate = nullptr);
+                                 const float *d_toep, cudaStream_t st, const RowGate *gate = nullptr,
+                                 const uint32_t *d_max_bits = nullptr);
 cudaError_t launch_col_dog_pass_umma(const ConvGeometry &g, const float *d_rows_t, float *d_dog_t,
                                      float *d_edge, const LevelTable &tbl, const ToeplitzTable &ttab,
-                                     const float *d_toep, cudaStream_t st);
+                                     const float *d_toep, cudaStream_t st,
+                                     const uint32_t *d_max_bits = nullptr);
 cudaError_t launch_col_levels_pass_umma(const ConvGeometry &g, const float *d_rows_t, float *d_lev_t,
                                         const LevelTable &unit_tbl, const ToeplitzTable &ttab,
-                                        const float *d_toep, cudaStream_t st);
+                                        const float *d_toep, cudaStream_t st,
+                                        const uint32_t *d_max_bits = nullptr);
 cudaError_t launch_untranspose(const float *d_src_t, int planes, int Hp, int Wp, int H, int W,
                                float *d_dst, cudaStream_t st);
 cudaError_t launch_dog_from_levels(int L, int64_t plane_elems, const float *d_levels,

@@ -39,7 +39,8 @@
 #include <cstring>
 #include <vector>
 
-#include <cuda.h>      // CUtensorMap (types only: the encoder is fetched through the runtime)
+#include <cuda.h>
+#include <cuda_fp16.h>      // CUtensorMap (types only: the encoder is fetched through the runtime)
 
 #include "common.cuh"
 
@@ -52,6 +53,12 @@ constexpr int kUT = 128;              // tile edge on both axes
 #define DOGBLOB_UMMA_ISSUERS 2
 #endif
 constexpr int kIssuers = DOGBLOB_UMMA_ISSUERS;      // issuing warps: warp 0 and warps 16 ..
+// DOGBLOB_UMMA_F16 = 1: fp16 hi/lo operands (kind::f16, K = 16 rows per MMA: half as many MMAs as
+// the tf32 split).  fp16's range is covered by power-of-two scales: the frame by 2^e (e from the
+// frame's max |x|, found by frame_max_kernel before the row pass), every level's taps by 2^t.
+#ifndef DOGBLOB_UMMA_F16
+#define DOGBLOB_UMMA_F16 1       // 0: tf32 hi/lo split (K = 8), no frame scale, streamed uploads possible
+#endif
 #ifndef DOGBLOB_UMMA_DRAIN_GROUPS
 #define DOGBLOB_UMMA_DRAIN_GROUPS 1      // 2: column pass -3 %, row pass +6 % (672 threads cap the registers at 80)
 #endif
@@ -87,6 +94,7 @@ struct UmmaArgs {
     float *out;
     int64_t out_pitch, out_plane;
     float *edge;            // DoG mode: parked boundary levels
+    const uint32_t *frame_max_bits;   // F16 mode: float bits of the frame's max |x| (device word)
     const float *toep;      // prebuilt Toeplitz arrays of every level (hi | lo), see build_toeplitz
     int raw_stages;         // raw input-row stages that fit in shared memory
     int by_order;           // units are single levels in tbl.order[] (longest first): row pass
@@ -253,6 +261,35 @@ __device__ __forceinline__ void umma_tf32_triple_elect(uint32_t d_tmem, uint32_t
         ::"r"(d_tmem), "r"(a_hi), "r"(a_lo), "r"(desc_b_lo), "r"(desc_b_hi), "r"(desc_upper), "r"(idesc)
         : "memory");
 }
+__device__ __forceinline__ void umma_f16_triple_elect(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo,
+                                                      uint32_t desc_b_lo, uint32_t desc_b_hi,
+                                                      uint32_t desc_upper, uint32_t idesc) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 dl, dh;\n\t"
+        "setp.eq.b32 p, 0, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "mov.b64 dl, {%3, %5};\n\t"
+        "mov.b64 dh, {%4, %5};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], dl, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], dh, %6, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], dh, %6, p;\n\t}"
+        ::"r"(d_tmem), "r"(a_hi), "r"(a_lo), "r"(desc_b_lo), "r"(desc_b_hi), "r"(desc_upper), "r"(idesc)
+        : "memory");
+}
+// F16 mode: exponent e with max|x| * 2^e in [2^12, 2^13) (0 for an all-zero, NaN or Inf frame)
+__device__ __forceinline__ int frame_scale_exp(const uint32_t *max_bits) {
+    const uint32_t b = __ldcg(max_bits);
+    const int ex = (int)((b >> 23) & 0xffu);
+    if (ex == 0 || ex == 255) return 0;
+    return 12 - (ex - 127);
+}
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((uint32_t)(127 + e) << 23); }
+// two floats -> packed f16x2 (first argument in the LOW half: K element 2c, second in the high half)
+__device__ __forceinline__ uint32_t pack_f16x2(float lo_elem, float hi_elem) {
+    uint32_t d;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi_elem), "f"(lo_elem));
+    return d;
+}
 __device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t"
@@ -316,6 +353,10 @@ __device__ __forceinline__ void tmem_wait_ld() {
 constexpr uint32_t kToepGroupBytes = 256, kToepHalfBytes = 128;
 // Instruction descriptor (cute::UMMA::InstrDescriptor): D = F32, A = B = TF32, both K-major,
 // dense, N at bits [17,23) as N >> 3, M at bits [24,29) as M >> 4.
+// kind::f16 with F16 operands: format fields 0, D = F32
+__host__ __device__ constexpr uint32_t instr_desc_f16(int M, int N) {
+    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
 __host__ __device__ constexpr uint32_t instr_desc(int M, int N) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
@@ -464,10 +505,15 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
             for (int level = lb; level < le; ++level, ++lvl_it) {
                 const int rpad2 = 2 * tbl.lv[level].rpad;
                 const int Kp = kUT + rpad2;
-                const int n_k = Kp >> 3;
-                const int n_stage = (n_k + kStageK - 1) / kStageK;
-                // my last stage with a k-step that feeds n < 64 (k-steps up to (63 + 2 rpad) / 8)
-                int st_low = ((kHalf - 1 + rpad2) >> 3) / kStageK;
+#if DOGBLOB_UMMA_F16
+                constexpr int kStepRows = 16, kSteps = kStageRows / 16;      // MMA steps of 16 rows
+#else
+                constexpr int kStepRows = 8, kSteps = kStageK;
+#endif
+                const int n_k = Kp / kStepRows;
+                const int n_stage = (n_k + kSteps - 1) / kSteps;
+                // my last stage with a step that feeds n < 64 (rows up to 63 + 2 rpad)
+                int st_low = ((kHalf - 1 + rpad2) / kStepRows) / kSteps;
                 st_low -= (int)((stage_it + (uint32_t)st_low + kIssuers - me) % kIssuers);
                 const uint32_t b = lvl_it & 1, par = (lvl_it >> 1) & 1, lpar = lvl_it & 1;
                 rc.lap(3);
@@ -480,11 +526,11 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                 // window up by 8 rows = one 256-byte group = 16 descriptor units
                 const uint32_t t_hi = smem_u32(toep + (size_t)(2 * b) * a.toep_floats);
                 const uint32_t lo_off = (uint32_t)ttab.rows[level] * 2u;            // hi -> lo array
-                const uint32_t win0 = ((t_hi + (uint32_t)((Kp - 8) >> 3) * kToepGroupBytes) >> 4) |
+                const uint32_t win0 = ((t_hi + (uint32_t)((Kp - kStepRows) >> 3) * kToepGroupBytes) >> 4) |
                                       ((kToepHalfBytes >> 4) << 16);
                 bool high_ok = false;
                 for (int st = (int)((me + kIssuers - stage_it % kIssuers) % kIssuers); st < n_stage; st += kIssuers) {
-                    if (!high_ok && st >= 8 / kStageK) {          // k-steps from 8 on reach n >= 64
+                    if (!high_ok && st >= 64 / kStageRows) {      // rows from 64 on reach n >= 64
                         mbar_wait(smem_u32(&ctl->acc_empty[1]), lpar ^ 1, 9);
                         high_ok = true;
                     }
@@ -495,17 +541,24 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                     rc.lap(2);
                     tc_fence_after();
 #pragma unroll
-                    for (int ks = 0; ks < kStageK; ++ks) {
-                        const int kidx = st * kStageK + ks;
+                    for (int ks = 0; ks < kSteps; ++ks) {
+                        const int kidx = st * kSteps + ks;
                         if (kidx < n_k && !(a.debug & 8)) {
-                            const int m0 = 8 * kidx;
-                            const uint32_t a_hi = a0 + ks * 16, a_lo = a_hi + 8;
+                            const int m0 = kStepRows * kidx;
                             const int ns = max(0, m0 - rpad2) & ~15;
-                            const int ne = min(kUT, (m0 + 8 + 15) & ~15);
-                            const uint32_t idesc = idesc0 | ((uint32_t)((ne - ns) >> 3) << 17);
-                            const uint32_t dh = win0 - 16u * (uint32_t)kidx + 2u * (uint32_t)ns;
+                            const int ne = min(kUT, (m0 + kStepRows + 15) & ~15);
+                            // the window moves up by kStepRows rows = kStepRows / 8 groups of 16 units
+                            const uint32_t dh = win0 - (uint32_t)(2 * kStepRows) * (uint32_t)kidx + 2u * (uint32_t)ns;
                             const uint32_t acc = tmem + me * kAccCols + ns;       // this warp's accumulator
+#if DOGBLOB_UMMA_F16
+                            const uint32_t a_hi = a0 + ks * 32, a_lo = a_hi + 8;
+                            const uint32_t idesc = instr_desc_f16(kUT, 0) | ((uint32_t)((ne - ns) >> 3) << 17);
+                            umma_f16_triple_elect(acc, a_hi, a_lo, dh + lo_off, dh, desc_hi, idesc);
+#else
+                            const uint32_t a_hi = a0 + ks * 16, a_lo = a_hi + 8;
+                            const uint32_t idesc = idesc0 | ((uint32_t)((ne - ns) >> 3) << 17);
                             umma_tf32_triple_elect(acc, a_hi, a_lo, dh + lo_off, dh, desc_hi, idesc);
+#endif
                         }
                     }
                     umma_commit_elect(smem_u32(&ctl->data_empty[sl]));
@@ -617,6 +670,9 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
         uint32_t lvl_it = 0;
         RoleClock rc(a.prof != nullptr && warp == 4 && lane == 0);
         const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
+#if DOGBLOB_UMMA_F16
+        const int frame_exp = frame_scale_exp(a.frame_max_bits);
+#endif
         for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
             const Unit un = decode_unit(u, a);
             const int lb = a.by_order ? tbl.order[un.g] : tbl.group_begin[un.g];
@@ -626,6 +682,9 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                 const bool park_first = MODE == kModeDog && level == lb && un.g > 0;
                 const bool park_last = MODE == kModeDog && level == le - 1 && un.g < tbl.n_groups - 1;
                 const float sig = MODE == kModeDog && level > lb ? tbl.lv[level - 1].sigma_f32 : 0.f;
+#if DOGBLOB_UMMA_F16
+                const float unscale = pow2f(-(frame_exp + ttab.tscale[level]));   // exact: powers of two
+#endif
 #pragma unroll 1
                 for (int half = 0; half < 2; ++half) {
                     rc.lap(1);
@@ -646,6 +705,9 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                             r[j] = __uint_as_float(ra[0][j]);
 #pragma unroll
                             for (int i = 1; i < kIssuers; ++i) r[j] = __fadd_rn(r[j], __uint_as_float(ra[i][j]));
+#if DOGBLOB_UMMA_F16
+                            r[j] = __fmul_rn(r[j], unscale);
+#endif
                         }
                         if (MODE == kModeRows) {
                             // lane = x (contiguous input axis), registers = 16 consecutive y of T[x][y]
@@ -701,6 +763,9 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
         const int grp = (warp - 8) >> 2;
         const int m = 32 * q + lane;
         RoleClock rc(a.prof != nullptr && warp == 8 && lane == 0);
+#if DOGBLOB_UMMA_F16
+        const float xscale = pow2f(frame_scale_exp(a.frame_max_bits));
+#endif
         int total = 0;                                   // stages this CTA processes
         for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
             const Unit un = decode_unit(u, a);
@@ -724,11 +789,24 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
 #pragma unroll
                 for (int k = 0; k < 16; ++k) v[k] = src[(16 * h + k) * kUT];
                 uint32_t r0[16], r1[16];
+#if DOGBLOB_UMMA_F16
+                // 16 rows = one MMA step: columns 0..7 hi (2 rows per column), 8..15 lo
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const float s0 = __fmul_rn(v[2 * k], xscale), s1 = __fmul_rn(v[2 * k + 1], xscale);
+                    const uint32_t hp = pack_f16x2(s0, s1);
+                    const float2 hf = __half22float2(*reinterpret_cast<const __half2 *>(&hp));
+                    r0[k] = hp;
+                    r0[8 + k] = pack_f16x2(__fsub_rn(s0, hf.x), __fsub_rn(s1, hf.y));
+                    r1[k] = 0; r1[8 + k] = 0;
+                }
+#else
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     split_tf32(v[k], r0[k], r0[8 + k]);
                     split_tf32(v[8 + k], r1[k], r1[8 + k]);
                 }
+#endif
                 if (h == kStageK / 2 - 1) {               // all rows of the raw stage are in registers
                     __syncwarp();
                     if (lane == 0) mbar_arrive(smem_u32(&ctl->raw_empty[rs]));
@@ -740,7 +818,9 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                     tc_fence_after();
                 }
                 tmem_st16(dst + 32 * h, r0);
+#if !DOGBLOB_UMMA_F16
                 tmem_st16(dst + 32 * h + 16, r1);
+#endif
             }
             tmem_wait_st();
             tc_fence_before();
@@ -756,7 +836,11 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+#if DOGBLOB_UMMA_F16
+int toeplitz_rows(int rpad) { return kUT + 2 * rpad - 16 + kUT; }
+#else
 int toeplitz_rows(int rpad) { return kUT + 2 * rpad - 8 + kUT; }
+#endif
 int toeplitz_floats(int max_rpad) { return toeplitz_rows(max_rpad) * 8; }
 
 constexpr size_t kSmemLimit = 227 * 1024;
@@ -877,9 +961,31 @@ void build_toeplitz(const LevelDesc *lv, int n_levels, const float2 *taps, std::
         const int rpad = lv[i].rpad, Kp = kUT + 2 * rpad, rows = toeplitz_rows(rpad);
         tab.ofs[i] = (int)out.size();
         tab.rows[i] = rows;
+        tab.tscale[i] = 0;
         out.resize(out.size() + (size_t)rows * 16, 0.f);
-        float *hi = out.data() + tab.ofs[i], *lo = hi + (size_t)rows * 8;
         const float2 *w = taps + lv[i].tap_ofs;
+#if DOGBLOB_UMMA_F16
+        // fp16 hi | lo arrays: rows of 16 taps (32 bytes), 8-row groups of 256 bytes =
+        // [K half 0: 8 rows x 8 taps][K half 1]; taps scaled by 2^t so that the largest is in [512, 1024)
+        float wmax = 0.f;
+        for (int t = 0; t <= 2 * rpad; ++t) wmax = std::max(wmax, w[t].x);
+        int tsc = 0;
+        if (wmax > 0.f) { int ex; std::frexp(wmax, &ex); tsc = 10 - ex; }      // wmax * 2^tsc in [512, 1024)
+        tab.tscale[i] = tsc;
+        __half *hi = reinterpret_cast<__half *>(out.data() + tab.ofs[i]);
+        __half *lo = hi + (size_t)rows * 16;
+        for (int p = 0; p < rows; ++p)
+            for (int kk = 0; kk < 16; ++kk) {
+                const int t = kk - p + (Kp - 16);
+                const float v = (t >= 0 && t <= 2 * rpad) ? std::ldexp(w[t].x, tsc) : 0.f;
+                const __half h = __float2half_rn(v);
+                const __half l = __float2half_rn(v - __half2float(h));
+                const size_t o = (size_t)(p >> 3) * 128 + (kk >> 3) * 64 + (p & 7) * 8 + (kk & 7);
+                hi[o] = h;
+                lo[o] = l;
+            }
+#else
+        float *hi = out.data() + tab.ofs[i], *lo = hi + (size_t)rows * 8;
         for (int p = 0; p < rows; ++p)
             for (int kk = 0; kk < 8; ++kk) {
                 const int t = kk - p + (Kp - 8);
@@ -894,7 +1000,26 @@ void build_toeplitz(const LevelDesc *lv, int n_levels, const float2 *taps, std::
                 hi[o] = hf;
                 lo[o] = lf;
             }
+#endif
     }
+}
+
+// F16 mode: max |x| of the frame as float bits (non-negative floats order like unsigned integers)
+__global__ void frame_max_kernel(const float *__restrict__ img, int64_t n4, uint32_t *__restrict__ max_bits) {
+    float m = 0.f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(img) + i);
+        m = fmaxf(fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))), m);
+    }
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(max_bits, __float_as_uint(m));
+}
+bool umma_needs_frame_max() { return DOGBLOB_UMMA_F16 != 0; }
+cudaError_t launch_frame_max(const float *d_img, int64_t n_floats, uint32_t *d_max_bits, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(d_max_bits, 0, sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+    frame_max_kernel<<<148, 256, 0, st>>>(d_img, n_floats / 4, d_max_bits);
+    return cudaGetLastError();
 }
 
 cudaError_t configure_umma_kernels(int device) {
@@ -911,8 +1036,10 @@ cudaError_t configure_umma_kernels(int device) {
 // img[y][x] -> T_i[x][y]: contiguous axis x, convolved axis y, stored transposed
 cudaError_t launch_row_pass_umma(const ConvGeometry &g, const float *d_img, float *d_rows_t,
                                  const LevelTable &tbl, const ToeplitzTable &ttab,
-                                 const float *d_toep, cudaStream_t st, const RowGate *gate) {
+                                 const float *d_toep, cudaStream_t st, const RowGate *gate,
+                                 const uint32_t *d_max_bits) {
     UmmaArgs a{};
+    a.frame_max_bits = d_max_bits;
     a.in = d_img; a.in_pitch = g.Wp; a.in_plane = 0; a.n_rows = g.H;
     a.out = d_rows_t; a.out_pitch = g.Hp; a.out_plane = (int64_t)g.Hp * g.Wp;
     a.edge = nullptr; a.toep = d_toep;
@@ -930,8 +1057,9 @@ cudaError_t launch_row_pass_umma(const ConvGeometry &g, const float *d_img, floa
 // T_i[x][y] -> D_i^T[x][y]: contiguous axis y, convolved axis x
 cudaError_t launch_col_dog_pass_umma(const ConvGeometry &g, const float *d_rows_t, float *d_dog_t,
                                      float *d_edge, const LevelTable &tbl, const ToeplitzTable &ttab,
-                                     const float *d_toep, cudaStream_t st) {
+                                     const float *d_toep, cudaStream_t st, const uint32_t *d_max_bits) {
     UmmaArgs a{};
+    a.frame_max_bits = d_max_bits;
     a.in = d_rows_t; a.in_pitch = g.Hp; a.in_plane = (int64_t)g.Hp * g.Wp; a.n_rows = g.W;
     a.out = d_dog_t; a.out_pitch = g.Hp; a.out_plane = a.in_plane;
     a.edge = d_edge; a.toep = d_toep;
@@ -942,8 +1070,9 @@ cudaError_t launch_col_dog_pass_umma(const ConvGeometry &g, const float *d_rows_
 
 cudaError_t launch_col_levels_pass_umma(const ConvGeometry &g, const float *d_rows_t, float *d_lev_t,
                                         const LevelTable &unit_tbl, const ToeplitzTable &ttab,
-                                        const float *d_toep, cudaStream_t st) {
+                                        const float *d_toep, cudaStream_t st, const uint32_t *d_max_bits) {
     UmmaArgs a{};
+    a.frame_max_bits = d_max_bits;
     a.in = d_rows_t; a.in_pitch = g.Hp; a.in_plane = (int64_t)g.Hp * g.Wp; a.n_rows = g.W;
     a.out = d_lev_t; a.out_pitch = g.Hp; a.out_plane = a.in_plane;
     a.edge = nullptr; a.toep = d_toep;
