@@ -40,7 +40,7 @@ sys.path.insert(0, str(ROOT))
 WORKLOAD = "C2"
 BATCH = 16
 KERNELS_PER_FRAME = 8    # reset, row pass, column+DoG, edge DoG, nms, plateau, finalize_small, prune_large
-KERNELS_PER_FRAME_TENSOR = 9   # + frame_max (scale of the fp16 operand split) in front of the row pass
+KERNELS_PER_FRAME_TENSOR = 9   # fp16 build only: + frame_max (scale of the operand split) in front of the row pass
 
 
 def params_kw():
@@ -337,29 +337,34 @@ def run_ours(args):
                     else "col_dog_kernel_dram_bytes_per_launch")
             except Exception:
                 traffic = None
-        tensor_engine = eng.plan.conv_engine == 1
+        tensor_engine = eng.plan.conv_engine >= 1
+        fp16_engine = eng.plan.conv_engine == 2
         if tensor_engine:
-            # tcgen05 Toeplitz GEMM: every level spends (128 + 2 rpad) / 16 steps of three
-            # 128 x 128 x 16 fp16 MMAs per 128 x 128 tile (hi*hi, hi*lo, lo*hi; full-width count,
-            # the kernel trims the band's triangular ends)
+            # tcgen05 Toeplitz GEMM: every level spends (128 + 2 rpad) / 8 steps of three 128 x 128 x 8
+            # tf32 MMAs per 128 x 128 tile (hi*hi, hi*lo, lo*hi; fp16 build: / 16 and x 16; full-width
+            # count, the kernel trims the band's triangular ends)
             rpads = [max(8, (int(r) + 7) // 8 * 8) for r in det.bank.radii]
             tiles = ((H + 127) // 128) * ((W + 127) // 128)
-            mma_flops = tiles * sum((128 + 2 * rp) // 16 for rp in rpads) * 3 * (2.0 * 128 * 128 * 16)
+            krows = 16 if fp16_engine else 8
+            mma_flops = tiles * sum((128 + 2 * rp) // krows for rp in rpads) * 3 * (2.0 * 128 * 128 * krows)
             try:
                 f16_peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["bf16_tflops"]
             except Exception:
                 f16_peak = 2250.0
+            if not fp16_engine:
+                f16_peak /= 2.0                       # kind::tf32 runs at half the bf16 / fp16 rate
             engine_roof = {
-                "note": "tcgen05 kind::f16 Toeplitz GEMM, float32 accuracy from an fp16 hi/lo split of both "
-                        "operands (3 MMAs per 16 rows); the kernel is bound by per-MMA dispatch and by its "
-                        "conversion / drain warps, not by the tensor pipe, see DESIGN.md 3a",
+                "note": ("tcgen05 kind::f16" if fp16_engine else "tcgen05 kind::tf32") +
+                        " Toeplitz GEMM, float32 accuracy from a hi/lo split of both operands (3 MMAs per "
+                        "k-step); the kernel is bound by per-MMA dispatch and by its conversion / drain "
+                        "warps, not by the tensor pipe, see DESIGN.md 3a",
                 "useful_flops_per_launch": col_flops,
                 "useful_tflops": col_flops / (col_ms_iso * 1e-3) / 1e12,
                 "issued_mma_flops_per_launch": mma_flops,
                 "issued_mma_tflops": mma_flops / (col_ms_iso * 1e-3) / 1e12,
-                "f16_peak_tflops": f16_peak,
-                "f16_peak_source": "MEASURED_PEAKS.json bf16_tflops (kind::f16 rate)",
-                "frac_of_f16_peak": mma_flops / (col_ms_iso * 1e-3) / 1e12 / f16_peak,
+                "mma_peak_tflops": f16_peak,
+                "mma_peak_source": "MEASURED_PEAKS.json bf16_tflops (kind::f16 rate; half of it for kind::tf32)",
+                "frac_of_mma_peak": mma_flops / (col_ms_iso * 1e-3) / 1e12 / f16_peak,
             }
             kernel_name = "umma_pass_kernel<kModeDog> (tcgen05 Toeplitz-GEMM column pass + fused DoG)"
         else:
@@ -401,7 +406,7 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "blobs_per_step": n_blobs,
                     "what": "Detector.run_batch over pinned host frames, wall clock"},
-            "gpu_launches": (KERNELS_PER_FRAME_TENSOR if tensor_engine else KERNELS_PER_FRAME) * BATCH * args.steps,
+            "gpu_launches": (KERNELS_PER_FRAME_TENSOR if fp16_engine else KERNELS_PER_FRAME) * BATCH * args.steps,
             "roofline": roofline,
             "clocks": clocks,
         }

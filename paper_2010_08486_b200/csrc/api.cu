@@ -331,7 +331,10 @@ size_t dogblob_result_bytes(const dogblob_plan *plan) {
 }
 int64_t dogblob_image_pitch(const dogblob_plan *plan) { return plan ? plan->geo.Wp : 0; }
 static bool use_umma(const dogblob_plan *plan);
-int dogblob_plan_conv_engine(const dogblob_plan *plan) { return plan && use_umma(plan) ? 1 : 0; }
+int dogblob_plan_conv_engine(const dogblob_plan *plan) {
+    if (!plan || !use_umma(plan)) return 0;
+    return umma_needs_frame_max() ? 2 : 1;       // 2: experimental fp16 build of the tensor passes
+}
 size_t dogblob_blobspace_bytes(int max_blobs) { return blobspace_bytes(std::max(max_blobs, 1)); }
 
 static int check_threshold_args(int neighborhood, double overlap) {

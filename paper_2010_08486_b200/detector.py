@@ -252,7 +252,7 @@ class _Plan:
         self.workspace_bytes = int(lib.dogblob_workspace_bytes(handle))
         self.result_bytes = int(lib.dogblob_result_bytes(handle))
         self.pitch = int(lib.dogblob_image_pitch(handle))
-        self.conv_engine = int(lib.dogblob_plan_conv_engine(handle))   # 0 FP32 kernels, 1 tcgen05
+        self.conv_engine = int(lib.dogblob_plan_conv_engine(handle))   # 0 FP32 kernels, 1 tcgen05 (2: fp16 build)
 
     def close(self):
         if self.handle is not None:
