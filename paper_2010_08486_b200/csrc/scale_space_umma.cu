@@ -847,8 +847,12 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
 #if !DOGBLOB_UMMA_F16
                 tmem_st16(dst + 32 * h + 16, r1);
 #endif
+                // tcgen05.st reads its source registers asynchronously: they must not be reused
+                // (the next half's values land in the same physical registers) before wait::st.
+                // Found the hard way: without this wait some builds returned a few corrupted
+                // stages per frame, different from run to run (tools/umma_repro.py).
+                tmem_wait_st();
             }
-            tmem_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&ctl->data_full[s]));
