@@ -333,7 +333,7 @@ def run_ours(args):
         if tp.exists():
             try:
                 traffic = json.loads(tp.read_text()).get(
-                    "umma_col_dog_kernel_dram_bytes_per_launch" if eng.plan.conv_engine == 1
+                    "umma_col_dog_kernel_dram_bytes_per_launch" if eng.plan.conv_engine >= 1
                     else "col_dog_kernel_dram_bytes_per_launch")
             except Exception:
                 traffic = None

@@ -104,8 +104,8 @@ size_t dogblob_result_bytes(const dogblob_plan *plan);
 /* row pitch (in floats) of the device image the plan expects, >= width */
 int64_t dogblob_image_pitch(const dogblob_plan *plan);
 /* convolution engine this plan's frames run on (same results within float32 rounding):
- * 0 = FP32 sliding-window kernels, 1 = tcgen05 tensor-core Toeplitz GEMM (tf32 hi/lo split),
- * 2 = the same with fp16 operands (experimental build option, adds a max reduction per frame).
+ * 0 = FP32 sliding-window kernels, 2 = tcgen05 tensor-core Toeplitz GEMM with an fp16 hi/lo operand
+ * split (default build; one max reduction per frame), 1 = the same with tf32 operands (build option).
  * Chosen at plan time from the ladder and the frame size; DOGBLOB_CONV=fma|umma overrides. */
 int dogblob_plan_conv_engine(const dogblob_plan *plan);
 

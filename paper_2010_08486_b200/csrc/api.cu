@@ -333,7 +333,7 @@ int64_t dogblob_image_pitch(const dogblob_plan *plan) { return plan ? plan->geo.
 static bool use_umma(const dogblob_plan *plan);
 int dogblob_plan_conv_engine(const dogblob_plan *plan) {
     if (!plan || !use_umma(plan)) return 0;
-    return umma_needs_frame_max() ? 2 : 1;       // 2: experimental fp16 build of the tensor passes
+    return umma_needs_frame_max() ? 2 : 1;       // 2: fp16 operands (default build), 1: tf32 operands
 }
 size_t dogblob_blobspace_bytes(int max_blobs) { return blobspace_bytes(std::max(max_blobs, 1)); }
 

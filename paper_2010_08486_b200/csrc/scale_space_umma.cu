@@ -49,24 +49,18 @@ namespace dogblob {
 namespace {
 
 constexpr int kUT = 128;              // tile edge on both axes
-// DOGBLOB_UMMA_F16 = 1: fp16 hi/lo operands (kind::f16, K = 16 rows per MMA: half as many MMAs as
-// the tf32 split).  fp16's range is covered by power-of-two scales: the frame by 2^e (e from the
-// frame's max |x|, found by frame_max_kernel before the row pass), every level's taps by 2^t.
-// EXPERIMENTAL, off: the fp16 build is 10 % faster (C2: 0.18 + 0.18 ms) and passed the whole GPU
-// suite, but some builds of it (same source up to unrelated edits) return a few corrupted
-// accumulator halves per frame that differ from run to run (tools/umma_repro.py), with one issuer
-// as well as with two.  No tf32 build has ever shown that, so tf32 stays the default until the
-// cause is found.
+// DOGBLOB_UMMA_F16 = 1 (default): fp16 hi/lo operands (kind::f16, K = 16 rows per MMA: half as many
+// MMAs as the tf32 split, 11 + 11 significand bits all the same).  fp16's range is covered by exact
+// power-of-two scales: the frame by 2^e (max |x| * 2^e in [2^12, 2^13), e from frame_max_kernel in
+// front of the row pass), every level's taps by 2^t (largest tap in [512, 1024)); the drain undoes
+// both.  Values far below the frame's maximum lose relative, not absolute, precision.
+// DOGBLOB_UMMA_F16 = 0: tf32 hi/lo operands (K = 8), no frame scale, so the row pass can start
+// under a streamed upload; 10 % slower.
 #ifndef DOGBLOB_UMMA_F16
-#define DOGBLOB_UMMA_F16 0
+#define DOGBLOB_UMMA_F16 1
 #endif
 #ifndef DOGBLOB_UMMA_ISSUERS
-#if DOGBLOB_UMMA_F16
-// fp16 operands: one issuing warp keeps up with half the MMAs (two issuers: same time, measured)
-#define DOGBLOB_UMMA_ISSUERS 1
-#else
-#define DOGBLOB_UMMA_ISSUERS 2
-#endif
+#define DOGBLOB_UMMA_ISSUERS 2       // fp16: 0.181 + 0.184 ms at C2 (one issuer: 0.189 + 0.188)
 #endif
 // accumulators: one per issuing warp; a single issuer alternates between two (even / odd steps)
 #define DOGBLOB_UMMA_ACCS (DOGBLOB_UMMA_ISSUERS > 1 ? DOGBLOB_UMMA_ISSUERS : 2)

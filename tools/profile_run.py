@@ -2,7 +2,7 @@
 """Tiny driver for ncu: N frames of the bench workload through Detector.run
 (the same call bench.py's latency leg times).  Usage under gpurun:
 
-  ncu --metrics gpu__time_duration.sum --clock-control none -s 33 -c 22 --csv \
+  ncu --metrics gpu__time_duration.sum --clock-control none -s 36 -c 9 --csv \
       --log-file gpurun_out/launches.csv python tools/profile_run.py --frames 5
 """
 import argparse
