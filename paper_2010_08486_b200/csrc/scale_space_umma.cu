@@ -8,13 +8,14 @@
 //
 //   m : 128 positions along the CONTIGUOUS axis of the input plane (one TMEM lane each)
 //   n : 128 outputs along the convolved (strided) axis
-//   k : the 128 + 2 rpad input rows the 128 outputs read, 8 per tcgen05.mma (kind::tf32)
+//   k : the 128 + 2 rpad input rows the 128 outputs read, 16 per tcgen05.mma (kind::f16)
 //
-// float32 accuracy from tf32 tensor cores: both operands are split x = hi + lo with
-// hi = rna_tf32(x), lo = rna_tf32(x - hi) (22 significant bits) and every k-step issues the three
-// products hi*hi, hi*lo and lo*hi (the lo*lo term is below 2^-22).  The tensor core truncates its
-// float32 accumulator after every MMA, so the hi*hi products of even / odd k-steps and the cross
-// terms go to three accumulators that the drain adds in float32 (see the issuer).
+// float32 accuracy from fp16 tensor-core operands: both operands are split x = hi + lo with
+// hi = fp16(x), lo = fp16(x - hi) (11 + 11 significand bits; exact power-of-two scales keep them in
+// fp16's range, see DOGBLOB_UMMA_F16 below) and every step issues the three products hi*hi, hi*lo
+// and lo*hi (the lo*lo term is below 2^-22).  The tensor core truncates its float32 accumulator
+// after every MMA, so each issuing warp owns one accumulator (half the chain) and the drain adds
+// them in float32.  Build option: tf32 operands (K = 8, no scales).
 //
 // Data flow of one CTA (persistent, one per SM, 544 threads):
 //   warps 2..3  "loaders"    32 input rows x 512 B per stage into shared memory: one TMA box
