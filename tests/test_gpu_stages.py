@@ -153,6 +153,24 @@ class TestEngines:
         dog = P.fused_dog(img, bank).slices
         assert (np.abs(dog - (truth[:-1] - truth[1:]) * sig) / sig).max() < 2e-6
 
+    @pytest.mark.parametrize("scale,offset", [(1e-3, 0.0), (255.0, 0.0), (6.0e4, 0.0), (1.0, -0.5), (3.0e-12, 0.0)])
+    def test_tensor_engine_any_value_range(self, monkeypatch, scale, offset):
+        """the fp16 operand split is range free: frames are scaled by an exact power of two taken
+        from their own maximum, so the relative accuracy does not depend on the units (sensor
+        counts, [0, 1], tiny values) or on the sign of the data"""
+        monkeypatch.setenv("DOGBLOB_CONV", "umma")
+        bank = bank_for(1.0, 20.0, 19)
+        base = np.random.default_rng(33).random((260, 390)).astype(np.float32)
+        img = ((base + np.float32(offset)) * np.float32(scale)).astype(np.float32)
+        truth = truth_levels(img, bank)
+        got = P.convolve_bank(img, bank).levels
+        assert np.abs(got - truth).max() < LEVEL_TOL_TENSOR_WIDE * np.abs(img).max()
+
+    def test_tensor_engine_zero_frame(self, monkeypatch):
+        monkeypatch.setenv("DOGBLOB_CONV", "umma")
+        bank = bank_for(1.0, 6.0, 5)
+        assert not P.convolve_bank(np.zeros((130, 140), np.float32), bank).levels.any()
+
     def test_tensor_engine_is_bit_reproducible(self, monkeypatch):
         monkeypatch.setenv("DOGBLOB_CONV", "umma")
         bank = bank_for(2.0, 30.0, 14)
