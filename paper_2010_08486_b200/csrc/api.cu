@@ -78,6 +78,7 @@ struct dogblob_plan {
     bool prefer_umma = false; // plan-time choice of the convolution engine (see dogblob_plan_create)
     ToeplitzTable toeplitz;  // tensor-core passes: prebuilt Toeplitz operands of every level
     float *d_toeplitz = nullptr;
+    int *d_sched_rows = nullptr, *d_sched_cols = nullptr;   // cost-balanced unit order of the two passes
     double *d_slice_sigma = nullptr;
     float *d_sigma_f32 = nullptr;
     // workspace layout (bytes from the workspace base)
@@ -294,6 +295,17 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
         PLAN_CUDA(cudaMalloc(&plan->d_toeplitz, toep.size() * sizeof(float)));
         PLAN_CUDA(cudaMemcpy(plan->d_toeplitz, toep.data(), toep.size() * sizeof(float),
                              cudaMemcpyHostToDevice));
+        // Cost-balanced unit order: measured a wash (C4 column pass -4 %, but at C2 the units of one
+        // level no longer run together and the halo rows are re-read from DRAM: +36 % traffic, -3 %
+        // frames/s), so it is opt-in.
+        if (std::getenv("DOGBLOB_UMMA_SCHED")) {
+            const std::vector<int> sr = build_umma_schedule(g, plan->table, true);
+            const std::vector<int> sc = build_umma_schedule(g, plan->umma_table, false);
+            PLAN_CUDA(cudaMalloc(&plan->d_sched_rows, sr.size() * sizeof(int)));
+            PLAN_CUDA(cudaMalloc(&plan->d_sched_cols, sc.size() * sizeof(int)));
+            PLAN_CUDA(cudaMemcpy(plan->d_sched_rows, sr.data(), sr.size() * sizeof(int), cudaMemcpyHostToDevice));
+            PLAN_CUDA(cudaMemcpy(plan->d_sched_cols, sc.data(), sc.size() * sizeof(int), cudaMemcpyHostToDevice));
+        }
     }
     PLAN_CUDA(configure_conv_kernels(device));
     PLAN_CUDA(configure_umma_kernels(device));
@@ -317,6 +329,8 @@ void dogblob_plan_destroy(dogblob_plan *plan) {
     DeviceGuard guard(plan->device);
     cudaFree(plan->d_taps);
     cudaFree(plan->d_toeplitz);
+    cudaFree(plan->d_sched_rows);
+    cudaFree(plan->d_sched_cols);
     cudaFree(plan->d_slice_sigma);
     cudaFree(plan->d_sigma_f32);
     delete plan;
@@ -366,7 +380,8 @@ static cudaError_t row_pass_any(const dogblob_plan *plan, const float *d_image, 
             if (e != cudaSuccess) return e;
         }
         return launch_row_pass_umma(plan->geo, d_image, rows_t, plan->table, plan->toeplitz,
-                                    plan->d_toeplitz, st, gate, mx);
+                                    plan->d_toeplitz, st, gate, mx,
+                                    std::getenv("DOGBLOB_UMMA_SCHED_ROWS") ? plan->d_sched_rows : nullptr);   // row pass: +4 % at C4
     }
     return launch_row_pass(plan->geo, d_image, rows_t, plan->table, plan->d_taps, st, gate);
 }
@@ -375,7 +390,8 @@ static cudaError_t col_dog_pass_any(const dogblob_plan *plan, const float *rows_
     if (use_umma(plan)) {
         cudaError_t e = launch_col_dog_pass_umma(plan->geo, rows_t, dog_t, edge, plan->umma_table,
                                                  plan->toeplitz, plan->d_toeplitz, st,
-                                                 frame_max_word(plan, const_cast<float *>(rows_t)));
+                                                 frame_max_word(plan, const_cast<float *>(rows_t)),
+                                                 plan->d_sched_cols);
         if (e != cudaSuccess) return e;
         return launch_edge_dog(plan->geo, edge, dog_t, plan->umma_table, st);
     }

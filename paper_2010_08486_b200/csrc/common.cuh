@@ -166,11 +166,12 @@ cudaError_t launch_frame_max(const float *d_img, int64_t n_floats, uint32_t *d_m
 cudaError_t launch_row_pass_umma(const ConvGeometry &g, const float *d_img, float *d_rows_t,
                                  const LevelTable &tbl, const ToeplitzTable &ttab,
                                  const float *d_toep, cudaStream_t st, const RowGate *gate = nullptr,
-                                 const uint32_t *d_max_bits = nullptr);
+                                 const uint32_t *d_max_bits = nullptr, const int *d_sched = nullptr);
+std::vector<int> build_umma_schedule(const ConvGeometry &g, const LevelTable &tbl, bool rows_pass);
 cudaError_t launch_col_dog_pass_umma(const ConvGeometry &g, const float *d_rows_t, float *d_dog_t,
                                      float *d_edge, const LevelTable &tbl, const ToeplitzTable &ttab,
                                      const float *d_toep, cudaStream_t st,
-                                     const uint32_t *d_max_bits = nullptr);
+                                     const uint32_t *d_max_bits = nullptr, const int *d_sched = nullptr);
 cudaError_t launch_col_levels_pass_umma(const ConvGeometry &g, const float *d_rows_t, float *d_lev_t,
                                         const LevelTable &unit_tbl, const ToeplitzTable &ttab,
                                         const float *d_toep, cudaStream_t st,

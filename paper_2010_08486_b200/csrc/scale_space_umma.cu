@@ -114,6 +114,7 @@ struct UmmaArgs {
     int tma_plane_rows;     // rows between level planes in the tensor map (0: one plane)
     int tiles_c, tiles_r;   // tiles along the contiguous / the convolved axis
     int n_units;            // tiles_c * tiles_r * n_groups
+    const int *sched;       // optional: position i of a CTA's round-robin walk -> unit (cost-balanced order)
     int toep_floats;        // floats of one Toeplitz array (hi or lo) of the widest level
     unsigned long long *prof;   // DOGBLOB_UMMA_PROF: per-role cycle counters (see launch_umma)
     int debug;              // DOGBLOB_UMMA_DEBUG: 1 loaders skip global loads, 2 builders build once,
@@ -403,7 +404,8 @@ struct RoleClock {
 };
 
 struct Unit { int g, r0, c0; };
-__device__ __forceinline__ Unit decode_unit(int u, const UmmaArgs &a) {
+__device__ __forceinline__ Unit decode_unit(int i, const UmmaArgs &a) {
+    const int u = a.sched ? __ldg(a.sched + i) : i;
     Unit x;
     x.c0 = (u % a.tiles_c) * kUT;
     const int t = u / a.tiles_c;
@@ -1047,6 +1049,46 @@ cudaError_t launch_frame_max(const float *d_img, int64_t n_floats, uint32_t *d_m
     return cudaGetLastError();
 }
 
+// Cost-balanced static schedule.  CTA b walks positions b, b + n_ctas, ... ; the units are sorted
+// by modelled cost (stages, +1.5 per stage that crosses the image border and goes through the
+// folded cp.async path, +1 per level) and dealt to the CTAs in boustrophedon order, so every CTA
+// gets a similar sum.  rows_axis = valid rows along the convolved axis (H for the row pass, W for
+// the column pass).
+std::vector<int> build_umma_schedule(const ConvGeometry &g, const LevelTable &tbl, bool rows_pass) {
+    const int tiles_c = (rows_pass ? g.Wp : g.Hp) / kUT, tiles_r = (rows_pass ? g.Hp : g.Wp) / kUT;
+    const int n_rows = rows_pass ? g.H : g.W;
+    const int n_g = rows_pass ? tbl.n_levels : tbl.n_groups;
+    const int n_units = tiles_c * tiles_r * n_g;
+    std::vector<std::pair<double, int>> cost(n_units);
+    for (int u = 0; u < n_units; ++u) {
+        const int t = u / tiles_c, tr = t % tiles_r, gi = t / tiles_r;
+        const int lb = rows_pass ? tbl.order[gi] : tbl.group_begin[gi];
+        const int le = rows_pass ? lb + 1 : tbl.group_begin[gi + 1];
+        double c = 0.0;
+        for (int level = lb; level < le; ++level) {
+            const int rpad = tbl.lv[level].rpad;
+            const int n_stage = (kUT + 2 * rpad + kStageRows - 1) / kStageRows;
+            int row0 = tr * kUT - rpad;
+            for (int st = 0; st < n_stage; ++st, row0 += kStageRows)
+                c += (row0 >= 0 && row0 + kStageRows <= n_rows) ? 1.0 : 2.5;
+            c += 1.0;
+        }
+        cost[u] = {c, u};
+    }
+    std::stable_sort(cost.begin(), cost.end(), [](const std::pair<double, int> &x, const std::pair<double, int> &y) {
+        return x.first > y.first;
+    });
+    const int ctas = persistent_ctas(n_units);
+    std::vector<int> sched(n_units);
+    for (int r = 0; r < n_units; ++r) {
+        const int round = r / ctas, k = r % ctas;
+        const int last = std::min(ctas, n_units - round * ctas);        // units in this round
+        const int pos = (round & 1) ? last - 1 - k : k;
+        sched[round * ctas + pos] = cost[r].second;
+    }
+    return sched;
+}
+
 cudaError_t configure_umma_kernels(int device) {
     int optin = 0;
     cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
@@ -1062,7 +1104,7 @@ cudaError_t configure_umma_kernels(int device) {
 cudaError_t launch_row_pass_umma(const ConvGeometry &g, const float *d_img, float *d_rows_t,
                                  const LevelTable &tbl, const ToeplitzTable &ttab,
                                  const float *d_toep, cudaStream_t st, const RowGate *gate,
-                                 const uint32_t *d_max_bits) {
+                                 const uint32_t *d_max_bits, const int *d_sched) {
     UmmaArgs a{};
     a.frame_max_bits = d_max_bits;
     a.in = d_img; a.in_pitch = g.Wp; a.in_plane = 0; a.n_rows = g.H;
@@ -1072,6 +1114,7 @@ cudaError_t launch_row_pass_umma(const ConvGeometry &g, const float *d_img, floa
     a.by_order = 1;                       // independent levels: finest units, longest first
     a.n_order = tbl.n_levels;
     a.n_units = a.tiles_c * a.tiles_r * tbl.n_levels;
+    a.sched = gate ? nullptr : d_sched;       // streamed uploads need the tile-row-major order
     if (gate) {
         a.gate_word = gate->word; a.gate_base = gate->base;
         a.gate_rows_per_chunk = gate->rows_per_chunk; a.gate_t_start = gate->t_start;
@@ -1082,9 +1125,11 @@ cudaError_t launch_row_pass_umma(const ConvGeometry &g, const float *d_img, floa
 // T_i[x][y] -> D_i^T[x][y]: contiguous axis y, convolved axis x
 cudaError_t launch_col_dog_pass_umma(const ConvGeometry &g, const float *d_rows_t, float *d_dog_t,
                                      float *d_edge, const LevelTable &tbl, const ToeplitzTable &ttab,
-                                     const float *d_toep, cudaStream_t st, const uint32_t *d_max_bits) {
+                                     const float *d_toep, cudaStream_t st, const uint32_t *d_max_bits,
+                                     const int *d_sched) {
     UmmaArgs a{};
     a.frame_max_bits = d_max_bits;
+    a.sched = d_sched;
     a.in = d_rows_t; a.in_pitch = g.Hp; a.in_plane = (int64_t)g.Hp * g.Wp; a.n_rows = g.W;
     a.out = d_dog_t; a.out_pitch = g.Hp; a.out_plane = a.in_plane;
     a.edge = d_edge; a.toep = d_toep;
