@@ -75,14 +75,16 @@ struct dogblob_plan {
     LevelTable unit_table;   // stage API: one level per group
     LevelTable umma_table;   // tensor-core column pass: groups balanced for persistent CTAs
     float2 *d_taps = nullptr;
-    bool prefer_umma = false; // plan-time choice of the convolution engine (see dogblob_plan_create)
+    bool use_umma = false;   // plan-time choice of the convolution engine (see dogblob_plan_create)
     ToeplitzTable toeplitz;  // tensor-core passes: prebuilt Toeplitz operands of every level
     float *d_toeplitz = nullptr;
-    int *d_sched_rows = nullptr, *d_sched_cols = nullptr;   // cost-balanced unit order of the two passes
     double *d_slice_sigma = nullptr;
     float *d_sigma_f32 = nullptr;
     // workspace layout (bytes from the workspace base)
-    size_t off_rows_t = 0, off_dog_t = 0, off_edge = 0, off_blobspace = 0, off_gate = 0, total = 0;
+    // FP32 engine: rows_t = row-filtered planes (x-major), dog_t = DoG^T planes, edge = parked levels;
+    // tensor engine: rows_t = R planes (fp16 hi | lo), x = X planes, dog_t = DoG planes (image
+    // orientation), no edge planes
+    size_t off_rows_t = 0, off_x = 0, off_dog_t = 0, off_edge = 0, off_blobspace = 0, off_gate = 0, total = 0;
 };
 
 namespace {
@@ -280,32 +282,25 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
                          cudaMemcpyHostToDevice));
     PLAN_CUDA(cudaMemcpy(plan->d_sigma_f32, sig32.data(), n_levels * sizeof(float),
                          cudaMemcpyHostToDevice));
-    // Engine choice.  The Toeplitz GEMM spends 128 + 2 rpad input rows per 128 outputs and level,
-    // the sliding window 2 rpad + 33, at about 2.4 times the cost per row (measured, C2): the
-    // tensor-core passes win for wide filters on frames that fill the 148 persistent CTAs.
+    // Engine choice (plan time).  The Toeplitz GEMM spends 128 + 2 rpad input rows per 128 outputs
+    // and level, the sliding window 2 rpad + 33: the tensor-core passes win for wide filters on frames
+    // that fill the 148 persistent CTAs.  DOGBLOB_CONV=fma|umma (read here, once per plan) overrides.
     {
         double sum_rpad = 0.0;
         for (int i = 0; i < n_levels; ++i) sum_rpad += plan->levels[i].rpad;
-        plan->prefer_umma = umma_supported(g) && sum_rpad / n_levels >= 48.0 && tiles >= 48;
+        plan->use_umma = umma_supported(g) && sum_rpad / n_levels >= 48.0 && tiles >= 48;
+        if (const char *e = std::getenv("DOGBLOB_CONV")) {
+            if (e[0] == 'f') plan->use_umma = false;
+            if (e[0] == 'u') plan->use_umma = umma_supported(g);
+        }
     }
-    if (umma_supported(g)) {
+    if (plan->use_umma) {
         std::vector<float> toep;
         std::memset(&plan->toeplitz, 0, sizeof(ToeplitzTable));
         build_toeplitz(plan->levels.data(), n_levels, table.data(), toep, plan->toeplitz);
         PLAN_CUDA(cudaMalloc(&plan->d_toeplitz, toep.size() * sizeof(float)));
         PLAN_CUDA(cudaMemcpy(plan->d_toeplitz, toep.data(), toep.size() * sizeof(float),
                              cudaMemcpyHostToDevice));
-        // Cost-balanced unit order: measured a wash (C4 column pass -4 %, but at C2 the units of one
-        // level no longer run together and the halo rows are re-read from DRAM: +36 % traffic, -3 %
-        // frames/s), so it is opt-in.
-        if (std::getenv("DOGBLOB_UMMA_SCHED")) {
-            const std::vector<int> sr = build_umma_schedule(g, plan->table, true);
-            const std::vector<int> sc = build_umma_schedule(g, plan->umma_table, false);
-            PLAN_CUDA(cudaMalloc(&plan->d_sched_rows, sr.size() * sizeof(int)));
-            PLAN_CUDA(cudaMalloc(&plan->d_sched_cols, sc.size() * sizeof(int)));
-            PLAN_CUDA(cudaMemcpy(plan->d_sched_rows, sr.data(), sr.size() * sizeof(int), cudaMemcpyHostToDevice));
-            PLAN_CUDA(cudaMemcpy(plan->d_sched_cols, sc.data(), sc.size() * sizeof(int), cudaMemcpyHostToDevice));
-        }
     }
     PLAN_CUDA(configure_conv_kernels(device));
     PLAN_CUDA(configure_umma_kernels(device));
@@ -314,9 +309,18 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
 
     const size_t plane = (size_t)g.Hp * g.Wp * sizeof(float);
     size_t off = 0;
-    plan->off_rows_t = off; off += align_up(plane * n_levels, 256);
-    plan->off_dog_t = off;  off += align_up(plane * n_levels, 256);   // L planes: also holds levels
-    plan->off_edge = off;   off += align_up(plane * 2 * std::max(g.G, plan->umma_table.n_groups), 256);   // boundary levels
+    if (plan->use_umma) {
+        const UmmaLayout ul = umma_layout(g);
+        plan->off_rows_t = off; off += align_up(ul.r_bytes, 1024);
+        plan->off_x = off;      off += align_up(ul.x_bytes, 1024);
+        plan->off_dog_t = off;  off += align_up(plane * n_levels, 1024);   // L planes: also holds levels
+        plan->off_edge = off;
+    } else {
+        plan->off_rows_t = off; off += align_up(plane * n_levels, 256);
+        plan->off_x = off;
+        plan->off_dog_t = off;  off += align_up(plane * n_levels, 256);   // L planes: also holds levels
+        plan->off_edge = off;   off += align_up(plane * 2 * g.G, 256);    // boundary levels
+    }
     plan->off_blobspace = off; off += blobspace_bytes(max_blobs);
     plan->off_gate = off;   off += 256;                                   // streamed upload: gate word
     plan->total = off;
@@ -329,8 +333,6 @@ void dogblob_plan_destroy(dogblob_plan *plan) {
     DeviceGuard guard(plan->device);
     cudaFree(plan->d_taps);
     cudaFree(plan->d_toeplitz);
-    cudaFree(plan->d_sched_rows);
-    cudaFree(plan->d_sched_cols);
     cudaFree(plan->d_slice_sigma);
     cudaFree(plan->d_sigma_f32);
     delete plan;
@@ -344,11 +346,7 @@ size_t dogblob_result_bytes(const dogblob_plan *plan) {
     return plan ? dogblob_result_bytes_for(plan->max_blobs) : 0;
 }
 int64_t dogblob_image_pitch(const dogblob_plan *plan) { return plan ? plan->geo.Wp : 0; }
-static bool use_umma(const dogblob_plan *plan);
-int dogblob_plan_conv_engine(const dogblob_plan *plan) {
-    if (!plan || !use_umma(plan)) return 0;
-    return umma_needs_frame_max() ? 2 : 1;       // 2: fp16 operands (default build), 1: tf32 operands
-}
+int dogblob_plan_conv_engine(const dogblob_plan *plan) { return plan && plan->use_umma ? 2 : 0; }
 size_t dogblob_blobspace_bytes(int max_blobs) { return blobspace_bytes(std::max(max_blobs, 1)); }
 
 static int check_threshold_args(int neighborhood, double overlap) {
@@ -357,56 +355,57 @@ static int check_threshold_args(int neighborhood, double overlap) {
     return DOGBLOB_OK;
 }
 
-// Which engine runs the two convolution passes: the tensor-core Toeplitz GEMM
-// (scale_space_umma.cu) or the FP32 sliding-window kernels (scale_space.cu).
-// DOGBLOB_CONV=fma|umma overrides (read per call: tools compare both in one process).
-static bool use_umma(const dogblob_plan *plan) {
-    if (!plan->d_toeplitz) return false;
-    const char *e = std::getenv("DOGBLOB_CONV");
-    if (e && e[0] == 'f') return false;
-    if (e && e[0] == 'u') return true;
-    return plan->prefer_umma;
-}
-// fp16 build of the tensor-core passes: float bits of the frame's max |x| (scale of the fp16 split)
+// tensor engine: float bits of the frame's max |x| (scale of the fp16 operand split)
 static uint32_t *frame_max_word(const dogblob_plan *plan, void *d_workspace) {
     return reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(d_workspace) + plan->off_gate + 64);
 }
-static cudaError_t row_pass_any(const dogblob_plan *plan, const float *d_image, float *rows_t,
+// Scale-space pass 1 on the plan's engine: the tensor-core Toeplitz GEMM (scale_space_umma.cu:
+// frame -> fp16 hi | lo planes -> level rows) or the FP32 sliding-window kernel (scale_space.cu).
+static cudaError_t row_pass_any(const dogblob_plan *plan, const float *d_image, void *d_workspace,
                                 cudaStream_t st, const RowGate *gate) {
-    if (use_umma(plan)) {
-        uint32_t *mx = frame_max_word(plan, rows_t);     // rows_t is the workspace base (off_rows_t = 0)
-        if (umma_needs_frame_max()) {
-            cudaError_t e = launch_frame_max(d_image, (int64_t)plan->geo.H * plan->geo.Wp, mx, st);
-            if (e != cudaSuccess) return e;
-        }
-        return launch_row_pass_umma(plan->geo, d_image, rows_t, plan->table, plan->toeplitz,
-                                    plan->d_toeplitz, st, gate, mx,
-                                    std::getenv("DOGBLOB_UMMA_SCHED_ROWS") ? plan->d_sched_rows : nullptr);   // row pass: +4 % at C4
-    }
-    return launch_row_pass(plan->geo, d_image, rows_t, plan->table, plan->d_taps, st, gate);
-}
-static cudaError_t col_dog_pass_any(const dogblob_plan *plan, const float *rows_t, float *dog_t,
-                                    float *edge, cudaStream_t st) {
-    if (use_umma(plan)) {
-        cudaError_t e = launch_col_dog_pass_umma(plan->geo, rows_t, dog_t, edge, plan->umma_table,
-                                                 plan->toeplitz, plan->d_toeplitz, st,
-                                                 frame_max_word(plan, const_cast<float *>(rows_t)),
-                                                 plan->d_sched_cols);
+    char *ws = reinterpret_cast<char *>(d_workspace);
+    if (plan->use_umma) {
+        uint32_t *mx = frame_max_word(plan, d_workspace);
+        cudaError_t e = launch_prep_umma(plan->geo, d_image, ws + plan->off_x, mx, st);
         if (e != cudaSuccess) return e;
-        return launch_edge_dog(plan->geo, edge, dog_t, plan->umma_table, st);
+        return launch_row_pass_umma(plan->geo, ws + plan->off_x, ws + plan->off_rows_t, plan->table,
+                                    plan->toeplitz, plan->d_toeplitz, st, mx);
     }
-    return launch_col_dog_pass(plan->geo, rows_t, dog_t, edge, plan->table, plan->d_taps, st);
+    return launch_row_pass(plan->geo, d_image, reinterpret_cast<float *>(ws + plan->off_rows_t), plan->table,
+                           plan->d_taps, st, gate);
+}
+// pass 2 fused with the DoG: tensor engine -> slices in image orientation, FP32 engine -> transposed
+static cudaError_t col_dog_pass_any(const dogblob_plan *plan, void *d_workspace, cudaStream_t st) {
+    char *ws = reinterpret_cast<char *>(d_workspace);
+    float *dog = reinterpret_cast<float *>(ws + plan->off_dog_t);
+    if (plan->use_umma)
+        return launch_col_pass_umma(plan->geo, ws + plan->off_rows_t, dog, plan->umma_table, plan->toeplitz,
+                                    plan->d_toeplitz, st, frame_max_word(plan, d_workspace), false);
+    return launch_col_dog_pass(plan->geo, reinterpret_cast<const float *>(ws + plan->off_rows_t), dog,
+                               reinterpret_cast<float *>(ws + plan->off_edge), plan->table, plan->d_taps, st);
+}
+// dense [planes][H][W] copy of the engine's plane stack (tensor engine: pitched rows; FP32: transposed)
+static cudaError_t planes_to_dense(const dogblob_plan *plan, const float *d_planes, int planes, float *d_dst,
+                                   cudaStream_t st) {
+    const ConvGeometry &g = plan->geo;
+    if (!plan->use_umma) return launch_untranspose(d_planes, planes, g.Hp, g.Wp, g.H, g.W, d_dst, st);
+    for (int i = 0; i < planes; ++i) {
+        cudaError_t e = cudaMemcpy2DAsync(d_dst + (size_t)i * g.H * g.W, (size_t)g.W * sizeof(float),
+                                          d_planes + (size_t)i * g.Hp * g.Wp, (size_t)g.Wp * sizeof(float),
+                                          (size_t)g.W * sizeof(float), g.H, cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 // reset + row pass (optionally gated on a streamed upload), then the rest of the frame
 static int launch_frame_head(const dogblob_plan *plan, const float *d_image, void *d_workspace,
                              cudaStream_t st, void *const *events, const RowGate *gate) {
     char *ws = reinterpret_cast<char *>(d_workspace);
-    float *rows_t = reinterpret_cast<float *>(ws + plan->off_rows_t);
     BlobSpace bs = carve_blobspace(ws + plan->off_blobspace, plan->max_blobs);
     if (events) DB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(events[0]), st));
     DB_CUDA(launch_reset_counters(bs, st));
-    DB_CUDA(row_pass_any(plan, d_image, rows_t, st, gate));
+    DB_CUDA(row_pass_any(plan, d_image, d_workspace, st, gate));
     if (events) DB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(events[1]), st));
     return DOGBLOB_OK;
 }
@@ -415,19 +414,21 @@ static int launch_frame_tail(const dogblob_plan *plan, float threshold, int neig
                              double overlap, int prune, void *d_workspace, void *d_result,
                              cudaStream_t st, void *const *events) {
     char *ws = reinterpret_cast<char *>(d_workspace);
-    float *rows_t = reinterpret_cast<float *>(ws + plan->off_rows_t);
-    float *dog_t = reinterpret_cast<float *>(ws + plan->off_dog_t);
+    float *dog = reinterpret_cast<float *>(ws + plan->off_dog_t);
     BlobSpace bs = carve_blobspace(ws + plan->off_blobspace, plan->max_blobs);
     const ConvGeometry &g = plan->geo;
     auto ev = [&](int k) -> cudaError_t {
         return events ? cudaEventRecord(reinterpret_cast<cudaEvent_t>(events[k]), st)
                       : cudaSuccess;
     };
-    DB_CUDA(col_dog_pass_any(plan, rows_t, dog_t, reinterpret_cast<float *>(ws + plan->off_edge), st));
+    DB_CUDA(col_dog_pass_any(plan, d_workspace, st));
     DB_CUDA(ev(2));
-    // D^T planes: rows = x (W valid), cols = y (H valid)
-    DB_CUDA(launch_extrema(dog_t, g.L - 1, g.W, g.H, g.Hp, (int64_t)g.Hp * g.Wp, true,
-                           plan->d_slice_sigma, threshold, neighborhood / 2, bs, st));
+    if (plan->use_umma)     // D planes in image orientation: rows = y, cols = x
+        DB_CUDA(launch_extrema(dog, g.L - 1, g.H, g.W, g.Wp, (int64_t)g.Hp * g.Wp, false,
+                               plan->d_slice_sigma, threshold, neighborhood / 2, bs, st));
+    else                    // D^T planes: rows = x (W valid), cols = y (H valid)
+        DB_CUDA(launch_extrema(dog, g.L - 1, g.W, g.H, g.Hp, (int64_t)g.Hp * g.Wp, true,
+                               plan->d_slice_sigma, threshold, neighborhood / 2, bs, st));
     DB_CUDA(ev(3));
     DB_CUDA(launch_prune_and_pack(bs, overlap, prune != 0, d_result, plan->max_blobs, st));
     DB_CUDA(ev(4));
@@ -486,7 +487,7 @@ int dogblob_detect_host_streamed(const dogblob_plan *plan, const float *h_image,
     DB_REQUIRE(copy_stream && h_gate && frame_done && copy_stream != stream,
                "streamed upload needs its own copy stream, a pinned gate array and an event");
     if (int rc = check_threshold_args(neighborhood, overlap)) return rc;
-    if (use_umma(plan) && umma_needs_frame_max())     // the fp16 split needs the whole frame's max first
+    if (plan->use_umma)     // the fp16 operand split needs the whole frame's max first
         return dogblob_detect_host(plan, h_image, threshold, neighborhood, overlap, prune, d_image,
                                    d_workspace, d_result, h_result, h_result_blobs, stream, events);
     DeviceGuard guard(plan->device);
@@ -572,16 +573,16 @@ int dogblob_scale_space(const dogblob_plan *plan, const float *d_image, void *d_
     DB_REQUIRE(guard.ok, "cannot select CUDA device");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     char *ws = reinterpret_cast<char *>(d_workspace);
-    float *rows_t = reinterpret_cast<float *>(ws + plan->off_rows_t);
-    float *lev_t = reinterpret_cast<float *>(ws + plan->off_dog_t);
+    float *lev = reinterpret_cast<float *>(ws + plan->off_dog_t);
     const ConvGeometry &g = plan->geo;
-    DB_CUDA(row_pass_any(plan, d_image, rows_t, st, nullptr));
-    if (use_umma(plan))
-        DB_CUDA(launch_col_levels_pass_umma(g, rows_t, lev_t, plan->unit_table, plan->toeplitz,
-                                            plan->d_toeplitz, st, frame_max_word(plan, rows_t)));
+    DB_CUDA(row_pass_any(plan, d_image, d_workspace, st, nullptr));
+    if (plan->use_umma)
+        DB_CUDA(launch_col_pass_umma(g, ws + plan->off_rows_t, lev, plan->unit_table, plan->toeplitz,
+                                     plan->d_toeplitz, st, frame_max_word(plan, d_workspace), true));
     else
-        DB_CUDA(launch_col_levels_pass(g, rows_t, lev_t, plan->unit_table, plan->d_taps, st));
-    DB_CUDA(launch_untranspose(lev_t, g.L, g.Hp, g.Wp, g.H, g.W, d_levels, st));
+        DB_CUDA(launch_col_levels_pass(g, reinterpret_cast<const float *>(ws + plan->off_rows_t), lev,
+                                       plan->unit_table, plan->d_taps, st));
+    DB_CUDA(planes_to_dense(plan, lev, g.L, d_levels, st));
     return DOGBLOB_OK;
 }
 
@@ -592,12 +593,10 @@ int dogblob_dog(const dogblob_plan *plan, const float *d_image, void *d_workspac
     DB_REQUIRE(guard.ok, "cannot select CUDA device");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     char *ws = reinterpret_cast<char *>(d_workspace);
-    float *rows_t = reinterpret_cast<float *>(ws + plan->off_rows_t);
-    float *dog_t = reinterpret_cast<float *>(ws + plan->off_dog_t);
-    const ConvGeometry &g = plan->geo;
-    DB_CUDA(row_pass_any(plan, d_image, rows_t, st, nullptr));
-    DB_CUDA(col_dog_pass_any(plan, rows_t, dog_t, reinterpret_cast<float *>(ws + plan->off_edge), st));
-    DB_CUDA(launch_untranspose(dog_t, g.L - 1, g.Hp, g.Wp, g.H, g.W, d_slices, st));
+    float *dog = reinterpret_cast<float *>(ws + plan->off_dog_t);
+    DB_CUDA(row_pass_any(plan, d_image, d_workspace, st, nullptr));
+    DB_CUDA(col_dog_pass_any(plan, d_workspace, st));
+    DB_CUDA(planes_to_dense(plan, dog, plan->geo.L - 1, d_slices, st));
     return DOGBLOB_OK;
 }
 

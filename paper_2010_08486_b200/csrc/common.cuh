@@ -151,31 +151,31 @@ cudaError_t launch_col_levels_pass(const ConvGeometry &g, const float *d_rows_t,
                                    cudaStream_t st);
 cudaError_t launch_edge_dog(const ConvGeometry &g, const float *d_edge, float *d_dog_t,
                             const LevelTable &tbl, cudaStream_t st);
-// tensor-core (tcgen05) versions of the three passes, scale_space_umma.cu
-struct ToeplitzTable {               // per level: float offset, rows, log2 of the tap scale (fp16 mode)
+// tensor-core (tcgen05) versions of the passes, scale_space_umma.cu
+struct ToeplitzTable {               // per level: float offset, rows, log2 of the tap scale
     int ofs[kMaxLevels];
     int rows[kMaxLevels];
     int tscale[kMaxLevels];
 };
+// Buffers of the tensor-core engine (all fp16, frame-scaled units):
+//   X planes [hi | lo][H + 2 Py][Wp]      the frame with its reflected halo rows
+//   R planes [hi | lo][L][Hp][Wq]         pass-1 output rows, interior at column Ppad, reflected
+//                                         halo columns on both sides (Wq = Wp + 2 Ppad)
+struct UmmaLayout { int Py, Ppad, Wq; size_t x_bytes, r_bytes; };
+UmmaLayout umma_layout(const ConvGeometry &g);
 bool umma_supported(const ConvGeometry &g);
 void build_toeplitz(const LevelDesc *lv, int n_levels, const float2 *taps, std::vector<float> &out,
                     ToeplitzTable &tab);
 cudaError_t configure_umma_kernels(int device);
-bool umma_needs_frame_max();
-cudaError_t launch_frame_max(const float *d_img, int64_t n_floats, uint32_t *d_max_bits, cudaStream_t st);
-cudaError_t launch_row_pass_umma(const ConvGeometry &g, const float *d_img, float *d_rows_t,
-                                 const LevelTable &tbl, const ToeplitzTable &ttab,
-                                 const float *d_toep, cudaStream_t st, const RowGate *gate = nullptr,
-                                 const uint32_t *d_max_bits = nullptr, const int *d_sched = nullptr);
-std::vector<int> build_umma_schedule(const ConvGeometry &g, const LevelTable &tbl, bool rows_pass);
-cudaError_t launch_col_dog_pass_umma(const ConvGeometry &g, const float *d_rows_t, float *d_dog_t,
-                                     float *d_edge, const LevelTable &tbl, const ToeplitzTable &ttab,
-                                     const float *d_toep, cudaStream_t st,
-                                     const uint32_t *d_max_bits = nullptr, const int *d_sched = nullptr);
-cudaError_t launch_col_levels_pass_umma(const ConvGeometry &g, const float *d_rows_t, float *d_lev_t,
-                                        const LevelTable &unit_tbl, const ToeplitzTable &ttab,
-                                        const float *d_toep, cudaStream_t st,
-                                        const uint32_t *d_max_bits = nullptr);
+cudaError_t launch_prep_umma(const ConvGeometry &g, const float *d_img, void *d_x, uint32_t *d_max_bits,
+                             cudaStream_t st);
+cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d_r, const LevelTable &tbl,
+                                 const ToeplitzTable &ttab, const float *d_toep, cudaStream_t st,
+                                 const uint32_t *d_max_bits);
+// DoG slices [L - 1][Hp][Wp] in image orientation (levels = true: the L levels themselves)
+cudaError_t launch_col_pass_umma(const ConvGeometry &g, const void *d_r, float *d_out, const LevelTable &tbl,
+                                 const ToeplitzTable &ttab, const float *d_toep, cudaStream_t st,
+                                 const uint32_t *d_max_bits, bool levels);
 cudaError_t launch_untranspose(const float *d_src_t, int planes, int Hp, int Wp, int H, int W,
                                float *d_dst, cudaStream_t st);
 cudaError_t launch_dog_from_levels(int L, int64_t plane_elems, const float *d_levels,

@@ -1,47 +1,53 @@
 // Separable Gaussian scale space + fused DoG on the 5th-generation tensor cores (tcgen05, sm_100a).
 //
-// Same two passes, same buffers and the same results (within float32 rounding) as
-// scale_space.cu (reference: convolve.py:63-218, detector.py:117-126), but the banded
-// correlation along the strided axis is issued as a Toeplitz GEMM:
+// Same results (within float32 rounding) as scale_space.cu (reference: convolve.py:63-218,
+// detector.py:117-126), but each banded 1-D correlation is issued as a Toeplitz GEMM with BOTH
+// operands in shared memory, brought there by TMA, and nothing is transposed anywhere:
 //
-//     D[m][n] = sum_k  X[k][m] * T[k][n],      T[k][n] = w[k - n]  (0 <= k - n <= 2 rpad)
+//   pass 1 (along y, the strided axis)      D1[y_out][x] = sum_k  T[y_out][k] * X[k][x]
+//       A = Toeplitz window (K-major, no swizzle)     B = image rows, MN-major, SWIZZLE_128B
+//   pass 2 (along x, the contiguous axis)   D2[y][x_out] = sum_k  R[y][k] * T[x_out][k]
+//       A = pass-1 rows, K-major, SWIZZLE_128B        B = Toeplitz window (K-major, no swizzle)
 //
-//   m : 128 positions along the CONTIGUOUS axis of the input plane (one TMEM lane each)
-//   n : 128 outputs along the convolved (strided) axis
-//   k : the 128 + 2 rpad input rows the 128 outputs read, 16 per tcgen05.mma (kind::f16)
+//   T[n][k] = w[k - n] (0 <= k - n <= 2 rpad), tiles of 128 x 128 outputs, K = 128 + 2 rpad inputs
+//   along the convolved axis, 16 per tcgen05.mma.kind::f16 (M = 128, N <= 128).
 //
-// float32 accuracy from fp16 tensor-core operands: both operands are split x = hi + lo with
-// hi = fp16(x), lo = fp16(x - hi) (11 + 11 significand bits; exact power-of-two scales keep them in
-// fp16's range, see DOGBLOB_UMMA_F16 below) and every step issues the three products hi*hi, hi*lo
-// and lo*hi (the lo*lo term is below 2^-22).  The tensor core truncates its float32 accumulator
-// after every MMA, so each issuing warp owns one accumulator (half the chain) and the drain adds
-// them in float32.  Build option: tf32 operands (K = 8, no scales).
+// float32 accuracy from fp16 operands: data and taps are split x = hi + lo, hi = fp16(x),
+// lo = fp16(x - hi) (11 + 11 significand bits; exact power-of-two scales keep both in range: the
+// frame by 2^e with max|x| 2^e in [2^12, 2^13), every level's taps by 2^t with the largest tap in
+// [512, 1024)) and every k-step issues hi*hi, hi*lo and lo*hi.  The tensor core truncates its
+// float32 accumulator after every MMA (-1/2 ulp of the running sum each), so the large products
+// (hi*hi) and the small ones (2^-11 of them) go to SEPARATE accumulators: the chain that carries the
+// magnitude is a third as long, the other one's truncation is negligible; the drain adds the two.
 //
-// Data flow of one CTA (persistent, one per SM, 544 threads):
-//   warps 2..3  "loaders"    32 input rows x 512 B per stage into shared memory: one TMA box
-//                            (interior) or 16-byte cp.async with folded rows (image border)
-//   warps 8..15 "converters" read the rows back with lane = m, split hi/lo, tcgen05.st into the A
-//                            staging columns of TMEM (A is an MMA operand from TMEM only)
-//   warp 1      "Toeplitz"   the level's Toeplitz operand, prebuilt on the host, one bulk copy per
-//                            level into shared memory (K-major, no swizzle).  T only depends on
-//                            k - n, so ONE array G[p][kk] = w[kk - p + Kp - 8] serves every k-step:
-//                            step m0 reads the 128-row window that starts at row Kp - 8 - m0 (the
-//                            descriptor's start address slides).  Double buffered across levels.
-//   warps 0, 16 "issuers"    stages alternate between the two warps; one elected lane issues
-//                            3 tcgen05.mma per k-step, tcgen05.commit releases the A stage / the
-//                            Toeplitz buffer / publishes the accumulator halves
-//   warps 4..7  "drain"      tcgen05.ld of a finished accumulator half (lane = m, so a warp's store
-//                            of one n is 128 contiguous bytes), sum of the three accumulators, DoG
-//                            against the previous level kept in thread-private shared-memory
-//                            slots, global stores; hands the half back zeroed
-// TMEM columns: [0,384) three 128 x 128 float32 accumulators, [384,512) two A stages.
+// The operands are pre-split in memory: the frame once (prep_split_kernel: fp16 hi | lo planes with
+// the reflected halo rows materialised), the pass-1 output by pass 1's drain (hi | lo planes with
+// the reflected halo columns written next to the interior) - the same 4 bytes per element as a
+// float32 plane, and every stage of both passes is one TMA box straight into MMA operand layout.
+//
+// One persistent CTA per SM, 384 threads:
+//   warp 0      issuer     one elected lane: 3 MMAs per k-step, tcgen05.commit frees the data stage /
+//                          the Toeplitz buffer / publishes the accumulator pair
+//   warp 1      loader     one TMA box per stage (pass 1: 32 input rows x 128 x, hi | lo = 16 KB;
+//                          pass 2: 128 rows x 64 k, hi | lo = 32 KB)
+//   warp 2      Toeplitz   the level's prebuilt Toeplitz array (hi | lo), one bulk copy per level,
+//                          double buffered.  T only depends on k - n, so ONE array
+//                          G[p][kk] = w[kk - p + Kp - 16] serves every k-step: step m0 reads the
+//                          128-row window that starts at row Kp - 16 - m0 (the descriptor slides).
+//   warps 4..11 drain      tcgen05.ld of the accumulator pair (lane = output row, 64 columns per
+//                          thread), scales, pass 1: hi/lo split -> swizzled staging -> TMA store
+//                          (+ mirrored halo columns); pass 2: DoG against the previous level kept in
+//                          REGISTERS, staging -> TMA store of the float32 slice
+// TMEM: two buffers of {main, small} 128 x 128 float32 accumulators (512 columns), so the drain of
+// one level overlaps the MMAs of the next.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
 
-#include <cuda.h>
-#include <cuda_fp16.h>      // CUtensorMap (types only: the encoder is fetched through the runtime)
+#include <cuda.h>           // CUtensorMap (types only: the encoder is fetched through the runtime)
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 
@@ -49,76 +55,34 @@ namespace dogblob {
 
 namespace {
 
-constexpr int kUT = 128;              // tile edge on both axes
-// DOGBLOB_UMMA_F16 = 1 (default): fp16 hi/lo operands (kind::f16, K = 16 rows per MMA: half as many
-// MMAs as the tf32 split, 11 + 11 significand bits all the same).  fp16's range is covered by exact
-// power-of-two scales: the frame by 2^e (max |x| * 2^e in [2^12, 2^13), e from frame_max_kernel in
-// front of the row pass), every level's taps by 2^t (largest tap in [512, 1024)); the drain undoes
-// both.  Values far below the frame's maximum lose relative, not absolute, precision.
-// DOGBLOB_UMMA_F16 = 0: tf32 hi/lo operands (K = 8), no frame scale, so the row pass can start
-// under a streamed upload; 10 % slower.
-#ifndef DOGBLOB_UMMA_F16
-#define DOGBLOB_UMMA_F16 1
-#endif
-#ifndef DOGBLOB_UMMA_ISSUERS
-#define DOGBLOB_UMMA_ISSUERS 2       // fp16: 0.181 + 0.184 ms at C2 (one issuer: 0.189 + 0.188)
-#endif
-// accumulators: one per issuing warp; a single issuer alternates between two (even / odd steps)
-#define DOGBLOB_UMMA_ACCS (DOGBLOB_UMMA_ISSUERS > 1 ? DOGBLOB_UMMA_ISSUERS : 2)
-constexpr int kIssuers = DOGBLOB_UMMA_ISSUERS;      // issuing warps: warp 0 and warps 16 ..
-#ifndef DOGBLOB_UMMA_DRAIN_GROUPS
-#define DOGBLOB_UMMA_DRAIN_GROUPS 1      // 2: column pass -3 %, row pass +6 % (672 threads cap the registers at 80)
-#endif
-constexpr int kDrainGroups = DOGBLOB_UMMA_DRAIN_GROUPS;   // 4 warps each; group 0 = warps 4..7, group 1 = the last 4 warps
-constexpr int kDrainB = 16 + kIssuers - 1;                 // first warp of the second drain group
-constexpr int kUThreads = 32 * (kDrainB + 4 * (kDrainGroups - 1));
-constexpr int kIssuerB = 16;          // warp index of the second issuer
-#ifndef DOGBLOB_UMMA_STAGEK
-#define DOGBLOB_UMMA_STAGEK 4
-#endif
-constexpr int kStageK = DOGBLOB_UMMA_STAGEK;          // k-steps (8 input rows each) per stage
-constexpr int kAccs = DOGBLOB_UMMA_ACCS;
-constexpr int kStages = (512 - 128 * DOGBLOB_UMMA_ACCS) / (16 * kStageK);   // A staging stages (the TMEM columns the accumulators leave)
-constexpr int kStageRows = 8 * kStageK;   // input rows per stage
-constexpr int kStageCols = 16 * kStageK;  // TMEM columns per stage: (hi 8 + lo 8) per k-step
+constexpr int kUT = 128;                  // tile edge on both axes
+constexpr int kThreads = 384;             // 12 warps
+constexpr int kDrainWarp0 = 4;            // warps 4..11 drain
+constexpr int kDrainWarps = 8;
 constexpr int kAccCols = 128;
-// TMEM columns: one 128 x 128 float32 accumulator per issuing warp, then the A staging
-constexpr int kStageCol0 = kAccs * kAccCols;
-constexpr int kHalf = kUT / 2;        // accumulators are handed to the drain in two column halves
-constexpr int kLoaderGroups = 2;      // groups of 4 warps; group g fills stages with index % 2 == g
-constexpr int kMaxRawStages = 8;      // raw input-row stages in shared memory (16 KB each)
+constexpr int kStageBytes1 = 16384;       // pass 1: [hi | lo][2 x-blocks][32 rows][128 B]
+constexpr int kStageBytes2 = 32768;       // pass 2: [hi | lo][128 rows][128 B]
+constexpr int kStagingBytes = 32768;      // drain staging: one 16 KB box per column half
+constexpr int kMaxStages = 8;
 constexpr unsigned long long kWaitLimitNs = 20ull * 1000 * 1000 * 1000;   // deadlock trap (20 s)
 
 enum UmmaMode { kModeRows = 0, kModeDog = 1, kModeLevels = 2 };
 
 struct UmmaArgs {
-    const float *in;        // rows: the image; columns: the row-filtered planes
-    int64_t in_pitch;       // elements between rows of `in`
-    int64_t in_plane;       // elements between level planes of `in` (0: every level reads plane 0)
-    int n_rows;             // valid rows of `in` along the convolved axis (reflect period)
-    float *out;
-    int64_t out_pitch, out_plane;
-    float *edge;            // DoG mode: parked boundary levels
-    const uint32_t *frame_max_bits;   // F16 mode: float bits of the frame's max |x| (device word)
+    int tiles_x, tiles_y;   // tiles along x (contiguous) and y
+    int n_units;            // tiles * (levels | level groups)
+    int by_order;           // units are single levels in tbl.order[] (pass 1) or groups (pass 2)
+    int H, W, Hp, Wp;
+    int Py;                 // halo rows above / below the frame in the X planes
+    int Ppad;               // halo columns left / right of the interior in the R planes
+    int64_t r_pitch;        // elements per row of the R planes (Wq)
+    int64_t r_plane;        // elements between the hi and the lo plane set (L * Hp * Wq)
+    __half *r_base;         // pass 1: R planes, for the mirrored halo columns
+    const uint32_t *frame_max_bits;   // float bits of the frame's max |x| (device word)
     const float *toep;      // prebuilt Toeplitz arrays of every level (hi | lo), see build_toeplitz
-    int raw_stages;         // raw input-row stages that fit in shared memory
-    int by_order;           // units are single levels in tbl.order[] (longest first): row pass
-    int n_order;            // by_order: number of levels
-    // streamed upload (row pass only, see RowGate in common.cuh): the frame arrives in row chunks
-    // while the kernel runs; *gate_word - gate_base = chunks resident.  Tile rows are then the
-    // slowest unit index, so early units only need early chunks.
-    const int *gate_word;
-    int gate_base, gate_rows_per_chunk;
-    unsigned long long *gate_t_start;
-    int use_tma;            // interior stages arrive as one TMA box (tensor map valid)
-    int tma_plane_rows;     // rows between level planes in the tensor map (0: one plane)
-    int tiles_c, tiles_r;   // tiles along the contiguous / the convolved axis
-    int n_units;            // tiles_c * tiles_r * n_groups
-    const int *sched;       // optional: position i of a CTA's round-robin walk -> unit (cost-balanced order)
-    int toep_floats;        // floats of one Toeplitz array (hi or lo) of the widest level
+    int toep_bytes;         // bytes of one Toeplitz buffer in shared memory (widest level, hi + lo)
+    int stages;             // data stages that fit in shared memory
     unsigned long long *prof;   // DOGBLOB_UMMA_PROF: per-role cycle counters (see launch_umma)
-    int debug;              // DOGBLOB_UMMA_DEBUG: 1 loaders skip global loads, 2 builders build once,
-                            // 4 drain skips stores, 8 issuer skips the MMAs (timing experiments only)
 };
 
 // ---- PTX wrappers -------------------------------------------------------------------
@@ -155,17 +119,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int tag
     while (!mbar_try_wait(bar, parity))
         if ((++spins & 0xfffu) == 0 && globaltimer_ns() - t0 > kWaitLimitNs) mbar_timeout(tag, parity);
 }
-// long waits (drain, copiers): back off so that the spinning warp leaves its issue slots to
-// the converters that share the SM sub-partition
-__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, int tag) {
-    if (mbar_try_wait(bar, parity)) return;
-    const unsigned long long t0 = globaltimer_ns();
-    uint32_t spins = 0;
-    while (!mbar_try_wait(bar, parity)) {
-        __nanosleep(64);
-        if ((++spins & 0xfffu) == 0 && globaltimer_ns() - t0 > kWaitLimitNs) mbar_timeout(tag, parity);
-    }
-}
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");
@@ -178,29 +131,33 @@ __device__ __forceinline__ void bulk_copy_g2s(uint32_t dst_smem, const void *src
         ::"r"(dst_smem), "l"(src), "r"(bytes), "r"(bar)
         : "memory");
 }
-__device__ __forceinline__ void mbar_expect_tx_only(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes)
-                 : "memory");
-}
-// one TMA box (tensor map: rows of the input planes, 128 floats x 16 rows, no swizzle)
-__device__ __forceinline__ void tma_load_2d(uint32_t dst_smem, const CUtensorMap *map, int col, int row,
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2,
                                             uint32_t bar) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-        ::"r"(dst_smem), "l"(map), "r"(col), "r"(row), "r"(bar)
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
         : "memory");
 }
-__device__ __forceinline__ void cp_async16(uint32_t dst_smem, const void *src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_smem), "l"(src) : "memory");
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                            int c3, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+        ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+        : "memory");
 }
-// the barrier gets one (pre-counted) arrival once all earlier cp.async of this thread landed
-__device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, int c0, int c1, uint32_t src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                 ::"l"(map), "r"(c0), "r"(c1), "r"(src) : "memory");
 }
-__device__ __forceinline__ uint64_t make_desc(uint32_t lo, uint32_t hi) {
-    uint64_t d;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "r"(lo), "r"(hi));
-    return d;
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, int c0, int c1, int c2, uint32_t src) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
+                 ::"l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(src) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 __device__ __forceinline__ void fence_barrier_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -223,78 +180,29 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols)
                  : "memory");
 }
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                 : "memory");
-}
-// D[tmem] (+)= A[tmem] * B[smem descriptor], kind::tf32, M = 128
-__device__ __forceinline__ void umma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
-                                             uint32_t idesc, uint32_t accumulate) {
+// The three MMAs of one k-step in ONE statement (the whole warp executes it, one elected lane
+// issues; the operands reach the uniform registers once):
+//     main  (+)= A_hi * B_hi        small (+)= A_hi * B_lo        small += A_lo * B_hi
+// `acc` = 0 on the first k-step of a level: the first two MMAs overwrite their accumulators.
+__device__ __forceinline__ void umma_f16_triple_ss(uint32_t d_main, uint32_t d_small, uint32_t a_hi,
+                                                   uint32_t a_lo, uint32_t b_hi, uint32_t b_lo,
+                                                   uint32_t a_upper, uint32_t b_upper, uint32_t idesc,
+                                                   uint32_t acc) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
-        ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-// Warp-uniform variants: the whole warp executes them, one elected lane issues.  Keeping the
-// issuer's control flow and operands warp uniform lets ptxas hold descriptors in uniform
-// registers instead of wrapping every tcgen05.mma in a per-lane (ELECT / R2UR) loop.
-__device__ __forceinline__ void umma_tf32_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
-                                                   uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
+        "{\n\t.reg .pred p, q, e;\n\t.reg .b64 a0, a1, b0, b1;\n\t"
+        "setp.ne.b32 p, %9, 0;\n\t"
+        "setp.eq.b32 q, 0, 0;\n\t"
         "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
-        ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        "mov.b64 a0, {%2, %6};\n\t"
+        "mov.b64 a1, {%3, %6};\n\t"
+        "mov.b64 b0, {%4, %7};\n\t"
+        "mov.b64 b1, {%5, %7};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a0, b0, %8, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%1], a0, b1, %8, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%1], a1, b0, %8, q;\n\t}"
+        ::"r"(d_main), "r"(d_small), "r"(a_hi), "r"(a_lo), "r"(b_hi), "r"(b_lo), "r"(a_upper),
+          "r"(b_upper), "r"(idesc), "r"(acc)
         : "memory");
-}
-// The three MMAs of one k-step (hi*lo, lo*hi, hi*hi into one accumulator) in ONE statement: the
-// operands are moved to uniform registers once per k-step instead of once per MMA.
-__device__ __forceinline__ void umma_tf32_triple_elect(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo,
-                                                       uint32_t desc_b_lo, uint32_t desc_b_hi,
-                                                       uint32_t desc_upper, uint32_t idesc) {
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\t.reg .b64 dl, dh;\n\t"
-        "setp.eq.b32 p, 0, 0;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "mov.b64 dl, {%3, %5};\n\t"
-        "mov.b64 dh, {%4, %5};\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], dl, %6, p;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], dh, %6, p;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], dh, %6, p;\n\t}"
-        ::"r"(d_tmem), "r"(a_hi), "r"(a_lo), "r"(desc_b_lo), "r"(desc_b_hi), "r"(desc_upper), "r"(idesc)
-        : "memory");
-}
-__device__ __forceinline__ void umma_f16_triple_elect(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo,
-                                                      uint32_t desc_b_lo, uint32_t desc_b_hi,
-                                                      uint32_t desc_upper, uint32_t idesc) {
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\t.reg .b64 dl, dh;\n\t"
-        "setp.eq.b32 p, 0, 0;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "mov.b64 dl, {%3, %5};\n\t"
-        "mov.b64 dh, {%4, %5};\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], dl, %6, p;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], dh, %6, p;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], dh, %6, p;\n\t}"
-        ::"r"(d_tmem), "r"(a_hi), "r"(a_lo), "r"(desc_b_lo), "r"(desc_b_hi), "r"(desc_upper), "r"(idesc)
-        : "memory");
-}
-// F16 mode: exponent e with max|x| * 2^e in [2^12, 2^13) (0 for an all-zero, NaN or Inf frame)
-__device__ __forceinline__ int frame_scale_exp(const uint32_t *max_bits) {
-    const uint32_t b = __ldcg(max_bits);
-    const int ex = (int)((b >> 23) & 0xffu);
-    if (ex == 0 || ex == 255) return 0;
-    return max(-100, min(100, 12 - (ex - 127)));       // the scale itself must stay a normal float
-}
-__device__ __forceinline__ float pow2f(int e) { return __int_as_float((uint32_t)(127 + e) << 23); }
-// two floats -> packed f16x2 (first argument in the LOW half: K element 2c, second in the high half)
-__device__ __forceinline__ uint32_t pack_f16x2(float lo_elem, float hi_elem) {
-    uint32_t d;
-    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi_elem), "f"(lo_elem));
-    return d;
 }
 __device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
     asm volatile(
@@ -303,81 +211,77 @@ __device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
         "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
         ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ uint32_t tf32_rna(float x) {
-    uint32_t u;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
-    return u;
+// exponent e with max|x| * 2^e in [2^12, 2^13) (0 for an all-zero, NaN or Inf frame)
+__device__ __forceinline__ int frame_scale_exp(const uint32_t *max_bits) {
+    const uint32_t b = __ldcg(max_bits);
+    const int ex = (int)((b >> 23) & 0xffu);
+    if (ex == 0 || ex == 255) return 0;
+    return max(-100, min(100, 12 - (ex - 127)));       // the scale itself must stay a normal float
 }
-__device__ __forceinline__ void split_tf32(float x, uint32_t &hi, uint32_t &lo) {
-    hi = tf32_rna(x);
-    lo = tf32_rna(__fsub_rn(x, __uint_as_float(hi)));
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((uint32_t)(127 + e) << 23); }
+// two floats -> packed f16x2 (first argument in the LOW half)
+__device__ __forceinline__ uint32_t pack_f16x2(float lo_elem, float hi_elem) {
+    uint32_t d;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi_elem), "f"(lo_elem));
+    return d;
 }
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-        "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};"
-        ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
-          "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]),
-          "r"(r[14]), "r"(r[15])
-        : "memory");
+// x0, x1 -> packed fp16 hi parts and packed fp16 residuals
+__device__ __forceinline__ void split_pair(float x0, float x1, uint32_t &hi, uint32_t &lo) {
+    hi = pack_f16x2(x0, x1);
+    const float2 hf = __half22float2(*reinterpret_cast<const __half2 *>(&hi));
+    lo = pack_f16x2(__fsub_rn(x0, hf.x), __fsub_rn(x1, hf.y));
 }
-__device__ __forceinline__ void tmem_wait_st() {
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+// tcgen05.ld is asynchronous: its destination registers are only valid after tcgen05.wait::ld.
+// Load and wait are one statement, so the compiler cannot place any use in between.
+__device__ __forceinline__ void tmem_ld32_pair(uint32_t taddr_a, uint32_t taddr_b, uint32_t (&r)[32],
+                                               uint32_t (&s)[32]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
         "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
-        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%64];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, "
+        "%48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63}, [%65];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
           "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
           "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
           "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
-          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr)
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]),
+          "=r"(s[0]), "=r"(s[1]), "=r"(s[2]), "=r"(s[3]), "=r"(s[4]), "=r"(s[5]), "=r"(s[6]),
+          "=r"(s[7]), "=r"(s[8]), "=r"(s[9]), "=r"(s[10]), "=r"(s[11]), "=r"(s[12]), "=r"(s[13]),
+          "=r"(s[14]), "=r"(s[15]), "=r"(s[16]), "=r"(s[17]), "=r"(s[18]), "=r"(s[19]),
+          "=r"(s[20]), "=r"(s[21]), "=r"(s[22]), "=r"(s[23]), "=r"(s[24]), "=r"(s[25]),
+          "=r"(s[26]), "=r"(s[27]), "=r"(s[28]), "=r"(s[29]), "=r"(s[30]), "=r"(s[31])
+        : "r"(taddr_a), "r"(taddr_b)
         : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr)
-        : "memory");
-}
-// tcgen05.ld is asynchronous: its destination registers are only valid after tcgen05.wait::ld.
-// The wait therefore names them as read-write operands, so the compiler cannot place any use (or
-// any register-to-register copy) of them between the load and the wait.
-__device__ __forceinline__ void tmem_wait_ld16(uint32_t (&r)[16]) {
-    asm volatile("tcgen05.wait::ld.sync.aligned;"
-                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
-                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
-                   "+r"(r[15])
-                 :: "memory");
-}
-__device__ __forceinline__ void tmem_wait_ld() {
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
 }
 
-// Shared-memory matrix descriptor (cute::UMMA::SmemDescriptor): K-major, no swizzle.
-//   bits [0,14)  start address >> 4        bits [16,30) leading byte offset >> 4 (between the
-//   bits [32,46) stride byte offset >> 4                two 16-byte K halves of a k-step)
-//   bits [46,48) version = 1 (Blackwell)   bits [61,64) layout type = 0 (SWIZZLE_NONE)
-// Toeplitz array: 8-row group g at g * 256 bytes: [K half 0: 8 rows x 16 B][K half 1: 8 rows x 16 B]
-constexpr uint32_t kToepGroupBytes = 256, kToepHalfBytes = 128;
-// Instruction descriptor (cute::UMMA::InstrDescriptor): D = F32, A = B = TF32, both K-major,
-// dense, N at bits [17,23) as N >> 3, M at bits [24,29) as M >> 4.
-// kind::f16 with F16 operands: format fields 0, D = F32
-__host__ __device__ constexpr uint32_t instr_desc_f16(int M, int N) {
-    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-__host__ __device__ constexpr uint32_t instr_desc(int M, int N) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// Shared-memory matrix descriptors (cute::UMMA::SmemDescriptor):
+//   bits [0,14) start address >> 4    [16,30) leading byte offset >> 4    [32,46) stride byte
+//   offset >> 4    [46,48) version = 1    [61,64) layout type (0 none, 2 SWIZZLE_128B)
+// Toeplitz array (K-major, no swizzle): 8-row group g at g * 256 bytes =
+//   [K half 0: 8 rows x 16 B][K half 1: 8 rows x 16 B]  -> LBO = 128 (K halves), SBO = 256 (row groups)
+constexpr uint32_t kToepLowLbo = (128u >> 4) << 16;
+constexpr uint32_t kToepUpper = (256u >> 4) | (1u << 14);
+// pass-1 data (MN-major, SWIZZLE_128B): x-block of 64 at LBO = 4096 (32 rows x 128 B), 8-row
+// k group at SBO = 1024
+constexpr uint32_t kData1LowLbo = (4096u >> 4) << 16;
+constexpr uint32_t kData1Upper = (1024u >> 4) | (1u << 14) | (2u << 29);
+// pass-2 data (K-major, SWIZZLE_128B): 8-row group at SBO = 1024, LBO unused
+constexpr uint32_t kData2LowLbo = 1u << 16;
+constexpr uint32_t kData2Upper = (1024u >> 4) | (1u << 14) | (2u << 29);
+// Instruction descriptor (cute::UMMA::InstrDescriptor), kind::f16: F16 operands (format 0),
+// D = F32 (bit 4), B MN-major (bit 16), N >> 3 at bits [17,23), M >> 4 at bits [24,29)
+__host__ __device__ constexpr uint32_t instr_desc_f16(int M, int N, int b_mn) {
+    return (1u << 4) | ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-__device__ __forceinline__ int fold_row_u(int i, int n) {
+__host__ __device__ __forceinline__ int fold_row_u(int i, int n) {
     if ((unsigned)i < (unsigned)n) return i;
     const int once = i < 0 ? -i - 1 : 2 * n - 1 - i;      // one reflection covers radius <= n
     if ((unsigned)once < (unsigned)n) return once;
@@ -403,37 +307,28 @@ struct RoleClock {
     }
 };
 
-struct Unit { int g, r0, c0; };
-__device__ __forceinline__ Unit decode_unit(int i, const UmmaArgs &a) {
-    const int u = a.sched ? __ldg(a.sched + i) : i;
-    Unit x;
-    x.c0 = (u % a.tiles_c) * kUT;
-    const int t = u / a.tiles_c;
-    if (a.gate_word) {                  // streamed: tile row slowest, levels (longest first) inside
-        x.g = t % a.n_order;
-        x.r0 = (t / a.n_order) * kUT;
+// unit -> (x0, y0, first level, end level).  Pass 1: single levels, longest first.  Pass 2 (DoG):
+// level groups that OVERLAP by one level (the first level of group g + 1 is computed by group g
+// too), so every DoG slice has both its levels inside one unit and nothing is parked in memory.
+struct Unit { int x0, y0, lb, le; };
+__device__ __forceinline__ Unit decode_unit(int u, const UmmaArgs &a, const LevelTable &tbl, int mode) {
+    Unit r;
+    r.x0 = (u % a.tiles_x) * kUT;
+    const int t = u / a.tiles_x;
+    r.y0 = (t % a.tiles_y) * kUT;
+    const int g = t / a.tiles_y;
+    if (a.by_order) {
+        r.lb = tbl.order[g];
+        r.le = r.lb + 1;
     } else {
-        x.r0 = (t % a.tiles_r) * kUT;
-        x.g = t / a.tiles_r;
+        r.lb = tbl.group_begin[g];
+        r.le = tbl.group_begin[g + 1] + ((mode == kModeDog && g + 1 < tbl.n_groups) ? 1 : 0);
     }
-    return x;
-}
-
-// this warp's 32 lanes x 64 columns of the three accumulators <- 0
-__device__ __forceinline__ void zero_acc_half(uint32_t lane_base, int half, int dgroup) {
-    const uint32_t z[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-    for (int c = dgroup; c < kHalf / 16; c += kDrainGroups) {
-        const uint32_t col = (uint32_t)(half * kHalf + c * 16);
-#pragma unroll
-        for (int i = 0; i < kAccs; ++i) tmem_st16(lane_base + i * kAccCols + col, z);
-    }
-    tmem_wait_st();
+    return r;
 }
 
 struct SharedCtl {
-    unsigned long long raw_full[kMaxRawStages], raw_empty[kMaxRawStages];
-    unsigned long long data_full[kStages], data_empty[kStages];
+    unsigned long long data_full[kMaxStages], data_empty[kMaxStages];
     unsigned long long toep_full[2], toep_empty[2];
     unsigned long long acc_full[2], acc_empty[2];
     uint32_t tmem_base;
@@ -442,32 +337,33 @@ struct SharedCtl {
 static_assert(sizeof(SharedCtl) <= 1024, "control block");
 
 template <int MODE>
-__global__ void __launch_bounds__(kUThreads, 1)
+__global__ void __launch_bounds__(kThreads, 1)
 umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
-                 const __grid_constant__ ToeplitzTable ttab, const __grid_constant__ CUtensorMap tmap) {
+                 const __grid_constant__ ToeplitzTable ttab, const __grid_constant__ CUtensorMap map_in,
+                 const __grid_constant__ CUtensorMap map_out) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     SharedCtl *ctl = reinterpret_cast<SharedCtl *>(smem_raw);
-    float *toep = reinterpret_cast<float *>(smem_raw + 1024);     // [buffer 2][hi | lo][toep_floats]
-    float *s_prev = toep + 4 * (size_t)a.toep_floats;              // DoG: [n 128][m 128]
-    float *raw = s_prev + (MODE == kModeDog ? kUT * kUT : 0);      // [raw stage][16 rows][128]
-    const int R = a.raw_stages;
+    unsigned char *toep = smem_raw + 1024;                               // [buffer 2][hi | lo]
+    unsigned char *staging = toep + 2 * (size_t)a.toep_bytes;            // [column half 2][16 KB box]
+    unsigned char *data = staging + kStagingBytes;                       // [stage][...]
+    constexpr bool kRows = MODE == kModeRows;
+    constexpr int kStageBytes = kRows ? kStageBytes1 : kStageBytes2;
+    constexpr int kStepsPerStage = kRows ? 2 : 4;                         // k-steps of 16 per data stage
+    const int S = a.stages;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < R; ++s) {
-            mbar_init(smem_u32(&ctl->raw_full[s]), 64);
-            mbar_init(smem_u32(&ctl->raw_empty[s]), 4);
-        }
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(smem_u32(&ctl->data_full[s]), 4);
+        if (smem_u32(smem_raw) & 1023u) __trap();                         // swizzled boxes need 1 KB alignment
+        for (int s = 0; s < S; ++s) {
+            mbar_init(smem_u32(&ctl->data_full[s]), 1);
             mbar_init(smem_u32(&ctl->data_empty[s]), 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(smem_u32(&ctl->toep_full[b]), 1);
-            mbar_init(smem_u32(&ctl->toep_empty[b]), kIssuers);
-            mbar_init(smem_u32(&ctl->acc_full[b]), kIssuers);
-            mbar_init(smem_u32(&ctl->acc_empty[b]), 4 * kDrainGroups);
+            mbar_init(smem_u32(&ctl->toep_empty[b]), 1);
+            mbar_init(smem_u32(&ctl->acc_full[b]), 1);
+            mbar_init(smem_u32(&ctl->acc_empty[b]), kDrainWarps);
         }
         fence_barrier_init();
     }
@@ -476,386 +372,281 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
     __syncthreads();
     tc_fence_after();
     // The CTA owns all 512 columns, so the allocation starts at TMEM address 0; using the literal
-    // keeps every TMEM address and descriptor of the issuer in uniform registers.
+    // keeps every TMEM address of the issuer in uniform registers.
     if (*reinterpret_cast<volatile uint32_t *>(&ctl->tmem_base) != 0u) __trap();
     constexpr uint32_t tmem = 0u;
 
-    // the accumulators start zeroed: the issuers only ever accumulate
-    const bool is_drain = (warp >= 4 && warp < 8) || (kDrainGroups > 1 && warp >= kDrainB);
-    const int dgroup = warp >= kDrainB ? 1 : 0;
-    if (is_drain) {
-        const uint32_t lane_base0 = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-        zero_acc_half(lane_base0, 0, dgroup);
-        zero_acc_half(lane_base0, 1, dgroup);
-        tc_fence_before();
-    }
-    __syncthreads();
-    tc_fence_after();
-
-    if (warp == 0 || (warp >= kIssuerB && warp < kDrainB)) {
-        // ================= issuers (whole warps, one elected lane issues) =================
-        // Band structure: k-step m0 only feeds outputs n in [m0 - 2 rpad, m0 + 7], so its MMAs are
-        // issued for that column range only (rounded to 16; the Toeplitz window and the
-        // accumulator address move with it).
-        // Accuracy: the tensor core truncates the float32 accumulator after every MMA, a bias of
-        // half an ulp of the running sum per MMA.  Every issuing warp owns one accumulator (half
-        // the chain length, about half the magnitude each); the drain adds them in float32.
-        // The accumulators are single buffered and handed over in two column halves: outputs
-        // n < 64 are complete after k-step (63 + 2 rpad) / 8 and the next level's first 8 k-steps
-        // only touch n < 64, so the drain of one half overlaps the MMAs of the other.
-        // Issue rate: preparing and issuing one tcgen05.mma costs the issuing warp about 120 cycles
-        // (operands travel vector -> uniform registers), three times what the tensor pipe needs
-        // for it (ncu: pipe 27 % busy with one issuer).  Stages therefore alternate between two
-        // issuing warps.  Each warp accumulates into its OWN accumulator, so the summation order
-        // of every output is fixed (results are bit-reproducible from run to run) however the
-        // tensor pipe interleaves the two instruction streams; the drain hands the accumulator
-        // halves back zeroed, so no MMA has to be "the first"; each warp commits what it issued.
-        const uint32_t me = warp == 0 ? 0u : (uint32_t)(warp - kIssuerB + 1);
+    if (warp == 0) {
+        // ================= issuer (whole warp, one elected lane issues) =================
+        // Every MMA is M = 128 x K = 16; the tensor pipe spends 64 cycles on it for any N <= 128
+        // (measured, tools/ubench_umma_ss.cu), so pass 2's band trimming (k-step m0 only feeds
+        // outputs n in [m0 - 2 rpad, m0 + 15]) saves shared-memory reads, not pipe time.
         uint32_t stage_it = 0, lvl_it = 0;
-        constexpr uint32_t idesc0 = instr_desc(kUT, 0);
-        constexpr uint32_t desc_hi = (kToepGroupBytes >> 4) | (1u << 14);        // SBO, version 1
-        RoleClock rc(a.prof != nullptr && lane == 0 && warp == 0);
+        RoleClock rc(a.prof != nullptr && lane == 0);
         for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
-            const Unit un = decode_unit(u, a);
-            const int lb = a.by_order ? tbl.order[un.g] : tbl.group_begin[un.g];
-            const int le = a.by_order ? lb + 1 : tbl.group_begin[un.g + 1];
-            for (int level = lb; level < le; ++level, ++lvl_it) {
+            const Unit un = decode_unit(u, a, tbl, MODE);
+            for (int level = un.lb; level < un.le; ++level, ++lvl_it) {
                 const int rpad2 = 2 * tbl.lv[level].rpad;
                 const int Kp = kUT + rpad2;
-#if DOGBLOB_UMMA_F16
-                constexpr int kStepRows = 16, kSteps = kStageRows / 16;      // MMA steps of 16 rows
-#else
-                constexpr int kStepRows = 8, kSteps = kStageK;
-#endif
-                const int n_k = Kp / kStepRows;
-                const int n_stage = (n_k + kSteps - 1) / kSteps;
-                // my last stage with a step that feeds n < 64 (rows up to 63 + 2 rpad)
-                int st_low = ((kHalf - 1 + rpad2) / kStepRows) / kSteps;
-                st_low -= (int)((stage_it + (uint32_t)st_low + kIssuers - me) % kIssuers);
-                const uint32_t b = lvl_it & 1, par = (lvl_it >> 1) & 1, lpar = lvl_it & 1;
+                const int n_k = Kp / 16;
+                const int n_stage = (n_k + kStepsPerStage - 1) / kStepsPerStage;
+                const uint32_t b = lvl_it & 1, par = (lvl_it >> 1) & 1;
                 rc.lap(3);
                 mbar_wait(smem_u32(&ctl->toep_full[b]), par, 1);
                 rc.lap(0);
-                mbar_wait(smem_u32(&ctl->acc_empty[0]), lpar ^ 1, 2);
+                mbar_wait(smem_u32(&ctl->acc_empty[b]), par ^ 1, 2);
                 rc.lap(1);
                 tc_fence_after();
-                // low descriptor word of the window of k-step 0 (row Kp - 8); every k-step moves the
-                // window up by 8 rows = one 256-byte group = 16 descriptor units
-                const uint32_t t_hi = smem_u32(toep + (size_t)(2 * b) * a.toep_floats);
-                const uint32_t lo_off = (uint32_t)ttab.rows[level] * 2u;            // hi -> lo array
-                const uint32_t win0 = ((t_hi + (uint32_t)((Kp - kStepRows) >> 3) * kToepGroupBytes) >> 4) |
-                                      ((kToepHalfBytes >> 4) << 16);
-                bool high_ok = false;
-                for (int st = (int)((me + kIssuers - stage_it % kIssuers) % kIssuers); st < n_stage; st += kIssuers) {
-                    if (!high_ok && st >= 64 / kStageRows) {      // rows from 64 on reach n >= 64
-                        mbar_wait(smem_u32(&ctl->acc_empty[1]), lpar ^ 1, 9);
-                        high_ok = true;
-                    }
-                    const uint32_t g = stage_it + (uint32_t)st, sl = g % kStages;
-                    const uint32_t a0 = tmem + kStageCol0 + sl * kStageCols;
+                // low descriptor word of the Toeplitz window of k-step 0 (row Kp - 16); every k-step
+                // moves the window up by 16 rows = two 256-byte groups = 32 descriptor units
+                const uint32_t t_hi = smem_u32(toep + (size_t)b * a.toep_bytes);
+                const uint32_t lo_off = (uint32_t)ttab.rows[level] * 2u;            // hi -> lo array (32 B per row)
+                const uint32_t win0 = ((t_hi + (uint32_t)(Kp - 16) * 32u) >> 4) | kToepLowLbo;
+                const uint32_t d_main = tmem + b * 2 * kAccCols, d_small = d_main + kAccCols;
+                for (int st = 0; st < n_stage; ++st) {
+                    const uint32_t g = stage_it + (uint32_t)st, sl = g % (uint32_t)S;
                     rc.lap(3);
-                    mbar_wait(smem_u32(&ctl->data_full[sl]), (g / kStages) & 1, 3);
+                    mbar_wait(smem_u32(&ctl->data_full[sl]), (g / (uint32_t)S) & 1, 3);
                     rc.lap(2);
                     tc_fence_after();
+                    const uint32_t sbase = smem_u32(data + (size_t)sl * kStageBytes);
+                    // pass 2: the last stage is shifted left so that it ends exactly at Kp (no read
+                    // beyond the halo); k-step j then sits (16 j - first_k) columns into the box
+                    const int first_k = kRows ? 32 * st : (st == n_stage - 1 ? Kp - 64 : 64 * st);
+                    const int j0 = kStepsPerStage * st;
+                    const int j1 = min(n_k, j0 + kStepsPerStage);
 #pragma unroll
-                    for (int ks = 0; ks < kSteps; ++ks) {
-                        const int kidx = st * kSteps + ks;
-                        if (kidx < n_k && !(a.debug & 8)) {
-                            const int m0 = kStepRows * kidx;
-                            int ns = max(0, m0 - rpad2) & ~15;
-                            int ne = min(kUT, (m0 + kStepRows + 15) & ~15);
-                            if (a.debug & 32) {          // experiment: untrimmed half / full width
-                                ns = m0 - rpad2 >= kHalf ? kHalf : 0;
-                                ne = m0 + kStepRows <= kHalf ? kHalf : kUT;
+                    for (int q = 0; q < kStepsPerStage; ++q) {
+                        const int j = j0 + q;
+                        if (j < j1) {
+                            const int m0 = 16 * j;
+                            const uint32_t win = win0 - 32u * (uint32_t)j;
+                            if (kRows) {
+                                // A = Toeplitz window, B = 16 image rows of the stage (2 KB per k-step)
+                                const uint32_t bd = ((sbase + (uint32_t)(m0 - first_k) * 128u) >> 4) | kData1LowLbo;
+                                umma_f16_triple_ss(d_main, d_small, win, win + lo_off, bd, bd + (8192u >> 4),
+                                                   kToepUpper, kData1Upper, instr_desc_f16(kUT, kUT, 1),
+                                                   j > 0);
+                            } else {
+                                // A = 16 k-columns of the stage (32 B into the swizzle atom per k-step),
+                                // B = Toeplitz window rows [ns, ne)
+                                const int ns = j == 0 ? 0 : (max(0, m0 - rpad2) & ~15);
+                                const int ne = j == 0 ? kUT : min(kUT, m0 + 16);
+                                const uint32_t ad = ((sbase + (uint32_t)(m0 - first_k) * 2u) >> 4) | kData2LowLbo;
+                                const uint32_t bw = win + 2u * (uint32_t)ns;
+                                umma_f16_triple_ss(d_main + ns, d_small + ns, ad, ad + (16384u >> 4), bw,
+                                                   bw + lo_off, kData2Upper, kToepUpper,
+                                                   instr_desc_f16(kUT, ne - ns, 0), j > 0);
                             }
-                            // the window moves up by kStepRows rows = kStepRows / 8 groups of 16 units
-                            const uint32_t dh = win0 - (uint32_t)(2 * kStepRows) * (uint32_t)kidx + 2u * (uint32_t)ns;
-                            const uint32_t acc = tmem + (kIssuers > 1 ? me : (uint32_t)(kidx & 1)) * kAccCols + ns;   // this warp's accumulator(s)
-#if DOGBLOB_UMMA_F16
-                            const uint32_t a_hi = a0 + ks * 32, a_lo = a_hi + 8;
-                            const uint32_t idesc = instr_desc_f16(kUT, 0) | ((uint32_t)((ne - ns) >> 3) << 17);
-                            umma_f16_triple_elect(acc, a_hi, a_lo, dh + lo_off, dh, desc_hi, idesc);
-#else
-                            const uint32_t a_hi = a0 + ks * 16, a_lo = a_hi + 8;
-                            const uint32_t idesc = idesc0 | ((uint32_t)((ne - ns) >> 3) << 17);
-                            umma_tf32_triple_elect(acc, a_hi, a_lo, dh + lo_off, dh, desc_hi, idesc);
-#endif
                         }
                     }
                     umma_commit_elect(smem_u32(&ctl->data_empty[sl]));
-                    if (st == st_low) umma_commit_elect(smem_u32(&ctl->acc_full[0]));
                 }
                 stage_it += (uint32_t)n_stage;
                 umma_commit_elect(smem_u32(&ctl->toep_empty[b]));
-                umma_commit_elect(smem_u32(&ctl->acc_full[1]));
+                umma_commit_elect(smem_u32(&ctl->acc_full[b]));
             }
         }
         rc.lap(3);
         rc.flush(a.prof, 0);
         if (rc.on) {        // slowest / fastest CTA (issuer's whole life)
             const unsigned long long tot = rc.acc[0] + rc.acc[1] + rc.acc[2] + rc.acc[3];
-            atomicMax(a.prof + 10, tot);
-            atomicMin(a.prof + 11, tot);
+            atomicMax(a.prof + 14, tot);
+            atomicMin(a.prof + 15, tot);
         }
     } else if (warp == 1) {
-        // ================= Toeplitz copier: prebuilt hi|lo arrays, one bulk copy per level ========
-        uint32_t lvl_it = 0;
+        // ================= loader: one TMA box per data stage =================
+        uint32_t g = 0;
         RoleClock rc(a.prof != nullptr && lane == 0);
-        for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
-            const Unit un = decode_unit(u, a);
-            const int lb = a.by_order ? tbl.order[un.g] : tbl.group_begin[un.g];
-            const int le = a.by_order ? lb + 1 : tbl.group_begin[un.g + 1];
-            for (int level = lb; level < le; ++level, ++lvl_it) {
-                const uint32_t b = lvl_it & 1, par = (lvl_it >> 1) & 1;
-                rc.lap(1);
-                mbar_wait_sleep(smem_u32(&ctl->toep_empty[b]), par ^ 1, 4);
-                rc.lap(0);
-                if (lane == 0) {
+        if (lane == 0) {
+            for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+                const Unit un = decode_unit(u, a, tbl, MODE);
+                for (int level = un.lb; level < un.le; ++level) {
+                    const int rpad = tbl.lv[level].rpad;
+                    const int Kp = kUT + 2 * rpad;
+                    const int n_stage = (Kp / 16 + kStepsPerStage - 1) / kStepsPerStage;
+                    for (int st = 0; st < n_stage; ++st, ++g) {
+                        const uint32_t sl = g % (uint32_t)S;
+                        rc.lap(1);
+                        mbar_wait(smem_u32(&ctl->data_empty[sl]), ((g / (uint32_t)S) & 1) ^ 1, 7);
+                        rc.lap(0);
+                        const uint32_t bar = smem_u32(&ctl->data_full[sl]);
+                        const uint32_t dst = smem_u32(data + (size_t)sl * kStageBytes);
+                        mbar_expect_tx(bar, kStageBytes);
+                        if (kRows)      // X planes: {64 x, rows, x-block, hi | lo}; rows beyond the planes read as 0
+                            tma_load_4d(dst, &map_in, 0, a.Py + un.y0 - rpad + 32 * st, un.x0 / 64, 0, bar);
+                        else            // R planes: {columns, rows of all levels, hi | lo}
+                            tma_load_3d(dst, &map_in,
+                                        a.Ppad + un.x0 - rpad + (st == n_stage - 1 ? Kp - 64 : 64 * st),
+                                        level * a.Hp + un.y0, 0, bar);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        rc.lap(1);
+        rc.flush(a.prof, 4);
+    } else if (warp == 2) {
+        // ================= Toeplitz copier: prebuilt hi | lo arrays, one bulk copy per level ========
+        uint32_t lvl_it = 0;
+        if (lane == 0) {
+            for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+                const Unit un = decode_unit(u, a, tbl, MODE);
+                for (int level = un.lb; level < un.le; ++level, ++lvl_it) {
+                    const uint32_t b = lvl_it & 1, par = (lvl_it >> 1) & 1;
+                    mbar_wait(smem_u32(&ctl->toep_empty[b]), par ^ 1, 4);
                     const uint32_t bytes = (uint32_t)ttab.rows[level] * 64u;     // hi + lo
                     const uint32_t bar = smem_u32(&ctl->toep_full[b]);
                     mbar_expect_tx(bar, bytes);
-                    bulk_copy_g2s(smem_u32(toep + (size_t)(2 * b) * a.toep_floats),
-                                  a.toep + ttab.ofs[level], bytes, bar);
-                }
-                __syncwarp();
-            }
-        }
-        rc.lap(1);
-        rc.flush(a.prof, 4);
-    } else if (warp < 4) {
-        // ================= row loaders: 32 input rows x 512 B per raw stage =====================
-        // interior stages: one TMA box; stages that cross the image border: 64 threads x 16
-        // LDGSTS of 16 bytes with folded rows (thread t: column group t & 31 of rows (t >> 5) + 2 i).
-        const int t = threadIdx.x - 64;
-        const int cg = t & 31, rsub = t >> 5;
-        uint32_t rs = 0, rp = 0;                          // raw stage and its phase parity
-        int gate_have = 0;
-        bool gate_stamped = false;
-        RoleClock rc(a.prof != nullptr && t == 0);
-        for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
-            const Unit un = decode_unit(u, a);
-            const int lb = a.by_order ? tbl.order[un.g] : tbl.group_begin[un.g];
-            const int le = a.by_order ? lb + 1 : tbl.group_begin[un.g + 1];
-            for (int level = lb; level < le; ++level) {
-                const int rpad = tbl.lv[level].rpad;
-                const int n_stage = (kUT + 2 * rpad + kStageRows - 1) / kStageRows;
-                const float *src = a.in + (int64_t)level * a.in_plane + un.c0 + 4 * cg;
-                int row0 = un.r0 - rpad;
-                for (int st = 0; st < n_stage; ++st, row0 += kStageRows, rp ^= (rs + 1 == (uint32_t)R),
-                         rs = (rs + 1 == (uint32_t)R) ? 0 : rs + 1) {
-                    rc.lap(1);
-                    mbar_wait(smem_u32(&ctl->raw_empty[rs]), rp ^ 1, 7);
-                    rc.lap(0);
-                    if (a.gate_word) {
-                        // last image row this stage reads (rows above 0 / below n_rows fold inwards)
-                        int need_row = row0 + kStageRows - 1;
-                        if (row0 < 0) need_row = max(need_row, -row0 - 1);
-                        need_row = min(need_row, a.n_rows - 1);
-                        if (a.n_rows < kStageRows + tbl.lv[level].rpad) need_row = a.n_rows - 1;
-                        const int need = need_row / a.gate_rows_per_chunk + 1;
-                        if (need > gate_have) {
-                            while ((gate_have = *(const volatile int *)a.gate_word - a.gate_base) < need)
-                                __nanosleep(200);
-                            __threadfence();
-                        }
-                        if (!gate_stamped) {
-                            gate_stamped = true;
-                            if (blockIdx.x == 0 && t == 0 && a.gate_t_start) *a.gate_t_start = globaltimer_ns();
-                        }
-                    }
-                    const uint32_t bar = smem_u32(&ctl->raw_full[rs]);
-                    if (a.use_tma && row0 >= 0 && row0 + kStageRows <= a.n_rows) {
-                        if (t == 0) {
-                            mbar_expect_tx_only(bar, kStageRows * kUT * 4);
-                            tma_load_2d(smem_u32(raw + (size_t)rs * kStageRows * kUT), &tmap, un.c0,
-                                        level * a.tma_plane_rows + row0, bar);
-                        }
-                        mbar_arrive(bar);
-                        continue;
-                    }
-                    const uint32_t dst = smem_u32(raw + ((size_t)rs * kStageRows + rsub) * kUT + 4 * cg);
-#pragma unroll 4
-                    for (int i = 0; i < kStageRows / 2; ++i)
-                        cp_async16(dst + i * 2 * kUT * 4,
-                                   src + (int64_t)fold_row_u(row0 + rsub + 2 * i, a.n_rows) * a.in_pitch);
-                    cp_async_arrive_noinc(bar);
+                    bulk_copy_g2s(smem_u32(toep + (size_t)b * a.toep_bytes), a.toep + ttab.ofs[level], bytes, bar);
                 }
             }
         }
-        rc.lap(1);
-        rc.flush(a.prof, 6);
-    } else if (is_drain) {
-        // ================= drain (accumulators -> DoG -> global), one column half at a time ======
-        const int q = warp & 3;
-        const int m = 32 * q + lane;
+        __syncwarp();
+    } else if (warp >= kDrainWarp0) {
+        // ================= drain: accumulators -> (hi | lo rows) or (DoG slice) -> TMA store ========
+        // warp = lane quarter q (TMEM lanes 32 q .. 32 q + 31 = output rows) x column half h
+        const int dw = warp - kDrainWarp0;
+        const int q = dw & 3, h = dw >> 2;
+        const int row = 32 * q + lane;                       // output row inside the tile
+        const bool store_leader = q == 0 && lane == 0;       // issues this half's TMA stores
+        const int bar_a = 1 + 2 * h, bar_b = 2 + 2 * h;      // named barriers of this half (128 threads)
         uint32_t lvl_it = 0;
-        RoleClock rc(a.prof != nullptr && warp == 4 && lane == 0);
-        const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
-#if DOGBLOB_UMMA_F16
+        RoleClock rc(a.prof != nullptr && dw == 0 && lane == 0);
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(64 * h);
+        const uint32_t stg = smem_u32(staging + (size_t)h * 16384);
+        const uint32_t stg_row = stg + (uint32_t)row * 128u;
+        const uint32_t swz = (uint32_t)(row & 7);
         const int frame_exp = frame_scale_exp(a.frame_max_bits);
-#endif
+        const float unscale_x = pow2f(-frame_exp);
+        float prev[64];                                      // pass 2: previous level of this thread's outputs
+#pragma unroll
+        for (int j = 0; j < 64; ++j) prev[j] = 0.f;
         for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
-            const Unit un = decode_unit(u, a);
-            const int lb = a.by_order ? tbl.order[un.g] : tbl.group_begin[un.g];
-            const int le = a.by_order ? lb + 1 : tbl.group_begin[un.g + 1];
-            for (int level = lb; level < le; ++level, ++lvl_it) {
-                const uint32_t lpar = lvl_it & 1;
-                const bool park_first = MODE == kModeDog && level == lb && un.g > 0;
-                const bool park_last = MODE == kModeDog && level == le - 1 && un.g < tbl.n_groups - 1;
-                const float sig = MODE == kModeDog && level > lb ? tbl.lv[level - 1].sigma_f32 : 0.f;
-#if DOGBLOB_UMMA_F16
+            const Unit un = decode_unit(u, a, tbl, MODE);
+            for (int level = un.lb; level < un.le; ++level, ++lvl_it) {
+                const uint32_t b = lvl_it & 1, par = (lvl_it >> 1) & 1;
                 // exact (powers of two), applied one after the other so neither factor underflows
-                const float unscale_t = pow2f(-ttab.tscale[level]), unscale_x = pow2f(-frame_exp);
-#endif
-#pragma unroll 1
-                for (int half = 0; half < 2; ++half) {
-                    rc.lap(1);
-                    mbar_wait_sleep(smem_u32(&ctl->acc_full[half]), lpar, 5);
-                    rc.lap(0);
-                    tc_fence_after();
-#pragma unroll 1
-                    for (int c = dgroup; c < kHalf / 16; c += kDrainGroups) {   // the groups share a half
-                        const int n0 = half * kHalf + c * 16;
-                        uint32_t ra[kAccs][16];
+                const float unscale_t = pow2f(-ttab.tscale[level]);
+                const uint32_t acc = lane_base + b * 2 * kAccCols;
+                rc.lap(1);
+                mbar_wait(smem_u32(&ctl->acc_full[b]), par, 5);
+                rc.lap(0);
+                tc_fence_after();
+                if (kRows) {
+                    // ---- pass 1: v = level value in frame-scaled units -> fp16 hi | lo words ----
+                    uint32_t hw[32], lw[32];                 // 64 columns: 32 packed pairs each
 #pragma unroll
-                        for (int i = 0; i < kAccs; ++i) tmem_ld16(lane_base + i * kAccCols + n0, ra[i]);
+                    for (int c = 0; c < 2; ++c) {
+                        uint32_t ra[32], rb[32];
+                        tmem_ld32_pair(acc + 32 * c, acc + kAccCols + 32 * c, ra, rb);
 #pragma unroll
-                        for (int i = 0; i < kAccs; ++i) tmem_wait_ld16(ra[i]);
-                        if (a.debug & 4) continue;
-                        float r[16];
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            r[j] = __uint_as_float(ra[0][j]);
-#pragma unroll
-                            for (int i = 1; i < kAccs; ++i) r[j] = __fadd_rn(r[j], __uint_as_float(ra[i][j]));
-#if DOGBLOB_UMMA_F16
-                            r[j] = __fmul_rn(__fmul_rn(r[j], unscale_t), unscale_x);
-#endif
+                        for (int j = 0; j < 32; j += 2) {
+                            const float v0 = __fmul_rn(__fadd_rn(__uint_as_float(ra[j]), __uint_as_float(rb[j])), unscale_t);
+                            const float v1 = __fmul_rn(__fadd_rn(__uint_as_float(ra[j + 1]), __uint_as_float(rb[j + 1])), unscale_t);
+                            split_pair(v0, v1, hw[16 * c + j / 2], lw[16 * c + j / 2]);
                         }
-                        if (MODE == kModeRows) {
-                            // lane = x (contiguous input axis), registers = 16 consecutive y of T[x][y]
-                            float *dst = a.out + (int64_t)level * a.out_plane +
-                                         (int64_t)(un.c0 + m) * a.out_pitch + un.r0 + n0;
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(smem_u32(&ctl->acc_empty[b]));
+                    rc.lap(2);
+                    // two rounds through this half's 16 KB staging box: hi plane, then lo plane
 #pragma unroll
-                            for (int j = 0; j < 16; j += 4)
-                                *reinterpret_cast<float4 *>(dst + j) = make_float4(r[j], r[j + 1], r[j + 2], r[j + 3]);
-                        } else {
-                            // lane = y (contiguous), registers = 16 consecutive output rows x
-                            const int64_t tile_ofs = (int64_t)(un.r0 + n0) * a.out_pitch + un.c0 + m;
-                            if (MODE == kModeLevels) {
-                                float *dst = a.out + (int64_t)level * a.out_plane + tile_ofs;
+                    for (int pl = 0; pl < 2; ++pl) {
+                        if (store_leader) bulk_wait_read();                 // the box's previous store has been read
+                        named_bar(bar_a, 128);
 #pragma unroll
-                                for (int j = 0; j < 16; ++j) dst[(int64_t)j * a.out_pitch] = r[j];
+                        for (int c = 0; c < 8; ++c) {
+                            const uint32_t *w = pl == 0 ? hw : lw;
+                            st_shared_v4(stg_row + (((uint32_t)c ^ swz) << 4), w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+                        }
+                        fence_proxy_async_smem();
+                        named_bar(bar_b, 128);
+                        if (store_leader) {
+                            tma_store_3d(&map_out, a.Ppad + un.x0 + 64 * h, level * a.Hp + un.y0, pl, stg);
+                            bulk_commit();
+                        }
+                    }
+                    // reflected halo columns of pass 2's input, written next to the interior:
+                    // column -1 - x <- x for x < rpad, column 2 W - 1 - x <- x for the last
+                    // rpad + (Wp - W) valid columns (ragged frames: pass 2 reads up to Wp + rpad)
+                    const int rpad = tbl.lv[level].rpad;
+                    const int xs0 = un.x0 + 64 * h;
+                    const int right_w = rpad + (a.Wp - a.W);
+                    if (xs0 < rpad || xs0 + 64 > a.W - right_w) {
+                        __half *rrow = a.r_base + ((int64_t)level * a.Hp + un.y0 + row) * a.r_pitch + a.Ppad;
+#pragma unroll
+                        for (int pl = 0; pl < 2; ++pl) {
+                            __half *prow = rrow + (int64_t)pl * a.r_plane;
+                            const uint32_t *w = pl == 0 ? hw : lw;
+                            if ((a.W & 7) == 0) {
+#pragma unroll
+                                for (int gq = 0; gq < 8; ++gq) {            // groups of 8 columns, reversed
+                                    const int xs = xs0 + 8 * gq;
+                                    const uint4 rev = make_uint4(__byte_perm(w[4 * gq + 3], 0, 0x1032), __byte_perm(w[4 * gq + 2], 0, 0x1032),
+                                                                 __byte_perm(w[4 * gq + 1], 0, 0x1032), __byte_perm(w[4 * gq], 0, 0x1032));
+                                    if (xs < rpad) *reinterpret_cast<uint4 *>(prow - 8 - xs) = rev;
+                                    if (xs >= a.W - right_w && xs < a.W) *reinterpret_cast<uint4 *>(prow + 2 * a.W - 8 - xs) = rev;
+                                }
                             } else {
-                                if (park_first || park_last) {
-                                    float *dst = a.edge + (int64_t)(2 * un.g + (park_first ? 0 : 1)) * a.out_plane + tile_ofs;
 #pragma unroll
-                                    for (int j = 0; j < 16; ++j) dst[(int64_t)j * a.out_pitch] = r[j];
-                                    if (park_first && park_last) {      // single-level group
-                                        dst = a.edge + (int64_t)(2 * un.g + 1) * a.out_plane + tile_ofs;
-#pragma unroll
-                                        for (int j = 0; j < 16; ++j) dst[(int64_t)j * a.out_pitch] = r[j];
-                                    }
-                                }
-                                float *slot = s_prev + n0 * kUT + m;
-                                if (level > lb) {
-                                    float *dst = a.out + (int64_t)(level - 1) * a.out_plane + tile_ofs;
-#pragma unroll
-                                    for (int j = 0; j < 16; ++j)
-                                        dst[(int64_t)j * a.out_pitch] = __fmul_rn(__fsub_rn(slot[j * kUT], r[j]), sig);
-                                }
-                                if (level < le - 1) {
-#pragma unroll
-                                    for (int j = 0; j < 16; ++j) slot[j * kUT] = r[j];
+                                for (int e = 0; e < 64; ++e) {              // odd widths: element by element
+                                    const int x = xs0 + e;
+                                    const unsigned short v = (unsigned short)((e & 1) ? (w[e >> 1] >> 16) : (w[e >> 1] & 0xffffu));
+                                    if (x < rpad) reinterpret_cast<unsigned short *>(prow)[-1 - x] = v;
+                                    if (x >= a.W - right_w && x < a.W) reinterpret_cast<unsigned short *>(prow)[2 * a.W - 1 - x] = v;
                                 }
                             }
                         }
                     }
-                    zero_acc_half(lane_base, half, dgroup);  // every MMA accumulates (none is "first")
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(smem_u32(&ctl->acc_empty[half]));
+                    rc.lap(3);
+                } else {
+                    // ---- pass 2: level value -> DoG slice against the previous level (registers) ----
+                    const bool emit = MODE == kModeLevels || level > un.lb;
+                    const float sig = MODE == kModeDog && level > un.lb ? tbl.lv[level - 1].sigma_f32 : 0.f;
+                    const int out_plane = MODE == kModeLevels ? level : level - 1;
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        uint32_t ra[32], rb[32];
+                        tmem_ld32_pair(acc + 32 * c, acc + kAccCols + 32 * c, ra, rb);
+                        if (c == 1) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(smem_u32(&ctl->acc_empty[b]));
+                        }
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const float v = __fmul_rn(__fmul_rn(__fadd_rn(__uint_as_float(ra[j]), __uint_as_float(rb[j])), unscale_t), unscale_x);
+                            if (MODE == kModeDog) {
+                                ra[j] = __float_as_uint(__fmul_rn(__fsub_rn(prev[32 * c + j], v), sig));
+                                prev[32 * c + j] = v;
+                            } else {
+                                ra[j] = __float_as_uint(v);
+                            }
+                        }
+                        rc.lap(2);
+                        if (emit) {                              // uniform per level
+                            if (store_leader) bulk_wait_read();
+                            named_bar(bar_a, 128);
+#pragma unroll
+                            for (int k = 0; k < 8; ++k)
+                                st_shared_v4(stg_row + (((uint32_t)k ^ swz) << 4), ra[4 * k], ra[4 * k + 1], ra[4 * k + 2], ra[4 * k + 3]);
+                            fence_proxy_async_smem();
+                            named_bar(bar_b, 128);
+                            if (store_leader) {
+                                tma_store_2d(&map_out, un.x0 + 64 * h + 32 * c, out_plane * a.Hp + un.y0, stg);
+                                bulk_commit();
+                            }
+                        }
+                        rc.lap(3);
+                    }
                 }
             }
         }
+        if (store_leader) bulk_wait_all();
         rc.lap(1);
         rc.flush(a.prof, 8);
-    } else {
-        // ================= converters (raw rows -> hi/lo -> TMEM A staging) =================
-        const int q = warp & 3;
-        const int grp = (warp - 8) >> 2;
-        const int m = 32 * q + lane;
-        RoleClock rc(a.prof != nullptr && warp == 8 && lane == 0);
-#if DOGBLOB_UMMA_F16
-        const float xscale = pow2f(frame_scale_exp(a.frame_max_bits));
-#endif
-        int total = 0;                                   // stages this CTA processes
-        for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
-            const Unit un = decode_unit(u, a);
-            const int lb = a.by_order ? tbl.order[un.g] : tbl.group_begin[un.g];
-            const int le = a.by_order ? lb + 1 : tbl.group_begin[un.g + 1];
-            for (int level = lb; level < le; ++level)
-                total += (kUT + 2 * tbl.lv[level].rpad + kStageRows - 1) / kStageRows;
-        }
-        uint32_t rs = grp % R, rp = (grp / R) & 1;
-        for (uint32_t stage_it = grp; stage_it < (uint32_t)total; stage_it += kLoaderGroups,
-                      rs += kLoaderGroups, rp ^= (rs >= (uint32_t)R), rs -= (rs >= (uint32_t)R) ? R : 0) {
-            const uint32_t s = stage_it % kStages, sp = (stage_it / kStages) & 1;
-            rc.lap(3);
-            mbar_wait(smem_u32(&ctl->raw_full[rs]), rp, 8);
-            rc.lap(0);
-            const float *src = raw + (size_t)rs * kStageRows * kUT + m;
-            const uint32_t dst = tmem + kStageCol0 + s * kStageCols + ((uint32_t)(32 * q) << 16);
-#pragma unroll
-            for (int h = 0; h < kStageK / 2; ++h) {       // 16 rows = 2 k-steps at a time
-                float v[16];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) v[k] = src[(16 * h + k) * kUT];
-                uint32_t r0[16], r1[16];
-#if DOGBLOB_UMMA_F16
-                // 16 rows = one MMA step: columns 0..7 hi (2 rows per column), 8..15 lo
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const float s0 = __fmul_rn(v[2 * k], xscale), s1 = __fmul_rn(v[2 * k + 1], xscale);
-                    const uint32_t hp = pack_f16x2(s0, s1);
-                    const float2 hf = __half22float2(*reinterpret_cast<const __half2 *>(&hp));
-                    r0[k] = hp;
-                    r0[8 + k] = pack_f16x2(__fsub_rn(s0, hf.x), __fsub_rn(s1, hf.y));
-                    r1[k] = 0; r1[8 + k] = 0;
-                }
-#else
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    split_tf32(v[k], r0[k], r0[8 + k]);
-                    split_tf32(v[8 + k], r1[k], r1[8 + k]);
-                }
-#endif
-                if (h == kStageK / 2 - 1) {               // all rows of the raw stage are in registers
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(smem_u32(&ctl->raw_empty[rs]));
-                }
-                if (h == 0) {
-                    rc.lap(1);
-                    mbar_wait(smem_u32(&ctl->data_empty[s]), sp ^ 1, 6);
-                    rc.lap(2);
-                    tc_fence_after();
-                }
-                tmem_st16(dst + 32 * h, r0);
-#if !DOGBLOB_UMMA_F16
-                tmem_st16(dst + 32 * h + 16, r1);
-#endif
-                // tcgen05.st reads its source registers asynchronously: they must not be reused
-                // (the next half's values land in the same physical registers) before wait::st.
-                // Found the hard way: without this wait some builds returned a few corrupted
-                // stages per frame, different from run to run (tools/umma_repro.py).
-                tmem_wait_st();
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&ctl->data_full[s]));
-        }
-        rc.lap(3);
-        rc.flush(a.prof, 12);
     }
 
     tc_fence_before();
@@ -863,35 +654,62 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
-#if DOGBLOB_UMMA_F16
+// Frame -> fp16 hi | lo planes [2][H + 2 Py][Wp] in frame-scaled units, reflected halo rows
+// materialised (row r of the planes = frame row fold(r - Py)), pad columns x >= W zero.
+__global__ void prep_split_kernel(const float *__restrict__ img, int64_t pitch, int H, int W, int Wp, int Py,
+                                  const uint32_t *__restrict__ max_bits, __half *__restrict__ xp) {
+    const float xscale = pow2f(frame_scale_exp(max_bits));
+    const int rows = H + 2 * Py, groups = Wp / 8;
+    const int64_t plane = (int64_t)rows * Wp;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)rows * groups;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i / groups), x = (int)(i % groups) * 8;
+        const float *src = img + (int64_t)fold_row_u(r - Py, H) * pitch + x;
+        float v[8];
+        if (x + 8 <= W) {
+            const float4 p = __ldg(reinterpret_cast<const float4 *>(src));
+            const float4 s = __ldg(reinterpret_cast<const float4 *>(src) + 1);
+            v[0] = p.x; v[1] = p.y; v[2] = p.z; v[3] = p.w; v[4] = s.x; v[5] = s.y; v[6] = s.z; v[7] = s.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = x + k < W ? __ldg(src + k) : 0.f;
+        }
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            split_pair(__fmul_rn(v[2 * k], xscale), __fmul_rn(v[2 * k + 1], xscale), hi[k], lo[k]);
+        *reinterpret_cast<uint4 *>(xp + (int64_t)r * Wp + x) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4 *>(xp + plane + (int64_t)r * Wp + x) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
+}
+
+// max |x| of the frame as float bits (non-negative floats order like unsigned integers)
+__global__ void frame_max_kernel(const float *__restrict__ img, int64_t n4, uint32_t *__restrict__ max_bits) {
+    float m = 0.f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(img) + i);
+        m = fmaxf(fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))), m);
+    }
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(max_bits, __float_as_uint(m));
+}
+
 int toeplitz_rows(int rpad) { return kUT + 2 * rpad - 16 + kUT; }
-#else
-int toeplitz_rows(int rpad) { return kUT + 2 * rpad - 8 + kUT; }
-#endif
-int toeplitz_floats(int max_rpad) { return toeplitz_rows(max_rpad) * 8; }
+int toeplitz_buffer_bytes(int max_rpad) { return (toeplitz_rows(max_rpad) * 64 + 1023) / 1024 * 1024; }
 
 constexpr size_t kSmemLimit = 227 * 1024;
-size_t umma_fixed_smem(int max_rpad, bool dog) {
-    return 1024 + 4 * (size_t)toeplitz_floats(max_rpad) * sizeof(float) +
-           (dog ? (size_t)kUT * kUT * sizeof(float) : 0);
-}
-int raw_stages_for(int max_rpad, bool dog) {
-    const size_t fixed = umma_fixed_smem(max_rpad, dog);
-    if (fixed + 2 * kStageRows * kUT * 4 > kSmemLimit) return 0;
-    // a multiple of the number of converter groups: a raw stage is then always converted by the
-    // same group, so no waiter is ever two phases behind its barrier (a parity wait cannot tell
-    // phase n from phase n + 2)
-    const size_t r = std::min<size_t>(kMaxRawStages, (kSmemLimit - fixed) / (kStageRows * kUT * 4));
-    return (int)(r / kLoaderGroups * kLoaderGroups);
+int data_stages_for(int max_rpad, bool rows_pass) {
+    const size_t fixed = 1024 + 2 * (size_t)toeplitz_buffer_bytes(max_rpad) + kStagingBytes;
+    const size_t per = rows_pass ? kStageBytes1 : kStageBytes2;
+    if (fixed + 2 * per > kSmemLimit) return 0;
+    return (int)std::min<size_t>(kMaxStages, (kSmemLimit - fixed) / per);
 }
 
-// 2-D tensor map over the input rows: inner dimension = the pitch (contiguous axis), outer = all
-// rows of all level planes; box = 128 floats x 16 rows, no swizzle, no interleave.
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
                                   CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
                                   CUtensorMapFloatOOBfill);
-bool encode_rows_map(CUtensorMap *map, const float *base, uint64_t pitch, uint64_t rows) {
+EncodeTiledFn tensor_map_encoder() {
     static EncodeTiledFn fn = [] {
         void *p = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -900,13 +718,16 @@ bool encode_rows_map(CUtensorMap *map, const float *base, uint64_t pitch, uint64
             p = nullptr;
         return reinterpret_cast<EncodeTiledFn>(p);
     }();
+    return fn;
+}
+// SWIZZLE_128B tensor map; dims / strides (bytes, dims 1..) / box in elements
+bool encode_map(CUtensorMap *map, CUtensorMapDataType type, int rank, const void *base, const cuuint64_t *dims,
+                const cuuint64_t *strides, const cuuint32_t *box) {
+    EncodeTiledFn fn = tensor_map_encoder();
     if (!fn) return false;
-    const cuuint64_t dims[2] = {pitch, rows};
-    const cuuint64_t strides[1] = {pitch * sizeof(float)};
-    const cuuint32_t box[2] = {(cuuint32_t)kUT, (cuuint32_t)kStageRows};
-    const cuuint32_t estr[2] = {1, 1};
-    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    return fn(map, type, (cuuint32_t)rank, const_cast<void *>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -915,72 +736,76 @@ int persistent_ctas(int n_units) {
         int dev = 0, n = 148;
         if (cudaGetDevice(&dev) == cudaSuccess)
             cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (const char *e = std::getenv("DOGBLOB_UMMA_CTAS")) n = std::max(1, std::atoi(e));
         return n;
     }();
     return std::min(n_units, sms);
 }
 
+// DOGBLOB_UMMA_PROF (read once): per-role cycle counters of every launch, printed to stderr
+bool umma_prof_enabled() {
+    static const bool on = std::getenv("DOGBLOB_UMMA_PROF") != nullptr;
+    return on;
+}
+
 template <int MODE>
-cudaError_t launch_umma(const UmmaArgs &a, const LevelTable &tbl, const ToeplitzTable &ttab,
-                        int max_rpad, cudaStream_t st) {
-    UmmaArgs b = a;
-    b.toep_floats = toeplitz_floats(max_rpad);
-    b.raw_stages = raw_stages_for(max_rpad, MODE == kModeDog);
-    if (const char *e = std::getenv("DOGBLOB_UMMA_RAW")) b.raw_stages = std::max(2, std::min(b.raw_stages, std::atoi(e))) / kLoaderGroups * kLoaderGroups;
-    const size_t smem = umma_fixed_smem(max_rpad, MODE == kModeDog) +
-                        (size_t)b.raw_stages * kStageRows * kUT * 4;
-    if (const char *e = std::getenv("DOGBLOB_UMMA_DEBUG")) b.debug = std::atoi(e);
+cudaError_t launch_umma(UmmaArgs b, const LevelTable &tbl, const ToeplitzTable &ttab, int max_rpad,
+                        const CUtensorMap &map_in, const CUtensorMap &map_out, cudaStream_t st) {
+    constexpr bool rows_pass = MODE == kModeRows;
+    b.toep_bytes = toeplitz_buffer_bytes(max_rpad);
+    b.stages = data_stages_for(max_rpad, rows_pass);
+    if (b.stages < 2) return cudaErrorInvalidConfiguration;
+    const size_t smem = 1024 + 2 * (size_t)b.toep_bytes + kStagingBytes +
+                        (size_t)b.stages * (rows_pass ? kStageBytes1 : kStageBytes2);
     static unsigned long long *d_prof = nullptr;
-    const bool prof = std::getenv("DOGBLOB_UMMA_PROF") != nullptr;
+    const bool prof = umma_prof_enabled();
     if (prof) {
         if (!d_prof) cudaMalloc(&d_prof, 16 * sizeof(unsigned long long));
         cudaMemsetAsync(d_prof, 0, 16 * sizeof(unsigned long long), st);
-        cudaMemsetAsync(d_prof + 11, 0xff, sizeof(unsigned long long), st);
+        cudaMemsetAsync(d_prof + 15, 0xff, sizeof(unsigned long long), st);
         b.prof = d_prof;
     }
-    CUtensorMap tmap;
-    std::memset(&tmap, 0, sizeof(tmap));
-    b.use_tma = 0;
-    if (!std::getenv("DOGBLOB_UMMA_NO_TMA")) {
-        const int planes = b.in_plane ? tbl.n_levels : 1;
-        const int plane_rows = b.in_plane ? (int)(b.in_plane / b.in_pitch) : b.n_rows;
-        b.tma_plane_rows = b.in_plane ? plane_rows : 0;
-        if (encode_rows_map(&tmap, b.in, (uint64_t)b.in_pitch, (uint64_t)planes * plane_rows)) b.use_tma = 1;
-    }
     const int ctas = persistent_ctas(b.n_units);
-    umma_pass_kernel<MODE><<<ctas, kUThreads, smem, st>>>(b, tbl, ttab, tmap);
+    umma_pass_kernel<MODE><<<ctas, kThreads, smem, st>>>(b, tbl, ttab, map_in, map_out);
     if (prof) {
         unsigned long long h[16];
         cudaStreamSynchronize(st);
         cudaMemcpy(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost);
         static const char *names[16] = {
-            "issuer    wait toeplitz", "issuer    wait acc free", "issuer    wait data", "issuer    issue+other",
-            "toeplitz  wait buffer", "toeplitz  issue", "rows      wait raw stage free", "rows      cp.async issue",
-            "drain     wait acc", "drain     ld+store", "-", "-",
-            "converter wait raw rows", "converter lds+split", "converter wait stage free", "converter st+arrive"};
-        fprintf(stderr, "umma mode %d, %d CTAs, %d raw stages, kilo-cycles per CTA:", MODE, ctas, b.raw_stages);
+            "issuer  wait toeplitz", "issuer  wait acc free", "issuer  wait data", "issuer  issue+other",
+            "loader  issue", "loader  wait stage free", "-", "-",
+            "drain   wait+tmem ld", "drain   wait acc", "drain   math", "drain   staging+store",
+            "-", "-", "-", "-"};
+        fprintf(stderr, "umma mode %d, %d CTAs, %d stages, kilo-cycles per CTA:", MODE, ctas, b.stages);
         for (int i = 0; i < 16; ++i)
             if (names[i][0] != '-') fprintf(stderr, "\n   %-34s %8.1f", names[i], h[i] / 1e3 / ctas);
-        fprintf(stderr, "\n   issuer total: slowest CTA %.1f, fastest %.1f\n", h[10] / 1e3, h[11] / 1e3);
+        fprintf(stderr, "\n   issuer total: slowest CTA %.1f, fastest %.1f\n", h[14] / 1e3, h[15] / 1e3);
     }
     return cudaGetLastError();
 }
 
 }  // namespace
 
-bool umma_supported(const ConvGeometry &g) { return raw_stages_for(g.max_rpad, true) >= 2; }
-
-// Toeplitz operand of every level, as the kernel wants it in shared memory (see the header of
-// this file): per level `rows` = Kp - 8 + 128 rows of 8 taps, hi array then lo array, 8-row groups
-// of 256 bytes = [K half 0: 8 rows x 16 B][K half 1: 8 rows x 16 B].
-// G[p][kk] = w[kk - p + Kp - 8]; taps: the plan's duplicated table (entry t = offset t - rpad).
-static uint32_t host_tf32_rna(float x) {
-    uint32_t u;
-    std::memcpy(&u, &x, 4);
-    u = (u + 0x1000u) & 0xFFFFE000u;        // round to nearest, ties away (finite inputs)
-    return u;
+// The tensor-core passes need: both Toeplitz buffers, the drain staging and >= 2 data stages in
+// shared memory; every halo column mirrored from inside the frame (one reflection).
+bool umma_supported(const ConvGeometry &g) {
+    return data_stages_for(g.max_rpad, true) >= 2 && data_stages_for(g.max_rpad, false) >= 2 &&
+           g.W >= g.max_rpad + (g.Wp - g.W) && tensor_map_encoder() != nullptr;
 }
+
+UmmaLayout umma_layout(const ConvGeometry &g) {
+    UmmaLayout l;
+    l.Py = g.max_rpad;
+    l.Ppad = (g.max_rpad + 63) / 64 * 64;
+    l.Wq = g.Wp + 2 * l.Ppad;
+    l.x_bytes = 2 * (size_t)(g.H + 2 * l.Py) * g.Wp * sizeof(__half);
+    l.r_bytes = 2 * (size_t)g.L * g.Hp * l.Wq * sizeof(__half);
+    return l;
+}
+
+// Toeplitz operand of every level, as the kernels want it in shared memory: per level
+// `rows` = Kp - 16 + 128 rows of 16 taps, fp16 hi array then lo array, 8-row groups of 256 bytes =
+// [K half 0: 8 rows x 8 taps][K half 1].  G[p][kk] = w[kk - p + Kp - 16]; taps scaled by 2^t so
+// that the largest is in [512, 1024).  taps: the plan's duplicated table (entry t = offset t - rpad).
 void build_toeplitz(const LevelDesc *lv, int n_levels, const float2 *taps, std::vector<float> &out,
                     ToeplitzTable &tab) {
     out.clear();
@@ -988,12 +813,8 @@ void build_toeplitz(const LevelDesc *lv, int n_levels, const float2 *taps, std::
         const int rpad = lv[i].rpad, Kp = kUT + 2 * rpad, rows = toeplitz_rows(rpad);
         tab.ofs[i] = (int)out.size();
         tab.rows[i] = rows;
-        tab.tscale[i] = 0;
         out.resize(out.size() + (size_t)rows * 16, 0.f);
         const float2 *w = taps + lv[i].tap_ofs;
-#if DOGBLOB_UMMA_F16
-        // fp16 hi | lo arrays: rows of 16 taps (32 bytes), 8-row groups of 256 bytes =
-        // [K half 0: 8 rows x 8 taps][K half 1]; taps scaled by 2^t so that the largest is in [512, 1024)
         float wmax = 0.f;
         for (int t = 0; t <= 2 * rpad; ++t) wmax = std::max(wmax, w[t].x);
         int tsc = 0;
@@ -1011,82 +832,7 @@ void build_toeplitz(const LevelDesc *lv, int n_levels, const float2 *taps, std::
                 hi[o] = h;
                 lo[o] = l;
             }
-#else
-        float *hi = out.data() + tab.ofs[i], *lo = hi + (size_t)rows * 8;
-        for (int p = 0; p < rows; ++p)
-            for (int kk = 0; kk < 8; ++kk) {
-                const int t = kk - p + (Kp - 8);
-                const float v = (t >= 0 && t <= 2 * rpad) ? w[t].x : 0.f;
-                const uint32_t h = host_tf32_rna(v);
-                float hf;
-                std::memcpy(&hf, &h, 4);
-                const uint32_t l = host_tf32_rna(v - hf);
-                float lf;
-                std::memcpy(&lf, &l, 4);
-                const size_t o = (size_t)(p >> 3) * 64 + (kk >> 2) * 32 + (p & 7) * 4 + (kk & 3);
-                hi[o] = hf;
-                lo[o] = lf;
-            }
-#endif
     }
-}
-
-// F16 mode: max |x| of the frame as float bits (non-negative floats order like unsigned integers)
-__global__ void frame_max_kernel(const float *__restrict__ img, int64_t n4, uint32_t *__restrict__ max_bits) {
-    float m = 0.f;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-        const float4 v = __ldg(reinterpret_cast<const float4 *>(img) + i);
-        m = fmaxf(fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))), m);
-    }
-    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(max_bits, __float_as_uint(m));
-}
-bool umma_needs_frame_max() { return DOGBLOB_UMMA_F16 != 0; }
-cudaError_t launch_frame_max(const float *d_img, int64_t n_floats, uint32_t *d_max_bits, cudaStream_t st) {
-    cudaError_t e = cudaMemsetAsync(d_max_bits, 0, sizeof(uint32_t), st);
-    if (e != cudaSuccess) return e;
-    frame_max_kernel<<<148, 256, 0, st>>>(d_img, n_floats / 4, d_max_bits);
-    return cudaGetLastError();
-}
-
-// Cost-balanced static schedule.  CTA b walks positions b, b + n_ctas, ... ; the units are sorted
-// by modelled cost (stages, +1.5 per stage that crosses the image border and goes through the
-// folded cp.async path, +1 per level) and dealt to the CTAs in boustrophedon order, so every CTA
-// gets a similar sum.  rows_axis = valid rows along the convolved axis (H for the row pass, W for
-// the column pass).
-std::vector<int> build_umma_schedule(const ConvGeometry &g, const LevelTable &tbl, bool rows_pass) {
-    const int tiles_c = (rows_pass ? g.Wp : g.Hp) / kUT, tiles_r = (rows_pass ? g.Hp : g.Wp) / kUT;
-    const int n_rows = rows_pass ? g.H : g.W;
-    const int n_g = rows_pass ? tbl.n_levels : tbl.n_groups;
-    const int n_units = tiles_c * tiles_r * n_g;
-    std::vector<std::pair<double, int>> cost(n_units);
-    for (int u = 0; u < n_units; ++u) {
-        const int t = u / tiles_c, tr = t % tiles_r, gi = t / tiles_r;
-        const int lb = rows_pass ? tbl.order[gi] : tbl.group_begin[gi];
-        const int le = rows_pass ? lb + 1 : tbl.group_begin[gi + 1];
-        double c = 0.0;
-        for (int level = lb; level < le; ++level) {
-            const int rpad = tbl.lv[level].rpad;
-            const int n_stage = (kUT + 2 * rpad + kStageRows - 1) / kStageRows;
-            int row0 = tr * kUT - rpad;
-            for (int st = 0; st < n_stage; ++st, row0 += kStageRows)
-                c += (row0 >= 0 && row0 + kStageRows <= n_rows) ? 1.0 : 2.5;
-            c += 1.0;
-        }
-        cost[u] = {c, u};
-    }
-    std::stable_sort(cost.begin(), cost.end(), [](const std::pair<double, int> &x, const std::pair<double, int> &y) {
-        return x.first > y.first;
-    });
-    const int ctas = persistent_ctas(n_units);
-    std::vector<int> sched(n_units);
-    for (int r = 0; r < n_units; ++r) {
-        const int round = r / ctas, k = r % ctas;
-        const int last = std::min(ctas, n_units - round * ctas);        // units in this round
-        const int pos = (round & 1) ? last - 1 - k : k;
-        sched[round * ctas + pos] = cost[r].second;
-    }
-    return sched;
 }
 
 cudaError_t configure_umma_kernels(int device) {
@@ -1100,55 +846,81 @@ cudaError_t configure_umma_kernels(int device) {
     return cudaFuncSetAttribute(umma_pass_kernel<kModeLevels>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
 }
 
-// img[y][x] -> T_i[x][y]: contiguous axis x, convolved axis y, stored transposed
-cudaError_t launch_row_pass_umma(const ConvGeometry &g, const float *d_img, float *d_rows_t,
-                                 const LevelTable &tbl, const ToeplitzTable &ttab,
-                                 const float *d_toep, cudaStream_t st, const RowGate *gate,
-                                 const uint32_t *d_max_bits, const int *d_sched) {
+// frame -> max |x| -> fp16 hi | lo planes with reflected halo rows (d_x: umma_layout().x_bytes)
+cudaError_t launch_prep_umma(const ConvGeometry &g, const float *d_img, void *d_x, uint32_t *d_max_bits,
+                             cudaStream_t st) {
+    const UmmaLayout l = umma_layout(g);
+    cudaError_t e = cudaMemsetAsync(d_max_bits, 0, sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+    frame_max_kernel<<<148, 256, 0, st>>>(d_img, (int64_t)g.H * g.Wp / 4, d_max_bits);
+    const int64_t items = (int64_t)(g.H + 2 * l.Py) * (g.Wp / 8);
+    const int blocks = (int)std::min<int64_t>((items + 255) / 256, 148 * 8);
+    prep_split_kernel<<<blocks, 256, 0, st>>>(d_img, g.Wp, g.H, g.W, g.Wp, l.Py, d_max_bits,
+                                              reinterpret_cast<__half *>(d_x));
+    return cudaGetLastError();
+}
+
+// pass 1: X planes -> R planes (level rows in frame-scaled fp16 hi | lo, halo columns mirrored)
+cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d_r, const LevelTable &tbl,
+                                 const ToeplitzTable &ttab, const float *d_toep, cudaStream_t st,
+                                 const uint32_t *d_max_bits) {
+    const UmmaLayout l = umma_layout(g);
     UmmaArgs a{};
-    a.frame_max_bits = d_max_bits;
-    a.in = d_img; a.in_pitch = g.Wp; a.in_plane = 0; a.n_rows = g.H;
-    a.out = d_rows_t; a.out_pitch = g.Hp; a.out_plane = (int64_t)g.Hp * g.Wp;
-    a.edge = nullptr; a.toep = d_toep;
-    a.tiles_c = g.Wp / kUT; a.tiles_r = g.Hp / kUT;
+    a.tiles_x = g.Wp / kUT; a.tiles_y = g.Hp / kUT;
     a.by_order = 1;                       // independent levels: finest units, longest first
-    a.n_order = tbl.n_levels;
-    a.n_units = a.tiles_c * a.tiles_r * tbl.n_levels;
-    a.sched = gate ? nullptr : d_sched;       // streamed uploads need the tile-row-major order
-    if (gate) {
-        a.gate_word = gate->word; a.gate_base = gate->base;
-        a.gate_rows_per_chunk = gate->rows_per_chunk; a.gate_t_start = gate->t_start;
+    a.n_units = a.tiles_x * a.tiles_y * tbl.n_levels;
+    a.H = g.H; a.W = g.W; a.Hp = g.Hp; a.Wp = g.Wp; a.Py = l.Py; a.Ppad = l.Ppad;
+    a.r_pitch = l.Wq; a.r_plane = (int64_t)g.L * g.Hp * l.Wq;
+    a.r_base = reinterpret_cast<__half *>(d_r);
+    a.frame_max_bits = d_max_bits; a.toep = d_toep;
+    CUtensorMap map_in, map_out;
+    const int xrows = g.H + 2 * l.Py;
+    {   // X planes as {64 x, rows, x-block, hi | lo}; box = 32 rows of one 128-column tile, both planes
+        const cuuint64_t dims[4] = {64, (cuuint64_t)xrows, (cuuint64_t)(g.Wp / 64), 2};
+        const cuuint64_t strides[3] = {(cuuint64_t)g.Wp * 2, 128, (cuuint64_t)xrows * g.Wp * 2};
+        const cuuint32_t box[4] = {64, 32, 2, 2};
+        if (!encode_map(&map_in, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, d_x, dims, strides, box))
+            return cudaErrorInvalidValue;
     }
-    return launch_umma<kModeRows>(a, tbl, ttab, g.max_rpad, st);
+    {   // R planes as {columns up to the last valid one, rows of all levels, hi | lo}: stores beyond W are clipped
+        const cuuint64_t dims[3] = {(cuuint64_t)(l.Ppad + g.W), (cuuint64_t)g.L * g.Hp, 2};
+        const cuuint64_t strides[2] = {(cuuint64_t)l.Wq * 2, (cuuint64_t)a.r_plane * 2};
+        const cuuint32_t box[3] = {64, 128, 1};
+        if (!encode_map(&map_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, d_r, dims, strides, box))
+            return cudaErrorInvalidValue;
+    }
+    return launch_umma<kModeRows>(a, tbl, ttab, g.max_rpad, map_in, map_out, st);
 }
 
-// T_i[x][y] -> D_i^T[x][y]: contiguous axis y, convolved axis x
-cudaError_t launch_col_dog_pass_umma(const ConvGeometry &g, const float *d_rows_t, float *d_dog_t,
-                                     float *d_edge, const LevelTable &tbl, const ToeplitzTable &ttab,
-                                     const float *d_toep, cudaStream_t st, const uint32_t *d_max_bits,
-                                     const int *d_sched) {
+// pass 2: R planes -> DoG slices [L - 1][Hp][Wp] (levels = true: the levels themselves, [L][Hp][Wp])
+cudaError_t launch_col_pass_umma(const ConvGeometry &g, const void *d_r, float *d_out, const LevelTable &tbl,
+                                 const ToeplitzTable &ttab, const float *d_toep, cudaStream_t st,
+                                 const uint32_t *d_max_bits, bool levels) {
+    const UmmaLayout l = umma_layout(g);
     UmmaArgs a{};
-    a.frame_max_bits = d_max_bits;
-    a.sched = d_sched;
-    a.in = d_rows_t; a.in_pitch = g.Hp; a.in_plane = (int64_t)g.Hp * g.Wp; a.n_rows = g.W;
-    a.out = d_dog_t; a.out_pitch = g.Hp; a.out_plane = a.in_plane;
-    a.edge = d_edge; a.toep = d_toep;
-    a.tiles_c = g.Hp / kUT; a.tiles_r = g.Wp / kUT;
-    a.n_units = a.tiles_c * a.tiles_r * tbl.n_groups;
-    return launch_umma<kModeDog>(a, tbl, ttab, g.max_rpad, st);
-}
-
-cudaError_t launch_col_levels_pass_umma(const ConvGeometry &g, const float *d_rows_t, float *d_lev_t,
-                                        const LevelTable &unit_tbl, const ToeplitzTable &ttab,
-                                        const float *d_toep, cudaStream_t st, const uint32_t *d_max_bits) {
-    UmmaArgs a{};
-    a.frame_max_bits = d_max_bits;
-    a.in = d_rows_t; a.in_pitch = g.Hp; a.in_plane = (int64_t)g.Hp * g.Wp; a.n_rows = g.W;
-    a.out = d_lev_t; a.out_pitch = g.Hp; a.out_plane = a.in_plane;
-    a.edge = nullptr; a.toep = d_toep;
-    a.tiles_c = g.Hp / kUT; a.tiles_r = g.Wp / kUT;
-    a.n_units = a.tiles_c * a.tiles_r * unit_tbl.n_groups;
-    return launch_umma<kModeLevels>(a, unit_tbl, ttab, g.max_rpad, st);
+    a.tiles_x = g.Wp / kUT; a.tiles_y = g.Hp / kUT;
+    a.by_order = 0;
+    a.n_units = a.tiles_x * a.tiles_y * tbl.n_groups;
+    a.H = g.H; a.W = g.W; a.Hp = g.Hp; a.Wp = g.Wp; a.Py = l.Py; a.Ppad = l.Ppad;
+    a.r_pitch = l.Wq; a.r_plane = (int64_t)g.L * g.Hp * l.Wq;
+    a.frame_max_bits = d_max_bits; a.toep = d_toep;
+    CUtensorMap map_in, map_out;
+    {   // R planes as {columns, rows of all levels, hi | lo}; box = 128 rows x 64 columns of both planes
+        const cuuint64_t dims[3] = {(cuuint64_t)l.Wq, (cuuint64_t)g.L * g.Hp, 2};
+        const cuuint64_t strides[2] = {(cuuint64_t)l.Wq * 2, (cuuint64_t)a.r_plane * 2};
+        const cuuint32_t box[3] = {64, 128, 2};
+        if (!encode_map(&map_in, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, d_r, dims, strides, box))
+            return cudaErrorInvalidValue;
+    }
+    {   // output planes {W valid columns, rows of all planes}; box = 128 rows x 32 floats
+        const cuuint64_t dims[2] = {(cuuint64_t)g.W, (cuuint64_t)g.L * g.Hp};
+        const cuuint64_t strides[1] = {(cuuint64_t)g.Wp * 4};
+        const cuuint32_t box[2] = {32, 128};
+        if (!encode_map(&map_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d_out, dims, strides, box))
+            return cudaErrorInvalidValue;
+    }
+    if (levels) return launch_umma<kModeLevels>(a, tbl, ttab, g.max_rpad, map_in, map_out, st);
+    return launch_umma<kModeDog>(a, tbl, ttab, g.max_rpad, map_in, map_out, st);
 }
 
 }  // namespace dogblob
