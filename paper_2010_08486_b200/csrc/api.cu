@@ -1,5 +1,6 @@
 // C ABI of libdogblob_b200 (see include/dogblob_b200.h).
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -78,6 +79,8 @@ struct dogblob_plan {
     bool use_umma = false;   // plan-time choice of the convolution engine (see dogblob_plan_create)
     ToeplitzTable toeplitz;  // tensor-core passes: prebuilt Toeplitz operands of every level
     float *d_toeplitz = nullptr;
+    int *d_umma_sched = nullptr;   // tensor-core column pass: unit of (slot, CTA), -1 = none (see plan_umma_schedule)
+    int umma_sched_slots = 0, umma_sched_ctas = 0;
     double *d_slice_sigma = nullptr;
     float *d_sigma_f32 = nullptr;
     // workspace layout (bytes from the workspace base)
@@ -138,6 +141,106 @@ int choose_groups(int tiles, int L, double slots = 2.0 * 148.0) {
         const double score = eff - 0.004 * G;
         if (score > best_score) { best_score = score; best = G; }
     }
+    return best;
+}
+
+// Tensor-core column pass: level groups and a static schedule for `ctas` persistent CTAs.
+// A unit = (tile, group); group g also computes the first level of group g + 1 (the DoG slice
+// between them needs both), so every boundary costs one duplicated level.  With equal groups the
+// 64 G units of a 1024^2 frame deal out as 4 / 4 / 4 / 3 per CTA: the kernel ends with its slowest
+// CTA, 4 equal units.  Unequal groups pack better: a few SMALL groups at the fine end of the ladder
+// (cheap levels: cheap duplicates) give the longest-processing-time-first assignment small units to
+// level the CTAs with.  Cost of a level = its k-steps + a fixed part (commits, drain hand-over).
+struct UmmaSchedule {
+    std::vector<int> begin;      // group boundaries
+    std::vector<int> flat;       // [slot][cta] -> unit (group * tiles + tile) or -1
+    int slots = 0;
+    double makespan = 0.0, mean = 0.0;
+};
+UmmaSchedule plan_umma_schedule(const std::vector<LevelDesc> &lv, int tiles, int ctas, double level_fixed,
+                                int force_groups) {
+    const int L = (int)lv.size();
+    std::vector<double> c(L), pre(L + 1, 0.0);
+    for (int i = 0; i < L; ++i) {
+        c[i] = (128 + 2 * lv[i].rpad) / 16 + level_fixed;
+        pre[i + 1] = pre[i] + c[i];
+    }
+    // cost of group q of a partition: its levels plus the first level of the next group
+    auto group_costs = [&](const std::vector<int> &begin, std::vector<double> &gc) {
+        const int G = (int)begin.size() - 1;
+        gc.resize(G);
+        for (int q = 0; q < G; ++q) gc[q] = pre[std::min(begin[q + 1] + (q + 1 < G ? 1 : 0), L)] - pre[begin[q]];
+    };
+    // makespan of the longest-processing-time-first assignment (units of a group are equal: deal
+    // them out group by group, largest first, always to the least loaded CTA)
+    std::vector<double> heap;
+    auto lpt = [&](const std::vector<double> &gc) {
+        std::vector<double> sorted(gc);
+        std::sort(sorted.begin(), sorted.end(), std::greater<double>());
+        heap.assign(ctas, 0.0);          // min-heap on the load
+        auto cmp = std::greater<double>();
+        for (double v : sorted)
+            for (int t = 0; t < tiles; ++t) {
+                std::pop_heap(heap.begin(), heap.end(), cmp);
+                heap.back() += v;
+                std::push_heap(heap.begin(), heap.end(), cmp);
+            }
+        return *std::max_element(heap.begin(), heap.end());
+    };
+    UmmaSchedule best;
+    best.makespan = 1e300;
+    uint32_t rng = 12345u;
+    std::vector<double> gc;
+    const int g_hi = std::min(L - 1, std::max(2, std::min(14, 4 * ctas / std::max(1, tiles) + 2)));
+    for (int G = 1; G <= g_hi; ++G) {
+        if (force_groups > 0 && G != std::min(force_groups, L - 1)) continue;
+        std::vector<int> begin(G + 1, 0);
+        begin[G] = L;
+        for (int g = 1; g < G; ++g) {             // start from groups of equal cost
+            int b = (int)(std::lower_bound(pre.begin(), pre.end(), pre[L] * g / G) - pre.begin());
+            begin[g] = std::min(std::max(b, begin[g - 1] + 1), L - (G - g));
+        }
+        group_costs(begin, gc);
+        double cur = lpt(gc);
+        for (int it = 0; G > 1 && it < 400; ++it) {       // hill climbing on the boundaries
+            rng = rng * 1664525u + 1013904223u;
+            const int g = 1 + (int)((rng >> 8) % (uint32_t)(G - 1));
+            const int d = ((rng >> 4) & 1) ? 1 : -1;
+            std::vector<int> nb(begin);
+            nb[g] += d * (1 + (int)((rng >> 5) & 1));
+            if (!(nb[g - 1] < nb[g] && nb[g] < nb[g + 1])) continue;
+            group_costs(nb, gc);
+            const double v = lpt(gc);
+            if (v <= cur) { cur = v; begin.swap(nb); }
+        }
+        if (cur < best.makespan * (1.0 - 1e-9)) {
+            best.makespan = cur;
+            best.begin = begin;
+        }
+    }
+    // the assignment itself, CTA by CTA
+    const int G = (int)best.begin.size() - 1;
+    group_costs(best.begin, gc);
+    std::vector<int> order(G);
+    for (int q = 0; q < G; ++q) order[q] = q;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return gc[a] > gc[b]; });
+    std::vector<double> load(ctas, 0.0);
+    std::vector<std::vector<int>> mine(ctas);
+    for (int q : order)
+        for (int t = 0; t < tiles; ++t) {
+            const int b = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+            load[b] += gc[q];
+            mine[b].push_back(q * tiles + t);
+        }
+    best.slots = 0;
+    for (auto &v : mine) best.slots = std::max(best.slots, (int)v.size());
+    best.flat.assign((size_t)best.slots * ctas, -1);
+    double sum = 0.0;
+    for (int b = 0; b < ctas; ++b) {
+        sum += load[b];
+        for (size_t k = 0; k < mine[b].size(); ++k) best.flat[k * ctas + b] = mine[b][k];
+    }
+    best.mean = sum / ctas;
     return best;
 }
 
@@ -258,20 +361,37 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
     for (int i = 0; i <= g.G; ++i) plan->table.group_begin[i] = group_begin[i];
     plan->unit_table.n_groups = n_levels;
     for (int i = 0; i <= n_levels; ++i) plan->unit_table.group_begin[i] = unit[i];
-    // tensor-core column pass: one persistent CTA per SM walks (tile, group) units round robin;
-    // a level costs (128 + 2 rpad) / 16 stages = n_mid + 9 (+1 for its drain)
-    int G_umma = choose_groups(tiles, n_levels, 148.0);
-    if (const char *env = std::getenv("DOGBLOB_UMMA_GROUPS")) G_umma = std::max(1, std::atoi(env));
+    // tensor-core column pass: one persistent CTA per SM, (tile, group) units on a static schedule
+    UmmaSchedule usched;
     {
-        static const double fixed_umma = [] {
-            const char *e = std::getenv("DOGBLOB_UMMA_LEVEL_COST");
-            return e ? std::atof(e) : 10.0;
-        }();
-        const std::vector<int> ub = balance_groups(plan->levels, G_umma, fixed_umma);
-        G_umma = (int)ub.size() - 1;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        const char *ec = std::getenv("DOGBLOB_UMMA_LEVEL_COST");       // plan time only
+        const char *eg = std::getenv("DOGBLOB_UMMA_GROUPS");
+        usched = plan_umma_schedule(plan->levels, tiles, std::min(sms, tiles * std::max(1, n_levels - 1)),
+                                    ec ? std::atof(ec) : 6.0, eg ? std::atoi(eg) : 0);
+        const int G_umma = (int)usched.begin.size() - 1;
         plan->umma_table = plan->table;
         plan->umma_table.n_groups = G_umma;
-        for (int i = 0; i <= G_umma; ++i) plan->umma_table.group_begin[i] = ub[i];
+        for (int i = 0; i <= G_umma; ++i) plan->umma_table.group_begin[i] = usched.begin[i];
+        plan->umma_sched_slots = usched.slots;
+        plan->umma_sched_ctas = (int)(usched.flat.size() / std::max(1, usched.slots));
+        if (std::getenv("DOGBLOB_UMMA_PROF"))
+            fprintf(stderr, "umma schedule: %d groups, %d slots, makespan %.1f vs mean %.1f k-step units\n", G_umma,
+                    usched.slots, usched.makespan, usched.mean);
+        if (std::getenv("DOGBLOB_UMMA_PROF_CTAS")) {
+            fprintf(stderr, "   groups:");
+            for (int i = 0; i <= G_umma; ++i) fprintf(stderr, " %d", usched.begin[i]);
+            fprintf(stderr, "\n   units per CTA (group ids):");
+            for (int b = 0; b < plan->umma_sched_ctas; ++b) {
+                fprintf(stderr, " [");
+                for (int k = 0; k < usched.slots; ++k)
+                    if (usched.flat[(size_t)k * plan->umma_sched_ctas + b] >= 0)
+                        fprintf(stderr, "%d", usched.flat[(size_t)k * plan->umma_sched_ctas + b] / tiles);
+                fprintf(stderr, "]");
+            }
+            fprintf(stderr, "\n");
+        }
     }
     PLAN_CUDA(cudaMalloc(&plan->d_taps, table.size() * sizeof(float2)));
     PLAN_CUDA(cudaMalloc(&plan->d_slice_sigma, n_levels * sizeof(double)));
@@ -300,6 +420,9 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
         build_toeplitz(plan->levels.data(), n_levels, table.data(), toep, plan->toeplitz);
         PLAN_CUDA(cudaMalloc(&plan->d_toeplitz, toep.size() * sizeof(float)));
         PLAN_CUDA(cudaMemcpy(plan->d_toeplitz, toep.data(), toep.size() * sizeof(float),
+                             cudaMemcpyHostToDevice));
+        PLAN_CUDA(cudaMalloc(&plan->d_umma_sched, usched.flat.size() * sizeof(int)));
+        PLAN_CUDA(cudaMemcpy(plan->d_umma_sched, usched.flat.data(), usched.flat.size() * sizeof(int),
                              cudaMemcpyHostToDevice));
     }
     PLAN_CUDA(configure_conv_kernels(device));
@@ -333,6 +456,7 @@ void dogblob_plan_destroy(dogblob_plan *plan) {
     DeviceGuard guard(plan->device);
     cudaFree(plan->d_taps);
     cudaFree(plan->d_toeplitz);
+    cudaFree(plan->d_umma_sched);
     cudaFree(plan->d_slice_sigma);
     cudaFree(plan->d_sigma_f32);
     delete plan;
@@ -380,7 +504,8 @@ static cudaError_t col_dog_pass_any(const dogblob_plan *plan, void *d_workspace,
     float *dog = reinterpret_cast<float *>(ws + plan->off_dog_t);
     if (plan->use_umma)
         return launch_col_pass_umma(plan->geo, ws + plan->off_rows_t, dog, plan->umma_table, plan->toeplitz,
-                                    plan->d_toeplitz, st, frame_max_word(plan, d_workspace), false);
+                                    plan->d_toeplitz, st, frame_max_word(plan, d_workspace), false,
+                                    plan->d_umma_sched, plan->umma_sched_slots, plan->umma_sched_ctas);
     return launch_col_dog_pass(plan->geo, reinterpret_cast<const float *>(ws + plan->off_rows_t), dog,
                                reinterpret_cast<float *>(ws + plan->off_edge), plan->table, plan->d_taps, st);
 }
@@ -578,7 +703,7 @@ int dogblob_scale_space(const dogblob_plan *plan, const float *d_image, void *d_
     DB_CUDA(row_pass_any(plan, d_image, d_workspace, st, nullptr));
     if (plan->use_umma)
         DB_CUDA(launch_col_pass_umma(g, ws + plan->off_rows_t, lev, plan->unit_table, plan->toeplitz,
-                                     plan->d_toeplitz, st, frame_max_word(plan, d_workspace), true));
+                                     plan->d_toeplitz, st, frame_max_word(plan, d_workspace), true, nullptr, 0, 0));
     else
         DB_CUDA(launch_col_levels_pass(g, reinterpret_cast<const float *>(ws + plan->off_rows_t), lev,
                                        plan->unit_table, plan->d_taps, st));

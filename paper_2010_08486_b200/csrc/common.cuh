@@ -175,7 +175,8 @@ cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d
 // DoG slices [L - 1][Hp][Wp] in image orientation (levels = true: the L levels themselves)
 cudaError_t launch_col_pass_umma(const ConvGeometry &g, const void *d_r, float *d_out, const LevelTable &tbl,
                                  const ToeplitzTable &ttab, const float *d_toep, cudaStream_t st,
-                                 const uint32_t *d_max_bits, bool levels);
+                                 const uint32_t *d_max_bits, bool levels, const int *d_sched, int sched_slots,
+                                 int sched_ctas);
 cudaError_t launch_untranspose(const float *d_src_t, int planes, int Hp, int Wp, int H, int W,
                                float *d_dst, cudaStream_t st);
 cudaError_t launch_dog_from_levels(int L, int64_t plane_elems, const float *d_levels,

@@ -60,10 +60,23 @@ constexpr int kThreads = 384;             // 12 warps
 constexpr int kDrainWarp0 = 4;            // warps 4..11 drain
 constexpr int kDrainWarps = 8;
 constexpr int kAccCols = 128;
-constexpr int kStageBytes1 = 16384;       // pass 1: [hi | lo][2 x-blocks][32 rows][128 B]
+#ifndef DOGBLOB_UMMA_ROWS1
+#define DOGBLOB_UMMA_ROWS1 64
+#endif
+constexpr int kRowsPerStage1 = DOGBLOB_UMMA_ROWS1;             // pass 1: input rows per data stage (16 per k-step)
+constexpr int kStageBytes1 = 512 * kRowsPerStage1;             // pass 1: [hi | lo][2 x-blocks][rows][128 B]
 constexpr int kStageBytes2 = 32768;       // pass 2: [hi | lo][128 rows][128 B]
-constexpr int kStagingBytes = 32768;      // drain staging: one 16 KB box per column half
+constexpr int kStagingBytes1 = 65536;     // pass 1 drain staging: two 16 KB boxes per column half (double buffered)
+constexpr int kStagingBytes2 = 32768;     // pass 2 drain staging: one 16 KB box per column half
 constexpr int kMaxStages = 8;
+#ifndef DOGBLOB_UMMA_TOEP1
+#define DOGBLOB_UMMA_TOEP1 2
+#endif
+#ifndef DOGBLOB_UMMA_TOEP2
+#define DOGBLOB_UMMA_TOEP2 2
+#endif
+constexpr int kToepBuffers1 = DOGBLOB_UMMA_TOEP1, kToepBuffers2 = DOGBLOB_UMMA_TOEP2;   // Toeplitz ring depth per pass
+constexpr int kMaxToepBuffers = 4;
 constexpr unsigned long long kWaitLimitNs = 20ull * 1000 * 1000 * 1000;   // deadlock trap (20 s)
 
 enum UmmaMode { kModeRows = 0, kModeDog = 1, kModeLevels = 2 };
@@ -71,6 +84,9 @@ enum UmmaMode { kModeRows = 0, kModeDog = 1, kModeLevels = 2 };
 struct UmmaArgs {
     int tiles_x, tiles_y;   // tiles along x (contiguous) and y
     int n_units;            // tiles * (levels | level groups)
+    const int *sched;       // static schedule: unit of (slot, CTA) or -1; nullptr = round robin over n_units
+    int n_sched;            // slots * CTAs (round robin: n_units)
+    int n_ctas;             // CTAs the schedule was made for (0: one per SM, at most n_units)
     int by_order;           // units are single levels in tbl.order[] (pass 1) or groups (pass 2)
     int H, W, Hp, Wp;
     int Py;                 // halo rows above / below the frame in the X planes
@@ -81,8 +97,10 @@ struct UmmaArgs {
     const uint32_t *frame_max_bits;   // float bits of the frame's max |x| (device word)
     const float *toep;      // prebuilt Toeplitz arrays of every level (hi | lo), see build_toeplitz
     int toep_bytes;         // bytes of one Toeplitz buffer in shared memory (widest level, hi + lo)
+    int staging_off;        // byte offset of the drain staging (1 KB aligned; the data stages follow it)
     int stages;             // data stages that fit in shared memory
     unsigned long long *prof;   // DOGBLOB_UMMA_PROF: per-role cycle counters (see launch_umma)
+    int debug;              // DOGBLOB_UMMA_DEBUG: timing experiments (results are garbage), see launch_umma
 };
 
 // ---- PTX wrappers -------------------------------------------------------------------
@@ -204,6 +222,34 @@ __device__ __forceinline__ void umma_f16_triple_ss(uint32_t d_main, uint32_t d_s
           "r"(b_upper), "r"(idesc), "r"(acc)
         : "memory");
 }
+// single-thread forms (the caller is the one elected thread of the issuer warp)
+__device__ __forceinline__ void umma_f16_triple_ss_1t(uint32_t d_main, uint32_t d_small, uint32_t a_hi,
+                                                      uint32_t a_lo, uint32_t b_hi, uint32_t b_lo,
+                                                      uint32_t a_upper, uint32_t b_upper, uint32_t idesc,
+                                                      uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t.reg .b64 a0, a1, b0, b1;\n\t"
+        "setp.ne.b32 p, %9, 0;\n\t"
+        "setp.eq.b32 q, 0, 0;\n\t"
+        "mov.b64 a0, {%2, %6};\n\t"
+        "mov.b64 a1, {%3, %6};\n\t"
+        "mov.b64 b0, {%4, %7};\n\t"
+        "mov.b64 b1, {%5, %7};\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a0, b0, %8, p;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], a0, b1, %8, p;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%1], a1, b0, %8, q;\n\t}"
+        ::"r"(d_main), "r"(d_small), "r"(a_hi), "r"(a_lo), "r"(b_hi), "r"(b_lo), "r"(a_upper),
+          "r"(b_upper), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_1t(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}" : "=r"(ok));
+    return ok != 0;
+}
 __device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t"
@@ -264,13 +310,15 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
 // Shared-memory matrix descriptors (cute::UMMA::SmemDescriptor):
 //   bits [0,14) start address >> 4    [16,30) leading byte offset >> 4    [32,46) stride byte
 //   offset >> 4    [46,48) version = 1    [61,64) layout type (0 none, 2 SWIZZLE_128B)
-// Toeplitz array (K-major, no swizzle): 8-row group g at g * 256 bytes =
-//   [K half 0: 8 rows x 16 B][K half 1: 8 rows x 16 B]  -> LBO = 128 (K halves), SBO = 256 (row groups)
+// Toeplitz array (K-major, no swizzle), COMPACT: the operand rows are indexed by the REVERSED output
+// n' = 127 - n, so T'[n'][k] = w[k + n' - 127] depends on k + n' only and the K half 1 of row n' is
+// the K half 0 of row n' + 8: one 16-byte chunk per row, C[r][e] = w[r + e - 127], 8-row groups at
+// SBO = 128 and the second K half at LBO = 128 (the core matrices overlap in memory).
 constexpr uint32_t kToepLowLbo = (128u >> 4) << 16;
-constexpr uint32_t kToepUpper = (256u >> 4) | (1u << 14);
+constexpr uint32_t kToepUpper = (128u >> 4) | (1u << 14);
 // pass-1 data (MN-major, SWIZZLE_128B): x-block of 64 at LBO = 4096 (32 rows x 128 B), 8-row
 // k group at SBO = 1024
-constexpr uint32_t kData1LowLbo = (4096u >> 4) << 16;
+constexpr uint32_t kData1LowLbo = ((128u * kRowsPerStage1) >> 4) << 16;
 constexpr uint32_t kData1Upper = (1024u >> 4) | (1u << 14) | (2u << 29);
 // pass-2 data (K-major, SWIZZLE_128B): 8-row group at SBO = 1024, LBO unused
 constexpr uint32_t kData2LowLbo = 1u << 16;
@@ -329,7 +377,7 @@ __device__ __forceinline__ Unit decode_unit(int u, const UmmaArgs &a, const Leve
 
 struct SharedCtl {
     unsigned long long data_full[kMaxStages], data_empty[kMaxStages];
-    unsigned long long toep_full[2], toep_empty[2];
+    unsigned long long toep_full[kMaxToepBuffers], toep_empty[kMaxToepBuffers];
     unsigned long long acc_full[2], acc_empty[2];
     uint32_t tmem_base;
     uint32_t pad[3];
@@ -340,28 +388,34 @@ template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                  const __grid_constant__ ToeplitzTable ttab, const __grid_constant__ CUtensorMap map_in,
-                 const __grid_constant__ CUtensorMap map_out) {
+                 const __grid_constant__ CUtensorMap map_out, const __grid_constant__ CUtensorMap map_aux) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     SharedCtl *ctl = reinterpret_cast<SharedCtl *>(smem_raw);
     unsigned char *toep = smem_raw + 1024;                               // [buffer 2][hi | lo]
-    unsigned char *staging = toep + 2 * (size_t)a.toep_bytes;            // [column half 2][16 KB box]
-    unsigned char *data = staging + kStagingBytes;                       // [stage][...]
+    unsigned char *staging = smem_raw + a.staging_off;                   // [column half 2][16 KB box (x 2 in pass 1)]
     constexpr bool kRows = MODE == kModeRows;
+    constexpr int NT = kRows ? kToepBuffers1 : kToepBuffers2;
+    unsigned char *data = staging + (kRows ? kStagingBytes1 : kStagingBytes2);     // [stage][...]
     constexpr int kStageBytes = kRows ? kStageBytes1 : kStageBytes2;
-    constexpr int kStepsPerStage = kRows ? 2 : 4;                         // k-steps of 16 per data stage
+    constexpr int kStepsPerStage = kRows ? kRowsPerStage1 / 16 : 4;                         // k-steps of 16 per data stage
     const int S = a.stages;
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // the shuffle makes the warp index provably warp-uniform: the role branches below are then uniform
+    // control flow and the issuer's descriptor arithmetic can live in uniform registers
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
 
+    if (a.prof != nullptr && threadIdx.x == 0) atomicMin(a.prof + 16, globaltimer_ns());      // first CTA in
     if (threadIdx.x == 0) {
         if (smem_u32(smem_raw) & 1023u) __trap();                         // swizzled boxes need 1 KB alignment
         for (int s = 0; s < S; ++s) {
             mbar_init(smem_u32(&ctl->data_full[s]), 1);
             mbar_init(smem_u32(&ctl->data_empty[s]), 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < NT; ++b) {
             mbar_init(smem_u32(&ctl->toep_full[b]), 1);
             mbar_init(smem_u32(&ctl->toep_empty[b]), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
             mbar_init(smem_u32(&ctl->acc_full[b]), 1);
             mbar_init(smem_u32(&ctl->acc_empty[b]), kDrainWarps);
         }
@@ -377,13 +431,21 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
     constexpr uint32_t tmem = 0u;
 
     if (warp == 0) {
-        // ================= issuer (whole warp, one elected lane issues) =================
+        // ================= issuer (ONE elected thread runs the whole loop) =================
         // Every MMA is M = 128 x K = 16; the tensor pipe spends 64 cycles on it for any N <= 128
         // (measured, tools/ubench_umma_ss.cu), so pass 2's band trimming (k-step m0 only feeds
         // outputs n in [m0 - 2 rpad, m0 + 15]) saves shared-memory reads, not pipe time.
-        uint32_t stage_it = 0, lvl_it = 0;
-        RoleClock rc(a.prof != nullptr && lane == 0);
-        for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+        uint32_t lvl_it = 0, sl = 0, sl_par = 0;            // data stage slot and its phase parity
+        uint32_t tb = 0, tb_par = 0;                        // Toeplitz buffer and its phase parity
+        RoleClock rc(a.prof != nullptr);
+        if (a.prof != nullptr && lane == 0) {
+            atomicMax(a.prof + 17, globaltimer_ns());      // last CTA reaches its issuer loop
+            atomicMin(a.prof + 20, globaltimer_ns());      // first CTA reaches it
+        }
+        if (elect_one())
+        for (int ui = blockIdx.x; ui < a.n_sched; ui += gridDim.x) {
+            const int u = a.sched ? __ldg(a.sched + ui) : ui;
+            if (u < 0) continue;
             const Unit un = decode_unit(u, a, tbl, MODE);
             for (int level = un.lb; level < un.le; ++level, ++lvl_it) {
                 const int rpad2 = 2 * tbl.lv[level].rpad;
@@ -392,39 +454,39 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                 const int n_stage = (n_k + kStepsPerStage - 1) / kStepsPerStage;
                 const uint32_t b = lvl_it & 1, par = (lvl_it >> 1) & 1;
                 rc.lap(3);
-                mbar_wait(smem_u32(&ctl->toep_full[b]), par, 1);
+                mbar_wait(smem_u32(&ctl->toep_full[tb]), tb_par, 1);
                 rc.lap(0);
                 mbar_wait(smem_u32(&ctl->acc_empty[b]), par ^ 1, 2);
                 rc.lap(1);
                 tc_fence_after();
-                // low descriptor word of the Toeplitz window of k-step 0 (row Kp - 16); every k-step
-                // moves the window up by 16 rows = two 256-byte groups = 32 descriptor units
-                const uint32_t t_hi = smem_u32(toep + (size_t)b * a.toep_bytes);
-                const uint32_t lo_off = (uint32_t)ttab.rows[level] * 2u;            // hi -> lo array (32 B per row)
-                const uint32_t win0 = ((t_hi + (uint32_t)(Kp - 16) * 32u) >> 4) | kToepLowLbo;
+                // low descriptor word of the Toeplitz window of k-step 0 (row 0); every k-step moves
+                // the window down by 16 rows of 16 bytes = 16 descriptor units
+                const uint32_t t_hi = smem_u32(toep + (size_t)tb * a.toep_bytes);
+                // hi -> lo array (16 B per row); pass 2 never reads the last 112 rows and leaves them out
+                const uint32_t lo_off = kRows ? (uint32_t)ttab.rows[level] : (uint32_t)(Kp + 8);
+                const uint32_t win0 = (t_hi >> 4) | kToepLowLbo;
                 const uint32_t d_main = tmem + b * 2 * kAccCols, d_small = d_main + kAccCols;
                 for (int st = 0; st < n_stage; ++st) {
-                    const uint32_t g = stage_it + (uint32_t)st, sl = g % (uint32_t)S;
                     rc.lap(3);
-                    mbar_wait(smem_u32(&ctl->data_full[sl]), (g / (uint32_t)S) & 1, 3);
+                    mbar_wait(smem_u32(&ctl->data_full[sl]), sl_par, 3);
                     rc.lap(2);
                     tc_fence_after();
                     const uint32_t sbase = smem_u32(data + (size_t)sl * kStageBytes);
                     // pass 2: the last stage is shifted left so that it ends exactly at Kp (no read
                     // beyond the halo); k-step j then sits (16 j - first_k) columns into the box
-                    const int first_k = kRows ? 32 * st : (st == n_stage - 1 ? Kp - 64 : 64 * st);
+                    const int first_k = kRows ? kRowsPerStage1 * st : (st == n_stage - 1 ? Kp - 64 : 64 * st);
                     const int j0 = kStepsPerStage * st;
                     const int j1 = min(n_k, j0 + kStepsPerStage);
 #pragma unroll
                     for (int q = 0; q < kStepsPerStage; ++q) {
                         const int j = j0 + q;
-                        if (j < j1) {
+                        if (j < j1 && !(a.debug & 8)) {
                             const int m0 = 16 * j;
-                            const uint32_t win = win0 - 32u * (uint32_t)j;
+                            const uint32_t win = win0 + 16u * (uint32_t)j;
                             if (kRows) {
                                 // A = Toeplitz window, B = 16 image rows of the stage (2 KB per k-step)
                                 const uint32_t bd = ((sbase + (uint32_t)(m0 - first_k) * 128u) >> 4) | kData1LowLbo;
-                                umma_f16_triple_ss(d_main, d_small, win, win + lo_off, bd, bd + (8192u >> 4),
+                                umma_f16_triple_ss_1t(d_main, d_small, win, win + lo_off, bd, bd + ((256u * kRowsPerStage1) >> 4),
                                                    kToepUpper, kData1Upper, instr_desc_f16(kUT, kUT, 1),
                                                    j > 0);
                             } else {
@@ -433,48 +495,63 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                                 const int ns = j == 0 ? 0 : (max(0, m0 - rpad2) & ~15);
                                 const int ne = j == 0 ? kUT : min(kUT, m0 + 16);
                                 const uint32_t ad = ((sbase + (uint32_t)(m0 - first_k) * 2u) >> 4) | kData2LowLbo;
-                                const uint32_t bw = win + 2u * (uint32_t)ns;
-                                umma_f16_triple_ss(d_main + ns, d_small + ns, ad, ad + (16384u >> 4), bw,
+                                // reversed operand rows: outputs [ns, ne) are rows / accumulator columns
+                                // [128 - ne, 128 - ns)
+                                const uint32_t bw = win + (uint32_t)(kUT - ne);
+                                umma_f16_triple_ss_1t(d_main + (kUT - ne), d_small + (kUT - ne), ad, ad + (16384u >> 4), bw,
                                                    bw + lo_off, kData2Upper, kToepUpper,
                                                    instr_desc_f16(kUT, ne - ns, 0), j > 0);
                             }
                         }
                     }
-                    umma_commit_elect(smem_u32(&ctl->data_empty[sl]));
+                    // A commit stalls the issuing thread (~250 cycles, the tensor pipe runs dry behind
+                    // it: tools/ubench_umma_commit.cu), hence stages of 4 k-steps in both passes.
+                    // (Releasing pass-1 stages of 2 k-steps in pairs was slower than one by one.)
+                    umma_commit_1t(smem_u32(&ctl->data_empty[sl]));
+                    if (++sl == (uint32_t)S) { sl = 0; sl_par ^= 1u; }
                 }
-                stage_it += (uint32_t)n_stage;
-                umma_commit_elect(smem_u32(&ctl->toep_empty[b]));
-                umma_commit_elect(smem_u32(&ctl->acc_full[b]));
+                umma_commit_1t(smem_u32(&ctl->toep_empty[tb]));
+                umma_commit_1t(smem_u32(&ctl->acc_full[b]));
+                if (++tb == (uint32_t)NT) { tb = 0; tb_par ^= 1u; }
             }
         }
+        __syncwarp();
+        if (lane != 0) rc.on = false;      // lane 0 is the elected thread in practice; only it reports
         rc.lap(3);
         rc.flush(a.prof, 0);
+        if (rc.on) {
+            atomicMax(a.prof + 18, globaltimer_ns());      // last issuer loop ends
+            atomicMin(a.prof + 21, globaltimer_ns());      // first one ends
+        }
         if (rc.on) {        // slowest / fastest CTA (issuer's whole life)
             const unsigned long long tot = rc.acc[0] + rc.acc[1] + rc.acc[2] + rc.acc[3];
+            a.prof[32 + blockIdx.x] = tot;
             atomicMax(a.prof + 14, tot);
             atomicMin(a.prof + 15, tot);
         }
     } else if (warp == 1) {
         // ================= loader: one TMA box per data stage =================
-        uint32_t g = 0;
-        RoleClock rc(a.prof != nullptr && lane == 0);
-        if (lane == 0) {
-            for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+        uint32_t sl = 0, sl_par = 1;                       // waits on `empty` start one phase ahead
+        RoleClock rc(a.prof != nullptr);
+        if (elect_one()) {
+            for (int ui = blockIdx.x; ui < a.n_sched; ui += gridDim.x) {
+            const int u = a.sched ? __ldg(a.sched + ui) : ui;
+            if (u < 0) continue;
                 const Unit un = decode_unit(u, a, tbl, MODE);
                 for (int level = un.lb; level < un.le; ++level) {
                     const int rpad = tbl.lv[level].rpad;
                     const int Kp = kUT + 2 * rpad;
                     const int n_stage = (Kp / 16 + kStepsPerStage - 1) / kStepsPerStage;
-                    for (int st = 0; st < n_stage; ++st, ++g) {
-                        const uint32_t sl = g % (uint32_t)S;
+                    for (int st = 0; st < n_stage; ++st, sl = (sl + 1 == (uint32_t)S ? 0 : sl + 1), sl_par ^= (sl == 0)) {
                         rc.lap(1);
-                        mbar_wait(smem_u32(&ctl->data_empty[sl]), ((g / (uint32_t)S) & 1) ^ 1, 7);
+                        mbar_wait(smem_u32(&ctl->data_empty[sl]), sl_par, 7);
                         rc.lap(0);
                         const uint32_t bar = smem_u32(&ctl->data_full[sl]);
                         const uint32_t dst = smem_u32(data + (size_t)sl * kStageBytes);
+                        if (a.debug & 1) { mbar_arrive(bar); continue; }
                         mbar_expect_tx(bar, kStageBytes);
                         if (kRows)      // X planes: {64 x, rows, x-block, hi | lo}; rows beyond the planes read as 0
-                            tma_load_4d(dst, &map_in, 0, a.Py + un.y0 - rpad + 32 * st, un.x0 / 64, 0, bar);
+                            tma_load_4d(dst, &map_in, 0, a.Py + un.y0 - rpad + kRowsPerStage1 * st, un.x0 / 64, 0, bar);
                         else            // R planes: {columns, rows of all levels, hi | lo}
                             tma_load_3d(dst, &map_in,
                                         a.Ppad + un.x0 - rpad + (st == n_stage - 1 ? Kp - 64 : 64 * st),
@@ -484,21 +561,33 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
             }
         }
         __syncwarp();
+        if (lane != 0) rc.on = false;
         rc.lap(1);
         rc.flush(a.prof, 4);
     } else if (warp == 2) {
-        // ================= Toeplitz copier: prebuilt hi | lo arrays, one bulk copy per level ========
-        uint32_t lvl_it = 0;
-        if (lane == 0) {
-            for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+        // ================= Toeplitz copier: prebuilt hi | lo arrays, bulk copies per level ========
+        uint32_t tb = 0, tb_par = 1;                       // waits on `empty` start one phase ahead
+        if (elect_one()) {
+            for (int ui = blockIdx.x; ui < a.n_sched; ui += gridDim.x) {
+            const int u = a.sched ? __ldg(a.sched + ui) : ui;
+            if (u < 0) continue;
                 const Unit un = decode_unit(u, a, tbl, MODE);
-                for (int level = un.lb; level < un.le; ++level, ++lvl_it) {
-                    const uint32_t b = lvl_it & 1, par = (lvl_it >> 1) & 1;
-                    mbar_wait(smem_u32(&ctl->toep_empty[b]), par ^ 1, 4);
-                    const uint32_t bytes = (uint32_t)ttab.rows[level] * 64u;     // hi + lo
-                    const uint32_t bar = smem_u32(&ctl->toep_full[b]);
-                    mbar_expect_tx(bar, bytes);
-                    bulk_copy_g2s(smem_u32(toep + (size_t)b * a.toep_bytes), a.toep + ttab.ofs[level], bytes, bar);
+                for (int level = un.lb; level < un.le; ++level) {
+                    mbar_wait(smem_u32(&ctl->toep_empty[tb]), tb_par, 4);
+                    const uint32_t bar = smem_u32(&ctl->toep_full[tb]);
+                    const uint32_t dst = smem_u32(toep + (size_t)tb * a.toep_bytes);
+                    if (++tb == (uint32_t)NT) { tb = 0; tb_par ^= 1u; }
+                    if (a.debug & 16) { mbar_arrive(bar); continue; }
+                    const uint32_t rows = (uint32_t)ttab.rows[level];
+                    if (kRows) {
+                        mbar_expect_tx(bar, rows * 32u);                              // hi + lo
+                        bulk_copy_g2s(dst, a.toep + ttab.ofs[level], rows * 32u, bar);
+                    } else {                                                        // all but the last 112 rows of each array
+                        const uint32_t part = (rows - 112u) * 16u;
+                        mbar_expect_tx(bar, 2u * part);
+                        bulk_copy_g2s(dst, a.toep + ttab.ofs[level], part, bar);
+                        bulk_copy_g2s(dst + part, a.toep + ttab.ofs[level] + rows * 4u, part, bar);
+                    }
                 }
             }
         }
@@ -508,13 +597,15 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
         // warp = lane quarter q (TMEM lanes 32 q .. 32 q + 31 = output rows) x column half h
         const int dw = warp - kDrainWarp0;
         const int q = dw & 3, h = dw >> 2;
-        const int row = 32 * q + lane;                       // output row inside the tile
+        // TMEM lane 32 q + lane; pass 1's operand rows are reversed (lane m' = output row 127 - m'),
+        // pass 2's accumulator COLUMNS are (column c = output column 127 - c)
+        const int row = kRows ? kUT - 1 - (32 * q + lane) : 32 * q + lane;     // output row inside the tile
         const bool store_leader = q == 0 && lane == 0;       // issues this half's TMA stores
         const int bar_a = 1 + 2 * h, bar_b = 2 + 2 * h;      // named barriers of this half (128 threads)
-        uint32_t lvl_it = 0;
+        uint32_t lvl_it = 0, round_it = 0;
         RoleClock rc(a.prof != nullptr && dw == 0 && lane == 0);
-        const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(64 * h);
-        const uint32_t stg = smem_u32(staging + (size_t)h * 16384);
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(kRows ? 64 * h : 64 * (1 - h));
+        const uint32_t stg = smem_u32(staging + (size_t)h * (kRows ? 32768 : 16384));
         const uint32_t stg_row = stg + (uint32_t)row * 128u;
         const uint32_t swz = (uint32_t)(row & 7);
         const int frame_exp = frame_scale_exp(a.frame_max_bits);
@@ -522,7 +613,9 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
         float prev[64];                                      // pass 2: previous level of this thread's outputs
 #pragma unroll
         for (int j = 0; j < 64; ++j) prev[j] = 0.f;
-        for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+        for (int ui = blockIdx.x; ui < a.n_sched; ui += gridDim.x) {
+            const int u = a.sched ? __ldg(a.sched + ui) : ui;
+            if (u < 0) continue;
             const Unit un = decode_unit(u, a, tbl, MODE);
             for (int level = un.lb; level < un.le; ++level, ++lvl_it) {
                 const uint32_t b = lvl_it & 1, par = (lvl_it >> 1) & 1;
@@ -551,52 +644,64 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                     __syncwarp();
                     if (lane == 0) mbar_arrive(smem_u32(&ctl->acc_empty[b]));
                     rc.lap(2);
-                    // two rounds through this half's 16 KB staging box: hi plane, then lo plane
-#pragma unroll
-                    for (int pl = 0; pl < 2; ++pl) {
-                        if (store_leader) bulk_wait_read();                 // the box's previous store has been read
-                        named_bar(bar_a, 128);
-#pragma unroll
-                        for (int c = 0; c < 8; ++c) {
-                            const uint32_t *w = pl == 0 ? hw : lw;
-                            st_shared_v4(stg_row + (((uint32_t)c ^ swz) << 4), w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
-                        }
-                        fence_proxy_async_smem();
-                        named_bar(bar_b, 128);
-                        if (store_leader) {
-                            tma_store_3d(&map_out, a.Ppad + un.x0 + 64 * h, level * a.Hp + un.y0, pl, stg);
-                            bulk_commit();
-                        }
-                    }
-                    // reflected halo columns of pass 2's input, written next to the interior:
-                    // column -1 - x <- x for x < rpad, column 2 W - 1 - x <- x for the last
-                    // rpad + (Wp - W) valid columns (ragged frames: pass 2 reads up to Wp + rpad)
+                    // Rounds through this half's two 16 KB staging boxes (alternating): hi plane, lo
+                    // plane, and for tiles next to the left / right frame border the same rows with
+                    // their columns REVERSED: the reflected halo columns of pass 2's input, stored next
+                    // to the interior (column -1 - x <- x, column 2 W - 1 - x <- x).  One barrier per
+                    // round: before it the leader waits until the PREVIOUS round's store has read its
+                    // box, which frees that box for the next round.
                     const int rpad = tbl.lv[level].rpad;
                     const int xs0 = un.x0 + 64 * h;
                     const int right_w = rpad + (a.Wp - a.W);
-                    if (xs0 < rpad || xs0 + 64 > a.W - right_w) {
+                    const bool left = xs0 < rpad, right = xs0 + 64 > a.W - right_w && xs0 < a.W;
+                    const bool right_tma = right && (a.W & 7) == 0 && xs0 + 64 <= a.W;    // no negative store coordinates
+                    const int n_rounds = (a.debug & 2) ? 0 : ((left || right_tma) && !(a.debug & 64)) ? 4 : 2;
+                    for (int rd = 0; rd < n_rounds; ++rd, ++round_it) {      // uniform per half
+                        const uint32_t dst = stg_row + (round_it & 1u) * 16384u;
+                        const bool lo_plane = rd & 1;
+                        if (rd < 2) {
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) {
+                                const uint32_t *w = lo_plane ? lw : hw;
+                                st_shared_v4(dst + (((uint32_t)c ^ swz) << 4), w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+                            }
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) {            // chunk c of the reversed row = chunk 7 - c, elements reversed
+                                const uint32_t *w = lo_plane ? lw : hw;
+                                st_shared_v4(dst + (((uint32_t)c ^ swz) << 4),
+                                             __byte_perm(w[4 * (7 - c) + 3], 0, 0x1032), __byte_perm(w[4 * (7 - c) + 2], 0, 0x1032),
+                                             __byte_perm(w[4 * (7 - c) + 1], 0, 0x1032), __byte_perm(w[4 * (7 - c)], 0, 0x1032));
+                            }
+                        }
+                        fence_proxy_async_smem();
+                        if (store_leader) bulk_wait_read();
+                        named_bar(bar_a, 128);
+                        if (store_leader && !(a.debug & 32)) {
+                            const uint32_t src = stg + (round_it & 1u) * 16384u;
+                            const int yrow = level * a.Hp + un.y0;
+                            if (rd < 2) {
+                                tma_store_3d(&map_out, a.Ppad + xs0, yrow, lo_plane, src);
+                            } else {
+                                // map_aux starts at the first column right of the frame (column W)
+                                if (left) tma_store_3d(&map_out, a.Ppad - xs0 - 64, yrow, lo_plane, src);
+                                if (right_tma) tma_store_3d(&map_aux, a.W - xs0 - 64, yrow, lo_plane, src);
+                            }
+                            bulk_commit();
+                        }
+                    }
+                    if (right && !right_tma && !(a.debug & (2 | 64))) {
+                        // widths that are not a multiple of 8: the right halo element by element
                         __half *rrow = a.r_base + ((int64_t)level * a.Hp + un.y0 + row) * a.r_pitch + a.Ppad;
 #pragma unroll
                         for (int pl = 0; pl < 2; ++pl) {
-                            __half *prow = rrow + (int64_t)pl * a.r_plane;
+                            unsigned short *prow = reinterpret_cast<unsigned short *>(rrow + (int64_t)pl * a.r_plane);
                             const uint32_t *w = pl == 0 ? hw : lw;
-                            if ((a.W & 7) == 0) {
 #pragma unroll
-                                for (int gq = 0; gq < 8; ++gq) {            // groups of 8 columns, reversed
-                                    const int xs = xs0 + 8 * gq;
-                                    const uint4 rev = make_uint4(__byte_perm(w[4 * gq + 3], 0, 0x1032), __byte_perm(w[4 * gq + 2], 0, 0x1032),
-                                                                 __byte_perm(w[4 * gq + 1], 0, 0x1032), __byte_perm(w[4 * gq], 0, 0x1032));
-                                    if (xs < rpad) *reinterpret_cast<uint4 *>(prow - 8 - xs) = rev;
-                                    if (xs >= a.W - right_w && xs < a.W) *reinterpret_cast<uint4 *>(prow + 2 * a.W - 8 - xs) = rev;
-                                }
-                            } else {
-#pragma unroll
-                                for (int e = 0; e < 64; ++e) {              // odd widths: element by element
-                                    const int x = xs0 + e;
-                                    const unsigned short v = (unsigned short)((e & 1) ? (w[e >> 1] >> 16) : (w[e >> 1] & 0xffffu));
-                                    if (x < rpad) reinterpret_cast<unsigned short *>(prow)[-1 - x] = v;
-                                    if (x >= a.W - right_w && x < a.W) reinterpret_cast<unsigned short *>(prow)[2 * a.W - 1 - x] = v;
-                                }
+                            for (int e = 0; e < 64; ++e) {
+                                const int x = xs0 + e;
+                                const unsigned short v = (unsigned short)((e & 1) ? (w[e >> 1] >> 16) : (w[e >> 1] & 0xffffu));
+                                if (x >= a.W - right_w && x < a.W) prow[2 * a.W - 1 - x] = v;
                             }
                         }
                     }
@@ -609,7 +714,8 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
 #pragma unroll
                     for (int c = 0; c < 2; ++c) {
                         uint32_t ra[32], rb[32];
-                        tmem_ld32_pair(acc + 32 * c, acc + kAccCols + 32 * c, ra, rb);
+                        // outputs 64 h + 32 c .. + 31 are accumulator columns 96 - 64 h - 32 c .. + 31, reversed
+                        tmem_ld32_pair(acc + 32 * (1 - c), acc + kAccCols + 32 * (1 - c), ra, rb);
                         if (c == 1) {
                             tc_fence_before();
                             __syncwarp();
@@ -626,15 +732,15 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                             }
                         }
                         rc.lap(2);
-                        if (emit) {                              // uniform per level
+                        if (emit && !(a.debug & 2)) {            // uniform per level
                             if (store_leader) bulk_wait_read();
                             named_bar(bar_a, 128);
 #pragma unroll
-                            for (int k = 0; k < 8; ++k)
-                                st_shared_v4(stg_row + (((uint32_t)k ^ swz) << 4), ra[4 * k], ra[4 * k + 1], ra[4 * k + 2], ra[4 * k + 3]);
+                            for (int k = 0; k < 8; ++k)      // output element i of the chunk is ra[31 - i]
+                                st_shared_v4(stg_row + (((uint32_t)k ^ swz) << 4), ra[31 - 4 * k], ra[30 - 4 * k], ra[29 - 4 * k], ra[28 - 4 * k]);
                             fence_proxy_async_smem();
                             named_bar(bar_b, 128);
-                            if (store_leader) {
+                            if (store_leader && !(a.debug & 32)) {
                                 tma_store_2d(&map_out, un.x0 + 64 * h + 32 * c, out_plane * a.Hp + un.y0, stg);
                                 bulk_commit();
                             }
@@ -652,6 +758,7 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, 512);
+    if (a.prof != nullptr && threadIdx.x == 0) atomicMax(a.prof + 19, globaltimer_ns());      // last CTA out
 }
 
 // Frame -> fp16 hi | lo planes [2][H + 2 Py][Wp] in frame-scaled units, reflected halo rows
@@ -694,12 +801,22 @@ __global__ void frame_max_kernel(const float *__restrict__ img, int64_t n4, uint
     if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(max_bits, __float_as_uint(m));
 }
 
-int toeplitz_rows(int rpad) { return kUT + 2 * rpad - 16 + kUT; }
-int toeplitz_buffer_bytes(int max_rpad) { return (toeplitz_rows(max_rpad) * 64 + 1023) / 1024 * 1024; }
+// rows of one compact Toeplitz array: the window of k-step j starts at row 16 j and spans 128 + 8 rows
+int toeplitz_rows(int rpad) { return kUT + 2 * rpad - 16 + kUT + 8; }
+// one Toeplitz buffer in shared memory: pass 2 (Toeplitz = B operand, band trimmed) never reads the
+// last 112 rows of the arrays and does not copy them
+int toeplitz_buffer_bytes(int max_rpad, bool rows_pass) {
+    return ((toeplitz_rows(max_rpad) - (rows_pass ? 0 : 112)) * 32 + 127) / 128 * 128;
+}
+// control block + Toeplitz ring, rounded up to the 1 KB alignment of the swizzled boxes behind it
+size_t staging_offset(int max_rpad, bool rows_pass) {
+    const size_t ring = (size_t)(rows_pass ? kToepBuffers1 : kToepBuffers2) * toeplitz_buffer_bytes(max_rpad, rows_pass);
+    return (1024 + ring + 1023) / 1024 * 1024;
+}
 
 constexpr size_t kSmemLimit = 227 * 1024;
 int data_stages_for(int max_rpad, bool rows_pass) {
-    const size_t fixed = 1024 + 2 * (size_t)toeplitz_buffer_bytes(max_rpad) + kStagingBytes;
+    const size_t fixed = staging_offset(max_rpad, rows_pass) + (rows_pass ? kStagingBytes1 : kStagingBytes2);
     const size_t per = rows_pass ? kStageBytes1 : kStageBytes2;
     if (fixed + 2 * per > kSmemLimit) return 0;
     return (int)std::min<size_t>(kMaxStages, (kSmemLimit - fixed) / per);
@@ -747,27 +864,42 @@ bool umma_prof_enabled() {
     return on;
 }
 
+// test tooling (tools/umma_masks.py sets it before every timed batch): re-read only while the
+// variable exists when the library is first used, so production launches never call getenv
+int umma_debug_mask() {
+    static const bool present = std::getenv("DOGBLOB_UMMA_DEBUG") != nullptr;
+    if (!present) return 0;
+    const char *e = std::getenv("DOGBLOB_UMMA_DEBUG");
+    return e ? std::atoi(e) : 0;
+}
+
 template <int MODE>
 cudaError_t launch_umma(UmmaArgs b, const LevelTable &tbl, const ToeplitzTable &ttab, int max_rpad,
-                        const CUtensorMap &map_in, const CUtensorMap &map_out, cudaStream_t st) {
+                        const CUtensorMap &map_in, const CUtensorMap &map_out, const CUtensorMap &map_aux,
+                        cudaStream_t st) {
     constexpr bool rows_pass = MODE == kModeRows;
-    b.toep_bytes = toeplitz_buffer_bytes(max_rpad);
+    b.toep_bytes = toeplitz_buffer_bytes(max_rpad, rows_pass);
+    b.staging_off = (int)staging_offset(max_rpad, rows_pass);
     b.stages = data_stages_for(max_rpad, rows_pass);
     if (b.stages < 2) return cudaErrorInvalidConfiguration;
-    const size_t smem = 1024 + 2 * (size_t)b.toep_bytes + kStagingBytes +
+    const size_t smem = (size_t)b.staging_off + (rows_pass ? kStagingBytes1 : kStagingBytes2) +
                         (size_t)b.stages * (rows_pass ? kStageBytes1 : kStageBytes2);
     static unsigned long long *d_prof = nullptr;
     const bool prof = umma_prof_enabled();
+    // DOGBLOB_UMMA_DEBUG (timing experiments, results are garbage): 1 no data TMA, 2 drain without
+    // staging / stores, 8 no MMAs, 16 no Toeplitz copies, 32 no TMA stores, 64 no halo column stores
+    b.debug = umma_debug_mask();
     if (prof) {
-        if (!d_prof) cudaMalloc(&d_prof, 16 * sizeof(unsigned long long));
-        cudaMemsetAsync(d_prof, 0, 16 * sizeof(unsigned long long), st);
-        cudaMemsetAsync(d_prof + 15, 0xff, sizeof(unsigned long long), st);
+        if (!d_prof) cudaMalloc(&d_prof, 256 * sizeof(unsigned long long));
+        cudaMemsetAsync(d_prof, 0, 24 * sizeof(unsigned long long), st);
+        cudaMemsetAsync(d_prof + 15, 0xff, 2 * sizeof(unsigned long long), st);
+        cudaMemsetAsync(d_prof + 20, 0xff, 2 * sizeof(unsigned long long), st);
         b.prof = d_prof;
     }
-    const int ctas = persistent_ctas(b.n_units);
-    umma_pass_kernel<MODE><<<ctas, kThreads, smem, st>>>(b, tbl, ttab, map_in, map_out);
+    const int ctas = b.n_ctas > 0 ? b.n_ctas : persistent_ctas(b.n_units);
+    umma_pass_kernel<MODE><<<ctas, kThreads, smem, st>>>(b, tbl, ttab, map_in, map_out, map_aux);
     if (prof) {
-        unsigned long long h[16];
+        unsigned long long h[256];
         cudaStreamSynchronize(st);
         cudaMemcpy(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost);
         static const char *names[16] = {
@@ -779,6 +911,13 @@ cudaError_t launch_umma(UmmaArgs b, const LevelTable &tbl, const ToeplitzTable &
         for (int i = 0; i < 16; ++i)
             if (names[i][0] != '-') fprintf(stderr, "\n   %-34s %8.1f", names[i], h[i] / 1e3 / ctas);
         fprintf(stderr, "\n   issuer total: slowest CTA %.1f, fastest %.1f\n", h[14] / 1e3, h[15] / 1e3);
+        if (std::getenv("DOGBLOB_UMMA_PROF_CTAS")) {
+            fprintf(stderr, "   issuer kilo-cycles per CTA:");
+            for (int i = 0; i < ctas && i < 224; ++i) fprintf(stderr, " %.0f", h[32 + i] / 1e3);
+            fprintf(stderr, "\n");
+        }
+        fprintf(stderr, "   timeline (us after the first CTA starts): issuer loops begin %.2f .. %.2f, end %.2f .. %.2f, last CTA exits %.2f\n",
+                (h[20] - h[16]) / 1e3, (h[17] - h[16]) / 1e3, (h[21] - h[16]) / 1e3, (h[18] - h[16]) / 1e3, (h[19] - h[16]) / 1e3);
     }
     return cudaGetLastError();
 }
@@ -802,18 +941,19 @@ UmmaLayout umma_layout(const ConvGeometry &g) {
     return l;
 }
 
-// Toeplitz operand of every level, as the kernels want it in shared memory: per level
-// `rows` = Kp - 16 + 128 rows of 16 taps, fp16 hi array then lo array, 8-row groups of 256 bytes =
-// [K half 0: 8 rows x 8 taps][K half 1].  G[p][kk] = w[kk - p + Kp - 16]; taps scaled by 2^t so
-// that the largest is in [512, 1024).  taps: the plan's duplicated table (entry t = offset t - rpad).
+// Toeplitz operand of every level, as the kernels want it in shared memory (compact form, see
+// kToepUpper): per level `rows` = Kp - 16 + 128 + 8 rows of 8 taps, fp16 hi array then lo array,
+// C[r][e] = w[r + e - 127]; taps scaled by 2^t so that the largest is in [512, 1024).  The window of
+// k-step j (inputs 16 j .. 16 j + 15) starts at row 16 j; its row n' holds the taps of output
+// n = 127 - n'.  taps: the plan's duplicated table (entry t = offset t - rpad).
 void build_toeplitz(const LevelDesc *lv, int n_levels, const float2 *taps, std::vector<float> &out,
                     ToeplitzTable &tab) {
     out.clear();
     for (int i = 0; i < n_levels; ++i) {
-        const int rpad = lv[i].rpad, Kp = kUT + 2 * rpad, rows = toeplitz_rows(rpad);
+        const int rpad = lv[i].rpad, rows = toeplitz_rows(rpad);
         tab.ofs[i] = (int)out.size();
         tab.rows[i] = rows;
-        out.resize(out.size() + (size_t)rows * 16, 0.f);
+        out.resize(out.size() + (size_t)rows * 8, 0.f);          // rows x (8 hi + 8 lo) halfs = rows x 8 floats
         const float2 *w = taps + lv[i].tap_ofs;
         float wmax = 0.f;
         for (int t = 0; t <= 2 * rpad; ++t) wmax = std::max(wmax, w[t].x);
@@ -821,16 +961,14 @@ void build_toeplitz(const LevelDesc *lv, int n_levels, const float2 *taps, std::
         if (wmax > 0.f) { int ex; std::frexp(wmax, &ex); tsc = 10 - ex; }      // wmax * 2^tsc in [512, 1024)
         tab.tscale[i] = tsc;
         __half *hi = reinterpret_cast<__half *>(out.data() + tab.ofs[i]);
-        __half *lo = hi + (size_t)rows * 16;
-        for (int p = 0; p < rows; ++p)
-            for (int kk = 0; kk < 16; ++kk) {
-                const int t = kk - p + (Kp - 16);
+        __half *lo = hi + (size_t)rows * 8;
+        for (int r = 0; r < rows; ++r)
+            for (int e = 0; e < 8; ++e) {
+                const int t = r + e - (kUT - 1);
                 const float v = (t >= 0 && t <= 2 * rpad) ? std::ldexp(w[t].x, tsc) : 0.f;
                 const __half h = __float2half_rn(v);
-                const __half l = __float2half_rn(v - __half2float(h));
-                const size_t o = (size_t)(p >> 3) * 128 + (kk >> 3) * 64 + (p & 7) * 8 + (kk & 7);
-                hi[o] = h;
-                lo[o] = l;
+                hi[(size_t)r * 8 + e] = h;
+                lo[(size_t)r * 8 + e] = __float2half_rn(v - __half2float(h));
             }
     }
 }
@@ -869,16 +1007,17 @@ cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d
     a.tiles_x = g.Wp / kUT; a.tiles_y = g.Hp / kUT;
     a.by_order = 1;                       // independent levels: finest units, longest first
     a.n_units = a.tiles_x * a.tiles_y * tbl.n_levels;
+    a.n_sched = a.n_units;
     a.H = g.H; a.W = g.W; a.Hp = g.Hp; a.Wp = g.Wp; a.Py = l.Py; a.Ppad = l.Ppad;
     a.r_pitch = l.Wq; a.r_plane = (int64_t)g.L * g.Hp * l.Wq;
     a.r_base = reinterpret_cast<__half *>(d_r);
     a.frame_max_bits = d_max_bits; a.toep = d_toep;
-    CUtensorMap map_in, map_out;
+    CUtensorMap map_in, map_out, map_aux;
     const int xrows = g.H + 2 * l.Py;
     {   // X planes as {64 x, rows, x-block, hi | lo}; box = 32 rows of one 128-column tile, both planes
         const cuuint64_t dims[4] = {64, (cuuint64_t)xrows, (cuuint64_t)(g.Wp / 64), 2};
         const cuuint64_t strides[3] = {(cuuint64_t)g.Wp * 2, 128, (cuuint64_t)xrows * g.Wp * 2};
-        const cuuint32_t box[4] = {64, 32, 2, 2};
+        const cuuint32_t box[4] = {64, kRowsPerStage1, 2, 2};
         if (!encode_map(&map_in, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, d_x, dims, strides, box))
             return cudaErrorInvalidValue;
     }
@@ -889,18 +1028,30 @@ cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d
         if (!encode_map(&map_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, d_r, dims, strides, box))
             return cudaErrorInvalidValue;
     }
-    return launch_umma<kModeRows>(a, tbl, ttab, g.max_rpad, map_in, map_out, st);
+    map_aux = map_out;
+    if ((g.W & 7) == 0) {   // right halo view: starts at the first column behind the frame (16-byte aligned)
+        const cuuint64_t dims[3] = {(cuuint64_t)(l.Wq - l.Ppad - g.W), (cuuint64_t)g.L * g.Hp, 2};
+        const cuuint64_t strides[2] = {(cuuint64_t)l.Wq * 2, (cuuint64_t)a.r_plane * 2};
+        const cuuint32_t box[3] = {64, 128, 1};
+        if (!encode_map(&map_aux, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
+                        reinterpret_cast<__half *>(d_r) + l.Ppad + g.W, dims, strides, box))
+            return cudaErrorInvalidValue;
+    }
+    return launch_umma<kModeRows>(a, tbl, ttab, g.max_rpad, map_in, map_out, map_aux, st);
 }
 
 // pass 2: R planes -> DoG slices [L - 1][Hp][Wp] (levels = true: the levels themselves, [L][Hp][Wp])
 cudaError_t launch_col_pass_umma(const ConvGeometry &g, const void *d_r, float *d_out, const LevelTable &tbl,
                                  const ToeplitzTable &ttab, const float *d_toep, cudaStream_t st,
-                                 const uint32_t *d_max_bits, bool levels) {
+                                 const uint32_t *d_max_bits, bool levels, const int *d_sched, int sched_slots,
+                                 int sched_ctas) {
     const UmmaLayout l = umma_layout(g);
     UmmaArgs a{};
     a.tiles_x = g.Wp / kUT; a.tiles_y = g.Hp / kUT;
     a.by_order = 0;
     a.n_units = a.tiles_x * a.tiles_y * tbl.n_groups;
+    a.sched = d_sched; a.n_sched = d_sched ? sched_slots * sched_ctas : a.n_units;
+    a.n_ctas = d_sched ? sched_ctas : 0;
     a.H = g.H; a.W = g.W; a.Hp = g.Hp; a.Wp = g.Wp; a.Py = l.Py; a.Ppad = l.Ppad;
     a.r_pitch = l.Wq; a.r_plane = (int64_t)g.L * g.Hp * l.Wq;
     a.frame_max_bits = d_max_bits; a.toep = d_toep;
@@ -919,8 +1070,8 @@ cudaError_t launch_col_pass_umma(const ConvGeometry &g, const void *d_r, float *
         if (!encode_map(&map_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d_out, dims, strides, box))
             return cudaErrorInvalidValue;
     }
-    if (levels) return launch_umma<kModeLevels>(a, tbl, ttab, g.max_rpad, map_in, map_out, st);
-    return launch_umma<kModeDog>(a, tbl, ttab, g.max_rpad, map_in, map_out, st);
+    if (levels) return launch_umma<kModeLevels>(a, tbl, ttab, g.max_rpad, map_in, map_out, map_out, st);
+    return launch_umma<kModeDog>(a, tbl, ttab, g.max_rpad, map_in, map_out, map_out, st);
 }
 
 }  // namespace dogblob
