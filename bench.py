@@ -4,10 +4,11 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
 
-Workload (BASELINE.json configs[1], SURVEY 8d "C2"): 1024x1024 PLIF-like synthetic
-frames, sigma in [1, 30], n_bin = 58 (59 levels, radii 5..150), threshold 0.1,
-overlap 0.5, pruning on, preprocess off.  A step is one pass of the hot path over
-a batch of BATCH distinct frames (scene seed 1000+f, noise seed 2000+f).
+Workload (BASELINE.json configs[1] as the batch of configs[2], SURVEY 8d "C2" / "C3"):
+1024x1024 PLIF-like synthetic frames, sigma in [1, 30], n_bin = 58 (59 levels, radii
+5..150), threshold 0.1, overlap 0.5, pruning on, preprocess off.  A step is one pass of
+the hot path over the C3 batch: BATCH = 256 distinct frames per GPU (scene seed 1000+f,
+noise seed 2000+f; frame f of the global batch runs on rank f mod N).
 
   value  : frames/s, kernels only, frames resident in HBM (CUDA events, max over ranks)
   e2e    : frames/s through Detector.run_batch with pinned HOST frames: H2D copy of
@@ -17,7 +18,9 @@ a batch of BATCH distinct frames (scene seed 1000+f, noise seed 2000+f).
   cpu_baseline: the oracle port of the reference CPU path timed on this host
 
 Multi-GPU: frames shard by index, frame f -> rank f mod N, no collective on the data
-path (weak scaling: BATCH frames per GPU per step).
+path (weak scaling: BATCH frames per GPU per step).  Under torchrun the ranks come from
+the environment; `python bench.py --gpus N` without one spawns the N ranks itself (one per
+device, wrapping around on a box with fewer devices) and relays rank 0's line.
 `--impl reference` times the reference CPU algorithm (oracle port) on all host cores.
 """
 
@@ -38,9 +41,20 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 WORKLOAD = "C2"
-BATCH = 16
-KERNELS_PER_FRAME = 8    # reset, row pass, column+DoG, edge DoG, nms, plateau, finalize_small, prune_large
-KERNELS_PER_FRAME_TENSOR = 9   # fp16 build only: + frame_max (scale of the operand split) in front of the row pass
+BATCH = int(os.environ.get("DOGBLOB_BENCH_BATCH", "256"))   # frames per GPU per step (the C3 batch)
+KERNELS_PER_FRAME = 8    # FP32 engine: reset, row pass, column+DoG, edge DoG, nms, plateau, finalize_small, prune_large
+KERNELS_PER_FRAME_TENSOR = 9   # tensor engine: reset, frame max, operand split, row pass, column+DoG, nms, plateau, finalize_small, prune_large
+METRIC = "frames/sec, 1024x1024 DoG detector (sigma<=30, n_bin=58)"
+
+
+def bench_config(world):
+    """The `config` object of both arms (identical keys and values for the same N)."""
+    return {"workload": f"{WORKLOAD}: 1024x1024 PLIF-like frames, sigma 1..30, n_bin 58, threshold 0.1, "
+                        f"overlap 0.5, prune on, preprocess off; batch C3 (scene seed 1000+f, noise seed 2000+f)",
+            "frames_per_step": BATCH * world, "frames_per_gpu": BATCH,
+            "sharding": "frame f -> rank f mod N, no collective",
+            "l2": f"per-frame working set 490 MB (59 + 58 planes of 4 MB) exceeds the 126 MB L2; "
+                  f"{BATCH} distinct frames per GPU rotate"}
 
 
 def params_kw():
@@ -48,9 +62,25 @@ def params_kw():
     return synth.config_params(WORKLOAD)
 
 
-def make_frames(indices):
+def _make_frame(f):
     from paper_2010_08486_b200 import synth
-    return [synth.config_frame("C3", int(f)) for f in indices]
+    return synth.config_frame("C3", int(f))
+
+
+def make_frames(indices):
+    """Frames of the C3 batch; generated in parallel worker processes (0.2 s each on one core).
+    Must run before CUDA is initialised in this process (fork)."""
+    indices = [int(f) for f in indices]
+    if len(indices) < 8:
+        return [_make_frame(f) for f in indices]
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    procs = max(1, min(32, cores // max(1, min(world, 8))))
+    if procs == 1:
+        return [_make_frame(f) for f in indices]
+    with mp.get_context("fork").Pool(procs) as pool:
+        return pool.map(_make_frame, indices, chunksize=4)
 
 
 def measured_peaks():
@@ -174,15 +204,14 @@ def run_reference(args):
         dt = time.perf_counter() - t0
     fps = per_step * args.steps / dt
     line = {
-        "impl": "reference", "metric": "frames/sec, 1024x1024 DoG detector (sigma<=30, n_bin=58)",
+        "impl": "reference", "metric": METRIC,
         "value": fps, "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{WORKLOAD}: 1024x1024 PLIF-like frames, sigma 1..30, n_bin 58, "
-                               "threshold 0.1, overlap 0.5, prune on, preprocess off",
-                   "frames_per_step": per_step},
+        "config": bench_config(args.gpus),
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": procs, "kind": "port",
-                         "sample": f"{per_step} frames per step, one per worker process "
+                         "sample": f"bounded sample of the batch: {per_step} frames per step (frames "
+                                   f"{0}..{per_step * args.steps - 1} of C3), one per worker process "
                                    f"({procs} processes, fft backend, float32)"},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -201,25 +230,28 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # frame f of the global batch goes to rank f mod world; generated in forked workers, so
+    # before this process touches CUDA
+    my_frames = [f for f in range(BATCH * world) if f % world == rank]
+    frames = make_frames(my_frames)
     if not torch.cuda.is_available():
         raise RuntimeError("bench.py --impl ours needs a CUDA device (no CPU fallback)")
-    local = local % torch.cuda.device_count()      # (a 1-GPU box can still exercise N > 1)
+    n_dev = torch.cuda.device_count()
+    local = local % n_dev                           # (a 1-GPU box can still exercise N > 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     ctl = None
     if world > 1:
-        # control plane only (barrier + max of one scalar): the data path has no collective,
-        # so the NCCL communicator is registered but never needed on the hot path
-        dist.init_process_group("cpu:gloo,cuda:nccl")
+        # control plane only (barrier + max of one scalar): the data path has no collective.  With one
+        # device per rank the NCCL backend is registered as the contract asks (never used on the hot
+        # path); ranks that share a device (N > devices) cannot form an NCCL communicator: gloo only.
+        dist.init_process_group("cpu:gloo,cuda:nccl" if n_dev >= world else "gloo")
         ctl = dist.new_group(backend="gloo")
 
     kw = params_kw()
     params = P.DetectionParams(preprocess=False, **kw)
     n_slots = int(os.environ.get("DOGBLOB_BENCH_SLOTS", "4"))   # frame slots = concurrent streams
     det = P.Detector(params, device=local, slots=n_slots)
-    # frame f of the global batch goes to rank f mod world
-    my_frames = [f for f in range(BATCH * world) if f % world == rank]
-    frames = make_frames(my_frames)
     H, W = frames[0].shape
     eng = det.plan_for((H, W))
     pitch = eng.plan.pitch
@@ -340,31 +372,46 @@ def run_ours(args):
         tensor_engine = eng.plan.conv_engine >= 1
         fp16_engine = eng.plan.conv_engine == 2
         if tensor_engine:
-            # tcgen05 Toeplitz GEMM: every level spends (128 + 2 rpad) / 8 steps of three 128 x 128 x 8
-            # tf32 MMAs per 128 x 128 tile (hi*hi, hi*lo, lo*hi; fp16 build: / 16 and x 16; full-width
-            # count, the kernel trims the band's triangular ends)
+            # tcgen05 Toeplitz GEMM: per 128 x 128 tile a level spends (128 + 2 rpad) / 16 k-steps of three
+            # kind::f16 MMAs (hi*hi, hi*lo, lo*hi; M = 128, K = 16).  The column pass trims every MMA to the
+            # band it can reach (k-step j feeds outputs [16 j - 2 rpad, 16 j + 15]: N = 16 .. 128) and
+            # computes the first level of every group but the first twice.  An MMA occupies the tensor pipe
+            # for 64 cycles whatever its N <= 128 (tools/ubench_umma_ss.cu), so flops understate the pipe.
             rpads = [max(8, (int(r) + 7) // 8 * 8) for r in det.bank.radii]
             tiles = ((H + 127) // 128) * ((W + 127) // 128)
-            krows = 16 if fp16_engine else 8
-            mma_flops = tiles * sum((128 + 2 * rp) // krows for rp in rpads) * 3 * (2.0 * 128 * 128 * krows)
+            groups = eng.plan.conv_groups
+            levels = []
+            for g in range(len(groups) - 1):
+                levels += list(range(groups[g], min(groups[g + 1] + (1 if g + 2 < len(groups) else 0), L)))
+            n_mma, mma_flops = 0, 0.0
+            for lv in levels:
+                rp2 = 2 * rpads[lv]
+                for j in range((128 + rp2) // 16):
+                    m0 = 16 * j
+                    ns = 0 if j == 0 else (max(0, m0 - rp2) & ~15)
+                    ne = 128 if j == 0 else min(128, m0 + 16)
+                    n_mma += 3
+                    mma_flops += 3 * 2.0 * 128 * (ne - ns) * 16
+            n_mma *= tiles
+            mma_flops *= tiles
             try:
                 f16_peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["bf16_tflops"]
             except Exception:
                 f16_peak = 2250.0
-            if not fp16_engine:
-                f16_peak /= 2.0                       # kind::tf32 runs at half the bf16 / fp16 rate
+            sm_hz = 1e6 * ((clocks or {}).get("sm_mhz") or 1965.0)
             engine_roof = {
-                "note": ("tcgen05 kind::f16" if fp16_engine else "tcgen05 kind::tf32") +
-                        " Toeplitz GEMM, float32 accuracy from a hi/lo split of both operands (3 MMAs per "
-                        "k-step); the kernel is bound by per-MMA dispatch and by its conversion / drain "
-                        "warps, not by the tensor pipe, see DESIGN.md 3a",
+                "note": "tcgen05 kind::f16 Toeplitz GEMM, float32 accuracy from a hi/lo split of both operands "
+                        "(3 MMAs per k-step); see DESIGN.md 3a for what bounds it",
                 "useful_flops_per_launch": col_flops,
                 "useful_tflops": col_flops / (col_ms_iso * 1e-3) / 1e12,
+                "mma_instructions_per_launch": n_mma,
                 "issued_mma_flops_per_launch": mma_flops,
                 "issued_mma_tflops": mma_flops / (col_ms_iso * 1e-3) / 1e12,
                 "mma_peak_tflops": f16_peak,
-                "mma_peak_source": "MEASURED_PEAKS.json bf16_tflops (kind::f16 rate; half of it for kind::tf32)",
+                "mma_peak_source": "MEASURED_PEAKS.json bf16_tflops (kind::f16 rate)",
                 "frac_of_mma_peak": mma_flops / (col_ms_iso * 1e-3) / 1e12 / f16_peak,
+                "tensor_pipe_busy_estimate": n_mma * 64.0 / 148.0 / (col_ms_iso * 1e-3 * sm_hz),
+                "level_groups": groups,
             }
             kernel_name = "umma_pass_kernel<kModeDog> (tcgen05 Toeplitz-GEMM column pass + fused DoG)"
         else:
@@ -385,17 +432,13 @@ def run_ours(args):
                     "whole_frame": {"bytes": frame_bytes, "flops": frame_flops,
                                     "hbm_frac_at_value": frame_bytes * value / world / 1e9 / peak}}
         line = {
-            "metric": "frames/sec, 1024x1024 DoG detector (sigma<=30, n_bin=58)",
+            "metric": METRIC,
             "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": f"{WORKLOAD}: 1024x1024 PLIF-like frames, sigma 1..30, n_bin 58, "
-                                   "threshold 0.1, overlap 0.5, prune on, preprocess off",
-                       "frames_per_step": frames_per_step, "frames_per_gpu": BATCH,
-                       "streams_per_gpu": len(slots), "sharding": "frame f -> rank f mod N, no collective",
-                       "l2": "per-frame working set 490 MB (59 + 58 planes of 4 MB) exceeds the 126 MB L2; "
-                             "16 distinct frames rotate"},
+            "config": bench_config(world),
+            "streams_per_gpu": len(slots), "devices": n_dev,
             "latency_ms": {"single_frame_e2e_median": float(np.median(lat)),
                            "p10": float(np.percentile(lat, 10)), "p90": float(np.percentile(lat, 90)),
                            "what": "Detector.run(pinned host frame): H2D + kernels + D2H + decode, batch 1",
@@ -406,7 +449,7 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "blobs_per_step": n_blobs,
                     "what": "Detector.run_batch over pinned host frames, wall clock"},
-            "gpu_launches": (KERNELS_PER_FRAME_TENSOR if fp16_engine else KERNELS_PER_FRAME) * BATCH * args.steps,
+            "gpu_launches": (KERNELS_PER_FRAME_TENSOR if tensor_engine else KERNELS_PER_FRAME) * BATCH * world * args.steps,
             "roofline": roofline,
             "clocks": clocks,
         }
@@ -431,9 +474,24 @@ def main():
         args.warmup = 1 if args.warmup is None else args.warmup
         run_reference(args)
     else:
-        args.steps = 20 if args.steps is None else args.steps
+        args.steps = 30 if args.steps is None else args.steps
         args.warmup = 3 if args.warmup is None else args.warmup
+        if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+            sys.exit(spawn_ranks(args))
         run_ours(args)
+
+
+def spawn_ranks(args):
+    """`python bench.py --gpus N` outside torchrun: launch the N ranks the way the driver does
+    (one process per GPU, rendezvous on 127.0.0.1) and pass their output through."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
+           "--gpus", str(args.gpus), "--steps", str(args.steps), "--warmup", str(args.warmup), "--impl", args.impl]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

@@ -108,6 +108,10 @@ int64_t dogblob_image_pitch(const dogblob_plan *plan);
  * split (default build; one max reduction per frame), 1 = the same with tf32 operands (build option).
  * Chosen at plan time from the ladder and the frame size; DOGBLOB_CONV=fma|umma overrides. */
 int dogblob_plan_conv_engine(const dogblob_plan *plan);
+/* level groups of the fused column + DoG pass on this plan's engine (diagnostics / flop accounting):
+ * writes min(n_groups + 1, cap) boundaries to `begin` and returns n_groups; group g sweeps levels
+ * begin[g] .. begin[g+1]-1 and, on the tensor engine, also level begin[g+1] (computed twice). */
+int dogblob_plan_conv_groups(const dogblob_plan *plan, int32_t *begin, int cap);
 
 /* ---- the hot path ---------------------------------------------------------
  * replaces Detector.run minus preprocessing (detector.py:343-359):
@@ -143,7 +147,9 @@ int dogblob_detect_host(const dogblob_plan *plan, const float *h_image,
  *   frame_done   event (dogblob_event_create) of this buffer set: recorded here behind the
  *                frame's last operation; the next call waits on it before it overwrites d_image
  * One buffer set (d_image, d_workspace, d_result, h_result, h_gate, frame_done) = one frame in
- * flight: synchronise `stream` before the set is used again. */
+ * flight: synchronise `stream` before the set is used again.
+ * FP32 engine only (dogblob_plan_conv_engine() == 0): the tensor engine scales its fp16 operands
+ * by the frame's maximum and needs the whole frame first; it returns DOGBLOB_EINVAL here. */
 #define DOGBLOB_GATE_CHUNKS 4
 #define DOGBLOB_GATE_INTS 16
 int dogblob_detect_host_streamed(const dogblob_plan *plan, const float *h_image,

@@ -42,6 +42,7 @@ SIGNATURES = {
     "dogblob_result_bytes": (_sz, [_vp]),
     "dogblob_image_pitch": (_i64, [_vp]),
     "dogblob_plan_conv_engine": (C.c_int, [_vp]),
+    "dogblob_plan_conv_groups": (C.c_int, [_vp, C.POINTER(C.c_int32), C.c_int]),
     "dogblob_detect": (_i, [_vp, _vp, _f, _i, _d, _i, _vp, _vp, _vp, _vp]),
     "dogblob_detect_host": (_i, [_vp, _vp, _f, _i, _d, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp]),
     "dogblob_detect_host_streamed": (_i, [_vp, _vp, _f, _i, _d, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp,

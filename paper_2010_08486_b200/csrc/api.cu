@@ -471,6 +471,12 @@ size_t dogblob_result_bytes(const dogblob_plan *plan) {
 }
 int64_t dogblob_image_pitch(const dogblob_plan *plan) { return plan ? plan->geo.Wp : 0; }
 int dogblob_plan_conv_engine(const dogblob_plan *plan) { return plan && plan->use_umma ? 2 : 0; }
+int dogblob_plan_conv_groups(const dogblob_plan *plan, int32_t *begin, int cap) {
+    if (!plan) return 0;
+    const LevelTable &t = plan->use_umma ? plan->umma_table : plan->table;
+    for (int i = 0; begin && i <= t.n_groups && i < cap; ++i) begin[i] = t.group_begin[i];
+    return t.n_groups;
+}
 size_t dogblob_blobspace_bytes(int max_blobs) { return blobspace_bytes(std::max(max_blobs, 1)); }
 
 static int check_threshold_args(int neighborhood, double overlap) {
@@ -612,9 +618,9 @@ int dogblob_detect_host_streamed(const dogblob_plan *plan, const float *h_image,
     DB_REQUIRE(copy_stream && h_gate && frame_done && copy_stream != stream,
                "streamed upload needs its own copy stream, a pinned gate array and an event");
     if (int rc = check_threshold_args(neighborhood, overlap)) return rc;
-    if (plan->use_umma)     // the fp16 operand split needs the whole frame's max first
-        return dogblob_detect_host(plan, h_image, threshold, neighborhood, overlap, prune, d_image,
-                                   d_workspace, d_result, h_result, h_result_blobs, stream, events);
+    // the tensor engine's fp16 operand split needs the whole frame's maximum before its first MMA
+    DB_REQUIRE(!plan->use_umma, "streamed upload is only available on the FP32 engine "
+                                "(dogblob_plan_conv_engine() == 0); use dogblob_detect_host");
     DeviceGuard guard(plan->device);
     DB_REQUIRE(guard.ok, "cannot select CUDA device");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);

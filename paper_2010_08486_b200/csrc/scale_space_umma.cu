@@ -25,21 +25,36 @@
 // the reflected halo columns written next to the interior) - the same 4 bytes per element as a
 // float32 plane, and every stage of both passes is one TMA box straight into MMA operand layout.
 //
+// Toeplitz operand, compact: the operand rows are indexed by the REVERSED output n' = 127 - n, so
+// T'[n'][k] = w[k + n' - 127] depends on k + n' only: the second K half of row n' is the first K
+// half of row n' + 8 and ONE 16-byte chunk per row, C[r][e] = w[r + e - 127], serves every k-step
+// (LBO = SBO = 128: overlapping core matrices; step j reads the window that starts at row 16 j).
+// Half the shared memory and half the copy of a [row][16 taps] array.  The drains undo the
+// reversal for free (pass 1: TMEM lane m' is output row 127 - m'; pass 2: accumulator column c
+// is output column 127 - c, a register renaming).
+//
 // One persistent CTA per SM, 384 threads:
-//   warp 0      issuer     one elected lane: 3 MMAs per k-step, tcgen05.commit frees the data stage /
-//                          the Toeplitz buffer / publishes the accumulator pair
-//   warp 1      loader     one TMA box per stage (pass 1: 32 input rows x 128 x, hi | lo = 16 KB;
+//   warp 0      issuer     ONE elected thread runs the whole loop (its descriptor arithmetic lives
+//                          in uniform registers): 3 MMAs per k-step, tcgen05.commit frees the data
+//                          stage / the Toeplitz buffer / publishes the accumulator pair.  A commit
+//                          costs the issuing thread ~250 cycles during which the tensor pipe runs
+//                          dry (tools/ubench_umma_commit.cu), hence stages of 4 k-steps
+//   warp 1      loader     one TMA box per stage (pass 1: 64 input rows x 128 x, hi | lo = 32 KB;
 //                          pass 2: 128 rows x 64 k, hi | lo = 32 KB)
-//   warp 2      Toeplitz   the level's prebuilt Toeplitz array (hi | lo), one bulk copy per level,
-//                          double buffered.  T only depends on k - n, so ONE array
-//                          G[p][kk] = w[kk - p + Kp - 16] serves every k-step: step m0 reads the
-//                          128-row window that starts at row Kp - 16 - m0 (the descriptor slides).
+//   warp 2      Toeplitz   the level's prebuilt compact arrays (hi | lo), bulk copies into a ring
+//                          of 2 buffers (pass 2 leaves out the 112 rows its trimmed band never reads)
 //   warps 4..11 drain      tcgen05.ld of the accumulator pair (lane = output row, 64 columns per
-//                          thread), scales, pass 1: hi/lo split -> swizzled staging -> TMA store
-//                          (+ mirrored halo columns); pass 2: DoG against the previous level kept in
+//                          thread), scales, pass 1: hi/lo split -> swizzled staging (two boxes per
+//                          column half, alternating: one barrier per round) -> TMA store, and for
+//                          tiles at the frame border the same rows with their columns reversed ->
+//                          TMA store into the halo columns (no negative store coordinates: a
+//                          partly outside box is illegal on stores; ragged widths fall back to
+//                          scalar stores); pass 2: DoG against the previous level kept in
 //                          REGISTERS, staging -> TMA store of the float32 slice
 // TMEM: two buffers of {main, small} 128 x 128 float32 accumulators (512 columns), so the drain of
 // one level overlaps the MMAs of the next.
+// Units: pass 1 = (tile, level), longest level first, round robin; pass 2 = (tile, level group) on
+// a static longest-processing-time schedule made at plan time (api.cu: plan_umma_schedule).
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>

@@ -41,11 +41,11 @@ RADIUS_PER_SIGMA = math.sqrt(2.0)
 DEFAULT_STACK_ELEMENT_CAP = 2 ** 28   # convolve.py:37 (the reference's host-RAM guard)
 DEFAULT_MAX_BLOBS = 1 << 16
 HOST_RESULT_BLOBS = 4096              # records copied back with the header in one D2H
-# Frames upload in row chunks under the row pass when that hides the copy (measured, round 1):
-# from 4 MiB on the tensor-core engine (wide ladders: C2 0.64 vs 0.65 ms, C4 2.68 vs 2.87 ms), from
-# 8 MiB on the FP32 engine; below that the gate only delays a row pass that is shorter than the
-# copy (C1 0.21 vs 0.16 ms, C5 0.88 vs 0.84 ms).
-STREAM_MIN_BYTES = 4 << 20
+# FP32 engine only: frames of at least 8 MiB upload in row chunks under the running row pass (below
+# that the gate only delays a row pass that is shorter than the copy: C1 0.21 vs 0.16 ms, C5 0.88
+# vs 0.84 ms).  The tensor-core engine needs the whole frame's maximum (scale of its fp16 operand
+# split) before its first MMA and always uploads in one piece; its 4 MiB copy is 15 % of a C2
+# frame's latency and overlaps the kernels of the other slots in run_batch.
 STREAM_MIN_BYTES_FP32 = 8 << 20
 STREAMED_UPLOAD = os.environ.get("DOGBLOB_STREAMED_UPLOAD", "1") != "0"
 
@@ -253,6 +253,10 @@ class _Plan:
         self.result_bytes = int(lib.dogblob_result_bytes(handle))
         self.pitch = int(lib.dogblob_image_pitch(handle))
         self.conv_engine = int(lib.dogblob_plan_conv_engine(handle))   # 0 FP32 kernels, 1 tcgen05 (2: fp16 build)
+        import ctypes
+        buf = (ctypes.c_int32 * 400)()
+        n = int(lib.dogblob_plan_conv_groups(handle, buf, 400))
+        self.conv_groups = [int(buf[i]) for i in range(n + 1)]        # level groups of the fused column pass
 
     def close(self):
         if self.handle is not None:
@@ -326,6 +330,7 @@ class _Slot:
         self.n_host = n_host
         torch.cuda.synchronize(dev)
         self.pending = None     # bookkeeping of run_batch
+        self.streamed = False   # whether the last launch() used the streamed upload
 
     # ---- one frame --------------------------------------------------------------
     def launch(self, frame, params: DetectionParams, prune: bool) -> None:
@@ -337,8 +342,9 @@ class _Slot:
             self._launch_with_preprocess(src, params, prune)
             return
         H, W = self.plan.shape
-        if STREAMED_UPLOAD and H * W * 4 >= (STREAM_MIN_BYTES if self.plan.conv_engine == 1
-                                             else STREAM_MIN_BYTES_FP32):
+        self.streamed = (STREAMED_UPLOAD and self.plan.conv_engine == 0
+                         and H * W * 4 >= STREAM_MIN_BYTES_FP32)
+        if self.streamed:
             # row chunks on the copy stream while the row pass already runs
             _lib.check(lib.dogblob_detect_host_streamed(
                 self.plan.handle, src, float(np.float32(params.threshold)), int(params.neighborhood),
@@ -450,14 +456,38 @@ class _Slot:
 
 
 class _Engine:
-    """Plan + slot pool for one image shape."""
+    """Plan + slot pool for one image shape.
+
+    `users` counts the calls that currently hold a lease on the engine (Detector._lease); an engine
+    that has been replaced (candidate capacity grown) is only marked `retired` and is closed by
+    the last call that still uses it, so no plan or slot is destroyed under a concurrent caller.
+    """
 
     def __init__(self, bank: TapBank, shape, device: int, max_blobs: int, n_slots: int):
         self.plan = _Plan(bank, shape, device, max_blobs)
-        self.slots = [_Slot(self.plan) for _ in range(n_slots)]
+        try:
+            self._check_memory(n_slots)
+            self.slots = [_Slot(self.plan) for _ in range(n_slots)]
+        except Exception:
+            self.plan.close()
+            raise
         self.free = queue.Queue()
         for s in self.slots:
             self.free.put(s)
+        self.users = 0
+        self.retired = False
+
+    def _check_memory(self, n_slots: int) -> None:
+        """The slot pool must fit the device: a parameter error like the reference's stack cap
+        (convolve.py:209-212), not an out-of-memory failure half way through the allocation."""
+        torch = _torch()
+        H, W = self.plan.shape
+        need = n_slots * (self.plan.workspace_bytes + self.plan.result_bytes + H * self.plan.pitch * 4)
+        free, _total = torch.cuda.mem_get_info(self.plan.device)
+        if need > 0.9 * free:
+            raise ValueError(f"scale-space workspace of {need / 2**30:.1f} GiB ({n_slots} slots of "
+                             f"{self.plan.workspace_bytes / 2**30:.1f} GiB) exceeds the device memory "
+                             f"available ({free / 2**30:.1f} GiB free)")
 
     def close(self):
         for s in self.slots:
@@ -531,19 +561,46 @@ class Detector:
                     self._engines[key] = eng
         return eng
 
-    def _grow(self, shape) -> None:
+    def _lease(self, shape) -> _Engine:
+        """The per-shape engine with a use count; every _lease needs one _release."""
         key = (int(shape[0]), int(shape[1]))
         with self._lock:
-            old = self._engines.pop(key, None)
-            self._max_blobs *= 4
-            if old is not None:
-                old.close()
+            eng = self._engines.get(key)
+            if eng is None:
+                eng = _Engine(self.bank, key, self.device, self._max_blobs, self._n_slots)
+                self._engines[key] = eng
+            eng.users += 1
+            return eng
+
+    def _release(self, eng: _Engine) -> None:
+        with self._lock:
+            eng.users -= 1
+            close_now = eng.retired and eng.users == 0
+        if close_now:
+            eng.close()
+
+    def _grow(self, shape, seen: _Engine) -> None:
+        """Candidate capacity exceeded on engine `seen`: replace it by one with 4x the room, once
+        (concurrent overflows of the same engine grow it a single time).  The caller still holds its
+        lease; the retired engine is closed by the last _release."""
+        key = (int(shape[0]), int(shape[1]))
+        with self._lock:
+            if self._engines.get(key) is seen:
+                del self._engines[key]
+                self._max_blobs *= 4
+            seen.retired = True
 
     def close(self) -> None:
         with self._lock:
-            for eng in self._engines.values():
-                eng.close()
+            engines = list(self._engines.values())
             self._engines.clear()
+            idle = []
+            for eng in engines:
+                eng.retired = True
+                if eng.users == 0:
+                    idle.append(eng)
+        for eng in idle:                # engines still in use are closed by their last user
+            eng.close()
 
     def _prepare(self, img, dtype):
         _check_dtype(dtype)
@@ -576,20 +633,21 @@ class Detector:
         p = self.params
         img = self._prepare(img, dtype)
         shape = tuple(img.shape)
-        if shape[0] * shape[1] * self.ladder.n_levels > (1 << 34):
-            raise ValueError(f"stack of {self.ladder.n_levels} x {shape} exceeds element cap")
         while True:
-            eng = self.plan_for(shape)
-            slot = eng.free.get()
+            eng = self._lease(shape)     # ValueError if the slot pool cannot fit the device
             try:
-                slot.launch(img, p, p.prune)
-                hdr, recs = slot.collect()
-                timings = slot.stage_times_ms(hdr)
+                slot = eng.free.get()
+                try:
+                    slot.launch(img, p, p.prune)
+                    hdr, recs = slot.collect()
+                    timings = slot.stage_times_ms(hdr)
+                finally:
+                    eng.free.put(slot)
+                if recs is not None:
+                    return self._finish(slot, hdr, recs, shape, timings)
+                self._grow(shape, eng)   # candidate capacity exceeded: retry with 4x the room
             finally:
-                eng.free.put(slot)
-            if recs is not None:
-                return self._finish(slot, hdr, recs, shape, timings)
-            self._grow(shape)   # candidate capacity exceeded: retry with 4x the room
+                self._release(eng)
 
     def run_batch(self, frames, timings: bool = False) -> list:
         """Detect over a sequence of equally shaped host frames, pipelined over the
@@ -602,8 +660,15 @@ class Detector:
         for f in frames:
             if tuple(f.shape) != shape:
                 raise ValueError("run_batch needs equally shaped frames")
-        eng = self.plan_for(shape)
-        slots = [eng.free.get() for _ in range(len(eng.slots))]
+        eng = self._lease(shape)
+        # one slot for certain, the others only if they are free right now: concurrent callers
+        # (batches or single frames) share the pool instead of waiting for each other's slots
+        slots = [eng.free.get()]
+        while len(slots) < len(eng.slots):
+            try:
+                slots.append(eng.free.get_nowait())
+            except queue.Empty:
+                break
         results = [None] * len(frames)
         retry = []
         try:
@@ -630,6 +695,9 @@ class Detector:
             for s in slots:
                 s.pending = None
                 eng.free.put(s)
+            if retry:
+                self._grow(shape, eng)
+            self._release(eng)
         for idx in retry:
             results[idx] = self.run(frames[idx])
         return results
@@ -670,6 +738,8 @@ def convolve_bank(img, bank: TapBank, backend: str = "cuda", dtype=np.float32, p
     if img.shape[0] * img.shape[1] * n_levels > stack_element_cap:
         raise ValueError(f"stack of {n_levels} x {img.shape} exceeds element cap {stack_element_cap}")
     _check_dtype(dtype)
+    if isinstance(plan, _Engine):        # the reference idiom: plan=det.plan_for(img.shape)
+        plan = plan.plan
     if plan is not None and tuple(plan.shape) != tuple(img.shape):
         raise ValueError(f"plan built for {plan.shape[1]}x{plan.shape[0]}, "
                          f"image is {img.shape[1]}x{img.shape[0]}")

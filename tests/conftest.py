@@ -7,6 +7,8 @@ import pytest
 ROOT = Path(__file__).resolve().parents[1]
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
+if str(ROOT / "tests") not in sys.path:
+    sys.path.insert(0, str(ROOT / "tests"))
 GOLDEN = ROOT / "tests" / "golden"
 
 
@@ -33,3 +35,12 @@ def golden():
     def load(name):
         return np.load(GOLDEN / name, allow_pickle=False)
     return load
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """The -m gpu configuration tests collect the parity report; write it out (see tests/parity.py)."""
+    try:
+        import parity
+        parity.write_report(ROOT)
+    except Exception as e:          # never turn a green session red over the report
+        print(f"parity report not written: {e}")

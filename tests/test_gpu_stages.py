@@ -425,6 +425,20 @@ class TestPruneOverlaps:
         out = P.prune_overlaps(bset(*top), 0.1)
         assert records_tuples(out.records) == golden_blobs(g, "t0_top2000_kept01_")
 
+    @pytest.mark.parametrize("thr", [0.5, 0.1, 0.99, 1.0])
+    def test_equal_response_same_pixel_ties_against_the_literal_reference(self, thr):
+        """The reference re-sorts its list after every merge (detector.py:279); the sort key ends in
+        sigma, the only field a merge changes, so only blobs with identical (response, y, x) could
+        change places.  Such twins sit next to each other, overlap completely (same centre) and
+        therefore absorb each other before either can absorb anything else: the order of the
+        survivors never changes.  Checked against the literal dense / re-sorting form
+        on sets full of exact ties: twins, triplets, twins next to overlapping neighbours."""
+        from test_oracle import tie_cases
+        for blobs in tie_cases():
+            pb = [P.Blob(b.x, b.y, b.sigma, b.radius, b.response, b.at_scale_boundary) for b in blobs]
+            out = P.prune_overlaps(bset(*pb), thr)
+            assert records_tuples(out.records) == oblob_tuples(O.prune_dense(blobs, thr))
+
     def test_threshold_bounds(self):
         with pytest.raises(ValueError):
             P.prune_overlaps(bset(), 1.5)

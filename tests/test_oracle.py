@@ -165,3 +165,39 @@ class TestPipeline:
         assert oblob_tuples(res.candidates) == golden_blobs(g, "t0_cand_")
         assert oblob_tuples(res.blobs) == golden_blobs(g, "t0_kept_")
         assert len(res.blobs) == 129 and len(res.candidates) == 138
+
+
+def tie_cases():
+    """Blob sets full of exact (response, y, x) ties: same-pixel twins / triplets in different
+    slices (equal float32 DoG values in neighbouring slices are all flagged, detector.py:165-166),
+    alone, next to overlapping neighbours, and mixed into random sets."""
+    import math
+    r2 = math.sqrt(2.0)
+    mk = lambda x, y, sigma, resp, edge=False: O.OBlob(x, y, sigma, sigma * r2, float(np.float32(resp)), edge)
+    cases = [
+        [mk(10, 10, 2.0, 0.5), mk(10, 10, 3.0, 0.5)],
+        [mk(10, 10, 2.0, 0.5), mk(10, 10, 3.0, 0.5), mk(10, 10, 9.0, 0.5)],
+        # twins with a stronger and a weaker overlapping neighbour on either side
+        [mk(10, 10, 2.0, 0.5), mk(10, 10, 6.0, 0.5), mk(12, 10, 4.0, 0.9), mk(9, 11, 5.0, 0.2), mk(30, 30, 3.0, 0.5)],
+        # the absorbed twin is the larger / the smaller one; boundary flags travel
+        [mk(20, 20, 8.0, 0.7, True), mk(20, 20, 1.5, 0.7), mk(26, 20, 8.0, 0.7), mk(20, 26, 1.5, 0.7)],
+        # two pairs of twins overlapping each other
+        [mk(15, 15, 3.0, 0.4), mk(15, 15, 5.0, 0.4), mk(17, 15, 3.5, 0.4), mk(17, 15, 4.5, 0.4), mk(16, 15, 4.0, 0.4)],
+    ]
+    rng = np.random.default_rng(5)
+    for _ in range(6):
+        blobs = []
+        for _k in range(25):
+            x, y = int(rng.integers(0, 40)), int(rng.integers(0, 40))
+            resp = float(rng.choice([0.25, 0.5, 0.75]))
+            for sigma in rng.choice([1.5, 2.0, 3.0, 4.5, 6.0], size=int(rng.integers(1, 4)), replace=False):
+                blobs.append(mk(x, y, float(sigma), resp, bool(rng.integers(0, 2))))
+        cases.append(blobs)
+    return cases
+
+
+class TestPruneTies:
+    @pytest.mark.parametrize("thr", [0.5, 0.1, 0.99, 1.0])
+    def test_cached_partner_form_equals_literal_resorting_form_on_exact_ties(self, thr):
+        for blobs in tie_cases():
+            assert O.prune(blobs, thr) == O.prune_dense(blobs, thr)
