@@ -87,7 +87,7 @@ struct dogblob_plan {
     // FP32 engine: rows_t = row-filtered planes (x-major), dog_t = DoG^T planes, edge = parked levels;
     // tensor engine: rows_t = R planes (fp16 hi | lo), x = X planes, dog_t = DoG planes (image
     // orientation), no edge planes
-    size_t off_rows_t = 0, off_x = 0, off_dog_t = 0, off_edge = 0, off_blobspace = 0, off_gate = 0, total = 0;
+    size_t off_rows_t = 0, off_x = 0, off_dog_t = 0, off_edge = 0, off_blobspace = 0, off_gate = 0, off_flags = 0, total = 0;
 };
 
 namespace {
@@ -446,6 +446,7 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
     }
     plan->off_blobspace = off; off += blobspace_bytes(max_blobs);
     plan->off_gate = off;   off += 256;                                   // streamed upload: gate word
+    plan->off_flags = off;  off += align_up(hit_flag_bytes(n_levels, g.Hp, g.Wp), 256);   // tensor engine: hit blocks
     plan->total = off;
     *out = plan;
     return DOGBLOB_OK;
@@ -504,14 +505,25 @@ static cudaError_t row_pass_any(const dogblob_plan *plan, const float *d_image, 
     return launch_row_pass(plan->geo, d_image, reinterpret_cast<float *>(ws + plan->off_rows_t), plan->table,
                            plan->d_taps, st, gate);
 }
-// pass 2 fused with the DoG: tensor engine -> slices in image orientation, FP32 engine -> transposed
-static cudaError_t col_dog_pass_any(const dogblob_plan *plan, void *d_workspace, cudaStream_t st) {
+static HitFlags hit_flags_of(const dogblob_plan *plan, void *d_workspace) {
+    HitFlags f;
+    f.data = reinterpret_cast<unsigned char *>(d_workspace) + plan->off_flags;
+    f.row_blocks = plan->geo.Hp / 8;
+    f.col_blocks = plan->geo.Wp / 64;
+    return f;
+}
+// pass 2 fused with the DoG: tensor engine -> slices in image orientation, FP32 engine -> transposed.
+// `threshold`: the tensor engine also records which blocks of the slices exceed it (for the extrema
+// kernel); NaN = not wanted (stage entry points).
+static cudaError_t col_dog_pass_any(const dogblob_plan *plan, void *d_workspace, cudaStream_t st,
+                                    float threshold = NAN) {
     char *ws = reinterpret_cast<char *>(d_workspace);
     float *dog = reinterpret_cast<float *>(ws + plan->off_dog_t);
     if (plan->use_umma)
         return launch_col_pass_umma(plan->geo, ws + plan->off_rows_t, dog, plan->umma_table, plan->toeplitz,
                                     plan->d_toeplitz, st, frame_max_word(plan, d_workspace), false,
-                                    plan->d_umma_sched, plan->umma_sched_slots, plan->umma_sched_ctas);
+                                    plan->d_umma_sched, plan->umma_sched_slots, plan->umma_sched_ctas,
+                                    threshold, std::isnan(threshold) ? HitFlags{} : hit_flags_of(plan, d_workspace));
     return launch_col_dog_pass(plan->geo, reinterpret_cast<const float *>(ws + plan->off_rows_t), dog,
                                reinterpret_cast<float *>(ws + plan->off_edge), plan->table, plan->d_taps, st);
 }
@@ -552,11 +564,13 @@ static int launch_frame_tail(const dogblob_plan *plan, float threshold, int neig
         return events ? cudaEventRecord(reinterpret_cast<cudaEvent_t>(events[k]), st)
                       : cudaSuccess;
     };
-    DB_CUDA(col_dog_pass_any(plan, d_workspace, st));
+    const bool use_flags = plan->use_umma && neighborhood == 3 && !std::isnan(threshold);
+    DB_CUDA(col_dog_pass_any(plan, d_workspace, st, use_flags ? threshold : NAN));
     DB_CUDA(ev(2));
     if (plan->use_umma)     // D planes in image orientation: rows = y, cols = x
         DB_CUDA(launch_extrema(dog, g.L - 1, g.H, g.W, g.Wp, (int64_t)g.Hp * g.Wp, false,
-                               plan->d_slice_sigma, threshold, neighborhood / 2, bs, st));
+                               plan->d_slice_sigma, threshold, neighborhood / 2, bs, st,
+                               use_flags ? hit_flags_of(plan, d_workspace) : HitFlags{}));
     else                    // D^T planes: rows = x (W valid), cols = y (H valid)
         DB_CUDA(launch_extrema(dog, g.L - 1, g.W, g.H, g.Hp, (int64_t)g.Hp * g.Wp, true,
                                plan->d_slice_sigma, threshold, neighborhood / 2, bs, st));

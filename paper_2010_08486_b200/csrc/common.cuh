@@ -151,6 +151,12 @@ cudaError_t launch_col_levels_pass(const ConvGeometry &g, const float *d_rows_t,
                                    cudaStream_t st);
 cudaError_t launch_edge_dog(const ConvGeometry &g, const float *d_edge, float *d_dog_t,
                             const LevelTable &tbl, cudaStream_t st);
+// which blocks of 8 rows x 64 columns of the DoG slices hold a value above the detection threshold
+struct HitFlags {
+    unsigned char *data = nullptr;       // [slice][col_blocks][row_blocks] (row blocks contiguous)
+    int row_blocks = 0, col_blocks = 0;
+};
+inline size_t hit_flag_bytes(int planes, int Hp, int Wp) { return (size_t)planes * (Hp / 8) * (Wp / 64); }
 // tensor-core (tcgen05) versions of the passes, scale_space_umma.cu
 struct ToeplitzTable {               // per level: float offset, rows, log2 of the tap scale
     int ofs[kMaxLevels];
@@ -176,7 +182,7 @@ cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d
 cudaError_t launch_col_pass_umma(const ConvGeometry &g, const void *d_r, float *d_out, const LevelTable &tbl,
                                  const ToeplitzTable &ttab, const float *d_toep, cudaStream_t st,
                                  const uint32_t *d_max_bits, bool levels, const int *d_sched, int sched_slots,
-                                 int sched_ctas);
+                                 int sched_ctas, float threshold = 0.f, HitFlags flags = HitFlags{});
 cudaError_t launch_untranspose(const float *d_src_t, int planes, int Hp, int Wp, int H, int W,
                                float *d_dst, cudaStream_t st);
 cudaError_t launch_dog_from_levels(int L, int64_t plane_elems, const float *d_levels,
@@ -184,10 +190,14 @@ cudaError_t launch_dog_from_levels(int L, int64_t plane_elems, const float *d_le
 cudaError_t configure_conv_kernels(int device);
 size_t col_pass_smem(int group_table, int max_rpad, bool dog);
 
-// extrema: NMS + compaction + plateau coalescing + ordering
+// extrema: NMS + compaction + plateau coalescing + ordering.  `flags` (optional): one byte per
+// 8-row x 64-column block of every slice, non-zero if the block holds a value above the threshold
+// (written by the tensor-core column pass); strips without a hit are skipped unread and inside a
+// strip only the rows next to a hit block are loaded.
 cudaError_t launch_extrema(const float *d_slices, int S, int rows, int cols, int64_t pitch,
                            int64_t plane, bool transposed, const double *d_slice_sigma,
-                           float threshold, int half, const BlobSpace &bs, cudaStream_t st);
+                           float threshold, int half, const BlobSpace &bs, cudaStream_t st,
+                           HitFlags flags = HitFlags{});
 // pruning + final packing into the result buffer
 cudaError_t launch_prune_and_pack(const BlobSpace &bs, double overlap, bool prune,
                                   void *d_result, int result_cap, cudaStream_t st);

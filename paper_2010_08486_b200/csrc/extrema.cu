@@ -14,6 +14,8 @@
 // voxels above the threshold (a few per million) touch their neighbours.
 #include <cstdlib>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace dogblob {
@@ -151,18 +153,37 @@ constexpr int kQueueCap = 1024;             // queued maxima per warp before a f
 
 struct RowRegs { float4 q; float halo; };      // halo: column c-1 (lane 0) or c+4 (lane 31)
 
-template <int kGroup, int kBandRows, int kMinCtas>
-__global__ void __launch_bounds__(256, kMinCtas)
-nms_window_kernel(Volume vol, float thr, bool transposed, const double *__restrict__ slice_sigma,
-                  BlobSpace bs) {
-    const int s = blockIdx.z;
+// one warp, one strip of 128 columns x kBandRows rows of slice s (tile = 8 strips side by side)
+template <int kGroup, int kBandRows, int kWarps>
+__device__ __forceinline__ void nms_strip(const Volume &vol, float thr, bool transposed,
+                                          const double *__restrict__ slice_sigma, const BlobSpace &bs,
+                                          const HitFlags &flags, int s, int tile_y, int tile_x,
+                                          unsigned short *queue) {
     const unsigned lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    if ((blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.x) == 0) bs.ctr->t_extrema = globaltimer_ns();
     // the 8 warps of a CTA sit side by side on the same rows: together they read 4 KB runs
-    const int r_first = blockIdx.y * kBandRows;            // first tested row
-    const int c = (blockIdx.x * 8 + warp) * 128 + 4 * (int)lane;
+    const int r_first = tile_y * kBandRows;                // first tested row
+    const int c = (tile_x * kWarps + warp) * 128 + 4 * (int)lane;
     if (c - 4 * (int)lane >= vol.cols) return;
+    // The producing kernel recorded which 8-row x 64-column blocks of the slice hold a value above
+    // the threshold at all.  A strip without one cannot emit anything and is not even read; in the
+    // others only the rows of hit blocks and their two neighbours are loaded (`need`, bit = local
+    // row with r_first - 1 as bit 0): a row further away is neither tested nor anybody's neighbour.
+    unsigned long long need = ~0ull;
+    if (flags.data != nullptr) {
+        static_assert(kBandRows + 2 <= 64, "row mask");
+        const int cb = (c - 4 * (int)lane) >> 6;
+        const int r_last = min(r_first + kBandRows - 1, vol.rows - 1);
+        const unsigned char *f0 = flags.data + ((int64_t)s * flags.col_blocks + cb) * flags.row_blocks;
+        const unsigned char *f1 = cb + 1 < flags.col_blocks ? f0 + flags.row_blocks : f0;
+        need = 0ull;
+        for (int rb = r_first >> 3; rb <= r_last >> 3; ++rb) {
+            if (!(f0[rb] | f1[rb])) continue;
+            const int lo = max(8 * rb, r_first) - r_first + 1, hi = min(8 * rb + 7, r_last) - r_first + 1;   // local rows
+            need |= ((hi + 2 >= 64 ? ~0ull : (1ull << (hi + 2)) - 1ull)) & ~((1ull << (lo - 1)) - 1ull);
+        }
+        if (need == 0ull) return;
+    }
     const int nvalid = min(max(vol.cols - c, 0), 4);       // valid columns of this lane
     const bool edge_lane = (lane == 0) || (lane == 31);
     const int halo_col = lane == 0 ? c - 1 : c + 4;
@@ -175,7 +196,7 @@ nms_window_kernel(Volume vol, float thr, bool transposed, const double *__restri
         RowRegs o;
         o.q = make_float4(ninf, ninf, ninf, ninf);
         o.halo = ninf;
-        if ((unsigned)r < (unsigned)vol.rows) {
+        if ((unsigned)r < (unsigned)vol.rows && ((need >> (r - (r_first - 1))) & 1ull)) {
             if (nvalid > 0) o.q = __ldg(reinterpret_cast<const float4 *>(ptr));   // pitch-padded: in bounds
             if (halo_ok) o.halo = __ldg(ptr + (lane == 0 ? -1 : 4));
         }
@@ -203,8 +224,6 @@ nms_window_kernel(Volume vol, float thr, bool transposed, const double *__restri
     // 2-D local maxima above the threshold are queued (16 bits: local row, local column) and
     // resolved against the neighbouring slices outside the streaming loop, so that the rare,
     // register-hungry part stays out of it
-    __shared__ unsigned short s_queue[8][kQueueCap];
-    unsigned short *queue = s_queue[warp];
     int qcount = 0;                                         // warp uniform
 
     // ring of kGroup rows in flight: a row's slot is reloaded (kGroup rows ahead) as soon as
@@ -279,6 +298,18 @@ nms_window_kernel(Volume vol, float thr, bool transposed, const double *__restri
         qcount = 0;
         if (g >= n_groups) break;
     }
+}
+
+// kWarps strips side by side per CTA.  With hit flags most strips return at once: one warp per CTA
+// then frees its slot immediately instead of idling next to a busy neighbour.
+template <int kGroup, int kBandRows, int kWarps, int kMinCtas>
+__global__ void __launch_bounds__(32 * kWarps, kMinCtas)
+nms_window_kernel(Volume vol, float thr, bool transposed, const double *__restrict__ slice_sigma,
+                  BlobSpace bs, HitFlags flags) {
+    __shared__ unsigned short s_queue[kWarps][kQueueCap];
+    if ((blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.x) == 0) bs.ctr->t_extrema = globaltimer_ns();
+    nms_strip<kGroup, kBandRows, kWarps>(vol, thr, transposed, slice_sigma, bs, flags, blockIdx.z, blockIdx.y, blockIdx.x,
+                                         s_queue[threadIdx.x >> 5]);
 }
 
 // ---- NMS + compaction -----------------------------------------------------------
@@ -478,9 +509,18 @@ cudaError_t launch_load_blobs(const BlobSpace &bs, const dogblob_blob *d_in, int
     return cudaGetLastError();
 }
 
+static int sm_count() {
+    static const int n = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
 cudaError_t launch_extrema(const float *d_slices, int S, int rows, int cols, int64_t pitch,
                            int64_t plane, bool transposed, const double *d_slice_sigma,
-                           float threshold, int half, const BlobSpace &bs, cudaStream_t st) {
+                           float threshold, int half, const BlobSpace &bs, cudaStream_t st, HitFlags flags) {
     Volume vol{d_slices, S, rows, cols, pitch, plane};
     const bool vec4 = (pitch % 4 == 0) && (plane % 4 == 0) &&
                       ((reinterpret_cast<uintptr_t>(d_slices) & 15u) == 0);
@@ -489,8 +529,13 @@ cudaError_t launch_extrema(const float *d_slices, int S, int rows, int cols, int
         // 3 rows in flight per lane, 31 tested rows per warp, 4 CTAs per SM: the best of the
         // measured variants ((6,34,3) ties; (6,34,2), (3,61,4), (3,31,3) are 5..10 % slower)
         constexpr int kBand = 31;
-        nms_window_kernel<3, kBand, 4><<<dim3((cols + 1023) / 1024, (rows + kBand - 1) / kBand, S), 256, 0, st>>>(
-            vol, threshold, transposed, d_slice_sigma, bs);
+        const int tiles_y = (rows + kBand - 1) / kBand;
+        if (flags.data != nullptr)
+            nms_window_kernel<3, kBand, 1, 32><<<dim3((cols + 127) / 128, tiles_y, S), 32, 0, st>>>(
+                vol, threshold, transposed, d_slice_sigma, bs, flags);
+        else
+            nms_window_kernel<3, kBand, 8, 4><<<dim3((cols + 1023) / 1024, tiles_y, S), 256, 0, st>>>(
+                vol, threshold, transposed, d_slice_sigma, bs, flags);
     } else if (vec4)
         nms_kernel<4><<<grid, 256, 0, st>>>(vol, threshold, half, transposed, d_slice_sigma, bs);
     else

@@ -81,7 +81,11 @@ constexpr int kAccCols = 128;
 constexpr int kRowsPerStage1 = DOGBLOB_UMMA_ROWS1;             // pass 1: input rows per data stage (16 per k-step)
 constexpr int kStageBytes1 = 512 * kRowsPerStage1;             // pass 1: [hi | lo][2 x-blocks][rows][128 B]
 constexpr int kStageBytes2 = 32768;       // pass 2: [hi | lo][128 rows][128 B]
-constexpr int kStagingBytes1 = 65536;     // pass 1 drain staging: two 16 KB boxes per column half (double buffered)
+#ifndef DOGBLOB_UMMA_STAGING1
+#define DOGBLOB_UMMA_STAGING1 2
+#endif
+constexpr int kStagingBufs1 = DOGBLOB_UMMA_STAGING1;           // pass 1 drain staging: 16 KB boxes per column half
+constexpr int kStagingBytes1 = 32768 * kStagingBufs1;
 constexpr int kStagingBytes2 = 32768;     // pass 2 drain staging: one 16 KB box per column half
 constexpr int kMaxStages = 8;
 #ifndef DOGBLOB_UMMA_TOEP1
@@ -115,6 +119,8 @@ struct UmmaArgs {
     int staging_off;        // byte offset of the drain staging (1 KB aligned; the data stages follow it)
     int stages;             // data stages that fit in shared memory
     unsigned long long *prof;   // DOGBLOB_UMMA_PROF: per-role cycle counters (see launch_umma)
+    HitFlags flags;         // pass 2 (DoG): blocks with a value above `thr` (nullptr: not wanted)
+    float thr;
     int debug;              // DOGBLOB_UMMA_DEBUG: timing experiments (results are garbage), see launch_umma
 };
 
@@ -620,7 +626,7 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
         uint32_t lvl_it = 0, round_it = 0;
         RoleClock rc(a.prof != nullptr && dw == 0 && lane == 0);
         const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(kRows ? 64 * h : 64 * (1 - h));
-        const uint32_t stg = smem_u32(staging + (size_t)h * (kRows ? 32768 : 16384));
+        const uint32_t stg = smem_u32(staging + (size_t)h * (kRows ? 16384 * kStagingBufs1 : 16384));
         const uint32_t stg_row = stg + (uint32_t)row * 128u;
         const uint32_t swz = (uint32_t)(row & 7);
         const int frame_exp = frame_scale_exp(a.frame_max_bits);
@@ -672,8 +678,13 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                     const bool right_tma = right && (a.W & 7) == 0 && xs0 + 64 <= a.W;    // no negative store coordinates
                     const int n_rounds = (a.debug & 2) ? 0 : ((left || right_tma) && !(a.debug & 64)) ? 4 : 2;
                     for (int rd = 0; rd < n_rounds; ++rd, ++round_it) {      // uniform per half
-                        const uint32_t dst = stg_row + (round_it & 1u) * 16384u;
+                        const uint32_t buf = kStagingBufs1 == 2 ? (round_it & 1u) : 0u;
+                        const uint32_t dst = stg_row + buf * 16384u;
                         const bool lo_plane = rd & 1;
+                        if (kStagingBufs1 == 1) {          // single box: the previous store must have read it
+                            if (store_leader) bulk_wait_read();
+                            named_bar(bar_b, 128);
+                        }
                         if (rd < 2) {
 #pragma unroll
                             for (int c = 0; c < 8; ++c) {
@@ -690,10 +701,10 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                             }
                         }
                         fence_proxy_async_smem();
-                        if (store_leader) bulk_wait_read();
+                        if (kStagingBufs1 == 2 && store_leader) bulk_wait_read();
                         named_bar(bar_a, 128);
                         if (store_leader && !(a.debug & 32)) {
-                            const uint32_t src = stg + (round_it & 1u) * 16384u;
+                            const uint32_t src = stg + buf * 16384u;
                             const int yrow = level * a.Hp + un.y0;
                             if (rd < 2) {
                                 tma_store_3d(&map_out, a.Ppad + xs0, yrow, lo_plane, src);
@@ -726,6 +737,7 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                     const bool emit = MODE == kModeLevels || level > un.lb;
                     const float sig = MODE == kModeDog && level > un.lb ? tbl.lv[level - 1].sigma_f32 : 0.f;
                     const int out_plane = MODE == kModeLevels ? level : level - 1;
+                    bool hit = false;
 #pragma unroll
                     for (int c = 0; c < 2; ++c) {
                         uint32_t ra[32], rb[32];
@@ -740,8 +752,10 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                         for (int j = 0; j < 32; ++j) {
                             const float v = __fmul_rn(__fmul_rn(__fadd_rn(__uint_as_float(ra[j]), __uint_as_float(rb[j])), unscale_t), unscale_x);
                             if (MODE == kModeDog) {
-                                ra[j] = __float_as_uint(__fmul_rn(__fsub_rn(prev[32 * c + j], v), sig));
+                                const float d = __fmul_rn(__fsub_rn(prev[32 * c + j], v), sig);
+                                ra[j] = __float_as_uint(d);
                                 prev[32 * c + j] = v;
+                                hit = hit || d > a.thr;
                             } else {
                                 ra[j] = __float_as_uint(v);
                             }
@@ -761,6 +775,18 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                             }
                         }
                         rc.lap(3);
+                    }
+                    // this warp's 32 rows x 64 columns of the slice: which of its four 8-row blocks hold a
+                    // value above the threshold?  (rows below the frame do not count; the extrema kernel
+                    // only reads the neighbourhood of hit blocks)
+                    if (MODE == kModeDog && emit && a.flags.data != nullptr) {
+                        const uint32_t m = __ballot_sync(0xffffffffu, hit && un.y0 + row < a.H);
+                        if (lane == 0) {
+                            const uint32_t word = ((m & 0xffu) ? 1u : 0u) | ((m & 0xff00u) ? 0x100u : 0u) |
+                                                  ((m & 0xff0000u) ? 0x10000u : 0u) | ((m & 0xff000000u) ? 0x1000000u : 0u);
+                            *reinterpret_cast<uint32_t *>(a.flags.data + ((int64_t)out_plane * a.flags.col_blocks + ((un.x0 >> 6) + h)) *
+                                                                             a.flags.row_blocks + ((un.y0 >> 3) + 4 * q)) = word;
+                        }
                     }
                 }
             }
@@ -1059,7 +1085,7 @@ cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d
 cudaError_t launch_col_pass_umma(const ConvGeometry &g, const void *d_r, float *d_out, const LevelTable &tbl,
                                  const ToeplitzTable &ttab, const float *d_toep, cudaStream_t st,
                                  const uint32_t *d_max_bits, bool levels, const int *d_sched, int sched_slots,
-                                 int sched_ctas) {
+                                 int sched_ctas, float threshold, HitFlags flags) {
     const UmmaLayout l = umma_layout(g);
     UmmaArgs a{};
     a.tiles_x = g.Wp / kUT; a.tiles_y = g.Hp / kUT;
@@ -1067,6 +1093,8 @@ cudaError_t launch_col_pass_umma(const ConvGeometry &g, const void *d_r, float *
     a.n_units = a.tiles_x * a.tiles_y * tbl.n_groups;
     a.sched = d_sched; a.n_sched = d_sched ? sched_slots * sched_ctas : a.n_units;
     a.n_ctas = d_sched ? sched_ctas : 0;
+    a.flags = levels ? HitFlags{} : flags;
+    a.thr = threshold;
     a.H = g.H; a.W = g.W; a.Hp = g.Hp; a.Wp = g.Wp; a.Py = l.Py; a.Ppad = l.Ppad;
     a.r_pitch = l.Wq; a.r_plane = (int64_t)g.L * g.Hp * l.Wq;
     a.frame_max_bits = d_max_bits; a.toep = d_toep;
