@@ -4,13 +4,16 @@
 set -x
 timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1
 DOGBLOB_CONV=umma DOGBLOB_STREAMED_UPLOAD=0 timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu_umma_forced.log 2>&1
-DOGBLOB_CONV=umma timeout 600 compute-sanitizer --tool memcheck python tools/sanitize_run.py > gpurun_out/san_memcheck_umma.log 2>&1
+DOGBLOB_CONV=umma timeout 900 compute-sanitizer --tool memcheck python tools/sanitize_run.py > gpurun_out/san_memcheck_umma.log 2>&1
+timeout 900 compute-sanitizer --tool memcheck python tools/sanitize_run.py > gpurun_out/san_memcheck.log 2>&1
 python tools/config_timings.py > gpurun_out/config_timings.jsonl 2>&1
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+python bench.py --gpus 2 --steps 5 > gpurun_out/bench_2ranks_1gpu.json 2>> gpurun_out/bench.err
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_reference.json 2>> gpurun_out/bench.err
+for c in C2 C4; do DOGBLOB_UMMA_DEBUG=0 DOGBLOB_UMMA_PROF=1 timeout 100 python tools/umma_masks.py $c 0 2>&1 | tail -28 > gpurun_out/roles_$c.txt; done
 export DOGBLOB_STREAMED_UPLOAD=0
-ncu --metrics gpu__time_duration.sum --clock-control none -s 36 -c 9 --csv --log-file gpurun_out/launches_one_frame.csv python tools/profile_run.py --frames 5 > gpurun_out/prof1.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:umma_pass -s 8 -c 2 -o gpurun_out/umma_full -f python tools/profile_run.py --frames 5 > gpurun_out/prof2.log 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s 30 -c 10 --csv --log-file gpurun_out/launches_one_frame.csv python tools/profile_run.py --frames 5 > gpurun_out/prof1.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"umma_pass|nms_window" -s 6 -c 3 -o gpurun_out/umma_full -f python tools/profile_run.py --frames 5 > gpurun_out/prof2.log 2>&1
 unset DOGBLOB_STREAMED_UPLOAD
-ncu --metrics gpu__time_duration.sum --clock-control none -s 48 -c 400 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 2 --warmup 1 > gpurun_out/prof3.log 2>&1
+DOGBLOB_BENCH_BATCH=16 ncu --metrics gpu__time_duration.sum --clock-control none -s 48 -c 400 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 2 --warmup 1 > gpurun_out/prof3.log 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
