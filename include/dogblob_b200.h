@@ -219,6 +219,36 @@ int dogblob_event_elapsed_ms(void *start, void *stop, float *ms);
 int dogblob_event_intervals_ms(void *const *events, int n_events, float *out_ms);
 int dogblob_stream_sync(void *stream);
 int dogblob_device_count(int *count);
+/* ---- float64 tier ------------------------------------------------------------------------------
+ * Detector.run(img, dtype=np.float64) / convolve_bank(dtype=np.float64) of the reference
+ * (detector.py:333, convolve.py:76-77,189-218): the whole path in float64 on the FP64 pipe, separable,
+ * slow and simple - the oracle-grade "truth" tier.  No plan: taps arrive as float64 (host arrays
+ * `sigmas`, `radii`, `taps`, `tap_offsets` as in dogblob_plan_create, but double taps); images and
+ * stacks are DENSE device arrays (pitch = width).
+ *   dogblob_scale_space_f64   d_levels[L][H][W] = k_i * img; d_tmp: one plane of scratch
+ *   dogblob_dog_inplace_f64   d_levels[i] <- (levels[i] - levels[i+1]) * sigma_i, i < L - 1
+ *   dogblob_extrema_f64       find_extrema on a float64 stack (same result layout as dogblob_extrema)
+ *   dogblob_detect_f64        all of it + pruning; d_workspace of dogblob_f64_workspace_bytes() */
+size_t dogblob_f64_workspace_bytes(int height, int width, int n_levels, int max_blobs);
+int dogblob_scale_space_f64(int height, int width, int n_levels, const int32_t *radii, const double *taps,
+                            const int64_t *tap_offsets, const double *d_image, double *d_tmp,
+                            double *d_levels, void *stream);
+int dogblob_dog_inplace_f64(int n_levels, int height, int width, double *d_levels, const double *sigmas,
+                            void *stream);
+int dogblob_extrema_f64(int n_slices, int height, int width, const double *d_slices,
+                        const double *slice_sigmas, double threshold, int neighborhood, int max_blobs,
+                        void *d_blobspace, void *d_result, void *stream);
+int dogblob_detect_f64(int height, int width, int n_levels, const double *sigmas, const int32_t *radii,
+                       const double *taps, const int64_t *tap_offsets, const double *d_image,
+                       double threshold, int neighborhood, double overlap, int prune, int max_blobs,
+                       void *d_workspace, void *d_result, void *stream);
+
+/* Raw buffers for hosts without CUDA bindings (the reference-side stub):
+ * zero-filled device memory on `device`, page-locked host memory. */
+int dogblob_device_alloc(int device, size_t bytes, void **out);
+int dogblob_device_free(int device, void *ptr);
+int dogblob_pinned_alloc(size_t bytes, void **out);
+int dogblob_pinned_free(void *ptr);
 
 #ifdef __cplusplus
 }

@@ -67,6 +67,16 @@ SIGNATURES = {
     "dogblob_event_intervals_ms": (_i, [_vp, _i, _vp]),
     "dogblob_stream_sync": (_i, [_vp]),
     "dogblob_device_count": (_i, [C.POINTER(_i)]),
+    "dogblob_f64_workspace_bytes": (C.c_size_t, [_i, _i, _i, _i]),
+    "dogblob_scale_space_f64": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "dogblob_dog_inplace_f64": (_i, [_i, _i, _i, _vp, _vp, _vp]),
+    "dogblob_extrema_f64": (_i, [_i, _i, _i, _vp, _vp, C.c_double, _i, _i, _vp, _vp, _vp]),
+    "dogblob_detect_f64": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, C.c_double, _i, C.c_double, _i, _i,
+                                _vp, _vp, _vp]),
+    "dogblob_device_alloc": (_i, [_i, C.c_size_t, C.POINTER(_vp)]),
+    "dogblob_device_free": (_i, [_i, _vp]),
+    "dogblob_pinned_alloc": (_i, [C.c_size_t, C.POINTER(_vp)]),
+    "dogblob_pinned_free": (_i, [_vp]),
 }
 
 _lock = threading.Lock()

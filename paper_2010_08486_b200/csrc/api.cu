@@ -244,6 +244,20 @@ UmmaSchedule plan_umma_schedule(const std::vector<LevelDesc> &lv, int tiles, int
     return best;
 }
 
+// float64 tier helpers
+static size_t f64_taps_count(int n_levels, const int32_t *radii, const int64_t *tap_offsets) {
+    size_t n = 0;
+    for (int i = 0; i < n_levels; ++i) n = std::max(n, (size_t)tap_offsets[i] + 2 * (size_t)radii[i] + 1);
+    return n;
+}
+// device copy of a small host array, freed behind the stream's work
+template <typename T>
+static cudaError_t upload_async(const T *h, size_t n, T **d, cudaStream_t st) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(d), n * sizeof(T), st);
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyAsync(*d, h, n * sizeof(T), cudaMemcpyHostToDevice, st);
+}
+
 }  // namespace
 
 extern "C" {
@@ -784,6 +798,88 @@ int dogblob_extrema(int n_slices, int height, int width, const float *d_slices,
     return DOGBLOB_OK;
 }
 
+// ---- float64 tier -------------------------------------------------------------------------------
+size_t dogblob_f64_workspace_bytes(int height, int width, int n_levels, int max_blobs) {
+    const size_t plane = align_up((size_t)std::max(height, 1) * std::max(width, 1) * sizeof(double), 256);
+    return plane * ((size_t)std::max(n_levels, 1) + 1) + blobspace_bytes(std::max(max_blobs, 1));
+}
+
+int dogblob_scale_space_f64(int height, int width, int n_levels, const int32_t *radii, const double *taps,
+                            const int64_t *tap_offsets, const double *d_image, double *d_tmp,
+                            double *d_levels, void *stream) {
+    DB_REQUIRE(height >= 1 && width >= 1, "expected a non-empty 2-D image");
+    DB_REQUIRE(n_levels >= 1 && radii && taps && tap_offsets && d_image && d_tmp && d_levels, "bad argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    double *d_taps = nullptr;
+    DB_CUDA(upload_async(taps, f64_taps_count(n_levels, radii, tap_offsets), &d_taps, st));
+    DB_CUDA(cudaStreamSynchronize(st));          // the host array may be released by the caller
+    DB_CUDA(launch_scale_space_f64(height, width, n_levels, radii, d_taps, tap_offsets, d_image, d_tmp, d_levels, st));
+    DB_CUDA(cudaFreeAsync(d_taps, st));
+    return DOGBLOB_OK;
+}
+
+int dogblob_dog_inplace_f64(int n_levels, int height, int width, double *d_levels, const double *sigmas,
+                            void *stream) {
+    DB_REQUIRE(n_levels >= 2 && height >= 1 && width >= 1 && d_levels && sigmas, "bad argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    double *d_sig = nullptr;
+    DB_CUDA(upload_async(sigmas, (size_t)n_levels, &d_sig, st));
+    DB_CUDA(cudaStreamSynchronize(st));
+    DB_CUDA(launch_dog_inplace_f64(n_levels, (int64_t)height * width, d_levels, d_sig, st));
+    DB_CUDA(cudaFreeAsync(d_sig, st));
+    return DOGBLOB_OK;
+}
+
+int dogblob_extrema_f64(int n_slices, int height, int width, const double *d_slices,
+                        const double *slice_sigmas, double threshold, int neighborhood, int max_blobs,
+                        void *d_blobspace, void *d_result, void *stream) {
+    DB_REQUIRE(n_slices >= 1 && height >= 1 && width >= 1, "bad stack shape");
+    DB_REQUIRE(d_slices && slice_sigmas && d_blobspace && d_result && max_blobs >= 1, "bad argument");
+    if (int rc = check_threshold_args(neighborhood, 0.0)) return rc;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    BlobSpace bs = carve_blobspace(d_blobspace, max_blobs);
+    double *d_sig = nullptr;
+    DB_CUDA(upload_async(slice_sigmas, (size_t)n_slices, &d_sig, st));
+    DB_CUDA(cudaStreamSynchronize(st));
+    DB_CUDA(configure_finalize_kernels());
+    DB_CUDA(launch_reset_counters(bs, st));
+    DB_CUDA(launch_extrema_f64(d_slices, n_slices, height, width, d_sig, threshold, neighborhood / 2, bs, st));
+    DB_CUDA(launch_prune_and_pack(bs, 0.0, false, d_result, max_blobs, st));
+    DB_CUDA(cudaFreeAsync(d_sig, st));
+    return DOGBLOB_OK;
+}
+
+int dogblob_detect_f64(int height, int width, int n_levels, const double *sigmas, const int32_t *radii,
+                       const double *taps, const int64_t *tap_offsets, const double *d_image,
+                       double threshold, int neighborhood, double overlap, int prune, int max_blobs,
+                       void *d_workspace, void *d_result, void *stream) {
+    DB_REQUIRE(height >= 1 && width >= 1, "expected a non-empty 2-D image");
+    DB_REQUIRE(n_levels >= 2, "a ladder needs at least two levels");
+    DB_REQUIRE(sigmas && radii && taps && tap_offsets && d_image && d_workspace && d_result && max_blobs >= 1,
+               "bad argument");
+    if (int rc = check_threshold_args(neighborhood, overlap)) return rc;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const size_t plane = align_up((size_t)height * width * sizeof(double), 256);
+    char *ws = reinterpret_cast<char *>(d_workspace);
+    double *d_tmp = reinterpret_cast<double *>(ws);
+    double *d_levels = reinterpret_cast<double *>(ws + plane);
+    BlobSpace bs = carve_blobspace(ws + plane * ((size_t)n_levels + 1), max_blobs);
+    double *d_taps = nullptr, *d_sig = nullptr;
+    DB_CUDA(upload_async(taps, f64_taps_count(n_levels, radii, tap_offsets), &d_taps, st));
+    DB_CUDA(upload_async(sigmas, (size_t)n_levels, &d_sig, st));
+    DB_CUDA(cudaStreamSynchronize(st));
+    DB_CUDA(configure_finalize_kernels());
+    DB_CUDA(launch_reset_counters(bs, st));
+    // dense planes of exactly H * W doubles: the level stack starts one (aligned) plane into the workspace
+    DB_CUDA(launch_scale_space_f64(height, width, n_levels, radii, d_taps, tap_offsets, d_image, d_tmp, d_levels, st));
+    DB_CUDA(launch_dog_inplace_f64(n_levels, (int64_t)height * width, d_levels, d_sig, st));
+    DB_CUDA(launch_extrema_f64(d_levels, n_levels - 1, height, width, d_sig, threshold, neighborhood / 2, bs, st));
+    DB_CUDA(launch_prune_and_pack(bs, overlap, prune != 0, d_result, max_blobs, st));
+    DB_CUDA(cudaFreeAsync(d_taps, st));
+    DB_CUDA(cudaFreeAsync(d_sig, st));
+    return DOGBLOB_OK;
+}
+
 int dogblob_prune(int n, const dogblob_blob *d_blobs_in, double overlap, int max_blobs,
                   void *d_blobspace, void *d_result, void *stream) {
     DB_REQUIRE(n >= 0 && max_blobs >= 1 && n <= max_blobs, "blob count exceeds max_blobs");
@@ -829,6 +925,33 @@ int dogblob_stream_sync(void *stream) {
 int dogblob_device_count(int *count) {
     DB_REQUIRE(count != nullptr, "NULL argument");
     DB_CUDA(cudaGetDeviceCount(count));
+    return DOGBLOB_OK;
+}
+int dogblob_device_alloc(int device, size_t bytes, void **out) {
+    DB_REQUIRE(out != nullptr && bytes > 0, "bad argument");
+    *out = nullptr;
+    DeviceGuard guard(device);
+    DB_REQUIRE(guard.ok, "cannot select CUDA device");
+    DB_CUDA(cudaMalloc(out, bytes));
+    DB_CUDA(cudaMemset(*out, 0, bytes));
+    return DOGBLOB_OK;
+}
+int dogblob_device_free(int device, void *ptr) {
+    if (!ptr) return DOGBLOB_OK;
+    DeviceGuard guard(device);
+    DB_REQUIRE(guard.ok, "cannot select CUDA device");
+    DB_CUDA(cudaFree(ptr));
+    return DOGBLOB_OK;
+}
+int dogblob_pinned_alloc(size_t bytes, void **out) {
+    DB_REQUIRE(out != nullptr && bytes > 0, "bad argument");
+    *out = nullptr;
+    DB_CUDA(cudaMallocHost(out, bytes));
+    std::memset(*out, 0, bytes);
+    return DOGBLOB_OK;
+}
+int dogblob_pinned_free(void *ptr) {
+    if (ptr) DB_CUDA(cudaFreeHost(ptr));
     return DOGBLOB_OK;
 }
 

@@ -80,7 +80,7 @@ struct Counters {            // one per result, lives in the blob space
     int pad[2];
 };
 
-struct Voxel { int s, row, col; float val; };
+struct Voxel { int s, row, col; int pad; double val; };     // val: the slice's value (float32 values are exact in it)
 
 // Device-side control block of prune_large_kernel (prune.cu): ticket dispenser, completion
 // counter and the log of published phases.
@@ -198,6 +198,14 @@ cudaError_t launch_extrema(const float *d_slices, int S, int rows, int cols, int
                            int64_t plane, bool transposed, const double *d_slice_sigma,
                            float threshold, int half, const BlobSpace &bs, cudaStream_t st,
                            HitFlags flags = HitFlags{});
+// float64 tier (fp64.cu, extrema.cu): dense [L][H][W] double planes, slow and simple
+cudaError_t launch_extrema_f64(const double *d_slices, int S, int rows, int cols, const double *d_slice_sigma,
+                               double threshold, int half, const BlobSpace &bs, cudaStream_t st);
+cudaError_t launch_scale_space_f64(int H, int W, int L, const int *h_radii, const double *d_taps,
+                                   const int64_t *h_tap_offsets, const double *d_image, double *d_tmp,
+                                   double *d_levels, cudaStream_t st);
+cudaError_t launch_dog_inplace_f64(int L, int64_t plane_elems, double *d_levels, const double *d_sigmas,
+                                   cudaStream_t st);
 // pruning + final packing into the result buffer
 cudaError_t launch_prune_and_pack(const BlobSpace &bs, double overlap, bool prune,
                                   void *d_result, int result_cap, cudaStream_t st);

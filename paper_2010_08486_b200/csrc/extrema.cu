@@ -22,17 +22,20 @@ namespace dogblob {
 
 namespace {
 
-struct Volume {
-    const float *__restrict__ data;
+template <typename T>
+struct VolumeT {
+    const T *__restrict__ data;
     int S, rows, cols;           // valid extents
     int64_t pitch, plane;
-    __device__ __forceinline__ float at(int s, int r, int c) const {
+    __device__ __forceinline__ T at(int s, int r, int c) const {
         return __ldg(data + (int64_t)s * plane + (int64_t)r * pitch + c);
     }
 };
+using Volume = VolumeT<float>;     // production path; VolumeT<double>: the float64 tier (fp64.cu)
 
 // no neighbour in the (2h+1)^3 block is strictly greater than v
-__device__ bool is_block_max(const Volume &vol, int s, int r, int c, float v, int h) {
+template <typename T>
+__device__ bool is_block_max(const VolumeT<T> &vol, int s, int r, int c, T v, int h) {
     const int s0 = max(s - h, 0), s1 = min(s + h, vol.S - 1);
     const int r0 = max(r - h, 0), r1 = min(r + h, vol.rows - 1);
     const int c0 = max(c - h, 0), c1 = min(c + h, vol.cols - 1);
@@ -46,27 +49,27 @@ __device__ bool is_block_max(const Volume &vol, int s, int r, int c, float v, in
 // does a flagged voxel share an in-slice 8-neighbour that is flagged too?  For
 // n >= 3 such a neighbour necessarily has the same value (each is >= the other);
 // for n == 1 every voxel above the threshold is flagged.
-__device__ bool has_flagged_neighbour(const Volume &vol, int s, int r, int c, float v, int h,
-                                      float thr) {
+template <typename T>
+__device__ bool has_flagged_neighbour(const VolumeT<T> &vol, int s, int r, int c, T v, int h, T thr) {
     for (int dr = -1; dr <= 1; ++dr)
         for (int dc = -1; dc <= 1; ++dc) {
             if (dr == 0 && dc == 0) continue;
             const int rr = r + dr, cc = c + dc;
             if (rr < 0 || rr >= vol.rows || cc < 0 || cc >= vol.cols) continue;
-            const float nv = vol.at(s, rr, cc);
+            const T nv = vol.at(s, rr, cc);
             if (h >= 1 ? (nv == v && is_block_max(vol, s, rr, cc, nv, h)) : (nv > thr)) return true;
         }
     return false;
 }
 
-__device__ __forceinline__ dogblob_blob make_blob(int s, double x, double y, float val, int S,
+__device__ __forceinline__ dogblob_blob make_blob(int s, double x, double y, double val, int S,
                                                   const double *__restrict__ slice_sigma) {
     dogblob_blob b;
     b.x = x;
     b.y = y;
     b.sigma = slice_sigma[s];
     b.radius = 1.4142135623730951 * b.sigma;   // math.sqrt(2.0) * sigma, one rounding
-    b.response = (double)val;
+    b.response = val;
     b.slice = s;
     b.flags = (s == 0 || s == S - 1) ? DOGBLOB_BLOB_SCALE_EDGE : 0u;
     return b;
@@ -75,8 +78,9 @@ __device__ __forceinline__ dogblob_blob make_blob(int s, double x, double y, flo
 // A voxel that passed the in-slice test (`cand`): finish the (2h+1)^3 test against the
 // neighbouring slices, classify single / plateau member, and append with one atomic per warp
 // and list (ballot + popc).  Called by all 32 lanes (convergent), cand may be false.
-__device__ __forceinline__ void resolve_and_append(const Volume &vol, int s, int r, int cc, float val,
-                                                   bool cand, int h, float thr, bool transposed,
+template <typename T>
+__device__ __forceinline__ void resolve_and_append(const VolumeT<T> &vol, int s, int r, int cc, T val,
+                                                   bool cand, int h, T thr, bool transposed,
                                                    const double *__restrict__ slice_sigma,
                                                    const BlobSpace &bs, unsigned lane) {
     bool flagged = false, plateau = false;
@@ -87,12 +91,12 @@ __device__ __forceinline__ void resolve_and_append(const Volume &vol, int s, int
             for (int ds = -1; ds <= 1; ds += 2) {
                 const int ss = s + ds;
                 if (ss < 0 || ss >= vol.S) continue;
-                float nb[9];
+                T nb[9];
 #pragma unroll
                 for (int j = 0; j < 9; ++j) {
                     const int rr = r + j / 3 - 1, c2 = cc + j % 3 - 1;
                     nb[j] = (rr >= 0 && rr < vol.rows && c2 >= 0 && c2 < vol.cols)
-                                ? vol.at(ss, rr, c2) : -INFINITY;
+                                ? vol.at(ss, rr, c2) : (T)-INFINITY;
                 }
 #pragma unroll
                 for (int j = 0; j < 9; ++j) flagged = flagged && !(nb[j] > val);
@@ -118,7 +122,7 @@ __device__ __forceinline__ void resolve_and_append(const Volume &vol, int s, int
     if (flagged && !plateau) {
         const int idx = base_s + __popc(m_single & lt);
         if (idx < bs.cap) {
-            bs.unsorted[idx] = make_blob(s, transposed ? r : cc, transposed ? cc : r, val,
+            bs.unsorted[idx] = make_blob(s, transposed ? r : cc, transposed ? cc : r, (double)val,
                                          vol.S, slice_sigma);
         } else {
             atomicOr(&bs.ctr->flags, DOGBLOB_FLAG_OVERFLOW);
@@ -126,7 +130,7 @@ __device__ __forceinline__ void resolve_and_append(const Volume &vol, int s, int
     } else if (flagged) {
         const int idx = base_p + __popc(m_plat & lt);
         if (idx < bs.cap) {
-            bs.plateau[idx] = Voxel{s, r, cc, val};
+            bs.plateau[idx] = Voxel{s, r, cc, 0, (double)val};
             bs.parent[idx] = idx;
             bs.pl_count[idx] = 0;
             bs.pl_sum_row[idx] = 0ull;
@@ -429,7 +433,7 @@ plateau_kernel(BlobSpace bs, int S, bool transposed, const double *__restrict__ 
     __shared__ bool last;
     for (int a0 = blockIdx.x * blockDim.x; a0 < n; a0 += gridDim.x * blockDim.x) {
         const int a = a0 + threadIdx.x;
-        Voxel va = (a < n) ? bs.plateau[a] : Voxel{-9, -9, -9, 0.f};
+        Voxel va = (a < n) ? bs.plateau[a] : Voxel{-9, -9, -9, 0, 0.0};
         for (int b0 = 0; b0 < a0 + (int)blockDim.x && b0 < n; b0 += blockDim.x) {
             __syncthreads();
             if (b0 + (int)threadIdx.x < n) tile[threadIdx.x] = bs.plateau[b0 + threadIdx.x];
@@ -509,6 +513,40 @@ cudaError_t launch_load_blobs(const BlobSpace &bs, const dogblob_blob *d_in, int
     if (blocks < 1) blocks = 1;
     if (blocks > 296) blocks = 296;
     load_blobs_kernel<<<blocks, 256, 0, st>>>(bs, d_in, n);
+    return cudaGetLastError();
+}
+
+// ---- float64 tier (Detector.run(img, dtype=np.float64), convolve.py:76-77): the simple form ----
+// One thread per voxel; a voxel above the threshold walks its whole (2h+1)^3 block.  Slow is fine:
+// this is the oracle-grade path (T1 of the near-tie classifier), not the production one.
+__global__ void __launch_bounds__(256)
+nms_point_f64_kernel(VolumeT<double> vol, double thr, int h, const double *__restrict__ slice_sigma, BlobSpace bs) {
+    if ((blockIdx.x | blockIdx.y | blockIdx.z | threadIdx.x) == 0) bs.ctr->t_extrema = globaltimer_ns();
+    const int s = blockIdx.z, r = blockIdx.y;
+    const unsigned lane = threadIdx.x & 31;
+    for (int c0 = blockIdx.x * 256; c0 < vol.cols; c0 += gridDim.x * 256) {      // whole warps stay convergent
+        const int c = c0 + (int)threadIdx.x;
+        const bool in = c < vol.cols;
+        const double val = in ? vol.at(s, r, c) : 0.0;
+        bool cand = in && val > thr;
+        if (!__any_sync(0xffffffffu, cand)) continue;
+        if (cand && h == 1) {       // the in-slice part of the 3x3x3 test (resolve_and_append does the rest)
+            for (int j = 0; j < 9 && cand; ++j) {
+                const int rr = r + j / 3 - 1, cc = c + j % 3 - 1;
+                if (j != 4 && rr >= 0 && rr < vol.rows && cc >= 0 && cc < vol.cols && vol.at(s, rr, cc) > val) cand = false;
+            }
+        }
+        resolve_and_append<double>(vol, s, r, c, val, cand, h, thr, false, slice_sigma, bs, lane);
+    }
+}
+
+cudaError_t launch_extrema_f64(const double *d_slices, int S, int rows, int cols, const double *d_slice_sigma,
+                               double threshold, int half, const BlobSpace &bs, cudaStream_t st) {
+    VolumeT<double> vol{d_slices, S, rows, cols, cols, (int64_t)rows * cols};
+    nms_point_f64_kernel<<<dim3((cols + 255) / 256, rows, S), 256, 0, st>>>(vol, threshold, half, d_slice_sigma, bs);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    plateau_kernel<<<148, 256, 0, st>>>(bs, S, false, d_slice_sigma);
     return cudaGetLastError();
 }
 

@@ -23,6 +23,7 @@ import math
 import os
 import queue
 import threading
+import time
 from dataclasses import asdict, dataclass, field
 
 import numpy as np
@@ -224,10 +225,21 @@ def _check_backend(backend: str) -> None:
         raise ValueError(f"unknown backend {backend!r}; expected one of {BACKENDS}")
 
 
-def _check_dtype(dtype) -> None:
-    if np.dtype(dtype) != np.float32:
-        raise ValueError("backend='cuda' computes the scale space in float32; "
-                         f"dtype={np.dtype(dtype).name} is not available")
+def _check_dtype(dtype) -> np.dtype:
+    """float32 (production kernels) or float64 (the oracle-grade tier, convolve.py:76-77)."""
+    dt = np.dtype(dtype)
+    if dt not in (np.dtype(np.float32), np.dtype(np.float64)):
+        raise ValueError(f"backend='cuda' computes the scale space in float32 or float64; dtype={dt.name} "
+                         "is not available")
+    return dt
+
+
+def _f64_tables(bank: TapBank):
+    """host tables of the float64 entry points: sigmas, radii, float64 taps, offsets"""
+    return (np.ascontiguousarray(bank.ladder.sigmas, dtype=np.float64),
+            np.ascontiguousarray(bank.radii, dtype=np.int32),
+            np.ascontiguousarray(bank.taps64, dtype=np.float64),
+            np.ascontiguousarray(bank.offsets, dtype=np.int64))
 
 
 class _Plan:
@@ -603,7 +615,8 @@ class Detector:
             eng.close()
 
     def _prepare(self, img, dtype):
-        _check_dtype(dtype)
+        if _check_dtype(dtype) == np.float64:
+            return np.ascontiguousarray(_check_image(img), dtype=np.float64)
         torch = _torch()
         if isinstance(img, torch.Tensor):
             if img.ndim != 2 or img.shape[0] < 1 or img.shape[1] < 1:
@@ -633,6 +646,8 @@ class Detector:
         p = self.params
         img = self._prepare(img, dtype)
         shape = tuple(img.shape)
+        if np.dtype(dtype) == np.float64:
+            return self._run_f64(img)
         while True:
             eng = self._lease(shape)     # ValueError if the slot pool cannot fit the device
             try:
@@ -648,6 +663,45 @@ class Detector:
                 self._grow(shape, eng)   # candidate capacity exceeded: retry with 4x the room
             finally:
                 self._release(eng)
+
+    def _run_f64(self, img: np.ndarray) -> DetectResult:
+        """The float64 tier (detector.py:333 with dtype=np.float64): every stage in float64 on the
+        device, buffers allocated per call - the oracle-grade path, ~100x slower than float32."""
+        torch = _torch()
+        lib = _lib.load()
+        p = self.params
+        t0 = time.perf_counter()
+        if p.preprocess:                  # host float64, like the reference (images.py:112-157)
+            from .images import preprocess
+            img = np.ascontiguousarray(preprocess(img, p.smooth_sigma, p.saturation), dtype=np.float64)
+        pre_ms = (time.perf_counter() - t0) * 1e3
+        H, W = img.shape
+        sig, rad, taps, offs = _f64_tables(self.bank)
+        L = int(sig.size)
+        dev = torch.device("cuda", self.device)
+        max_blobs = self._max_blobs
+        with torch.cuda.device(dev):
+            st = torch.cuda.current_stream(dev)
+            d_img = torch.from_numpy(img).to(dev)
+            while True:
+                need = int(lib.dogblob_f64_workspace_bytes(H, W, L, max_blobs))
+                free, _total = torch.cuda.mem_get_info(dev)
+                if need > 0.9 * free:
+                    raise ValueError(f"float64 scale-space workspace of {need / 2**30:.1f} GiB exceeds the device "
+                                     f"memory available ({free / 2**30:.1f} GiB free)")
+                work = torch.empty(need, dtype=torch.uint8, device=dev)
+                res = torch.zeros(int(lib.dogblob_result_bytes_for(max_blobs)), dtype=torch.uint8, device=dev)
+                _lib.check(lib.dogblob_detect_f64(H, W, L, _lib.ptr(sig), _lib.ptr(rad), _lib.ptr(taps), _lib.ptr(offs),
+                                                  d_img.data_ptr(), float(p.threshold), int(p.neighborhood),
+                                                  float(p.overlap), 1 if p.prune else 0, max_blobs,
+                                                  work.data_ptr(), res.data_ptr(), st.cuda_stream))
+                hdr, recs = _read_result(res, max_blobs)
+                if recs is not None:
+                    break
+                max_blobs *= 4
+        timings = {"preprocess_ms": pre_ms, "convolve_ms": int(hdr["conv_ns"]) * 1e-6,
+                   "extrema_ms": int(hdr["extrema_ns"]) * 1e-6, "prune_ms": int(hdr["prune_ns"]) * 1e-6}
+        return self._finish(None, hdr, recs, (H, W), timings)
 
     def run_batch(self, frames, timings: bool = False) -> list:
         """Detect over a sequence of equally shaped host frames, pipelined over the
@@ -737,7 +791,8 @@ def convolve_bank(img, bank: TapBank, backend: str = "cuda", dtype=np.float32, p
     n_levels = bank.ladder.n_levels
     if img.shape[0] * img.shape[1] * n_levels > stack_element_cap:
         raise ValueError(f"stack of {n_levels} x {img.shape} exceeds element cap {stack_element_cap}")
-    _check_dtype(dtype)
+    if _check_dtype(dtype) == np.float64:
+        return _convolve_bank_f64(img, bank)
     if isinstance(plan, _Engine):        # the reference idiom: plan=det.plan_for(img.shape)
         plan = plan.plan
     if plan is not None and tuple(plan.shape) != tuple(img.shape):
@@ -764,6 +819,22 @@ def convolve_bank(img, bank: TapBank, backend: str = "cuda", dtype=np.float32, p
         if own:
             plan.close()
     return ScaleStack(levels=levels, sigmas=bank.ladder.sigmas)
+
+
+def _convolve_bank_f64(img, bank: TapBank) -> ScaleStack:
+    """float64 levels (convolve.py:76-77 with dtype=np.float64) on the FP64 pipe"""
+    torch = _torch()
+    lib = _lib.load()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    sig, rad, taps, offs = _f64_tables(bank)
+    H, W = img.shape
+    d_img = torch.from_numpy(np.ascontiguousarray(img, dtype=np.float64)).to(dev)
+    d_tmp = torch.empty((H, W), dtype=torch.float64, device=dev)
+    out = torch.empty((int(sig.size), H, W), dtype=torch.float64, device=dev)
+    st = torch.cuda.current_stream(dev)
+    _lib.check(lib.dogblob_scale_space_f64(H, W, int(sig.size), _lib.ptr(rad), _lib.ptr(taps), _lib.ptr(offs),
+                                           d_img.data_ptr(), d_tmp.data_ptr(), out.data_ptr(), st.cuda_stream))
+    return ScaleStack(levels=out.cpu().numpy(), sigmas=bank.ladder.sigmas)
 
 
 def fused_dog(img, bank: TapBank) -> DoGStack:
@@ -793,12 +864,18 @@ def dog_stack(stack: ScaleStack, ladder: SigmaLadder) -> DoGStack:
     """Adjacent differences scaled by the lower sigma of each pair (detector.py:117-126)."""
     if stack.n_levels != ladder.n_levels:
         raise ValueError(f"stack has {stack.n_levels} levels, ladder expects {ladder.n_levels}")
-    if stack.levels.dtype != np.float32:
-        raise ValueError("backend='cuda' differences float32 stacks only")
     torch = _torch()
     lib = _lib.load()
     dev = torch.device("cuda", torch.cuda.current_device())
     L, H, W = stack.levels.shape
+    if stack.levels.dtype == np.float64:
+        d_lv = torch.from_numpy(np.ascontiguousarray(stack.levels)).to(dev)
+        sig = np.ascontiguousarray(ladder.sigmas, dtype=np.float64)
+        _lib.check(lib.dogblob_dog_inplace_f64(L, H, W, d_lv.data_ptr(), _lib.ptr(sig),
+                                               torch.cuda.current_stream(dev).cuda_stream))
+        return DoGStack(slices=d_lv[:L - 1].cpu().numpy(), sigmas=ladder.sigmas[:-1])
+    if stack.levels.dtype != np.float32:
+        raise ValueError("backend='cuda' differences float32 and float64 stacks only")
     d_lv = torch.from_numpy(np.ascontiguousarray(stack.levels)).to(dev)
     out = torch.empty((L - 1, H, W), dtype=torch.float32, device=dev)
     sig = np.ascontiguousarray(ladder.sigmas, dtype=np.float64)
@@ -828,8 +905,9 @@ def find_extrema(dog: DoGStack, threshold: float = 0.1, neighborhood: int = 3,
     data = np.asarray(dog.slices)
     if data.ndim != 3:
         raise ValueError(f"expected (n_slices, height, width) slices, got shape {data.shape}")
-    if data.dtype != np.float32:
-        raise ValueError("backend='cuda' searches float32 stacks only")
+    if data.dtype not in (np.float32, np.float64):
+        raise ValueError("backend='cuda' searches float32 and float64 stacks only")
+    f64 = data.dtype == np.float64
     torch = _torch()
     lib = _lib.load()
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -840,9 +918,14 @@ def find_extrema(dog: DoGStack, threshold: float = 0.1, neighborhood: int = 3,
     while True:
         space = torch.zeros(int(lib.dogblob_blobspace_bytes(max_blobs)), dtype=torch.uint8, device=dev)
         res = torch.zeros(int(lib.dogblob_result_bytes_for(max_blobs)), dtype=torch.uint8, device=dev)
-        _lib.check(lib.dogblob_extrema(S, H, W, d_sl.data_ptr(), _lib.ptr(sig),
-                                       float(np.float32(threshold)), int(neighborhood), max_blobs,
-                                       space.data_ptr(), res.data_ptr(), st.cuda_stream))
+        if f64:      # the comparison `data > threshold` promotes to float64 (detector.py:166)
+            _lib.check(lib.dogblob_extrema_f64(S, H, W, d_sl.data_ptr(), _lib.ptr(sig), float(threshold),
+                                               int(neighborhood), max_blobs, space.data_ptr(), res.data_ptr(),
+                                               st.cuda_stream))
+        else:
+            _lib.check(lib.dogblob_extrema(S, H, W, d_sl.data_ptr(), _lib.ptr(sig),
+                                           float(np.float32(threshold)), int(neighborhood), max_blobs,
+                                           space.data_ptr(), res.data_ptr(), st.cuda_stream))
         hdr, recs = _read_result(res, max_blobs)
         if recs is not None:
             break

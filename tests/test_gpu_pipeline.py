@@ -333,8 +333,8 @@ class TestDetectorBehaviour:
         det = P.Detector(params_for("C1"))
         with pytest.raises(ValueError):
             det.run(np.zeros((4, 4, 3), np.float32))
-        with pytest.raises(ValueError):
-            det.run(np.zeros((16, 16), np.float32), dtype=np.float64)
+        with pytest.raises(ValueError, match="float32 or float64"):
+            det.run(np.zeros((16, 16), np.float32), dtype=np.int32)
         det.close()
 
 
@@ -580,3 +580,52 @@ class TestService:
                            "p90_ms,hardware")
         assert len(rows) == 3 and rows[1].startswith("cuda,6,4.0,256,256,1,3,")
         assert "median" in capsys.readouterr().out
+
+
+class TestReferenceSideStub:
+    def test_cuda_stub_of_integration_md_returns_the_detectors_records(self, monkeypatch):
+        """the ctypes stub a reference maintainer drops into pkg/src/dogblob (INTEGRATION.md 2,
+        paper_2010_08486_b200/integration/_cuda.py: numpy + the C ABI only, no torch) against
+        Detector.run on the same frames"""
+        from paper_2010_08486_b200 import _lib
+        from paper_2010_08486_b200.integration import _cuda
+        monkeypatch.setenv("DOGBLOB_B200_LIB", str(_lib.LIB_PATH))
+        for name in ("C1", "C2"):
+            frame = synth.config_frame(name)
+            params = params_for(name)
+            det = P.Detector(params)
+            want = det.run(frame).blobs.records
+            plan = _cuda.CudaPlan(det.ladder, det.bank, frame.shape)
+            try:
+                for _ in range(2):
+                    got = plan.detect(frame, np.float32(params.threshold), params.neighborhood, params.overlap,
+                                      params.prune)
+                    assert got.dtype == _cuda.BLOB and np.array_equal(got, want.astype(_cuda.BLOB))
+            finally:
+                plan.close()
+                det.close()
+
+
+class TestFloat64Detector:
+    """Detector.run(img, dtype=np.float64): the reference's T1 tier (float64 / direct) on the device."""
+
+    @pytest.mark.parametrize("name", ["C1", "C2", "C5"])
+    def test_float64_run_equals_the_reference_t1_lists(self, golden, name):
+        g = golden(f"config_{name}.npz")
+        det = P.Detector(params_for(name))
+        res = det.run(synth.config_frame(name), dtype=np.float64)
+        det.close()
+        strip = lambda ts: [(t[0], t[1], t[2], t[3], t[5]) for t in ts]
+        got, want = records_tuples(res.blobs.records), golden_blobs(g, "t1_kept_")
+        assert strip(got) == strip(want)
+        assert max(abs(a[4] - b[4]) for a, b in zip(got, want)) < 1e-12
+        assert set(res.timings_ms) == {"preprocess_ms", "convolve_ms", "extrema_ms", "prune_ms"}
+
+    def test_float64_candidates_without_pruning(self, golden):
+        g = golden("config_C2.npz")
+        p = P.DetectionParams(**{**params_for("C2").to_dict(), "prune": False})
+        det = P.Detector(p)
+        got = records_tuples(det.run(synth.config_frame("C2"), dtype=np.float64).blobs.records)
+        det.close()
+        want = golden_blobs(g, "t1_cand_")
+        assert [(t[0], t[1], t[2]) for t in got] == [(t[0], t[1], t[2]) for t in want]

@@ -121,8 +121,8 @@ class TestConvolveBank:
             P.convolve_bank(np.ones((0, 4)), bank)
         with pytest.raises(ValueError, match="cap"):
             P.convolve_bank(np.ones((64, 64), np.float32), bank, stack_element_cap=1000)
-        with pytest.raises(ValueError):
-            P.convolve_bank(np.ones((8, 8)), bank, dtype=np.float64)
+        with pytest.raises(ValueError, match="float32 or float64"):
+            P.convolve_bank(np.ones((8, 8)), bank, dtype=np.float16)
 
 
 class TestEngines:
@@ -442,3 +442,38 @@ class TestPruneOverlaps:
     def test_threshold_bounds(self):
         with pytest.raises(ValueError):
             P.prune_overlaps(bset(), 1.5)
+
+
+class TestFloat64Tier:
+    """dtype=np.float64 (detector.py:333, convolve.py:76-77): every stage in float64 on the device.
+    Levels and slices agree with the reference's float64 outputs to rounding (the reference sums a
+    2-D kernel by GEMM / FFT, the device two 1-D correlations: ~1e-15 on O(1) levels)."""
+
+    def test_levels_and_dog_against_reference_float64(self, golden):
+        g = golden("small_stages.npz")
+        ladder = P.build_ladder(1.0, 4.0, 3)
+        bank = P.build_kernel_bank(ladder, 5.0)
+        stack = P.convolve_bank(g["a_img"], bank, dtype=np.float64)
+        assert stack.levels.dtype == np.float64
+        assert np.abs(stack.levels - g["a_levels_direct_f64"]).max() < 1e-13
+        assert np.abs(stack.levels - g["a_levels_fft_f64"]).max() < 1e-13
+        dog = P.dog_stack(stack, ladder)
+        assert dog.slices.dtype == np.float64 and np.abs(dog.slices - g["a_dog_f64"]).max() < 1e-13
+        # bit-exact differences on the reference's own float64 levels
+        ref_stack = P.ScaleStack(g["a_levels_fft_f64"], ladder.sigmas)
+        assert np.array_equal(P.dog_stack(ref_stack, ladder).slices, g["a_dog_f64"])
+
+    @pytest.mark.parametrize("tag", ["c1", "c2", "c3", "c4"])
+    def test_ragged_and_wide_cases(self, golden, tag):
+        g = golden("small_stages.npz")
+        bank = bank_for(0.8, 2.4, 2)
+        got = P.convolve_bank(g[tag + "_img"], bank, dtype=np.float64).levels
+        assert np.abs(got - g[tag + "_levels_fft_f64"]).max() < 1e-12
+
+    def test_extrema_on_float64_slices_match_the_float32_rules(self, golden):
+        """plateau, corner voxel and threshold cases of the float32 goldens, promoted to float64"""
+        g = golden("small_stages.npz")
+        sig = np.asarray([1.0, 2.0, 3.0])
+        for n, key in ((3, "d_cand_"), (1, "d_n1_cand_"), (5, "d_n5_cand_")):
+            d64 = P.find_extrema(P.DoGStack(g["d_slices"].astype(np.float64), sig), float(np.float32(0.2)), neighborhood=n)
+            assert records_tuples(d64.records) == golden_blobs(g, key), n
