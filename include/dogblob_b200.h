@@ -243,6 +243,26 @@ int dogblob_detect_f64(int height, int width, int n_levels, const double *sigmas
                        double threshold, int neighborhood, double overlap, int prune, int max_blobs,
                        void *d_workspace, void *d_result, void *stream);
 
+/* ---- evaluation and scene generation on the device (sweeps over thousands of frames) -------------
+ * dogblob_match_voc: evaluate.py:48-109 (match_voc) for n_jobs independent frames, one CTA each.
+ *   d_pred        (x, y, radius) float64 triples of all jobs, each job's predictions in visiting
+ *                 order (descending response, ties by y, x); job j owns [pred_begin[j], pred_begin[j+1])
+ *   d_truth       (x, y, r) float64 triples; job j owns [truth_begin[j], truth_begin[j+1])
+ *   d_taken       scratch, one byte per truth
+ *   d_match       per prediction: index of the matched truth inside its job, -1 = false positive
+ *   d_match_iou   per prediction: IoU of the match (0 if none);  d_tp: per job true positives
+ * Identical to the host loop (float64, same operation order, first truth among equal maxima).
+ * dogblob_synth_frames: PLIF-like frames + their truth circles generated on the device (the scene
+ * model of synth.py:50-162 with allow_overlap=True).  PERF ONLY: counter-based random streams, not
+ * numpy's - statistically like the reference's frames, never bit-identical; parity always uses host
+ * frames.  d_frames[n_frames][height][pitch] float32, d_truth[n_frames][n_droplets][3] float64. */
+int dogblob_match_voc(int n_jobs, const double *d_pred, const int32_t *d_pred_begin, const double *d_truth,
+                      const int32_t *d_truth_begin, double iou_threshold, void *d_taken, int32_t *d_match,
+                      double *d_match_iou, int32_t *d_tp, void *stream);
+int dogblob_synth_frames(int n_frames, int height, int width, int64_t pitch, int n_droplets, double r_min,
+                         double r_max, uint64_t seed, double poisson_scale, double gaussian_sigma,
+                         float *d_frames, double *d_truth, void *stream);
+
 /* Raw buffers for hosts without CUDA bindings (the reference-side stub):
  * zero-filled device memory on `device`, page-locked host memory. */
 int dogblob_device_alloc(int device, size_t bytes, void **out);

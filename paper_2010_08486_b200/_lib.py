@@ -73,6 +73,9 @@ SIGNATURES = {
     "dogblob_extrema_f64": (_i, [_i, _i, _i, _vp, _vp, C.c_double, _i, _i, _vp, _vp, _vp]),
     "dogblob_detect_f64": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, C.c_double, _i, C.c_double, _i, _i,
                                 _vp, _vp, _vp]),
+    "dogblob_match_voc": (_i, [_i, _vp, _vp, _vp, _vp, C.c_double, _vp, _vp, _vp, _vp, _vp]),
+    "dogblob_synth_frames": (_i, [_i, _i, _i, _i64, _i, C.c_double, C.c_double, C.c_uint64, C.c_double, C.c_double,
+                                  _vp, _vp, _vp]),
     "dogblob_device_alloc": (_i, [_i, C.c_size_t, C.POINTER(_vp)]),
     "dogblob_device_free": (_i, [_i, _vp]),
     "dogblob_pinned_alloc": (_i, [C.c_size_t, C.POINTER(_vp)]),

@@ -19,7 +19,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libdogblob_b200.so"
 STAMP = PKG / "csrc" / ".build_stamp"
-SOURCES = ["api.cu", "scale_space.cu", "scale_space_umma.cu", "extrema.cu", "prune.cu", "preprocess.cu", "fp64.cu"]
+SOURCES = ["api.cu", "scale_space.cu", "scale_space_umma.cu", "extrema.cu", "prune.cu", "preprocess.cu", "fp64.cu", "evaluate.cu", "synth_device.cu"]
 HEADERS = [CSRC / "common.cuh", PKG.parent / "include" / "dogblob_b200.h"]
 
 NVCC_FLAGS = [

@@ -1,9 +1,9 @@
-"""Command line of the CUDA backend: detect, simulate, bench, serve.
+"""Command line of the CUDA backend: detect, simulate, evaluate, parity, bench, serve.
 
 Flags, outputs and exit codes follow the reference CLI (`cli.py:38-136,288-301`): 0 on
-success, 1 on usage errors, 2 on runtime failures; `--backend` accepts `cuda` only.  The
-reference's `evaluate` and `parity` subcommands score blob sets and are independent of the
-backend: run them from the reference package on the JSON this CLI writes.
+success, 1 on usage errors, 2 on runtime failures; `--backend` accepts `cuda` only.  `parity`
+compares the float32 production kernels with the float64 tier (`--dtype-a / --dtype-b`) where the
+reference compares its two CPU backends.
 
     python -m paper_2010_08486_b200 detect --input f.raw --min-sigma 1 --max-sigma 30 --n-bin 58 \
         --out-json blobs.json [--out-hist hist.csv]
@@ -112,8 +112,21 @@ def build_parser() -> _Parser:
     p.add_argument("--max-request-mb", type=float, default=16.0)
     _add_detector_flags(p, ladder_required=False)
 
-    for name in ("evaluate", "parity"):
-        sub.add_parser(name, help="backend independent: use the reference package's subcommand")
+    p = sub.add_parser("evaluate", help="score a blob set against ground truth")
+    p.add_argument("--pred", required=True)
+    p.add_argument("--truth", required=True)
+    p.add_argument("--iou", type=float, default=0.5)
+    p.add_argument("--out", required=True)
+
+    p = sub.add_parser("parity", help="compare two arithmetic tiers over a scene directory")
+    p.add_argument("--scenes", required=True, help="directory of .raw image files + <stem>.csv truths")
+    # the reference compares its direct and fft backends (--backend-a / --backend-b); both sides run on
+    # the device here and differ in the arithmetic tier
+    p.add_argument("--dtype-a", choices=("float32", "float64"), default="float64")
+    p.add_argument("--dtype-b", choices=("float32", "float64"), default="float32")
+    _add_detector_flags(p, ladder_required=True)
+    p.add_argument("--iou", type=float, default=0.5)
+    p.add_argument("--out", required=True)
     return parser
 
 
@@ -170,10 +183,7 @@ def _cmd_simulate(args) -> int:
     if Path(args.out_image).suffix.lower() not in RAW_SUFFIXES:
         raise ValueError("simulate writes the raw float format: use an --out-image ending in .raw or .bin")
     formats.write_raw(args.out_image, frame.image)
-    with open(args.out_truth, "w") as f:            # reference synth.write_truth_csv layout
-        f.write(f"# seed={args.seed}\nx,y,r\n")
-        for d in frame.truths:
-            f.write(f"{float(d.x)!r},{float(d.y)!r},{float(d.r)!r}\n")
+    synth.write_truth_csv(args.out_truth, synth.Frame(frame.image, frame.truths, args.seed))
     print(f"scene with {len(frame.truths)} spheres -> {args.out_image}")
     return 0
 
@@ -255,13 +265,48 @@ def _cmd_serve(args) -> int:
     return 0
 
 
-def _cmd_reference_only(args) -> int:
-    raise RuntimeError(f"`{args.command}` does not depend on the backend: run `dogblob {args.command}` from "
-                       "the reference package on the JSON written by `detect`")
+def _cmd_evaluate(args) -> int:
+    """cli.py:166-181 of the reference: score a blob JSON against a truth CSV"""
+    from . import evaluate as ev
+    preds = formats.read_blobset_json(args.pred)
+    truths = synth.read_truth_csv(args.truth)
+    report = ev.match_voc(preds, truths, args.iou)
+    ev.write_report_json(args.out, report)
+    print(f"precision={report.precision:.4f} recall={report.recall:.4f} "
+          f"(tp={report.tp} fp={report.fp} fn={report.fn})")
+    return 0
+
+
+def _cmd_parity(args) -> int:
+    """cli.py:184-213 of the reference, with arithmetic tiers in place of CPU backends"""
+    from . import evaluate as ev
+    scene_dir = Path(args.scenes)
+    if not scene_dir.is_dir():
+        raise FileNotFoundError(f"scene directory not found: {scene_dir}")
+    paths = sorted(p for p in scene_dir.iterdir() if p.suffix.lower() in (".png", ".tif", ".tiff", ".raw"))
+    if not paths:
+        raise FileNotFoundError(f"no scene images in {scene_dir}")
+    imgs, truths, names = [], [], []
+    for p in paths:
+        truth_path = p.with_suffix(".csv")
+        if not truth_path.is_file():
+            raise FileNotFoundError(f"missing truth file {truth_path}")
+        imgs.append(np.asarray(load_image(p)))
+        truths.append(synth.read_truth_csv(truth_path))
+        names.append(p.stem)
+    if args.device is not None:
+        import torch
+        torch.cuda.set_device(args.device)
+    params = _params(args)
+    stats = ev.parity(imgs, params, params, truths, args.iou, dtype_a=np.dtype(args.dtype_a),
+                      dtype_b=np.dtype(args.dtype_b))
+    ev.write_parity_csv(args.out, stats, names)
+    print(f"{len(imgs)} scenes: mean dP={stats.mean_dp:+.2e} mean dR={stats.mean_dr:+.2e}")
+    return 0
 
 
 _COMMANDS = {"detect": _cmd_detect, "simulate": _cmd_simulate, "bench": _cmd_bench, "serve": _cmd_serve,
-             "evaluate": _cmd_reference_only, "parity": _cmd_reference_only}
+             "evaluate": _cmd_evaluate, "parity": _cmd_parity}
 
 
 def main(argv=None) -> int:

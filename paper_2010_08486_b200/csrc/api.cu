@@ -880,6 +880,33 @@ int dogblob_detect_f64(int height, int width, int n_levels, const double *sigmas
     return DOGBLOB_OK;
 }
 
+int dogblob_match_voc(int n_jobs, const double *d_pred, const int32_t *d_pred_begin, const double *d_truth,
+                      const int32_t *d_truth_begin, double iou_threshold, void *d_taken, int32_t *d_match,
+                      double *d_match_iou, int32_t *d_tp, void *stream) {
+    DB_REQUIRE(n_jobs >= 0, "bad job count");
+    DB_REQUIRE(iou_threshold > 0.0 && iou_threshold <= 1.0, "iou_threshold must be in (0, 1]");
+    if (n_jobs == 0) return DOGBLOB_OK;
+    DB_REQUIRE(d_pred_begin && d_truth_begin && d_tp, "NULL argument");
+    DB_CUDA(launch_match_voc(n_jobs, d_pred, d_pred_begin, d_truth, d_truth_begin, iou_threshold,
+                             reinterpret_cast<unsigned char *>(d_taken), d_match, d_match_iou, d_tp,
+                             reinterpret_cast<cudaStream_t>(stream)));
+    return DOGBLOB_OK;
+}
+
+int dogblob_synth_frames(int n_frames, int height, int width, int64_t pitch, int n_droplets, double r_min,
+                         double r_max, uint64_t seed, double poisson_scale, double gaussian_sigma,
+                         float *d_frames, double *d_truth, void *stream) {
+    DB_REQUIRE(n_frames >= 1 && height >= 1 && width >= 1 && pitch >= width, "bad frame geometry");
+    DB_REQUIRE(n_droplets >= 0, "n_spheres must be >= 0");
+    DB_REQUIRE(r_min > 0.0 && r_max >= r_min, "bad radius range");
+    DB_REQUIRE(std::min(width, height) >= 2.0 * r_max + 3.0, "radius cannot fit inside the frame");
+    DB_REQUIRE(poisson_scale >= 0.0 && gaussian_sigma >= 0.0, "bad noise parameters");
+    DB_REQUIRE(d_frames && (n_droplets == 0 || d_truth), "NULL argument");
+    DB_CUDA(launch_synth_frames(n_frames, height, width, pitch, n_droplets, r_min, r_max, seed, poisson_scale,
+                                gaussian_sigma, d_frames, d_truth, reinterpret_cast<cudaStream_t>(stream)));
+    return DOGBLOB_OK;
+}
+
 int dogblob_prune(int n, const dogblob_blob *d_blobs_in, double overlap, int max_blobs,
                   void *d_blobspace, void *d_result, void *stream) {
     DB_REQUIRE(n >= 0 && max_blobs >= 1 && n <= max_blobs, "blob count exceeds max_blobs");

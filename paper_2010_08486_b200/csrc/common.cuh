@@ -206,6 +206,14 @@ cudaError_t launch_scale_space_f64(int H, int W, int L, const int *h_radii, cons
                                    double *d_levels, cudaStream_t st);
 cudaError_t launch_dog_inplace_f64(int L, int64_t plane_elems, double *d_levels, const double *d_sigmas,
                                    cudaStream_t st);
+// evaluation on the device (evaluate.cu): greedy VOC matching, one CTA per job (frame)
+cudaError_t launch_match_voc(int n_jobs, const double *d_pred, const int *d_pred_begin, const double *d_truth,
+                             const int *d_truth_begin, double thr, unsigned char *d_taken, int *d_match,
+                             double *d_match_iou, int *d_tp, cudaStream_t st);
+// perf-only scene generator on the device (synth_device.cu)
+cudaError_t launch_synth_frames(int n_frames, int H, int W, int64_t pitch, int n_droplets, double r_min,
+                                double r_max, unsigned long long seed, double poisson_scale, double gaussian_sigma,
+                                float *d_frames, double *d_truth, cudaStream_t st);
 // pruning + final packing into the result buffer
 cudaError_t launch_prune_and_pack(const BlobSpace &bs, double overlap, bool prune,
                                   void *d_result, int result_cap, cudaStream_t st);

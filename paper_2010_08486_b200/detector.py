@@ -348,6 +348,10 @@ class _Slot:
     def launch(self, frame, params: DetectionParams, prune: bool) -> None:
         """H2D + all kernels + D2H of header/records, asynchronously on self.stream."""
         lib = _lib.load()
+        torch = _torch()
+        if isinstance(frame, torch.Tensor) and frame.device.type == "cuda":
+            self._launch_resident(frame, params, prune)
+            return
         src = self._host_pointer(frame)
         self.preprocessed = bool(params.preprocess)
         if params.preprocess:
@@ -400,6 +404,31 @@ class _Slot:
         self.launch_device(self.d_image, params, prune)
         n = min(self.n_host, self.plan.max_blobs)
         _lib.check(lib.dogblob_fetch_result(self.d_result.data_ptr(), n, self.h_result.data_ptr(), st))
+
+    def _launch_resident(self, frame, params: DetectionParams, prune: bool) -> None:
+        """A frame that already lives on the device (float32 CUDA tensor [H][W], e.g. from
+        synth.device_frames or an upstream GPU stage): no host round trip for the pixels."""
+        torch = _torch()
+        lib = _lib.load()
+        H, W = self.plan.shape
+        if params.preprocess:
+            raise ValueError("device-resident frames are detected as they are: use preprocess=False")
+        if frame.dtype != torch.float32 or tuple(frame.shape) != (H, W) or frame.device.index != self.plan.device:
+            raise ValueError(f"expected a float32 CUDA tensor of shape {(H, W)} on device {self.plan.device}")
+        self.preprocessed = False
+        self.streamed = False
+        self.stream.wait_stream(torch.cuda.current_stream(frame.device))     # the producer's work is ordered first
+        with torch.cuda.stream(self.stream):
+            if W == self.plan.pitch and frame.is_contiguous():
+                src = frame                                   # the detector's own layout: zero copy
+                self._keepalive = frame
+            else:
+                self.d_image[:, :W].copy_(frame, non_blocking=True)
+                src = self.d_image
+        self.launch_device(src, params, prune)
+        n = min(self.n_host, self.plan.max_blobs)
+        _lib.check(lib.dogblob_fetch_result(self.d_result.data_ptr(), n, self.h_result.data_ptr(),
+                                            self.stream.cuda_stream))
 
     def launch_device(self, d_frame, params: DetectionParams, prune: bool, events=None) -> None:
         """Same, for a frame that is already resident: a float32 CUDA tensor [H][pitch]."""

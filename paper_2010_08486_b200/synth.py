@@ -154,3 +154,50 @@ def config_frame(name: str, index: int | None = None) -> np.ndarray:
 
 def config_params(name: str) -> dict:
     return dict(CONFIGS["C2" if name == "C3" else name][4])
+
+
+def write_truth_csv(path, frame: Frame) -> None:
+    """synth.py:165-171 layout: `# seed=`, header `x,y,r`, one repr() row per droplet."""
+    with open(path, "w") as f:
+        f.write(f"# seed={frame.seed}\nx,y,r\n")
+        for d in frame.truths:
+            f.write(f"{float(d.x)!r},{float(d.y)!r},{float(d.r)!r}\n")
+
+
+def read_truth_csv(path) -> tuple:
+    """synth.py:174-182"""
+    out = []
+    with open(path) as f:
+        for line in f:
+            line = line.strip()
+            if not line or line.startswith("#") or line.startswith("x,"):
+                continue
+            x, y, r = (float(v) for v in line.split(","))
+            out.append(Droplet(x=x, y=y, r=r))
+    return tuple(out)
+
+
+def device_frames(n_frames: int, width: int, height: int, count: int, r_range, seed: int,
+                  photons: float = 255.0, read_sigma: float = 0.01, device: int | None = None):
+    """PLIF-like frames generated ON the device for throughput / precision-recall sweeps over
+    thousands of frames: same scene model as droplet_scene(allow_overlap=True) +
+    sensor_noise, but counter-based random streams - PERF ONLY, never bit-identical to the
+    reference's numpy streams; parity is always judged on host frames.
+
+    Returns (frames, truths): a float32 CUDA tensor [n_frames][height][pitch] (pitch = width rounded
+    up to 128, the detector's device layout: frames[f] can go straight into dogblob_detect) and a
+    float64 array [n_frames][count][3] of (x, y, r)."""
+    import torch
+    from . import _lib
+    lib = _lib.load()
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    pitch = (int(width) + 127) // 128 * 128
+    frames = torch.empty((int(n_frames), int(height), pitch), dtype=torch.float32, device=dev)
+    truth = torch.zeros((int(n_frames), max(int(count), 1), 3), dtype=torch.float64, device=dev)
+    with torch.cuda.device(dev):
+        st = torch.cuda.current_stream(dev)
+        _lib.check(lib.dogblob_synth_frames(int(n_frames), int(height), int(width), pitch, int(count),
+                                            float(r_range[0]), float(r_range[1]), int(seed) & (2**64 - 1),
+                                            float(photons), float(read_sigma), frames.data_ptr(),
+                                            truth.data_ptr(), st.cuda_stream))
+    return frames, truth[:, :int(count)].cpu().numpy()

@@ -22,11 +22,13 @@ def test_runtime_errors_exit_2(tmp_path, capsys):
     assert cli.main(["detect", "--input", str(tmp_path / "missing.raw")] + common) == 2
     (tmp_path / "short.raw").write_bytes(b"\x01\x02\x03")
     assert cli.main(["detect", "--input", str(tmp_path / "short.raw")] + common) == 2
-    assert cli.main(["evaluate"]) == 2 and cli.main(["parity"]) == 2
+    assert cli.main(["evaluate"]) == 1 and cli.main(["parity"]) == 1          # usage errors, like the reference
+    assert cli.main(["evaluate", "--pred", str(tmp_path / "nope.json"), "--truth", str(tmp_path / "nope.csv"),
+                     "--out", str(tmp_path / "r.json")]) == 2
     assert cli.main(["simulate", "--r-min", "3", "--r-max", "9", "--seed", "1", "--out-image",
                      str(tmp_path / "s.png"), "--out-truth", str(tmp_path / "s.csv")]) == 2
     err = capsys.readouterr().err
-    assert "no such image" in err and "truncated raw header" in err and "reference package" in err
+    assert "no such image" in err and "truncated raw header" in err and "nope.json" in err
 
 
 def test_simulate_writes_the_reference_scene(tmp_path, capsys):

@@ -629,3 +629,56 @@ class TestFloat64Detector:
         det.close()
         want = golden_blobs(g, "t1_cand_")
         assert [(t[0], t[1], t[2]) for t in got] == [(t[0], t[1], t[2]) for t in want]
+
+
+class TestDeviceEvaluation:
+    """scoring and scene generation on the device for large sweeps."""
+
+    def test_device_matcher_equals_host_matcher(self):
+        from paper_2010_08486_b200 import evaluate as ev
+        from test_evaluate import random_case
+        rng = np.random.default_rng(77)
+        cases = [random_case(rng, int(rng.integers(0, 60)), int(rng.integers(0, 60)),
+                             span=25 if k % 2 else 80, integer=k % 3 == 0) for k in range(24)]
+        cases.append(random_case(rng, 1500, 1400, span=600))          # more truths than threads
+        for thr in (0.5, 0.15):
+            got = ev.match_voc_batch([c[0] for c in cases], [c[1] for c in cases], thr)
+            for (preds, truths), g in zip(cases, got):
+                assert g == ev.match_voc(preds, truths, thr)
+
+    def test_device_frames_have_the_scene_statistics(self):
+        frames, truths = synth.device_frames(6, 512, 384, 40, (3.0, 15.0), seed=5)
+        assert tuple(frames.shape) == (6, 384, 512) and truths.shape == (6, 40, 3)
+        f = frames.cpu().numpy()
+        assert np.isfinite(f).all() and f.min() >= 0.0 and 0.9 < f.max() < 1.6
+        # droplets are where the truth says: bright centres, dark background (median ~ read noise)
+        for k in range(6):
+            for x, y, r in truths[k][:10]:
+                assert f[k, int(round(y)), int(round(x))] > 0.5
+                assert 3.0 <= r <= 15.0 and r + 1 <= x <= 512 - 2 - r and r + 1 <= y <= 384 - 2 - r
+            assert np.median(f[k]) < 0.02
+        # same seed, same frames; another seed, other frames
+        again, _ = synth.device_frames(6, 512, 384, 40, (3.0, 15.0), seed=5)
+        other, _ = synth.device_frames(6, 512, 384, 40, (3.0, 15.0), seed=6)
+        assert torch_equal(frames, again) and not torch_equal(frames, other)
+        # noise-free frames reproduce the host painter's sphere caps
+        clean, tr = synth.device_frames(1, 256, 256, 8, (4.0, 12.0), seed=9, photons=0.0, read_sigma=0.0)
+        host = np.zeros((256, 256), np.float32)
+        for x, y, r in tr[0]:
+            synth.paint_droplet(host, synth.Droplet(x, y, r))
+        assert np.abs(clean[0].cpu().numpy() - host).max() < 1e-6
+
+    def test_detection_scores_on_device_frames(self):
+        """end to end on the device: generate, detect (resident frames), score - the droplets are found"""
+        from paper_2010_08486_b200 import evaluate as ev
+        frames, truths = synth.device_frames(4, 512, 512, 30, (4.0, 14.0), seed=11)
+        det = P.Detector(P.DetectionParams(min_sigma=2.0, max_sigma=12.0, n_bin=20, preprocess=False))
+        blobs = [det.run(frames[k]).blobs for k in range(4)]
+        det.close()
+        reps = ev.match_voc_batch(blobs, [[synth.Droplet(*t) for t in truths[k]] for k in range(4)], 0.5)
+        assert all(r.recall > 0.6 and r.precision > 0.6 for r in reps), [(r.precision, r.recall) for r in reps]
+
+
+def torch_equal(a, b):
+    import torch
+    return bool(torch.equal(a, b))
