@@ -18,7 +18,7 @@ namespace dogblob {
 
 namespace {
 
-constexpr int kMaxSmoothRadius = 63;
+constexpr int kMaxSmoothRadius = 255;     // smooth_sigma <= 50 (the service's bound): radius int(5 sigma + 0.5) <= 250
 
 struct SmoothWeights {
     double w[kMaxSmoothRadius + 1];   // w[0] centre ... w[radius]
@@ -205,7 +205,7 @@ int dogblob_preprocess(int height, int width, const float *d_src, int64_t src_pi
     DB_REQUIRE(height >= 1 && width >= 1, "expected a non-empty 2-D image");
     DB_REQUIRE(d_src && weights && d_scratch && d_dst, "NULL argument");
     DB_REQUIRE(radius >= 0 && radius <= kMaxSmoothRadius,
-               "smoothing radius above 63 (smooth_sigma > 12.5) is not supported");
+               "smoothing radius above 255 (smooth_sigma > 51) is not supported");
     DB_REQUIRE(src_pitch >= width && dst_pitch >= width, "pitch smaller than the image width");
     const int64_t n = (int64_t)height * width;
     DB_REQUIRE(rank_lo >= 0 && rank_lo < n && rank_hi >= 0 && rank_hi < n, "rank out of range");

@@ -393,7 +393,8 @@ class TestPreprocess:
 
     @pytest.mark.parametrize("shape,sigma,sat", [((97, 131), 1.0, 0.0035), ((64, 200), 2.3, 0.01),
                                                   ((33, 47), 0.0, 0.0), ((1, 50), 1.0, 0.1),
-                                                  ((300, 1), 0.7, 0.3)])
+                                                  ((300, 1), 0.7, 0.3), ((120, 90), 20.0, 0.02),
+                                                  ((64, 64), 50.0, 0.0035)])      # radius 100 / 250: wider than the image
     def test_preprocess_against_oracle(self, shape, sigma, sat):
         rng = np.random.default_rng(shape[0] + shape[1])
         img = (rng.random(shape) ** 3).astype(np.float32)
