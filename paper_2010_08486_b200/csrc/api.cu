@@ -81,6 +81,7 @@ struct dogblob_plan {
     float *d_toeplitz = nullptr;
     int *d_umma_sched = nullptr;   // tensor-core column pass: unit of (slot, CTA), -1 = none (see plan_umma_schedule)
     int umma_sched_slots = 0, umma_sched_ctas = 0;
+    int umma_ctas = 0;             // persistent CTAs of the tensor-core passes (SMs minus the spare ones)
     double *d_slice_sigma = nullptr;
     float *d_sigma_f32 = nullptr;
     // workspace layout (bytes from the workspace base)
@@ -380,6 +381,13 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
     {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        // The persistent passes leave `spare` SMs free: their CTAs fill an SM's shared memory, so the small
+        // kernels of OTHER frames (other streams: single-CTA finalize, plateau, counters) could otherwise only
+        // run in the gaps between two passes.  DOGBLOB_UMMA_SPARE_SMS overrides (plan time only).
+        int spare = 1;
+        if (const char *es = std::getenv("DOGBLOB_UMMA_SPARE_SMS")) spare = std::max(0, std::atoi(es));
+        sms = std::max(1, sms - spare);
+        plan->umma_ctas = sms;
         const char *ec = std::getenv("DOGBLOB_UMMA_LEVEL_COST");       // plan time only
         const char *eg = std::getenv("DOGBLOB_UMMA_GROUPS");
         usched = plan_umma_schedule(plan->levels, tiles, std::min(sms, tiles * std::max(1, n_levels - 1)),
@@ -514,7 +522,7 @@ static cudaError_t row_pass_any(const dogblob_plan *plan, const float *d_image, 
         cudaError_t e = launch_prep_umma(plan->geo, d_image, ws + plan->off_x, mx, st);
         if (e != cudaSuccess) return e;
         return launch_row_pass_umma(plan->geo, ws + plan->off_x, ws + plan->off_rows_t, plan->table,
-                                    plan->toeplitz, plan->d_toeplitz, st, mx);
+                                    plan->toeplitz, plan->d_toeplitz, st, mx, plan->umma_ctas);
     }
     return launch_row_pass(plan->geo, d_image, reinterpret_cast<float *>(ws + plan->off_rows_t), plan->table,
                            plan->d_taps, st, gate);

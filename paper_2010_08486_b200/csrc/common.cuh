@@ -177,7 +177,7 @@ cudaError_t launch_prep_umma(const ConvGeometry &g, const float *d_img, void *d_
                              cudaStream_t st);
 cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d_r, const LevelTable &tbl,
                                  const ToeplitzTable &ttab, const float *d_toep, cudaStream_t st,
-                                 const uint32_t *d_max_bits);
+                                 const uint32_t *d_max_bits, int max_ctas = 0);
 // DoG slices [L - 1][Hp][Wp] in image orientation (levels = true: the L levels themselves)
 cudaError_t launch_col_pass_umma(const ConvGeometry &g, const void *d_r, float *d_out, const LevelTable &tbl,
                                  const ToeplitzTable &ttab, const float *d_toep, cudaStream_t st,

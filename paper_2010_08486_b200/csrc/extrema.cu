@@ -193,17 +193,32 @@ __device__ __forceinline__ void nms_strip(const Volume &vol, float thr, bool tra
     const bool edge_lane = (lane == 0) || (lane == 31);
     const int halo_col = lane == 0 ? c - 1 : c + 4;
     const bool halo_ok = edge_lane && halo_col >= 0 && halo_col < vol.cols;
-    const float *p = vol.data + (int64_t)s * vol.plane + (int64_t)(r_first - 1) * vol.pitch + c;
+    const int halo_off = lane == 0 ? -1 : 4;
     const float ninf = -INFINITY;
+    // rows outside the plane are never loaded either: fold the bounds into the row mask once
+    // (local row l is plane row r_first - 1 + l), so that the streaming loop tests one mask bit per row
+    {
+        const int first_ok = r_first == 0 ? 1 : 0;                             // local row 0 is row -1 of the plane
+        const int n_ok = min(kBandRows + 2, vol.rows - (r_first - 1));         // local rows below this are inside
+        unsigned long long inside = (n_ok >= 64 ? ~0ull : (1ull << n_ok) - 1ull);
+        if (first_ok) inside &= ~1ull;
+        need &= inside;
+    }
+    // three running row pointers (one per ring slot), advanced by kGroup rows per group
+    const int64_t step = (int64_t)kGroup * vol.pitch;
+    const float *pr[kGroup];
+#pragma unroll
+    for (int k = 0; k < kGroup; ++k)
+        pr[k] = vol.data + (int64_t)s * vol.plane + (int64_t)(r_first - 1 + k) * vol.pitch + c;
 
-    const bool ragged = nvalid < 4;                         // only in the last strip of a plane
-    auto load_row = [&](int r, const float *ptr) -> RowRegs {
+    const bool strip_ragged = (c - 4 * (int)lane) + 128 > vol.cols;             // warp uniform: the plane's last strip
+    auto load_row = [&](bool wanted, const float *ptr) -> RowRegs {
         RowRegs o;
         o.q = make_float4(ninf, ninf, ninf, ninf);
         o.halo = ninf;
-        if ((unsigned)r < (unsigned)vol.rows && ((need >> (r - (r_first - 1))) & 1ull)) {
+        if (wanted) {
             if (nvalid > 0) o.q = __ldg(reinterpret_cast<const float4 *>(ptr));   // pitch-padded: in bounds
-            if (halo_ok) o.halo = __ldg(ptr + (lane == 0 ? -1 : 4));
+            if (halo_ok) o.halo = __ldg(ptr + halo_off);
         }
         return o;
     };
@@ -213,11 +228,11 @@ __device__ __forceinline__ void nms_strip(const Volume &vol, float thr, bool tra
     float w[3][6];
     auto widen = [&](const RowRegs &g, float (&o)[6]) {
         float4 q = g.q;
-        if (ragged) {
+        if (strip_ragged) {
             if (nvalid < 1) q.x = ninf;
             if (nvalid < 2) q.y = ninf;
             if (nvalid < 3) q.z = ninf;
-            q.w = ninf;
+            if (nvalid < 4) q.w = ninf;
         }
         const float l = __shfl_up_sync(0xffffffffu, q.w, 1);
         const float rgt = __shfl_down_sync(0xffffffffu, q.x, 1);
@@ -235,8 +250,11 @@ __device__ __forceinline__ void nms_strip(const Volume &vol, float thr, bool tra
     // it has moved into the window
     RowRegs ring[kGroup];
 #pragma unroll
-    for (int k = 0; k < kGroup; ++k) ring[k] = load_row(r_first - 1 + k, p + (int64_t)k * vol.pitch);
-    p += (int64_t)kGroup * vol.pitch;
+    for (int k = 0; k < kGroup; ++k) {
+        ring[k] = load_row((need >> k) & 1ull, pr[k]);
+        pr[k] += step;
+    }
+    unsigned long long ahead = need >> kGroup;             // bit k: the row that ring[k] loads next
 #pragma unroll
     for (int k = 0; k < 6; ++k) { w[0][k] = ninf; w[1][k] = ninf; w[2][k] = ninf; }
 
@@ -244,6 +262,8 @@ __device__ __forceinline__ void nms_strip(const Volume &vol, float thr, bool tra
     static_assert((kBandRows + 2) % kGroup == 0, "band + halo rows must be whole groups");
     const unsigned lt = (1u << lane) - 1u;
     const int rows_here = min(kBandRows, vol.rows - r_first);    // tested local rows are 1 .. rows_here
+    // bit k + 1: is the row tested at step k of the current group (local row rg + k - 1) inside 1 .. rows_here?
+    unsigned long long live_bits = ((rows_here >= 63 ? ~0ull : (1ull << (rows_here + 1)) - 1ull) & ~1ull) << 2;
     int g = 0;
     while (true) {
 #pragma unroll 1
@@ -259,11 +279,13 @@ __device__ __forceinline__ void nms_strip(const Volume &vol, float thr, bool tra
                 // (skipping the widening / the test of rows outside the hit blocks with uniform branches
                 // on the row masks was measured: 30 % SLOWER, the branches break the unrolled rotation)
                 widen(ring[k], dn);
-                if (g + 1 < n_groups)
-                    ring[k] = load_row(r_first - 1 + rg + kGroup + k, p + (int64_t)k * vol.pitch);
+                if (g + 1 < n_groups) {
+                    ring[k] = load_row((ahead >> k) & 1ull, pr[k]);
+                    pr[k] += step;
+                }
                 const int rl = rg + k - 1;
                 const float top = fmaxf(fmaxf(mid[1], mid[2]), fmaxf(mid[3], mid[4]));
-                const bool live = (unsigned)(rl - 1) < (unsigned)rows_here;
+                const bool live = (live_bits >> (k + 1)) & 1ull;
                 if (!__any_sync(0xffffffffu, live && top > thr)) continue;
                 // max over the 8 in-slice neighbours of voxel v: columns v and v+2 whole, column
                 // v+1 without the centre
@@ -288,7 +310,8 @@ __device__ __forceinline__ void nms_strip(const Volume &vol, float thr, bool tra
                     qcount += __popc(m);
                 }
             }
-            p += (int64_t)kGroup * vol.pitch;
+            ahead >>= kGroup;
+            live_bits >>= kGroup;
         }
         // ---- resolve the queued maxima (cross-slice test, plateau test, append) ----
         __syncwarp();

@@ -527,7 +527,8 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                     }
                     // A commit stalls the issuing thread (~250 cycles, the tensor pipe runs dry behind
                     // it: tools/ubench_umma_commit.cu), hence stages of 4 k-steps in both passes.
-                    // (Releasing pass-1 stages of 2 k-steps in pairs was slower than one by one.)
+                    // (Releasing stages in pairs - one commit per 8 k-steps - is slower in both passes: the
+                    // later release costs more than the saved bubble.)
                     umma_commit_1t(smem_u32(&ctl->data_empty[sl]));
                     if (++sl == (uint32_t)S) { sl = 0; sl_par ^= 1u; }
                 }
@@ -1042,13 +1043,14 @@ cudaError_t launch_prep_umma(const ConvGeometry &g, const float *d_img, void *d_
 // pass 1: X planes -> R planes (level rows in frame-scaled fp16 hi | lo, halo columns mirrored)
 cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d_r, const LevelTable &tbl,
                                  const ToeplitzTable &ttab, const float *d_toep, cudaStream_t st,
-                                 const uint32_t *d_max_bits) {
+                                 const uint32_t *d_max_bits, int max_ctas) {
     const UmmaLayout l = umma_layout(g);
     UmmaArgs a{};
     a.tiles_x = g.Wp / kUT; a.tiles_y = g.Hp / kUT;
     a.by_order = 1;                       // independent levels: finest units, longest first
     a.n_units = a.tiles_x * a.tiles_y * tbl.n_levels;
     a.n_sched = a.n_units;
+    a.n_ctas = max_ctas > 0 ? std::min(max_ctas, a.n_units) : 0;
     a.H = g.H; a.W = g.W; a.Hp = g.Hp; a.Wp = g.Wp; a.Py = l.Py; a.Ppad = l.Ppad;
     a.r_pitch = l.Wq; a.r_plane = (int64_t)g.L * g.Hp * l.Wq;
     a.r_base = reinterpret_cast<__half *>(d_r);

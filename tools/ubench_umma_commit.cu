@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const Args a) {
     __shared__ __align__(8) unsigned long long seq[2];
     const int warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 9; ++i) mbar_init(smem_u32(&bar[i]), (i == 8 && a.waiter == 4) ? 2 : 1);
+        for (int i = 0; i < 9; ++i) mbar_init(smem_u32(&bar[i]), (i == 8 && a.waiter >= 4) ? 2 : 1);
         mbar_init(smem_u32(&seq[0]), 1); mbar_init(smem_u32(&seq[1]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -160,6 +160,25 @@ __global__ void __launch_bounds__(128, 1) commit_kernel(const Args a) {
         while (!mbar_try_wait(smem_u32(&bar[8]), 0)) {}
         const long long t2 = clock64();
         if (blockIdx.x == 0 && threadIdx.x == 0) { a.cycles[0] = t1 - t0; a.cycles[1] = t2 - t0; }
+    } else if ((warp == 0 || warp == 1) && a.waiter == 5) {
+        // two INDEPENDENT issuer warps: each owns an accumulator pair and its own barriers, no hand-over
+        const uint32_t a_lo = ((smem_u32(smem) & 0x3ffffu) >> 4) | ((128u >> 4) << 16);
+        const uint32_t b_lo = ((smem_u32(smem + 32768) & 0x3ffffu) >> 4) | ((128u >> 4) << 16);
+        const uint32_t upper = (256u >> 4) | (1u << 14);
+        const uint32_t acc = tmem + 256u * (uint32_t)warp;
+        const long long t0 = clock64();
+        for (int it = warp; it < a.iters; it += 2) {
+            for (int m = 0; m < a.mmas; ++m) {
+                const uint32_t w = a_lo + 32u * (uint32_t)(m & 7);
+                umma_f16_triple_ss(acc, acc + 128, w, w + 1024, b_lo + 16u * (uint32_t)(m & 3), b_lo + 512, upper, upper, idesc, 1);
+            }
+            for (int k = 0; k < a.commits; ++k) umma_commit_elect(smem_u32(&bar[(it & 3) * 2 + (k & 1)]));
+        }
+        const long long t1 = clock64();
+        umma_commit_elect(smem_u32(&bar[8]));     // count 2 in this mode
+        while (!mbar_try_wait(smem_u32(&bar[8]), 0)) {}
+        const long long t2 = clock64();
+        if (blockIdx.x == 0 && threadIdx.x == 0) { a.cycles[0] = t1 - t0; a.cycles[1] = t2 - t0; }
     } else if (threadIdx.x == 9999) {
         const uint32_t total = (uint32_t)a.iters * a.commits;
         for (uint32_t c = 0; c < total; ++c)
@@ -190,7 +209,8 @@ int main() {
     // kernel-style: k-steps of 3 MMAs (192 cycles of tensor pipe each)
     const int cfg2[][3] = {{0, 1, 2}, {1, 0, 2}, {2, 0, 2}, {4, 0, 2}, {1, 1, 2}, {2, 1, 2}, {4, 1, 2}, {8, 1, 2}, {16, 1, 2},
                            {2, 1, 3}, {4, 1, 3}, {4, 0, 3}, {2, 2, 2}, {4, 3, 2},
-                           {1, 1, 4}, {2, 1, 4}, {4, 1, 4}, {2, 0, 4}, {2, 2, 4}};
+                           {1, 1, 4}, {2, 1, 4}, {4, 1, 4}, {2, 0, 4}, {2, 2, 4},
+                           {2, 0, 5}, {2, 1, 5}, {4, 1, 5}, {4, 0, 5}, {8, 1, 5}};
     for (auto &c : cfg2) {
         Args a{1000, c[0], c[1], c[2], d_cyc};
         for (int rep = 0; rep < 2; ++rep) {
@@ -200,7 +220,7 @@ int main() {
         long long h[2];
         CK(cudaMemcpy(h, d_cyc, 16, cudaMemcpyDeviceToHost));
         printf("warp issue (%s): %2d k-steps (3 MMAs each) + %d commits: issue %.1f cyc/group, complete %.1f cyc/group (MMA floor %d)\n",
-               c[2] == 2 ? "rolled" : c[2] == 4 ? "two issuers" : "unrolled", c[0], c[1], h[0] / 1000.0, h[1] / 1000.0, c[0] * 192);
+               c[2] == 2 ? "rolled" : c[2] == 4 ? "two issuers" : c[2] == 5 ? "two independent issuers" : "unrolled", c[0], c[1], h[0] / 1000.0, h[1] / 1000.0, c[0] * 192);
     }
     return 0;
 }
