@@ -43,7 +43,7 @@ sys.path.insert(0, str(ROOT))
 WORKLOAD = "C2"
 BATCH = int(os.environ.get("DOGBLOB_BENCH_BATCH", "256"))   # frames per GPU per step (the C3 batch)
 KERNELS_PER_FRAME = 8    # FP32 engine: reset, row pass, column+DoG, edge DoG, nms, plateau, finalize_small, prune_large
-KERNELS_PER_FRAME_TENSOR = 9   # tensor engine: reset, frame max, operand split, row pass, column+DoG, nms, plateau, finalize_small, prune_large
+KERNELS_PER_FRAME_TENSOR = 8   # tensor engine: frame max (+ counter reset), operand split, row pass, column+DoG, nms, plateau, finalize_small, prune_large
 METRIC = "frames/sec, 1024x1024 DoG detector (sigma<=30, n_bin=58)"
 
 

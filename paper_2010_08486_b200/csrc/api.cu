@@ -467,7 +467,7 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
         plan->off_edge = off;   off += align_up(plane * 2 * g.G, 256);    // boundary levels
     }
     plan->off_blobspace = off; off += blobspace_bytes(max_blobs);
-    plan->off_gate = off;   off += 256;                                   // streamed upload: gate word
+    plan->off_gate = off;   off += 4096;                                  // streamed upload: gate word; +64: frame max word + partial maxima
     plan->off_flags = off;  off += align_up(hit_flag_bytes(n_levels, g.Hp, g.Wp), 256);   // tensor engine: hit blocks
     plan->total = off;
     *out = plan;
@@ -514,12 +514,13 @@ static uint32_t *frame_max_word(const dogblob_plan *plan, void *d_workspace) {
 }
 // Scale-space pass 1 on the plan's engine: the tensor-core Toeplitz GEMM (scale_space_umma.cu:
 // frame -> fp16 hi | lo planes -> level rows) or the FP32 sliding-window kernel (scale_space.cu).
+// `reset` (tensor engine only): the frame's counters are cleared by the first kernel of the pass
 static cudaError_t row_pass_any(const dogblob_plan *plan, const float *d_image, void *d_workspace,
-                                cudaStream_t st, const RowGate *gate) {
+                                cudaStream_t st, const RowGate *gate, const BlobSpace *reset = nullptr) {
     char *ws = reinterpret_cast<char *>(d_workspace);
     if (plan->use_umma) {
         uint32_t *mx = frame_max_word(plan, d_workspace);
-        cudaError_t e = launch_prep_umma(plan->geo, d_image, ws + plan->off_x, mx, st);
+        cudaError_t e = launch_prep_umma(plan->geo, d_image, ws + plan->off_x, mx, st, reset);
         if (e != cudaSuccess) return e;
         return launch_row_pass_umma(plan->geo, ws + plan->off_x, ws + plan->off_rows_t, plan->table,
                                     plan->toeplitz, plan->d_toeplitz, st, mx, plan->umma_ctas);
@@ -569,8 +570,8 @@ static int launch_frame_head(const dogblob_plan *plan, const float *d_image, voi
     char *ws = reinterpret_cast<char *>(d_workspace);
     BlobSpace bs = carve_blobspace(ws + plan->off_blobspace, plan->max_blobs);
     if (events) DB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(events[0]), st));
-    DB_CUDA(launch_reset_counters(bs, st));
-    DB_CUDA(row_pass_any(plan, d_image, d_workspace, st, gate));
+    if (!plan->use_umma) DB_CUDA(launch_reset_counters(bs, st));     // tensor engine: folded into its first kernel
+    DB_CUDA(row_pass_any(plan, d_image, d_workspace, st, gate, plan->use_umma ? &bs : nullptr));
     if (events) DB_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(events[1]), st));
     return DOGBLOB_OK;
 }

@@ -174,7 +174,8 @@ void build_toeplitz(const LevelDesc *lv, int n_levels, const float2 *taps, std::
                     ToeplitzTable &tab);
 cudaError_t configure_umma_kernels(int device);
 cudaError_t launch_prep_umma(const ConvGeometry &g, const float *d_img, void *d_x, uint32_t *d_max_bits,
-                             cudaStream_t st);
+                             cudaStream_t st, const BlobSpace *bs = nullptr);
+int umma_max_words();      // uint32 words behind d_max_bits: the frame's max + the partial maxima
 cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d_r, const LevelTable &tbl,
                                  const ToeplitzTable &ttab, const float *d_toep, cudaStream_t st,
                                  const uint32_t *d_max_bits, int max_ctas = 0);

@@ -279,12 +279,12 @@ __device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
         ::"r"(bar) : "memory");
 }
 // exponent e with max|x| * 2^e in [2^12, 2^13) (0 for an all-zero, NaN or Inf frame)
-__device__ __forceinline__ int frame_scale_exp(const uint32_t *max_bits) {
-    const uint32_t b = __ldcg(max_bits);
+__device__ __forceinline__ int frame_scale_exp_bits(uint32_t b) {
     const int ex = (int)((b >> 23) & 0xffu);
     if (ex == 0 || ex == 255) return 0;
     return max(-100, min(100, 12 - (ex - 127)));       // the scale itself must stay a normal float
 }
+__device__ __forceinline__ int frame_scale_exp(const uint32_t *max_bits) { return frame_scale_exp_bits(__ldcg(max_bits)); }
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((uint32_t)(127 + e) << 23); }
 // two floats -> packed f16x2 (first argument in the LOW half)
 __device__ __forceinline__ uint32_t pack_f16x2(float lo_elem, float hi_elem) {
@@ -803,11 +803,36 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
     if (a.prof != nullptr && threadIdx.x == 0) atomicMax(a.prof + 19, globaltimer_ns());      // last CTA out
 }
 
+constexpr int kMaxParts = 256;          // partial maxima of frame_max_kernel (one per CTA)
+
+// max |x| over the partial maxima of frame_max_kernel, as float bits (non-negative floats order like
+// unsigned integers); every CTA of the consumer reduces the <= 256 words itself: no atomics, no memset
+__device__ __forceinline__ uint32_t reduce_parts(const uint32_t *__restrict__ parts, int n_parts) {
+    __shared__ uint32_t s_m[8];
+    __shared__ uint32_t s_all;
+    uint32_t m = (int)threadIdx.x < n_parts ? __ldcg(parts + threadIdx.x) : 0u;
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t a = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) a = max(a, s_m[i]);
+        s_all = a;
+    }
+    __syncthreads();
+    return s_all;
+}
+
 // Frame -> fp16 hi | lo planes [2][H + 2 Py][Wp] in frame-scaled units, reflected halo rows
-// materialised (row r of the planes = frame row fold(r - Py)), pad columns x >= W zero.
-__global__ void prep_split_kernel(const float *__restrict__ img, int64_t pitch, int H, int W, int Wp, int Py,
-                                  const uint32_t *__restrict__ max_bits, __half *__restrict__ xp) {
-    const float xscale = pow2f(frame_scale_exp(max_bits));
+// materialised (row r of the planes = frame row fold(r - Py)), pad columns x >= W zero.  Also
+// publishes the frame's max |x| word for the passes that follow.
+__global__ void __launch_bounds__(256)
+prep_split_kernel(const float *__restrict__ img, int64_t pitch, int H, int W, int Wp, int Py,
+                  const uint32_t *__restrict__ parts, int n_parts, uint32_t *__restrict__ max_bits,
+                  __half *__restrict__ xp) {
+    const uint32_t mbits = reduce_parts(parts, n_parts);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *max_bits = mbits;
+    const float xscale = pow2f(frame_scale_exp_bits(mbits));
     const int rows = H + 2 * Py, groups = Wp / 8;
     const int64_t plane = (int64_t)rows * Wp;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)rows * groups;
@@ -832,18 +857,34 @@ __global__ void prep_split_kernel(const float *__restrict__ img, int64_t pitch, 
     }
 }
 
-// max |x| of the frame as float bits (non-negative floats order like unsigned integers)
-__global__ void frame_max_kernel(const float *__restrict__ img, int64_t n4, uint32_t *__restrict__ max_bits) {
+// per-CTA max |x| of the frame -> parts[blockIdx.x]; CTA 0 also resets the frame's counters
+// (reset_counters_kernel folded in: one launch less in front of every frame)
+__global__ void __launch_bounds__(256)
+frame_max_kernel(const float *__restrict__ img, int64_t n4, uint32_t *__restrict__ parts, Counters *ctr, int *ctl) {
+    __shared__ float s_m[8];
+    if (blockIdx.x == 0 && ctr != nullptr) {
+        if (threadIdx.x == 0) {
+            Counters z = {};
+            z.t_start = globaltimer_ns();
+            *ctr = z;
+        }
+        if (threadIdx.x < 8) ctl[threadIdx.x] = 0;      // ticket, done, n_phases, ... of the pruning control block
+    }
     float m = 0.f;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
         const float4 v = __ldg(reinterpret_cast<const float4 *>(img) + i);
         m = fmaxf(fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))), m);
     }
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(max_bits, __float_as_uint(m));
+    if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < 8; ++i) m = fmaxf(m, s_m[i]);
+        // NaN compares false everywhere above: a NaN frame yields the max of its other pixels (scale only)
+        parts[blockIdx.x] = m > 0.f ? __float_as_uint(m) : 0u;
+    }
 }
 
-// rows of one compact Toeplitz array: the window of k-step j starts at row 16 j and spans 128 + 8 rows
 int toeplitz_rows(int rpad) { return kUT + 2 * rpad - 16 + kUT + 8; }
 // one Toeplitz buffer in shared memory: pass 2 (Toeplitz = B operand, band trimmed) never reads the
 // last 112 rows of the arrays and does not copy them
@@ -1027,18 +1068,23 @@ cudaError_t configure_umma_kernels(int device) {
 }
 
 // frame -> max |x| -> fp16 hi | lo planes with reflected halo rows (d_x: umma_layout().x_bytes)
+// d_max_bits: the frame's max word followed by kMaxParts partial words (umma_max_words() uint32 in all);
+// bs (optional): the frame's counters are reset by the first kernel
 cudaError_t launch_prep_umma(const ConvGeometry &g, const float *d_img, void *d_x, uint32_t *d_max_bits,
-                             cudaStream_t st) {
+                             cudaStream_t st, const BlobSpace *bs) {
     const UmmaLayout l = umma_layout(g);
-    cudaError_t e = cudaMemsetAsync(d_max_bits, 0, sizeof(uint32_t), st);
-    if (e != cudaSuccess) return e;
-    frame_max_kernel<<<148, 256, 0, st>>>(d_img, (int64_t)g.H * g.Wp / 4, d_max_bits);
+    const int64_t n4 = (int64_t)g.H * g.Wp / 4;
+    const int parts = (int)std::min<int64_t>(kMaxParts, std::max<int64_t>(1, n4 / 1024));
+    uint32_t *d_parts = d_max_bits + 1;
+    frame_max_kernel<<<parts, 256, 0, st>>>(d_img, n4, d_parts, bs ? bs->ctr : nullptr,
+                                            bs ? reinterpret_cast<int *>(bs->ctl) : nullptr);
     const int64_t items = (int64_t)(g.H + 2 * l.Py) * (g.Wp / 8);
     const int blocks = (int)std::min<int64_t>((items + 255) / 256, 148 * 8);
-    prep_split_kernel<<<blocks, 256, 0, st>>>(d_img, g.Wp, g.H, g.W, g.Wp, l.Py, d_max_bits,
+    prep_split_kernel<<<blocks, 256, 0, st>>>(d_img, g.Wp, g.H, g.W, g.Wp, l.Py, d_parts, parts, d_max_bits,
                                               reinterpret_cast<__half *>(d_x));
     return cudaGetLastError();
 }
+int umma_max_words() { return 1 + kMaxParts; }
 
 // pass 1: X planes -> R planes (level rows in frame-scaled fp16 hi | lo, halo columns mirrored)
 cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d_r, const LevelTable &tbl,
