@@ -263,6 +263,28 @@ __device__ __forceinline__ void umma_f16_triple_ss_1t(uint32_t d_main, uint32_t 
           "r"(b_upper), "r"(idesc), "r"(acc)
         : "memory");
 }
+// Pass 1: the hi and lo planes of a data stage are consecutive N blocks of ONE MN-major operand, and
+// the small accumulator sits right behind the main one, so  main (+)= A_hi * B_hi  and
+// small (+)= A_hi * B_lo  are a single MMA with N = 256 (the Toeplitz window is read once for both:
+// 20 instead of 24 KB of operand reads per k-step, two instructions instead of three); then
+// small += A_lo * B_hi  (N = 128).
+__device__ __forceinline__ void umma_f16_wide_pair_ss_1t(uint32_t d_main, uint32_t a_hi, uint32_t a_lo, uint32_t b_hi,
+                                                         uint32_t a_upper, uint32_t b_upper, uint32_t idesc256,
+                                                         uint32_t idesc128, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t.reg .b64 a0, a1, b0;\n\t.reg .b32 ds;\n\t"
+        "setp.ne.b32 p, %8, 0;\n\t"
+        "setp.eq.b32 q, 0, 0;\n\t"
+        "add.u32 ds, %0, 128;\n\t"
+        "mov.b64 a0, {%1, %4};\n\t"
+        "mov.b64 a1, {%2, %4};\n\t"
+        "mov.b64 b0, {%3, %5};\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a0, b0, %6, p;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [ds], a1, b0, %7, q;\n\t}"
+        ::"r"(d_main), "r"(a_hi), "r"(a_lo), "r"(b_hi), "r"(a_upper), "r"(b_upper), "r"(idesc256), "r"(idesc128),
+          "r"(acc)
+        : "memory");
+}
 __device__ __forceinline__ void umma_commit_1t(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
@@ -507,9 +529,13 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                             if (kRows) {
                                 // A = Toeplitz window, B = 16 image rows of the stage (2 KB per k-step)
                                 const uint32_t bd = ((sbase + (uint32_t)(m0 - first_k) * 128u) >> 4) | kData1LowLbo;
-                                umma_f16_triple_ss_1t(d_main, d_small, win, win + lo_off, bd, bd + ((256u * kRowsPerStage1) >> 4),
-                                                   kToepUpper, kData1Upper, instr_desc_f16(kUT, kUT, 1),
-                                                   j > 0);
+                                if (a.debug & 256)        // the three-instruction form (A/B comparison)
+                                    umma_f16_triple_ss_1t(d_main, d_small, win, win + lo_off, bd, bd + ((256u * kRowsPerStage1) >> 4),
+                                                          kToepUpper, kData1Upper, instr_desc_f16(kUT, kUT, 1), j > 0);
+                                else
+                                    umma_f16_wide_pair_ss_1t(d_main, win, win + lo_off, bd, kToepUpper, kData1Upper,
+                                                             instr_desc_f16(kUT, 2 * kUT, 1), instr_desc_f16(kUT, kUT, 1),
+                                                             j > 0);
                             } else {
                                 // A = 16 k-columns of the stage (32 B into the swizzle atom per k-step),
                                 // B = Toeplitz window rows [ns, ne)
