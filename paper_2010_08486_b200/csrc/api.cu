@@ -531,8 +531,8 @@ static cudaError_t row_pass_any(const dogblob_plan *plan, const float *d_image, 
 static HitFlags hit_flags_of(const dogblob_plan *plan, void *d_workspace) {
     HitFlags f;
     f.data = reinterpret_cast<unsigned char *>(d_workspace) + plan->off_flags;
-    f.row_blocks = plan->geo.Hp / 8;
-    f.col_blocks = plan->geo.Wp / 64;
+    f.row_blocks = plan->geo.Hp >> kFlagRowShift;
+    f.col_blocks = plan->geo.Wp >> kFlagColShift;
     return f;
 }
 // pass 2 fused with the DoG: tensor engine -> slices in image orientation, FP32 engine -> transposed.

@@ -151,12 +151,17 @@ cudaError_t launch_col_levels_pass(const ConvGeometry &g, const float *d_rows_t,
                                    cudaStream_t st);
 cudaError_t launch_edge_dog(const ConvGeometry &g, const float *d_edge, float *d_dog_t,
                             const LevelTable &tbl, cudaStream_t st);
-// which blocks of 8 rows x 64 columns of the DoG slices hold a value above the detection threshold
+// which blocks of 8 rows x 32 columns of the DoG slices hold a value above the detection threshold;
+// the tensor-core column pass only STORES the 128 x 32 boxes that contain such a block, so the flags
+// are also the validity map of the slice memory (everything else reads as -inf in the extrema kernel)
 struct HitFlags {
     unsigned char *data = nullptr;       // [slice][col_blocks][row_blocks] (row blocks contiguous)
     int row_blocks = 0, col_blocks = 0;
 };
-inline size_t hit_flag_bytes(int planes, int Hp, int Wp) { return (size_t)planes * (Hp / 8) * (Wp / 64); }
+constexpr int kFlagColShift = 5, kFlagRowShift = 3;      // 32 columns x 8 rows
+inline size_t hit_flag_bytes(int planes, int Hp, int Wp) {
+    return (size_t)planes * (Hp >> kFlagRowShift) * (Wp >> kFlagColShift);
+}
 // tensor-core (tcgen05) versions of the passes, scale_space_umma.cu
 struct ToeplitzTable {               // per level: float offset, rows, log2 of the tap scale
     int ofs[kMaxLevels];
@@ -192,9 +197,10 @@ cudaError_t configure_conv_kernels(int device);
 size_t col_pass_smem(int group_table, int max_rpad, bool dog);
 
 // extrema: NMS + compaction + plateau coalescing + ordering.  `flags` (optional): one byte per
-// 8-row x 64-column block of every slice, non-zero if the block holds a value above the threshold
-// (written by the tensor-core column pass); strips without a hit are skipped unread and inside a
-// strip only the rows next to a hit block are loaded.
+// 8-row x 32-column block of every slice, non-zero if the block holds a value above the threshold
+// (written by the tensor-core column pass, which does not store blocks without one); strips without
+// a hit are skipped unread, inside a strip only the rows next to a hit block are loaded, and every
+// block without a hit reads as -inf.
 cudaError_t launch_extrema(const float *d_slices, int S, int rows, int cols, int64_t pitch,
                            int64_t plane, bool transposed, const double *d_slice_sigma,
                            float threshold, int half, const BlobSpace &bs, cudaStream_t st,

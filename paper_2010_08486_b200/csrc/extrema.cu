@@ -27,7 +27,17 @@ struct VolumeT {
     const T *__restrict__ data;
     int S, rows, cols;           // valid extents
     int64_t pitch, plane;
+    // Optional validity map (tensor engine): one byte per 8-row x 32-column block of every slice, as
+    // HitFlags.  The producer does not even STORE blocks without a value above the threshold, so
+    // whatever the memory of such a block holds (an older frame) must read as -inf: it can never beat
+    // a candidate, which is above the threshold by definition.
+    const unsigned char *__restrict__ valid = nullptr;
+    int v_row_blocks = 0, v_col_blocks = 0;
+    __device__ __forceinline__ bool block_valid(int s, int r, int c) const {
+        return valid == nullptr || valid[((int64_t)s * v_col_blocks + (c >> kFlagColShift)) * v_row_blocks + (r >> kFlagRowShift)] != 0;
+    }
     __device__ __forceinline__ T at(int s, int r, int c) const {
+        if (!block_valid(s, r, c)) return (T)-INFINITY;
         return __ldg(data + (int64_t)s * plane + (int64_t)r * pitch + c);
     }
 };
@@ -174,20 +184,43 @@ __device__ __forceinline__ void nms_strip(const Volume &vol, float thr, bool tra
     // others only the rows of hit blocks and their two neighbours are loaded (`need`, bit = local
     // row with r_first - 1 as bit 0): a row further away is neither tested nor anybody's neighbour.
     unsigned long long need = ~0ull;                       // rows to load (local row bits)
+    unsigned long long valid_q = ~0ull, valid_h = ~0ull;   // rows whose own columns / halo column hold stored data
     if (flags.data != nullptr) {
         static_assert(kBandRows + 2 <= 64, "row mask");
-        const int cb = (c - 4 * (int)lane) >> 6;
+        const int cb = (c - 4 * (int)lane) >> kFlagColShift;
         const int r_last = min(r_first + kBandRows - 1, vol.rows - 1);
-        const unsigned char *f0 = flags.data + ((int64_t)s * flags.col_blocks + cb) * flags.row_blocks;
-        const unsigned char *f1 = cb + 1 < flags.col_blocks ? f0 + flags.row_blocks : f0;
-        unsigned long long test = 0ull;
-        for (int rb = r_first >> 3; rb <= r_last >> 3; ++rb) {
-            if (!(f0[rb] | f1[rb])) continue;
-            const int lo = max(8 * rb, r_first) - r_first + 1, hi = min(8 * rb + 7, r_last) - r_first + 1;   // local rows
-            test |= ((1ull << (hi + 1)) - 1ull) & ~((1ull << lo) - 1ull);
+        // row masks of the six 32-column blocks the strip can touch (halo left, its four quarters, halo
+        // right) over the <= 5 row blocks of its 33 rows: ONE flag load per lane (lane = 5 k + j: column
+        // block k, row block j), a ballot, and the masks are rebuilt from the ballot bits
+        unsigned long long v[6] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
+        const int rb_lo = max(r_first - 1, 0) >> 3, rb_hi = min(r_last + 1, vol.rows - 1) >> 3;
+        const int nrb = rb_hi - rb_lo + 1;
+        unsigned char f = 0;
+        {
+            const int k = (int)lane / 5, j = (int)lane % 5, cbk = cb - 1 + k;
+            if (lane < 30 && j < nrb && cbk >= 0 && cbk < flags.col_blocks)
+                f = __ldg(flags.data + ((int64_t)s * flags.col_blocks + cbk) * flags.row_blocks + rb_lo + j);
         }
+        const unsigned ball = __ballot_sync(0xffffffffu, f != 0);
+        if ((ball & 0x01ffffe0u) == 0u) return;              // no hit block in the strip's own four quarters
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            if (j >= nrb) break;
+            const int rb = rb_lo + j;
+            const int lo = max(8 * rb, r_first - 1) - (r_first - 1), hi = min(8 * rb + 7, r_last + 1) - (r_first - 1);   // local rows
+            const unsigned long long bits = ((hi + 1 >= 64 ? ~0ull : (1ull << (hi + 1)) - 1ull)) & ~((1ull << lo) - 1ull);
+#pragma unroll
+            for (int k = 0; k < 6; ++k)
+                if ((ball >> (5 * k + j)) & 1u) v[k] |= bits;
+        }
+        // tested rows are local rows 1 .. r_last - r_first + 1; a strip without a hit cannot emit anything
+        const int n_tested = r_last - r_first + 1;
+        const unsigned long long test = (v[1] | v[2] | v[3] | v[4]) & (((1ull << (n_tested + 1)) - 1ull) & ~1ull);
         if (test == 0ull) return;
         need = test | (test << 1) | (test >> 1);
+        const unsigned quarter = lane >> 3;
+        valid_q = quarter == 0 ? v[1] : quarter == 1 ? v[2] : quarter == 2 ? v[3] : v[4];
+        valid_h = lane == 0 ? v[0] : v[5];
     }
     const int nvalid = min(max(vol.cols - c, 0), 4);       // valid columns of this lane
     const bool edge_lane = (lane == 0) || (lane == 31);
@@ -212,14 +245,15 @@ __device__ __forceinline__ void nms_strip(const Volume &vol, float thr, bool tra
         pr[k] = vol.data + (int64_t)s * vol.plane + (int64_t)(r_first - 1 + k) * vol.pitch + c;
 
     const bool strip_ragged = (c - 4 * (int)lane) + 128 > vol.cols;             // warp uniform: the plane's last strip
-    auto load_row = [&](bool wanted, const float *ptr) -> RowRegs {
+    // needq / needh: rows this lane loads its four columns / its halo column from (wanted by the strip AND
+    // stored by the producer: blocks without a hit were never written and read as -inf)
+    const unsigned long long needq = need & valid_q, needh = need & valid_h;
+    auto load_row = [&](bool want_q, bool want_h, const float *ptr) -> RowRegs {
         RowRegs o;
         o.q = make_float4(ninf, ninf, ninf, ninf);
         o.halo = ninf;
-        if (wanted) {
-            if (nvalid > 0) o.q = __ldg(reinterpret_cast<const float4 *>(ptr));   // pitch-padded: in bounds
-            if (halo_ok) o.halo = __ldg(ptr + halo_off);
-        }
+        if (want_q && nvalid > 0) o.q = __ldg(reinterpret_cast<const float4 *>(ptr));   // pitch-padded: in bounds
+        if (want_h && halo_ok) o.halo = __ldg(ptr + halo_off);
         return o;
     };
     // window rows as [left, x, y, z, w, right]; the three rows rotate through w[0..2]
@@ -251,10 +285,10 @@ __device__ __forceinline__ void nms_strip(const Volume &vol, float thr, bool tra
     RowRegs ring[kGroup];
 #pragma unroll
     for (int k = 0; k < kGroup; ++k) {
-        ring[k] = load_row((need >> k) & 1ull, pr[k]);
+        ring[k] = load_row((needq >> k) & 1ull, (needh >> k) & 1ull, pr[k]);
         pr[k] += step;
     }
-    unsigned long long ahead = need >> kGroup;             // bit k: the row that ring[k] loads next
+    unsigned long long ahead_q = needq >> kGroup, ahead_h = needh >> kGroup;      // bit k: the row that ring[k] loads next
 #pragma unroll
     for (int k = 0; k < 6; ++k) { w[0][k] = ninf; w[1][k] = ninf; w[2][k] = ninf; }
 
@@ -280,7 +314,7 @@ __device__ __forceinline__ void nms_strip(const Volume &vol, float thr, bool tra
                 // on the row masks was measured: 30 % SLOWER, the branches break the unrolled rotation)
                 widen(ring[k], dn);
                 if (g + 1 < n_groups) {
-                    ring[k] = load_row((ahead >> k) & 1ull, pr[k]);
+                    ring[k] = load_row((ahead_q >> k) & 1ull, (ahead_h >> k) & 1ull, pr[k]);
                     pr[k] += step;
                 }
                 const int rl = rg + k - 1;
@@ -310,7 +344,8 @@ __device__ __forceinline__ void nms_strip(const Volume &vol, float thr, bool tra
                     qcount += __popc(m);
                 }
             }
-            ahead >>= kGroup;
+            ahead_q >>= kGroup;
+            ahead_h >>= kGroup;
             live_bits >>= kGroup;
         }
         // ---- resolve the queued maxima (cross-slice test, plateau test, append) ----
@@ -586,6 +621,11 @@ cudaError_t launch_extrema(const float *d_slices, int S, int rows, int cols, int
                            int64_t plane, bool transposed, const double *d_slice_sigma,
                            float threshold, int half, const BlobSpace &bs, cudaStream_t st, HitFlags flags) {
     Volume vol{d_slices, S, rows, cols, pitch, plane};
+    if (flags.data != nullptr) {
+        vol.valid = flags.data;
+        vol.v_row_blocks = flags.row_blocks;
+        vol.v_col_blocks = flags.col_blocks;
+    }
     const bool vec4 = (pitch % 4 == 0) && (plane % 4 == 0) &&
                       ((reinterpret_cast<uintptr_t>(d_slices) & 15u) == 0);
     const dim3 grid((cols + kNmsCols - 1) / kNmsCols, (rows + kNmsRows - 1) / kNmsRows, S);

@@ -424,6 +424,7 @@ struct SharedCtl {
     unsigned long long acc_full[2], acc_empty[2];
     uint32_t tmem_base;
     uint32_t pad[3];
+    uint32_t box_hit[2][2][4];      // pass 2: [store round parity][column half][drain warp] ballots "above the threshold"
 };
 static_assert(sizeof(SharedCtl) <= 1024, "control block");
 
@@ -764,9 +765,15 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                     const bool emit = MODE == kModeLevels || level > un.lb;
                     const float sig = MODE == kModeDog && level > un.lb ? tbl.lv[level - 1].sigma_f32 : 0.f;
                     const int out_plane = MODE == kModeLevels ? level : level - 1;
-                    bool hit = false;
+                    // With a threshold (detection), a 128 x 32 box of the slice in which nothing exceeds it is
+                    // not even stored: the extrema kernel reads blocks without a hit as -inf (HitFlags double
+                    // as the validity map), so whatever that memory holds is never looked at.
+                    const bool want_flags = MODE == kModeDog && a.flags.data != nullptr;
+                    const bool may_skip = want_flags && !(a.debug & 512);
+                    const bool row_in = un.y0 + row < a.H;
 #pragma unroll
                     for (int c = 0; c < 2; ++c) {
+                        bool hit = false;
                         uint32_t ra[32], rb[32];
                         // outputs 64 h + 32 c .. + 31 are accumulator columns 96 - 64 h - 32 c .. + 31, reversed
                         tmem_ld32_pair(acc + 32 * (1 - c), acc + kAccCols + 32 * (1 - c), ra, rb);
@@ -789,31 +796,40 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                         }
                         rc.lap(2);
                         if (emit && !(a.debug & 2)) {            // uniform per level
+                            bool store = true;
+                            if (want_flags) {
+                                // this warp's 32 rows x 32 columns: which of its four 8-row blocks hold a value
+                                // above the threshold (rows below the frame do not count)?
+                                const uint32_t m = __ballot_sync(0xffffffffu, hit && row_in);
+                                if (lane == 0) {
+                                    const uint32_t word = ((m & 0xffu) ? 1u : 0u) | ((m & 0xff00u) ? 0x100u : 0u) |
+                                                          ((m & 0xff0000u) ? 0x10000u : 0u) | ((m & 0xff000000u) ? 0x1000000u : 0u);
+                                    *reinterpret_cast<uint32_t *>(a.flags.data +
+                                        ((int64_t)out_plane * a.flags.col_blocks + ((un.x0 >> 5) + 2 * h + c)) * a.flags.row_blocks +
+                                        ((un.y0 >> 3) + 4 * q)) = word;
+                                    if (may_skip) ctl->box_hit[round_it & 1u][h][q] = m;
+                                }
+                            }
                             if (store_leader) bulk_wait_read();
-                            named_bar(bar_a, 128);
+                            named_bar(bar_a, 128);               // also publishes the four ballots of this box
+                            if (may_skip) {
+                                const volatile uint32_t *bh = ctl->box_hit[round_it & 1u][h];
+                                store = (bh[0] | bh[1] | bh[2] | bh[3]) != 0u;      // uniform over the half
+                                ++round_it;
+                            }
+                            if (store) {
 #pragma unroll
-                            for (int k = 0; k < 8; ++k)      // output element i of the chunk is ra[31 - i]
-                                st_shared_v4(stg_row + (((uint32_t)k ^ swz) << 4), ra[31 - 4 * k], ra[30 - 4 * k], ra[29 - 4 * k], ra[28 - 4 * k]);
-                            fence_proxy_async_smem();
-                            named_bar(bar_b, 128);
-                            if (store_leader && !(a.debug & 32)) {
-                                tma_store_2d(&map_out, un.x0 + 64 * h + 32 * c, out_plane * a.Hp + un.y0, stg);
-                                bulk_commit();
+                                for (int k = 0; k < 8; ++k)      // output element i of the chunk is ra[31 - i]
+                                    st_shared_v4(stg_row + (((uint32_t)k ^ swz) << 4), ra[31 - 4 * k], ra[30 - 4 * k], ra[29 - 4 * k], ra[28 - 4 * k]);
+                                fence_proxy_async_smem();
+                                named_bar(bar_b, 128);
+                                if (store_leader && !(a.debug & 32)) {
+                                    tma_store_2d(&map_out, un.x0 + 64 * h + 32 * c, out_plane * a.Hp + un.y0, stg);
+                                    bulk_commit();
+                                }
                             }
                         }
                         rc.lap(3);
-                    }
-                    // this warp's 32 rows x 64 columns of the slice: which of its four 8-row blocks hold a
-                    // value above the threshold?  (rows below the frame do not count; the extrema kernel
-                    // only reads the neighbourhood of hit blocks)
-                    if (MODE == kModeDog && emit && a.flags.data != nullptr) {
-                        const uint32_t m = __ballot_sync(0xffffffffu, hit && un.y0 + row < a.H);
-                        if (lane == 0) {
-                            const uint32_t word = ((m & 0xffu) ? 1u : 0u) | ((m & 0xff00u) ? 0x100u : 0u) |
-                                                  ((m & 0xff0000u) ? 0x10000u : 0u) | ((m & 0xff000000u) ? 0x1000000u : 0u);
-                            *reinterpret_cast<uint32_t *>(a.flags.data + ((int64_t)out_plane * a.flags.col_blocks + ((un.x0 >> 6) + h)) *
-                                                                             a.flags.row_blocks + ((un.y0 >> 3) + 4 * q)) = word;
-                        }
                     }
                 }
             }

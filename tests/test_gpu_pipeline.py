@@ -683,3 +683,35 @@ class TestDeviceEvaluation:
 def torch_equal(a, b):
     import torch
     return bool(torch.equal(a, b))
+
+
+class TestStaleSliceMemory:
+    """The tensor engine does not store DoG boxes without a value above the threshold and the extrema
+    kernel reads blocks without a hit as -inf: whatever an older frame left in a slot's slice buffer
+    must never show up in a later result."""
+
+    def test_frame_sequences_through_one_slot_equal_fresh_detectors(self):
+        params = params_for("C2")
+        frames = {"a": synth.config_frame("C3", 0), "b": synth.config_frame("C3", 1),
+                  "blank": np.zeros((1024, 1024), np.float32),
+                  "bright": np.full((1024, 1024), 0.9, np.float32) + synth.config_frame("C3", 2),
+                  "sparse": np.where(np.add.outer(np.arange(1024), np.arange(1024)) % 512 < 40,
+                                     synth.config_frame("C3", 3), 0).astype(np.float32)}
+        want = {}
+        for k, f in frames.items():
+            det = P.Detector(params, slots=1)
+            want[k] = det.run(f).blobs.records
+            det.close()
+        det = P.Detector(params, slots=1)
+        assert det.plan_for((1024, 1024)).plan.conv_engine == 2
+        for k in ["a", "b", "a", "blank", "a", "bright", "sparse", "b", "sparse", "blank", "bright", "a"]:
+            assert np.array_equal(det.run(frames[k]).blobs.records, want[k]), k
+        # other thresholds on the same slot: the validity map follows the threshold of the call
+        lo = P.Detector(P.DetectionParams(**{**params.to_dict(), "threshold": 0.02}), slots=1)
+        hi = P.Detector(P.DetectionParams(**{**params.to_dict(), "threshold": 0.3}), slots=1)
+        w_lo, w_hi = lo.run(frames["a"]).blobs.records, hi.run(frames["a"]).blobs.records
+        for d, w in ((hi, w_hi), (lo, w_lo)):
+            d.run(frames["bright"]); d.run(frames["b"])
+            assert np.array_equal(d.run(frames["a"]).blobs.records, w)
+        for d in (det, lo, hi):
+            d.close()
