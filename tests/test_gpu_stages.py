@@ -189,6 +189,20 @@ class TestEngines:
         for _ in range(5):
             assert np.array_equal(P.fused_dog(img, bank).slices, ref)
 
+    @pytest.mark.parametrize("width", [897, 898, 899, 901, 907, 961, 769])
+    def test_right_edge_inside_a_16_byte_chunk(self, monkeypatch, width):
+        """frame widths whose right edge cuts a stored box in the middle of a 16-byte chunk: those
+        columns and the reflected halo next to them are written by different CTAs (found by
+        tools/stress_engines.py at 725 x 898: a clipped TMA store there lost the neighbours' halo)"""
+        bank = bank_for(1.5, 24.9, 26)
+        img = synth.sensor_noise(synth.droplet_scene(width, 725, 30, (2.0, 40.0), seed=3, allow_overlap=True),
+                                 seed=4).image
+        out = {}
+        for eng in ("fma", "umma"):
+            monkeypatch.setenv("DOGBLOB_CONV", eng)
+            out[eng] = P.convolve_bank(img, bank).levels
+        assert np.abs(out["fma"].astype(np.float64) - out["umma"]).max() < 2 * LEVEL_TOL_TENSOR_WIDE
+
     def test_engines_agree(self, monkeypatch):
         bank = bank_for(1.0, 12.0, 11)
         img = synth.sensor_noise(synth.droplet_scene(333, 270, 20, (3.0, 12.0), seed=8, allow_overlap=True),

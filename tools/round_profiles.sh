@@ -6,6 +6,7 @@ timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1
 DOGBLOB_CONV=umma DOGBLOB_STREAMED_UPLOAD=0 timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu_umma_forced.log 2>&1
 DOGBLOB_CONV=umma timeout 900 compute-sanitizer --tool memcheck python tools/sanitize_run.py > gpurun_out/san_memcheck_umma.log 2>&1
 timeout 900 compute-sanitizer --tool memcheck python tools/sanitize_run.py > gpurun_out/san_memcheck.log 2>&1
+timeout 900 python tools/stress_engines.py 120 5 > gpurun_out/stress_engines.txt 2>&1
 python tools/config_timings.py > gpurun_out/config_timings.jsonl 2>&1
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 python bench.py --gpus 2 --steps 5 > gpurun_out/bench_2ranks_1gpu.json 2>> gpurun_out/bench.err

@@ -36,6 +36,13 @@ with open(P / f"{tag}_sanitizer.md", "w") as f:
         if (G / name).exists():
             f.write(f"\n{title}:\n```\n" + "\n".join((G / name).read_text().splitlines()[-4:]) + "\n```\n")
 
+if (G / "stress_engines.txt").exists():
+    txt = (G / "stress_engines.txt").read_text().splitlines()
+    (P / f"{tag}_stress_engines.md").write_text(
+        f"# Round {tag[1:]} - randomised engine cross-check (tools/stress_engines.py 120 5): random ragged shapes, ladders, "
+        "thresholds; tensor-core DoG slices vs the FP32 engine's, detector vs stage functions on the same stack, frame "
+        "sequences through one slot (stale slice memory)\n\n```\n" + "\n".join(txt[:12] + ["..."] + txt[-3:]) + "\n```\n")
+
 rows = list(csv.reader(open(G / "launches_one_frame.csv")))
 h = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
 cols = rows[h]
