@@ -4,7 +4,7 @@ random frame shapes (ragged, odd widths), ladders and thresholds; the tensor-cor
 slices against the FP32 engine's (within 2e-6 sigma) and the detected blob lists of both engines on
 frame SEQUENCES through one detector (stale slice memory must never show).  Test tooling only.
 
-    python tools/stress_engines.py [n_cases] [seed]
+    python tools/stress_engines.py [n_cases] [seed] [large]        # large: frames up to 2600 px, sigma up to 60
 """
 import os
 import sys
@@ -18,15 +18,17 @@ from paper_2010_08486_b200 import synth  # noqa: E402
 
 n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+large = len(sys.argv) > 3 and sys.argv[3] == "large"
 worst, n_tensor, n_list_diff, failures = 0.0, 0, 0, 0
 for case in range(n_cases):
-    H, W = int(rng.integers(140, 1300)), int(rng.integers(140, 1300))
+    H, W = (int(rng.integers(600, 2600)), int(rng.integers(600, 2600))) if large else \
+           (int(rng.integers(140, 1300)), int(rng.integers(140, 1300)))
     if rng.random() < 0.3:
         W = W // 8 * 8
     if rng.random() < 0.2:
         H, W = H // 128 * 128 + 128, W // 128 * 128 + 128
     lo = float(rng.choice([1.0, 1.5, 2.0, 3.0]))
-    hi = float(min(lo + rng.uniform(4, 28), min(H, W) / 6.0))
+    hi = float(min(lo + rng.uniform(4, 58 if large else 28), min(H, W) / 6.0))
     n_bin = int(rng.integers(3, 40))
     kw = dict(min_sigma=lo, max_sigma=max(hi, lo + 1.0), n_bin=n_bin)
     thr = float(rng.choice([0.02, 0.05, 0.1, 0.2]))
@@ -61,14 +63,15 @@ for case in range(n_cases):
     n_list_diff += diff
     print(f"case {case}: {H}x{W} sigma {lo}..{kw['max_sigma']:.1f} n_bin {n_bin} thr {thr}: max |dDoG|/sigma = {err:.2e}, "
           f"blobs {len(out['umma'][2][0])}, engine list differences {diff}, repeat-stable {same_seq}", flush=True)
-    if err >= 2e-6:
+    tol = 2e-6 if int(bank.radii.max()) <= 150 else 3e-6      # two float32 results: rounding grows with the taps
+    if err >= tol:
         failures += 1
         d = np.abs(out["fma"][1].astype(np.float64) - out["umma"][1]) / sig
         per = d.reshape(d.shape[0], -1).max(axis=1)
-        bad = np.nonzero(per >= 2e-6)[0]
+        bad = np.nonzero(per >= tol)[0]
         print("   DoG slices differ: slices", bad.tolist(), "radii", [int(bank.radii[i]) for i in bad], [int(bank.radii[i + 1]) for i in bad])
         for i in bad[:4]:
-            ys, xs = np.nonzero(d[i] >= 2e-6)
+            ys, xs = np.nonzero(d[i] >= tol)
             print(f"   slice {i}: err {per[i]:.2e}, {ys.size} px, rows {ys.min()}..{ys.max()}, cols {xs.min()}..{xs.max()}")
         continue
     for eng in ("fma", "umma"):
