@@ -142,6 +142,29 @@ class TestConfigs:
                     oblob_tuples(ref.candidates), oblob_tuples(ref.blobs), "1000x900")
 
 
+class TestRandomisedParity:
+    """Seeded random frames, ladders and detection parameters against the oracle run live, on both
+    convolution engines (ragged shapes, 5^3 neighbourhoods, low thresholds on sensor noise,
+    overlap thresholds either side of the default)."""
+
+    @pytest.mark.parametrize("engine", ["fma", "umma"])
+    @pytest.mark.parametrize("seed", range(6))
+    def test_random_case(self, monkeypatch, seed, engine):
+        monkeypatch.setenv("DOGBLOB_CONV", engine)
+        rng = np.random.default_rng(1000 + seed)
+        H, W = int(rng.integers(200, 560)), int(rng.integers(200, 560))
+        lo = float(rng.choice([1.0, 1.5, 2.0, 3.0]))
+        kw = dict(min_sigma=lo, max_sigma=lo + float(rng.uniform(3, 16)), n_bin=int(rng.integers(3, 22)),
+                  threshold=float(rng.choice([0.03, 0.05, 0.1, 0.2])), neighborhood=int(rng.choice([3, 3, 5])),
+                  overlap=float(rng.choice([0.3, 0.5, 0.8])))
+        frame = synth.sensor_noise(synth.droplet_scene(W, H, int(rng.integers(5, 60)), (2.5, 24.0),
+                                                       seed=int(rng.integers(1 << 30)), allow_overlap=True),
+                                   seed=int(rng.integers(1 << 30))).image
+        ref = O.OracleDetector(preprocess=False, **kw).run(frame)
+        check_frame(frame, P.DetectionParams(preprocess=False, **kw), oblob_tuples(ref.candidates),
+                    oblob_tuples(ref.blobs), f"random{seed}_{engine}_{H}x{W}")
+
+
 class TestDetectorBehaviour:
     def test_blank_and_dark_images_yield_nothing(self):
         p = P.DetectionParams(min_sigma=1, max_sigma=4, n_bin=6, preprocess=False)
