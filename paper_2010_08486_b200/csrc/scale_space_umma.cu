@@ -434,7 +434,8 @@ struct SharedCtl {
     uint32_t pad[3];
     uint32_t box_hit[2][2][4];      // pass 2: [store round parity][column half][drain warp] ballots "above the threshold"
 };
-static_assert(sizeof(SharedCtl) <= 1024, "control block");
+constexpr int kCtlBytes = 512;
+static_assert(sizeof(SharedCtl) <= kCtlBytes, "control block");
 
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -443,7 +444,7 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                  const __grid_constant__ CUtensorMap map_out, const __grid_constant__ CUtensorMap map_aux) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     SharedCtl *ctl = reinterpret_cast<SharedCtl *>(smem_raw);
-    unsigned char *toep = smem_raw + 1024;                               // [buffer 2][hi | lo]
+    unsigned char *toep = smem_raw + kCtlBytes;                               // [buffer 2][hi | lo]
     unsigned char *staging = smem_raw + a.staging_off;                   // [column half 2][16 KB box (x 2 in pass 1)]
     constexpr bool kRows = MODE == kModeRows;
     constexpr int NT = kRows ? kToepBuffers1 : kToepBuffers2;
@@ -712,10 +713,6 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                     const int right_w = rpad + (a.Wp - a.W);
                     const bool left = xs0 < rpad, right = xs0 + 64 > a.W - right_w && xs0 < a.W;
                     const bool right_tma = right && (a.W & 7) == 0 && xs0 + 64 <= a.W;    // no negative store coordinates
-                    // A box cut by the frame's right edge in the middle of a 16-byte chunk is not stored by TMA:
-                    // other CTAs write the halo columns of that very chunk at the same time, and a clipped
-                    // chunk did not prove to be a byte-exact write under that race (tools/stress_engines.py).
-                    const bool cut = xs0 < a.W && xs0 + 64 > a.W && (a.W & 7) != 0;
                     const int n_rounds = (a.debug & 2) ? 0 : ((left || right_tma) && !(a.debug & 64)) ? 4 : 2;
                     for (int rd = 0; rd < n_rounds; ++rd, ++round_it) {      // uniform per half
                         const uint32_t buf = kStagingBufs1 == 2 ? (round_it & 1u) : 0u;
@@ -747,7 +744,7 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                             const uint32_t src = stg + buf * 16384u;
                             const int yrow = level * a.Hp + un.y0;
                             if (rd < 2) {
-                                if (!cut) tma_store_3d(&map_out, a.Ppad + xs0, yrow, lo_plane, src);
+                                tma_store_3d(&map_out, a.Ppad + xs0, yrow, lo_plane, src);
                             } else {
                                 // map_aux starts at the first column right of the frame (column W)
                                 if (left) tma_store_3d(&map_out, a.Ppad - xs0 - 64, yrow, lo_plane, src);
@@ -768,7 +765,6 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                                 const int x = xs0 + e;
                                 const unsigned short v = (unsigned short)((e & 1) ? (w[e >> 1] >> 16) : (w[e >> 1] & 0xffffu));
                                 if (x >= a.W - right_w && x < a.W) prow[2 * a.W - 1 - x] = v;
-                                if (cut && x < a.W && !(a.debug & 32)) prow[x] = v;
                             }
                         }
                     }
@@ -949,7 +945,7 @@ int toeplitz_buffer_bytes(int max_rpad, bool rows_pass) {
 // control block + Toeplitz ring, rounded up to the 1 KB alignment of the swizzled boxes behind it
 size_t staging_offset(int max_rpad, bool rows_pass) {
     const size_t ring = (size_t)(rows_pass ? kToepBuffers1 : kToepBuffers2) * toeplitz_buffer_bytes(max_rpad, rows_pass);
-    return (1024 + ring + 1023) / 1024 * 1024;
+    return (kCtlBytes + ring + 1023) / 1024 * 1024;
 }
 
 constexpr size_t kSmemLimit = 227 * 1024;
@@ -1009,6 +1005,15 @@ int umma_debug_mask() {
     if (!present) return 0;
     const char *e = std::getenv("DOGBLOB_UMMA_DEBUG");
     return e ? std::atoi(e) : 0;
+}
+
+// Frame widths that are not a multiple of 8: the halo columns [W, W + n) that share a 16-byte chunk with
+// the frame's last columns, in every row of both planes (column W + i <- column W - 1 - i).
+__global__ void edge_halo_kernel(__half *r, int64_t n_rows, int64_t pitch, int edge, int n) {
+    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= n_rows) return;
+    __half *p = r + row * pitch + edge;
+    for (int i = 0; i < n; ++i) p[i] = p[-1 - i];
 }
 
 template <int MODE>
@@ -1165,8 +1170,13 @@ cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d
         if (!encode_map(&map_in, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, d_x, dims, strides, box))
             return cudaErrorInvalidValue;
     }
-    {   // R planes as {columns up to the last valid one, rows of all levels, hi | lo}: stores beyond W are clipped
-        const cuuint64_t dims[3] = {(cuuint64_t)(l.Ppad + g.W), (cuuint64_t)g.L * g.Hp, 2};
+    const int w8 = (g.W + 7) & ~7;
+    {   // R planes as {columns up to the end of the last valid 16-byte chunk, rows of all levels, hi | lo}: stores
+        // beyond are clipped.  The clip must not fall INSIDE a chunk: other CTAs write the halo columns next to
+        // the frame at the same time, and a partially clipped chunk proved not to be a byte-exact write under
+        // that race (tools/stress_engines.py, 725 x 898).  The up to 7 halo columns [W, w8) this leaves wrong
+        // are rewritten by edge_halo_kernel below.
+        const cuuint64_t dims[3] = {(cuuint64_t)(l.Ppad + w8), (cuuint64_t)g.L * g.Hp, 2};
         const cuuint64_t strides[2] = {(cuuint64_t)l.Wq * 2, (cuuint64_t)a.r_plane * 2};
         const cuuint32_t box[3] = {64, 128, 1};
         if (!encode_map(&map_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, d_r, dims, strides, box))
@@ -1181,7 +1191,11 @@ cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d
                         reinterpret_cast<__half *>(d_r) + l.Ppad + g.W, dims, strides, box))
             return cudaErrorInvalidValue;
     }
-    return launch_umma<kModeRows>(a, tbl, ttab, g.max_rpad, map_in, map_out, map_aux, st);
+    const cudaError_t err = launch_umma<kModeRows>(a, tbl, ttab, g.max_rpad, map_in, map_out, map_aux, st);
+    if (err != cudaSuccess || w8 == g.W) return err;
+    const int64_t n_rows = 2 * (int64_t)g.L * g.Hp;
+    edge_halo_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(a.r_base, n_rows, a.r_pitch, l.Ppad + g.W, w8 - g.W);
+    return cudaGetLastError();
 }
 
 // pass 2: R planes -> DoG slices [L - 1][Hp][Wp] (levels = true: the levels themselves, [L][Hp][Wp])
