@@ -82,10 +82,12 @@ constexpr int kRowsPerStage1 = DOGBLOB_UMMA_ROWS1;             // pass 1: input 
 constexpr int kStageBytes1 = 512 * kRowsPerStage1;             // pass 1: [hi | lo][2 x-blocks][rows][128 B]
 constexpr int kStageBytes2 = 32768;       // pass 2: [hi | lo][128 rows][128 B]
 #ifndef DOGBLOB_UMMA_STAGING1
-#define DOGBLOB_UMMA_STAGING1 2
+#define DOGBLOB_UMMA_STAGING1 0
 #endif
-constexpr int kStagingBufs1 = DOGBLOB_UMMA_STAGING1;           // pass 1 drain staging: 16 KB boxes per column half
-constexpr int kStagingBytes1 = 32768 * kStagingBufs1;
+// pass 1 drain staging: 16 KB boxes per column half, two per half (one being stored while the next is filled)
+// unless that costs the fourth data stage (wide ladders: large Toeplitz buffers); 0 = choose, 1 / 2 = force
+constexpr int kStagingForce1 = DOGBLOB_UMMA_STAGING1;
+__host__ __device__ constexpr int staging_bytes1(int bufs) { return 32768 * bufs; }
 constexpr int kStagingBytes2 = 32768;     // pass 2 drain staging: one 16 KB box per column half
 constexpr int kMaxStages = 8;
 #ifndef DOGBLOB_UMMA_BACKOFF
@@ -437,7 +439,7 @@ struct SharedCtl {
 constexpr int kCtlBytes = 512;
 static_assert(sizeof(SharedCtl) <= kCtlBytes, "control block");
 
-template <int MODE>
+template <int MODE, int kStagingBufs1>
 __global__ void __launch_bounds__(kThreads, 1)
 umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                  const __grid_constant__ ToeplitzTable ttab, const __grid_constant__ CUtensorMap map_in,
@@ -448,7 +450,7 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
     unsigned char *staging = smem_raw + a.staging_off;                   // [column half 2][16 KB box (x 2 in pass 1)]
     constexpr bool kRows = MODE == kModeRows;
     constexpr int NT = kRows ? kToepBuffers1 : kToepBuffers2;
-    unsigned char *data = staging + (kRows ? kStagingBytes1 : kStagingBytes2);     // [stage][...]
+    unsigned char *data = staging + (kRows ? staging_bytes1(kStagingBufs1) : kStagingBytes2);     // [stage][...]
     constexpr int kStageBytes = kRows ? kStageBytes1 : kStageBytes2;
     constexpr int kStepsPerStage = kRows ? kRowsPerStage1 / 16 : 4;                         // k-steps of 16 per data stage
     const int S = a.stages;
@@ -949,11 +951,18 @@ size_t staging_offset(int max_rpad, bool rows_pass) {
 }
 
 constexpr size_t kSmemLimit = 227 * 1024;
-int data_stages_for(int max_rpad, bool rows_pass) {
-    const size_t fixed = staging_offset(max_rpad, rows_pass) + (rows_pass ? kStagingBytes1 : kStagingBytes2);
+int data_stages_for(int max_rpad, bool rows_pass, int staging_bufs) {
+    const size_t fixed = staging_offset(max_rpad, rows_pass) + (rows_pass ? staging_bytes1(staging_bufs) : kStagingBytes2);
     const size_t per = rows_pass ? kStageBytes1 : kStageBytes2;
     if (fixed + 2 * per > kSmemLimit) return 0;
     return (int)std::min<size_t>(kMaxStages, (kSmemLimit - fixed) / per);
+}
+
+// pass 1: the second staging box per half is worth less than a fourth data stage (C2: 4 stages either way,
+// 0.109 vs 0.116 ms with one box; C4: 0.526 ms with one box and 4 stages, 0.559 with two boxes and 3)
+int staging_bufs_for(int max_rpad) {
+    if (kStagingForce1 == 1 || kStagingForce1 == 2) return kStagingForce1;
+    return data_stages_for(max_rpad, true, 2) >= 4 || data_stages_for(max_rpad, true, 1) < 4 ? 2 : 1;
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -1023,9 +1032,10 @@ cudaError_t launch_umma(UmmaArgs b, const LevelTable &tbl, const ToeplitzTable &
     constexpr bool rows_pass = MODE == kModeRows;
     b.toep_bytes = toeplitz_buffer_bytes(max_rpad, rows_pass);
     b.staging_off = (int)staging_offset(max_rpad, rows_pass);
-    b.stages = data_stages_for(max_rpad, rows_pass);
+    const int staging_bufs = rows_pass ? staging_bufs_for(max_rpad) : 1;
+    b.stages = data_stages_for(max_rpad, rows_pass, staging_bufs);
     if (b.stages < 2) return cudaErrorInvalidConfiguration;
-    const size_t smem = (size_t)b.staging_off + (rows_pass ? kStagingBytes1 : kStagingBytes2) +
+    const size_t smem = (size_t)b.staging_off + (rows_pass ? staging_bytes1(staging_bufs) : kStagingBytes2) +
                         (size_t)b.stages * (rows_pass ? kStageBytes1 : kStageBytes2);
     static unsigned long long *d_prof = nullptr;
     const bool prof = umma_prof_enabled();
@@ -1040,7 +1050,10 @@ cudaError_t launch_umma(UmmaArgs b, const LevelTable &tbl, const ToeplitzTable &
         b.prof = d_prof;
     }
     const int ctas = b.n_ctas > 0 ? b.n_ctas : persistent_ctas(b.n_units);
-    umma_pass_kernel<MODE><<<ctas, kThreads, smem, st>>>(b, tbl, ttab, map_in, map_out, map_aux);
+    if (staging_bufs == 2)
+        umma_pass_kernel<MODE, rows_pass ? 2 : 1><<<ctas, kThreads, smem, st>>>(b, tbl, ttab, map_in, map_out, map_aux);
+    else
+        umma_pass_kernel<MODE, 1><<<ctas, kThreads, smem, st>>>(b, tbl, ttab, map_in, map_out, map_aux);
     if (prof) {
         unsigned long long h[256];
         cudaStreamSynchronize(st);
@@ -1070,7 +1083,7 @@ cudaError_t launch_umma(UmmaArgs b, const LevelTable &tbl, const ToeplitzTable &
 // The tensor-core passes need: both Toeplitz buffers, the drain staging and >= 2 data stages in
 // shared memory; every halo column mirrored from inside the frame (one reflection).
 bool umma_supported(const ConvGeometry &g) {
-    return data_stages_for(g.max_rpad, true) >= 2 && data_stages_for(g.max_rpad, false) >= 2 &&
+    return data_stages_for(g.max_rpad, true, 1) >= 2 && data_stages_for(g.max_rpad, false, 1) >= 2 &&
            g.W >= g.max_rpad + (g.Wp - g.W) && tensor_map_encoder() != nullptr;
 }
 
@@ -1120,11 +1133,13 @@ cudaError_t configure_umma_kernels(int device) {
     int optin = 0;
     cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(umma_pass_kernel<kModeRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    e = cudaFuncSetAttribute(umma_pass_kernel<kModeRows, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(umma_pass_kernel<kModeDog>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    e = cudaFuncSetAttribute(umma_pass_kernel<kModeRows, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(umma_pass_kernel<kModeLevels>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    e = cudaFuncSetAttribute(umma_pass_kernel<kModeDog, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(umma_pass_kernel<kModeLevels, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
 }
 
 // frame -> max |x| -> fp16 hi | lo planes with reflected halo rows (d_x: umma_layout().x_bytes)
