@@ -250,7 +250,7 @@ def run_ours(args):
 
     kw = params_kw()
     params = P.DetectionParams(preprocess=False, **kw)
-    n_slots = int(os.environ.get("DOGBLOB_BENCH_SLOTS", "4"))   # frame slots = concurrent streams
+    n_slots = int(os.environ.get("DOGBLOB_BENCH_SLOTS", "8"))   # frame slots = concurrent streams
     det = P.Detector(params, device=local, slots=n_slots)
     H, W = frames[0].shape
     eng = det.plan_for((H, W))

@@ -74,7 +74,8 @@ typedef struct dogblob_result_header {
      * [0..2] six 16-bit marks in us since its first ticket (grid build, first sweep, part
      * labelling, merge loops, packing, end; saturating), [3] sweeps << 24 | parts */
     int32_t prune_profile[4];
-    int32_t reserved[2];
+    int32_t n_seeds;        /* tensor-core engine: voxels the column pass handed to the extrema kernel (diagnostic) */
+    int32_t reserved;
 } dogblob_result_header;
 
 #define DOGBLOB_FLAG_OVERFLOW 1u     /* a capacity was exceeded: result incomplete */

@@ -28,7 +28,7 @@ BLOB_DTYPE = np.dtype([("x", "<f8"), ("y", "<f8"), ("sigma", "<f8"), ("radius", 
 HEADER_DTYPE = np.dtype([("n_blobs", "<i4"), ("n_candidates", "<i4"), ("n_flagged", "<i4"),
                          ("n_plateau", "<i4"), ("n_merges", "<i4"), ("flags", "<u4"),
                          ("capacity", "<i4"), ("conv_ns", "<i4"), ("extrema_ns", "<i4"),
-                         ("prune_ns", "<i4"), ("prune_profile", "<i4", (4,)), ("reserved", "<i4", (2,))])
+                         ("prune_ns", "<i4"), ("prune_profile", "<i4", (4,)), ("n_seeds", "<i4"), ("reserved", "<i4")])
 assert BLOB_DTYPE.itemsize == 48 and HEADER_DTYPE.itemsize == RESULT_HEADER_BYTES
 
 # every symbol include/dogblob_b200.h declares: name -> (restype, argtypes)

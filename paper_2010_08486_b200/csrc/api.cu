@@ -88,7 +88,8 @@ struct dogblob_plan {
     // FP32 engine: rows_t = row-filtered planes (x-major), dog_t = DoG^T planes, edge = parked levels;
     // tensor engine: rows_t = R planes (fp16 hi | lo), x = X planes, dog_t = DoG planes (image
     // orientation), no edge planes
-    size_t off_rows_t = 0, off_x = 0, off_dog_t = 0, off_edge = 0, off_blobspace = 0, off_gate = 0, off_flags = 0, total = 0;
+    size_t off_rows_t = 0, off_x = 0, off_dog_t = 0, off_edge = 0, off_blobspace = 0, off_gate = 0, off_flags = 0, off_seeds = 0, total = 0;
+    int seed_cap = 0;               // tensor engine: capacity of the column pass's seed list (0 = no seeds, strip kernel)
 };
 
 namespace {
@@ -469,6 +470,14 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
     plan->off_blobspace = off; off += blobspace_bytes(max_blobs);
     plan->off_gate = off;   off += 4096;                                  // streamed upload: gate word; +64: frame max word + partial maxima
     plan->off_flags = off;  off += align_up(hit_flag_bytes(n_levels, g.Hp, g.Wp), 256);   // tensor engine: hit blocks
+    if (plan->use_umma) {
+        // seeds: a few thousand per frame; one per 64 voxels is far beyond any frame with distinct blobs, and a
+        // frame beyond that (flat noise above the threshold) falls back to the strip kernel
+        const int64_t voxels = (int64_t)(n_levels - 1) * g.H * g.W;
+        plan->seed_cap = (int)std::min<int64_t>(1 << 20, std::max<int64_t>(1 << 16, voxels / 64));
+        if (const char *e = std::getenv("DOGBLOB_SEED_CAP")) plan->seed_cap = std::max(0, std::atoi(e));   // tests: force the fallback
+        plan->off_seeds = off;  off += align_up((size_t)plan->seed_cap * sizeof(unsigned long long), 256);
+    }
     plan->total = off;
     *out = plan;
     return DOGBLOB_OK;
@@ -533,6 +542,12 @@ static HitFlags hit_flags_of(const dogblob_plan *plan, void *d_workspace) {
     f.data = reinterpret_cast<unsigned char *>(d_workspace) + plan->off_flags;
     f.row_blocks = plan->geo.Hp >> kFlagRowShift;
     f.col_blocks = plan->geo.Wp >> kFlagColShift;
+    if (plan->seed_cap > 0) {
+        char *ws = reinterpret_cast<char *>(d_workspace);
+        f.seeds = reinterpret_cast<unsigned long long *>(ws + plan->off_seeds);
+        f.n_seeds = &carve_blobspace(ws + plan->off_blobspace, plan->max_blobs).ctr->n_seeds;
+        f.seed_cap = plan->seed_cap;
+    }
     return f;
 }
 // pass 2 fused with the DoG: tensor engine -> slices in image orientation, FP32 engine -> transposed.

@@ -77,7 +77,8 @@ struct Counters {            // one per result, lives in the blob space
     // device-side stage stamps (globaltimer, ns): start of the frame, start of extrema, start of
     // ordering/pruning; the kernel that finishes the frame turns them into the header's stage times
     unsigned long long t_start, t_extrema, t_prune;
-    int pad[2];
+    int n_seeds;             // tensor engine: seeds appended by the column pass (HitFlags::seeds), may exceed the capacity
+    int pad;
 };
 
 struct Voxel { int s, row, col; int pad; double val; };     // val: the slice's value (float32 values are exact in it)
@@ -157,6 +158,15 @@ cudaError_t launch_edge_dog(const ConvGeometry &g, const float *d_edge, float *d
 struct HitFlags {
     unsigned char *data = nullptr;       // [slice][col_blocks][row_blocks] (row blocks contiguous)
     int row_blocks = 0, col_blocks = 0;
+    // Seeds (optional): the column pass also tests every value above the threshold against the in-slice
+    // neighbours it has in registers (same row: the thread's own columns; rows above / below: the
+    // neighbouring lanes) and appends the survivors - a superset of the in-slice local maxima, some ten
+    // thousand voxels per frame - to this list as slice << 48 | row << 24 | column.  The extrema kernel
+    // then only visits the seeds (nms_seed_kernel) instead of walking the slices.  *n_seeds counts past
+    // the capacity: more seeds than seed_cap = the list is incomplete and the strip kernel runs instead.
+    unsigned long long *seeds = nullptr;
+    int *n_seeds = nullptr;
+    int seed_cap = 0;
 };
 constexpr int kFlagColShift = 5, kFlagRowShift = 3;      // 32 columns x 8 rows
 inline size_t hit_flag_bytes(int planes, int Hp, int Wp) {

@@ -377,6 +377,57 @@ nms_window_kernel(Volume vol, float thr, bool transposed, const double *__restri
                                          s_queue[threadIdx.x >> 5]);
 }
 
+// ---- seeds of the tensor-core column pass (HitFlags::seeds) ------------------------------
+// The column pass has already tested every value above the threshold against the in-slice neighbours
+// it holds in registers; what it could not see (neighbours owned by another thread-chunk, warp or CTA)
+// is finished here, one seed per lane: the 8 in-slice neighbours, then the two neighbouring slices.
+// A few thousand seeds per frame instead of a walk over every block with a hit.
+__global__ void __launch_bounds__(256)
+nms_seed_kernel(Volume vol, float thr, int h, bool transposed, const double *__restrict__ slice_sigma, BlobSpace bs,
+                HitFlags flags) {
+    if ((blockIdx.x | threadIdx.x) == 0) bs.ctr->t_extrema = globaltimer_ns();
+    const int n = *flags.n_seeds;
+    if (n > flags.seed_cap) return;                 // incomplete list: nms_fallback_kernel walks the slices
+    const unsigned lane = threadIdx.x & 31;
+    for (int base = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; base < n; base += gridDim.x * blockDim.x) {
+        const int i = base + (int)lane;             // whole warps stay convergent
+        bool cand = i < n;
+        int s = 0, r = 0, c = 0;
+        float val = 0.f;
+        if (cand) {
+            const unsigned long long key = flags.seeds[i];
+            s = (int)(key >> 48); r = (int)((key >> 24) & 0xffffffull); c = (int)(key & 0xffffffull);
+            val = __ldg(vol.data + (int64_t)s * vol.plane + (int64_t)r * vol.pitch + c);      // its block has a hit: stored
+            float nb[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int k = j < 4 ? j : j + 1;
+                const int rr = r + k / 3 - 1, cc = c + k % 3 - 1;
+                nb[j] = (rr >= 0 && rr < vol.rows && cc >= 0 && cc < vol.cols) ? vol.at(s, rr, cc) : -INFINITY;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) cand = cand && !(nb[j] > val);
+        }
+        if (!__any_sync(0xffffffffu, cand)) continue;
+        resolve_and_append(vol, s, r, c, val, cand, h, thr, transposed, slice_sigma, bs, lane);
+    }
+}
+
+// The strip kernel over a fixed grid, for frames with more seeds than the list holds (flat noise above
+// the threshold): returns at once otherwise.
+__global__ void __launch_bounds__(32)
+nms_fallback_kernel(Volume vol, float thr, bool transposed, const double *__restrict__ slice_sigma, BlobSpace bs,
+                    HitFlags flags, int strips_x, int bands_y) {
+    __shared__ unsigned short s_queue[1][kQueueCap];
+    if (*flags.n_seeds <= flags.seed_cap) return;
+    const int total = strips_x * bands_y * vol.S;
+    for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+        const int x = idx % strips_x, t = idx / strips_x;
+        nms_strip<3, 31, 1>(vol, thr, transposed, slice_sigma, bs, flags, t / bands_y, t % bands_y, x, s_queue[0]);
+        __syncwarp();
+    }
+}
+
 // ---- NMS + compaction -----------------------------------------------------------
 // A CTA stages a (kNmsRows + 2) x (1024 + 2) tile of one DoG slice in shared memory
 // (every load issued up front: 10 independent 16-byte loads per thread), so the
@@ -634,7 +685,11 @@ cudaError_t launch_extrema(const float *d_slices, int S, int rows, int cols, int
         // measured variants ((6,34,3) ties; (6,34,2), (3,61,4), (3,31,3) are 5..10 % slower)
         constexpr int kBand = 31;
         const int tiles_y = (rows + kBand - 1) / kBand;
-        if (flags.data != nullptr)
+        if (flags.data != nullptr && flags.seeds != nullptr) {
+            nms_seed_kernel<<<sm_count(), 256, 0, st>>>(vol, threshold, half, transposed, d_slice_sigma, bs, flags);
+            nms_fallback_kernel<<<sm_count() * 16, 32, 0, st>>>(vol, threshold, transposed, d_slice_sigma, bs, flags,
+                                                                (cols + 127) / 128, tiles_y);
+        } else if (flags.data != nullptr)
             nms_window_kernel<3, kBand, 1, 32><<<dim3((cols + 127) / 128, tiles_y, S), 32, 0, st>>>(
                 vol, threshold, transposed, d_slice_sigma, bs, flags);
         else

@@ -732,7 +732,7 @@ prune_large_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_header
                         hdr->prune_profile[1] = (int)(u16(mark[2]) | (u16(mark[3]) << 16));
                         hdr->prune_profile[2] = (int)(u16(mark[4]) | (u16(total) << 16));
                         hdr->prune_profile[3] = (ctl->sweeps << 24) | (__ldcg(&ctl->n_roots) & 0xFFFFFF);
-                        hdr->reserved[0] = hdr->reserved[1] = 0;
+                        hdr->n_seeds = c.n_seeds; hdr->reserved = 0;
                         write_stage_times(c, hdr);
                         break;
                     }
@@ -922,7 +922,7 @@ finalize_small_kernel(BlobSpace bs, double thr, int do_prune, dogblob_result_hea
         hdr->flags = f;
         hdr->capacity = out_cap;
         for (int q = 0; q < 4; ++q) hdr->prune_profile[q] = 0;
-        hdr->reserved[0] = hdr->reserved[1] = 0;
+        hdr->n_seeds = c.n_seeds; hdr->reserved = 0;
         write_stage_times(c, hdr);
         bs.ctr->small_done = 1;
     }

@@ -71,7 +71,9 @@ namespace dogblob {
 namespace {
 
 constexpr int kUT = 128;                  // tile edge on both axes
-constexpr int kThreads = 384;             // 12 warps
+// 12 warps = 3 per scheduler: 168 registers per thread (dropping the idle fourth role warp would not raise
+// the limit: one scheduler would still hold three warps)
+constexpr int kThreads = 384;
 constexpr int kDrainWarp0 = 4;            // warps 4..11 drain
 constexpr int kDrainWarps = 8;
 constexpr int kAccCols = 128;
@@ -808,10 +810,11 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                         rc.lap(2);
                         if (emit && !(a.debug & 2)) {            // uniform per level
                             bool store = true;
+                            uint32_t hit_rows = 0u;          // ballot: this warp's rows with a value above the threshold
                             if (want_flags) {
                                 // this warp's 32 rows x 32 columns: which of its four 8-row blocks hold a value
                                 // above the threshold (rows below the frame do not count)?
-                                const uint32_t m = __ballot_sync(0xffffffffu, hit && row_in);
+                                const uint32_t m = hit_rows = __ballot_sync(0xffffffffu, hit && row_in);
                                 if (lane == 0) {
                                     const uint32_t word = ((m & 0xffu) ? 1u : 0u) | ((m & 0xff00u) ? 0x100u : 0u) |
                                                           ((m & 0xff0000u) ? 0x10000u : 0u) | ((m & 0xff000000u) ? 0x1000000u : 0u);
@@ -837,6 +840,39 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                                 if (store_leader && !(a.debug & 32)) {
                                     tma_store_2d(&map_out, un.x0 + 64 * h + 32 * c, out_plane * a.Hp + un.y0, stg);
                                     bulk_commit();
+                                }
+                            }
+                            if (a.flags.seeds != nullptr && hit_rows != 0u) {      // uniform per warp; after the store: the box is read meanwhile
+                                // Seeds: values above the threshold that no in-slice neighbour KNOWN HERE exceeds
+                                // (same row: this thread's other columns of the chunk; rows above / below: the
+                                // adjacent lanes; everything else, and everything outside the frame, counts as
+                                // -inf).  A lane without a neighbour lane gets its own row maximum back from the
+                                // shuffle, which a row maximum passes by construction.
+                                const int xbase = un.x0 + 64 * h + 32 * c;
+                                const int nvalid = row_in ? a.W - xbase : 0;         // output elements i < nvalid are inside
+                                if (a.W - xbase < 32 || !row_in) {                    // frame edge: rare
+#pragma unroll
+                                    for (int j = 0; j < 32; ++j)
+                                        if (31 - j >= nvalid) ra[j] = 0xff800000u;   // -inf
+                                }
+                                uint32_t seedmask = 0u;
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) {
+                                    const float e = __uint_as_float(ra[j]);
+                                    const float side = fmaxf(j > 0 ? __uint_as_float(ra[j - 1]) : -INFINITY,
+                                                             j < 31 ? __uint_as_float(ra[j + 1]) : -INFINITY);
+                                    const float mm = fmaxf(side, e);
+                                    const float up = __shfl_up_sync(0xffffffffu, mm, 1);
+                                    const float dn = __shfl_down_sync(0xffffffffu, mm, 1);
+                                    if (e > a.thr && e >= side && e >= up && e >= dn) seedmask |= 1u << j;
+                                }
+                                if (seedmask != 0u) {
+                                    int at = atomicAdd(a.flags.n_seeds, __popc(seedmask));
+                                    const unsigned long long key = ((unsigned long long)out_plane << 48) |
+                                                                   ((unsigned long long)(un.y0 + row) << 24);
+                                    for (; seedmask != 0u; seedmask &= seedmask - 1u, ++at)
+                                        if (at < a.flags.seed_cap)
+                                            a.flags.seeds[at] = key | (unsigned long long)(xbase + 32 - __ffs(seedmask));
                                 }
                             }
                         }

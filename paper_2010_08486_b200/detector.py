@@ -658,7 +658,7 @@ class Detector:
 
     def _finish(self, slot: _Slot, hdr, recs, shape, timings) -> DetectResult:
         blobs = BlobSet(records=recs, source_shape=(shape[1], shape[0]), params=self.params)
-        stats = {k: int(hdr[k]) for k in ("n_flagged", "n_plateau", "n_candidates", "n_merges")}
+        stats = {k: int(hdr[k]) for k in ("n_flagged", "n_plateau", "n_candidates", "n_merges", "n_seeds")}
         prof = [int(v) & 0xFFFFFFFF for v in hdr["prune_profile"]]
         if prof[3]:                      # whole-GPU pruning kernel ran: its phase profile
             r = [prof[0] & 0xFFFF, prof[0] >> 16, prof[1] & 0xFFFF, prof[1] >> 16, prof[2] & 0xFFFF, prof[2] >> 16]

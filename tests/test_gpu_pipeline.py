@@ -738,3 +738,53 @@ class TestStaleSliceMemory:
             assert np.array_equal(d.run(frames["a"]).blobs.records, w)
         for d in (det, lo, hi):
             d.close()
+
+
+class TestSeedList:
+    """Tensor engine, 3^3 neighbourhood: the column pass hands the extrema kernel a list of seeds (values
+    above the threshold that none of the in-slice neighbours it holds in registers exceeds).  The list
+    path, the strip kernel without a list (DOGBLOB_SEED_CAP=0 at plan creation) and the strip kernel as
+    the overflow fallback (a list far too short) must return the same records."""
+
+    @pytest.mark.parametrize("name,frame_of", [("C2", lambda: synth.config_frame("C2")),
+                                               ("C2", lambda: synth.config_frame("C3", 5)),
+                                               ("C4", lambda: synth.config_frame("C4"))])
+    def test_seed_list_equals_strip_kernel_and_overflow_fallback(self, monkeypatch, name, frame_of):
+        params = P.DetectionParams(**{**params_for(name).to_dict(), "prune": False})
+        frame = frame_of()
+        got = {}
+        for cap in (None, "0", "4096"):
+            if cap is None:
+                monkeypatch.delenv("DOGBLOB_SEED_CAP", raising=False)
+            else:
+                monkeypatch.setenv("DOGBLOB_SEED_CAP", cap)
+            det = P.Detector(params, slots=1)
+            assert det.plan_for(frame.shape).plan.conv_engine == 2
+            res = det.run(frame)
+            res2 = det.run(frame)
+            assert np.array_equal(res.blobs.records, res2.blobs.records)
+            got[cap] = (res.blobs.records, res.stats["n_seeds"])
+            det.close()
+        n_seeds = got[None][1]
+        assert n_seeds > len(got[None][0]) > 0            # every maximum is a seed; most seeds are not maxima
+        assert got["0"][1] == 0                           # no list: nothing is appended
+        assert got["4096"][1] == n_seeds > 4096           # the count runs past the capacity: incomplete list
+        assert np.array_equal(got[None][0], got["0"][0])
+        assert np.array_equal(got[None][0], got["4096"][0])
+
+    def test_low_threshold_on_noise(self, monkeypatch):
+        """many seeds (noise maxima above a low threshold), frame edges inside the last chunk"""
+        frame = synth.sensor_noise(synth.droplet_scene(1000, 900, 60, (4.0, 20.0), seed=11, allow_overlap=True),
+                                   seed=12).image
+        kw = dict(min_sigma=1.0, max_sigma=24.0, n_bin=40, threshold=0.01, preprocess=False, prune=False)
+        got = {}
+        for cap in (None, "0"):
+            if cap is None:
+                monkeypatch.delenv("DOGBLOB_SEED_CAP", raising=False)
+            else:
+                monkeypatch.setenv("DOGBLOB_SEED_CAP", cap)
+            det = P.Detector(P.DetectionParams(**kw), slots=1)
+            assert det.plan_for(frame.shape).plan.conv_engine == 2
+            got[cap] = det.run(frame).blobs.records
+            det.close()
+        assert len(got[None]) > 100 and np.array_equal(got[None], got["0"])

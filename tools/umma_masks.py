@@ -23,7 +23,8 @@ masks = [int(x) for x in sys.argv[2:]] or [0]
 frame, kw = synth.config_frame(name), synth.config_params(name)
 params = P.DetectionParams(preprocess=False, **kw)
 import dataclasses  # noqa: E402
-run_params = dataclasses.replace(params, threshold=float("inf"))   # garbage planes: nothing is flagged
+# garbage planes under a mask: nothing may be flagged; UMMA_MASKS_THR=<threshold> times the real detection path (mask 0 only)
+run_params = dataclasses.replace(params, threshold=float(os.environ.get("UMMA_MASKS_THR", "inf")))
 H, W = frame.shape
 det = P.Detector(params, slots=1)
 eng = det.plan_for((H, W))
@@ -41,6 +42,6 @@ for m in masks:
         slot.launch_device(d_img, run_params, True, events=es)
     torch.cuda.synchronize()
     med = np.median(np.array([D.event_intervals_ms(es) for es in sets]), axis=0)
-    print(f"{name} mask {m:3d}: row {med[0]:.4f}  col+dog {med[1]:.4f} ms", flush=True)
+    print(f"{name} mask {m:3d}: row {med[0]:.4f}  col+dog {med[1]:.4f}  extrema {med[2]:.4f}  prune {med[3]:.4f} ms", flush=True)
 os.environ["DOGBLOB_UMMA_DEBUG"] = "0"
 det.close()
