@@ -37,8 +37,10 @@ struct VolumeT {
         return valid == nullptr || valid[((int64_t)s * v_col_blocks + (c >> kFlagColShift)) * v_row_blocks + (r >> kFlagRowShift)] != 0;
     }
     __device__ __forceinline__ T at(int s, int r, int c) const {
-        if (!block_valid(s, r, c)) return (T)-INFINITY;
-        return __ldg(data + (int64_t)s * plane + (int64_t)r * pitch + c);
+        // both loads are issued at once (one memory round trip, not two): an unstored block is readable
+        // memory of the same buffer, its stale value is simply dropped
+        const T v = __ldg(data + (int64_t)s * plane + (int64_t)r * pitch + c);
+        return block_valid(s, r, c) ? v : (T)-INFINITY;
     }
 };
 using Volume = VolumeT<float>;     // production path; VolumeT<double>: the float64 tier (fp64.cu)
@@ -384,11 +386,23 @@ nms_window_kernel(Volume vol, float thr, bool transposed, const double *__restri
 // A few thousand seeds per frame instead of a walk over every block with a hit.
 __global__ void __launch_bounds__(256)
 nms_seed_kernel(Volume vol, float thr, int h, bool transposed, const double *__restrict__ slice_sigma, BlobSpace bs,
-                HitFlags flags) {
+                HitFlags flags, int strips_x, int bands_y) {
+    __shared__ unsigned short s_queue[8][kQueueCap];
     if ((blockIdx.x | threadIdx.x) == 0) bs.ctr->t_extrema = globaltimer_ns();
     const int n = *flags.n_seeds;
-    if (n > flags.seed_cap) return;                 // incomplete list: nms_fallback_kernel walks the slices
     const unsigned lane = threadIdx.x & 31;
+    if (n > flags.seed_cap) {
+        // More seeds than the list holds (flat noise above the threshold): the list is incomplete, the strip
+        // kernel's walk over the slices runs instead, on this grid (8 strips side by side per CTA).
+        const int total = strips_x * bands_y * vol.S;
+        for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+            const int x = idx % strips_x, t = idx / strips_x;
+            nms_strip<3, 31, 8>(vol, thr, transposed, slice_sigma, bs, flags, t / bands_y, t % bands_y, x,
+                                s_queue[threadIdx.x >> 5]);
+            __syncwarp();
+        }
+        return;
+    }
     for (int base = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; base < n; base += gridDim.x * blockDim.x) {
         const int i = base + (int)lane;             // whole warps stay convergent
         bool cand = i < n;
@@ -410,21 +424,6 @@ nms_seed_kernel(Volume vol, float thr, int h, bool transposed, const double *__r
         }
         if (!__any_sync(0xffffffffu, cand)) continue;
         resolve_and_append(vol, s, r, c, val, cand, h, thr, transposed, slice_sigma, bs, lane);
-    }
-}
-
-// The strip kernel over a fixed grid, for frames with more seeds than the list holds (flat noise above
-// the threshold): returns at once otherwise.
-__global__ void __launch_bounds__(32)
-nms_fallback_kernel(Volume vol, float thr, bool transposed, const double *__restrict__ slice_sigma, BlobSpace bs,
-                    HitFlags flags, int strips_x, int bands_y) {
-    __shared__ unsigned short s_queue[1][kQueueCap];
-    if (*flags.n_seeds <= flags.seed_cap) return;
-    const int total = strips_x * bands_y * vol.S;
-    for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
-        const int x = idx % strips_x, t = idx / strips_x;
-        nms_strip<3, 31, 1>(vol, thr, transposed, slice_sigma, bs, flags, t / bands_y, t % bands_y, x, s_queue[0]);
-        __syncwarp();
     }
 }
 
@@ -686,9 +685,8 @@ cudaError_t launch_extrema(const float *d_slices, int S, int rows, int cols, int
         constexpr int kBand = 31;
         const int tiles_y = (rows + kBand - 1) / kBand;
         if (flags.data != nullptr && flags.seeds != nullptr) {
-            nms_seed_kernel<<<sm_count(), 256, 0, st>>>(vol, threshold, half, transposed, d_slice_sigma, bs, flags);
-            nms_fallback_kernel<<<sm_count() * 16, 32, 0, st>>>(vol, threshold, transposed, d_slice_sigma, bs, flags,
-                                                                (cols + 127) / 128, tiles_y);
+            nms_seed_kernel<<<sm_count(), 256, 0, st>>>(vol, threshold, half, transposed, d_slice_sigma, bs, flags,
+                                                        (cols + 1023) / 1024, tiles_y);
         } else if (flags.data != nullptr)
             nms_window_kernel<3, kBand, 1, 32><<<dim3((cols + 127) / 128, tiles_y, S), 32, 0, st>>>(
                 vol, threshold, transposed, d_slice_sigma, bs, flags);

@@ -90,7 +90,11 @@ constexpr int kStageBytes2 = 32768;       // pass 2: [hi | lo][128 rows][128 B]
 // unless that costs the fourth data stage (wide ladders: large Toeplitz buffers); 0 = choose, 1 / 2 = force
 constexpr int kStagingForce1 = DOGBLOB_UMMA_STAGING1;
 __host__ __device__ constexpr int staging_bytes1(int bufs) { return 32768 * bufs; }
-constexpr int kStagingBytes2 = 32768;     // pass 2 drain staging: one 16 KB box per column half
+#ifndef DOGBLOB_UMMA_STAGING2
+#define DOGBLOB_UMMA_STAGING2 1
+#endif
+constexpr int kStagingBufs2 = DOGBLOB_UMMA_STAGING2;     // pass 2 drain staging: 16 KB boxes per column half
+constexpr int kStagingBytes2 = 32768 * kStagingBufs2;
 constexpr int kMaxStages = 8;
 #ifndef DOGBLOB_UMMA_BACKOFF
 #define DOGBLOB_UMMA_BACKOFF 0
@@ -664,10 +668,10 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
         const int row = kRows ? kUT - 1 - (32 * q + lane) : 32 * q + lane;     // output row inside the tile
         const bool store_leader = q == 0 && lane == 0;       // issues this half's TMA stores
         const int bar_a = 1 + 2 * h, bar_b = 2 + 2 * h;      // named barriers of this half (128 threads)
-        uint32_t lvl_it = 0, round_it = 0;
+        uint32_t lvl_it = 0, round_it = 0, store_it = 0;
         RoleClock rc(a.prof != nullptr && dw == 0 && lane == 0);
         const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(kRows ? 64 * h : 64 * (1 - h));
-        const uint32_t stg = smem_u32(staging + (size_t)h * (kRows ? 16384 * kStagingBufs1 : 16384));
+        const uint32_t stg = smem_u32(staging + (size_t)h * 16384 * (kRows ? kStagingBufs1 : kStagingBufs2));
         const uint32_t stg_row = stg + (uint32_t)row * 128u;
         const uint32_t swz = (uint32_t)(row & 7);
         const int frame_exp = frame_scale_exp(a.frame_max_bits);
@@ -824,7 +828,7 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                                     if (may_skip) ctl->box_hit[round_it & 1u][h][q] = m;
                                 }
                             }
-                            if (store_leader) bulk_wait_read();
+                            if (kStagingBufs2 == 1 && store_leader) bulk_wait_read();
                             named_bar(bar_a, 128);               // also publishes the four ballots of this box
                             if (may_skip) {
                                 const volatile uint32_t *bh = ctl->box_hit[round_it & 1u][h];
@@ -832,13 +836,18 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                                 ++round_it;
                             }
                             if (store) {
+                                // two boxes per half: this one was last stored two stores ago, and that store's
+                                // read was waited for before the previous barrier b
+                                const uint32_t box = kStagingBufs2 == 2 ? (store_it & 1u) * 16384u : 0u;
+                                ++store_it;
 #pragma unroll
                                 for (int k = 0; k < 8; ++k)      // output element i of the chunk is ra[31 - i]
-                                    st_shared_v4(stg_row + (((uint32_t)k ^ swz) << 4), ra[31 - 4 * k], ra[30 - 4 * k], ra[29 - 4 * k], ra[28 - 4 * k]);
+                                    st_shared_v4(stg_row + box + (((uint32_t)k ^ swz) << 4), ra[31 - 4 * k], ra[30 - 4 * k], ra[29 - 4 * k], ra[28 - 4 * k]);
                                 fence_proxy_async_smem();
+                                if (kStagingBufs2 == 2 && store_leader) bulk_wait_read();      // the previous store (other box)
                                 named_bar(bar_b, 128);
                                 if (store_leader && !(a.debug & 32)) {
-                                    tma_store_2d(&map_out, un.x0 + 64 * h + 32 * c, out_plane * a.Hp + un.y0, stg);
+                                    tma_store_2d(&map_out, un.x0 + 64 * h + 32 * c, out_plane * a.Hp + un.y0, stg + box);
                                     bulk_commit();
                                 }
                             }
