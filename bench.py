@@ -413,7 +413,8 @@ def run_ours(args):
                 "tensor_pipe_busy_estimate": n_mma * 64.0 / 148.0 / (col_ms_iso * 1e-3 * sm_hz),
                 "level_groups": groups,
             }
-            kernel_name = "umma_pass_kernel<kModeDog> (tcgen05 Toeplitz-GEMM column pass + fused DoG)"
+            kernel_name = ("umma_pass_kernel<kModeDog> (tcgen05 Toeplitz-GEMM column pass + fused DoG + in-slice part of "
+                           "the extrema search: seed list)")
         else:
             engine_roof = {"note": "this kernel is FP32-FMA bound, not HBM bound (SURVEY 7, 8d): "
                                    "arithmetic intensity 38 FLOP/B",
@@ -429,6 +430,12 @@ def run_ours(args):
                     "bytes_per_launch": col_bytes, "ms_per_launch_isolated": col_ms_iso,
                     "ms_per_launch_in_timed_region": col_ms,
                     "tensor" if tensor_engine else "fp32": engine_roof,
+                    # the kernel also does the in-slice half of the extrema search (DESIGN 3a, seeds), which is what lets
+                    # the extrema stage skip its 4HWS-byte read of the slices: the pair against the pair's bytes
+                    "column_pass_plus_extrema": {
+                        "bytes": col_bytes + 4.0 * H * W * S,
+                        "ms_isolated": col_ms_iso + float(iso[:, 2].mean()),
+                        "frac": (col_bytes + 4.0 * H * W * S) / ((col_ms_iso + float(iso[:, 2].mean())) * 1e-3) / 1e9 / peak},
                     "whole_frame": {"bytes": frame_bytes, "flops": frame_flops,
                                     "hbm_frac_at_value": frame_bytes * value / world / 1e9 / peak}}
         line = {

@@ -14,7 +14,7 @@ python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_referen
 for c in C2 C4; do DOGBLOB_UMMA_DEBUG=0 DOGBLOB_UMMA_PROF=1 timeout 100 python tools/umma_masks.py $c 0 2>&1 | tail -28 > gpurun_out/roles_$c.txt; done
 export DOGBLOB_STREAMED_UPLOAD=0
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s 30 -c 10 --csv --log-file gpurun_out/launches_one_frame.csv python tools/profile_run.py --frames 5 > gpurun_out/prof1.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"umma_pass|nms_window" -s 6 -c 3 -o gpurun_out/umma_full -f python tools/profile_run.py --frames 5 > gpurun_out/prof2.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"umma_pass|nms_seed|nms_window" -s 6 -c 3 -o gpurun_out/umma_full -f python tools/profile_run.py --frames 5 > gpurun_out/prof2.log 2>&1
 unset DOGBLOB_STREAMED_UPLOAD
 DOGBLOB_BENCH_BATCH=16 ncu --metrics gpu__time_duration.sum --clock-control none -s 48 -c 400 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 2 --warmup 1 > gpurun_out/prof3.log 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1

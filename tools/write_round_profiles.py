@@ -70,9 +70,9 @@ lines.append(f"| | total | {tot:.1f} | | |")
 (P / f"{tag}_launches_one_frame.md").write_text("\n".join(lines) + "\n")
 old = json.loads((P / "ncu_traffic.json").read_text())
 old.update({"source": f"profiles/{tag}_launches_one_frame.md (ncu dram__bytes_read.sum + dram__bytes_write.sum per launch, C2 frame)",
-            "umma_col_dog_kernel_dram_bytes_per_launch": traffic.get("umma_pass_kernel<1>"),
-            "umma_row_kernel_dram_bytes_per_launch": traffic.get("umma_pass_kernel<0>"),
-            "nms_window_kernel_dram_bytes_per_launch": next((v for k, v in traffic.items() if k.startswith("nms_window")), None)})
+            "umma_col_dog_kernel_dram_bytes_per_launch": next((v for k, v in traffic.items() if k.startswith("umma_pass_kernel<1")), None),
+            "umma_row_kernel_dram_bytes_per_launch": next((v for k, v in traffic.items() if k.startswith("umma_pass_kernel<0")), None),
+            "nms_kernel_dram_bytes_per_launch": next((v for k, v in traffic.items() if k.startswith("nms_")), None)})
 (P / "ncu_traffic.json").write_text(json.dumps(old, indent=1) + "\n")
 
 py = sys.executable
