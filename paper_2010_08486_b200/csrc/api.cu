@@ -195,7 +195,7 @@ UmmaSchedule plan_umma_schedule(const std::vector<LevelDesc> &lv, int tiles, int
     std::vector<double> gc;
     const int g_hi = std::min(L - 1, std::max(2, std::min(14, 4 * ctas / std::max(1, tiles) + 2)));
     for (int G = 1; G <= g_hi; ++G) {
-        if (force_groups > 0 && G != std::min(force_groups, L - 1)) continue;
+        if (force_groups > 0 && G != std::min(force_groups, g_hi)) continue;
         std::vector<int> begin(G + 1, 0);
         begin[G] = L;
         for (int g = 1; g < G; ++g) {             // start from groups of equal cost
