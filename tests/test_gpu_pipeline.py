@@ -788,3 +788,22 @@ class TestSeedList:
             got[cap] = det.run(frame).blobs.records
             det.close()
         assert len(got[None]) > 100 and np.array_equal(got[None], got["0"])
+
+    @pytest.mark.parametrize("thr", [0.0, -0.05])
+    def test_thresholds_at_and_below_zero(self, monkeypatch, thr):
+        """every block has a hit and the in-slice maxima of flat noise overflow the list: the strip walk
+        inside the seed kernel must return what the plan without a list returns"""
+        monkeypatch.setenv("DOGBLOB_CONV", "umma")
+        frame = synth.sensor_noise(synth.droplet_scene(400, 300, 10, (4.0, 20.0), seed=3), seed=4).image
+        kw = dict(min_sigma=2.0, max_sigma=20.0, n_bin=12, threshold=thr, preprocess=False, prune=False)
+        got = {}
+        for cap in (None, "0"):
+            if cap is None:
+                monkeypatch.delenv("DOGBLOB_SEED_CAP", raising=False)
+            else:
+                monkeypatch.setenv("DOGBLOB_SEED_CAP", cap)
+            det = P.Detector(P.DetectionParams(**kw), slots=1, max_blobs=1 << 20)
+            assert det.plan_for(frame.shape).plan.conv_engine == 2
+            got[cap] = det.run(frame).blobs.records
+            det.close()
+        assert len(got[None]) > 1000 and np.array_equal(got[None], got["0"])
