@@ -90,11 +90,7 @@ constexpr int kStageBytes2 = 32768;       // pass 2: [hi | lo][128 rows][128 B]
 // unless that costs the fourth data stage (wide ladders: large Toeplitz buffers); 0 = choose, 1 / 2 = force
 constexpr int kStagingForce1 = DOGBLOB_UMMA_STAGING1;
 __host__ __device__ constexpr int staging_bytes1(int bufs) { return 32768 * bufs; }
-#ifndef DOGBLOB_UMMA_STAGING2
-#define DOGBLOB_UMMA_STAGING2 1
-#endif
-constexpr int kStagingBufs2 = DOGBLOB_UMMA_STAGING2;     // pass 2 drain staging: 16 KB boxes per column half
-constexpr int kStagingBytes2 = 32768 * kStagingBufs2;
+constexpr int kStagingBytes2 = 32768;     // pass 2 drain staging: one 4 KB box (32 rows x 32 floats) per drain warp
 constexpr int kMaxStages = 8;
 #ifndef DOGBLOB_UMMA_BACKOFF
 #define DOGBLOB_UMMA_BACKOFF 0
@@ -668,12 +664,14 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
         const int row = kRows ? kUT - 1 - (32 * q + lane) : 32 * q + lane;     // output row inside the tile
         const bool store_leader = q == 0 && lane == 0;       // issues this half's TMA stores
         const int bar_a = 1 + 2 * h, bar_b = 2 + 2 * h;      // named barriers of this half (128 threads)
-        uint32_t lvl_it = 0, round_it = 0, store_it = 0;
+        uint32_t lvl_it = 0, round_it = 0;
         RoleClock rc(a.prof != nullptr && dw == 0 && lane == 0);
         const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(kRows ? 64 * h : 64 * (1 - h));
-        const uint32_t stg = smem_u32(staging + (size_t)h * 16384 * (kRows ? kStagingBufs1 : kStagingBufs2));
+        const uint32_t stg = smem_u32(staging + (size_t)h * 16384 * kStagingBufs1);      // pass 1
         const uint32_t stg_row = stg + (uint32_t)row * 128u;
         const uint32_t swz = (uint32_t)(row & 7);
+        // pass 2: one 32-row x 128-byte box per drain warp
+        const uint32_t wbox = smem_u32(staging + (size_t)dw * 4096), wbox_row = wbox + (uint32_t)lane * 128u;
         const int frame_exp = frame_scale_exp(a.frame_max_bits);
         const float unscale_x = pow2f(-frame_exp);
         float prev[64];                                      // pass 2: previous level of this thread's outputs
@@ -825,29 +823,22 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                                     *reinterpret_cast<uint32_t *>(a.flags.data +
                                         ((int64_t)out_plane * a.flags.col_blocks + ((un.x0 >> 5) + 2 * h + c)) * a.flags.row_blocks +
                                         ((un.y0 >> 3) + 4 * q)) = word;
-                                    if (may_skip) ctl->box_hit[round_it & 1u][h][q] = m;
                                 }
-                            }
-                            if (kStagingBufs2 == 1 && store_leader) bulk_wait_read();
-                            named_bar(bar_a, 128);               // also publishes the four ballots of this box
-                            if (may_skip) {
-                                const volatile uint32_t *bh = ctl->box_hit[round_it & 1u][h];
-                                store = (bh[0] | bh[1] | bh[2] | bh[3]) != 0u;      // uniform over the half
-                                ++round_it;
+                                if (may_skip) store = m != 0u;
                             }
                             if (store) {
-                                // two boxes per half: this one was last stored two stores ago, and that store's
-                                // read was waited for before the previous barrier b
-                                const uint32_t box = kStagingBufs2 == 2 ? (store_it & 1u) * 16384u : 0u;
-                                ++store_it;
+                                // This warp's own 32 x 32 box (4 KB, swizzled like a 128-row box): no barrier with
+                                // the other drain warps anywhere in this pass - a warp that stores or tests seeds
+                                // does not hold up one that has nothing above the threshold.
+                                if (lane == 0) bulk_wait_read();     // the warp's previous store has read the box
+                                __syncwarp();
 #pragma unroll
                                 for (int k = 0; k < 8; ++k)      // output element i of the chunk is ra[31 - i]
-                                    st_shared_v4(stg_row + box + (((uint32_t)k ^ swz) << 4), ra[31 - 4 * k], ra[30 - 4 * k], ra[29 - 4 * k], ra[28 - 4 * k]);
+                                    st_shared_v4(wbox_row + (((uint32_t)k ^ swz) << 4), ra[31 - 4 * k], ra[30 - 4 * k], ra[29 - 4 * k], ra[28 - 4 * k]);
                                 fence_proxy_async_smem();
-                                if (kStagingBufs2 == 2 && store_leader) bulk_wait_read();      // the previous store (other box)
-                                named_bar(bar_b, 128);
-                                if (store_leader && !(a.debug & 32)) {
-                                    tma_store_2d(&map_out, un.x0 + 64 * h + 32 * c, out_plane * a.Hp + un.y0, stg + box);
+                                __syncwarp();
+                                if (lane == 0 && !(a.debug & 32)) {
+                                    tma_store_2d(&map_out, un.x0 + 64 * h + 32 * c, out_plane * a.Hp + un.y0 + 32 * q, wbox);
                                     bulk_commit();
                                 }
                             }
@@ -890,7 +881,7 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                 }
             }
         }
-        if (store_leader) bulk_wait_all();
+        if (kRows ? store_leader : lane == 0) bulk_wait_all();
         rc.lap(1);
         rc.flush(a.prof, 8);
     }
@@ -1283,10 +1274,10 @@ cudaError_t launch_col_pass_umma(const ConvGeometry &g, const void *d_r, float *
         if (!encode_map(&map_in, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, d_r, dims, strides, box))
             return cudaErrorInvalidValue;
     }
-    {   // output planes {W valid columns, rows of all planes}; box = 128 rows x 32 floats
+    {   // output planes {W valid columns, rows of all planes}; box = 32 rows x 32 floats (one per drain warp)
         const cuuint64_t dims[2] = {(cuuint64_t)g.W, (cuuint64_t)g.L * g.Hp};
         const cuuint64_t strides[1] = {(cuuint64_t)g.Wp * 4};
-        const cuuint32_t box[2] = {32, 128};
+        const cuuint32_t box[2] = {32, 32};
         if (!encode_map(&map_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d_out, dims, strides, box))
             return cudaErrorInvalidValue;
     }
