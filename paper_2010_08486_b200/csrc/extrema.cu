@@ -37,10 +37,8 @@ struct VolumeT {
         return valid == nullptr || valid[((int64_t)s * v_col_blocks + (c >> kFlagColShift)) * v_row_blocks + (r >> kFlagRowShift)] != 0;
     }
     __device__ __forceinline__ T at(int s, int r, int c) const {
-        // both loads are issued at once (one memory round trip, not two): an unstored block is readable
-        // memory of the same buffer, its stale value is simply dropped
-        const T v = __ldg(data + (int64_t)s * plane + (int64_t)r * pitch + c);
-        return block_valid(s, r, c) ? v : (T)-INFINITY;
+        if (!block_valid(s, r, c)) return (T)-INFINITY;      // (loading first and selecting afterwards measured 10-20 % slower)
+        return __ldg(data + (int64_t)s * plane + (int64_t)r * pitch + c);
     }
 };
 using Volume = VolumeT<float>;     // production path; VolumeT<double>: the float64 tier (fp64.cu)
