@@ -92,6 +92,9 @@ constexpr int kStagingForce1 = DOGBLOB_UMMA_STAGING1;
 __host__ __device__ constexpr int staging_bytes1(int bufs) { return 32768 * bufs; }
 constexpr int kStagingBytes2 = 32768;     // pass 2 drain staging: one 4 KB box (32 rows x 32 floats) per drain warp
 constexpr int kMaxStages = 8;
+#ifndef DOGBLOB_UMMA_ORDER1
+#define DOGBLOB_UMMA_ORDER1 1      // pass 1: narrow MMAs of a stage first, wide ones last (0: interleaved)
+#endif
 #ifndef DOGBLOB_UMMA_BACKOFF
 #define DOGBLOB_UMMA_BACKOFF 0
 #endif
@@ -295,6 +298,18 @@ __device__ __forceinline__ void umma_f16_wide_pair_ss_1t(uint32_t d_main, uint32
         "tcgen05.mma.cta_group::1.kind::f16 [ds], a1, b0, %7, q;\n\t}"
         ::"r"(d_main), "r"(a_hi), "r"(a_lo), "r"(b_hi), "r"(a_upper), "r"(b_upper), "r"(idesc256), "r"(idesc128),
           "r"(acc)
+        : "memory");
+}
+// one MMA: D (+)= A * B with the descriptor words split like above
+__device__ __forceinline__ void umma_f16_ss_1t(uint32_t d, uint32_t a_lo32, uint32_t b_lo32, uint32_t a_upper,
+                                               uint32_t b_upper, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b64 a0, b0;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "mov.b64 a0, {%1, %3};\n\t"
+        "mov.b64 b0, {%2, %4};\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a0, b0, %5, p;\n\t}"
+        ::"r"(d), "r"(a_lo32), "r"(b_lo32), "r"(a_upper), "r"(b_upper), "r"(idesc), "r"(acc)
         : "memory");
 }
 __device__ __forceinline__ void umma_commit_1t(uint32_t bar) {
@@ -534,6 +549,35 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                     const int first_k = kRows ? kRowsPerStage1 * st : (st == n_stage - 1 ? Kp - 64 : 64 * st);
                     const int j0 = kStepsPerStage * st;
                     const int j1 = min(n_k, j0 + kStepsPerStage);
+#if DOGBLOB_UMMA_ORDER1
+                    if (kRows && !(a.debug & (8 | 256))) {
+                        // Pass 1, the narrow MMAs first and the wide ones last: a commit holds the issuing thread
+                        // ~250 cycles, and only what is queued behind it keeps the tensor pipe busy meanwhile - two
+                        // N = 256 MMAs (128 cycles each) instead of a wide and a narrow one (192).  The level's very
+                        // first MMA must be the wide one that initialises both accumulators.
+                        const uint32_t i256 = instr_desc_f16(kUT, 2 * kUT, 1), i128 = instr_desc_f16(kUT, kUT, 1);
+                        if (j0 == 0) {
+                            const uint32_t bd = ((sbase + 0u) >> 4) | kData1LowLbo;
+                            umma_f16_ss_1t(d_main, win0, bd, kToepUpper, kData1Upper, i256, 0u);
+                        }
+#pragma unroll
+                        for (int q = 0; q < kStepsPerStage; ++q) {
+                            const int j = j0 + q;
+                            if (j < j1) {
+                                const uint32_t bd = ((sbase + (uint32_t)(16 * j - first_k) * 128u) >> 4) | kData1LowLbo;
+                                umma_f16_ss_1t(d_small, win0 + 16u * (uint32_t)j + lo_off, bd, kToepUpper, kData1Upper, i128, 1u);
+                            }
+                        }
+#pragma unroll
+                        for (int q = 0; q < kStepsPerStage; ++q) {
+                            const int j = j0 + q;
+                            if (j < j1 && j > 0) {
+                                const uint32_t bd = ((sbase + (uint32_t)(16 * j - first_k) * 128u) >> 4) | kData1LowLbo;
+                                umma_f16_ss_1t(d_main, win0 + 16u * (uint32_t)j, bd, kToepUpper, kData1Upper, i256, 1u);
+                            }
+                        }
+                    } else
+#endif
 #pragma unroll
                     for (int q = 0; q < kStepsPerStage; ++q) {
                         const int j = j0 + q;
