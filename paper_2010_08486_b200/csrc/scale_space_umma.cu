@@ -377,6 +377,10 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
                  : "memory");
 }
 
+__device__ __forceinline__ void st_shared_b32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
 // Shared-memory matrix descriptors (cute::UMMA::SmemDescriptor):
 //   bits [0,14) start address >> 4    [16,30) leading byte offset >> 4    [32,46) stride byte
 //   offset >> 4    [46,48) version = 1    [61,64) layout type (0 none, 2 SWIZZLE_128B)
@@ -534,8 +538,8 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                 // low descriptor word of the Toeplitz window of k-step 0 (row 0); every k-step moves
                 // the window down by 16 rows of 16 bytes = 16 descriptor units
                 const uint32_t t_hi = smem_u32(toep + (size_t)tb * a.toep_bytes);
-                // hi -> lo array (16 B per row); pass 2 never reads the last 112 rows and leaves them out
-                const uint32_t lo_off = kRows ? (uint32_t)ttab.rows[level] : (uint32_t)(Kp + 8);
+                // hi -> lo array (16 B per row)
+                const uint32_t lo_off = (uint32_t)ttab.rows[level];
                 const uint32_t win0 = (t_hi >> 4) | kToepLowLbo;
                 const uint32_t d_main = tmem + b * 2 * kAccCols, d_small = d_main + kAccCols;
                 for (int st = 0; st < n_stage; ++st) {
@@ -549,64 +553,36 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                     const int first_k = kRows ? kRowsPerStage1 * st : (st == n_stage - 1 ? Kp - 64 : 64 * st);
                     const int j0 = kStepsPerStage * st;
                     const int j1 = min(n_k, j0 + kStepsPerStage);
-#if DOGBLOB_UMMA_ORDER1
-                    if (kRows && !(a.debug & (8 | 256))) {
-                        // Pass 1, the narrow MMAs first and the wide ones last: a commit holds the issuing thread
-                        // ~250 cycles, and only what is queued behind it keeps the tensor pipe busy meanwhile - two
-                        // N = 256 MMAs (128 cycles each) instead of a wide and a narrow one (192).  The level's very
-                        // first MMA must be the wide one that initialises both accumulators.
-                        const uint32_t i256 = instr_desc_f16(kUT, 2 * kUT, 1), i128 = instr_desc_f16(kUT, kUT, 1);
-                        if (j0 == 0) {
-                            const uint32_t bd = ((sbase + 0u) >> 4) | kData1LowLbo;
-                            umma_f16_ss_1t(d_main, win0, bd, kToepUpper, kData1Upper, i256, 0u);
+                    if (!(a.debug & 8)) {
+                        // Both passes: A = Toeplitz window (M = 128 outputs of the convolved axis), B = 16 inputs of
+                        // the stage with the hi and the lo plane as ONE operand of N = 256 (pass 1: MN-major image
+                        // rows, N = x; pass 2: K-major rows of R, N = y - the lo box sits 128 rows = 16 KB behind the
+                        // hi box, exactly where rows 128..255 of a 256-row operand belong).  Per k-step
+                        //     [main | small] += T_hi * [X_hi | X_lo]   (N = 256)      small += T_lo * X_hi   (N = 128)
+                        // The narrow MMAs of a stage go first and the wide ones last: a commit holds the issuing
+                        // thread ~250 cycles, and only what is queued behind it keeps the tensor pipe busy meanwhile
+                        // (two N = 256 MMAs = 256 cycles).  The level's very first MMA must be the wide one that
+                        // initialises both accumulators.
+                        constexpr int b_mn = kRows ? 1 : 0;
+                        const uint32_t i256 = instr_desc_f16(kUT, 2 * kUT, b_mn), i128 = instr_desc_f16(kUT, kUT, b_mn);
+                        constexpr uint32_t b_upper = kRows ? kData1Upper : kData2Upper;
+                        // byte offset of k-step j inside the stage: pass 1: 16 rows of 128 B; pass 2: 32 B along the row
+                        auto b_desc = [&](int j) {
+                            return kRows ? ((sbase + (uint32_t)(16 * j - first_k) * 128u) >> 4) | kData1LowLbo
+                                         : ((sbase + (uint32_t)(16 * j - first_k) * 2u) >> 4) | kData2LowLbo;
+                        };
+                        if (j0 == 0) umma_f16_ss_1t(d_main, win0, b_desc(0), kToepUpper, b_upper, i256, 0u);
+#pragma unroll
+                        for (int q = 0; q < kStepsPerStage; ++q) {
+                            const int j = j0 + q;
+                            if (j < j1)
+                                umma_f16_ss_1t(d_small, win0 + 16u * (uint32_t)j + lo_off, b_desc(j), kToepUpper, b_upper, i128, 1u);
                         }
 #pragma unroll
                         for (int q = 0; q < kStepsPerStage; ++q) {
                             const int j = j0 + q;
-                            if (j < j1) {
-                                const uint32_t bd = ((sbase + (uint32_t)(16 * j - first_k) * 128u) >> 4) | kData1LowLbo;
-                                umma_f16_ss_1t(d_small, win0 + 16u * (uint32_t)j + lo_off, bd, kToepUpper, kData1Upper, i128, 1u);
-                            }
-                        }
-#pragma unroll
-                        for (int q = 0; q < kStepsPerStage; ++q) {
-                            const int j = j0 + q;
-                            if (j < j1 && j > 0) {
-                                const uint32_t bd = ((sbase + (uint32_t)(16 * j - first_k) * 128u) >> 4) | kData1LowLbo;
-                                umma_f16_ss_1t(d_main, win0 + 16u * (uint32_t)j, bd, kToepUpper, kData1Upper, i256, 1u);
-                            }
-                        }
-                    } else
-#endif
-#pragma unroll
-                    for (int q = 0; q < kStepsPerStage; ++q) {
-                        const int j = j0 + q;
-                        if (j < j1 && !(a.debug & 8)) {
-                            const int m0 = 16 * j;
-                            const uint32_t win = win0 + 16u * (uint32_t)j;
-                            if (kRows) {
-                                // A = Toeplitz window, B = 16 image rows of the stage (2 KB per k-step)
-                                const uint32_t bd = ((sbase + (uint32_t)(m0 - first_k) * 128u) >> 4) | kData1LowLbo;
-                                if (a.debug & 256)        // the three-instruction form (A/B comparison)
-                                    umma_f16_triple_ss_1t(d_main, d_small, win, win + lo_off, bd, bd + ((256u * kRowsPerStage1) >> 4),
-                                                          kToepUpper, kData1Upper, instr_desc_f16(kUT, kUT, 1), j > 0);
-                                else
-                                    umma_f16_wide_pair_ss_1t(d_main, win, win + lo_off, bd, kToepUpper, kData1Upper,
-                                                             instr_desc_f16(kUT, 2 * kUT, 1), instr_desc_f16(kUT, kUT, 1),
-                                                             j > 0);
-                            } else {
-                                // A = 16 k-columns of the stage (32 B into the swizzle atom per k-step),
-                                // B = Toeplitz window rows [ns, ne)
-                                const int ns = j == 0 ? 0 : (max(0, m0 - rpad2) & ~15);
-                                const int ne = j == 0 ? kUT : min(kUT, m0 + 16);
-                                const uint32_t ad = ((sbase + (uint32_t)(m0 - first_k) * 2u) >> 4) | kData2LowLbo;
-                                // reversed operand rows: outputs [ns, ne) are rows / accumulator columns
-                                // [128 - ne, 128 - ns)
-                                const uint32_t bw = win + (uint32_t)(kUT - ne);
-                                umma_f16_triple_ss_1t(d_main + (kUT - ne), d_small + (kUT - ne), ad, ad + (16384u >> 4), bw,
-                                                   bw + lo_off, kData2Upper, kToepUpper,
-                                                   instr_desc_f16(kUT, ne - ns, 0), j > 0);
-                            }
+                            if (j < j1 && j > 0)
+                                umma_f16_ss_1t(d_main, win0 + 16u * (uint32_t)j, b_desc(j), kToepUpper, b_upper, i256, 1u);
                         }
                     }
                     // A commit stalls the issuing thread (~250 cycles, the tensor pipe runs dry behind
@@ -685,15 +661,8 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                     if (++tb == (uint32_t)NT) { tb = 0; tb_par ^= 1u; }
                     if (a.debug & 16) { mbar_arrive(bar); continue; }
                     const uint32_t rows = (uint32_t)ttab.rows[level];
-                    if (kRows) {
-                        mbar_expect_tx(bar, rows * 32u);                              // hi + lo
-                        bulk_copy_g2s(dst, a.toep + ttab.ofs[level], rows * 32u, bar);
-                    } else {                                                        // all but the last 112 rows of each array
-                        const uint32_t part = (rows - 112u) * 16u;
-                        mbar_expect_tx(bar, 2u * part);
-                        bulk_copy_g2s(dst, a.toep + ttab.ofs[level], part, bar);
-                        bulk_copy_g2s(dst + part, a.toep + ttab.ofs[level] + rows * 4u, part, bar);
-                    }
+                    mbar_expect_tx(bar, rows * 32u);                              // hi + lo
+                    bulk_copy_g2s(dst, a.toep + ttab.ofs[level], rows * 32u, bar);
                 }
             }
         }
@@ -703,19 +672,19 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
         // warp = lane quarter q (TMEM lanes 32 q .. 32 q + 31 = output rows) x column half h
         const int dw = warp - kDrainWarp0;
         const int q = dw & 3, h = dw >> 2;
-        // TMEM lane 32 q + lane; pass 1's operand rows are reversed (lane m' = output row 127 - m'),
-        // pass 2's accumulator COLUMNS are (column c = output column 127 - c)
-        const int row = kRows ? kUT - 1 - (32 * q + lane) : 32 * q + lane;     // output row inside the tile
+        // TMEM lane 32 q + lane; the Toeplitz operand's rows are reversed: lane m' = output row (pass 1) /
+        // output column (pass 2) 127 - m'
+        const int row = kUT - 1 - (32 * q + lane);                             // pass 1: output row inside the tile
         const bool store_leader = q == 0 && lane == 0;       // issues this half's TMA stores
         const int bar_a = 1 + 2 * h, bar_b = 2 + 2 * h;      // named barriers of this half (128 threads)
         uint32_t lvl_it = 0, round_it = 0;
         RoleClock rc(a.prof != nullptr && dw == 0 && lane == 0);
-        const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(kRows ? 64 * h : 64 * (1 - h));
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(64 * h);
         const uint32_t stg = smem_u32(staging + (size_t)h * 16384 * kStagingBufs1);      // pass 1
         const uint32_t stg_row = stg + (uint32_t)row * 128u;
         const uint32_t swz = (uint32_t)(row & 7);
         // pass 2: one 32-row x 128-byte box per drain warp
-        const uint32_t wbox = smem_u32(staging + (size_t)dw * 4096), wbox_row = wbox + (uint32_t)lane * 128u;
+        const uint32_t wbox = smem_u32(staging + (size_t)dw * 4096);
         const int frame_exp = frame_scale_exp(a.frame_max_bits);
         const float unscale_x = pow2f(-frame_exp);
         float prev[64];                                      // pass 2: previous level of this thread's outputs
@@ -821,21 +790,28 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                     rc.lap(3);
                 } else {
                     // ---- pass 2: level value -> DoG slice against the previous level (registers) ----
+                    // TMEM lane = output COLUMN (reversed: lane m' is column 127 - m'), accumulator column = row y:
+                    // this thread owns column xbase + xi of rows 64 h .. 64 h + 63, the warp a 32 x 32 box per chunk.
                     const bool emit = MODE == kModeLevels || level > un.lb;
                     const float sig = MODE == kModeDog && level > un.lb ? tbl.lv[level - 1].sigma_f32 : 0.f;
                     const int out_plane = MODE == kModeLevels ? level : level - 1;
-                    // With a threshold (detection), a 128 x 32 box of the slice in which nothing exceeds it is
+                    // With a threshold (detection), a 32 x 32 box of the slice in which nothing exceeds it is
                     // not even stored: the extrema kernel reads blocks without a hit as -inf (HitFlags double
                     // as the validity map), so whatever that memory holds is never looked at.
                     const bool want_flags = MODE == kModeDog && a.flags.data != nullptr;
                     const bool may_skip = want_flags && !(a.debug & 512);
-                    const bool row_in = un.y0 + row < a.H;
+                    const int xbase = un.x0 + 96 - 32 * q;       // first column of the warp's boxes
+                    const uint32_t xi = 31u - (uint32_t)lane;    // this thread's column inside the box
+                    // staging address of element (row j, column xi) of the swizzled 32 x 128-byte box:
+                    // j * 128 + ((xi / 4) ^ (j & 7)) * 16 + (xi & 3) * 4 - the lanes of a store cover all 32 banks
+                    const uint32_t st_col = wbox + ((xi & 3u) << 2), st_chunk = (xi >> 2) << 4;
 #pragma unroll
                     for (int c = 0; c < 2; ++c) {
-                        bool hit = false;
+                        const int ybase = un.y0 + 64 * h + 32 * c;
+                        const int nrows = a.H - ybase;           // rows j < nrows of the box are inside the frame
+                        bool hit0 = false, hit1 = false, hit2 = false, hit3 = false;     // per 8-row block
                         uint32_t ra[32], rb[32];
-                        // outputs 64 h + 32 c .. + 31 are accumulator columns 96 - 64 h - 32 c .. + 31, reversed
-                        tmem_ld32_pair(acc + 32 * (1 - c), acc + kAccCols + 32 * (1 - c), ra, rb);
+                        tmem_ld32_pair(acc + 32 * c, acc + kAccCols + 32 * c, ra, rb);
                         if (c == 1) {
                             tc_fence_before();
                             __syncwarp();
@@ -848,7 +824,10 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                                 const float d = __fmul_rn(__fsub_rn(prev[32 * c + j], v), sig);
                                 ra[j] = __float_as_uint(d);
                                 prev[32 * c + j] = v;
-                                hit = hit || d > a.thr;
+                                if (j < 8) hit0 = hit0 || d > a.thr;
+                                else if (j < 16) hit1 = hit1 || d > a.thr;
+                                else if (j < 24) hit2 = hit2 || d > a.thr;
+                                else hit3 = hit3 || d > a.thr;
                             } else {
                                 ra[j] = __float_as_uint(v);
                             }
@@ -856,19 +835,29 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                         rc.lap(2);
                         if (emit && !(a.debug & 2)) {            // uniform per level
                             bool store = true;
-                            uint32_t hit_rows = 0u;          // ballot: this warp's rows with a value above the threshold
+                            uint32_t hit_any = 0u;
                             if (want_flags) {
                                 // this warp's 32 rows x 32 columns: which of its four 8-row blocks hold a value
                                 // above the threshold (rows below the frame do not count)?
-                                const uint32_t m = hit_rows = __ballot_sync(0xffffffffu, hit && row_in);
-                                if (lane == 0) {
-                                    const uint32_t word = ((m & 0xffu) ? 1u : 0u) | ((m & 0xff00u) ? 0x100u : 0u) |
-                                                          ((m & 0xff0000u) ? 0x10000u : 0u) | ((m & 0xff000000u) ? 0x1000000u : 0u);
-                                    *reinterpret_cast<uint32_t *>(a.flags.data +
-                                        ((int64_t)out_plane * a.flags.col_blocks + ((un.x0 >> 5) + 2 * h + c)) * a.flags.row_blocks +
-                                        ((un.y0 >> 3) + 4 * q)) = word;
+                                if (nrows < 32) {                // bottom edge of the frame: rare
+                                    hit0 = hit1 = hit2 = hit3 = false;
+#pragma unroll
+                                    for (int j = 0; j < 32; ++j) {
+                                        const bool t = j < nrows && __uint_as_float(ra[j]) > a.thr;
+                                        if (j < 8) hit0 = hit0 || t;
+                                        else if (j < 16) hit1 = hit1 || t;
+                                        else if (j < 24) hit2 = hit2 || t;
+                                        else hit3 = hit3 || t;
+                                    }
                                 }
-                                if (may_skip) store = m != 0u;
+                                const uint32_t word = (__any_sync(0xffffffffu, hit0) ? 1u : 0u) | (__any_sync(0xffffffffu, hit1) ? 0x100u : 0u) |
+                                                      (__any_sync(0xffffffffu, hit2) ? 0x10000u : 0u) | (__any_sync(0xffffffffu, hit3) ? 0x1000000u : 0u);
+                                hit_any = word;
+                                if (lane == 0)
+                                    *reinterpret_cast<uint32_t *>(a.flags.data +
+                                        ((int64_t)out_plane * a.flags.col_blocks + ((un.x0 >> 5) + 3 - q)) * a.flags.row_blocks +
+                                        ((un.y0 >> 3) + 8 * h + 4 * c)) = word;
+                                if (may_skip) store = word != 0u;
                             }
                             if (store) {
                                 // This warp's own 32 x 32 box (4 KB, swizzled like a 128-row box): no barrier with
@@ -877,27 +866,26 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                                 if (lane == 0) bulk_wait_read();     // the warp's previous store has read the box
                                 __syncwarp();
 #pragma unroll
-                                for (int k = 0; k < 8; ++k)      // output element i of the chunk is ra[31 - i]
-                                    st_shared_v4(wbox_row + (((uint32_t)k ^ swz) << 4), ra[31 - 4 * k], ra[30 - 4 * k], ra[29 - 4 * k], ra[28 - 4 * k]);
+                                for (int j = 0; j < 32; ++j)
+                                    st_shared_b32(st_col + (uint32_t)(j * 128) + (st_chunk ^ (uint32_t)((j & 7) << 4)), ra[j]);
                                 fence_proxy_async_smem();
                                 __syncwarp();
                                 if (lane == 0 && !(a.debug & 32)) {
-                                    tma_store_2d(&map_out, un.x0 + 64 * h + 32 * c, out_plane * a.Hp + un.y0 + 32 * q, wbox);
+                                    tma_store_2d(&map_out, xbase, out_plane * a.Hp + ybase, wbox);
                                     bulk_commit();
                                 }
                             }
-                            if (a.flags.seeds != nullptr && hit_rows != 0u) {      // uniform per warp; after the store: the box is read meanwhile
+                            if (a.flags.seeds != nullptr && hit_any != 0u) {      // uniform per warp; after the store: the box is read meanwhile
                                 // Seeds: values above the threshold that no in-slice neighbour KNOWN HERE exceeds
-                                // (same row: this thread's other columns of the chunk; rows above / below: the
+                                // (same column: this thread's other rows of the chunk; columns left / right: the
                                 // adjacent lanes; everything else, and everything outside the frame, counts as
-                                // -inf).  A lane without a neighbour lane gets its own row maximum back from the
-                                // shuffle, which a row maximum passes by construction.
-                                const int xbase = un.x0 + 64 * h + 32 * c;
-                                const int nvalid = row_in ? a.W - xbase : 0;         // output elements i < nvalid are inside
-                                if (a.W - xbase < 32 || !row_in) {                    // frame edge: rare
+                                // -inf).  A lane without a neighbour lane gets its own column maximum back from the
+                                // shuffle, which a column maximum passes by construction.
+                                const int x = xbase + (int)xi;
+                                if (nrows < 32 || x >= a.W) {                       // frame edge: rare
 #pragma unroll
                                     for (int j = 0; j < 32; ++j)
-                                        if (31 - j >= nvalid) ra[j] = 0xff800000u;   // -inf
+                                        if (j >= nrows || x >= a.W) ra[j] = 0xff800000u;   // -inf
                                 }
                                 uint32_t seedmask = 0u;
 #pragma unroll
@@ -912,11 +900,10 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                                 }
                                 if (seedmask != 0u) {
                                     int at = atomicAdd(a.flags.n_seeds, __popc(seedmask));
-                                    const unsigned long long key = ((unsigned long long)out_plane << 48) |
-                                                                   ((unsigned long long)(un.y0 + row) << 24);
+                                    const unsigned long long key = ((unsigned long long)out_plane << 48) | (unsigned long long)x;
                                     for (; seedmask != 0u; seedmask &= seedmask - 1u, ++at)
                                         if (at < a.flags.seed_cap)
-                                            a.flags.seeds[at] = key | (unsigned long long)(xbase + 32 - __ffs(seedmask));
+                                            a.flags.seeds[at] = key | ((unsigned long long)(ybase + __ffs(seedmask) - 1) << 24);
                                 }
                             }
                         }
@@ -1022,7 +1009,8 @@ int toeplitz_rows(int rpad) { return kUT + 2 * rpad - 16 + kUT + 8; }
 // one Toeplitz buffer in shared memory: pass 2 (Toeplitz = B operand, band trimmed) never reads the
 // last 112 rows of the arrays and does not copy them
 int toeplitz_buffer_bytes(int max_rpad, bool rows_pass) {
-    return ((toeplitz_rows(max_rpad) - (rows_pass ? 0 : 112)) * 32 + 127) / 128 * 128;
+    (void)rows_pass;
+    return (toeplitz_rows(max_rpad) * 32 + 127) / 128 * 128;
 }
 // control block + Toeplitz ring, rounded up to the 1 KB alignment of the swizzled boxes behind it
 size_t staging_offset(int max_rpad, bool rows_pass) {
