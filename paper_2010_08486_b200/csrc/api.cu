@@ -540,8 +540,8 @@ static cudaError_t row_pass_any(const dogblob_plan *plan, const float *d_image, 
 static HitFlags hit_flags_of(const dogblob_plan *plan, void *d_workspace) {
     HitFlags f;
     f.data = reinterpret_cast<unsigned char *>(d_workspace) + plan->off_flags;
-    f.row_blocks = plan->geo.Hp >> kFlagRowShift;
-    f.col_blocks = plan->geo.Wp >> kFlagColShift;
+    f.row_blocks = plan->geo.Wp >> kFlagRowShift;      // blocks of the transposed slices: rows = x, columns = y
+    f.col_blocks = plan->geo.Hp >> kFlagColShift;
     if (plan->seed_cap > 0) {
         char *ws = reinterpret_cast<char *>(d_workspace);
         f.seeds = reinterpret_cast<unsigned long long *>(ws + plan->off_seeds);
@@ -550,7 +550,7 @@ static HitFlags hit_flags_of(const dogblob_plan *plan, void *d_workspace) {
     }
     return f;
 }
-// pass 2 fused with the DoG: tensor engine -> slices in image orientation, FP32 engine -> transposed.
+// pass 2 fused with the DoG: both engines write the slices transposed (D^T[slice][x][y]).
 // `threshold`: the tensor engine also records which blocks of the slices exceed it (for the extrema
 // kernel); NaN = not wanted (stage entry points).
 static cudaError_t col_dog_pass_any(const dogblob_plan *plan, void *d_workspace, cudaStream_t st,
@@ -565,18 +565,11 @@ static cudaError_t col_dog_pass_any(const dogblob_plan *plan, void *d_workspace,
     return launch_col_dog_pass(plan->geo, reinterpret_cast<const float *>(ws + plan->off_rows_t), dog,
                                reinterpret_cast<float *>(ws + plan->off_edge), plan->table, plan->d_taps, st);
 }
-// dense [planes][H][W] copy of the engine's plane stack (tensor engine: pitched rows; FP32: transposed)
+// dense [planes][H][W] copy of the engine's transposed plane stack
 static cudaError_t planes_to_dense(const dogblob_plan *plan, const float *d_planes, int planes, float *d_dst,
                                    cudaStream_t st) {
     const ConvGeometry &g = plan->geo;
-    if (!plan->use_umma) return launch_untranspose(d_planes, planes, g.Hp, g.Wp, g.H, g.W, d_dst, st);
-    for (int i = 0; i < planes; ++i) {
-        cudaError_t e = cudaMemcpy2DAsync(d_dst + (size_t)i * g.H * g.W, (size_t)g.W * sizeof(float),
-                                          d_planes + (size_t)i * g.Hp * g.Wp, (size_t)g.Wp * sizeof(float),
-                                          (size_t)g.W * sizeof(float), g.H, cudaMemcpyDeviceToDevice, st);
-        if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
+    return launch_untranspose(d_planes, planes, g.Hp, g.Wp, g.H, g.W, d_dst, st);
 }
 
 // reset + row pass (optionally gated on a streamed upload), then the rest of the frame
@@ -605,13 +598,10 @@ static int launch_frame_tail(const dogblob_plan *plan, float threshold, int neig
     const bool use_flags = plan->use_umma && neighborhood == 3 && !std::isnan(threshold);
     DB_CUDA(col_dog_pass_any(plan, d_workspace, st, use_flags ? threshold : NAN));
     DB_CUDA(ev(2));
-    if (plan->use_umma)     // D planes in image orientation: rows = y, cols = x
-        DB_CUDA(launch_extrema(dog, g.L - 1, g.H, g.W, g.Wp, (int64_t)g.Hp * g.Wp, false,
-                               plan->d_slice_sigma, threshold, neighborhood / 2, bs, st,
-                               use_flags ? hit_flags_of(plan, d_workspace) : HitFlags{}));
-    else                    // D^T planes: rows = x (W valid), cols = y (H valid)
-        DB_CUDA(launch_extrema(dog, g.L - 1, g.W, g.H, g.Hp, (int64_t)g.Hp * g.Wp, true,
-                               plan->d_slice_sigma, threshold, neighborhood / 2, bs, st));
+    // both engines: D^T planes, rows = x (W valid), cols = y (H valid)
+    DB_CUDA(launch_extrema(dog, g.L - 1, g.W, g.H, g.Hp, (int64_t)g.Hp * g.Wp, true,
+                           plan->d_slice_sigma, threshold, neighborhood / 2, bs, st,
+                           use_flags ? hit_flags_of(plan, d_workspace) : HitFlags{}));
     DB_CUDA(ev(3));
     DB_CUDA(launch_prune_and_pack(bs, overlap, prune != 0, d_result, plan->max_blobs, st));
     DB_CUDA(ev(4));

@@ -688,6 +688,15 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
         const int frame_exp = frame_scale_exp(a.frame_max_bits);
         const float unscale_x = pow2f(-frame_exp);
         float prev[64];                                      // pass 2: previous level of this thread's outputs
+        // pass 2: seeds of the previous chunk waiting for their list index (column bits, first index, key of column 0)
+        uint32_t p_mask = 0u;
+        int p_at = 0;
+        unsigned long long p_key = 0ull;
+        auto flush_seeds = [&]() {
+            for (; p_mask != 0u; p_mask &= p_mask - 1u, ++p_at)
+                if (p_at < a.flags.seed_cap)
+                    a.flags.seeds[p_at] = p_key + (unsigned long long)(__ffs(p_mask) - 1);
+        };
 #pragma unroll
         for (int j = 0; j < 64; ++j) prev[j] = 0.f;
         for (int ui = blockIdx.x; ui < a.n_sched; ui += gridDim.x) {
@@ -790,8 +799,9 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                     rc.lap(3);
                 } else {
                     // ---- pass 2: level value -> DoG slice against the previous level (registers) ----
-                    // TMEM lane = output COLUMN (reversed: lane m' is column 127 - m'), accumulator column = row y:
-                    // this thread owns column xbase + xi of rows 64 h .. 64 h + 63, the warp a 32 x 32 box per chunk.
+                    // TMEM lane = output COLUMN x (reversed: lane m' is column 127 - m'), accumulator column = row y.
+                    // The slices are written TRANSPOSED, D^T[slice][x][y] (like the FP32 engine's): a thread's 32
+                    // accumulator columns are 128 contiguous bytes of row x of D^T, staged with 16-byte stores.
                     const bool emit = MODE == kModeLevels || level > un.lb;
                     const float sig = MODE == kModeDog && level > un.lb ? tbl.lv[level - 1].sigma_f32 : 0.f;
                     const int out_plane = MODE == kModeLevels ? level : level - 1;
@@ -800,16 +810,14 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                     // as the validity map), so whatever that memory holds is never looked at.
                     const bool want_flags = MODE == kModeDog && a.flags.data != nullptr;
                     const bool may_skip = want_flags && !(a.debug & 512);
-                    const int xbase = un.x0 + 96 - 32 * q;       // first column of the warp's boxes
-                    const uint32_t xi = 31u - (uint32_t)lane;    // this thread's column inside the box
-                    // staging address of element (row j, column xi) of the swizzled 32 x 128-byte box:
-                    // j * 128 + ((xi / 4) ^ (j & 7)) * 16 + (xi & 3) * 4 - the lanes of a store cover all 32 banks
-                    const uint32_t st_col = wbox + ((xi & 3u) << 2), st_chunk = (xi >> 2) << 4;
+                    const int xbox = un.x0 + 96 - 32 * q;        // first row of D^T in this warp's boxes
+                    const int br = 31 - lane;                    // this thread's row inside the box
+                    const bool row_in = xbox + br < a.W;
+                    const uint32_t wbox_row = wbox + (uint32_t)br * 128u, bswz = (uint32_t)(br & 7);
 #pragma unroll
                     for (int c = 0; c < 2; ++c) {
-                        const int ybase = un.y0 + 64 * h + 32 * c;
-                        const int nrows = a.H - ybase;           // rows j < nrows of the box are inside the frame
-                        bool hit0 = false, hit1 = false, hit2 = false, hit3 = false;     // per 8-row block
+                        const int ybase = un.y0 + 64 * h + 32 * c;      // first column of D^T in this box
+                        bool hit = false;
                         uint32_t ra[32], rb[32];
                         tmem_ld32_pair(acc + 32 * c, acc + kAccCols + 32 * c, ra, rb);
                         if (c == 1) {
@@ -824,40 +832,28 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                                 const float d = __fmul_rn(__fsub_rn(prev[32 * c + j], v), sig);
                                 ra[j] = __float_as_uint(d);
                                 prev[32 * c + j] = v;
-                                if (j < 8) hit0 = hit0 || d > a.thr;
-                                else if (j < 16) hit1 = hit1 || d > a.thr;
-                                else if (j < 24) hit2 = hit2 || d > a.thr;
-                                else hit3 = hit3 || d > a.thr;
+                                hit = hit || d > a.thr;
                             } else {
                                 ra[j] = __float_as_uint(v);
                             }
                         }
                         rc.lap(2);
+                        if (MODE == kModeDog) flush_seeds();
                         if (emit && !(a.debug & 2)) {            // uniform per level
                             bool store = true;
-                            uint32_t hit_any = 0u;
+                            uint32_t hit_rows = 0u;          // bit r: row r of the box has a value above the threshold
                             if (want_flags) {
-                                // this warp's 32 rows x 32 columns: which of its four 8-row blocks hold a value
-                                // above the threshold (rows below the frame do not count)?
-                                if (nrows < 32) {                // bottom edge of the frame: rare
-                                    hit0 = hit1 = hit2 = hit3 = false;
-#pragma unroll
-                                    for (int j = 0; j < 32; ++j) {
-                                        const bool t = j < nrows && __uint_as_float(ra[j]) > a.thr;
-                                        if (j < 8) hit0 = hit0 || t;
-                                        else if (j < 16) hit1 = hit1 || t;
-                                        else if (j < 24) hit2 = hit2 || t;
-                                        else hit3 = hit3 || t;
-                                    }
-                                }
-                                const uint32_t word = (__any_sync(0xffffffffu, hit0) ? 1u : 0u) | (__any_sync(0xffffffffu, hit1) ? 0x100u : 0u) |
-                                                      (__any_sync(0xffffffffu, hit2) ? 0x10000u : 0u) | (__any_sync(0xffffffffu, hit3) ? 0x1000000u : 0u);
-                                hit_any = word;
-                                if (lane == 0)
+                                // this warp's 32 rows x 32 columns of D^T: which of its four 8-row blocks hold a value
+                                // above the threshold (rows right of the frame do not count)?
+                                const uint32_t m = hit_rows = __brev(__ballot_sync(0xffffffffu, hit && row_in));
+                                if (lane == 0) {
+                                    const uint32_t word = ((m & 0xffu) ? 1u : 0u) | ((m & 0xff00u) ? 0x100u : 0u) |
+                                                          ((m & 0xff0000u) ? 0x10000u : 0u) | ((m & 0xff000000u) ? 0x1000000u : 0u);
                                     *reinterpret_cast<uint32_t *>(a.flags.data +
-                                        ((int64_t)out_plane * a.flags.col_blocks + ((un.x0 >> 5) + 3 - q)) * a.flags.row_blocks +
-                                        ((un.y0 >> 3) + 8 * h + 4 * c)) = word;
-                                if (may_skip) store = word != 0u;
+                                        ((int64_t)out_plane * a.flags.col_blocks + ((un.y0 >> 5) + 2 * h + c)) * a.flags.row_blocks +
+                                        (xbox >> 3)) = word;
+                                }
+                                if (may_skip) store = m != 0u;
                             }
                             if (store) {
                                 // This warp's own 32 x 32 box (4 KB, swizzled like a 128-row box): no barrier with
@@ -866,26 +862,26 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                                 if (lane == 0) bulk_wait_read();     // the warp's previous store has read the box
                                 __syncwarp();
 #pragma unroll
-                                for (int j = 0; j < 32; ++j)
-                                    st_shared_b32(st_col + (uint32_t)(j * 128) + (st_chunk ^ (uint32_t)((j & 7) << 4)), ra[j]);
+                                for (int k = 0; k < 8; ++k)
+                                    st_shared_v4(wbox_row + (((uint32_t)k ^ bswz) << 4), ra[4 * k], ra[4 * k + 1], ra[4 * k + 2], ra[4 * k + 3]);
                                 fence_proxy_async_smem();
                                 __syncwarp();
                                 if (lane == 0 && !(a.debug & 32)) {
-                                    tma_store_2d(&map_out, xbase, out_plane * a.Hp + ybase, wbox);
+                                    tma_store_2d(&map_out, ybase, out_plane * a.Wp + xbox, wbox);
                                     bulk_commit();
                                 }
                             }
-                            if (a.flags.seeds != nullptr && hit_any != 0u) {      // uniform per warp; after the store: the box is read meanwhile
+                            if (a.flags.seeds != nullptr && hit_rows != 0u && !(a.debug & 1024)) {      // uniform per warp; after the store: the box is read meanwhile
                                 // Seeds: values above the threshold that no in-slice neighbour KNOWN HERE exceeds
-                                // (same column: this thread's other rows of the chunk; columns left / right: the
+                                // (same row of D^T: this thread's other columns of the chunk; rows above / below: the
                                 // adjacent lanes; everything else, and everything outside the frame, counts as
-                                // -inf).  A lane without a neighbour lane gets its own column maximum back from the
-                                // shuffle, which a column maximum passes by construction.
-                                const int x = xbase + (int)xi;
-                                if (nrows < 32 || x >= a.W) {                       // frame edge: rare
+                                // -inf).  A lane without a neighbour lane gets its own row maximum back from the
+                                // shuffle, which a row maximum passes by construction.
+                                const int nvalid = row_in ? a.H - ybase : 0;         // elements j < nvalid are inside
+                                if (nvalid < 32) {                                    // frame edge: rare
 #pragma unroll
                                     for (int j = 0; j < 32; ++j)
-                                        if (j >= nrows || x >= a.W) ra[j] = 0xff800000u;   // -inf
+                                        if (j >= nvalid) ra[j] = 0xff800000u;        // -inf
                                 }
                                 uint32_t seedmask = 0u;
 #pragma unroll
@@ -898,12 +894,13 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                                     const float dn = __shfl_down_sync(0xffffffffu, mm, 1);
                                     if (e > a.thr && e >= side && e >= up && e >= dn) seedmask |= 1u << j;
                                 }
-                                if (seedmask != 0u) {
-                                    int at = atomicAdd(a.flags.n_seeds, __popc(seedmask));
-                                    const unsigned long long key = ((unsigned long long)out_plane << 48) | (unsigned long long)x;
-                                    for (; seedmask != 0u; seedmask &= seedmask - 1u, ++at)
-                                        if (at < a.flags.seed_cap)
-                                            a.flags.seeds[at] = key | ((unsigned long long)(ybase + __ffs(seedmask) - 1) << 24);
+                                if (seedmask != 0u && !(a.debug & 2048)) {
+                                    // the list index comes back from L2 ~1 us later: the entries are written after the
+                                    // next chunk's accumulator load and arithmetic (flush_seeds above)
+                                    p_at = atomicAdd(a.flags.n_seeds, __popc(seedmask));
+                                    p_mask = seedmask;
+                                    p_key = ((unsigned long long)out_plane << 48) | ((unsigned long long)(xbox + br) << 24) |
+                                            (unsigned long long)ybase;
                                 }
                             }
                         }
@@ -912,6 +909,7 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                 }
             }
         }
+        if (MODE == kModeDog) flush_seeds();
         if (kRows ? store_leader : lane == 0) bulk_wait_all();
         rc.lap(1);
         rc.flush(a.prof, 8);
@@ -1281,7 +1279,7 @@ cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d
     return cudaGetLastError();
 }
 
-// pass 2: R planes -> DoG slices [L - 1][Hp][Wp] (levels = true: the levels themselves, [L][Hp][Wp])
+// pass 2: R planes -> transposed DoG slices D^T [L - 1][Wp][Hp] (levels = true: the levels themselves, [L][Wp][Hp])
 cudaError_t launch_col_pass_umma(const ConvGeometry &g, const void *d_r, float *d_out, const LevelTable &tbl,
                                  const ToeplitzTable &ttab, const float *d_toep, cudaStream_t st,
                                  const uint32_t *d_max_bits, bool levels, const int *d_sched, int sched_slots,
@@ -1306,9 +1304,9 @@ cudaError_t launch_col_pass_umma(const ConvGeometry &g, const void *d_r, float *
         if (!encode_map(&map_in, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, d_r, dims, strides, box))
             return cudaErrorInvalidValue;
     }
-    {   // output planes {W valid columns, rows of all planes}; box = 32 rows x 32 floats (one per drain warp)
-        const cuuint64_t dims[2] = {(cuuint64_t)g.W, (cuuint64_t)g.L * g.Hp};
-        const cuuint64_t strides[1] = {(cuuint64_t)g.Wp * 4};
+    {   // transposed output planes D^T {H valid columns (y), rows x of all planes}; box = 32 rows x 32 floats (one per drain warp)
+        const cuuint64_t dims[2] = {(cuuint64_t)g.H, (cuuint64_t)g.L * g.Wp};
+        const cuuint64_t strides[1] = {(cuuint64_t)g.Hp * 4};
         const cuuint32_t box[2] = {32, 32};
         if (!encode_map(&map_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d_out, dims, strides, box))
             return cudaErrorInvalidValue;
