@@ -810,6 +810,8 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                     // as the validity map), so whatever that memory holds is never looked at.
                     const bool want_flags = MODE == kModeDog && a.flags.data != nullptr;
                     const bool may_skip = want_flags && !(a.debug & 512);
+                    // the float after the threshold: e > thr  <=>  e >= thr_next (thr is not NaN; +inf never gets here)
+                    const float thr_next = __uint_as_float(a.thr == 0.f ? 1u : a.thr > 0.f ? __float_as_uint(a.thr) + 1u : __float_as_uint(a.thr) - 1u);
                     const int xbox = un.x0 + 96 - 32 * q;        // first row of D^T in this warp's boxes
                     const int br = 31 - lane;                    // this thread's row inside the box
                     const bool row_in = xbox + br < a.W;
@@ -883,16 +885,19 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                                     for (int j = 0; j < 32; ++j)
                                         if (j >= nvalid) ra[j] = 0xff800000u;        // -inf
                                 }
+                                // e > thr and e >= its neighbours  <=>  e >= max(neighbours, the float after thr):
+                                // three 3-input maxima, two shuffles and one comparison per element
                                 uint32_t seedmask = 0u;
 #pragma unroll
                                 for (int j = 0; j < 32; ++j) {
                                     const float e = __uint_as_float(ra[j]);
-                                    const float side = fmaxf(j > 0 ? __uint_as_float(ra[j - 1]) : -INFINITY,
-                                                             j < 31 ? __uint_as_float(ra[j + 1]) : -INFINITY);
-                                    const float mm = fmaxf(side, e);
+                                    const float l = j > 0 ? __uint_as_float(ra[j - 1]) : -INFINITY;
+                                    const float r = j < 31 ? __uint_as_float(ra[j + 1]) : -INFINITY;
+                                    const float mm = fmaxf(fmaxf(l, r), e);
                                     const float up = __shfl_up_sync(0xffffffffu, mm, 1);
                                     const float dn = __shfl_down_sync(0xffffffffu, mm, 1);
-                                    if (e > a.thr && e >= side && e >= up && e >= dn) seedmask |= 1u << j;
+                                    const float t = fmaxf(fmaxf(up, dn), fmaxf(fmaxf(l, r), thr_next));
+                                    if (e >= t) seedmask |= 1u << j;
                                 }
                                 if (seedmask != 0u && !(a.debug & 2048)) {
                                     // the list index comes back from L2 ~1 us later: the entries are written after the
