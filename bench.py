@@ -372,11 +372,11 @@ def run_ours(args):
         tensor_engine = eng.plan.conv_engine >= 1
         fp16_engine = eng.plan.conv_engine == 2
         if tensor_engine:
-            # tcgen05 Toeplitz GEMM: per 128 x 128 tile a level spends (128 + 2 rpad) / 16 k-steps of three
-            # kind::f16 MMAs (hi*hi, hi*lo, lo*hi; M = 128, K = 16).  The column pass trims every MMA to the
-            # band it can reach (k-step j feeds outputs [16 j - 2 rpad, 16 j + 15]: N = 16 .. 128) and
-            # computes the first level of every group but the first twice.  An MMA occupies the tensor pipe
-            # for 64 cycles whatever its N <= 128 (tools/ubench_umma_ss.cu), so flops understate the pipe.
+            # tcgen05 Toeplitz GEMM: per 128 x 128 tile a level spends (128 + 2 rpad) / 16 k-steps of two
+            # kind::f16 MMAs (M = 128, K = 16): [main | small] += T_hi * [X_hi | X_lo] with N = 256 and
+            # small += T_lo * X_hi with N = 128.  The tensor pipe spends 64 cycles per 128 columns of N
+            # (tools/ubench_umma_ss.cu).  The column pass computes the first level of every group but the
+            # first twice.
             rpads = [max(8, (int(r) + 7) // 8 * 8) for r in det.bank.radii]
             tiles = ((H + 127) // 128) * ((W + 127) // 128)
             groups = eng.plan.conv_groups
@@ -386,12 +386,9 @@ def run_ours(args):
             n_mma, mma_flops = 0, 0.0
             for lv in levels:
                 rp2 = 2 * rpads[lv]
-                for j in range((128 + rp2) // 16):
-                    m0 = 16 * j
-                    ns = 0 if j == 0 else (max(0, m0 - rp2) & ~15)
-                    ne = 128 if j == 0 else min(128, m0 + 16)
-                    n_mma += 3
-                    mma_flops += 3 * 2.0 * 128 * (ne - ns) * 16
+                n_k = (128 + rp2) // 16
+                n_mma += 2 * n_k
+                mma_flops += n_k * 2.0 * 128 * (256 + 128) * 16
             n_mma *= tiles
             mma_flops *= tiles
             try:
@@ -401,7 +398,7 @@ def run_ours(args):
             sm_hz = 1e6 * ((clocks or {}).get("sm_mhz") or 1965.0)
             engine_roof = {
                 "note": "tcgen05 kind::f16 Toeplitz GEMM, float32 accuracy from a hi/lo split of both operands "
-                        "(3 MMAs per k-step); see DESIGN.md 3a for what bounds it",
+                        "(2 MMAs per k-step: N = 256 and N = 128); see DESIGN.md 3a for what bounds it",
                 "useful_flops_per_launch": col_flops,
                 "useful_tflops": col_flops / (col_ms_iso * 1e-3) / 1e12,
                 "mma_instructions_per_launch": n_mma,
@@ -410,7 +407,7 @@ def run_ours(args):
                 "mma_peak_tflops": f16_peak,
                 "mma_peak_source": "MEASURED_PEAKS.json bf16_tflops (kind::f16 rate)",
                 "frac_of_mma_peak": mma_flops / (col_ms_iso * 1e-3) / 1e12 / f16_peak,
-                "tensor_pipe_busy_estimate": n_mma * 64.0 / 148.0 / (col_ms_iso * 1e-3 * sm_hz),
+                "tensor_pipe_busy_estimate": n_mma * 96.0 / 148.0 / (col_ms_iso * 1e-3 * sm_hz),
                 "level_groups": groups,
             }
             kernel_name = ("umma_pass_kernel<kModeDog> (tcgen05 Toeplitz-GEMM column pass + fused DoG + in-slice part of "

@@ -32,7 +32,7 @@ NVCC_FLAGS = [
 
 
 # experiment knobs of the tensor-core passes (compile-time): DOGBLOB_UMMA_ISSUERS, DOGBLOB_UMMA_STAGEK
-for _k in ("DOGBLOB_UMMA_ISSUERS", "DOGBLOB_UMMA_STAGEK", "DOGBLOB_UMMA_DRAIN_GROUPS", "DOGBLOB_UMMA_F16", "DOGBLOB_UMMA_ROWS1", "DOGBLOB_UMMA_TOEP1", "DOGBLOB_UMMA_TOEP2", "DOGBLOB_UMMA_STAGING1", "DOGBLOB_UMMA_BACKOFF", "DOGBLOB_UMMA_ORDER1"):
+for _k in ("DOGBLOB_UMMA_ISSUERS", "DOGBLOB_UMMA_STAGEK", "DOGBLOB_UMMA_DRAIN_GROUPS", "DOGBLOB_UMMA_F16", "DOGBLOB_UMMA_ROWS1", "DOGBLOB_UMMA_TOEP1", "DOGBLOB_UMMA_TOEP2", "DOGBLOB_UMMA_STAGING1", "DOGBLOB_UMMA_BACKOFF"):
     if os.environ.get(_k):
         NVCC_FLAGS.append(f"-D{_k}={os.environ[_k]}")
 

@@ -2,15 +2,21 @@
 //
 // Same results (within float32 rounding) as scale_space.cu (reference: convolve.py:63-218,
 // detector.py:117-126), but each banded 1-D correlation is issued as a Toeplitz GEMM with BOTH
-// operands in shared memory, brought there by TMA, and nothing is transposed anywhere:
+// operands in shared memory, brought there by TMA, and no operand is transposed anywhere:
 //
 //   pass 1 (along y, the strided axis)      D1[y_out][x] = sum_k  T[y_out][k] * X[k][x]
 //       A = Toeplitz window (K-major, no swizzle)     B = image rows, MN-major, SWIZZLE_128B
-//   pass 2 (along x, the contiguous axis)   D2[y][x_out] = sum_k  R[y][k] * T[x_out][k]
-//       A = pass-1 rows, K-major, SWIZZLE_128B        B = Toeplitz window (K-major, no swizzle)
+//   pass 2 (along x, the contiguous axis)   D2^T[x_out][y] = sum_k  T[x_out][k] * R[y][k]
+//       A = Toeplitz window (K-major, no swizzle)     B = pass-1 rows, K-major, SWIZZLE_128B
+//   Both passes issue the SAME two instructions per k-step (the stage's hi and lo planes are the two N halves
+//   of one B operand, the small accumulator sits right behind the main one in TMEM):
+//       [main | small] += T_hi * [X_hi | X_lo]   (N = 256)        small += T_lo * X_hi   (N = 128)
+//   Pass 2's accumulator therefore holds the TRANSPOSED tile (TMEM lane = output column x, accumulator
+//   column = row y) and the slices are written transposed, D^T[slice][x][y] - the orientation the FP32
+//   engine writes too, which the extrema kernels take as a flag.
 //
 //   T[n][k] = w[k - n] (0 <= k - n <= 2 rpad), tiles of 128 x 128 outputs, K = 128 + 2 rpad inputs
-//   along the convolved axis, 16 per tcgen05.mma.kind::f16 (M = 128, N <= 128).
+//   along the convolved axis, 16 per tcgen05.mma.kind::f16 (M = 128).
 //
 // float32 accuracy from fp16 operands: data and taps are split x = hi + lo, hi = fp16(x),
 // lo = fp16(x - hi) (11 + 11 significand bits; exact power-of-two scales keep both in range: the
@@ -30,19 +36,19 @@
 // half of row n' + 8 and ONE 16-byte chunk per row, C[r][e] = w[r + e - 127], serves every k-step
 // (LBO = SBO = 128: overlapping core matrices; step j reads the window that starts at row 16 j).
 // Half the shared memory and half the copy of a [row][16 taps] array.  The drains undo the
-// reversal for free (pass 1: TMEM lane m' is output row 127 - m'; pass 2: accumulator column c
-// is output column 127 - c, a register renaming).
+// reversal for free (TMEM lane m' is output row 127 - m' of the tile in pass 1, output column
+// 127 - m' = row of the transposed tile in pass 2: an address).
 //
 // One persistent CTA per SM, 384 threads:
 //   warp 0      issuer     ONE elected thread runs the whole loop (its descriptor arithmetic lives
-//                          in uniform registers): 3 MMAs per k-step, tcgen05.commit frees the data
+//                          in uniform registers): 2 MMAs per k-step, tcgen05.commit frees the data
 //                          stage / the Toeplitz buffer / publishes the accumulator pair.  A commit
 //                          costs the issuing thread ~250 cycles during which the tensor pipe runs
 //                          dry (tools/ubench_umma_commit.cu), hence stages of 4 k-steps
 //   warp 1      loader     one TMA box per stage (pass 1: 64 input rows x 128 x, hi | lo = 32 KB;
 //                          pass 2: 128 rows x 64 k, hi | lo = 32 KB)
 //   warp 2      Toeplitz   the level's prebuilt compact arrays (hi | lo), bulk copies into a ring
-//                          of 2 buffers (pass 2 leaves out the 112 rows its trimmed band never reads)
+//                          of 2 buffers
 //   warps 4..11 drain      tcgen05.ld of the accumulator pair (lane = output row, 64 columns per
 //                          thread), scales, pass 1: hi/lo split -> swizzled staging (two boxes per
 //                          column half, alternating: one barrier per round) -> TMA store, and for
@@ -50,7 +56,8 @@
 //                          TMA store into the halo columns (no negative store coordinates: a
 //                          partly outside box is illegal on stores; ragged widths fall back to
 //                          scalar stores); pass 2: DoG against the previous level kept in
-//                          REGISTERS, staging -> TMA store of the float32 slice
+//                          REGISTERS, per-warp staging box -> TMA store into the transposed float32
+//                          slice (boxes without a value above the threshold are not stored), seed test
 // TMEM: two buffers of {main, small} 128 x 128 float32 accumulators (512 columns), so the drain of
 // one level overlaps the MMAs of the next.
 // Units: pass 1 = (tile, level), longest level first, round robin; pass 2 = (tile, level group) on
@@ -92,9 +99,6 @@ constexpr int kStagingForce1 = DOGBLOB_UMMA_STAGING1;
 __host__ __device__ constexpr int staging_bytes1(int bufs) { return 32768 * bufs; }
 constexpr int kStagingBytes2 = 32768;     // pass 2 drain staging: one 4 KB box (32 rows x 32 floats) per drain warp
 constexpr int kMaxStages = 8;
-#ifndef DOGBLOB_UMMA_ORDER1
-#define DOGBLOB_UMMA_ORDER1 1      // pass 1: narrow MMAs of a stage first, wide ones last (0: interleaved)
-#endif
 #ifndef DOGBLOB_UMMA_BACKOFF
 #define DOGBLOB_UMMA_BACKOFF 0
 #endif
@@ -234,73 +238,8 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t cols) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols)
                  : "memory");
 }
-// The three MMAs of one k-step in ONE statement (the whole warp executes it, one elected lane
-// issues; the operands reach the uniform registers once):
-//     main  (+)= A_hi * B_hi        small (+)= A_hi * B_lo        small += A_lo * B_hi
-// `acc` = 0 on the first k-step of a level: the first two MMAs overwrite their accumulators.
-__device__ __forceinline__ void umma_f16_triple_ss(uint32_t d_main, uint32_t d_small, uint32_t a_hi,
-                                                   uint32_t a_lo, uint32_t b_hi, uint32_t b_lo,
-                                                   uint32_t a_upper, uint32_t b_upper, uint32_t idesc,
-                                                   uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p, q, e;\n\t.reg .b64 a0, a1, b0, b1;\n\t"
-        "setp.ne.b32 p, %9, 0;\n\t"
-        "setp.eq.b32 q, 0, 0;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "mov.b64 a0, {%2, %6};\n\t"
-        "mov.b64 a1, {%3, %6};\n\t"
-        "mov.b64 b0, {%4, %7};\n\t"
-        "mov.b64 b1, {%5, %7};\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a0, b0, %8, p;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%1], a0, b1, %8, p;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%1], a1, b0, %8, q;\n\t}"
-        ::"r"(d_main), "r"(d_small), "r"(a_hi), "r"(a_lo), "r"(b_hi), "r"(b_lo), "r"(a_upper),
-          "r"(b_upper), "r"(idesc), "r"(acc)
-        : "memory");
-}
-// single-thread forms (the caller is the one elected thread of the issuer warp)
-__device__ __forceinline__ void umma_f16_triple_ss_1t(uint32_t d_main, uint32_t d_small, uint32_t a_hi,
-                                                      uint32_t a_lo, uint32_t b_hi, uint32_t b_lo,
-                                                      uint32_t a_upper, uint32_t b_upper, uint32_t idesc,
-                                                      uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p, q;\n\t.reg .b64 a0, a1, b0, b1;\n\t"
-        "setp.ne.b32 p, %9, 0;\n\t"
-        "setp.eq.b32 q, 0, 0;\n\t"
-        "mov.b64 a0, {%2, %6};\n\t"
-        "mov.b64 a1, {%3, %6};\n\t"
-        "mov.b64 b0, {%4, %7};\n\t"
-        "mov.b64 b1, {%5, %7};\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], a0, b0, %8, p;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%1], a0, b1, %8, p;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%1], a1, b0, %8, q;\n\t}"
-        ::"r"(d_main), "r"(d_small), "r"(a_hi), "r"(a_lo), "r"(b_hi), "r"(b_lo), "r"(a_upper),
-          "r"(b_upper), "r"(idesc), "r"(acc)
-        : "memory");
-}
-// Pass 1: the hi and lo planes of a data stage are consecutive N blocks of ONE MN-major operand, and
-// the small accumulator sits right behind the main one, so  main (+)= A_hi * B_hi  and
-// small (+)= A_hi * B_lo  are a single MMA with N = 256 (the Toeplitz window is read once for both:
-// 20 instead of 24 KB of operand reads per k-step, two instructions instead of three); then
-// small += A_lo * B_hi  (N = 128).
-__device__ __forceinline__ void umma_f16_wide_pair_ss_1t(uint32_t d_main, uint32_t a_hi, uint32_t a_lo, uint32_t b_hi,
-                                                         uint32_t a_upper, uint32_t b_upper, uint32_t idesc256,
-                                                         uint32_t idesc128, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p, q;\n\t.reg .b64 a0, a1, b0;\n\t.reg .b32 ds;\n\t"
-        "setp.ne.b32 p, %8, 0;\n\t"
-        "setp.eq.b32 q, 0, 0;\n\t"
-        "add.u32 ds, %0, 128;\n\t"
-        "mov.b64 a0, {%1, %4};\n\t"
-        "mov.b64 a1, {%2, %4};\n\t"
-        "mov.b64 b0, {%3, %5};\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], a0, b0, %6, p;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [ds], a1, b0, %7, q;\n\t}"
-        ::"r"(d_main), "r"(a_hi), "r"(a_lo), "r"(b_hi), "r"(a_upper), "r"(b_upper), "r"(idesc256), "r"(idesc128),
-          "r"(acc)
-        : "memory");
-}
-// one MMA: D (+)= A * B with the descriptor words split like above
+// one MMA: D (+)= A * B; the descriptors arrive as their low words plus the constant upper words
+// (single-thread form: the caller is the one elected thread of the issuer warp)
 __device__ __forceinline__ void umma_f16_ss_1t(uint32_t d, uint32_t a_lo32, uint32_t b_lo32, uint32_t a_upper,
                                                uint32_t b_upper, uint32_t idesc, uint32_t acc) {
     asm volatile(
@@ -508,9 +447,8 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
 
     if (warp == 0) {
         // ================= issuer (ONE elected thread runs the whole loop) =================
-        // Every MMA is M = 128 x K = 16; the tensor pipe spends 64 cycles on it for any N <= 128
-        // (measured, tools/ubench_umma_ss.cu), so pass 2's band trimming (k-step m0 only feeds
-        // outputs n in [m0 - 2 rpad, m0 + 15]) saves shared-memory reads, not pipe time.
+        // Every MMA is M = 128 x K = 16; the tensor pipe spends 64 cycles on it per 128 columns of N
+        // (measured, tools/ubench_umma_ss.cu).
         uint32_t lvl_it = 0, sl = 0, sl_par = 0;            // data stage slot and its phase parity
         uint32_t tb = 0, tb_par = 0;                        // Toeplitz buffer and its phase parity
         RoleClock rc(a.prof != nullptr);
@@ -1009,8 +947,7 @@ frame_max_kernel(const float *__restrict__ img, int64_t n4, uint32_t *__restrict
 }
 
 int toeplitz_rows(int rpad) { return kUT + 2 * rpad - 16 + kUT + 8; }
-// one Toeplitz buffer in shared memory: pass 2 (Toeplitz = B operand, band trimmed) never reads the
-// last 112 rows of the arrays and does not copy them
+// one Toeplitz buffer in shared memory (hi + lo arrays of the widest level)
 int toeplitz_buffer_bytes(int max_rpad, bool rows_pass) {
     (void)rows_pass;
     return (toeplitz_rows(max_rpad) * 32 + 127) / 128 * 128;
