@@ -806,7 +806,7 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                                     st_shared_v4(wbox_row + (((uint32_t)k ^ bswz) << 4), ra[4 * k], ra[4 * k + 1], ra[4 * k + 2], ra[4 * k + 3]);
                                 fence_proxy_async_smem();
                                 __syncwarp();
-                                if (lane == 0 && !(a.debug & 32)) {
+                                if (lane == 0 && !(a.debug & (32 | 4096))) {
                                     tma_store_2d(&map_out, ybase, out_plane * a.Wp + xbox, wbox);
                                     bulk_commit();
                                 }
@@ -1048,7 +1048,9 @@ cudaError_t launch_umma(UmmaArgs b, const LevelTable &tbl, const ToeplitzTable &
     static unsigned long long *d_prof = nullptr;
     const bool prof = umma_prof_enabled();
     // DOGBLOB_UMMA_DEBUG (timing experiments, results are garbage): 1 no data TMA, 2 drain without
-    // staging / stores, 8 no MMAs, 16 no Toeplitz copies, 32 no TMA stores, 64 no halo column stores
+    // staging / stores, 8 no MMAs, 16 no Toeplitz copies, 32 no TMA stores, 64 no halo column stores,
+    // 512 every box stored (no skipping), 1024 no seed test, 2048 seed test without the list appends,
+    // 4096 column pass stages its boxes but does not issue their TMA stores
     b.debug = umma_debug_mask();
     if (prof) {
         if (!d_prof) cudaMalloc(&d_prof, 256 * sizeof(unsigned long long));
