@@ -42,6 +42,16 @@ if (G / "stress_engines.txt").exists():
         f"# Round {tag[1:]} - randomised engine cross-check (tools/stress_engines.py 120 5): random ragged shapes, ladders, "
         "thresholds; tensor-core DoG slices vs the FP32 engine's, detector vs stage functions on the same stack, frame "
         "sequences through one slot (stale slice memory)\n\n```\n" + "\n".join(txt[:12] + ["..."] + txt[-3:]) + "\n```\n")
+    extra = [(n, c) for n, c in (("stress_400.txt", "python tools/stress_engines.py 400 77"),
+                                 ("stress_large.txt", "python tools/stress_engines.py 60 78 large        # frames up to 2600 px, sigma up to 60"))
+             if (G / n).exists()]
+    if extra:
+        with open(P / f"{tag}_stress_engines.md", "a") as f:
+            f.write("\nExtended runs with the final build (FAIL lines: "
+                    + str(sum((G / n).read_text().count("FAIL") for n, _ in extra)) + "):\n\n```\n")
+            for n, c in extra:
+                f.write(c + "\n" + (G / n).read_text().splitlines()[-1] + "\n")
+            f.write("```\n")
 
 rows = list(csv.reader(open(G / "launches_one_frame.csv")))
 h = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
