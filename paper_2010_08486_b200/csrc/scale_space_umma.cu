@@ -372,12 +372,10 @@ struct RoleClock {
 // level groups that OVERLAP by one level (the first level of group g + 1 is computed by group g
 // too), so every DoG slice has both its levels inside one unit and nothing is parked in memory.
 struct Unit { int x0, y0, lb, le; };
-__device__ __forceinline__ Unit decode_unit(int u, const UmmaArgs &a, const LevelTable &tbl, int mode) {
+__device__ __forceinline__ Unit unit_of(int tx, int ty, int g, const UmmaArgs &a, const LevelTable &tbl, int mode) {
     Unit r;
-    r.x0 = (u % a.tiles_x) * kUT;
-    const int t = u / a.tiles_x;
-    r.y0 = (t % a.tiles_y) * kUT;
-    const int g = t / a.tiles_y;
+    r.x0 = tx * kUT;
+    r.y0 = ty * kUT;
     if (a.by_order) {
         r.lb = tbl.order[g];
         r.le = r.lb + 1;
@@ -387,6 +385,26 @@ __device__ __forceinline__ Unit decode_unit(int u, const UmmaArgs &a, const Leve
     }
     return r;
 }
+__device__ __forceinline__ Unit decode_unit(int u, const UmmaArgs &a, const LevelTable &tbl, int mode) {
+    const int t = u / a.tiles_x;
+    return unit_of(u % a.tiles_x, t % a.tiles_y, t / a.tiles_y, a, tbl, mode);
+}
+// Round robin without a schedule (pass 1: a unit per level): unit blockIdx.x + i * gridDim.x as (tile x, tile y,
+// group), advanced by carries instead of three integer divisions per unit on the issuing thread's critical path
+struct UnitWalk {
+    int tx, ty, g, dx, dy, dg;
+    __device__ __forceinline__ explicit UnitWalk(const UmmaArgs &a) {
+        int u = blockIdx.x;
+        tx = u % a.tiles_x; u /= a.tiles_x; ty = u % a.tiles_y; g = u / a.tiles_y;
+        u = gridDim.x;
+        dx = u % a.tiles_x; u /= a.tiles_x; dy = u % a.tiles_y; dg = u / a.tiles_y;
+    }
+    __device__ __forceinline__ void advance(const UmmaArgs &a) {
+        tx += dx; ty += dy; g += dg;
+        if (tx >= a.tiles_x) { tx -= a.tiles_x; ++ty; }
+        if (ty >= a.tiles_y) { ty -= a.tiles_y; ++g; }      // ty < 2 tiles_y: one carry
+    }
+};
 
 struct SharedCtl {
     unsigned long long data_full[kMaxStages], data_empty[kMaxStages];
@@ -456,11 +474,12 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
             atomicMax(a.prof + 17, globaltimer_ns());      // last CTA reaches its issuer loop
             atomicMin(a.prof + 20, globaltimer_ns());      // first CTA reaches it
         }
+        UnitWalk walk(a);
         if (elect_one())
-        for (int ui = blockIdx.x; ui < a.n_sched; ui += gridDim.x) {
+        for (int ui = blockIdx.x; ui < a.n_sched; ui += gridDim.x, walk.advance(a)) {
             const int u = a.sched ? __ldg(a.sched + ui) : ui;
             if (u < 0) continue;
-            const Unit un = decode_unit(u, a, tbl, MODE);
+            const Unit un = a.sched ? decode_unit(u, a, tbl, MODE) : unit_of(walk.tx, walk.ty, walk.g, a, tbl, MODE);
             for (int level = un.lb; level < un.le; ++level, ++lvl_it) {
                 const int rpad2 = 2 * tbl.lv[level].rpad;
                 const int Kp = kUT + rpad2;
