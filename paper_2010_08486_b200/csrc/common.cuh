@@ -152,8 +152,8 @@ cudaError_t launch_col_levels_pass(const ConvGeometry &g, const float *d_rows_t,
                                    cudaStream_t st);
 cudaError_t launch_edge_dog(const ConvGeometry &g, const float *d_edge, float *d_dog_t,
                             const LevelTable &tbl, cudaStream_t st);
-// which blocks of 8 rows x 32 columns of the DoG slices hold a value above the detection threshold;
-// the tensor-core column pass only STORES the 128 x 32 boxes that contain such a block, so the flags
+// which blocks of 8 rows x 32 columns of the (x-major) DoG slices hold a value above the detection threshold;
+// the tensor-core column pass only STORES the 32 x 32 boxes that contain such a block, so the flags
 // are also the validity map of the slice memory (everything else reads as -inf in the extrema kernel)
 struct HitFlags {
     unsigned char *data = nullptr;       // [slice][col_blocks][row_blocks] (row blocks contiguous)
@@ -161,7 +161,8 @@ struct HitFlags {
     // Seeds (optional): the column pass also tests every value above the threshold against the in-slice
     // neighbours it has in registers (same row: the thread's own columns; rows above / below: the
     // neighbouring lanes) and appends the survivors - a superset of the in-slice local maxima, some ten
-    // thousand voxels per frame - to this list as slice << 48 | row << 24 | column.  The extrema kernel
+    // thousand voxels per frame - to this list as slice << 48 | row << 24 | column of the x-major slice
+    // (row = x, column = y).  The extrema kernel
     // then only visits the seeds (nms_seed_kernel) instead of walking the slices.  *n_seeds counts past
     // the capacity: more seeds than seed_cap = the list is incomplete and the strip kernel runs instead.
     unsigned long long *seeds = nullptr;
@@ -194,7 +195,7 @@ int umma_max_words();      // uint32 words behind d_max_bits: the frame's max + 
 cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d_r, const LevelTable &tbl,
                                  const ToeplitzTable &ttab, const float *d_toep, cudaStream_t st,
                                  const uint32_t *d_max_bits, int max_ctas = 0);
-// DoG slices [L - 1][Hp][Wp] in image orientation (levels = true: the L levels themselves)
+// x-major DoG slices D^T [L - 1][Wp][Hp], like the FP32 engine's (levels = true: the L levels themselves)
 cudaError_t launch_col_pass_umma(const ConvGeometry &g, const void *d_r, float *d_out, const LevelTable &tbl,
                                  const ToeplitzTable &ttab, const float *d_toep, cudaStream_t st,
                                  const uint32_t *d_max_bits, bool levels, const int *d_sched, int sched_slots,
