@@ -86,8 +86,8 @@ struct dogblob_plan {
     float *d_sigma_f32 = nullptr;
     // workspace layout (bytes from the workspace base)
     // FP32 engine: rows_t = row-filtered planes (x-major), dog_t = DoG^T planes, edge = parked levels;
-    // tensor engine: rows_t = R planes (fp16 hi | lo), x = X planes, dog_t = DoG planes (image
-    // orientation), no edge planes
+    // tensor engine: rows_t = R planes (fp16 hi | lo), x = X planes, dog_t = DoG^T planes too (x-major),
+    // no edge planes
     size_t off_rows_t = 0, off_x = 0, off_dog_t = 0, off_edge = 0, off_blobspace = 0, off_gate = 0, off_flags = 0, off_seeds = 0, total = 0;
     int seed_cap = 0;               // tensor engine: capacity of the column pass's seed list (0 = no seeds, strip kernel)
 };
