@@ -421,7 +421,8 @@ template <int MODE, int kStagingBufs1>
 __global__ void __launch_bounds__(kThreads, 1)
 umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                  const __grid_constant__ ToeplitzTable ttab, const __grid_constant__ CUtensorMap map_in,
-                 const __grid_constant__ CUtensorMap map_out, const __grid_constant__ CUtensorMap map_aux) {
+                 const __grid_constant__ CUtensorMap map_out, const __grid_constant__ CUtensorMap map_aux,
+                 const __grid_constant__ CUtensorMap map_cut) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     SharedCtl *ctl = reinterpret_cast<SharedCtl *>(smem_raw);
     unsigned char *toep = smem_raw + kCtlBytes;                               // [buffer 2][hi | lo]
@@ -698,7 +699,12 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                     const int right_w = rpad + (a.Wp - a.W);
                     const bool left = xs0 < rpad, right = xs0 + 64 > a.W - right_w && xs0 < a.W;
                     const bool right_tma = right && (a.W & 7) == 0 && xs0 + 64 <= a.W;    // no negative store coordinates
-                    const int n_rounds = (a.debug & 2) ? 0 : ((left || right_tma) && !(a.debug & 64)) ? 4 : 2;
+                    // the half that the frame's right edge cuts (W a multiple of 8, not of 64): its W - xs0 valid columns,
+                    // reversed, are the FIRST halo columns - the reversed row is staged (xs0 + 64 - W) / 8 chunks further
+                    // left and stored through a map that starts at column W and ends after W - xs0 columns
+                    const bool right_cut = right && (a.W & 7) == 0 && xs0 + 64 > a.W && !left;
+                    const int cut_chunks = right_cut ? (xs0 + 64 - a.W) >> 3 : 0;
+                    const int n_rounds = (a.debug & 2) ? 0 : ((left || right_tma || right_cut) && !(a.debug & 64)) ? 4 : 2;
                     for (int rd = 0; rd < n_rounds; ++rd, ++round_it) {      // uniform per half
                         const uint32_t buf = kStagingBufs1 == 2 ? (round_it & 1u) : 0u;
                         const uint32_t dst = stg_row + buf * 16384u;
@@ -717,9 +723,11 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
 #pragma unroll
                             for (int c = 0; c < 8; ++c) {            // chunk c of the reversed row = chunk 7 - c, elements reversed
                                 const uint32_t *w = lo_plane ? lw : hw;
-                                st_shared_v4(dst + (((uint32_t)c ^ swz) << 4),
-                                             __byte_perm(w[4 * (7 - c) + 3], 0, 0x1032), __byte_perm(w[4 * (7 - c) + 2], 0, 0x1032),
-                                             __byte_perm(w[4 * (7 - c) + 1], 0, 0x1032), __byte_perm(w[4 * (7 - c)], 0, 0x1032));
+                                const int at = c - cut_chunks;      // uniform; a cut half drops its first chunks (columns >= W)
+                                if (at >= 0)
+                                    st_shared_v4(dst + (((uint32_t)at ^ swz) << 4),
+                                                 __byte_perm(w[4 * (7 - c) + 3], 0, 0x1032), __byte_perm(w[4 * (7 - c) + 2], 0, 0x1032),
+                                                 __byte_perm(w[4 * (7 - c) + 1], 0, 0x1032), __byte_perm(w[4 * (7 - c)], 0, 0x1032));
                             }
                         }
                         fence_proxy_async_smem();
@@ -734,11 +742,12 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                                 // map_aux starts at the first column right of the frame (column W)
                                 if (left) tma_store_3d(&map_out, a.Ppad - xs0 - 64, yrow, lo_plane, src);
                                 if (right_tma) tma_store_3d(&map_aux, a.W - xs0 - 64, yrow, lo_plane, src);
+                                if (right_cut) tma_store_3d(&map_cut, 0, yrow, lo_plane, src);
                             }
                             bulk_commit();
                         }
                     }
-                    if (right && !right_tma && !(a.debug & (2 | 64))) {
+                    if (right && !right_tma && !right_cut && !(a.debug & (2 | 64))) {
                         // widths that are not a multiple of 8: the right halo element by element
                         __half *rrow = a.r_base + ((int64_t)level * a.Hp + un.y0 + row) * a.r_pitch + a.Ppad;
 #pragma unroll
@@ -1054,7 +1063,7 @@ __global__ void edge_halo_kernel(__half *r, int64_t n_rows, int64_t pitch, int e
 
 template <int MODE>
 cudaError_t launch_umma(UmmaArgs b, const LevelTable &tbl, const ToeplitzTable &ttab, int max_rpad,
-                        const CUtensorMap &map_in, const CUtensorMap &map_out, const CUtensorMap &map_aux,
+                        const CUtensorMap &map_in, const CUtensorMap &map_out, const CUtensorMap &map_aux, const CUtensorMap &map_cut,
                         cudaStream_t st) {
     constexpr bool rows_pass = MODE == kModeRows;
     b.toep_bytes = toeplitz_buffer_bytes(max_rpad, rows_pass);
@@ -1080,9 +1089,9 @@ cudaError_t launch_umma(UmmaArgs b, const LevelTable &tbl, const ToeplitzTable &
     }
     const int ctas = b.n_ctas > 0 ? b.n_ctas : persistent_ctas(b.n_units);
     if (staging_bufs == 2)
-        umma_pass_kernel<MODE, rows_pass ? 2 : 1><<<ctas, kThreads, smem, st>>>(b, tbl, ttab, map_in, map_out, map_aux);
+        umma_pass_kernel<MODE, rows_pass ? 2 : 1><<<ctas, kThreads, smem, st>>>(b, tbl, ttab, map_in, map_out, map_aux, map_cut);
     else
-        umma_pass_kernel<MODE, 1><<<ctas, kThreads, smem, st>>>(b, tbl, ttab, map_in, map_out, map_aux);
+        umma_pass_kernel<MODE, 1><<<ctas, kThreads, smem, st>>>(b, tbl, ttab, map_in, map_out, map_aux, map_cut);
     if (prof) {
         unsigned long long h[256];
         cudaStreamSynchronize(st);
@@ -1205,7 +1214,7 @@ cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d
     a.r_pitch = l.Wq; a.r_plane = (int64_t)g.L * g.Hp * l.Wq;
     a.r_base = reinterpret_cast<__half *>(d_r);
     a.frame_max_bits = d_max_bits; a.toep = d_toep;
-    CUtensorMap map_in, map_out, map_aux;
+    CUtensorMap map_in, map_out, map_aux, map_cut;
     const int xrows = g.H + 2 * l.Py;
     {   // X planes as {64 x, rows, x-block, hi | lo}; box = 32 rows of one 128-column tile, both planes
         const cuuint64_t dims[4] = {64, (cuuint64_t)xrows, (cuuint64_t)(g.Wp / 64), 2};
@@ -1235,7 +1244,16 @@ cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d
                         reinterpret_cast<__half *>(d_r) + l.Ppad + g.W, dims, strides, box))
             return cudaErrorInvalidValue;
     }
-    const cudaError_t err = launch_umma<kModeRows>(a, tbl, ttab, g.max_rpad, map_in, map_out, map_aux, st);
+    map_cut = map_out;
+    if ((g.W & 7) == 0 && (g.W & 63) != 0) {   // the half tile that the right edge cuts: its W % 64 mirrored columns behind the frame
+        const cuuint64_t dims[3] = {(cuuint64_t)(g.W & 63), (cuuint64_t)g.L * g.Hp, 2};
+        const cuuint64_t strides[2] = {(cuuint64_t)l.Wq * 2, (cuuint64_t)a.r_plane * 2};
+        const cuuint32_t box[3] = {64, 128, 1};
+        if (!encode_map(&map_cut, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
+                        reinterpret_cast<__half *>(d_r) + l.Ppad + g.W, dims, strides, box))
+            return cudaErrorInvalidValue;
+    }
+    const cudaError_t err = launch_umma<kModeRows>(a, tbl, ttab, g.max_rpad, map_in, map_out, map_aux, map_cut, st);
     if (err != cudaSuccess || w8 == g.W) return err;
     const int64_t n_rows = 2 * (int64_t)g.L * g.Hp;
     edge_halo_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(a.r_base, n_rows, a.r_pitch, l.Ppad + g.W, w8 - g.W);
@@ -1274,8 +1292,8 @@ cudaError_t launch_col_pass_umma(const ConvGeometry &g, const void *d_r, float *
         if (!encode_map(&map_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d_out, dims, strides, box))
             return cudaErrorInvalidValue;
     }
-    if (levels) return launch_umma<kModeLevels>(a, tbl, ttab, g.max_rpad, map_in, map_out, map_out, st);
-    return launch_umma<kModeDog>(a, tbl, ttab, g.max_rpad, map_in, map_out, map_out, st);
+    if (levels) return launch_umma<kModeLevels>(a, tbl, ttab, g.max_rpad, map_in, map_out, map_out, map_out, st);
+    return launch_umma<kModeDog>(a, tbl, ttab, g.max_rpad, map_in, map_out, map_out, map_out, st);
 }
 
 }  // namespace dogblob

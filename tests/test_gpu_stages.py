@@ -132,13 +132,22 @@ class TestEngines:
         monkeypatch.delenv("DOGBLOB_CONV", raising=False)
         wide = P.Detector(P.DetectionParams(min_sigma=1, max_sigma=30, n_bin=58, preprocess=False))
         narrow = P.Detector(P.DetectionParams(min_sigma=1, max_sigma=10, n_bin=18, preprocess=False))
+        dense = P.Detector(P.DetectionParams(min_sigma=1, max_sigma=6, n_bin=10, preprocess=False))
         try:
+            # measured crossover (tools/engine_crossover.py)
             assert wide.plan_for((1024, 1024)).plan.conv_engine >= 1      # C2: tensor cores
-            assert wide.plan_for((256, 256)).plan.conv_engine == 0        # too few tiles for 148 CTAs
-            assert narrow.plan_for((512, 512)).plan.conv_engine == 0      # C1: FP32 sliding window
+            assert wide.plan_for((256, 256)).plan.conv_engine >= 1        # wide ladder: even on 4 tiles
+            assert wide.plan_for((128, 128)).plan.conv_engine == 0        # a single tile
+            assert wide.plan_for((500, 500)).plan.conv_engine == 0        # width not a multiple of 8, few tiles
+            assert wide.plan_for((900, 900)).plan.conv_engine >= 1        # ... but enough tiles
+            assert narrow.plan_for((512, 512)).plan.conv_engine >= 1      # C1: mean padded radius 31
+            assert narrow.plan_for((128, 128)).plan.conv_engine == 0      # ... a single tile
+            assert dense.plan_for((1024, 1024)).plan.conv_engine == 0     # C5: narrow ladder (mean 21): FP32 sliding window
+            assert dense.plan_for((2048, 2048)).plan.conv_engine >= 1     # ... unless the frame exceeds the L2
         finally:
             wide.close()
             narrow.close()
+            dense.close()
 
     @pytest.mark.parametrize("shape,lo,hi,n", [((384, 512), 2.0, 40.0, 19), ((256, 384), 20.0, 60.0, 2),
                                                ((200, 150), 1.0, 4.0, 3)])

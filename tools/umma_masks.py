@@ -21,6 +21,9 @@ from paper_2010_08486_b200 import detector as D, synth  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"
 masks = [int(x) for x in sys.argv[2:]] or [0]
 frame, kw = synth.config_frame(name), synth.config_params(name)
+if os.environ.get("UMMA_MASKS_SHAPE"):      # HxW: the config's frame cropped / tiled to another shape
+    hh, ww = (int(v) for v in os.environ["UMMA_MASKS_SHAPE"].split("x"))
+    frame = np.ascontiguousarray(np.tile(frame, (hh // frame.shape[0] + 1, ww // frame.shape[1] + 1))[:hh, :ww])
 params = P.DetectionParams(preprocess=False, **kw)
 import dataclasses  # noqa: E402
 # garbage planes under a mask: nothing may be flagged; UMMA_MASKS_THR=<threshold> times the real detection path (mask 0 only)
