@@ -212,6 +212,22 @@ class TestEngines:
             out[eng] = P.convolve_bank(img, bank).levels
         assert np.abs(out["fma"].astype(np.float64) - out["umma"]).max() < 2 * LEVEL_TOL_TENSOR_WIDE
 
+    @pytest.mark.parametrize("width", [200, 456, 840, 1000])
+    def test_right_edge_cuts_a_half_tile(self, monkeypatch, width):
+        """frame widths that are a multiple of 8 but not of 64: the half tile under the right edge mirrors
+        its valid columns through a shifted staging box and a TMA store clipped behind them (row pass);
+        the detector's blob list must not depend on the engine either"""
+        bank = bank_for(1.5, 24.9, 26)
+        img = synth.sensor_noise(synth.droplet_scene(width, 300, 30, (2.0, 30.0), seed=5, allow_overlap=True),
+                                 seed=6).image
+        out = {}
+        for eng in ("fma", "umma"):
+            monkeypatch.setenv("DOGBLOB_CONV", eng)
+            out[eng] = P.convolve_bank(img, bank).levels
+        assert np.abs(out["fma"].astype(np.float64) - out["umma"]).max() < 2 * LEVEL_TOL_TENSOR_WIDE
+        # the last columns of the widest level are where a wrong halo shows first
+        assert np.abs(out["fma"][-1, :, -8:].astype(np.float64) - out["umma"][-1, :, -8:]).max() < 2 * LEVEL_TOL_TENSOR_WIDE
+
     def test_engines_agree(self, monkeypatch):
         bank = bank_for(1.0, 12.0, 11)
         img = synth.sensor_noise(synth.droplet_scene(333, 270, 20, (3.0, 12.0), seed=8, allow_overlap=True),

@@ -2,7 +2,7 @@
 """Where the tensor-core engine starts to beat the FP32 engine: scale-space time of both for a grid of frame sizes and
 ladders (the plan's own choice is marked).  Test tooling only.
 
-    python tools/engine_crossover.py
+    python tools/engine_crossover.py [HxW ...]
 """
 import os
 import sys
@@ -39,7 +39,8 @@ def conv_ms(frame, kw, engine):
 shapes = [(int(a), int(b)) for a, b in (s.split("x") for s in sys.argv[1:])] or [(n, n) for n in (512, 768, 1024, 1536)]
 for Hh, Ww in shapes:
     size = f"{Hh}x{Ww}"
-    frame = synth.sensor_noise(synth.droplet_scene(Hh, Ww, 40, (3.0, min(20.0, Hh / 12, Ww / 12)), seed=3), seed=4).image
+    frame = synth.sensor_noise(synth.droplet_scene(Ww, Hh, 40, (3.0, min(20.0, Hh / 12, Ww / 12)), seed=3), seed=4).image
+    assert frame.shape == (Hh, Ww)
     for max_sigma, n_bin in ((3, 6), (6, 12), (10, 20), (15, 30), (20, 40), (30, 58)):
         kw = dict(min_sigma=1.0, max_sigma=float(max_sigma), n_bin=n_bin)
         f, _, nb = conv_ms(frame, kw, "fma")
