@@ -54,8 +54,10 @@
 //                          column half, alternating: one barrier per round) -> TMA store, and for
 //                          tiles at the frame border the same rows with their columns reversed ->
 //                          TMA store into the halo columns (no negative store coordinates: a
-//                          partly outside box is illegal on stores; ragged widths fall back to
-//                          scalar stores); pass 2: DoG against the previous level kept in
+//                          partly outside box is illegal on stores; the half tile under the right
+//                          edge shifts its reversed row instead; widths that are not a multiple of
+//                          8 get their right halo from edge_halo_kernel); pass 2: DoG against the
+//                          previous level kept in
 //                          REGISTERS, per-warp staging box -> TMA store into the transposed float32
 //                          slice (boxes without a value above the threshold are not stored), seed test
 // TMEM: two buffers of {main, small} 128 x 128 float32 accumulators (512 columns), so the drain of
@@ -747,8 +749,9 @@ umma_pass_kernel(const UmmaArgs a, const __grid_constant__ LevelTable tbl,
                             bulk_commit();
                         }
                     }
-                    if (right && !right_tma && !right_cut && !(a.debug & (2 | 64))) {
-                        // widths that are not a multiple of 8: the right halo element by element
+                    if (right && (a.W & 7) == 0 && !right_tma && !right_cut && !(a.debug & (2 | 64))) {
+                        // a frame narrower than a kernel radius, cut half that also feeds the left halo: element by
+                        // element (widths that are not a multiple of 8: edge_halo_kernel mirrors the right halo)
                         __half *rrow = a.r_base + ((int64_t)level * a.Hp + un.y0 + row) * a.r_pitch + a.Ppad;
 #pragma unroll
                         for (int pl = 0; pl < 2; ++pl) {
@@ -1052,13 +1055,19 @@ int umma_debug_mask() {
     return e ? std::atoi(e) : 0;
 }
 
-// Frame widths that are not a multiple of 8: the halo columns [W, W + n) that share a 16-byte chunk with
-// the frame's last columns, in every row of both planes (column W + i <- column W - 1 - i).
-__global__ void edge_halo_kernel(__half *r, int64_t n_rows, int64_t pitch, int edge, int n) {
-    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// Frame widths that are not a multiple of 8: the reflected halo right of the frame cannot be written with 16-byte
+// chunks (the reflection shifts the columns by an odd distance), so the row pass leaves it out and this kernel
+// mirrors it afterwards: column W + i <- column W - 1 - i for i < rpad(level) + Wp - W, one warp per row of both
+// planes (rows = [hi | lo][level][Hp]).  It also overwrites the columns [W, w8) that the interior stores, clipped at
+// the next 16-byte chunk, filled with pad-region outputs.
+__global__ void __launch_bounds__(256)
+edge_halo_kernel(__half *r, int64_t n_rows, int64_t pitch, int edge, int pad_w, int Hp, int L,
+                 const __grid_constant__ LevelTable tbl) {
+    const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (row >= n_rows) return;
+    const int n = tbl.lv[(int)((row / Hp) % L)].rpad + pad_w;
     __half *p = r + row * pitch + edge;
-    for (int i = 0; i < n; ++i) p[i] = p[-1 - i];
+    for (int i = threadIdx.x & 31; i < n; i += 32) p[i] = p[-1 - i];
 }
 
 template <int MODE>
@@ -1228,7 +1237,7 @@ cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d
         // beyond are clipped.  The clip must not fall INSIDE a chunk: other CTAs write the halo columns next to
         // the frame at the same time, and a partially clipped chunk proved not to be a byte-exact write under
         // that race (tools/stress_engines.py, 725 x 898).  The up to 7 halo columns [W, w8) this leaves wrong
-        // are rewritten by edge_halo_kernel below.
+        // are rewritten by edge_halo_kernel below, together with the rest of the right halo.
         const cuuint64_t dims[3] = {(cuuint64_t)(l.Ppad + w8), (cuuint64_t)g.L * g.Hp, 2};
         const cuuint64_t strides[2] = {(cuuint64_t)l.Wq * 2, (cuuint64_t)a.r_plane * 2};
         const cuuint32_t box[3] = {64, 128, 1};
@@ -1256,7 +1265,7 @@ cudaError_t launch_row_pass_umma(const ConvGeometry &g, const void *d_x, void *d
     const cudaError_t err = launch_umma<kModeRows>(a, tbl, ttab, g.max_rpad, map_in, map_out, map_aux, map_cut, st);
     if (err != cudaSuccess || w8 == g.W) return err;
     const int64_t n_rows = 2 * (int64_t)g.L * g.Hp;
-    edge_halo_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(a.r_base, n_rows, a.r_pitch, l.Ppad + g.W, w8 - g.W);
+    edge_halo_kernel<<<(unsigned)((n_rows + 7) / 8), 256, 0, st>>>(a.r_base, n_rows, a.r_pitch, l.Ppad + g.W, g.Wp - g.W, g.Hp, g.L, tbl);
     return cudaGetLastError();
 }
 
