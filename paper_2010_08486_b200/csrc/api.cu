@@ -431,17 +431,16 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
     // from a mean padded radius of ~28 on (sigma <= 10 at truncate 5: C1) as soon as the frame has four
     // tiles, and for any ladder on frames that exceed what the FP32 engine keeps in L2 (>= 128 tiles).
     // Narrower ladders on smaller frames gain at most 1.4 x on sparse frames and nothing on a dense one
-    // (C5: the tensor column pass then stores and seed-tests nearly every box): FP32 engine.  Frame
-    // widths that are not a multiple of 8 take the element-wise halo path of the row pass (3 x slower):
-    // only wide ladders on many tiles, as before.  The wider choice is limited to the radii it was
-    // measured and validated with (sigma <= 30 at truncate 5).
+    // (C5: the tensor column pass then stores and seed-tests nearly every box): FP32 engine.  The wider
+    // choice is limited to the radii it was measured and validated with (sigma <= 30 at truncate 5);
+    // beyond them round 1's rule stands (C4).
     // DOGBLOB_CONV=fma|umma (read here, once per plan) overrides.
     {
         double sum_rpad = 0.0;
         for (int i = 0; i < n_levels; ++i) sum_rpad += plan->levels[i].rpad;
         const double mean_rpad = sum_rpad / n_levels;
         const bool wins = (mean_rpad >= 48.0 && tiles >= 48) ||
-                          ((g.W & 7) == 0 && g.max_rpad <= 152 && (tiles >= 128 || (mean_rpad >= 28.0 && tiles >= 4)));
+                          (g.max_rpad <= 152 && (tiles >= 128 || (mean_rpad >= 28.0 && tiles >= 4)));
         plan->use_umma = umma_supported(g) && wins;
         if (const char *e = std::getenv("DOGBLOB_CONV")) {
             if (e[0] == 'f') plan->use_umma = false;
