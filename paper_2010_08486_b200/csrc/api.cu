@@ -428,19 +428,20 @@ int dogblob_plan_create(int device, int height, int width, int n_levels, const d
     // Engine choice (plan time).  The Toeplitz GEMM spends 128 + 2 rpad input rows per 128 outputs
     // and level, the sliding window 2 rpad + 33, but on the tensor cores: measured over frame sizes and
     // ladders (tools/engine_crossover.py, profiles/r02_engine_crossover.md) the tensor-core passes win
-    // from a mean padded radius of ~28 on (sigma <= 10 at truncate 5: C1) as soon as the frame has four
-    // tiles, and for any ladder on frames that exceed what the FP32 engine keeps in L2 (>= 128 tiles).
-    // Narrower ladders on smaller frames gain at most 1.4 x on sparse frames and nothing on a dense one
-    // (C5: the tensor column pass then stores and seed-tests nearly every box): FP32 engine.  The wider
-    // choice is limited to the radii it was measured and validated with (sigma <= 30 at truncate 5);
-    // beyond them round 1's rule stands (C4).
+    // from a mean padded radius of ~28 on (sigma <= 10 at truncate 5: C1) as soon as the frame has six
+    // tiles (four from ~40 on), from ~20 on (sigma <= 6: C5) with 36 tiles (1.25 .. 1.7 x on sparse frames; on the dense C5
+    // frame, where the column pass stores and seed-tests nearly every box, the two engines are equal),
+    // and for any ladder on frames that exceed what the FP32 engine keeps in L2 (>= 128 tiles).  The
+    // wider choice is limited to the radii it was measured and validated with (sigma <= 30 at truncate
+    // 5); beyond them round 1's rule stands (C4).
     // DOGBLOB_CONV=fma|umma (read here, once per plan) overrides.
     {
         double sum_rpad = 0.0;
         for (int i = 0; i < n_levels; ++i) sum_rpad += plan->levels[i].rpad;
         const double mean_rpad = sum_rpad / n_levels;
         const bool wins = (mean_rpad >= 48.0 && tiles >= 48) ||
-                          (g.max_rpad <= 152 && (tiles >= 128 || (mean_rpad >= 28.0 && tiles >= 4)));
+                          (g.max_rpad <= 152 && (tiles >= 128 || (mean_rpad >= 40.0 && tiles >= 4) || (mean_rpad >= 28.0 && tiles >= 6) ||
+                                                 (mean_rpad >= 20.0 && tiles >= 36)));
         plan->use_umma = umma_supported(g) && wins;
         if (const char *e = std::getenv("DOGBLOB_CONV")) {
             if (e[0] == 'f') plan->use_umma = false;

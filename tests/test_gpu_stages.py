@@ -133,6 +133,7 @@ class TestEngines:
         wide = P.Detector(P.DetectionParams(min_sigma=1, max_sigma=30, n_bin=58, preprocess=False))
         narrow = P.Detector(P.DetectionParams(min_sigma=1, max_sigma=10, n_bin=18, preprocess=False))
         dense = P.Detector(P.DetectionParams(min_sigma=1, max_sigma=6, n_bin=10, preprocess=False))
+        sparse3 = P.Detector(P.DetectionParams(min_sigma=1, max_sigma=3, n_bin=6, preprocess=False))
         try:
             # measured crossover (tools/engine_crossover.py)
             assert wide.plan_for((1024, 1024)).plan.conv_engine >= 1      # C2: tensor cores
@@ -141,12 +142,15 @@ class TestEngines:
             assert wide.plan_for((500, 500)).plan.conv_engine >= 1        # width not a multiple of 8: same rule
             assert narrow.plan_for((512, 512)).plan.conv_engine >= 1      # C1: mean padded radius 31
             assert narrow.plan_for((128, 128)).plan.conv_engine == 0      # ... a single tile
-            assert dense.plan_for((1024, 1024)).plan.conv_engine == 0     # C5: narrow ladder (mean 21): FP32 sliding window
-            assert dense.plan_for((2048, 2048)).plan.conv_engine >= 1     # ... unless the frame exceeds the L2
+            assert dense.plan_for((1024, 1024)).plan.conv_engine >= 1     # C5: narrow ladder (mean 21) on 64 tiles
+            assert dense.plan_for((512, 512)).plan.conv_engine == 0       # ... on 16: FP32 sliding window
+            assert sparse3.plan_for((1024, 1024)).plan.conv_engine == 0   # sigma <= 3 (mean 14): FP32 sliding window
+            assert sparse3.plan_for((2048, 2048)).plan.conv_engine >= 1   # ... unless the frame exceeds the L2
         finally:
             wide.close()
             narrow.close()
             dense.close()
+            sparse3.close()
 
     @pytest.mark.parametrize("shape,lo,hi,n", [((384, 512), 2.0, 40.0, 19), ((256, 384), 20.0, 60.0, 2),
                                                ((200, 150), 1.0, 4.0, 3)])
